@@ -1,0 +1,172 @@
+"""Generate the golden fixtures under tests/golden from the REFERENCE itself.
+
+Run in the build container only (it imports ``specrank`` from
+/root/reference/pkg/src, which does not exist on the GPU box):
+
+    python tests/golden/make_golden.py
+
+The fixtures pin both the CPU oracle (tests/test_oracle.py) and the CUDA path
+(tests/test_gpu_*.py).  Inputs are seeded (paper_1703_06935_b200.workloads).
+"""
+
+from __future__ import annotations
+
+import hashlib
+import os
+import sys
+import time
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+REPO = os.path.dirname(os.path.dirname(HERE))
+sys.path.insert(0, REPO)
+sys.path.insert(0, "/root/reference/pkg/src")
+
+from specrank import graph, ranking, spectral  # noqa: E402
+from specrank.descriptors import DescriptorSet  # noqa: E402
+from specrank.sparsemat import SparseSymmetricMatrix  # noqa: E402
+
+from paper_1703_06935_b200.workloads import CONFIGS, cluster_descriptors  # noqa: E402
+
+
+def support_hash(flat_sorted: np.ndarray) -> str:
+    return hashlib.sha256(np.ascontiguousarray(flat_sorted, dtype=np.int64).tobytes()).hexdigest()
+
+
+def csr_support(U) -> np.ndarray:
+    coo = U.tocoo()
+    return np.sort(coo.row.astype(np.int64) * U.shape[1] + coo.col.astype(np.int64))
+
+
+def gaussian_cases():
+    cases = [(7, 5, 0), (3, 3, 1), (64, 10, 12345), (33, 7, 2 ** 40 + 3), (1, 1, 7)]
+    out = {}
+    for i, (r, c, s) in enumerate(cases):
+        out[f"g{i}_shape"] = np.array([r, c, s], dtype=np.uint64)
+        out[f"g{i}"] = spectral.gaussian_matrix(r, c, s)
+        gen = np.random.Generator(np.random.Philox(s))
+        out[f"g{i}_uniforms"] = gen.random(16)
+    out["count"] = np.array(len(cases))
+    np.savez_compressed(os.path.join(HERE, "gaussian.npz"), **out)
+
+
+def random_adjacency(n: int, density: float, seed: int):
+    rng = np.random.default_rng(seed)
+    M = rng.random((n, n)) * (rng.random((n, n)) < density)
+    M = np.triu(M, 1)
+    M = M + M.T
+    return SparseSymmetricMatrix.from_dense(M)
+
+
+def kat_cases():
+    out = {}
+    # rank-3 A = X X^T, r_hat=5, q=3 -> ||A - QQ^T A||_2 < 1e-8
+    rng = np.random.default_rng(11)
+    X = rng.standard_normal((64, 3))
+    A = SparseSymmetricMatrix.from_dense(X @ X.T)
+    basis = spectral.range_finder(A, 5, 3, 0)
+    out["rank3_A"] = A.to_dense()
+    out["rank3_Q"] = basis.Q
+    out["rank3_B"] = basis.B
+
+    # 2-node edge: Lambda = {1, -1}
+    W2 = SparseSymmetricMatrix.from_dense(np.array([[0.0, 1.0], [1.0, 0.0]]))
+    d2 = spectral.decompose(W2, 2, p=0, q=3, seed=0)
+    out["two_U"] = d2.U
+    out["two_lam"] = d2.eigenvalues
+
+    # random normalized W, n=64, r=16
+    Wr = random_adjacency(64, 0.15, 5)
+    Sr = graph.normalize_adjacency(Wr, graph.degrees(Wr))
+    dr = spectral.decompose(Sr, 16, p=10, q=4, seed=3)
+    out["rand_W_dense"] = Sr.to_dense()
+    out["rand_U"] = dr.U
+    out["rand_lam"] = dr.eigenvalues
+    out["rand_eta"] = dr.eta
+    sp_dec = spectral.sparsify(dr, 200)
+    out["rand_sparse_flat"] = csr_support(sp_dec.U)
+    out["rand_sparse_eta"] = sp_dec.eta
+    y = ranking.ObservationVector(64, np.array([1, 5, 9, 40]), np.array([0.5, 0.25, 1.0, 0.125]), cap=4)
+    h = ranking.h_alpha(0.99)
+    out["rand_y_idx"] = y.indices
+    out["rand_y_val"] = y.values
+    out["rand_x_approx"] = ranking.filter(dr, h, y)
+    out["rand_x_sparse"] = ranking.filter(sp_dec, h, y)
+    heat = ranking.custom_transfer(lambda x: np.exp(-10.0 * (1.0 - x)), nondecreasing=True, positive=True)
+    out["rand_x_heat"] = ranking.filter(dr, heat, y)
+
+    # n=12 graph with an isolated vertex -> eta = 0 rows exercise copy_uncovered
+    Wi = random_adjacency(12, 0.5, 9).to_dense()
+    Wi[3, :] = 0.0
+    Wi[:, 3] = 0.0
+    Wi = SparseSymmetricMatrix.from_dense(Wi)
+    Si = graph.normalize_adjacency(Wi, graph.degrees(Wi))
+    di = spectral.decompose(Si, 6, p=2, q=3, seed=1)
+    yi = ranking.ObservationVector(12, np.array([0, 3, 7]), np.array([1.0, 2.0, 0.5]), cap=3)
+    out["iso_W_dense"] = Si.to_dense()
+    out["iso_lam"] = di.eigenvalues
+    out["iso_eta"] = di.eta
+    out["iso_x"] = ranking.filter(di, h, yi)
+    si = spectral.sparsify(di, 30)  # row 3 keeps nothing -> eta == 0 exactly
+    out["iso_sparse_eta"] = si.eta
+    out["iso_sparse_flat"] = csr_support(si.U)
+    out["iso_x_sparse"] = ranking.filter(si, h, yi)
+    out["iso_y_idx"] = yi.indices
+    out["iso_y_val"] = yi.values
+    np.savez_compressed(os.path.join(HERE, "kat.npz"), **out)
+
+
+def c1_case(n_x: int = 20):
+    cfg = CONFIGS["C1"]
+    t0 = time.perf_counter()
+    data, queries, _ = cluster_descriptors(cfg)
+    ds = DescriptorSet(data)
+    W = graph.build_mutual_knn_graph(ds, cfg.k, cfg.gamma)
+    S = graph.normalize_adjacency(W, graph.degrees(W))
+    t1 = time.perf_counter()
+    dec = spectral.decompose(S, cfg.r, p=cfg.p, q=cfg.q, seed=0)
+    t2 = time.perf_counter()
+    sdec = spectral.sparsify(dec, cfg.tau)
+    t3 = time.perf_counter()
+    h = ranking.h_alpha(cfg.alpha)
+    ys = [ranking.observation_vector(qv, ds, cfg.y_top, cfg.gamma) for qv in queries]
+    y_ptr = np.zeros(len(ys) + 1, dtype=np.int64)
+    y_ptr[1:] = np.cumsum([y.nnz for y in ys])
+    y_idx = np.concatenate([y.indices for y in ys])
+    y_val = np.concatenate([y.values for y in ys])
+    top_a, top_s, xa, xs = [], [], [], []
+    for j, y in enumerate(ys):
+        x = ranking.filter(dec, h, y)
+        x2 = ranking.filter(sdec, h, y)
+        top_a.append(ranking.rank(x)[:100])
+        top_s.append(ranking.rank(x2)[:100])
+        if j < n_x:
+            xa.append(x)
+            xs.append(x2)
+    t4 = time.perf_counter()
+    flat = csr_support(sdec.U)
+    print(f"C1: graph {t1 - t0:.1f}s decompose {t2 - t1:.1f}s sparsify {t3 - t2:.1f}s "
+          f"queries {t4 - t3:.1f}s nnz(W)={W.nnz}")
+    np.savez_compressed(
+        os.path.join(HERE, "c1.npz"),
+        W_indptr=W.csr.indptr.astype(np.int64), W_indices=W.csr.indices.astype(np.int32),
+        W_data=W.csr.data, S_data=S.csr.data,
+        lam=dec.eigenvalues, eta=dec.eta, U_cols=dec.U[:, :4].copy(),
+        U_colsum_abs=np.abs(dec.U).sum(axis=0),
+        sparse_eta=sdec.eta, sparse_nnz=np.array(sdec.U.nnz),
+        sparse_hash=np.array(support_hash(flat)),
+        sparse_flat_head=flat[:2000],
+        y_ptr=y_ptr, y_idx=y_idx, y_val=y_val,
+        x_approx=np.array(xa), x_sparse=np.array(xs),
+        top_approx=np.array(top_a, dtype=np.int32), top_sparse=np.array(top_s, dtype=np.int32),
+        params=np.array([cfg.n, cfg.r, cfg.p, cfg.q, cfg.tau, 0]),
+        alpha=np.array(cfg.alpha),
+    )
+
+
+if __name__ == "__main__":
+    gaussian_cases()
+    kat_cases()
+    c1_case()
+    print("ok")

@@ -1,0 +1,107 @@
+"""Pin the CPU oracle against fixtures produced by the reference itself."""
+
+import numpy as np
+import scipy.sparse as sp
+
+from oracle import fsr_oracle as O
+
+
+def c1_matrices(g):
+    n = int(g["params"][0])
+    W = sp.csr_matrix((g["W_data"], g["W_indices"], g["W_indptr"]), shape=(n, n))
+    S = sp.csr_matrix((g["S_data"], g["W_indices"], g["W_indptr"]), shape=(n, n))
+    return W, S
+
+
+def test_philox_block_matches_numpy_stream():
+    for seed in (0, 1, 12345, 2 ** 40 + 3):
+        raw = np.random.Philox(seed).random_raw(8)
+        key = O.philox_key(seed)
+        mine = [O.philox4x64_10((1, 0, 0, 0), key), O.philox4x64_10((2, 0, 0, 0), key)]
+        assert [int(v) for v in raw] == [int(v) for blk in mine for v in blk]
+
+
+def test_gaussian_matches_reference(golden):
+    g = golden("gaussian")
+    for i in range(int(g["count"])):
+        r, c, s = (int(v) for v in g[f"g{i}_shape"])
+        np.testing.assert_array_equal(O.gaussian_matrix(r, c, s), g[f"g{i}"])
+        np.testing.assert_array_equal(O.philox_uniforms(s, 0, 16), g[f"g{i}_uniforms"])
+
+
+def test_normalize_matches_reference_bitwise(golden):
+    g = golden("c1")
+    W, S = c1_matrices(g)
+    S2 = O.normalize_adjacency(W, O.degrees(W))
+    S2.sort_indices()
+    np.testing.assert_array_equal(S2.indptr, S.indptr)
+    np.testing.assert_array_equal(S2.data, S.data)
+
+
+def test_kat_rank3_range_finder(golden):
+    k = golden("kat")
+    A = sp.csr_matrix(k["rank3_A"])
+    Q, B = O.range_finder(A, 5, 3, 0)
+    np.testing.assert_allclose(np.abs(Q.T @ k["rank3_Q"]).max(), 1.0, atol=1e-12)
+    resid = np.linalg.norm(k["rank3_A"] - Q @ (Q.T @ k["rank3_A"]), 2)
+    assert resid < 1e-8
+
+
+def test_kat_two_node(golden):
+    k = golden("kat")
+    U, lam, eta = O.decompose(sp.csr_matrix(np.array([[0.0, 1.0], [1.0, 0.0]])), 2, p=0, q=3, seed=0)
+    np.testing.assert_allclose(lam, [1.0, -1.0], atol=1e-12)
+    np.testing.assert_allclose(lam, k["two_lam"], atol=1e-14)
+    np.testing.assert_allclose(U, k["two_U"], atol=1e-12)
+
+
+def test_kat_random_and_filter(golden):
+    k = golden("kat")
+    S = sp.csr_matrix(k["rand_W_dense"])
+    U, lam, eta = O.decompose(S, 16, p=10, q=4, seed=3)
+    np.testing.assert_allclose(lam, k["rand_lam"], rtol=0, atol=1e-12)
+    np.testing.assert_allclose(U, k["rand_U"], atol=1e-10)
+    Ut, eta_s = O.sparsify(U, 200)
+    coo = Ut.tocoo()
+    np.testing.assert_array_equal(np.sort(coo.row.astype(np.int64) * 16 + coo.col), k["rand_sparse_flat"])
+    np.testing.assert_array_equal(O.sparsify_support(U, 200), k["rand_sparse_flat"])
+    w = O.transfer_values(O.h_alpha(0.99), lam)
+    x = O.filter_scores(U, lam, eta, w, k["rand_y_idx"], k["rand_y_val"])
+    np.testing.assert_allclose(x, k["rand_x_approx"], rtol=1e-10, atol=1e-13)
+    xs = O.filter_scores(Ut, lam, eta_s, w, k["rand_y_idx"], k["rand_y_val"])
+    np.testing.assert_allclose(xs, k["rand_x_sparse"], rtol=1e-10, atol=1e-13)
+    wh = O.transfer_values(O.heat_kernel(10.0), lam, analytic=False)
+    xh = O.filter_scores(U, lam, eta, wh, k["rand_y_idx"], k["rand_y_val"])
+    np.testing.assert_allclose(xh, k["rand_x_heat"], rtol=1e-10, atol=1e-13)
+
+
+def test_kat_isolated_vertex_copy_uncovered(golden):
+    k = golden("kat")
+    U, lam, eta = O.decompose(sp.csr_matrix(k["iso_W_dense"]), 6, p=2, q=3, seed=1)
+    w = O.transfer_values(O.h_alpha(0.99), lam)
+    x = O.filter_scores(U, lam, eta, w, k["iso_y_idx"], k["iso_y_val"])
+    np.testing.assert_allclose(x, k["iso_x"], rtol=1e-10, atol=1e-13)
+    Ut, eta_s = O.sparsify(U, 30)
+    assert eta_s[3] == 0.0
+    np.testing.assert_array_equal(eta_s, k["iso_sparse_eta"])
+    xs = O.filter_scores(Ut, lam, eta_s, w, k["iso_y_idx"], k["iso_y_val"])
+    np.testing.assert_allclose(xs, k["iso_x_sparse"], rtol=1e-10, atol=1e-13)
+    assert xs[3] == 2.0
+
+
+def test_c1_oracle_matches_reference(golden):
+    g = golden("c1")
+    _, S = c1_matrices(g)
+    n, r, p, q, tau, seed = (int(v) for v in g["params"])
+    U, lam, eta = O.decompose(S, r, p=p, q=q, seed=seed)
+    np.testing.assert_allclose(lam, g["lam"], rtol=0, atol=1e-12)
+    np.testing.assert_allclose(eta, g["eta"], atol=1e-10)
+    w = O.transfer_values(O.h_alpha(float(g["alpha"])), lam)
+    for j in range(3):
+        sl = slice(g["y_ptr"][j], g["y_ptr"][j + 1])
+        x = O.filter_scores(U, lam, eta, w, g["y_idx"][sl], g["y_val"][sl])
+        np.testing.assert_allclose(x, g["x_approx"][j], rtol=1e-8, atol=1e-12)
+    flat = O.sparsify_support(U, tau)
+    assert flat.size == int(g["sparse_nnz"])
+    import hashlib
+    assert hashlib.sha256(flat.astype(np.int64).tobytes()).hexdigest() == str(g["sparse_hash"])
