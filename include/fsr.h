@@ -1,0 +1,185 @@
+/*
+ * fsr.h -- C ABI of libfsr, the B200 (sm_100a) kernels behind the FSR hot path.
+ *
+ * The reference (specrank, pure Python) has no FFI; its "operator API" is the
+ * module-level functions of spectral.py / ranking.py.  Each entry point below
+ * replaces one numeric call site of those functions (cited file:line,
+ * relative to /root/reference/pkg/src/specrank).  The Python host layer
+ * (paper_1703_06935_b200.spectral / .ranking) keeps the reference signatures
+ * and calls these through ctypes; a C/C++ host can bind them directly.
+ *
+ * Conventions
+ *  - Plain C: no torch or CUDA types in the signatures.  `stream` arguments
+ *    are cudaStream_t passed as void* (NULL = the context's stream).
+ *  - Every matrix pointer is DEVICE memory, allocated by the caller.  Dense
+ *    blocks are row-major with an explicit leading dimension (elements).
+ *  - `dtype` selects the storage/arithmetic type: FSR_F32 or FSR_F64.  Small
+ *    r_hat x r_hat matrices (Gram, projection, Cholesky factor, eigenvectors)
+ *    are always float64.
+ *  - CSR matrices: int64 row pointers, int32 column indices, values in dtype.
+ *  - Return value: FSR_OK or an FSR_E* code; fsr_last_error(ctx) describes
+ *    the most recent failure.  Calls are asynchronous on the context stream
+ *    unless they return a host value (documented per function).
+ *  - Deterministic: no floating-point atomics; for a fixed dtype, shapes and
+ *    shard layout the results are bitwise reproducible.
+ */
+#ifndef FSR_H_
+#define FSR_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FSR_ABI_VERSION 1
+
+enum fsr_status {
+  FSR_OK = 0,
+  FSR_EINVAL = 1,      /* contract violation (reference: ValueError)          */
+  FSR_ENUMERICAL = 2,  /* non-finite / breakdown (reference: NumericalError)  */
+  FSR_ECUDA = 3,
+  FSR_ENOMEM = 4,
+  FSR_ELIBRARY = 5,    /* cuBLAS / cuSOLVER failure                          */
+  FSR_ENOTSPD = 6      /* Cholesky breakdown: caller falls back to Householder */
+};
+
+enum fsr_dtype { FSR_F32 = 0, FSR_F64 = 1 };
+
+typedef struct fsr_ctx fsr_ctx;
+
+/* ---- context --------------------------------------------------------- */
+int fsr_abi_version(void);
+int fsr_ctx_create(int device, fsr_ctx** out);
+void fsr_ctx_destroy(fsr_ctx* ctx);
+int fsr_ctx_set_stream(fsr_ctx* ctx, void* stream);
+const char* fsr_last_error(const fsr_ctx* ctx);
+/* Number of libfsr kernels launched on this context so far (own kernels only;
+ * cuBLAS/cuSOLVER calls are counted separately by fsr_library_calls). */
+uint64_t fsr_launch_count(const fsr_ctx* ctx);
+uint64_t fsr_library_calls(const fsr_ctx* ctx);
+int fsr_synchronize(fsr_ctx* ctx);
+
+/* ---- K0: start block  (spectral.py:55-65 gaussian_matrix) -------------
+ * Rows [row_begin, row_end) of the (total_rows x cols) Box-Muller block drawn
+ * from numpy's Philox4x64-10 stream with key (key0, key1) =
+ * SeedSequence(seed).generate_state(2, uint64).  Uniforms are bit-identical to
+ * numpy's; the transcendental step is fp64 (CUDA libm, <= 2 ulp).
+ * out: (row_end-row_begin) x cols, ld = cols, dtype. */
+int fsr_gaussian_block(fsr_ctx* ctx, int dtype, int64_t total_rows, int64_t cols,
+                       int64_t row_begin, int64_t row_end, uint64_t key0, uint64_t key1,
+                       void* out);
+
+/* ---- K1: normalisation  (graph.py:118-139 degrees / normalize_adjacency) --
+ * deg[i] = sum_j w_ij over the local rows (fp64). */
+int fsr_csr_row_sums(fsr_ctx* ctx, int64_t n_rows, const int64_t* indptr, const double* data,
+                     double* deg);
+/* out[e] = (w_e * s_i) * s_j, s = 1/sqrt(deg) (0 where deg == 0).  `deg` is the
+ * GLOBAL degree vector (indexed by column), local row i is global row
+ * row_offset + i.  out has dtype `dtype_out`. */
+int fsr_csr_normalize(fsr_ctx* ctx, int dtype_out, int64_t n_rows, int64_t row_offset,
+                      const int64_t* indptr, const int32_t* indices, const double* data,
+                      const double* deg, void* out);
+/* Elementwise fp64 -> dtype conversion of n values (out may alias for F64). */
+int fsr_convert_from_f64(fsr_ctx* ctx, int dtype, int64_t n, const double* in, void* out);
+
+/* ---- K2: CSR SpMM  (spectral.py:170 -> sparsemat.py:63-64 -> csr_matvecs) --
+ * Y[i, :ncols] = sum_e A_ie X[col_e, :ncols] for the n_rows local rows of A.
+ * Accumulation follows CSR order per output element; in F64 the multiply and
+ * add are rounded separately (no FMA), matching scipy's csr_matvecs bitwise. */
+int fsr_csr_spmm(fsr_ctx* ctx, int dtype, int64_t n_rows, const int64_t* indptr,
+                 const int32_t* indices, const void* values, int64_t ncols, const void* X,
+                 int64_t ldx, void* Y, int64_t ldy);
+
+/* ---- K3: orthonormalisation  (spectral.py:165-169 np.linalg.qr + check) ---
+ * G (k x k, fp64, row-major, symmetric) = A^T A over n_rows rows
+ * (accumulate != 0: G += A^T A). */
+int fsr_gram(fsr_ctx* ctx, int dtype, int64_t n_rows, int64_t k, const void* A, int64_t lda,
+             double* G, int accumulate);
+/* In-place Cholesky G = R^T R (R upper).  Returns FSR_ENOTSPD on breakdown
+ * (host-synchronous: reads the factorisation status). */
+int fsr_cholesky(fsr_ctx* ctx, int64_t k, double* G);
+/* A <- A R^-1 for the R produced by fsr_cholesky (row-major A, n_rows x k). */
+int fsr_apply_rinv(fsr_ctx* ctx, int dtype, int64_t n_rows, int64_t k, const double* R, void* A,
+                   int64_t lda);
+/* Householder QR (single device): A <- Q, the reduced orthonormal factor.
+ * Fallback for rank-deficient blocks, mirroring spectral.py:165. */
+int fsr_householder_qr(fsr_ctx* ctx, int dtype, int64_t n_rows, int64_t k, void* A, int64_t lda);
+/* max_ij |G_ij - delta_ij| written to *err_host (host-synchronous). */
+int fsr_max_offdiag_error(fsr_ctx* ctx, int64_t k, const double* G, double* err_host);
+
+/* ---- K4-K6: Rayleigh-Ritz  (spectral.py:174-198) ----------------------
+ * C (k x k fp64) (+)= Q^T B over n_rows rows. */
+int fsr_cross(fsr_ctx* ctx, int dtype, int64_t n_rows, int64_t k, const void* Q, int64_t ldq,
+              const void* B, int64_t ldb, double* C, int accumulate);
+/* C <- (C + C^T)/2; eigh; keep the r algebraically largest pairs in
+ * argsort(-lambda, stable) order (spectral.py:141-144).  lam_host[r] gets the
+ * eigenvalues (host-synchronous), V (k x r, fp64, row-major) the eigenvectors.
+ * C is destroyed. */
+int fsr_eigh_desc(fsr_ctx* ctx, int64_t k, double* C, int64_t r, double* lam_host, double* V);
+/* U (n_rows x r, dtype) = Q (n_rows x k) V (k x r). */
+int fsr_lift(fsr_ctx* ctx, int dtype, int64_t n_rows, int64_t k, int64_t r, const void* Q,
+             int64_t ldq, const double* V, void* U, int64_t ldu);
+/* Per column j: the first (lowest global row) entry of maximal |U_ij| over the
+ * local rows; best_abs[j], best_row[j] (= row_offset + i) and best_val[j]
+ * (signed).  (spectral.py:133-138 _fix_column_signs, first half.) */
+int fsr_col_absmax(fsr_ctx* ctx, int dtype, int64_t n_rows, int64_t r, const void* U, int64_t ldu,
+                   int64_t row_offset, double* best_abs, int64_t* best_row, double* best_val);
+/* U[:, j] *= sign_j where sign_j = sign(best_val[j]) (0 -> +1), then
+ * eta[i] = ||U_i,:|| (spectral.py:127-130, 133-138 second half). */
+int fsr_apply_signs_rownorm(fsr_ctx* ctx, int dtype, int64_t n_rows, int64_t r, void* U,
+                            int64_t ldu, const double* best_val, double* eta);
+/* eta[i] = ||U_i,:|| without touching U. */
+int fsr_row_norms(fsr_ctx* ctx, int dtype, int64_t n_rows, int64_t r, const void* U, int64_t ldu,
+                  double* eta);
+
+/* ---- K7: thresholding  (spectral.py:269-294 sparsify) ------------------
+ * Entries are ordered by the key |u| (IEEE bits with the sign cleared:
+ * 31-bit keys for F32, 63-bit for F64); exact zeros never count.
+ * Histogram of digit ((key >> shift) & (2^bits-1)) over entries whose key
+ * satisfies (key & ~(2^(shift+bits)-1)) == prefix.  hist (2^bits uint64) is
+ * accumulated into (caller zeroes it).  bits <= 12. */
+int fsr_abs_histogram(fsr_ctx* ctx, int dtype, int64_t n_rows, int64_t r, const void* U,
+                      int64_t ldu, uint64_t prefix, int shift, int bits, uint64_t* hist);
+/* Per row: gt[i] = #{key > T}, eq[i] = #{key == T}. */
+int fsr_threshold_counts(fsr_ctx* ctx, int dtype, int64_t n_rows, int64_t r, const void* U,
+                         int64_t ldu, uint64_t T, int64_t* gt, int64_t* eq);
+/* Build the kept CSR rows: all entries with key > T plus the ties (key == T)
+ * whose global (row, col) tie rank is < ties_to_take, where the local rows'
+ * tie ranks start at tie_offset (ties held by lower-ranked shards).
+ * indptr_out (n_rows+1) local, starting at 0; *nnz_host = kept count
+ * (host-synchronous).  eta = row norms of the kept rows.  indices/values
+ * must hold at least the kept count (<= sum(gt) + ties_to_take). */
+int fsr_threshold_compact(fsr_ctx* ctx, int dtype, int64_t n_rows, int64_t r, const void* U,
+                          int64_t ldu, uint64_t T, int64_t tie_offset, int64_t ties_to_take,
+                          const int64_t* gt, const int64_t* eq, int64_t* indptr_out,
+                          int32_t* indices_out, void* values_out, double* eta, int64_t* nnz_host);
+
+/* ---- K8/K9: online batch  (ranking.py:219-255 _project / filter) ------------
+ * For b observation columns y_j (CSC: y_ptr[b+1], y_idx row ids, y_val in dtype):
+ *   z_j = U[supp y_j]^T y_j            (K8, ranking.py:219-226)
+ *   x_j = U (w .* z_j)                 (K9, ranking.py:246)
+ *   x_j[i] = y_ij where eta_i == 0     (copy_uncovered, ranking.py:248-254)
+ * U is CSR (u_indptr/u_indices/u_values, n x r) when u_sparse, else dense
+ * u_dense (n x r, ld ldu).  w: r weights h(lambda) (dtype).  eta: n fp64 (may
+ * be NULL when copy_uncovered == 0).
+ * Outputs: X (b x n, row j = x_j) when X != NULL; and/or the top `topk`
+ * entries of every x_j ordered by (-x, index) (ranking.py:390-395) into
+ * top_idx (b x topk int64) / top_val (b x topk dtype) when topk > 0.
+ * workspace: device scratch of fsr_filter_workspace_bytes(...) bytes. */
+int64_t fsr_filter_workspace_bytes(int dtype, int64_t n, int64_t r, int64_t b, int need_x);
+int fsr_filter_batch(fsr_ctx* ctx, int dtype, int64_t n, int64_t r, int u_sparse,
+                     const int64_t* u_indptr, const int32_t* u_indices, const void* u_values,
+                     const void* u_dense, int64_t ldu, const void* w, const double* eta,
+                     int64_t b, const int64_t* y_ptr, const int64_t* y_idx, const void* y_val,
+                     int copy_uncovered, void* workspace, void* X, int64_t topk,
+                     int64_t* top_idx, void* top_val);
+/* Top-k of every row of X (b x n): indices/values ordered by (-x, index). */
+int fsr_topk_rows(fsr_ctx* ctx, int dtype, int64_t b, int64_t n, const void* X, int64_t ldx,
+                  int64_t topk, int64_t* top_idx, void* top_val);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* FSR_H_ */

@@ -1,0 +1,187 @@
+"""ctypes binding of libfsr.so (include/fsr.h) and the per-device context.
+
+There is no fallback: if the library is missing or no CUDA device is present,
+every entry point raises.  Device buffers are torch CUDA tensors; only their
+raw pointers cross the C ABI, together with torch's current CUDA stream.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libfsr.so")
+
+F32, F64 = 0, 1
+OK, EINVAL, ENUMERICAL, ECUDA, ENOMEM, ELIBRARY, ENOTSPD = range(7)
+
+_c_i64 = ctypes.c_int64
+_c_u64 = ctypes.c_uint64
+_c_int = ctypes.c_int
+_c_p = ctypes.c_void_p
+_c_dp = ctypes.POINTER(ctypes.c_double)
+_c_i64p = ctypes.POINTER(ctypes.c_int64)
+
+# name -> (restype, argtypes)
+_SIGS = {
+    "fsr_abi_version": (_c_int, []),
+    "fsr_ctx_create": (_c_int, [_c_int, ctypes.POINTER(_c_p)]),
+    "fsr_ctx_destroy": (None, [_c_p]),
+    "fsr_ctx_set_stream": (_c_int, [_c_p, _c_p]),
+    "fsr_last_error": (ctypes.c_char_p, [_c_p]),
+    "fsr_launch_count": (_c_u64, [_c_p]),
+    "fsr_library_calls": (_c_u64, [_c_p]),
+    "fsr_synchronize": (_c_int, [_c_p]),
+    "fsr_gaussian_block": (_c_int, [_c_p, _c_int, _c_i64, _c_i64, _c_i64, _c_i64, _c_u64, _c_u64, _c_p]),
+    "fsr_csr_row_sums": (_c_int, [_c_p, _c_i64, _c_p, _c_p, _c_p]),
+    "fsr_csr_normalize": (_c_int, [_c_p, _c_int, _c_i64, _c_i64, _c_p, _c_p, _c_p, _c_p, _c_p]),
+    "fsr_convert_from_f64": (_c_int, [_c_p, _c_int, _c_i64, _c_p, _c_p]),
+    "fsr_csr_spmm": (_c_int, [_c_p, _c_int, _c_i64, _c_p, _c_p, _c_p, _c_i64, _c_p, _c_i64, _c_p, _c_i64]),
+    "fsr_gram": (_c_int, [_c_p, _c_int, _c_i64, _c_i64, _c_p, _c_i64, _c_p, _c_int]),
+    "fsr_cholesky": (_c_int, [_c_p, _c_i64, _c_p]),
+    "fsr_apply_rinv": (_c_int, [_c_p, _c_int, _c_i64, _c_i64, _c_p, _c_p, _c_i64]),
+    "fsr_householder_qr": (_c_int, [_c_p, _c_int, _c_i64, _c_i64, _c_p, _c_i64]),
+    "fsr_max_offdiag_error": (_c_int, [_c_p, _c_i64, _c_p, _c_dp]),
+    "fsr_cross": (_c_int, [_c_p, _c_int, _c_i64, _c_i64, _c_p, _c_i64, _c_p, _c_i64, _c_p, _c_int]),
+    "fsr_eigh_desc": (_c_int, [_c_p, _c_i64, _c_p, _c_i64, _c_dp, _c_p]),
+    "fsr_lift": (_c_int, [_c_p, _c_int, _c_i64, _c_i64, _c_i64, _c_p, _c_i64, _c_p, _c_p, _c_i64]),
+    "fsr_col_absmax": (_c_int, [_c_p, _c_int, _c_i64, _c_i64, _c_p, _c_i64, _c_i64, _c_p, _c_p, _c_p]),
+    "fsr_apply_signs_rownorm": (_c_int, [_c_p, _c_int, _c_i64, _c_i64, _c_p, _c_i64, _c_p, _c_p]),
+    "fsr_row_norms": (_c_int, [_c_p, _c_int, _c_i64, _c_i64, _c_p, _c_i64, _c_p]),
+    "fsr_abs_histogram": (_c_int, [_c_p, _c_int, _c_i64, _c_i64, _c_p, _c_i64, _c_u64, _c_int, _c_int, _c_p]),
+    "fsr_threshold_counts": (_c_int, [_c_p, _c_int, _c_i64, _c_i64, _c_p, _c_i64, _c_u64, _c_p, _c_p]),
+    "fsr_threshold_compact": (_c_int, [_c_p, _c_int, _c_i64, _c_i64, _c_p, _c_i64, _c_u64, _c_i64, _c_i64, _c_p,
+                                       _c_p, _c_p, _c_p, _c_p, _c_p, _c_i64p]),
+    "fsr_filter_workspace_bytes": (_c_i64, [_c_int, _c_i64, _c_i64, _c_i64, _c_int]),
+    "fsr_filter_batch": (_c_int, [_c_p, _c_int, _c_i64, _c_i64, _c_int, _c_p, _c_p, _c_p, _c_p, _c_i64, _c_p, _c_p,
+                                  _c_i64, _c_p, _c_p, _c_p, _c_int, _c_p, _c_p, _c_i64, _c_p, _c_p]),
+    "fsr_topk_rows": (_c_int, [_c_p, _c_int, _c_i64, _c_i64, _c_p, _c_i64, _c_i64, _c_p, _c_p]),
+}
+
+EXPORTED = tuple(_SIGS)
+
+_lib = None
+_lock = threading.Lock()
+
+
+class FsrError(RuntimeError):
+    """A libfsr call failed (CUDA / library error)."""
+
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"libfsr error {code}: {msg}")
+        self.code = code
+
+
+def load_library(path: str = LIB_PATH):
+    """Load libfsr.so and declare every exported signature (no device needed)."""
+    global _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(path):
+                raise ImportError(f"libfsr.so not built at {path}; run `python -m paper_1703_06935_b200.build`")
+            lib = ctypes.CDLL(path)
+            for name, (res, args) in _SIGS.items():
+                fn = getattr(lib, name)
+                fn.restype = res
+                fn.argtypes = args
+            if lib.fsr_abi_version() != 1:
+                raise ImportError("libfsr ABI version mismatch")
+            _lib = lib
+    return _lib
+
+
+def dtype_code(dtype) -> int:
+    import torch
+
+    if dtype in (torch.float64, "float64", "fp64", "f64"):
+        return F64
+    if dtype in (torch.float32, "float32", "fp32", "f32"):
+        return F32
+    raise ValueError(f"unsupported dtype {dtype!r}")
+
+
+def torch_dtype(code_or_name):
+    import torch
+
+    if code_or_name in (F64, "float64", "fp64", "f64", torch.float64):
+        return torch.float64
+    if code_or_name in (F32, "float32", "fp32", "f32", torch.float32):
+        return torch.float32
+    raise ValueError(f"unsupported dtype {code_or_name!r}")
+
+
+class Context:
+    """One libfsr context per CUDA device; calls run on torch's current stream."""
+
+    _by_device: dict = {}
+
+    def __init__(self, device: int):
+        import torch
+
+        if not torch.cuda.is_available():
+            raise RuntimeError("paper_1703_06935_b200 needs a CUDA device (no CPU fallback)")
+        self.lib = load_library()
+        self.device = device
+        h = _c_p()
+        with torch.cuda.device(device):
+            st = self.lib.fsr_ctx_create(device, ctypes.byref(h))
+        if st != OK:
+            raise FsrError(st, "fsr_ctx_create failed")
+        self.handle = h
+        self._stream = None
+
+    @classmethod
+    def get(cls, device=None) -> "Context":
+        import torch
+
+        if device is None:
+            device = torch.cuda.current_device()
+        if isinstance(device, torch.device):
+            device = device.index if device.index is not None else torch.cuda.current_device()
+        ctx = cls._by_device.get(device)
+        if ctx is None:
+            ctx = cls._by_device[device] = Context(device)
+        ctx.bind_stream()
+        return ctx
+
+    def bind_stream(self):
+        import torch
+
+        s = torch.cuda.current_stream(self.device).cuda_stream
+        if s != self._stream:
+            self.check(self.lib.fsr_ctx_set_stream(self.handle, _c_p(s)))
+            self._stream = s
+
+    def check(self, status: int):
+        if status == OK:
+            return
+        msg = self.lib.fsr_last_error(self.handle).decode(errors="replace")
+        if status == EINVAL:
+            raise ValueError(msg)
+        if status == ENUMERICAL:
+            from .spectral import NumericalError
+
+            raise NumericalError(msg)
+        raise FsrError(status, msg)
+
+    def call(self, name: str, *args) -> int:
+        """Invoke fsr_<name>(ctx, *args); raise on failure, return the status."""
+        st = getattr(self.lib, "fsr_" + name)(self.handle, *args)
+        if st not in (OK, ENOTSPD):
+            self.check(st)
+        return st
+
+    @property
+    def launches(self) -> int:
+        return int(self.lib.fsr_launch_count(self.handle))
+
+    @property
+    def library_calls(self) -> int:
+        return int(self.lib.fsr_library_calls(self.handle))
+
+
+def ptr(t) -> _c_p:
+    """Raw device pointer of a torch tensor (None -> NULL)."""
+    return _c_p(0 if t is None else t.data_ptr())

@@ -1,0 +1,169 @@
+// K2 / K9: CSR x dense-block product, warp per (row, column panel).
+//
+// Reference call site: spectral.py:170 `block = A @ Q` -> sparsemat.py:63-64 ->
+// scipy _sparsetools.csr_matvecs (one thread, float64, y += a*x per nonzero in
+// CSR order).  On the device one warp owns one output row-panel: the row's
+// (col, val) pairs are loaded 32 at a time with one coalesced load and
+// broadcast by shuffle; for each nonzero the warp streams the matching row
+// panel of the dense block with 16-byte vector loads (512 B per warp per
+// vector for fp32).  Work items are ordered panel-major so the panel of X in
+// use (n x panel_width) stays L2-resident while all rows sweep over it.
+// Accumulation keeps CSR order per output element; in fp64 the product and
+// sum are rounded separately, so the result is bitwise equal to scipy's.
+#pragma once
+
+#include "fsr_common.cuh"
+
+namespace fsr {
+
+template <typename T, int VEC>
+struct VecT;
+template <>
+struct VecT<float, 4> {
+  using type = float4;
+};
+template <>
+struct VecT<float, 2> {
+  using type = float2;
+};
+template <>
+struct VecT<float, 1> {
+  using type = float;
+};
+template <>
+struct VecT<double, 2> {
+  using type = double2;
+};
+template <>
+struct VecT<double, 1> {
+  using type = double;
+};
+
+template <typename T, int VEC>
+__device__ __forceinline__ void load_vec(const T* p, T (&v)[VEC]) {
+  using V = typename VecT<T, VEC>::type;
+  V t = __ldg(reinterpret_cast<const V*>(p));
+  const T* s = reinterpret_cast<const T*>(&t);
+#pragma unroll
+  for (int i = 0; i < VEC; ++i) v[i] = s[i];
+}
+
+template <typename T, int VEC>
+__device__ __forceinline__ void store_vec(T* p, const T (&v)[VEC]) {
+  using V = typename VecT<T, VEC>::type;
+  V t;
+  T* d = reinterpret_cast<T*>(&t);
+#pragma unroll
+  for (int i = 0; i < VEC; ++i) d[i] = v[i];
+  *reinterpret_cast<V*>(p) = t;
+}
+
+// One warp per (row, panel); panel width = 32 lanes * VEC * NV columns.
+template <typename T, int VEC, int NV>
+__global__ void __launch_bounds__(256) spmm_rowpanel_kernel(int64_t n_rows, const int64_t* __restrict__ indptr,
+                                                            const int32_t* __restrict__ indices,
+                                                            const T* __restrict__ vals, int64_t ncols,
+                                                            const T* __restrict__ X, int64_t ldx,
+                                                            T* __restrict__ Y, int64_t ldy, int64_t n_panels) {
+  constexpr int PW = 32 * VEC * NV;
+  const int lane = threadIdx.x & 31;
+  const int64_t total = n_rows * n_panels;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < total; w += nwarps) {
+    const int64_t p = w / n_rows;
+    const int64_t i = w - p * n_rows;
+    const int64_t c0 = p * PW + (int64_t)lane * VEC;
+    T acc[NV][VEC];
+#pragma unroll
+    for (int u = 0; u < NV; ++u)
+#pragma unroll
+      for (int q = 0; q < VEC; ++q) acc[u][q] = T(0);
+    bool live[NV];
+#pragma unroll
+    for (int u = 0; u < NV; ++u) live[u] = c0 + u * 32 * VEC < ncols;
+    const int64_t e0 = __ldg(indptr + i), e1 = __ldg(indptr + i + 1);
+    for (int64_t base = e0; base < e1; base += 32) {
+      const int m = (e1 - base) < 32 ? (int)(e1 - base) : 32;
+      int my_col = 0;
+      T my_val = T(0);
+      if (lane < m) {
+        my_col = __ldg(indices + base + lane);
+        my_val = __ldg(vals + base + lane);
+      }
+#pragma unroll 4
+      for (int j = 0; j < m; ++j) {
+        const int c = __shfl_sync(0xffffffffu, my_col, j);
+        const T a = __shfl_sync(0xffffffffu, my_val, j);
+        const T* xr = X + (int64_t)c * ldx + c0;
+#pragma unroll
+        for (int u = 0; u < NV; ++u) {
+          if (live[u]) {
+            T v[VEC];
+            load_vec<T, VEC>(xr + u * 32 * VEC, v);
+#pragma unroll
+            for (int q = 0; q < VEC; ++q) acc[u][q] = mul_add_rn(acc[u][q], a, v[q]);
+          }
+        }
+      }
+    }
+    T* yr = Y + i * ldy + c0;
+#pragma unroll
+    for (int u = 0; u < NV; ++u)
+      if (live[u]) store_vec<T, VEC>(yr + u * 32 * VEC, acc[u]);
+  }
+}
+
+// Single dense column (SpMV): warp per row, lanes over nonzeros, tree reduce.
+template <typename T>
+__global__ void __launch_bounds__(256) spmv_kernel(int64_t n_rows, const int64_t* __restrict__ indptr,
+                                                   const int32_t* __restrict__ indices,
+                                                   const T* __restrict__ vals, const T* __restrict__ x,
+                                                   T* __restrict__ y, int64_t ldy) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < n_rows; i += nwarps) {
+    T acc = T(0);
+    const int64_t e1 = __ldg(indptr + i + 1);
+    for (int64_t e = __ldg(indptr + i) + lane; e < e1; e += 32)
+      acc = mul_add_rn(acc, __ldg(vals + e), __ldg(x + __ldg(indices + e)));
+#pragma unroll
+    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (!lane) y[i * ldy] = acc;
+  }
+}
+
+inline bool aligned(const void* p, int bytes) { return ((uintptr_t)p % bytes) == 0; }
+
+template <typename T>
+int launch_spmm(fsr_ctx* ctx, int64_t n_rows, const int64_t* indptr, const int32_t* indices, const T* vals,
+                int64_t ncols, const T* X, int64_t ldx, T* Y, int64_t ldy) {
+  if (n_rows <= 0 || ncols <= 0) return FSR_OK;
+  const int block = 256;
+  if (ncols == 1) {
+    spmv_kernel<T><<<grid_for(n_rows * 32, block, ctx, 8), block, 0, ctx->stream>>>(n_rows, indptr, indices,
+                                                                                      vals, X, Y, ldy);
+    return launched(ctx, "spmv_kernel");
+  }
+  constexpr int VW = sizeof(T) == 4 ? 4 : 2;  // 16-byte vectors
+  const bool vec_ok = ncols % VW == 0 && ldx % VW == 0 && ldy % VW == 0 && aligned(X, 16) && aligned(Y, 16);
+  if (vec_ok) {
+    constexpr int NV = 2;
+    constexpr int PW = 32 * VW * NV;
+    if (ncols > PW / 2) {
+      const int64_t panels = ceil_div(ncols, PW);
+      spmm_rowpanel_kernel<T, VW, NV><<<grid_for(n_rows * panels * 32, block, ctx, 8), block, 0, ctx->stream>>>(
+          n_rows, indptr, indices, vals, ncols, X, ldx, Y, ldy, panels);
+    } else {
+      const int64_t panels = ceil_div(ncols, 32 * VW);
+      spmm_rowpanel_kernel<T, VW, 1><<<grid_for(n_rows * panels * 32, block, ctx, 8), block, 0, ctx->stream>>>(
+          n_rows, indptr, indices, vals, ncols, X, ldx, Y, ldy, panels);
+    }
+  } else {
+    const int64_t panels = ceil_div(ncols, 32);
+    spmm_rowpanel_kernel<T, 1, 1><<<grid_for(n_rows * panels * 32, block, ctx, 8), block, 0, ctx->stream>>>(
+        n_rows, indptr, indices, vals, ncols, X, ldx, Y, ldy, panels);
+  }
+  return launched(ctx, "spmm_rowpanel_kernel");
+}
+
+}  // namespace fsr

@@ -1,0 +1,427 @@
+"""Offline FSR on the device: range finder, Rayleigh-Ritz, sparsification.
+
+Drop-in for the reference ``spectral`` module (``spectral.py``): the same
+function names, argument meaning, defaults, validation errors and result
+types; the arithmetic runs in libfsr (include/fsr.h) on a CUDA device.
+
+Precision: ``dtype="float64"`` (default, the reference's precision -- "parity
+mode") keeps every n x r_hat block in fp64.  ``dtype="float32"`` stores the
+blocks and runs the SpMM in fp32 while Gram, projection, Cholesky and the
+eigensolve stay fp64 ("fast mode").
+
+Device residency: ``RangeBasis.Q/B`` and ``SpectralDecomposition.U`` are
+torch CUDA tensors (``U_device``); ``SpectralDecomposition.U`` / ``.eta``
+materialise host numpy/scipy copies only when touched.
+"""
+
+from __future__ import annotations
+
+import enum
+import math
+from dataclasses import dataclass, replace
+
+import numpy as np
+import scipy.sparse as sp
+
+from . import _native as N
+from .graph import ComponentLabeling
+from .sparsemat import DeviceCSR, SparseSymmetricMatrix
+
+DEFAULT_OVERSAMPLING = 10
+DEFAULT_POWER_ITERATIONS = 4
+DENSE_GUARD = 4096
+
+# re-orthogonalisation trigger of spectral.py:167 (fp64); fp32 blocks cannot
+# be orthonormal beyond ~1e-7, so their trigger is scaled accordingly.
+ORTH_TOL = {N.F64: 1e-8, N.F32: 1e-4}
+# CholeskyQR2 is orthogonal to O(eps) when the second Gram is this close to I
+# (Yamamoto et al. 2015); beyond it an explicit check runs (spectral.py:167).
+CHOLQR2_SAFE = 0.1
+
+_MASK64 = (1 << 64) - 1
+
+
+class NumericalError(RuntimeError):
+    """A computation left its supported regime (guards, non-finite values)."""
+
+
+class Variant(str, enum.Enum):
+    EXACT = "exact"
+    RANK_R = "rank_r"
+    APPROX = "approx"
+    SPARSE = "sparse"
+
+
+@dataclass(frozen=True)
+class Provenance:
+    r: int | None = None
+    p: int | None = None
+    q: int | None = None
+    tau: int | None = None
+    seed: int | None = None
+
+
+@dataclass(frozen=True, eq=False)
+class RangeBasis:
+    """Q orthonormal (n x r_hat) and B = A Q, as device tensors."""
+
+    Q: object
+    B: object
+    iterations_used: int
+    seed: int | None = None
+
+    @property
+    def r_hat(self) -> int:
+        return int(self.Q.shape[1])
+
+
+class SpectralDecomposition:
+    """Rank-r eigenpair approximation U diag(eigenvalues) U^T of A.
+
+    ``U_device`` is a dense CUDA tensor (n x r) or a ``DeviceCSR`` after
+    sparsification; ``eta_device`` the float64 row norms on the device.  The
+    reference-facing attributes ``U`` (numpy / scipy CSR, float64) and ``eta``
+    are host copies made on first access.
+    """
+
+    def __init__(self, U_device, eigenvalues, eta_device, components, variant, provenance):
+        self.U_device = U_device
+        self.eigenvalues = np.asarray(eigenvalues, dtype=np.float64)
+        self.eta_device = eta_device
+        self.components = components
+        self.variant = Variant(variant)
+        self.provenance = provenance
+        self._U_host = None
+        self._eta_host = None
+
+    @property
+    def n(self) -> int:
+        return int(self.U_device.shape[0])
+
+    @property
+    def r(self) -> int:
+        return int(self.U_device.shape[1])
+
+    @property
+    def is_sparse(self) -> bool:
+        return isinstance(self.U_device, DeviceCSR)
+
+    @property
+    def dtype(self):
+        return self.U_device.dtype if not self.is_sparse else self.U_device.values.dtype
+
+    @property
+    def U(self):
+        if self._U_host is None:
+            if self.is_sparse:
+                self._U_host = self.U_device.to_scipy()
+            else:
+                self._U_host = self.U_device.double().cpu().numpy()
+        return self._U_host
+
+    @property
+    def eta(self) -> np.ndarray:
+        if self._eta_host is None:
+            self._eta_host = self.eta_device.cpu().numpy()
+        return self._eta_host
+
+    def dense_u(self) -> np.ndarray:
+        return self.U.toarray() if self.is_sparse else self.U
+
+    @classmethod
+    def from_host(cls, dec, dtype="float64", device=None) -> "SpectralDecomposition":
+        """Upload a reference (or any duck-typed) decomposition to the device."""
+        import torch
+
+        if isinstance(dec, cls):
+            return dec
+        dt = N.torch_dtype(dtype)
+        device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+        U = dec.U
+        if sp.issparse(U):
+            Ud = DeviceCSR.from_scipy(sp.csr_matrix(U), dt, device)
+        else:
+            Ud = torch.as_tensor(np.ascontiguousarray(U, dtype=np.float64)).to(device=device, dtype=dt)
+        eta = torch.as_tensor(np.asarray(dec.eta, dtype=np.float64)).to(device)
+        variant = Variant(getattr(dec.variant, "value", dec.variant))
+        prov = getattr(dec, "provenance", None)
+        prov = Provenance(**{f: getattr(prov, f, None) for f in ("r", "p", "q", "tau", "seed")}) if prov else Provenance()
+        comps = getattr(dec, "components", None) or ComponentLabeling.trivial(Ud.shape[0])
+        return cls(Ud, dec.eigenvalues, eta, comps, variant, prov)
+
+
+# ---------------------------------------------------------------------------
+# K0: start block
+# ---------------------------------------------------------------------------
+
+def philox_key(seed: int):
+    """The Philox key numpy derives for ``Philox(seed)`` (SeedSequence state)."""
+    words = np.random.SeedSequence(seed & _MASK64).generate_state(2, np.uint64)
+    return int(words[0]), int(words[1])
+
+
+def gaussian_block(rows: int, cols: int, seed: int, row_begin: int = 0, row_end: int | None = None,
+                   dtype="float64", device=None, out=None):
+    """Rows [row_begin, row_end) of ``gaussian_matrix(rows, cols, seed)`` on the device."""
+    import torch
+
+    row_end = rows if row_end is None else row_end
+    dt = N.torch_dtype(dtype)
+    if out is None:
+        out = torch.empty(row_end - row_begin, cols, dtype=dt,
+                          device=device if device is not None else torch.cuda.current_device())
+    ctx = N.Context.get(out.device)
+    k0, k1 = philox_key(seed)
+    ctx.call("gaussian_block", N.dtype_code(dt), rows, cols, row_begin, row_end, k0, k1, N.ptr(out))
+    return out
+
+
+def gaussian_matrix(rows: int, cols: int, seed: int, dtype="float64", device=None):
+    """Standard Gaussian block from the counter-based stream (``spectral.py:55-65``), on the device."""
+    return gaussian_block(rows, cols, seed, dtype=dtype, device=device)
+
+
+# ---------------------------------------------------------------------------
+# K3: orthonormalisation
+# ---------------------------------------------------------------------------
+
+def _gram(ctx, dt, Y, G, accumulate=False):
+    n, k = Y.shape
+    ctx.call("gram", dt, n, k, N.ptr(Y), Y.stride(0), N.ptr(G), int(accumulate))
+
+
+def _max_dev(ctx, G) -> float:
+    import ctypes
+
+    err = ctypes.c_double()
+    ctx.call("max_offdiag_error", G.shape[0], N.ptr(G), ctypes.byref(err))
+    return err.value
+
+
+def _cholqr_pass(ctx, dt, Y, G, gram_hook=None) -> tuple[bool, float]:
+    """One CholeskyQR pass in place: Y <- Y R^-1.  Returns (ok, max|G - I|)."""
+    _gram(ctx, dt, Y, G)
+    if gram_hook is not None:
+        gram_hook(G)
+    dev = _max_dev(ctx, G)
+    st = ctx.call("cholesky", G.shape[0], N.ptr(G))
+    if st == N.ENOTSPD:
+        return False, dev
+    ctx.call("apply_rinv", dt, Y.shape[0], Y.shape[1], N.ptr(G), N.ptr(Y), Y.stride(0))
+    return True, dev
+
+
+def orthonormalize(Y, ctx=None, stats=None):
+    """Replace Y by an orthonormal basis of its span (CholeskyQR2, Householder fallback).
+
+    Mirrors ``spectral.py:165-169``: the result is checked against the
+    re-orthogonalisation trigger and re-factorised when it fails.
+    """
+    import torch
+
+    ctx = ctx or N.Context.get(Y.device)
+    dt = N.dtype_code(Y.dtype)
+    n, k = Y.shape
+    G = torch.empty(k, k, dtype=torch.float64, device=Y.device)
+    ok1, _ = _cholqr_pass(ctx, dt, Y, G)
+    ok2, dev2 = _cholqr_pass(ctx, dt, Y, G) if ok1 else (False, math.inf)
+    method = "cholqr2"
+    if not (ok1 and ok2):
+        ctx.call("householder_qr", dt, n, k, N.ptr(Y), Y.stride(0))
+        method = "householder"
+        dev2 = math.inf
+    if dev2 > CHOLQR2_SAFE:
+        _gram(ctx, dt, Y, G)
+        if _max_dev(ctx, G) > ORTH_TOL[dt]:
+            ctx.call("householder_qr", dt, n, k, N.ptr(Y), Y.stride(0))
+            method += "+householder"
+    if stats is not None:
+        stats.append(method)
+    return Y
+
+
+# ---------------------------------------------------------------------------
+# range finder / Rayleigh-Ritz / decompose
+# ---------------------------------------------------------------------------
+
+def _spmm(ctx, dt, Ad: DeviceCSR, X, Y):
+    ctx.call("csr_spmm", dt, Ad.shape[0], N.ptr(Ad.indptr), N.ptr(Ad.indices), N.ptr(Ad.values), X.shape[1],
+             N.ptr(X), X.stride(0), N.ptr(Y), Y.stride(0))
+
+
+def range_finder(A, r_hat: int, q: int, seed: int, dtype="float64", device=None, stats=None) -> RangeBasis:
+    """Simultaneous iteration (``spectral.py:147-171``) on the device.
+
+    Start block from the seeded counter stream (K0); q rounds of
+    {orthonormalise (K3), B = A Q (K2)}.  Returns the last Q and B = A Q.
+    """
+    import torch
+
+    A = SparseSymmetricMatrix.coerce(A)
+    n = A.n
+    if r_hat < 1 or r_hat > n:
+        raise ValueError(f"r_hat must lie in [1, n], got {r_hat} for n={n}")
+    if q < 1:
+        raise ValueError("q must be at least 1")
+    dt_t = N.torch_dtype(dtype)
+    Ad = A.device(dt_t, device)
+    ctx = N.Context.get(Ad.device)
+    dt = N.dtype_code(dt_t)
+    Y = gaussian_block(n, r_hat, seed, dtype=dt_t, device=Ad.device)
+    Q = torch.empty_like(Y)
+    for _ in range(q):
+        orthonormalize(Y, ctx, stats)
+        Q, Y = Y, Q  # Y now holds the orthonormal block
+        _spmm(ctx, dt, Ad, Q, Y)
+    return RangeBasis(Q=Q, B=Y, iterations_used=q, seed=seed)
+
+
+def _rayleigh_ritz(ctx, dt, Q, B, r):
+    """C = Q^T B, eigh, U = Q V, sign fix, eta (K4-K6). Returns (U, lam, eta)."""
+    import torch
+
+    n, k = Q.shape
+    C = torch.empty(k, k, dtype=torch.float64, device=Q.device)
+    ctx.call("cross", dt, n, k, N.ptr(Q), Q.stride(0), N.ptr(B), B.stride(0), N.ptr(C), 0)
+    lam = np.empty(r, dtype=np.float64)
+    V = torch.empty(k, r, dtype=torch.float64, device=Q.device)
+    ctx.call("eigh_desc", k, N.ptr(C), r, lam.ctypes.data_as(N._c_dp), N.ptr(V))
+    del C
+    U = torch.empty(n, r, dtype=Q.dtype, device=Q.device)
+    ctx.call("lift", dt, n, k, r, N.ptr(Q), Q.stride(0), N.ptr(V), N.ptr(U), U.stride(0))
+    best_abs = torch.empty(r, dtype=torch.float64, device=Q.device)
+    best_row = torch.empty(r, dtype=torch.int64, device=Q.device)
+    best_val = torch.empty(r, dtype=torch.float64, device=Q.device)
+    ctx.call("col_absmax", dt, n, r, N.ptr(U), U.stride(0), 0, N.ptr(best_abs), N.ptr(best_row), N.ptr(best_val))
+    eta = torch.empty(n, dtype=torch.float64, device=Q.device)
+    ctx.call("apply_signs_rownorm", dt, n, r, N.ptr(U), U.stride(0), N.ptr(best_val), N.ptr(eta))
+    return U, lam, eta
+
+
+def approx_eigendecomposition(A, basis: RangeBasis, r: int) -> SpectralDecomposition:
+    """Rayleigh-Ritz step (``spectral.py:174-198``) on the device."""
+    if r < 1 or r > basis.r_hat:
+        raise ValueError(f"r must lie in [1, r_hat={basis.r_hat}], got {r}")
+    A = SparseSymmetricMatrix.coerce(A)
+    Q, B = basis.Q, basis.B
+    if Q.shape[0] != A.n:
+        raise ValueError("basis dimension does not match A")
+    ctx = N.Context.get(Q.device)
+    U, lam, eta = _rayleigh_ritz(ctx, N.dtype_code(Q.dtype), Q, B, r)
+    return SpectralDecomposition(U, lam, eta, ComponentLabeling.trivial(A.n), Variant.APPROX,
+                                 Provenance(r=r, p=basis.r_hat - r, q=basis.iterations_used, seed=basis.seed))
+
+
+def decompose(A, r: int, p: int = DEFAULT_OVERSAMPLING, q: int = DEFAULT_POWER_ITERATIONS, seed: int = 0,
+              dtype="float64", device=None) -> SpectralDecomposition:
+    """Stages 1-2 (``spectral.py:297-309``): r_hat = min(r + p, n)."""
+    A = SparseSymmetricMatrix.coerce(A)
+    r_hat = min(r + p, A.n)
+    if r > r_hat:
+        raise ValueError(f"r={r} exceeds n={A.n}")
+    basis = range_finder(A, r_hat, q, seed, dtype=dtype, device=device)
+    dec = approx_eigendecomposition(A, basis, r)
+    del basis
+    return dec
+
+
+# ---------------------------------------------------------------------------
+# K7: sparsify
+# ---------------------------------------------------------------------------
+
+HIST_BITS = 12
+
+
+def key_bits(dt: int) -> int:
+    return 63 if dt == N.F64 else 31
+
+
+def select_threshold(hist_fn, dt: int, tau: int):
+    """Radix-select the tau-th largest |u| key.
+
+    ``hist_fn(prefix, shift, bits) -> np.uint64[2**bits]`` returns the
+    (globally summed) digit histogram of nonzero keys matching ``prefix``.
+    Returns (T, ties_to_take, keep): keep = min(tau, nnz) entries are the keys
+    > T plus the first ``ties_to_take`` keys == T in (row, col) order.
+    """
+    kb = key_bits(dt)
+    shift = kb - HIST_BITS
+    h = hist_fn(0, shift, HIST_BITS)
+    nnz = int(h.sum())
+    keep = min(tau, nnz)
+    if keep == nnz:
+        return 0, 0, keep
+    need = keep
+    prefix = 0
+    bits = HIST_BITS
+    while True:
+        cum = np.cumsum(h[::-1].astype(np.int64))
+        pos = int(np.searchsorted(cum, need))  # first bin (from the top) reaching need
+        b = (1 << bits) - 1 - pos
+        above = int(cum[pos] - h[b])
+        need -= above
+        prefix |= b << shift
+        if shift == 0:
+            return prefix, need, keep
+        bits = min(HIST_BITS, shift)
+        shift -= bits
+        h = hist_fn(prefix, shift, bits)
+
+
+def sparsify(dec: SpectralDecomposition, tau: int) -> SpectralDecomposition:
+    """Keep the tau largest-magnitude entries of U, ties in (row, col) order
+    (``spectral.py:269-294``); eta is recomputed from the kept U."""
+    import torch
+
+    if not isinstance(dec, SpectralDecomposition):
+        dec = SpectralDecomposition.from_host(dec)
+    if dec.variant is Variant.SPARSE:
+        raise ValueError("decomposition is already sparse")
+    if tau < 1:
+        raise ValueError("tau must be positive")
+    U = dec.U_device
+    n, r = U.shape
+    ctx = N.Context.get(U.device)
+    dt = N.dtype_code(U.dtype)
+
+    def hist_fn(prefix, shift, bits):
+        h = torch.zeros(1 << bits, dtype=torch.int64, device=U.device)
+        ctx.call("abs_histogram", dt, n, r, N.ptr(U), U.stride(0), prefix, shift, bits, N.ptr(h))
+        return h.cpu().numpy().astype(np.uint64)
+
+    T, ties, keep = select_threshold(hist_fn, dt, tau)
+    Ut, eta = compact_rows(ctx, dt, U, T, 0, ties, keep)
+    return SpectralDecomposition(Ut, dec.eigenvalues, eta, dec.components, Variant.SPARSE,
+                                 replace(dec.provenance, tau=tau))
+
+
+def compact_rows(ctx, dt, U, T, tie_offset, ties_to_take, capacity, counts=None):
+    """Count + compact the kept entries of the local rows of U into a DeviceCSR."""
+    import ctypes
+
+    import torch
+
+    n, r = U.shape
+    if counts is None:
+        gt = torch.empty(n, dtype=torch.int64, device=U.device)
+        eq = torch.empty(n, dtype=torch.int64, device=U.device)
+        ctx.call("threshold_counts", dt, n, r, N.ptr(U), U.stride(0), T, N.ptr(gt), N.ptr(eq))
+    else:
+        gt, eq = counts
+    indptr = torch.empty(n + 1, dtype=torch.int64, device=U.device)
+    cap = max(1, int(capacity))
+    indices = torch.empty(cap, dtype=torch.int32, device=U.device)
+    values = torch.empty(cap, dtype=U.dtype, device=U.device)
+    eta = torch.empty(n, dtype=torch.float64, device=U.device)
+    nnz = ctypes.c_int64()
+    ctx.call("threshold_compact", dt, n, r, N.ptr(U), U.stride(0), T, tie_offset, ties_to_take, N.ptr(gt),
+             N.ptr(eq), N.ptr(indptr), N.ptr(indices), N.ptr(values), N.ptr(eta), ctypes.byref(nnz))
+    k = int(nnz.value)
+    return DeviceCSR(indptr, indices[:k], values[:k], (n, r)), eta
+
+
+def row_norms(U) -> np.ndarray:
+    """Host helper matching ``spectral.py:127-130``."""
+    if sp.issparse(U):
+        return np.sqrt(np.asarray(U.multiply(U).sum(axis=1)).ravel())
+    return np.linalg.norm(U, axis=1)

@@ -1,0 +1,53 @@
+"""CPU-side checks of the C-ABI boundary: the library loads and exports every
+entry point declared in include/fsr.h; the ctypes table covers all of them."""
+
+import ctypes
+import os
+import re
+
+import pytest
+
+from paper_1703_06935_b200 import _native
+
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def header_functions():
+    text = open(os.path.join(REPO, "include", "fsr.h")).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(fsr_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_header_declares_entry_points():
+    names = header_functions()
+    assert "fsr_csr_spmm" in names and "fsr_filter_batch" in names and len(names) >= 25
+
+
+def test_library_exports_every_header_symbol():
+    if not os.path.exists(_native.LIB_PATH):
+        from paper_1703_06935_b200 import build
+
+        build.build()
+    lib = ctypes.CDLL(_native.LIB_PATH)
+    missing = [n for n in header_functions() if not hasattr(lib, n)]
+    assert not missing, missing
+
+
+def test_ctypes_table_matches_header():
+    assert sorted(_native.EXPORTED) == header_functions()
+
+
+def test_load_library_and_version():
+    lib = _native.load_library()
+    assert lib.fsr_abi_version() == 1
+    # pure-host helper, no device needed
+    assert lib.fsr_filter_workspace_bytes(1, 100, 10, 4, 1) > 0
+
+
+def test_no_cuda_device_fails_loudly():
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    with pytest.raises(RuntimeError):
+        _native.Context.get(0)
