@@ -76,13 +76,43 @@ __global__ void gaussian_kernel(int64_t count, int64_t half, int64_t f0, int64_t
   }
 }
 
+// numpy's pairwise summation (numpy/_core/src/umath/loops_utils.h.src,
+// pairwise_sum): < 8 terms sequential from 0; <= 128 terms eight strided
+// accumulators combined as ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) plus a
+// sequential tail; longer runs split at n/2 rounded down to a multiple of 8.
+__device__ double pairwise_sum(const double* a, int64_t n) {
+  if (n < 8) {
+    double res = 0.0;
+    for (int64_t i = 0; i < n; ++i) res = __dadd_rn(res, a[i]);
+    return res;
+  }
+  if (n <= 128) {
+    double r[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) r[j] = a[j];
+    int64_t i = 8;
+    for (; i < n - (n % 8); i += 8)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], a[i + j]);
+    double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                           __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+    for (; i < n; ++i) res = __dadd_rn(res, a[i]);
+    return res;
+  }
+  int64_t n2 = n / 2;
+  n2 -= n2 % 8;
+  return __dadd_rn(pairwise_sum(a, n2), pairwise_sum(a + n2, n - n2));
+}
+
+// Degrees exactly as the reference computes them: W.sum(axis=1) on a CSR
+// matrix reduces each nonempty row with np.add.reduceat, i.e. a[0] +
+// pairwise_sum(a[1:]) (graph.py:121 -> scipy _cs_matrix.sum/_minor_reduce).
 __global__ void row_sums_kernel(int64_t n_rows, const int64_t* __restrict__ indptr,
                                 const double* __restrict__ data, double* __restrict__ deg) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_rows;
        i += (int64_t)gridDim.x * blockDim.x) {
-    double s = 0.0;
-    for (int64_t e = indptr[i]; e < indptr[i + 1]; ++e) s = __dadd_rn(s, data[e]);
-    deg[i] = s;
+    const int64_t e0 = indptr[i], len = indptr[i + 1] - e0;
+    deg[i] = len ? __dadd_rn(data[e0], pairwise_sum(data + e0 + 1, len - 1)) : 0.0;
   }
 }
 

@@ -57,7 +57,7 @@ def test_normalize_bitwise(golden):
     W, S = c1_mats(g)
     A = SparseSymmetricMatrix.from_scipy(W)
     deg = graph.degrees(A)
-    np.testing.assert_allclose(deg, O.degrees(W), rtol=1e-15)
+    np.testing.assert_array_equal(deg, O.degrees(W))
     Sd = graph.normalize_adjacency(A, deg)
     np.testing.assert_array_equal(Sd.csr.data, S.data)
 
@@ -166,9 +166,18 @@ def test_kat_random_decompose(golden, dtype, tol):
     # column signs are fixed by the same rule; compare directly
     assert np.abs(U - k["rand_U"]).max() < (1e-8 if dtype == "float64" else 1e-4)
     np.testing.assert_allclose(dec.eta, k["rand_eta"], atol=tol * 10)
-    # exact dense eigh oracle
+
+
+@pytest.mark.parametrize("dtype,tol", [("float64", 1e-10), ("float32", 1e-5)])
+def test_kat_full_rank_reproduces_exact_spectrum(golden, dtype, tol):
+    # q >= 8 with r_hat = n reproduces the exact eigenvalues
+    k = golden("kat")
+    A = SparseSymmetricMatrix.from_dense(k["rand_W_dense"])
+    dec = spectral.decompose(A, 16, p=48, q=8, seed=3, dtype=dtype)
     ev = np.sort(np.linalg.eigvalsh(k["rand_W_dense"]))[::-1][:16]
-    assert np.abs(dec.eigenvalues - ev).max() < 1e-3
+    assert np.abs(dec.eigenvalues - ev).max() < tol
+    U = dec.U
+    assert np.abs(U.T @ U - np.eye(16)).max() < (1e-12 if dtype == "float64" else 1e-6)
 
 
 def test_kat_random_sparsify_and_filter(golden):
