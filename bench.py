@@ -1,0 +1,432 @@
+#!/usr/bin/env python
+"""FSR hot-path benchmark on B200 (one JSON line on rank 0).
+
+Headline (BASELINE.json metric "... online ranked queries/sec at n=1M"):
+ranked queries per second of the online path -- K8 projection, K9 sparse
+filtering, copy-uncovered, exact top-100 -- on the sparsified decomposition
+of config C3 (n=1e6, r=5000, U~ density 2%), one step = one batch of b
+k=50-sparse queries.  The offline part of the metric (simultaneous-iteration
+time and SpMM HBM GB/s) is measured in the same run and reported under
+"offline".
+
+    python bench.py [--gpus N --steps K --warmup W] [--config C2|C3] [--impl reference]
+
+Under torchrun each rank builds the same inputs, runs the offline pipeline as
+a replica and answers its own query batches (weak scaling: b queries per GPU
+per step); `value` = all ranks' queries / max-over-ranks device time.
+
+`--impl reference` times the reference's CPU path (the oracle port of
+``ranking.filter`` + ``rank``, /root/reference is absent on the GPU box) on a
+structure-equivalent synthetic decomposition (same n, r, tau) on host cores.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+METRIC = "online ranked queries/sec at n=1M (+ offline SI time & SpMM HBM GB/s)"
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="fsr", choices=["fsr", "reference"])
+    ap.add_argument("--config", default="C3", choices=["C1", "C2", "C3"])
+    ap.add_argument("--n", type=int, default=None, help="override n (development)")
+    ap.add_argument("--batch", type=int, default=1024)
+    ap.add_argument("--density", type=float, default=None)
+    ap.add_argument("--topk", type=int, default=100)
+    ap.add_argument("--dtype", default="float32", choices=["float32", "float64"])
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--skip-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def load_peaks():
+    path = os.path.join(REPO, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi sampling of SM clocks and throttle reasons while the bench runs."""
+
+    FIELDS = ["clocks.sm", "clocks.max.sm", "power.draw", "clocks_event_reasons.hw_slowdown",
+              "clocks_event_reasons.hw_thermal_slowdown", "clocks_event_reasons.sw_thermal_slowdown",
+              "clocks_event_reasons.sw_power_cap"]
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+
+    def __init__(self, index: int):
+        self.lines = []
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(index), "--query-gpu=" + ",".join(self.FIELDS),
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], None, set()
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < len(self.FIELDS):
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for name, flag in zip(self.NAMES, parts[3:]):
+                if flag.lower().startswith("active"):
+                    reasons.add(name)
+        if not sm:
+            return None
+        loaded = [s for s in sm if mx and s >= 0.5 * mx] or sm
+        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# reference arm: the CPU oracle port of the reference's online path
+# ---------------------------------------------------------------------------
+
+def synthetic_sparse_decomposition(n, r, tau, seed=7):
+    import scipy.sparse as sp
+
+    rng = np.random.default_rng(seed)
+    per = max(1, tau // n)
+    cols = rng.integers(0, r, size=(n, per)).astype(np.int32)
+    cols.sort(axis=1)
+    vals = rng.standard_normal((n, per)) / math.sqrt(per)
+    indptr = np.arange(0, n * per + 1, per, dtype=np.int64)
+    U = sp.csr_matrix((vals.ravel(), cols.ravel(), indptr), shape=(n, r))
+    U.sum_duplicates()
+    lam = np.sort(rng.uniform(-0.2, 1.0, r))[::-1].copy()
+    eta = np.sqrt(np.asarray(U.multiply(U).sum(axis=1)).ravel())
+    return U, lam, eta
+
+
+def synthetic_queries(n, b, k, seed=11):
+    rng = np.random.default_rng(seed)
+    ys = []
+    for _ in range(b):
+        idx = np.unique(rng.integers(0, n, size=k))
+        ys.append((idx.astype(np.int64), rng.random(idx.size) ** 3))
+    return ys
+
+
+def time_oracle_queries(U, lam, eta, ys, alpha, budget_s, topk):
+    """Reference per-query path: filter (ranking.py:229-255) + rank[:topk] (ranking.py:390-395)."""
+    from oracle import fsr_oracle as O
+
+    w = O.transfer_values(O.h_alpha(alpha), lam)
+    done, t0 = 0, time.perf_counter()
+    while done < len(ys):
+        idx, val = ys[done % len(ys)]
+        x = O.filter_scores(U, lam, eta, w, idx, val)
+        O.rank(x)[:topk]
+        done += 1
+        if time.perf_counter() - t0 > budget_s and done >= 2:
+            break
+    return done, time.perf_counter() - t0
+
+
+def run_reference(args, cfg, n, rank, world):
+    if rank != 0:
+        return
+    r = cfg.r
+    density = args.density if args.density is not None else cfg.density
+    tau = int(round(density * n * r))
+    U, lam, eta = synthetic_sparse_decomposition(n, r, tau)
+    ys = synthetic_queries(n, max(args.steps + args.warmup, 4), cfg.y_top)
+    # warm-up queries (untimed), then one query per step
+    time_oracle_queries(U, lam, eta, ys[:args.warmup], cfg.alpha, 1e9, args.topk)
+    done, secs = time_oracle_queries(U, lam, eta, ys[args.warmup:args.warmup + args.steps], cfg.alpha, 1e9,
+                                     args.topk)
+    qps = done / secs
+    cores = 1
+    line = {
+        "metric": METRIC, "value": qps, "unit": "queries/s", "n_gpus": args.gpus, "steps": done,
+        "warmup": args.warmup, "ms_per_step": 1e3 * secs / done, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
+        "config": {"workload": f"{cfg.name}/C5 online: oracle port of ranking.filter + rank on a synthetic "
+                               f"U~ with n={n}, r={r}, tau={tau} (density {density}), k={cfg.y_top}-sparse y, "
+                               f"h_alpha({cfg.alpha}), top-{args.topk}",
+                   "step": "one query (reference has no batch API)"},
+        "cpu_baseline": {"value": qps, "unit": "queries/s", "cores": cores, "kind": "port",
+                         "sample": f"{done} queries, {secs:.1f} s, scipy csr_matvec (single-threaded)"},
+        "e2e": {"value": qps, "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# FSR arm
+# ---------------------------------------------------------------------------
+
+def build_inputs(cfg, n, n_queries, device, dtype):
+    import torch
+
+    from paper_1703_06935_b200 import graph, knn, workloads
+
+    t0 = time.perf_counter()
+    X, Qv, _ = workloads.device_cluster_descriptors(cfg, device, n=n, queries=n_queries)
+    W = knn.mutual_knn_graph_device(X, cfg.k, cfg.gamma)
+    deg = graph.degrees_device(W, device)
+    S = graph.normalize_adjacency(W, deg, dtype=dtype, device=device)
+    y_ptr, y_idx, y_val = knn.observation_batch_device(Qv, X, cfg.y_top, cfg.gamma)
+    del X, Qv
+    torch.cuda.synchronize()
+    return S, (y_ptr, y_idx, y_val), time.perf_counter() - t0, int(W.nnz), int((deg == 0).sum())
+
+
+def max_over_ranks(x, world):
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+
+
+def run_fsr(args, cfg, n, rank, world, local_rank):
+    import torch
+
+    from paper_1703_06935_b200 import _native as N
+    from paper_1703_06935_b200 import ranking, spectral
+
+    device = torch.device("cuda", local_rank)
+    torch.cuda.set_device(device)
+    peak_gbs, peak_kind = load_peaks()
+    dt = args.dtype
+    es = 4 if dt == "float32" else 8
+    density = args.density if args.density is not None else cfg.density
+    r, r_hat, q = cfg.r, min(cfg.r + cfg.p, n), cfg.q
+    tau = int(round(density * n * r))
+    b = args.batch
+    n_batches = 4
+    n_queries = b * n_batches * world
+
+    S, (y_ptr, y_idx, y_val), t_inputs, nnz_w, isolated = build_inputs(cfg, n, n_queries, device, dt)
+    all_queries = ranking.QueryBatch(n, y_ptr, y_idx, y_val)
+    ctx = N.Context.get(device)
+
+    # ---------------- offline: SI + Rayleigh-Ritz + sparsify (timed once) ----
+    ctx.enable_timing(True)
+    ctx.stage_reset()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+    torch.cuda.synchronize()
+    ev[0].record()
+    basis = spectral.range_finder(S, r_hat, q, 0, dtype=dt, device=device)
+    ev[1].record()
+    dec = spectral.approx_eigendecomposition(S, basis, r)
+    del basis
+    ev[2].record()
+    sdec = spectral.sparsify(dec, tau)
+    ev[3].record()
+    torch.cuda.synchronize()
+    stages = {name: ctx.stage_time(name) for name in N.STAGES}
+    del dec
+    torch.cuda.empty_cache()
+    si_s = ev[0].elapsed_time(ev[1]) / 1e3
+    rr_s = ev[1].elapsed_time(ev[2]) / 1e3
+    sp_s = ev[2].elapsed_time(ev[3]) / 1e3
+    spmm_ms, spmm_cnt = stages["spmm"]
+    spmm_ms_iter = spmm_ms / max(spmm_cnt, 1)
+    nnz_s = S.nnz
+    spmm_bytes = nnz_s * (es + 4) + (n + 1) * 8 + 2 * es * n * r_hat
+    spmm_gbs = spmm_bytes / (spmm_ms_iter * 1e-3) / 1e9
+    offline = {
+        "si_time_s": si_s, "rayleigh_ritz_s": rr_s, "sparsify_s": sp_s, "decompose_total_s": si_s + rr_s + sp_s,
+        "spmm_ms_per_iter": spmm_ms_iter, "spmm_launches": spmm_cnt, "spmm_algorithmic_bytes": spmm_bytes,
+        "spmm_gbs": spmm_gbs, "spmm_hbm_frac": spmm_gbs / peak_gbs,
+        "spmm_fp32_tflops": 2.0 * nnz_s * r_hat / (spmm_ms_iter * 1e-3) / 1e12,
+        "stage_ms": {k: round(v[0], 3) for k, v in stages.items() if v[1]},
+        "nnz_W": nnz_w, "isolated_vertices": isolated, "kept_nnz": sdec.U_device.nnz, "inputs_build_s": t_inputs,
+    }
+
+    # ---------------- online: device-resident batches ------------------------
+    h = ranking.h_alpha(cfg.alpha)
+    per_rank = [all_queries.split(world * n_batches, rank * n_batches + i) for i in range(n_batches)]
+    dqs = [ranking.DeviceQueries(qb, sdec.dtype, device) for qb in per_rank]
+    K = args.topk
+    res = ranking.FilterResult(top_idx=torch.empty(b, K, dtype=torch.int64, device=device),
+                               top_val=torch.empty(b, K, dtype=sdec.dtype, device=device))
+    ws = torch.empty(int(ctx.lib.fsr_filter_workspace_bytes(N.dtype_code(sdec.dtype), n, r, b, 1)),
+                     dtype=torch.uint8, device=device)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=device)  # > L2 (126 MB)
+
+    def step(i):
+        ranking.filter_device(sdec, h, dqs[i % n_batches], topk=K, want_x=False, out=res, workspace=ws)
+
+    clocks = ClockSampler(local_rank)
+    for i in range(args.warmup):
+        step(i)
+    torch.cuda.synchronize()
+    ctx.stage_reset()
+    launches0 = ctx.launches
+    barrier(world)
+    torch.cuda.synchronize()
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    for i in range(args.steps):
+        flush.zero_()  # untimed: evict U~ / Zs from L2 between steps
+        starts[i].record()
+        step(i)
+        ends[i].record()
+    torch.cuda.synchronize()
+    barrier(world)
+    launches = ctx.launches - launches0
+    dev_ms = sum(s.elapsed_time(e) for s, e in zip(starts, ends))
+    on_stages = {name: ctx.stage_time(name) for name in ("project", "filter_spmm", "transpose",
+                                                          "copy_uncovered", "topk")}
+    dev_ms_max = max_over_ranks(dev_ms, world)
+    value = world * b * args.steps / (dev_ms_max / 1e3)
+
+    # roofline of the dominant kernel: K9 (sparse U~ x Zs)
+    k9_ms, k9_cnt = on_stages["filter_spmm"]
+    k9_ms_launch = k9_ms / max(k9_cnt, 1)
+    kept = sdec.U_device.nnz
+    k9_bytes = kept * (es + 4) + (n + 1) * 8 + es * r * b + es * n * b
+    k9_gbs = k9_bytes / (k9_ms_launch * 1e-3) / 1e9
+    k9_share = k9_ms / max(sum(v[0] for v in on_stages.values()), 1e-9)
+
+    # ---------------- e2e through the public API with host buffers ----------
+    e2e = None
+    if not args.skip_e2e:
+        host_batches = per_rank
+        for i in range(args.warmup):
+            qd = ranking.DeviceQueries(host_batches[i % n_batches], sdec.dtype, device)
+            ranking.filter_device(sdec, h, qd, topk=K, want_x=False, out=res, workspace=ws)
+            res.top_idx.cpu()
+        torch.cuda.synchronize()
+        barrier(world)
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record()
+        h2d = d2h = 0
+        for i in range(args.steps):
+            qd = ranking.DeviceQueries(host_batches[i % n_batches], sdec.dtype, device)
+            ranking.filter_device(sdec, h, qd, topk=K, want_x=False, out=res, workspace=ws)
+            ti, tv = res.top_idx.cpu(), res.top_val.cpu()
+            h2d += qd.h2d_bytes
+            d2h += ti.numel() * 8 + tv.numel() * tv.element_size()
+        t1.record()
+        torch.cuda.synchronize()
+        e2e_ms = max_over_ranks(t0.elapsed_time(t1), world)
+        e2e = {"value": world * b * args.steps / (e2e_ms / 1e3), "unit": "queries/s",
+               "h2d_bytes_per_step": h2d // args.steps, "d2h_bytes_per_step": d2h // args.steps,
+               "api": "ranking.DeviceQueries (pinned H2D) + ranking.filter_device(topk) + top-k D2H"}
+    clk = clocks.stop()
+
+    # ---------------- CPU baseline (rank 0, N=1) -----------------------------
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        Uh = sdec.U_device.to_scipy()
+        eta = sdec.eta
+        ys = [(all_queries.y_idx[all_queries.y_ptr[j]:all_queries.y_ptr[j + 1]],
+               all_queries.y_val[all_queries.y_ptr[j]:all_queries.y_ptr[j + 1]]) for j in range(64)]
+        done, secs = time_oracle_queries(Uh, sdec.eigenvalues, eta, ys, cfg.alpha, args.cpu_seconds, K)
+        cpu = {"value": done / secs, "unit": "queries/s", "cores": 1, "kind": "port",
+               "sample": f"{done} queries of this workload on the GPU-produced U~ (scipy CSR f64), "
+                         f"oracle filter + rank, {secs:.1f} s"}
+
+    if rank != 0:
+        return
+    line = {
+        "metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": dev_ms_max / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32" if dt == "float32" else "f64",
+        "data": "synthetic (seeded Gaussian clusters, BASELINE config shapes; datasets absent)",
+        "config": {"workload": f"{cfg.name}/C5: n={n}, d={cfg.d}, k={cfg.k}, r={r}, p={cfg.p}, q={q}, "
+                               f"U~ density {density} (tau={tau}), batch b={b} per GPU, y {cfg.y_top}-sparse, "
+                               f"h_alpha({cfg.alpha}), top-{K}",
+                   "global_batch": b * world, "parallelism": f"replicas x{world} (batch split)",
+                   "l2": "256 MB buffer written between timed steps (L2 flush); U~ itself > L2"},
+        "roofline": {"kernel": "K9 filter SpMM (spmm_rowpanel_kernel on U~ x Zs)", "bound": "hbm",
+                     "achieved": k9_gbs, "peak": peak_gbs, "unit": "GB/s", "frac": k9_gbs / peak_gbs,
+                     "peak_kind": peak_kind, "traffic": None, "algorithmic_bytes_per_launch": k9_bytes,
+                     "ms_per_launch": k9_ms_launch, "share_of_step": k9_share,
+                     "fp32_tflops": 2.0 * kept * b / (k9_ms_launch * 1e-3) / 1e12},
+        "online_stage_ms_per_step": {k: v[0] / args.steps for k, v in on_stages.items()},
+        "offline": offline,
+        "gpu_launches": launches,
+        "e2e": e2e,
+        "cpu_baseline": cpu,
+        "clocks": clk,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    from paper_1703_06935_b200.workloads import CONFIGS
+
+    cfg = CONFIGS[args.config]
+    n = args.n or cfg.n
+    if args.impl == "reference":
+        run_reference(args, cfg, n, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl")
+    try:
+        run_fsr(args, cfg, n, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

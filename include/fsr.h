@@ -60,6 +60,21 @@ uint64_t fsr_launch_count(const fsr_ctx* ctx);
 uint64_t fsr_library_calls(const fsr_ctx* ctx);
 int fsr_synchronize(fsr_ctx* ctx);
 
+/* Optional per-stage device timing: when enabled every entry point brackets
+ * its device work with CUDA events on the context stream.  fsr_stage_time
+ * synchronises, folds finished events into per-stage totals and returns the
+ * accumulated milliseconds and launch count of one stage. */
+enum fsr_stage {
+  FSR_STAGE_GAUSSIAN = 0, FSR_STAGE_NORMALIZE = 1, FSR_STAGE_SPMM = 2, FSR_STAGE_GRAM = 3,
+  FSR_STAGE_CHOLESKY = 4, FSR_STAGE_APPLY = 5, FSR_STAGE_EIGH = 6, FSR_STAGE_LIFT = 7,
+  FSR_STAGE_SIGNS = 8, FSR_STAGE_HISTOGRAM = 9, FSR_STAGE_COMPACT = 10, FSR_STAGE_PROJECT = 11,
+  FSR_STAGE_FILTER_SPMM = 12, FSR_STAGE_TRANSPOSE = 13, FSR_STAGE_COPY_UNCOVERED = 14,
+  FSR_STAGE_TOPK = 15, FSR_STAGE_HOUSEHOLDER = 16, FSR_NUM_STAGES = 17
+};
+int fsr_ctx_enable_timing(fsr_ctx* ctx, int on);
+int fsr_stage_time(fsr_ctx* ctx, int stage, double* ms, uint64_t* count);
+int fsr_stage_reset(fsr_ctx* ctx);
+
 /* ---- K0: start block  (spectral.py:55-65 gaussian_matrix) -------------
  * Rows [row_begin, row_end) of the (total_rows x cols) Box-Muller block drawn
  * from numpy's Philox4x64-10 stream with key (key0, key1) =

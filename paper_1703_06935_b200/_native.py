@@ -15,6 +15,9 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libfsr.so")
 
 F32, F64 = 0, 1
+STAGES = {name: i for i, name in enumerate((
+    "gaussian", "normalize", "spmm", "gram", "cholesky", "apply", "eigh", "lift", "signs", "histogram",
+    "compact", "project", "filter_spmm", "transpose", "copy_uncovered", "topk", "householder"))}
 OK, EINVAL, ENUMERICAL, ECUDA, ENOMEM, ELIBRARY, ENOTSPD = range(7)
 
 _c_i64 = ctypes.c_int64
@@ -34,6 +37,9 @@ _SIGS = {
     "fsr_launch_count": (_c_u64, [_c_p]),
     "fsr_library_calls": (_c_u64, [_c_p]),
     "fsr_synchronize": (_c_int, [_c_p]),
+    "fsr_ctx_enable_timing": (_c_int, [_c_p, _c_int]),
+    "fsr_stage_time": (_c_int, [_c_p, _c_int, _c_dp, ctypes.POINTER(_c_u64)]),
+    "fsr_stage_reset": (_c_int, [_c_p]),
     "fsr_gaussian_block": (_c_int, [_c_p, _c_int, _c_i64, _c_i64, _c_i64, _c_i64, _c_u64, _c_u64, _c_p]),
     "fsr_csr_row_sums": (_c_int, [_c_p, _c_i64, _c_p, _c_p, _c_p]),
     "fsr_csr_normalize": (_c_int, [_c_p, _c_int, _c_i64, _c_i64, _c_p, _c_p, _c_p, _c_p, _c_p]),
@@ -172,6 +178,18 @@ class Context:
         if st not in (OK, ENOTSPD):
             self.check(st)
         return st
+
+    def enable_timing(self, on: bool = True):
+        self.check(self.lib.fsr_ctx_enable_timing(self.handle, int(on)))
+
+    def stage_time(self, stage: str):
+        """(total ms, launches) accumulated for one stage since the last reset."""
+        ms, cnt = ctypes.c_double(), _c_u64()
+        self.check(self.lib.fsr_stage_time(self.handle, STAGES[stage], ctypes.byref(ms), ctypes.byref(cnt)))
+        return ms.value, int(cnt.value)
+
+    def stage_reset(self):
+        self.check(self.lib.fsr_stage_reset(self.handle))
 
     @property
     def launches(self) -> int:

@@ -9,6 +9,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <string>
+#include <vector>
 
 #include "../../include/fsr.h"
 
@@ -27,6 +28,16 @@ struct fsr_ctx {
   std::string err;
   uint64_t launches = 0;
   uint64_t library_calls = 0;
+  // optional per-stage device timing (CUDA events on the context stream)
+  bool timing = false;
+  struct Pending {
+    int stage;
+    cudaEvent_t start, stop;
+  };
+  std::vector<Pending> pending;
+  std::vector<cudaEvent_t> event_pool;
+  double stage_ms[FSR_NUM_STAGES] = {};
+  uint64_t stage_count[FSR_NUM_STAGES] = {};
 };
 
 namespace fsr {
@@ -130,6 +141,38 @@ __device__ __forceinline__ uint64_t abs_key(float v) {
 __device__ __forceinline__ uint64_t abs_key(double v) {
   return (uint64_t)__double_as_longlong(v) & 0x7fffffffffffffffull;
 }
+
+inline cudaEvent_t pooled_event(fsr_ctx* ctx) {
+  if (!ctx->event_pool.empty()) {
+    cudaEvent_t e = ctx->event_pool.back();
+    ctx->event_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+
+// Brackets the device work issued in its scope with CUDA events when the
+// context has timing enabled (fsr_ctx_enable_timing); no cost otherwise.
+struct StageTimer {
+  fsr_ctx* ctx;
+  int stage;
+  cudaEvent_t start = nullptr;
+  StageTimer(fsr_ctx* c, int s) : ctx(c), stage(s) {
+    if (ctx->timing) {
+      start = pooled_event(ctx);
+      cudaEventRecord(start, ctx->stream);
+    }
+  }
+  ~StageTimer() {
+    if (start) {
+      cudaEvent_t stop = pooled_event(ctx);
+      cudaEventRecord(stop, ctx->stream);
+      ctx->pending.push_back({stage, start, stop});
+    }
+  }
+};
 
 }  // namespace fsr
 

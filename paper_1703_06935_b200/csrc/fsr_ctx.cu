@@ -1,6 +1,8 @@
 // Context lifecycle, error reporting and launch accounting for libfsr.
 #include "fsr_common.cuh"
 
+static void fold_pending(fsr_ctx* ctx);
+
 extern "C" {
 
 int fsr_abi_version(void) { return FSR_ABI_VERSION; }
@@ -37,6 +39,8 @@ void fsr_ctx_destroy(fsr_ctx* ctx) {
   if (ctx->scratch) cudaFree(ctx->scratch);
   if (ctx->dev_info) cudaFree(ctx->dev_info);
   if (ctx->host_stage) cudaFreeHost(ctx->host_stage);
+  fold_pending(ctx);
+  for (auto e : ctx->event_pool) cudaEventDestroy(e);
   if (ctx->blas) cublasDestroy(ctx->blas);
   if (ctx->solver) cusolverDnDestroy(ctx->solver);
   delete ctx;
@@ -55,6 +59,50 @@ const char* fsr_last_error(const fsr_ctx* ctx) { return ctx ? ctx->err.c_str() :
 uint64_t fsr_launch_count(const fsr_ctx* ctx) { return ctx ? ctx->launches : 0; }
 
 uint64_t fsr_library_calls(const fsr_ctx* ctx) { return ctx ? ctx->library_calls : 0; }
+
+}  // extern "C"
+
+static void fold_pending(fsr_ctx* ctx) {
+  for (auto& p : ctx->pending) {
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, p.start, p.stop) == cudaSuccess) {
+      ctx->stage_ms[p.stage] += ms;
+      ctx->stage_count[p.stage] += 1;
+    }
+    ctx->event_pool.push_back(p.start);
+    ctx->event_pool.push_back(p.stop);
+  }
+  ctx->pending.clear();
+  cudaGetLastError();
+}
+
+extern "C" {
+
+int fsr_ctx_enable_timing(fsr_ctx* ctx, int on) {
+  if (!ctx) return FSR_EINVAL;
+  ctx->timing = on != 0;
+  return FSR_OK;
+}
+
+int fsr_stage_time(fsr_ctx* ctx, int stage, double* ms, uint64_t* count) {
+  if (!ctx || stage < 0 || stage >= FSR_NUM_STAGES) return FSR_EINVAL;
+  FSR_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  fold_pending(ctx);
+  if (ms) *ms = ctx->stage_ms[stage];
+  if (count) *count = ctx->stage_count[stage];
+  return FSR_OK;
+}
+
+int fsr_stage_reset(fsr_ctx* ctx) {
+  if (!ctx) return FSR_EINVAL;
+  FSR_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  fold_pending(ctx);
+  for (int i = 0; i < FSR_NUM_STAGES; ++i) {
+    ctx->stage_ms[i] = 0.0;
+    ctx->stage_count[i] = 0;
+  }
+  return FSR_OK;
+}
 
 int fsr_synchronize(fsr_ctx* ctx) {
   if (!ctx) return FSR_EINVAL;

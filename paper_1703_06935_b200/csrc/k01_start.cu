@@ -169,6 +169,7 @@ int fsr_gaussian_block(fsr_ctx* ctx, int dtype, int64_t total_rows, int64_t cols
   const int64_t groups = (aLen + 3) / 4 + (bLen + 3) / 4;
   const int block = 256;
   const int grid = fsr::grid_for(groups, block, ctx, 32);
+  fsr::StageTimer timer(ctx, FSR_STAGE_GAUSSIAN);
   if (dtype == FSR_F64)
     gaussian_kernel<double><<<grid, block, 0, ctx->stream>>>(count, half, f0, f1, aLo & ~int64_t(3), aLen,
                                                              bLo & ~int64_t(3), bLen, key0, key1,
@@ -183,6 +184,7 @@ int fsr_gaussian_block(fsr_ctx* ctx, int dtype, int64_t total_rows, int64_t cols
 int fsr_csr_row_sums(fsr_ctx* ctx, int64_t n_rows, const int64_t* indptr, const double* data, double* deg) {
   FSR_REQUIRE(ctx, n_rows >= 0, "row_sums: bad shape");
   if (!n_rows) return FSR_OK;
+  fsr::StageTimer timer(ctx, FSR_STAGE_NORMALIZE);
   row_sums_kernel<<<fsr::grid_for(n_rows, 256, ctx), 256, 0, ctx->stream>>>(n_rows, indptr, data, deg);
   return fsr::launched(ctx, "row_sums_kernel");
 }
@@ -192,6 +194,7 @@ int fsr_csr_normalize(fsr_ctx* ctx, int dtype_out, int64_t n_rows, int64_t row_o
   FSR_REQUIRE(ctx, n_rows >= 0 && row_offset >= 0, "normalize: bad shape");
   if (!n_rows) return FSR_OK;
   const int grid = fsr::grid_for(n_rows * 32, 256, ctx);
+  fsr::StageTimer timer(ctx, FSR_STAGE_NORMALIZE);
   if (dtype_out == FSR_F64)
     normalize_kernel<double><<<grid, 256, 0, ctx->stream>>>(n_rows, row_offset, indptr, indices, data, deg,
                                                             (double*)out);

@@ -176,6 +176,7 @@ int dgemm_nt_accum(fsr_ctx* ctx, int64_t k, int64_t rows, const double* A, int64
 int cross_impl(fsr_ctx* ctx, int dtype, int64_t n_rows, int64_t k, const void* A, int64_t lda, const void* B,
                int64_t ldb, double* C, int accumulate) {
   FSR_REQUIRE(ctx, n_rows >= 0 && k >= 1 && lda >= k && ldb >= k, "gram/cross: bad shape");
+  fsr::StageTimer timer(ctx, FSR_STAGE_GRAM);
   if (n_rows == 0) {
     if (!accumulate) FSR_CUDA(ctx, cudaMemsetAsync(C, 0, k * k * 8, ctx->stream));
     return FSR_OK;
@@ -214,6 +215,7 @@ int fsr_cross(fsr_ctx* ctx, int dtype, int64_t n_rows, int64_t k, const void* Q,
 
 int fsr_cholesky(fsr_ctx* ctx, int64_t k, double* G) {
   FSR_REQUIRE(ctx, k >= 1, "cholesky: bad shape");
+  fsr::StageTimer timer(ctx, FSR_STAGE_CHOLESKY);
   int lwork = 0;
   FSR_SOLVER(ctx, cusolverDnDpotrf_bufferSize(ctx->solver, CUBLAS_FILL_MODE_UPPER, (int)k, G, (int)k, &lwork));
   void* work = nullptr;
@@ -231,6 +233,7 @@ int fsr_cholesky(fsr_ctx* ctx, int64_t k, double* G) {
 int fsr_apply_rinv(fsr_ctx* ctx, int dtype, int64_t n_rows, int64_t k, const double* R, void* A, int64_t lda) {
   FSR_REQUIRE(ctx, n_rows >= 0 && k >= 1 && lda >= k, "apply_rinv: bad shape");
   if (!n_rows) return FSR_OK;
+  fsr::StageTimer timer(ctx, FSR_STAGE_APPLY);
   // (A R^-1)^T = R^-T A^T: solve R^T X = A_c with A_c the column-major k x n view
   if (dtype == FSR_F64) {
     const double one = 1.0;
@@ -252,6 +255,7 @@ int fsr_householder_qr(fsr_ctx* ctx, int dtype, int64_t n_rows, int64_t k, void*
   FSR_REQUIRE(ctx, n_rows >= k && k >= 1 && lda >= k, "householder_qr: need n_rows >= k");
   FSR_REQUIRE(ctx, n_rows < (1ll << 31) && n_rows * k < (1ll << 40), "householder_qr: too large");
   const int m = (int)n_rows, kk = (int)k;
+  fsr::StageTimer timer(ctx, FSR_STAGE_HOUSEHOLDER);
   const size_t es = fsr::dtype_size(dtype);
   int lw1 = 0, lw2 = 0;
   void* buf = nullptr;
@@ -314,6 +318,7 @@ int fsr_max_offdiag_error(fsr_ctx* ctx, int64_t k, const double* G, double* err_
 int fsr_eigh_desc(fsr_ctx* ctx, int64_t k, double* C, int64_t r, double* lam_host, double* V) {
   FSR_REQUIRE(ctx, k >= 1 && r >= 1 && r <= k && lam_host, "eigh_desc: bad shape");
   FSR_REQUIRE(ctx, k < (1 << 20), "eigh_desc: k too large");
+  fsr::StageTimer timer(ctx, FSR_STAGE_EIGH);
   symmetrize_kernel<<<fsr::grid_for(k * k, 256, ctx, 8), 256, 0, ctx->stream>>>(k, C);
   FSR_TRY(fsr::launched(ctx, "symmetrize_kernel"));
   int lwork = 0;
@@ -353,6 +358,7 @@ int fsr_lift(fsr_ctx* ctx, int dtype, int64_t n_rows, int64_t k, int64_t r, cons
              const double* V, void* U, int64_t ldu) {
   FSR_REQUIRE(ctx, n_rows >= 0 && k >= 1 && r >= 1 && r <= k && ldq >= k && ldu >= r, "lift: bad shape");
   if (!n_rows) return FSR_OK;
+  fsr::StageTimer timer(ctx, FSR_STAGE_LIFT);
   // U_c (r x n) = V_c' (r x k; row-major V viewed column-major) * Q_c (k x n)
   if (dtype == FSR_F64) {
     const double one = 1.0, zero = 0.0;
@@ -373,6 +379,7 @@ int fsr_lift(fsr_ctx* ctx, int dtype, int64_t n_rows, int64_t k, int64_t r, cons
 int fsr_col_absmax(fsr_ctx* ctx, int dtype, int64_t n_rows, int64_t r, const void* U, int64_t ldu,
                    int64_t row_offset, double* best_abs, int64_t* best_row, double* best_val) {
   FSR_REQUIRE(ctx, n_rows >= 0 && r >= 1 && ldu >= r, "col_absmax: bad shape");
+  fsr::StageTimer timer(ctx, FSR_STAGE_SIGNS);
   const int64_t col_blocks = fsr::ceil_div(r, 32);
   int64_t nchunks = std::max<int64_t>(1, std::min<int64_t>(fsr::ceil_div((int64_t)ctx->num_sms * 8, col_blocks),
                                                            fsr::ceil_div(std::max<int64_t>(n_rows, 1), 64)));
@@ -401,6 +408,7 @@ int fsr_apply_signs_rownorm(fsr_ctx* ctx, int dtype, int64_t n_rows, int64_t r, 
                             const double* best_val, double* eta) {
   FSR_REQUIRE(ctx, n_rows >= 0 && r >= 1 && ldu >= r, "apply_signs: bad shape");
   if (!n_rows) return FSR_OK;
+  fsr::StageTimer timer(ctx, FSR_STAGE_SIGNS);
   const int grid = fsr::grid_for(n_rows * 32, 256, ctx, 8);
   if (dtype == FSR_F64)
     signs_rownorm_kernel<double, true><<<grid, 256, 0, ctx->stream>>>(n_rows, r, (double*)U, ldu, best_val, eta);
@@ -412,6 +420,7 @@ int fsr_apply_signs_rownorm(fsr_ctx* ctx, int dtype, int64_t n_rows, int64_t r, 
 int fsr_row_norms(fsr_ctx* ctx, int dtype, int64_t n_rows, int64_t r, const void* U, int64_t ldu, double* eta) {
   FSR_REQUIRE(ctx, n_rows >= 0 && r >= 1 && ldu >= r, "row_norms: bad shape");
   if (!n_rows) return FSR_OK;
+  fsr::StageTimer timer(ctx, FSR_STAGE_SIGNS);
   const int grid = fsr::grid_for(n_rows * 32, 256, ctx, 8);
   if (dtype == FSR_F64)
     signs_rownorm_kernel<double, false><<<grid, 256, 0, ctx->stream>>>(n_rows, r, (double*)U, ldu, nullptr, eta);

@@ -141,6 +141,7 @@ int fsr_abs_histogram(fsr_ctx* ctx, int dtype, int64_t n_rows, int64_t r, const 
   const int block = 512;
   const int grid = fsr::grid_for(n_rows * r, block, ctx, 4);
   const size_t smem = (size_t)4 << bits;
+  fsr::StageTimer timer(ctx, FSR_STAGE_HISTOGRAM);
   if (dtype == FSR_F64)
     abs_hist_kernel<double><<<grid, block, smem, ctx->stream>>>(n_rows, r, (const double*)U, ldu, prefix & himask,
                                                                  himask, shift, bits, (unsigned long long*)hist);
@@ -155,6 +156,7 @@ int fsr_threshold_counts(fsr_ctx* ctx, int dtype, int64_t n_rows, int64_t r, con
   FSR_REQUIRE(ctx, n_rows >= 0 && r >= 1 && ldu >= r, "threshold_counts: bad shape");
   if (!n_rows) return FSR_OK;
   const int grid = fsr::grid_for(n_rows * 32, 256, ctx, 8);
+  fsr::StageTimer timer(ctx, FSR_STAGE_COMPACT);
   if (dtype == FSR_F64)
     counts_kernel<double><<<grid, 256, 0, ctx->stream>>>(n_rows, r, (const double*)U, ldu, T, gt, eq);
   else
@@ -172,6 +174,7 @@ int fsr_threshold_compact(fsr_ctx* ctx, int dtype, int64_t n_rows, int64_t r, co
     *nnz_host = 0;
     return FSR_OK;
   }
+  fsr::StageTimer timer(ctx, FSR_STAGE_COMPACT);
   size_t scan_bytes = 0, scan2 = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, eq, indptr_out, n_rows, ctx->stream);
   cub::DeviceScan::ExclusiveSum(nullptr, scan2, indptr_out, indptr_out, n_rows + 1, ctx->stream);

@@ -310,6 +310,8 @@ int filter_impl(fsr_ctx* ctx, int64_t n, int64_t r, int u_sparse, const int64_t*
   T* Xout = X;
   if (!Xout) Xout = (T*)ws;
 
+  {
+  fsr::StageTimer timer(ctx, FSR_STAGE_PROJECT);
   if (u_sparse)
     project_kernel<T, true><<<(unsigned)b, 256, 0, ctx->stream>>>(r, b, u_indptr, u_indices, u_values, nullptr, 0, w,
                                                                   y_ptr, y_idx, y_val, Zt, Zs);
@@ -317,17 +319,24 @@ int filter_impl(fsr_ctx* ctx, int64_t n, int64_t r, int u_sparse, const int64_t*
     project_kernel<T, false><<<(unsigned)b, 256, 0, ctx->stream>>>(r, b, nullptr, nullptr, nullptr, u_dense, ldu, w,
                                                                    y_ptr, y_idx, y_val, Zt, nullptr);
   FSR_TRY(fsr::launched(ctx, "project_kernel"));
+  }
 
   if (u_sparse) {
     if (b == 1) {
+      fsr::StageTimer timer(ctx, FSR_STAGE_FILTER_SPMM);
       FSR_TRY(fsr::launch_spmm<T>(ctx, n, u_indptr, u_indices, u_values, 1, Zs, 1, Xout, 1));
     } else {
-      FSR_TRY(fsr::launch_spmm<T>(ctx, n, u_indptr, u_indices, u_values, b, Zs, b, Xnb, b));
+      {
+        fsr::StageTimer timer(ctx, FSR_STAGE_FILTER_SPMM);
+        FSR_TRY(fsr::launch_spmm<T>(ctx, n, u_indptr, u_indices, u_values, b, Zs, b, Xnb, b));
+      }
+      fsr::StageTimer timer(ctx, FSR_STAGE_TRANSPOSE);
       dim3 grid((unsigned)fsr::ceil_div(b, 32), (unsigned)fsr::ceil_div(n, 32)), block(32, 8);
       transpose_kernel<T><<<grid, block, 0, ctx->stream>>>(n, b, Xnb, Xout);
       FSR_TRY(fsr::launched(ctx, "transpose_kernel"));
     }
   } else {
+    fsr::StageTimer timer(ctx, FSR_STAGE_FILTER_SPMM);
     // X_c (n x b, col-major) = U_c^T (n x r) * Zt_c (r x b)
     if (sizeof(T) == 8) {
       const double one = 1.0, zero = 0.0;
@@ -340,10 +349,14 @@ int filter_impl(fsr_ctx* ctx, int64_t n, int64_t r, int u_sparse, const int64_t*
     }
   }
   if (copy_uncovered && eta) {
+    fsr::StageTimer timer(ctx, FSR_STAGE_COPY_UNCOVERED);
     copy_uncovered_kernel<T><<<(unsigned)b, 128, 0, ctx->stream>>>(n, y_ptr, y_idx, y_val, eta, Xout, n);
     FSR_TRY(fsr::launched(ctx, "copy_uncovered_kernel"));
   }
-  if (topk > 0) FSR_TRY(launch_topk<T>(ctx, b, n, Xout, n, topk, top_idx, top_val));
+  if (topk > 0) {
+    fsr::StageTimer timer(ctx, FSR_STAGE_TOPK);
+    FSR_TRY(launch_topk<T>(ctx, b, n, Xout, n, topk, top_idx, top_val));
+  }
   return FSR_OK;
 }
 
