@@ -259,6 +259,7 @@ def run_fsr(args, cfg, n, rank, world, local_rank):
     ctx.stage_reset()
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
     torch.cuda.synchronize()
+    torch.cuda.nvtx.range_push("fsr:offline")
     ev[0].record()
     basis = spectral.range_finder(S, r_hat, q, 0, dtype=dt, device=device)
     ev[1].record()
@@ -268,6 +269,7 @@ def run_fsr(args, cfg, n, rank, world, local_rank):
     sdec = spectral.sparsify(dec, tau)
     ev[3].record()
     torch.cuda.synchronize()
+    torch.cuda.nvtx.range_pop()
     stages = {name: ctx.stage_time(name) for name in N.STAGES}
     del dec
     torch.cuda.empty_cache()
@@ -312,12 +314,14 @@ def run_fsr(args, cfg, n, rank, world, local_rank):
     torch.cuda.synchronize()
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    torch.cuda.nvtx.range_push("fsr:online")
     for i in range(args.steps):
         flush.zero_()  # untimed: evict U~ / Zs from L2 between steps
         starts[i].record()
         step(i)
         ends[i].record()
     torch.cuda.synchronize()
+    torch.cuda.nvtx.range_pop()
     barrier(world)
     launches = ctx.launches - launches0
     dev_ms = sum(s.elapsed_time(e) for s, e in zip(starts, ends))
