@@ -72,6 +72,12 @@ enum fsr_stage {
   FSR_STAGE_TOPK = 15, FSR_STAGE_HOUSEHOLDER = 16, FSR_NUM_STAGES = 17
 };
 int fsr_ctx_enable_timing(fsr_ctx* ctx, int on);
+
+/* Context options.  FSR_OPT_DENSE_PATH: 0 = auto (F32 Gram / cross / apply /
+ * lift on tcgen05 3xTF32 kernels), 1 = cuBLAS/cuSOLVER (fp64-upcast Gram,
+ * TRSM, SGEMM) -- kept for A/B checks. */
+enum fsr_option { FSR_OPT_DENSE_PATH = 0 };
+int fsr_ctx_set_option(fsr_ctx* ctx, int option, int64_t value);
 int fsr_stage_time(fsr_ctx* ctx, int stage, double* ms, uint64_t* count);
 int fsr_stage_reset(fsr_ctx* ctx);
 
@@ -111,6 +117,11 @@ int fsr_csr_spmm(fsr_ctx* ctx, int dtype, int64_t n_rows, const int64_t* indptr,
  * (accumulate != 0: G += A^T A). */
 int fsr_gram(fsr_ctx* ctx, int dtype, int64_t n_rows, int64_t k, const void* A, int64_t lda,
              double* G, int accumulate);
+/* F32 only: G (+)= A^T A on the tcgen05 path with `products` = 3 (3xTF32,
+ * ~fp32-accurate) or 1 (plain TF32; enough for the first CholeskyQR pass,
+ * whose Gram only needs to be well conditioned). */
+int fsr_gram_tf32(fsr_ctx* ctx, int64_t n_rows, int64_t k, const float* A, int64_t lda, double* G,
+                  int accumulate, int products);
 /* In-place Cholesky G = R^T R (R upper).  Returns FSR_ENOTSPD on breakdown
  * (host-synchronous: reads the factorisation status). */
 int fsr_cholesky(fsr_ctx* ctx, int64_t k, double* G);

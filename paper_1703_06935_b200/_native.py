@@ -38,6 +38,8 @@ _SIGS = {
     "fsr_library_calls": (_c_u64, [_c_p]),
     "fsr_synchronize": (_c_int, [_c_p]),
     "fsr_ctx_enable_timing": (_c_int, [_c_p, _c_int]),
+    "fsr_ctx_set_option": (_c_int, [_c_p, _c_int, _c_i64]),
+    "fsr_gram_tf32": (_c_int, [_c_p, _c_i64, _c_i64, _c_p, _c_i64, _c_p, _c_int, _c_int]),
     "fsr_stage_time": (_c_int, [_c_p, _c_int, _c_dp, ctypes.POINTER(_c_u64)]),
     "fsr_stage_reset": (_c_int, [_c_p]),
     "fsr_gaussian_block": (_c_int, [_c_p, _c_int, _c_i64, _c_i64, _c_i64, _c_i64, _c_u64, _c_u64, _c_p]),
@@ -178,6 +180,10 @@ class Context:
         if st not in (OK, ENOTSPD):
             self.check(st)
         return st
+
+    def set_dense_path(self, path: str):
+        """'auto' (tcgen05 3xTF32 kernels for float32 blocks) or 'cublas'."""
+        self.check(self.lib.fsr_ctx_set_option(self.handle, 0, {"auto": 0, "tcgen05": 0, "cublas": 1}[path]))
 
     def enable_timing(self, on: bool = True):
         self.check(self.lib.fsr_ctx_enable_timing(self.handle, int(on)))

@@ -22,6 +22,9 @@ struct fsr_ctx {
   // grow-only scratch arena, stream-ordered (all work runs on `stream`)
   void* scratch = nullptr;
   size_t scratch_bytes = 0;
+  void* scratch_aux = nullptr;  // caller-level temporaries that outlive a scratch() user
+  size_t scratch_aux_bytes = 0;
+  int dense_path = 0;           // FSR_OPT_DENSE_PATH: 0 auto (tcgen05 for F32), 1 cuBLAS
   int* dev_info = nullptr;
   double* host_stage = nullptr;  // pinned staging for small host reads
   size_t host_stage_bytes = 0;
@@ -99,6 +102,31 @@ inline int scratch(fsr_ctx* ctx, size_t bytes, void** out) {
   *out = ctx->scratch;
   return FSR_OK;
 }
+
+inline int scratch_aux(fsr_ctx* ctx, size_t bytes, void** out) {
+  if (bytes <= ctx->scratch_aux_bytes) {
+    *out = ctx->scratch_aux;
+    return FSR_OK;
+  }
+  cudaStreamSynchronize(ctx->stream);
+  if (ctx->scratch_aux) cudaFree(ctx->scratch_aux);
+  ctx->scratch_aux = nullptr;
+  ctx->scratch_aux_bytes = 0;
+  cudaError_t e = cudaMalloc(&ctx->scratch_aux, bytes);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return set_error(ctx, FSR_ENOMEM, "aux scratch alloc of %zu bytes failed", bytes);
+  }
+  ctx->scratch_aux_bytes = bytes;
+  *out = ctx->scratch_aux;
+  return FSR_OK;
+}
+
+// tcgen05 kernels (tc_gemm.cu)
+int tc_gram(fsr_ctx* ctx, int64_t n, int64_t ka, const float* A, int64_t lda, int64_t kb, const float* B,
+            int64_t ldb, double* C, int accumulate, int nprod, int symmetric);
+int tc_apply(fsr_ctx* ctx, int64_t n, int64_t K, const float* A, int64_t lda, int64_t N2, const double* M,
+             int64_t ldm, int m_col_major, float* Out, int64_t ldo);
 
 inline int host_stage(fsr_ctx* ctx, size_t bytes, void** out) {
   if (bytes > ctx->host_stage_bytes) {

@@ -37,6 +37,7 @@ void fsr_ctx_destroy(fsr_ctx* ctx) {
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   else cudaDeviceSynchronize();
   if (ctx->scratch) cudaFree(ctx->scratch);
+  if (ctx->scratch_aux) cudaFree(ctx->scratch_aux);
   if (ctx->dev_info) cudaFree(ctx->dev_info);
   if (ctx->host_stage) cudaFreeHost(ctx->host_stage);
   fold_pending(ctx);
@@ -77,6 +78,18 @@ static void fold_pending(fsr_ctx* ctx) {
 }
 
 extern "C" {
+
+int fsr_ctx_set_option(fsr_ctx* ctx, int option, int64_t value) {
+  if (!ctx) return FSR_EINVAL;
+  switch (option) {
+    case FSR_OPT_DENSE_PATH:
+      if (value < 0 || value > 1) return fsr::set_error(ctx, FSR_EINVAL, "dense path must be 0 or 1");
+      ctx->dense_path = (int)value;
+      return FSR_OK;
+    default:
+      return fsr::set_error(ctx, FSR_EINVAL, "unknown option %d", option);
+  }
+}
 
 int fsr_ctx_enable_timing(fsr_ctx* ctx, int on) {
   if (!ctx) return FSR_EINVAL;

@@ -70,6 +70,11 @@ __global__ void gather_cols_kernel(int64_t k, int64_t r, const double* __restric
   }
 }
 
+__global__ void identity_kernel(int64_t k, double* __restrict__ M) {
+  for (int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; f < k * k; f += (int64_t)gridDim.x * blockDim.x)
+    M[f] = (f / k == f % k) ? 1.0 : 0.0;
+}
+
 __global__ void d2s_kernel(int64_t n, const double* __restrict__ in, float* __restrict__ out) {
   for (int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; f < n; f += (int64_t)gridDim.x * blockDim.x)
     out[f] = (float)in[f];
@@ -184,6 +189,8 @@ int cross_impl(fsr_ctx* ctx, int dtype, int64_t n_rows, int64_t k, const void* A
   if (dtype == FSR_F64)
     return dgemm_nt_accum(ctx, k, n_rows, (const double*)A, lda, (const double*)B, ldb, C, accumulate ? 1.0 : 0.0);
   const bool same = A == B && lda == ldb;
+  if (ctx->dense_path == 0)
+    return fsr::tc_gram(ctx, n_rows, k, (const float*)A, lda, k, (const float*)B, ldb, C, accumulate, 3, same);
   const int64_t m = chunk_rows(n_rows, k, same ? 1 : 2);
   void* buf = nullptr;
   FSR_TRY(fsr::scratch(ctx, (size_t)m * k * 8 * (same ? 1 : 2), &buf));
@@ -213,6 +220,17 @@ int fsr_cross(fsr_ctx* ctx, int dtype, int64_t n_rows, int64_t k, const void* Q,
   return cross_impl(ctx, dtype, n_rows, k, Q, ldq, B, ldb, C, accumulate);
 }
 
+int fsr_gram_tf32(fsr_ctx* ctx, int64_t n_rows, int64_t k, const float* A, int64_t lda, double* G, int accumulate,
+                  int products) {
+  FSR_REQUIRE(ctx, n_rows >= 0 && k >= 1 && lda >= k && (products == 1 || products == 3), "gram_tf32: bad args");
+  fsr::StageTimer timer(ctx, FSR_STAGE_GRAM);
+  if (n_rows == 0) {
+    if (!accumulate) FSR_CUDA(ctx, cudaMemsetAsync(G, 0, k * k * 8, ctx->stream));
+    return FSR_OK;
+  }
+  return fsr::tc_gram(ctx, n_rows, k, A, lda, k, A, lda, G, accumulate, products, 1);
+}
+
 int fsr_cholesky(fsr_ctx* ctx, int64_t k, double* G) {
   FSR_REQUIRE(ctx, k >= 1, "cholesky: bad shape");
   fsr::StageTimer timer(ctx, FSR_STAGE_CHOLESKY);
@@ -240,6 +258,18 @@ int fsr_apply_rinv(fsr_ctx* ctx, int dtype, int64_t n_rows, int64_t k, const dou
     FSR_BLAS(ctx, cublasDtrsm_64(ctx->blas, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_T,
                                  CUBLAS_DIAG_NON_UNIT, k, n_rows, &one, R, k, (double*)A, lda));
     return FSR_OK;
+  }
+  if (ctx->dense_path == 0) {
+    // explicit R^-1 (fp64 TRSM on the identity), then Q = B R^-1 on tensor cores
+    void* aux = nullptr;
+    FSR_TRY(fsr::scratch_aux(ctx, (size_t)k * k * 8, &aux));
+    double* Rinv = (double*)aux;
+    identity_kernel<<<fsr::grid_for(k * k, 256, ctx), 256, 0, ctx->stream>>>(k, Rinv);
+    FSR_TRY(fsr::launched(ctx, "identity_kernel"));
+    const double done = 1.0;
+    FSR_BLAS(ctx, cublasDtrsm_64(ctx->blas, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_N,
+                                 CUBLAS_DIAG_NON_UNIT, k, k, &done, R, k, Rinv, k));
+    return fsr::tc_apply(ctx, n_rows, k, (const float*)A, lda, k, Rinv, k, 1, (float*)A, lda);
   }
   void* buf = nullptr;
   FSR_TRY(fsr::scratch(ctx, (size_t)k * k * 4, &buf));
@@ -366,6 +396,8 @@ int fsr_lift(fsr_ctx* ctx, int dtype, int64_t n_rows, int64_t k, int64_t r, cons
                                  ldq, &zero, (double*)U, ldu));
     return FSR_OK;
   }
+  if (ctx->dense_path == 0)
+    return fsr::tc_apply(ctx, n_rows, k, (const float*)Q, ldq, r, V, r, 0, (float*)U, ldu);
   void* buf = nullptr;
   FSR_TRY(fsr::scratch(ctx, (size_t)k * r * 4, &buf));
   d2s_kernel<<<fsr::grid_for(k * r, 256, ctx), 256, 0, ctx->stream>>>(k * r, V, (float*)buf);

@@ -37,6 +37,8 @@ ORTH_TOL = {N.F64: 1e-8, N.F32: 1e-4}
 # CholeskyQR2 is orthogonal to O(eps) when the second Gram is this close to I
 # (Yamamoto et al. 2015); beyond it an explicit check runs (spectral.py:167).
 CHOLQR2_SAFE = 0.1
+# first CholeskyQR pass of a float32 block with a 1xTF32 Gram (see _cholqr_pass)
+FAST_FIRST_GRAM = True
 
 _MASK64 = (1 << 64) - 1
 
@@ -198,9 +200,18 @@ def _max_dev(ctx, G) -> float:
     return err.value
 
 
-def _cholqr_pass(ctx, dt, Y, G, gram_hook=None) -> tuple[bool, float]:
-    """One CholeskyQR pass in place: Y <- Y R^-1.  Returns (ok, max|G - I|)."""
-    _gram(ctx, dt, Y, G)
+def _cholqr_pass(ctx, dt, Y, G, gram_hook=None, fast_gram=False) -> tuple[bool, float]:
+    """One CholeskyQR pass in place: Y <- Y R^-1.  Returns (ok, max|G - I|).
+
+    ``fast_gram`` (float32 blocks only): a single-TF32-product Gram.  The first
+    pass of CholeskyQR2 only needs R to be a decent preconditioner -- span(Y R^-1)
+    equals span(Y) whatever R is -- so its Gram can skip the 3xTF32 split.
+    """
+    if fast_gram and dt == N.F32:
+        n, k = Y.shape
+        ctx.call("gram_tf32", n, k, N.ptr(Y), Y.stride(0), N.ptr(G), 0, 1)
+    else:
+        _gram(ctx, dt, Y, G)
     if gram_hook is not None:
         gram_hook(G)
     dev = _max_dev(ctx, G)
@@ -223,7 +234,7 @@ def orthonormalize(Y, ctx=None, stats=None):
     dt = N.dtype_code(Y.dtype)
     n, k = Y.shape
     G = torch.empty(k, k, dtype=torch.float64, device=Y.device)
-    ok1, _ = _cholqr_pass(ctx, dt, Y, G)
+    ok1, _ = _cholqr_pass(ctx, dt, Y, G, fast_gram=FAST_FIRST_GRAM)
     ok2, dev2 = _cholqr_pass(ctx, dt, Y, G) if ok1 else (False, math.inf)
     method = "cholqr2"
     if not (ok1 and ok2):
