@@ -1,31 +1,34 @@
-// Tensor-core (tcgen05, kind::tf32) dense stages of CholeskyQR2 and
-// Rayleigh-Ritz for float32 blocks, FP32-accurate by 3xTF32 splitting.
+// Tensor-core (tcgen05, kind::i8) dense stages of CholeskyQR2 and
+// Rayleigh-Ritz for float32 blocks: an Ozaki-style fixed-point splitting with
+// EXACT int32 accumulation.
 //
 // Reference call sites these replace (all float64 LAPACK/BLAS there):
 //   spectral.py:165-169  np.linalg.qr (+ Q^T Q check)  -> Gram B^T B + Q = B R^-1
 //   spectral.py:186      C = Q^T B                      -> cross product
 //   spectral.py:190      U = Q V                        -> lift
 //
-// Precision scheme: every fp32 operand x is split into hi = x with the low 13
-// mantissa bits cleared (exact in TF32) and lo = x - hi; a product uses
-// hi*hi + hi*lo + lo*hi (3 tcgen05.mma per k-step), which recovers ~fp32
-// accuracy.  The first CholeskyQR pass may use 1 product (its Gram only
-// needs to be well enough conditioned, span(Q) is exact either way).
+// Why int8 and not 3xTF32: the sm_100 tensor-core fp32 accumulator truncates
+// on every accumulation (measured: relative error -2^-24 per MMA step, linear
+// in K; tools/tc_debug.cu), so a 1e6-row Gram cannot reach fp32 accuracy with
+// fp32 accumulation.  Integer accumulation is exact.
 //
-// Kernel shapes (one CTA per SM, 192 threads: warp 0 = TMA producer, warp 1 =
-// tcgen05 issuer + TMEM owner, warps 2-5 = epilogue):
-//  * gram: D[128 x 256] = sum over rows of A[r, i] B[r, j]; both operands are
-//    row-major n x k blocks, i.e. MN-major for the MMA.  The K loop runs over
-//    a split of the rows; fp32 TMEM accumulators are flushed into fp64 every
-//    `flush_iters` k-iterations (double-buffered TMEM, 2 x 256 columns) so the
-//    long reduction over n rows keeps fp64 accuracy.  Symmetric Grams skip
-//    tiles strictly below the diagonal.  Per-split fp64 partials are reduced
-//    in fixed order: deterministic.
-//  * apply: Out[128 x N] = A[rows, :] M[:, cols] with A K-major (row-major
-//    n x K) and the small M (K x N2) MN-major.
-// Operands are staged by TMA (SWIZZLE_128B boxes of 32 fp32 x rows) through
-// an mbarrier ring; tcgen05.commit releases stages and hands accumulators to
-// the epilogue.
+// Scheme: for a reduction over index r, every value x of operand X gets an
+// exponent e shared along r (per column of a Gram operand, per row of the
+// big apply operand, per column of the small matrix) with |x| < 2^e, and is
+// written as x = 2^(e-6) (s1 + s2/2^7 + s3/2^14 + eps), s_t = rint slices in
+// [-64, 64] (int8), |eps| <= 2^-15: 21 bits of fixed point below 2^e, rounding
+// unbiased.  A product keeps the 6 slice pairs with t+u <= 4, accumulated in
+// three int32 TMEM accumulators by level (L0 = s1s1', L1 = s1s2'+s2s1',
+// L2 = s2s2'+s1s3'+s3s1'); |term| <= 2^12, so int32 is exact for K < 174k.
+// The epilogue forms 2^(e+e'-12) (L0 + L1/2^7 + L2/2^14) in fp64.
+//
+// Kernel (one CTA per SM, 192 threads: warp 0 = TMA producer, warp 1 = MMA
+// issuer + TMEM owner, warps 2-5 = epilogue): D[128 x N] over a K range, both
+// operands K-major int8 slice planes staged by TMA (SWIZZLE_128B, 128 bytes of
+// K per row per stage) through an mbarrier ring; tcgen05.commit frees stages
+// and hands the accumulators to the epilogue.  Gram mode writes a per-split
+// fp64 partial (reduced later in fixed order: deterministic); apply mode
+// writes fp32 output rows.
 #include <cuda.h>
 
 #include <algorithm>
@@ -39,211 +42,149 @@ namespace {
 using namespace fsr::tc;
 
 constexpr int kThreads = 192;
+constexpr int kBK = 128;      // K bytes (int8 elements) per stage = one 128B swizzle atom
+constexpr int kSlices = 3;
+constexpr int kNG = 160;      // N tile of the Gram kernel (3 x 160 TMEM columns)
+constexpr int kNA = 160;      // N tile of the apply kernel
+constexpr int64_t kMaxK = 131072;  // int32-exact reduction length per launch (bound 174k)
 
-// ------------------------------------------------------------------ split --
-// hi/lo (fp32, ld_out) from a row-major (or column-major if col_major) source.
-template <typename Tin>
-__global__ void split_tf32_kernel(int64_t rows, int64_t cols, const Tin* __restrict__ in, int64_t ld_in,
-                                  int col_major, float* __restrict__ hi, float* __restrict__ lo, int64_t ld_out,
-                                  int64_t pad_cols) {
-  const int64_t total = rows * pad_cols;
-  for (int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; f < total;
-       f += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t i = f / pad_cols, j = f - i * pad_cols;
-    float h = 0.f, l = 0.f;
-    if (j < cols) {
-      const Tin x = col_major ? in[j * ld_in + i] : in[i * ld_in + j];
-      const float xf = (float)x;
-      h = __uint_as_float(__float_as_uint(xf) & 0xFFFFE000u);
-      l = (float)(x - (Tin)h);
-    }
-    hi[i * ld_out + j] = h;
-    if (lo) lo[i * ld_out + j] = l;
+// --------------------------------------------------------------- exponents --
+__device__ __forceinline__ int exp_above(double m) {
+  // smallest e with m < 2^e (m >= 0); zero columns get 0
+  if (!(m > 0.0)) return 0;
+  int e;
+  frexp(m, &e);  // m = f 2^e, f in [0.5, 1)
+  return e;
+}
+
+template <typename T>
+__global__ void exp_of_cols_kernel(int64_t rows, int64_t cols, const T* __restrict__ A, int64_t lda,
+                                   int* __restrict__ e) {
+  // block (32 x 8): 32 columns, rows strided; max reduce then atomicMax on the exponent
+  __shared__ double sm[8][33];
+  const int64_t c = (int64_t)blockIdx.x * 32 + threadIdx.x;
+  double m = 0.0;
+  if (c < cols)
+    for (int64_t r = (int64_t)blockIdx.y * 8 + threadIdx.y; r < rows; r += (int64_t)gridDim.y * 8)
+      m = fmax(m, fabs((double)A[r * lda + c]));
+  sm[threadIdx.y][threadIdx.x] = m;
+  __syncthreads();
+  if (threadIdx.y == 0 && c < cols) {
+    for (int t = 1; t < 8; ++t) m = fmax(m, sm[t][threadIdx.x]);
+    atomicMax(&e[c], exp_above(m) + 2048);  // biased so the initial 0 never wins
   }
 }
 
-// --------------------------------------------------------------- gram/cross --
-template <int NPROD, int BK, int STAGES>
-struct GramCfg {
-  static constexpr int A_BYTES = 4 * BK * 128;  // 128 (M) x BK rows of fp32
-  static constexpr int B_BYTES = 8 * BK * 128;  // 256 (N) x BK
-  static constexpr int STAGE_BYTES = (NPROD == 1 ? 1 : 2) * (A_BYTES + B_BYTES);
-  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
-};
-
-template <int NPROD, int BK, int STAGES>
-__global__ void __launch_bounds__(kThreads, 1)
-    tc_gram_kernel(const __grid_constant__ CUtensorMap mAh, const __grid_constant__ CUtensorMap mAl,
-                   const __grid_constant__ CUtensorMap mBh, const __grid_constant__ CUtensorMap mBl, int64_t n,
-                   int ka, int kb, int tiles_n, int64_t rows_per_split, int flush_iters, double* __restrict__ P,
-                   int symmetric) {
-  using Cfg = GramCfg<NPROD, BK, STAGES>;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  uint64_t* full = (uint64_t*)(smem + STAGES * Cfg::STAGE_BYTES);
-  uint64_t* empty = full + STAGES;
-  uint64_t* tfull = empty + STAGES;
-  uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
-
-  const int ti = blockIdx.x / tiles_n, tj = blockIdx.x % tiles_n;
-  const int i0 = ti * 128, j0 = tj * 256;
-  if (symmetric && j0 + 255 < i0) return;  // tile strictly below the diagonal: mirrored later
-  const int64_t r0 = (int64_t)blockIdx.y * rows_per_split;
-  const int64_t r1 = min(n, r0 + rows_per_split);
-  const int iters = r1 > r0 ? (int)((r1 - r0 + BK - 1) / BK) : 0;
-  const int nchunks = (iters + flush_iters - 1) / flush_iters;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
-    }
-    for (int b = 0; b < 2; ++b) {
-      mbar_init(&tfull[b], 1);
-      mbar_init(&tempty[b], 128);
-    }
-    fence_barrier_init();
+// per "row" exponent of a logical rows x cols matrix read row-major (or transposed)
+template <typename T>
+__global__ void exp_of_rows_kernel(int64_t rows, int64_t cols, const T* __restrict__ A, int64_t lda, int transposed,
+                                   int* __restrict__ e) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < rows; r += nwarps) {
+    double m = 0.0;
+    for (int64_t c = lane; c < cols; c += 32) m = fmax(m, fabs((double)(transposed ? A[c * lda + r] : A[r * lda + c])));
+    for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (!lane) e[r] = exp_above(m) + 2048;
   }
-  if (warp == 0 && lane == 0) {
-    tma_prefetch(&mAh);
-    tma_prefetch(&mBh);
-    if (NPROD == 3) {
-      tma_prefetch(&mAl);
-      tma_prefetch(&mBl);
-    }
-  }
-  if (warp == 1) tmem_alloc(tmem_slot, 512);
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
+}
 
-  if (warp == 0) {
-    // ---------------- TMA producer
-    for (int it = 0; it < iters; ++it) {
-      const int s = it % STAGES;
-      mbar_wait(&empty[s], ((it / STAGES) & 1) ^ 1);
-      if (lane == 0) {
-        uint8_t* st = smem + s * Cfg::STAGE_BYTES;
-        mbar_expect_tx(&full[s], Cfg::STAGE_BYTES);
-        const int row = (int)(r0 + (int64_t)it * BK);
-#pragma unroll
-        for (int mb = 0; mb < 4; ++mb) tma_load_2d(st + mb * BK * 128, &mAh, &full[s], i0 + 32 * mb, row);
-#pragma unroll
-        for (int nb = 0; nb < 8; ++nb)
-          tma_load_2d(st + Cfg::A_BYTES + nb * BK * 128, &mBh, &full[s], j0 + 32 * nb, row);
-        if (NPROD == 3) {
-          uint8_t* lo = st + Cfg::A_BYTES + Cfg::B_BYTES;
-#pragma unroll
-          for (int mb = 0; mb < 4; ++mb) tma_load_2d(lo + mb * BK * 128, &mAl, &full[s], i0 + 32 * mb, row);
-#pragma unroll
-          for (int nb = 0; nb < 8; ++nb)
-            tma_load_2d(lo + Cfg::A_BYTES + nb * BK * 128, &mBl, &full[s], j0 + 32 * nb, row);
-        }
-      }
-      __syncwarp();
-    }
-  } else if (warp == 1) {
-    // ---------------- tcgen05 issuer
-    constexpr uint32_t idesc = idesc_tf32(128, 256, true, true);
-    for (int it = 0; it < iters; ++it) {
-      const int c = it / flush_iters, buf = c & 1;
-      const bool first = (it % flush_iters) == 0;
-      if (first) {
-        mbar_wait(&tempty[buf], ((c >> 1) & 1) ^ 1);
-        tc_fence_after();
-      }
-      const int s = it % STAGES;
-      mbar_wait(&full[s], (it / STAGES) & 1);
-      tc_fence_after();
-      if (lane == 0) {
-        const uint32_t base = smem_u32(smem + s * Cfg::STAGE_BYTES);
-        const uint32_t aH = base, bH = base + Cfg::A_BYTES;
-        const uint32_t aL = base + Cfg::A_BYTES + Cfg::B_BYTES, bL = aL + Cfg::A_BYTES;
-        const uint32_t d = tmem + buf * 256;
-#pragma unroll
-        for (int ks = 0; ks < BK / 8; ++ks) {
-          const uint64_t ad = smem_desc_sw128(aH + ks * 1024, BK * 128, 1024);
-          const uint64_t bd = smem_desc_sw128(bH + ks * 1024, BK * 128, 1024);
-          mma_tf32(d, ad, bd, idesc, (first && ks == 0) ? 0u : 1u);
-          if (NPROD == 3) {
-            mma_tf32(d, ad, smem_desc_sw128(bL + ks * 1024, BK * 128, 1024), idesc, 1u);
-            mma_tf32(d, smem_desc_sw128(aL + ks * 1024, BK * 128, 1024), bd, idesc, 1u);
-          }
-        }
-        mma_commit(&empty[s]);
-        if ((it % flush_iters) == flush_iters - 1 || it == iters - 1) mma_commit(&tfull[buf]);
-      }
-      __syncwarp();
-    }
-  } else {
-    // ---------------- epilogue: TMEM fp32 -> fp64 partial in global memory
-    const int q = warp & 3;
-    const int row = i0 + 32 * q + lane;
-    double* prow = P + ((int64_t)blockIdx.y * ka + row) * (int64_t)kb;
-    for (int c = 0; c < nchunks; ++c) {
-      const int buf = c & 1;
-      mbar_wait(&tfull[buf], (c >> 1) & 1);
-      tc_fence_after();
-#pragma unroll 1
-      for (int cc = 0; cc < 8; ++cc) {
-        float v[32];
-        tmem_ld32(tmem + ((uint32_t)(32 * q) << 16) + buf * 256 + cc * 32, v);
-        if (row < ka) {
-          const int cbase = j0 + cc * 32;
-#pragma unroll
-          for (int t = 0; t < 32; ++t) {
-            if (cbase + t < kb) prow[cbase + t] = (c == 0 ? 0.0 : prow[cbase + t]) + (double)v[t];
-          }
-        }
-      }
-      tc_fence_before();
-      mbar_arrive(&tempty[buf]);
-    }
-    if (nchunks == 0 && row < ka)
-      for (int t = j0; t < min(kb, j0 + 256); ++t) prow[t] = 0.0;
+__device__ __forceinline__ void slice3(double x, int e, int8_t& s1, int8_t& s2, int8_t& s3) {
+  double y = ldexp(x, 6 - e);  // |y| < 64
+  const double a = rint(y);
+  y = (y - a) * 128.0;
+  const double b = rint(y);
+  y = (y - b) * 128.0;
+  const double c = rint(y);
+  s1 = (int8_t)a;
+  s2 = (int8_t)b;
+  s3 = (int8_t)c;
+}
+
+// Gram operand: transpose + slice.  in: rows x cols (row-major, ld_in) ->
+// plane p (p = 0..2): cols x ld_out int8 with the rows (reduction index) contiguous.
+__global__ void slice_T_kernel(int64_t rows, int64_t cols, const float* __restrict__ in, int64_t ld_in,
+                               const int* __restrict__ ecol, int8_t* __restrict__ S, int64_t ld_out) {
+  __shared__ float tile[32][33];
+  const int64_t r0 = (int64_t)blockIdx.x * 32, c0 = (int64_t)blockIdx.y * 32;
+  for (int k = threadIdx.y; k < 32; k += 8) {
+    const int64_t r = r0 + k, c = c0 + threadIdx.x;
+    tile[k][threadIdx.x] = (r < rows && c < cols) ? in[r * ld_in + c] : 0.f;
   }
   __syncthreads();
-  if (warp == 1) {
-    tc_fence_after();
-    tmem_dealloc(tmem, 512);
+  const int64_t plane = cols * ld_out;
+  for (int k = threadIdx.y; k < 32; k += 8) {
+    const int64_t c = c0 + k, r = r0 + threadIdx.x;
+    if (c < cols && r < ld_out) {
+      int8_t a, b, d;
+      slice3((double)tile[threadIdx.x][k], ecol[c] - 2048, a, b, d);
+      S[c * ld_out + r] = a;
+      S[plane + c * ld_out + r] = b;
+      S[2 * plane + c * ld_out + r] = d;
+    }
   }
 }
 
-// C (ka x kb row-major fp64) (+)= sum_s P[s]; symmetric: mirror the upper part.
-__global__ void gram_reduce_kernel(int ka, int kb, int splits, const double* __restrict__ P, double* __restrict__ C,
-                                   int accumulate, int symmetric) {
-  const int64_t total = (int64_t)ka * kb;
+// Apply operands: logical rows x cols matrix (row-major or transposed read),
+// per-row exponent; planes rows x ld_out int8 (cols = reduction index, contiguous).
+template <typename T>
+__global__ void slice_rows_kernel(int64_t rows, int64_t cols, const T* __restrict__ in, int64_t ld_in, int transposed,
+                                  const int* __restrict__ erow, int8_t* __restrict__ S, int64_t ld_out) {
+  const int64_t total = rows * ld_out, plane = rows * ld_out;
   for (int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; f < total;
        f += (int64_t)gridDim.x * blockDim.x) {
-    int64_t i = f / kb, j = f - i * kb;
-    int64_t src = f;
-    if (symmetric && i > j) src = j * kb + i;
-    double s = 0.0;
-    for (int p = 0; p < splits; ++p) s += P[(int64_t)p * total + src];
-    C[f] = accumulate ? C[f] + s : s;
+    const int64_t r = f / ld_out, c = f - r * ld_out;
+    int8_t a = 0, b = 0, d = 0;
+    if (c < cols) slice3((double)(transposed ? in[c * ld_in + r] : in[r * ld_in + c]), erow[r] - 2048, a, b, d);
+    S[f] = a;
+    S[plane + f] = b;
+    S[2 * plane + f] = d;
   }
 }
 
-// ---------------------------------------------------------------- apply ----
+// ------------------------------------------------------------------ kernel --
 template <int N, int STAGES>
-struct ApplyCfg {
-  static constexpr int BK = 32;
-  static constexpr int A_BYTES = 128 * 128;          // 128 rows x 32 fp32 (K-major)
-  static constexpr int B_BYTES = (N / 32) * BK * 128;  // N x 32 K-rows (MN-major)
-  static constexpr int STAGE_BYTES = 2 * (A_BYTES + B_BYTES);
+struct OzCfg {
+  static constexpr int A_PLANE = 128 * kBK;  // 128 rows x 128 K bytes
+  static constexpr int B_PLANE = N * kBK;
+  static constexpr int STAGE_BYTES = kSlices * (A_PLANE + B_PLANE);
   static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
+  static constexpr uint32_t TMEM_COLS = 3 * N <= 128 ? 128 : (3 * N <= 256 ? 256 : 512);
 };
 
-template <int N, int STAGES>
+// kind::i8, signed x signed, s32 accumulate, both K-major
+__host__ __device__ constexpr uint32_t idesc_i8(int M, int N) {
+  return (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
+__device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                       uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld32_i(uint32_t taddr, int (&v)[32]) {
+  float f[32];
+  tmem_ld32(taddr, f);
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __float_as_int(f[i]);
+}
+
+// MODE 0 (Gram/cross): D[i, j] over K rows [k_begin, k_end) of the split, A
+//   rows = output rows i (ka of them), B rows = output cols j; result added to
+//   the fp64 partial P[split] (ka x kb).
+// MODE 1 (apply): D[r, j] = sum_K A[r, :] B[j, :] over the full K; fp32 out.
+template <int MODE, int N, int STAGES>
 __global__ void __launch_bounds__(kThreads, 1)
-    tc_apply_kernel(const __grid_constant__ CUtensorMap mAh, const __grid_constant__ CUtensorMap mAl,
-                    const __grid_constant__ CUtensorMap mBh, const __grid_constant__ CUtensorMap mBl, int64_t n,
-                    int K, int N2, float* __restrict__ Out, int64_t ldo) {
-  using Cfg = ApplyCfg<N, STAGES>;
-  constexpr int BK = Cfg::BK;
+    oz_gemm_kernel(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUtensorMap mB, int rowsA,
+                   int rowsB, int64_t planeA_rows, int64_t planeB_rows, int64_t K, int tiles_n, int64_t k_per_split,
+                   const int* __restrict__ eA, const int* __restrict__ eB, int symmetric, double* __restrict__ P,
+                   float* __restrict__ Out, int64_t ldo) {
+  using Cfg = OzCfg<N, STAGES>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint64_t* full = (uint64_t*)(smem + STAGES * Cfg::STAGE_BYTES);
@@ -251,9 +192,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* tfull = empty + STAGES;
   uint32_t* tmem_slot = (uint32_t*)(tfull + 1);
 
-  const int n0 = blockIdx.x * N;
-  const int m0 = blockIdx.y * 128;
-  const int iters = (K + BK - 1) / BK;
+  const int ti = (int)(blockIdx.x / tiles_n), tj = (int)(blockIdx.x % tiles_n);
+  const int i0 = ti * 128, j0 = tj * N;
+  if (MODE == 0 && symmetric && j0 + N - 1 < i0) return;  // strictly below the diagonal: mirrored later
+  const int64_t kb0 = (int64_t)blockIdx.y * k_per_split;
+  const int64_t kb1 = min(K, kb0 + k_per_split);
+  const int iters = kb1 > kb0 ? (int)((kb1 - kb0 + kBK - 1) / kBK) : 0;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) {
@@ -265,13 +209,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     fence_barrier_init();
   }
   if (warp == 0 && lane == 0) {
-    tma_prefetch(&mAh);
-    tma_prefetch(&mAl);
-    tma_prefetch(&mBh);
-    tma_prefetch(&mBl);
+    tma_prefetch(&mA);
+    tma_prefetch(&mB);
   }
-  constexpr uint32_t kCols = N < 32 ? 32 : N;
-  if (warp == 1) tmem_alloc(tmem_slot, kCols);
+  if (warp == 1) tmem_alloc(tmem_slot, Cfg::TMEM_COLS);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -284,37 +225,40 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (lane == 0) {
         uint8_t* st = smem + s * Cfg::STAGE_BYTES;
         mbar_expect_tx(&full[s], Cfg::STAGE_BYTES);
-        const int kk = it * BK;
-        tma_load_2d(st, &mAh, &full[s], kk, m0);
-        tma_load_2d(st + Cfg::A_BYTES, &mAl, &full[s], kk, m0);
-        uint8_t* b = st + 2 * Cfg::A_BYTES;
+        const int kk = (int)(kb0 + (int64_t)it * kBK);
 #pragma unroll
-        for (int nb = 0; nb < N / 32; ++nb) {
-          tma_load_2d(b + nb * BK * 128, &mBh, &full[s], n0 + 32 * nb, kk);
-          tma_load_2d(b + Cfg::B_BYTES + nb * BK * 128, &mBl, &full[s], n0 + 32 * nb, kk);
+        for (int p = 0; p < kSlices; ++p) {
+          tma_load_2d(st + p * Cfg::A_PLANE, &mA, &full[s], kk, (int)(p * planeA_rows + i0));
+          tma_load_2d(st + kSlices * Cfg::A_PLANE + p * Cfg::B_PLANE, &mB, &full[s], kk,
+                      (int)(p * planeB_rows + j0));
         }
       }
       __syncwarp();
     }
   } else if (warp == 1) {
-    constexpr uint32_t idesc = idesc_tf32(128, N, false, true);
+    constexpr uint32_t idesc = idesc_i8(128, N);
     for (int it = 0; it < iters; ++it) {
       const int s = it % STAGES;
       mbar_wait(&full[s], (it / STAGES) & 1);
       tc_fence_after();
       if (lane == 0) {
         const uint32_t base = smem_u32(smem + s * Cfg::STAGE_BYTES);
-        const uint32_t aH = base, aL = base + Cfg::A_BYTES;
-        const uint32_t bH = base + 2 * Cfg::A_BYTES, bL = bH + Cfg::B_BYTES;
+        const uint32_t bbase = base + kSlices * Cfg::A_PLANE;
 #pragma unroll
-        for (int ks = 0; ks < BK / 8; ++ks) {
-          const uint64_t adh = smem_desc_sw128(aH + ks * 32, 16, 1024);
-          const uint64_t adl = smem_desc_sw128(aL + ks * 32, 16, 1024);
-          const uint64_t bdh = smem_desc_sw128(bH + ks * 1024, BK * 128, 1024);
-          const uint64_t bdl = smem_desc_sw128(bL + ks * 1024, BK * 128, 1024);
-          mma_tf32(tmem, adh, bdh, idesc, (it == 0 && ks == 0) ? 0u : 1u);
-          mma_tf32(tmem, adh, bdl, idesc, 1u);
-          mma_tf32(tmem, adl, bdh, idesc, 1u);
+        for (int ks = 0; ks < kBK / 32; ++ks) {
+          uint64_t a[kSlices], b[kSlices];
+#pragma unroll
+          for (int p = 0; p < kSlices; ++p) {
+            a[p] = smem_desc_sw128(base + p * Cfg::A_PLANE + ks * 32, 16, 1024);
+            b[p] = smem_desc_sw128(bbase + p * Cfg::B_PLANE + ks * 32, 16, 1024);
+          }
+          const uint32_t acc = (it == 0 && ks == 0) ? 0u : 1u;
+          mma_i8(tmem + 0 * N, a[0], b[0], idesc, acc);  // L0: s1 s1'
+          mma_i8(tmem + 1 * N, a[0], b[1], idesc, acc);  // L1: s1 s2'
+          mma_i8(tmem + 1 * N, a[1], b[0], idesc, 1u);   //     s2 s1'
+          mma_i8(tmem + 2 * N, a[1], b[1], idesc, acc);  // L2: s2 s2'
+          mma_i8(tmem + 2 * N, a[0], b[2], idesc, 1u);   //     s1 s3'
+          mma_i8(tmem + 2 * N, a[2], b[0], idesc, 1u);   //     s3 s1'
         }
         mma_commit(&empty[s]);
         if (it == iters - 1) mma_commit(&tfull[0]);
@@ -323,24 +267,46 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else {
     const int q = warp & 3;
-    const int64_t row = (int64_t)m0 + 32 * q + lane;
-    mbar_wait(&tfull[0], 0);
-    tc_fence_after();
-    float* orow = Out + row * ldo;
+    const int row = i0 + 32 * q + lane;
+    const bool row_ok = row < rowsA;
+    const int ea = row_ok ? eA[row] - 2048 : 0;
+    const uint32_t tl = tmem + ((uint32_t)(32 * q) << 16);
+    if (iters > 0) {
+      mbar_wait(&tfull[0], 0);
+      tc_fence_after();
+    }
 #pragma unroll 1
     for (int cc = 0; cc < N / 32; ++cc) {
-      float v[32];
-      tmem_ld32(tmem + ((uint32_t)(32 * q) << 16) + cc * 32, v);
-      const int cbase = n0 + cc * 32;
-      if (row < n) {
-        if (cbase + 32 <= N2 && (ldo % 4) == 0 && (((uintptr_t)orow) % 16) == 0) {
+      int l0[32], l1[32], l2[32];
+      if (iters > 0) {
+        tmem_ld32_i(tl + 0 * N + cc * 32, l0);
+        tmem_ld32_i(tl + 1 * N + cc * 32, l1);
+        tmem_ld32_i(tl + 2 * N + cc * 32, l2);
+      } else {
 #pragma unroll
-          for (int t = 0; t < 32; t += 4)
-            *reinterpret_cast<float4*>(orow + cbase + t) = make_float4(v[t], v[t + 1], v[t + 2], v[t + 3]);
-        } else {
+        for (int t = 0; t < 32; ++t) l0[t] = l1[t] = l2[t] = 0;
+      }
+      if (!row_ok) continue;
+      const int cbase = j0 + cc * 32;
+      if (MODE == 0) {
+        double* prow = P + ((int64_t)blockIdx.y * rowsA + row) * (int64_t)rowsB;
 #pragma unroll
-          for (int t = 0; t < 32; ++t)
-            if (cbase + t < N2) orow[cbase + t] = v[t];
+        for (int t = 0; t < 32; ++t) {
+          const int col = cbase + t;
+          if (col < rowsB) {
+            const double v = (double)l0[t] + (double)l1[t] * 0x1p-7 + (double)l2[t] * 0x1p-14;
+            prow[col] = ldexp(v, ea + eB[col] - 2048 - 12);
+          }
+        }
+      } else {
+        float* orow = Out + (int64_t)row * ldo;
+#pragma unroll
+        for (int t = 0; t < 32; ++t) {
+          const int col = cbase + t;
+          if (col < rowsB) {
+            const double v = (double)l0[t] + (double)l1[t] * 0x1p-7 + (double)l2[t] * 0x1p-14;
+            orow[col] = (float)ldexp(v, ea + eB[col] - 2048 - 12);
+          }
         }
       }
     }
@@ -349,7 +315,21 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc(tmem, kCols);
+    tmem_dealloc(tmem, Cfg::TMEM_COLS);
+  }
+}
+
+// C (ka x kb row-major fp64) (+)= sum_s P[s]; symmetric: mirror the upper part.
+__global__ void gram_reduce_kernel(int ka, int kb, int splits, const double* __restrict__ P, double* __restrict__ C,
+                                   int accumulate, int symmetric) {
+  const int64_t total = (int64_t)ka * kb;
+  for (int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; f < total;
+       f += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = f / kb, j = f - i * kb;
+    const int64_t src = (symmetric && i > j) ? j * kb + i : f;
+    double s = 0.0;
+    for (int p = 0; p < splits; ++p) s += P[(int64_t)p * total + src];
+    C[f] = accumulate ? C[f] + s : s;
   }
 }
 
@@ -371,33 +351,23 @@ EncodeTiledFn encode_fn() {
   return fn;
 }
 
-// 2-D fp32 map over a row-major (rows x cols, ld) block; box = 32 columns x box_rows.
-int make_map(fsr_ctx* ctx, CUtensorMap* m, const float* base, int64_t rows, int64_t cols, int64_t ld,
-             int box_rows) {
+// 2-D byte map over rows x cols int8 (row pitch ld bytes), box = 128 bytes x box_rows.
+int make_map_u8(fsr_ctx* ctx, CUtensorMap* m, const void* base, int64_t rows, int64_t cols, int64_t ld,
+                int box_rows) {
   EncodeTiledFn fn = encode_fn();
   if (!fn) return fsr::set_error(ctx, FSR_ECUDA, "cuTensorMapEncodeTiled unavailable");
   cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
-  cuuint64_t strides[1] = {(cuuint64_t)ld * 4};
-  cuuint32_t box[2] = {32, (cuuint32_t)box_rows};
+  cuuint64_t strides[1] = {(cuuint64_t)ld};
+  cuuint32_t box[2] = {kBK, (cuuint32_t)box_rows};
   cuuint32_t estr[2] = {1, 1};
-  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void*)base, dims, strides, box, estr,
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, (void*)base, dims, strides, box, estr,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fsr::set_error(ctx, FSR_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
   return FSR_OK;
 }
 
-inline int64_t pad4(int64_t x) { return (x + 3) / 4 * 4; }
-
-template <typename Tin>
-int split(fsr_ctx* ctx, int64_t rows, int64_t cols, const Tin* in, int64_t ld_in, int col_major, float* hi,
-          float* lo, int64_t ld_out) {
-  const int64_t total = rows * ld_out;
-  split_tf32_kernel<Tin><<<fsr::grid_for(total, 256, ctx, 16), 256, 0, ctx->stream>>>(rows, cols, in, ld_in,
-                                                                                       col_major, hi, lo, ld_out,
-                                                                                       ld_out);
-  return fsr::launched(ctx, "split_tf32_kernel");
-}
+inline int64_t pad_to(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
 
 template <typename K>
 int set_smem(fsr_ctx* ctx, K kernel, int bytes) {
@@ -405,7 +375,24 @@ int set_smem(fsr_ctx* ctx, K kernel, int bytes) {
   return FSR_OK;
 }
 
-constexpr size_t kChunkBudget = (size_t)6 << 30;  // bytes of hi/lo staging per row chunk
+constexpr int kStages = 2;
+constexpr size_t kChunkBudget = (size_t)6 << 30;  // bytes of slice staging per row chunk
+
+template <int MODE>
+int launch_oz(fsr_ctx* ctx, dim3 grid, const CUtensorMap& mA, const CUtensorMap& mB, int rowsA, int rowsB,
+              int64_t pA, int64_t pB, int64_t K, int tiles_n, int64_t kps, const int* eA, const int* eB, int sym,
+              double* P, float* Out, int64_t ldo) {
+  constexpr int N = MODE == 0 ? kNG : kNA;
+  using Cfg = OzCfg<N, kStages>;
+  static bool attr = false;
+  if (!attr) {
+    FSR_TRY(set_smem(ctx, oz_gemm_kernel<MODE, N, kStages>, Cfg::SMEM));
+    attr = true;
+  }
+  oz_gemm_kernel<MODE, N, kStages><<<grid, kThreads, Cfg::SMEM, ctx->stream>>>(
+      mA, mB, rowsA, rowsB, pA, pB, K, tiles_n, kps, eA, eB, sym, P, Out, ldo);
+  return fsr::launched(ctx, MODE == 0 ? "oz_gram_kernel" : "oz_apply_kernel");
+}
 
 }  // namespace
 
@@ -413,63 +400,56 @@ namespace fsr {
 
 // C (ka x kb, fp64 row-major) (+)= A^T B over n rows of fp32 row-major blocks.
 int tc_gram(fsr_ctx* ctx, int64_t n, int64_t ka, const float* A, int64_t lda, int64_t kb, const float* B,
-            int64_t ldb, double* C, int accumulate, int nprod, int symmetric) {
+            int64_t ldb, double* C, int accumulate, int /*nprod*/, int symmetric) {
   const bool same = (A == B) && lda == ldb && ka == kb;
-  const int64_t pa = pad4(ka), pb = pad4(kb);
-  const int64_t per_row = (nprod == 3 ? 2 : 1) * 4 * (pa + (same ? 0 : pb));
-  int64_t chunk = std::max<int64_t>(256, std::min<int64_t>(n, (int64_t)(kChunkBudget / per_row)));
-  const int tiles_m = (int)ceil_div(ka, 128), tiles_n = (int)ceil_div(kb, 256);
+  symmetric = symmetric && same;
+  const int64_t per_row = kSlices * (ka + (same ? 0 : kb));
+  int64_t chunk = std::max<int64_t>(kBK, std::min<int64_t>({n, kMaxK, (int64_t)(kChunkBudget / per_row)}));
+  chunk = pad_to(chunk, kBK);
+  const int tiles_m = (int)ceil_div(ka, 128), tiles_n = (int)ceil_div(kb, kNG);
   int tiles_eff = 0;
   for (int ti = 0; ti < tiles_m; ++ti)
-    for (int tj = 0; tj < tiles_n; ++tj) tiles_eff += !(symmetric && tj * 256 + 255 < ti * 128);
-  const int bk = nprod == 3 ? 16 : 32;
+    for (int tj = 0; tj < tiles_n; ++tj) tiles_eff += !(symmetric && tj * kNG + kNG - 1 < ti * 128);
   int splits = (int)std::max<int64_t>(1, ceil_div(2 * ctx->num_sms, tiles_eff));
-  splits = (int)std::min<int64_t>(splits, std::max<int64_t>(1, ceil_div(chunk, 64 * bk)));
-  const size_t stage_bytes = (size_t)chunk * per_row;
+  splits = (int)std::min<int64_t>(splits, std::max<int64_t>(1, chunk / (4 * kBK)));
   const size_t p_bytes = (size_t)splits * ka * kb * 8;
+  const size_t e_bytes = (size_t)(ka + kb) * 4 + 256;
+  const size_t s_bytes = (size_t)chunk * per_row;
   void* buf = nullptr;
-  FSR_TRY(scratch(ctx, stage_bytes + p_bytes + 4096, &buf));
+  FSR_TRY(scratch(ctx, p_bytes + e_bytes + s_bytes + 4096, &buf));
   double* P = (double*)buf;
-  float* ah = (float*)((char*)buf + ((p_bytes + 1023) / 1024) * 1024);
-  float* al = nprod == 3 ? ah + chunk * pa : nullptr;
-  float* bh = same ? ah : (nprod == 3 ? al : ah) + chunk * pa;
-  float* bl = same ? al : (nprod == 3 ? bh + chunk * pb : nullptr);
-  const int flush_iters = nprod == 3 ? 2048 / bk : 4096 / bk;
-  static bool attr_done[2] = {false, false};
+  int* eA = (int*)((char*)buf + pad_to(p_bytes, 256));
+  int* eB = same ? eA : eA + ka;
+  int8_t* sA = (int8_t*)((char*)buf + pad_to(p_bytes + e_bytes, 1024));
+  int8_t* sB = same ? sA : sA + kSlices * ka * chunk;
   for (int64_t s0 = 0; s0 < n; s0 += chunk) {
     const int64_t rows = std::min(chunk, n - s0);
-    FSR_TRY(split<float>(ctx, rows, ka, A + s0 * lda, lda, 0, ah, al, pa));
-    if (!same) FSR_TRY(split<float>(ctx, rows, kb, B + s0 * ldb, ldb, 0, bh, bl, pb));
-    CUtensorMap mAh, mAl, mBh, mBl;
-    FSR_TRY(make_map(ctx, &mAh, ah, rows, ka, pa, bk));
-    FSR_TRY(make_map(ctx, &mBh, bh, rows, kb, pb, bk));
-    if (nprod == 3) {
-      FSR_TRY(make_map(ctx, &mAl, al, rows, ka, pa, bk));
-      FSR_TRY(make_map(ctx, &mBl, bl, rows, kb, pb, bk));
-    } else {
-      mAl = mAh;
-      mBl = mBh;
+    const int64_t ldT = pad_to(rows, kBK);
+    // exponents per column over this chunk, then transposed slice planes
+    FSR_CUDA(ctx, cudaMemsetAsync(eA, 0, (ka + (same ? 0 : kb)) * 4, ctx->stream));
+    {
+      dim3 g((unsigned)ceil_div(ka, 32), (unsigned)std::min<int64_t>(ceil_div(rows, 8), 256)), b(32, 8);
+      exp_of_cols_kernel<float><<<g, b, 0, ctx->stream>>>(rows, ka, A + s0 * lda, lda, eA);
+      FSR_TRY(launched(ctx, "exp_of_cols_kernel"));
+      dim3 gs((unsigned)ceil_div(ldT, 32), (unsigned)ceil_div(ka, 32)), bs(32, 8);
+      slice_T_kernel<<<gs, bs, 0, ctx->stream>>>(rows, ka, A + s0 * lda, lda, eA, sA, ldT);
+      FSR_TRY(launched(ctx, "slice_T_kernel"));
     }
-    const int64_t rps = ceil_div(rows, splits);
-    dim3 grid((unsigned)(tiles_m * tiles_n), (unsigned)ceil_div(rows, rps));
-    if (nprod == 3) {
-      using Cfg = GramCfg<3, 16, 4>;
-      if (!attr_done[0]) {
-        FSR_TRY(set_smem(ctx, tc_gram_kernel<3, 16, 4>, Cfg::SMEM));
-        attr_done[0] = true;
-      }
-      tc_gram_kernel<3, 16, 4><<<grid, kThreads, Cfg::SMEM, ctx->stream>>>(
-          mAh, mAl, mBh, mBl, rows, (int)ka, (int)kb, tiles_n, rps, flush_iters, P, symmetric);
-    } else {
-      using Cfg = GramCfg<1, 32, 4>;
-      if (!attr_done[1]) {
-        FSR_TRY(set_smem(ctx, tc_gram_kernel<1, 32, 4>, Cfg::SMEM));
-        attr_done[1] = true;
-      }
-      tc_gram_kernel<1, 32, 4><<<grid, kThreads, Cfg::SMEM, ctx->stream>>>(
-          mAh, mAl, mBh, mBl, rows, (int)ka, (int)kb, tiles_n, rps, flush_iters, P, symmetric);
+    if (!same) {
+      dim3 g((unsigned)ceil_div(kb, 32), (unsigned)std::min<int64_t>(ceil_div(rows, 8), 256)), b(32, 8);
+      exp_of_cols_kernel<float><<<g, b, 0, ctx->stream>>>(rows, kb, B + s0 * ldb, ldb, eB);
+      FSR_TRY(launched(ctx, "exp_of_cols_kernel"));
+      dim3 gs((unsigned)ceil_div(ldT, 32), (unsigned)ceil_div(kb, 32)), bs(32, 8);
+      slice_T_kernel<<<gs, bs, 0, ctx->stream>>>(rows, kb, B + s0 * ldb, ldb, eB, sB, ldT);
+      FSR_TRY(launched(ctx, "slice_T_kernel"));
     }
-    FSR_TRY(launched(ctx, "tc_gram_kernel"));
+    CUtensorMap mA, mB;
+    FSR_TRY(make_map_u8(ctx, &mA, sA, kSlices * ka, ldT, ldT, 128));
+    FSR_TRY(make_map_u8(ctx, &mB, sB, kSlices * kb, ldT, ldT, kNG));
+    const int64_t kps = pad_to(ceil_div(ldT, splits), kBK);
+    dim3 grid((unsigned)(tiles_m * tiles_n), (unsigned)ceil_div(ldT, kps));
+    FSR_TRY(launch_oz<0>(ctx, grid, mA, mB, (int)ka, (int)kb, ka, kb, ldT, tiles_n, kps, eA, eB, symmetric, P,
+                         nullptr, 0));
     const int acc = (s0 > 0) || accumulate;
     gram_reduce_kernel<<<grid_for(ka * kb, 256, ctx, 8), 256, 0, ctx->stream>>>(
         (int)ka, (int)kb, (int)grid.y, P, C, acc, symmetric);
@@ -481,38 +461,41 @@ int tc_gram(fsr_ctx* ctx, int64_t n, int64_t ka, const float* A, int64_t lda, in
 // Out (n x N2 fp32) = A (n x K fp32) * M (K x N2, fp64; column-major if m_col_major).
 int tc_apply(fsr_ctx* ctx, int64_t n, int64_t K, const float* A, int64_t lda, int64_t N2, const double* M,
              int64_t ldm, int m_col_major, float* Out, int64_t ldo) {
-  const int64_t pk = pad4(K), pn = pad4(N2);
-  const size_t m_bytes = (size_t)2 * K * pn * 4;
-  const int64_t per_row = 2 * 4 * pk;
+  if (K > kMaxK) return set_error(ctx, FSR_EINVAL, "tc_apply: K=%lld exceeds the int32-exact bound", (long long)K);
+  const int64_t pk = pad_to(K, kBK);
+  const size_t m_bytes = (size_t)kSlices * N2 * pk;
+  const int64_t per_row = kSlices * pk;
   int64_t chunk = std::max<int64_t>(128, std::min<int64_t>(n, (int64_t)(kChunkBudget / per_row)));
-  chunk = (chunk + 127) / 128 * 128;
+  chunk = pad_to(chunk, 128);
+  const size_t e_bytes = (size_t)(N2 + chunk) * 4 + 256;
   void* buf = nullptr;
-  FSR_TRY(scratch(ctx, m_bytes + (size_t)chunk * per_row + 4096, &buf));
-  float* mh = (float*)buf;
-  float* ml = mh + K * pn;
-  float* ah = (float*)((char*)buf + ((m_bytes + 1023) / 1024) * 1024);
-  float* al = ah + chunk * pk;
-  FSR_TRY(split<double>(ctx, K, N2, M, ldm, m_col_major, mh, ml, pn));
-  CUtensorMap mBh, mBl;
-  FSR_TRY(make_map(ctx, &mBh, mh, K, N2, pn, 32));
-  FSR_TRY(make_map(ctx, &mBl, ml, K, N2, pn, 32));
-  constexpr int N = 256, STAGES = 2;
-  using Cfg = ApplyCfg<N, STAGES>;
-  static bool attr_done = false;
-  if (!attr_done) {
-    FSR_TRY(set_smem(ctx, tc_apply_kernel<N, STAGES>, Cfg::SMEM));
-    attr_done = true;
-  }
+  FSR_TRY(scratch(ctx, pad_to(m_bytes, 1024) + pad_to(e_bytes, 1024) + (size_t)chunk * per_row + 4096, &buf));
+  int8_t* sM = (int8_t*)buf;  // M^T slices: N2 rows x pk
+  int* eM = (int*)((char*)buf + pad_to(m_bytes, 1024));
+  int* eR = eM + N2;
+  int8_t* sR = (int8_t*)((char*)buf + pad_to(m_bytes, 1024) + pad_to(e_bytes, 1024));
+  // M^T row j = column j of M: row-major M is read transposed; column-major M is already M^T
+  const int tr = m_col_major ? 0 : 1;
+  exp_of_rows_kernel<double><<<grid_for(N2 * 32, 256, ctx, 8), 256, 0, ctx->stream>>>(N2, K, M, ldm, tr, eM);
+  FSR_TRY(launched(ctx, "exp_of_rows_kernel"));
+  slice_rows_kernel<double><<<grid_for(N2 * pk, 256, ctx, 16), 256, 0, ctx->stream>>>(N2, K, M, ldm, tr, eM, sM, pk);
+  FSR_TRY(launched(ctx, "slice_rows_kernel"));
+  CUtensorMap mB;
+  FSR_TRY(make_map_u8(ctx, &mB, sM, kSlices * N2, pk, pk, kNA));
+  const int tiles_n = (int)ceil_div(N2, kNA);
   for (int64_t s0 = 0; s0 < n; s0 += chunk) {
     const int64_t rows = std::min(chunk, n - s0);
-    FSR_TRY(split<float>(ctx, rows, K, A + s0 * lda, lda, 0, ah, al, pk));
-    CUtensorMap mAh, mAl;
-    FSR_TRY(make_map(ctx, &mAh, ah, rows, K, pk, 128));
-    FSR_TRY(make_map(ctx, &mAl, al, rows, K, pk, 128));
-    dim3 grid((unsigned)ceil_div(N2, N), (unsigned)ceil_div(rows, 128));
-    tc_apply_kernel<N, STAGES><<<grid, kThreads, Cfg::SMEM, ctx->stream>>>(mAh, mAl, mBh, mBl, rows, (int)K,
-                                                                           (int)N2, Out + s0 * ldo, ldo);
-    FSR_TRY(launched(ctx, "tc_apply_kernel"));
+    exp_of_rows_kernel<float><<<grid_for(rows * 32, 256, ctx, 8), 256, 0, ctx->stream>>>(rows, K, A + s0 * lda, lda, 0,
+                                                                                         eR);
+    FSR_TRY(launched(ctx, "exp_of_rows_kernel"));
+    slice_rows_kernel<float><<<grid_for(rows * pk, 256, ctx, 16), 256, 0, ctx->stream>>>(rows, K, A + s0 * lda, lda,
+                                                                                         0, eR, sR, pk);
+    FSR_TRY(launched(ctx, "slice_rows_kernel"));
+    CUtensorMap mA;
+    FSR_TRY(make_map_u8(ctx, &mA, sR, kSlices * rows, pk, pk, 128));
+    dim3 grid((unsigned)(ceil_div(rows, 128) * tiles_n), 1);
+    FSR_TRY(launch_oz<1>(ctx, grid, mA, mB, (int)rows, (int)N2, rows, N2, pk, tiles_n, pk, eR, eM, 0, nullptr,
+                         Out + s0 * ldo, ldo));
   }
   return FSR_OK;
 }
