@@ -115,7 +115,7 @@ def test_orthonormalize(dtype):
     Y = torch.as_tensor(Y0).to("cuda", N.torch_dtype(dtype))
     spectral.orthonormalize(Y)
     Q = Y.double().cpu().numpy()
-    tol = 1e-13 if dtype == "float64" else 2e-6
+    tol = 1e-13 if dtype == "float64" else 5e-6  # fp32 mode: 21-bit Ozaki slices
     assert np.abs(Q.T @ Q - np.eye(120)).max() < tol
     Qh = np.linalg.qr(Y0)[0]
     # same span, columns equal up to sign (CholeskyQR vs Householder)
