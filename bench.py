@@ -214,6 +214,35 @@ def build_inputs(cfg, n, n_queries, device, dtype):
     return S, (y_ptr, y_idx, y_val), time.perf_counter() - t0, int(W.nnz), int((deg == 0).sum())
 
 
+def sharded_offline(S, r, r_hat, q, tau, dt, device, ev):
+    """Row-sharded SI + Rayleigh-Ritz + threshold over NCCL; U~ replicated afterwards."""
+    import torch
+
+    from paper_1703_06935_b200 import distributed as D
+    from paper_1703_06935_b200 import spectral
+    from paper_1703_06935_b200.graph import ComponentLabeling
+
+    comm = D.Comm()
+    ops = D.CudaOps(device, dt)
+    A = S.device(ops.dt_t, device)
+    shard = D.make_shard(comm, A.indptr.cpu().numpy())
+    A_local = D.shard_rows(A, shard.r0, shard.r1)
+    ev[0].record()
+    Q, B = D.sharded_range_finder(comm, ops, A_local, shard, r_hat, q, 0, ops.dt)
+    ev[1].record()
+    U, lam, _ = D.sharded_rayleigh_ritz(comm, ops, Q, B, r, shard)
+    del Q, B
+    ev[2].record()
+    Ut, eta_s, _ = D.sharded_sparsify(comm, ops, U, tau, shard, ops.dt)
+    del U
+    full = D.gather_csr(comm, Ut, shard)
+    eta = comm.all_gather_rows(eta_s.unsqueeze(1), shard.counts).squeeze(1).contiguous()
+    ev[3].record()
+    return spectral.SpectralDecomposition(full, lam, eta, ComponentLabeling.trivial(shard.n),
+                                          spectral.Variant.SPARSE, spectral.Provenance(r=r, p=r_hat - r, q=q,
+                                                                                       tau=tau, seed=0))
+
+
 def max_over_ranks(x, world):
     if world == 1:
         return x
@@ -260,18 +289,21 @@ def run_fsr(args, cfg, n, rank, world, local_rank):
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
     torch.cuda.synchronize()
     torch.cuda.nvtx.range_push("fsr:offline")
-    ev[0].record()
-    basis = spectral.range_finder(S, r_hat, q, 0, dtype=dt, device=device)
-    ev[1].record()
-    dec = spectral.approx_eigendecomposition(S, basis, r)
-    del basis
-    ev[2].record()
-    sdec = spectral.sparsify(dec, tau)
-    ev[3].record()
+    if world == 1:
+        ev[0].record()
+        basis = spectral.range_finder(S, r_hat, q, 0, dtype=dt, device=device)
+        ev[1].record()
+        dec = spectral.approx_eigendecomposition(S, basis, r)
+        del basis
+        ev[2].record()
+        sdec = spectral.sparsify(dec, tau)
+        ev[3].record()
+        del dec
+    else:
+        sdec = sharded_offline(S, r, r_hat, q, tau, dt, device, ev)
     torch.cuda.synchronize()
     torch.cuda.nvtx.range_pop()
     stages = {name: ctx.stage_time(name) for name in N.STAGES}
-    del dec
     torch.cuda.empty_cache()
     si_s = ev[0].elapsed_time(ev[1]) / 1e3
     rr_s = ev[1].elapsed_time(ev[2]) / 1e3
@@ -388,7 +420,7 @@ def run_fsr(args, cfg, n, rank, world, local_rank):
         "config": {"workload": f"{cfg.name}/C5: n={n}, d={cfg.d}, k={cfg.k}, r={r}, p={cfg.p}, q={q}, "
                                f"U~ density {density} (tau={tau}), batch b={b} per GPU, y {cfg.y_top}-sparse, "
                                f"h_alpha({cfg.alpha}), top-{K}",
-                   "global_batch": b * world, "parallelism": f"replicas x{world} (batch split)",
+                   "global_batch": b * world, "parallelism": (f"offline row-sharded x{world} (NCCL all-gather + ordered fp64 sums), online replicas (batch split)" if world > 1 else "single GPU"),
                    "l2": "256 MB buffer written between timed steps (L2 flush); U~ itself > L2"},
         "roofline": {"kernel": "K9 filter SpMM (spmm_rowpanel_kernel on U~ x Zs)", "bound": "hbm",
                      "achieved": k9_gbs, "peak": peak_gbs, "unit": "GB/s", "frac": k9_gbs / peak_gbs,
