@@ -298,14 +298,9 @@ int filter_impl(fsr_ctx* ctx, int64_t n, int64_t r, int u_sparse, const int64_t*
   T* Zt = (T*)ws;
   ws += align256((size_t)b * r * es);
   T* Zs = nullptr;
-  T* Xnb = nullptr;
   if (u_sparse) {
     Zs = (T*)ws;
     ws += align256((size_t)r * b * es);
-    if (b > 1) {
-      Xnb = (T*)ws;
-      ws += align256((size_t)n * b * es);
-    }
   }
   T* Xout = X;
   if (!Xout) Xout = (T*)ws;
@@ -326,14 +321,9 @@ int filter_impl(fsr_ctx* ctx, int64_t n, int64_t r, int u_sparse, const int64_t*
       fsr::StageTimer timer(ctx, FSR_STAGE_FILTER_SPMM);
       FSR_TRY(fsr::launch_spmm<T>(ctx, n, u_indptr, u_indices, u_values, 1, Zs, 1, Xout, 1));
     } else {
-      {
-        fsr::StageTimer timer(ctx, FSR_STAGE_FILTER_SPMM);
-        FSR_TRY(fsr::launch_spmm<T>(ctx, n, u_indptr, u_indices, u_values, b, Zs, b, Xnb, b));
-      }
-      fsr::StageTimer timer(ctx, FSR_STAGE_TRANSPOSE);
-      dim3 grid((unsigned)fsr::ceil_div(b, 32), (unsigned)fsr::ceil_div(n, 32)), block(32, 8);
-      transpose_kernel<T><<<grid, block, 0, ctx->stream>>>(n, b, Xnb, Xout);
-      FSR_TRY(fsr::launched(ctx, "transpose_kernel"));
+      // K9 writes X (b x n) directly: smem-staged transposed tiles, no separate pass
+      fsr::StageTimer timer(ctx, FSR_STAGE_FILTER_SPMM);
+      FSR_TRY(fsr::launch_spmm_T<T>(ctx, n, u_indptr, u_indices, u_values, b, Zs, b, Xout, n));
     }
   } else {
     fsr::StageTimer timer(ctx, FSR_STAGE_FILTER_SPMM);
@@ -367,7 +357,6 @@ extern "C" {
 int64_t fsr_filter_workspace_bytes(int dtype, int64_t n, int64_t r, int64_t b, int need_x) {
   const size_t es = fsr::dtype_size(dtype);
   size_t total = align256((size_t)b * r * es) + align256((size_t)r * b * es);
-  if (b > 1) total += align256((size_t)n * b * es);
   if (need_x) total += align256((size_t)n * b * es);
   return (int64_t)total + 256;
 }

@@ -58,6 +58,67 @@ __device__ __forceinline__ void store_vec(T* p, const T (&v)[VEC]) {
   *reinterpret_cast<V*>(p) = t;
 }
 
+// acc + a*x: fp64 keeps the product and the sum separately rounded (scipy's
+// sequential y += a*x, bitwise); fp32 has no bitwise target and uses FMA.
+__device__ __forceinline__ double axpy1(double acc, double a, double x) { return mul_add_rn(acc, a, x); }
+__device__ __forceinline__ float axpy1(float acc, float a, float x) { return fmaf(a, x, acc); }
+
+constexpr int kGatherDepth = 4;  // dense rows gathered before their FMAs (memory-level parallelism)
+
+// Accumulate row i of the CSR matrix against the dense panel columns
+// [c0 + u*32*VEC, +VEC) (u < NV) into acc; nonzeros are consumed in CSR order.
+template <typename T, int VEC, int NV>
+__device__ __forceinline__ void row_panel_accumulate(int64_t e0, int64_t e1, const int32_t* __restrict__ indices,
+                                                     const T* __restrict__ vals, const T* __restrict__ X,
+                                                     int64_t ldx, int64_t c0, const bool (&live)[NV],
+                                                     T (&acc)[NV][VEC]) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t base = e0; base < e1; base += 32) {
+    const int m = (e1 - base) < 32 ? (int)(e1 - base) : 32;
+    int my_col = 0;
+    T my_val = T(0);
+    if (lane < m) {
+      my_col = __ldg(indices + base + lane);
+      my_val = __ldg(vals + base + lane);
+    }
+    int j = 0;
+    for (; j + kGatherDepth <= m; j += kGatherDepth) {
+      int c[kGatherDepth];
+      T a[kGatherDepth];
+#pragma unroll
+      for (int g = 0; g < kGatherDepth; ++g) {
+        c[g] = __shfl_sync(0xffffffffu, my_col, j + g);
+        a[g] = __shfl_sync(0xffffffffu, my_val, j + g);
+      }
+      T v[kGatherDepth][NV][VEC];
+#pragma unroll
+      for (int g = 0; g < kGatherDepth; ++g)
+#pragma unroll
+        for (int u = 0; u < NV; ++u)
+          if (live[u]) load_vec<T, VEC>(X + (int64_t)c[g] * ldx + c0 + u * 32 * VEC, v[g][u]);
+#pragma unroll
+      for (int g = 0; g < kGatherDepth; ++g)
+#pragma unroll
+        for (int u = 0; u < NV; ++u)
+#pragma unroll
+          for (int q = 0; q < VEC; ++q) acc[u][q] = axpy1(acc[u][q], a[g], v[g][u][q]);
+    }
+    for (; j < m; ++j) {
+      const int c = __shfl_sync(0xffffffffu, my_col, j);
+      const T a = __shfl_sync(0xffffffffu, my_val, j);
+#pragma unroll
+      for (int u = 0; u < NV; ++u) {
+        if (live[u]) {
+          T v[VEC];
+          load_vec<T, VEC>(X + (int64_t)c * ldx + c0 + u * 32 * VEC, v);
+#pragma unroll
+          for (int q = 0; q < VEC; ++q) acc[u][q] = axpy1(acc[u][q], a, v[q]);
+        }
+      }
+    }
+  }
+}
+
 // One warp per (row, panel); panel width = 32 lanes * VEC * NV columns.
 template <typename T, int VEC, int NV>
 __global__ void __launch_bounds__(256) spmm_rowpanel_kernel(int64_t n_rows, const int64_t* __restrict__ indptr,
@@ -81,35 +142,52 @@ __global__ void __launch_bounds__(256) spmm_rowpanel_kernel(int64_t n_rows, cons
     bool live[NV];
 #pragma unroll
     for (int u = 0; u < NV; ++u) live[u] = c0 + u * 32 * VEC < ncols;
-    const int64_t e0 = __ldg(indptr + i), e1 = __ldg(indptr + i + 1);
-    for (int64_t base = e0; base < e1; base += 32) {
-      const int m = (e1 - base) < 32 ? (int)(e1 - base) : 32;
-      int my_col = 0;
-      T my_val = T(0);
-      if (lane < m) {
-        my_col = __ldg(indices + base + lane);
-        my_val = __ldg(vals + base + lane);
-      }
-#pragma unroll 4
-      for (int j = 0; j < m; ++j) {
-        const int c = __shfl_sync(0xffffffffu, my_col, j);
-        const T a = __shfl_sync(0xffffffffu, my_val, j);
-        const T* xr = X + (int64_t)c * ldx + c0;
-#pragma unroll
-        for (int u = 0; u < NV; ++u) {
-          if (live[u]) {
-            T v[VEC];
-            load_vec<T, VEC>(xr + u * 32 * VEC, v);
-#pragma unroll
-            for (int q = 0; q < VEC; ++q) acc[u][q] = mul_add_rn(acc[u][q], a, v[q]);
-          }
-        }
-      }
-    }
+    row_panel_accumulate<T, VEC, NV>(__ldg(indptr + i), __ldg(indptr + i + 1), indices, vals, X, ldx, c0, live, acc);
     T* yr = Y + i * ldy + c0;
 #pragma unroll
     for (int u = 0; u < NV; ++u)
       if (live[u]) store_vec<T, VEC>(yr + u * 32 * VEC, acc[u]);
+  }
+}
+
+// K9 variant with a transposed output: CTA = 32 consecutive rows x one panel;
+// each warp computes 4 rows, the 32 x PW tile is staged in shared memory
+// (padded) and written as Y^T (ldy = n): 128-byte coalesced column segments.
+template <typename T, int VEC, int NV>
+__global__ void __launch_bounds__(256) spmm_rowpanel_T_kernel(int64_t n_rows, const int64_t* __restrict__ indptr,
+                                                              const int32_t* __restrict__ indices,
+                                                              const T* __restrict__ vals, int64_t ncols,
+                                                              const T* __restrict__ X, int64_t ldx,
+                                                              T* __restrict__ Yt, int64_t ldy) {
+  constexpr int PW = 32 * VEC * NV;
+  __shared__ T tile[32][PW + 1];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t row0 = (int64_t)blockIdx.x * 32;
+  const int64_t p0 = (int64_t)blockIdx.y * PW;
+  const int64_t c0 = p0 + (int64_t)lane * VEC;
+  bool live[NV];
+#pragma unroll
+  for (int u = 0; u < NV; ++u) live[u] = c0 + u * 32 * VEC < ncols;
+  for (int rr = warp; rr < 32; rr += 8) {
+    const int64_t i = row0 + rr;
+    T acc[NV][VEC];
+#pragma unroll
+    for (int u = 0; u < NV; ++u)
+#pragma unroll
+      for (int q = 0; q < VEC; ++q) acc[u][q] = T(0);
+    if (i < n_rows)
+      row_panel_accumulate<T, VEC, NV>(__ldg(indptr + i), __ldg(indptr + i + 1), indices, vals, X, ldx, c0, live,
+                                       acc);
+#pragma unroll
+    for (int u = 0; u < NV; ++u)
+#pragma unroll
+      for (int q = 0; q < VEC; ++q) tile[rr][lane * VEC + u * 32 * VEC + q] = acc[u][q];
+  }
+  __syncthreads();
+  const int64_t i = row0 + lane;
+  for (int c = warp; c < PW; c += 8) {
+    const int64_t col = p0 + c;
+    if (col < ncols && i < n_rows) Yt[col * ldy + i] = tile[lane][c];
   }
 }
 
@@ -133,6 +211,31 @@ __global__ void __launch_bounds__(256) spmv_kernel(int64_t n_rows, const int64_t
 }
 
 inline bool aligned(const void* p, int bytes) { return ((uintptr_t)p % bytes) == 0; }
+
+// Y^T (ncols x n_rows, ld = ldy) = A X for ncols >= 2 (online K9 output layout).
+template <typename T>
+int launch_spmm_T(fsr_ctx* ctx, int64_t n_rows, const int64_t* indptr, const int32_t* indices, const T* vals,
+                  int64_t ncols, const T* X, int64_t ldx, T* Yt, int64_t ldy) {
+  if (n_rows <= 0 || ncols <= 0) return FSR_OK;
+  constexpr int VW = sizeof(T) == 4 ? 4 : 2;
+  const bool vec_ok = ncols % VW == 0 && ldx % VW == 0 && aligned(X, 16);
+  dim3 block(256);
+  if (vec_ok && ncols > 32 * VW) {
+    constexpr int NV = 2, PW = 32 * VW * NV;
+    dim3 grid((unsigned)ceil_div(n_rows, 32), (unsigned)ceil_div(ncols, PW));
+    spmm_rowpanel_T_kernel<T, VW, NV><<<grid, block, 0, ctx->stream>>>(n_rows, indptr, indices, vals, ncols, X, ldx,
+                                                                        Yt, ldy);
+  } else if (vec_ok) {
+    dim3 grid((unsigned)ceil_div(n_rows, 32), (unsigned)ceil_div(ncols, 32 * VW));
+    spmm_rowpanel_T_kernel<T, VW, 1><<<grid, block, 0, ctx->stream>>>(n_rows, indptr, indices, vals, ncols, X, ldx,
+                                                                       Yt, ldy);
+  } else {
+    dim3 grid((unsigned)ceil_div(n_rows, 32), (unsigned)ceil_div(ncols, 32));
+    spmm_rowpanel_T_kernel<T, 1, 1><<<grid, block, 0, ctx->stream>>>(n_rows, indptr, indices, vals, ncols, X, ldx,
+                                                                      Yt, ldy);
+  }
+  return launched(ctx, "spmm_rowpanel_T_kernel");
+}
 
 template <typename T>
 int launch_spmm(fsr_ctx* ctx, int64_t n_rows, const int64_t* indptr, const int32_t* indices, const T* vals,
