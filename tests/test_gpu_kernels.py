@@ -177,7 +177,8 @@ def test_kat_full_rank_reproduces_exact_spectrum(golden, dtype, tol):
     ev = np.sort(np.linalg.eigvalsh(k["rand_W_dense"]))[::-1][:16]
     assert np.abs(dec.eigenvalues - ev).max() < tol
     U = dec.U
-    assert np.abs(U.T @ U - np.eye(16)).max() < (1e-12 if dtype == "float64" else 1e-6)
+    # fp32 mode: 21-bit Ozaki slices in the dense stages
+    assert np.abs(U.T @ U - np.eye(16)).max() < (1e-12 if dtype == "float64" else 1e-5)
 
 
 def test_kat_random_sparsify_and_filter(golden):
