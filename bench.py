@@ -55,6 +55,7 @@ def parse_args():
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--skip-e2e", action="store_true")
+    ap.add_argument("--no-sweep", action="store_true", help="skip the C5 online sweep")
     return ap.parse_args()
 
 
@@ -243,6 +244,75 @@ def sharded_offline(S, r, r_hat, q, tau, dt, device, ev):
                                                                                        tau=tau, seed=0))
 
 
+def online_sweep(dec, sdec_default, density_default, cfg, n, r, queries, device, ctx, es, steps=3, warmup=2):
+    """BASELINE C5: batches {1, 64, 1024, 10000} x U~ density {1, 2, 5}% with h_alpha(0.99),
+    plus h_alpha(0.9) and heat exp(-10(1-x)) at 2% / b=1024.  Device-resident, top-100."""
+    import torch
+
+    from paper_1703_06935_b200 import ranking, spectral
+
+    out = []
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=device)
+    dens = sorted({0.01, 0.02, 0.05, density_default})
+    batches = [1, 64, 1024, 10000]
+    pool = queries.b
+    for d in dens:
+        sd = sdec_default if d == density_default else spectral.sparsify(dec, int(round(d * n * r)))
+        tfs = [("h_alpha(0.99)", ranking.h_alpha(0.99))]
+        if d == 0.02:
+            tfs += [("h_alpha(0.9)", ranking.h_alpha(0.9)), ("heat(10)", ranking.heat_kernel(10.0))]
+        for b in batches:
+            if b > pool:
+                reps = -(-b // pool)
+                qb = ranking.QueryBatch(n, *_repeat_batch(queries, reps, b))
+            else:
+                e = queries.y_ptr[b]
+                qb = ranking.QueryBatch(n, queries.y_ptr[:b + 1], queries.y_idx[:e], queries.y_val[:e])
+            dq = ranking.DeviceQueries(qb, sd.dtype, device)
+            for name, h in tfs:
+                if name != "h_alpha(0.99)" and b != 1024:
+                    continue
+                res = ranking.FilterResult()
+                for _ in range(warmup):
+                    ranking.filter_device(sd, h, dq, topk=100, want_x=False, out=res)
+                torch.cuda.synchronize()
+                ctx.stage_reset()
+                ms = 0.0
+                for _ in range(steps):
+                    flush.zero_()
+                    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    e0.record()
+                    ranking.filter_device(sd, h, dq, topk=100, want_x=False, out=res)
+                    e1.record()
+                    torch.cuda.synchronize()
+                    ms += e0.elapsed_time(e1)
+                k9_ms, k9_cnt = ctx.stage_time("filter_spmm")
+                kept = sd.U_device.nnz
+                k9_bytes = kept * (es + 4) + (n + 1) * 8 + es * r * b + es * n * b
+                out.append({"density": d, "b": b, "h": name, "queries_per_s": b * steps / (ms / 1e3),
+                            "ms_per_batch": ms / steps, "k9_ms": k9_ms / max(k9_cnt, 1),
+                            "k9_algorithmic_gbs": k9_bytes / (k9_ms / max(k9_cnt, 1) * 1e-3) / 1e9,
+                            "k9_fp32_tflops": 2.0 * kept * b / (k9_ms / max(k9_cnt, 1) * 1e-3) / 1e12})
+                del res
+            del dq
+        if sd is not sdec_default:
+            del sd
+        torch.cuda.empty_cache()
+    return out
+
+
+def _repeat_batch(queries, reps, b):
+    ptr = [0]
+    idx, val = [], []
+    for j in range(b):
+        k = j % queries.b
+        s, e = queries.y_ptr[k], queries.y_ptr[k + 1]
+        idx.append(queries.y_idx[s:e])
+        val.append(queries.y_val[s:e])
+        ptr.append(ptr[-1] + (e - s))
+    return np.asarray(ptr, np.int64), np.concatenate(idx), np.concatenate(val)
+
+
 def max_over_ranks(x, world):
     if world == 1:
         return x
@@ -298,7 +368,8 @@ def run_fsr(args, cfg, n, rank, world, local_rank):
         ev[2].record()
         sdec = spectral.sparsify(dec, tau)
         ev[3].record()
-        del dec
+        if args.no_sweep:
+            del dec
     else:
         sdec = sharded_offline(S, r, r_hat, q, tau, dt, device, ev)
     torch.cuda.synchronize()
@@ -398,6 +469,13 @@ def run_fsr(args, cfg, n, rank, world, local_rank):
                "api": "ranking.DeviceQueries (pinned H2D) + ranking.filter_device(topk) + top-k D2H"}
     clk = clocks.stop()
 
+    # ---------------- C5 online sweep (BASELINE config 5) ----------------------
+    sweep = None
+    if world == 1 and not args.no_sweep:
+        del ws, res
+        sweep = online_sweep(dec, sdec, density, cfg, n, r, all_queries, device, ctx, es)
+        del dec
+
     # ---------------- CPU baseline (rank 0, N=1) -----------------------------
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -433,6 +511,7 @@ def run_fsr(args, cfg, n, rank, world, local_rank):
         "e2e": e2e,
         "cpu_baseline": cpu,
         "clocks": clk,
+        "c5_sweep": sweep,
     }
     print(json.dumps(line), flush=True)
 
