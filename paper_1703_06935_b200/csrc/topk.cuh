@@ -1,0 +1,353 @@
+// Exact top-k per row in the reference's rank order (ranking.py:390-395:
+// descending score, ties by ascending index), for b rows of length n.
+//
+// One CTA selects the top K of a contiguous range of a row:
+//  * order keys: IEEE bits mapped to unsigned so that key order == value order
+//    (-0 folded onto +0, numpy compares values);
+//  * long ranges: a 1/16 block sample (two 12-bit digit histograms) proposes a
+//    threshold key, ONE pass over the range collects every key >= threshold
+//    into shared memory, a bitonic sort on (key desc, index asc) finishes;
+//  * short ranges, and whenever the sampled threshold yields fewer than K or
+//    more than kCap candidates: the exact path -- a digit histogram pins the
+//    K-th key bin, candidates >= that bin are collected (or, if that overflows,
+//    the exact threshold key T is pinned digit by digit and the ties at T are
+//    taken in index order).
+// Few rows (b small) are split into segments: stage 1 emits each segment's
+// top K (sorted, so equal keys stay in index order), stage 2 selects from the
+// per-row candidate lists with their explicit indices.
+#pragma once
+
+#include <cub/cub.cuh>
+
+#include <algorithm>
+
+#include "fsr_common.cuh"
+
+namespace fsr {
+namespace topk {
+
+constexpr int kThreads = 512;
+constexpr int kCap = 4096;  // candidates held in shared memory
+constexpr int kHistBits = 12;
+constexpr int kSampleChunk = 1024;  // elements per sampled block
+constexpr int kSampleEvery = 16;    // one block of every 16 is sampled
+
+__device__ __forceinline__ uint64_t order_key(float x) {
+  if (x == 0.0f) x = 0.0f;
+  const uint32_t u = __float_as_uint(x);
+  return (uint64_t)((u & 0x80000000u) ? ~u : (u | 0x80000000u));
+}
+__device__ __forceinline__ uint64_t order_key(double x) {
+  if (x == 0.0) x = 0.0;
+  const uint64_t u = (uint64_t)__double_as_longlong(x);
+  return (u & 0x8000000000000000ull) ? ~u : (u | 0x8000000000000000ull);
+}
+
+struct Shared {
+  unsigned int hist[1 << kHistBits];
+  unsigned int count;
+  unsigned int found_bin;
+  unsigned long long above;
+  unsigned long long warp_sums[kThreads / 32];
+};
+
+// The bin (scanning from the top) where the running count first reaches `need`
+// (or the lowest bin if the total is smaller); found_bin / above (count strictly above).
+__device__ void find_bin(Shared& sh, int nb, unsigned long long need) {
+  typedef cub::BlockScan<unsigned long long, kThreads> Scan;
+  __shared__ typename Scan::TempStorage scan_tmp;
+  const int per = nb / kThreads > 0 ? nb / kThreads : 1;
+  unsigned long long mine = 0;
+  const int hi = nb - 1 - (int)threadIdx.x * per;
+  for (int q = 0; q < per; ++q) {
+    const int bin = hi - q;
+    if (bin >= 0) mine += sh.hist[bin];
+  }
+  if (threadIdx.x == 0) {
+    sh.found_bin = 0;
+    sh.above = 0;
+  }
+  __syncthreads();
+  unsigned long long before = 0, total = 0;
+  Scan(scan_tmp).ExclusiveSum(mine, before, total);
+  unsigned long long run = before;
+  for (int q = 0; q < per; ++q) {
+    const int bin = hi - q;
+    if (bin < 0) break;
+    const unsigned long long h = sh.hist[bin];
+    if (run < need && run + h >= need) {
+      sh.found_bin = (unsigned)bin;
+      sh.above = run;
+    }
+    run += h;
+  }
+  if (total < need && threadIdx.x == 0) sh.above = total;  // everything qualifies; bin 0
+  __syncthreads();
+}
+
+__device__ __forceinline__ bool before_in_rank(uint64_t ka, int64_t ia, uint64_t kb, int64_t ib) {
+  return ka > kb || (ka == kb && ia < ib);
+}
+
+__device__ void bitonic_sort(uint64_t* key, int64_t* idx, int count) {
+  int P = 1;
+  while (P < count) P <<= 1;
+  for (int t = count + threadIdx.x; t < P; t += blockDim.x) {
+    key[t] = 0;
+    idx[t] = INT64_MAX;
+  }
+  __syncthreads();
+  for (int size = 2; size <= P; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int t = threadIdx.x; t < P / 2; t += blockDim.x) {
+        const int lo = 2 * t - (t & (stride - 1));
+        const int hi = lo + stride;
+        const bool up = (lo & size) == 0;
+        const bool swap = up ? before_in_rank(key[hi], idx[hi], key[lo], idx[lo])
+                             : before_in_rank(key[lo], idx[lo], key[hi], idx[hi]);
+        if (swap) {
+          const uint64_t tk = key[lo];
+          key[lo] = key[hi];
+          key[hi] = tk;
+          const int64_t ti = idx[lo];
+          idx[lo] = idx[hi];
+          idx[hi] = ti;
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+// Range view: element e (0 <= e < m) is value v[e] with index ix(e).
+template <typename T, bool EXPLICIT>
+struct Range {
+  const T* v;
+  const int64_t* ix;
+  int64_t m;
+  int64_t base;  // implicit index of element 0
+  __device__ __forceinline__ int64_t index(int64_t e) const { return EXPLICIT ? ix[e] : base + e; }
+};
+
+// Exact selection of the top K of a range (keys, indices into ckey/cidx, sorted).
+template <typename T, bool EXPLICIT>
+__device__ void select_exact(const Range<T, EXPLICIT>& R, int64_t K, Shared& sh, uint64_t* ckey, int64_t* cidx) {
+  constexpr int KB = sizeof(T) * 8;
+  constexpr int nb = 1 << kHistBits;
+  for (int t = threadIdx.x; t < nb; t += blockDim.x) sh.hist[t] = 0;
+  if (!threadIdx.x) sh.count = 0;
+  __syncthreads();
+  for (int64_t e = threadIdx.x; e < R.m; e += blockDim.x)
+    atomicAdd(&sh.hist[order_key(R.v[e]) >> (KB - kHistBits)], 1u);
+  __syncthreads();
+  find_bin(sh, nb, (unsigned long long)K);
+  uint64_t prefix = sh.found_bin;
+  int pbits = kHistBits;
+  const unsigned long long above = sh.above;
+  const unsigned long long in_bin = sh.hist[prefix];
+  __syncthreads();
+  if (above + in_bin <= (unsigned long long)kCap) {
+    for (int64_t e = threadIdx.x; e < R.m; e += blockDim.x) {
+      const uint64_t k = order_key(R.v[e]);
+      if ((k >> (KB - kHistBits)) >= prefix) {
+        const unsigned slot = atomicAdd(&sh.count, 1u);
+        ckey[slot] = k;
+        cidx[slot] = R.index(e);
+      }
+    }
+    __syncthreads();
+    bitonic_sort(ckey, cidx, (int)sh.count);
+    return;
+  }
+  // pin the exact threshold key, then take ties in position (= index) order
+  unsigned long long need = (unsigned long long)K - above;
+  while (pbits < KB) {
+    const int d = KB - pbits < kHistBits ? KB - pbits : kHistBits;
+    const int shift = KB - pbits - d;
+    for (int t = threadIdx.x; t < nb; t += blockDim.x) sh.hist[t] = 0;
+    __syncthreads();
+    for (int64_t e = threadIdx.x; e < R.m; e += blockDim.x) {
+      const uint64_t k = order_key(R.v[e]);
+      if ((k >> (KB - pbits)) == prefix) atomicAdd(&sh.hist[(k >> shift) & ((1u << d) - 1u)], 1u);
+    }
+    __syncthreads();
+    find_bin(sh, 1 << d, need);
+    need -= sh.above;
+    prefix = (prefix << d) | sh.found_bin;
+    pbits += d;
+    __syncthreads();
+  }
+  const uint64_t Tk = prefix;
+  const unsigned long long gt_total = (unsigned long long)K - need;
+  for (int64_t e = threadIdx.x; e < R.m; e += blockDim.x) {
+    const uint64_t k = order_key(R.v[e]);
+    if (k > Tk) {
+      const unsigned slot = atomicAdd(&sh.count, 1u);
+      ckey[slot] = k;
+      cidx[slot] = R.index(e);
+    }
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  unsigned long long taken = 0;
+  for (int64_t base = 0; base < R.m && taken < need; base += blockDim.x) {
+    const int64_t e = base + threadIdx.x;
+    const bool tie = e < R.m && order_key(R.v[e]) == Tk;
+    const unsigned msk = __ballot_sync(0xffffffffu, tie);
+    if (!lane) sh.warp_sums[wid] = __popc(msk);
+    __syncthreads();
+    unsigned long long off = 0, tot = 0;
+    for (int w = 0; w < kThreads / 32; ++w) {
+      if (w < wid) off += sh.warp_sums[w];
+      tot += sh.warp_sums[w];
+    }
+    const unsigned long long rnk = taken + off + __popc(msk & ((1u << lane) - 1u));
+    if (tie && rnk < need) {
+      ckey[gt_total + rnk] = Tk;
+      cidx[gt_total + rnk] = R.index(e);
+    }
+    taken += tot;
+    __syncthreads();
+  }
+  bitonic_sort(ckey, cidx, (int)K);
+}
+
+// Sampled single-pass selection; returns false when the caller must fall back.
+template <typename T>
+__device__ bool select_sampled(const Range<T, false>& R, int64_t K, Shared& sh, uint64_t* ckey, int64_t* cidx) {
+  constexpr int KB = sizeof(T) * 8;
+  constexpr int nb = 1 << kHistBits;
+  // sample: two digit levels over blocks 0, 16, 32, ... of kSampleChunk elements
+  const int64_t nblk = (R.m + kSampleChunk - 1) / kSampleChunk;
+  const unsigned long long target = (unsigned long long)((3 * K + kSampleEvery - 1) / kSampleEvery) + 4;
+  uint64_t prefix = 0;
+  unsigned long long above0 = 0;
+  for (int level = 0; level < 2; ++level) {
+    for (int t = threadIdx.x; t < nb; t += blockDim.x) sh.hist[t] = 0;
+    __syncthreads();
+    for (int64_t b = 0; b < nblk; b += kSampleEvery) {
+      const int64_t e0 = b * kSampleChunk, e1 = min(R.m, e0 + kSampleChunk);
+      for (int64_t e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
+        const uint64_t k = order_key(R.v[e]);
+        if (level == 0)
+          atomicAdd(&sh.hist[k >> (KB - kHistBits)], 1u);
+        else if ((k >> (KB - kHistBits)) == prefix)
+          atomicAdd(&sh.hist[(k >> (KB - 2 * kHistBits)) & (nb - 1)], 1u);
+      }
+    }
+    __syncthreads();
+    find_bin(sh, nb, level == 0 ? target : target - above0);
+    if (level == 0) above0 = sh.above;
+    prefix = (prefix << kHistBits) | sh.found_bin;
+    __syncthreads();
+  }
+  const uint64_t T_lo = prefix << (KB - 2 * kHistBits);  // candidates: key >= T_lo
+  if (!threadIdx.x) sh.count = 0;
+  __syncthreads();
+  for (int64_t e = threadIdx.x; e < R.m; e += blockDim.x) {
+    const uint64_t k = order_key(R.v[e]);
+    if (k >= T_lo) {
+      const unsigned slot = atomicAdd(&sh.count, 1u);
+      if (slot < (unsigned)kCap) {
+        ckey[slot] = k;
+        cidx[slot] = R.base + e;
+      }
+    }
+  }
+  __syncthreads();
+  const unsigned c = sh.count;
+  if (c < (unsigned)K || c > (unsigned)kCap) return false;
+  bitonic_sort(ckey, cidx, (int)c);
+  return true;
+}
+
+// grid.x = rows * segs; row q = blockIdx.x / segs, segment s = blockIdx.x % segs.
+// Input element e of (q, s): src[q * ld + s * seg + e] (e < len - s * seg, <= seg),
+// index = EXPLICIT ? isrc[same] : s * seg + e.  Output: K (value, index) pairs at
+// out_*[blockIdx.x * K], sorted in rank order; padded with (-inf, INT64_MAX).
+template <typename T, bool EXPLICIT>
+__global__ void __launch_bounds__(kThreads) select_kernel(const T* __restrict__ src, const int64_t* __restrict__ isrc,
+                                                          int64_t ld, int64_t len, int64_t seg, int segs, int64_t K,
+                                                          int use_sample, T* __restrict__ out_val,
+                                                          int64_t* __restrict__ out_idx) {
+  extern __shared__ __align__(16) unsigned char dyn[];
+  uint64_t* ckey = (uint64_t*)dyn;
+  int64_t* cidx = (int64_t*)(ckey + kCap);
+  __shared__ Shared sh;
+  const int64_t q = blockIdx.x / segs, s = blockIdx.x % segs;
+  const int64_t b0 = s * seg, b1 = min(len, b0 + seg);
+  Range<T, EXPLICIT> R{src + q * ld + b0, EXPLICIT ? isrc + q * ld + b0 : nullptr, b1 > b0 ? b1 - b0 : 0, b0};
+  const int64_t Kr = min(K, R.m);
+  bool done = false;
+  if (!EXPLICIT && use_sample && R.m >= (int64_t)kSampleChunk * kSampleEvery * 4 && Kr == K)
+    done = select_sampled<T>(*reinterpret_cast<const Range<T, false>*>(&R), K, sh, ckey, cidx);
+  __syncthreads();
+  if (!done && Kr > 0) select_exact<T, EXPLICIT>(R, Kr, sh, ckey, cidx);
+  __syncthreads();
+  for (int64_t m = threadIdx.x; m < K; m += blockDim.x) {
+    const int64_t o = (int64_t)blockIdx.x * K + m;
+    if (m < Kr) {
+      const int64_t i = cidx[m];
+      out_idx[o] = i;
+      out_val[o] = EXPLICIT ? T(0) : R.v[i - b0];
+    } else {
+      out_idx[o] = INT64_MAX;
+      out_val[o] = -INFINITY;
+    }
+  }
+  if (EXPLICIT) {
+    // values: recover from the key order (search the candidate list for the index)
+    __syncthreads();
+    for (int64_t m = threadIdx.x; m < Kr; m += blockDim.x) {
+      const uint64_t k = ckey[m];
+      const uint64_t u = (k & (1ull << (sizeof(T) * 8 - 1))) ? (k & ~(1ull << (sizeof(T) * 8 - 1))) : ~k;
+      T v;
+      if (sizeof(T) == 4) {
+        const uint32_t u32 = (uint32_t)u;
+        memcpy(&v, &u32, 4);
+      } else {
+        memcpy(&v, &u, 8);
+      }
+      out_val[(int64_t)blockIdx.x * K + m] = v;
+    }
+  }
+}
+
+template <typename T>
+int launch(fsr_ctx* ctx, int64_t b, int64_t n, const T* X, int64_t ldx, int64_t K, int64_t* top_idx, T* top_val) {
+  const size_t smem = (size_t)kCap * 16;
+  static bool configured[2][2] = {{false, false}, {false, false}};
+  const int ti = sizeof(T) == 8;
+  if (!configured[ti][0]) {
+    FSR_CUDA(ctx, cudaFuncSetAttribute(select_kernel<T, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem));
+    FSR_CUDA(ctx, cudaFuncSetAttribute(select_kernel<T, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem));
+    configured[ti][0] = configured[ti][1] = true;
+  }
+  int segs = 1;
+  if (b < ctx->num_sms) {
+    segs = (int)std::min<int64_t>(ceil_div(2 * ctx->num_sms, b), std::max<int64_t>(1, n / (8 * K)));
+    segs = std::max(segs, 1);
+  }
+  if (segs == 1) {
+    select_kernel<T, false><<<(unsigned)b, kThreads, smem, ctx->stream>>>(X, nullptr, ldx, n, n, 1, K, 1, top_val,
+                                                                          top_idx);
+    return launched(ctx, "topk_select_kernel");
+  }
+  const int64_t seg = ceil_div(n, segs);
+  void* buf = nullptr;
+  const size_t cand = (size_t)b * segs * K;
+  FSR_TRY(scratch(ctx, cand * (sizeof(T) + 8) + 256, &buf));
+  int64_t* cidx = (int64_t*)buf;
+  T* cval = (T*)(cidx + cand);
+  select_kernel<T, false><<<(unsigned)(b * segs), kThreads, smem, ctx->stream>>>(X, nullptr, ldx, n, seg, segs, K, 1,
+                                                                                 cval, cidx);
+  FSR_TRY(launched(ctx, "topk_select_kernel"));
+  select_kernel<T, true><<<(unsigned)b, kThreads, smem, ctx->stream>>>(cval, cidx, segs * K, segs * K, segs * K, 1, K,
+                                                                       0, top_val, top_idx);
+  return launched(ctx, "topk_merge_kernel");
+}
+
+}  // namespace topk
+}  // namespace fsr
