@@ -197,16 +197,102 @@ __global__ void __launch_bounds__(256) spmv_kernel(int64_t n_rows, const int64_t
                                                    const int32_t* __restrict__ indices,
                                                    const T* __restrict__ vals, const T* __restrict__ x,
                                                    T* __restrict__ y, int64_t ldy) {
+  // 4 nonzeros per lane in flight (128 per warp iteration): the index/value
+  // streams are the HBM traffic, the gathers of x hit L1/L2.
   const int lane = threadIdx.x & 31;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < n_rows; i += nwarps) {
     T acc = T(0);
-    const int64_t e1 = __ldg(indptr + i + 1);
-    for (int64_t e = __ldg(indptr + i) + lane; e < e1; e += 32)
-      acc = mul_add_rn(acc, __ldg(vals + e), __ldg(x + __ldg(indices + e)));
+    const int64_t e0 = __ldg(indptr + i), e1 = __ldg(indptr + i + 1);
+    for (int64_t base = e0 + lane; base < e1; base += 128) {
+      int c[4];
+      T a[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int64_t e = base + 32 * u;
+        c[u] = e < e1 ? __ldg(indices + e) : -1;
+        a[u] = e < e1 ? __ldg(vals + e) : T(0);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (c[u] >= 0) acc = axpy1(acc, a[u], __ldg(x + c[u]));
+    }
 #pragma unroll
     for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
     if (!lane) y[i * ldy] = acc;
+  }
+}
+
+// Narrow dense blocks (ncols <= 16 * VEC): LPR lanes per row, 32/LPR rows per
+// warp, each sub-group broadcasting its row's (col, val) chunk with a width-LPR
+// shuffle.  Output Y^T (ldy = n) via a padded shared tile, like the wide kernel.
+template <typename T, int VEC, int LPR>
+__global__ void __launch_bounds__(256) spmm_narrow_T_kernel(int64_t n_rows, const int64_t* __restrict__ indptr,
+                                                            const int32_t* __restrict__ indices,
+                                                            const T* __restrict__ vals, int64_t ncols,
+                                                            const T* __restrict__ X, int64_t ldx,
+                                                            T* __restrict__ Yt, int64_t ldy) {
+  constexpr int PW = LPR * VEC;
+  constexpr int RPW = 32 / LPR;  // rows per warp pass
+  __shared__ T tile[64][PW + 1];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int sub = lane / LPR, sl = lane % LPR;
+  const unsigned mask = LPR == 32 ? 0xffffffffu : (((1u << LPR) - 1u) << (sub * LPR));
+  const int64_t row0 = (int64_t)blockIdx.x * 64;
+  const int64_t c0 = (int64_t)sl * VEC;
+  const bool live = c0 < ncols;
+  for (int rr = warp * RPW + sub; rr < 64; rr += 8 * RPW) {
+    const int64_t i = row0 + rr;
+    T acc[VEC];
+#pragma unroll
+    for (int q = 0; q < VEC; ++q) acc[q] = T(0);
+    if (i < n_rows) {
+      const int64_t e0 = __ldg(indptr + i), e1 = __ldg(indptr + i + 1);
+      for (int64_t base = e0; base < e1; base += LPR) {
+        const int m = (e1 - base) < LPR ? (int)(e1 - base) : LPR;
+        int my_col = 0;
+        T my_val = T(0);
+        if (sl < m) {
+          my_col = __ldg(indices + base + sl);
+          my_val = __ldg(vals + base + sl);
+        }
+        int j = 0;
+        for (; j + 4 <= m; j += 4) {
+          int c[4];
+          T a[4], v[4][VEC];
+#pragma unroll
+          for (int g = 0; g < 4; ++g) {
+            c[g] = __shfl_sync(mask, my_col, j + g, LPR);
+            a[g] = __shfl_sync(mask, my_val, j + g, LPR);
+          }
+#pragma unroll
+          for (int g = 0; g < 4; ++g)
+            if (live) load_vec<T, VEC>(X + (int64_t)c[g] * ldx + c0, v[g]);
+#pragma unroll
+          for (int g = 0; g < 4; ++g)
+#pragma unroll
+            for (int q = 0; q < VEC; ++q) acc[q] = axpy1(acc[q], a[g], v[g][q]);
+        }
+        for (; j < m; ++j) {
+          const int c = __shfl_sync(mask, my_col, j, LPR);
+          const T a = __shfl_sync(mask, my_val, j, LPR);
+          if (live) {
+            T v[VEC];
+            load_vec<T, VEC>(X + (int64_t)c * ldx + c0, v);
+#pragma unroll
+            for (int q = 0; q < VEC; ++q) acc[q] = axpy1(acc[q], a, v[q]);
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < VEC; ++q) tile[rr][sl * VEC + q] = acc[q];
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < 64 * PW; t += blockDim.x) {
+    const int c = t / 64, rr = t % 64;
+    const int64_t i = row0 + rr;
+    if (c < ncols && i < n_rows) Yt[(int64_t)c * ldy + i] = tile[rr][c];
   }
 }
 
@@ -220,6 +306,18 @@ int launch_spmm_T(fsr_ctx* ctx, int64_t n_rows, const int64_t* indptr, const int
   constexpr int VW = sizeof(T) == 4 ? 4 : 2;
   const bool vec_ok = ncols % VW == 0 && ldx % VW == 0 && aligned(X, 16);
   dim3 block(256);
+  if (vec_ok && ncols <= 8 * VW) {
+    dim3 grid((unsigned)ceil_div(n_rows, 64));
+    spmm_narrow_T_kernel<T, VW, 8><<<grid, block, 0, ctx->stream>>>(n_rows, indptr, indices, vals, ncols, X, ldx, Yt,
+                                                                     ldy);
+    return launched(ctx, "spmm_narrow_T_kernel");
+  }
+  if (vec_ok && ncols <= 16 * VW) {
+    dim3 grid((unsigned)ceil_div(n_rows, 64));
+    spmm_narrow_T_kernel<T, VW, 16><<<grid, block, 0, ctx->stream>>>(n_rows, indptr, indices, vals, ncols, X, ldx,
+                                                                      Yt, ldy);
+    return launched(ctx, "spmm_narrow_T_kernel");
+  }
   if (vec_ok && ncols > 32 * VW) {
     constexpr int NV = 2, PW = 32 * VW * NV;
     dim3 grid((unsigned)ceil_div(n_rows, 32), (unsigned)ceil_div(ncols, PW));

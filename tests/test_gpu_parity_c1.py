@@ -122,3 +122,23 @@ def test_single_query_filter_matches_batch(c1, decs):
             x = ranking.filter(d, h, batch.column(j))
             tol = 1e-12 if dtype == "float64" else 1e-5
             assert rel_l2(x, X[j]) <= tol
+
+
+@pytest.mark.parametrize("b", [2, 5, 17, 32, 33, 64, 65, 130])
+def test_batch_widths_agree_with_single_queries(c1, decs, b):
+    # every K9 code path (SpMV, narrow 8/16-lane, wide 1/2-vector panels) gives
+    # the same scores and top-100 as one-query-at-a-time filtering
+    g, A, batch, P = c1
+    dtype, dec, sdec = decs
+    h = ranking.h_alpha(float(g["alpha"]))
+    sub = ranking.QueryBatch(batch.size, batch.y_ptr[:b + 1], batch.y_idx[:batch.y_ptr[b]],
+                             batch.y_val[:batch.y_ptr[b]]) if b <= batch.b else None
+    if sub is None:
+        pytest.skip("not enough golden queries")
+    X = ranking.filter_batch(sdec, h, sub)
+    idx, _ = ranking.filter_batch(sdec, h, sub, topk=100)
+    tol = 1e-12 if dtype == "float64" else 1e-5
+    for j in range(b):
+        x = ranking.filter(sdec, h, sub.column(j))
+        assert rel_l2(X[j], x) <= tol
+        np.testing.assert_array_equal(idx[j], ranking.rank(X[j])[:100])
