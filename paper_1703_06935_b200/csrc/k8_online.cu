@@ -57,6 +57,81 @@ __global__ void __launch_bounds__(256) project_kernel(int64_t r, int64_t b, cons
   }
 }
 
+// Same result as project_kernel<T, true> (rows in query order, entries of a
+// row in parallel), but z lives in shared memory and every (col, val) entry of
+// the query's rows is prefetched into shared memory first, so the ordered
+// accumulation runs at smem latency instead of one HBM round trip per row.
+constexpr int kProjCap = 4096;     // prefetched entries
+constexpr int kProjMaxRows = 256;  // rows of U~ per query on this path
+
+template <typename T>
+__global__ void __launch_bounds__(256) project_smem_kernel(int64_t r, int64_t b, const int64_t* __restrict__ u_indptr,
+                                                           const int32_t* __restrict__ u_indices,
+                                                           const T* __restrict__ u_values, const T* __restrict__ w,
+                                                           const int64_t* __restrict__ y_ptr,
+                                                           const int64_t* __restrict__ y_idx,
+                                                           const T* __restrict__ y_val, T* __restrict__ Zt,
+                                                           T* __restrict__ Zs) {
+  extern __shared__ __align__(16) unsigned char dyn[];
+  T* z = (T*)dyn;
+  T* ev = (T*)(dyn + ((r * sizeof(T) + 15) / 16) * 16);
+  int32_t* ec = (int32_t*)(ev + kProjCap);
+  __shared__ int64_t offs[kProjMaxRows + 1];
+  __shared__ int64_t starts[kProjMaxRows];
+  const int64_t j = blockIdx.x;
+  const int64_t y0 = y_ptr[j], ny = y_ptr[j + 1] - y0;
+  for (int64_t c = threadIdx.x; c < r; c += blockDim.x) z[c] = T(0);
+  bool fits = ny <= kProjMaxRows;
+  if (fits) {
+    for (int64_t e = threadIdx.x; e < ny; e += blockDim.x) {
+      const int64_t i = y_idx[y0 + e];
+      starts[e] = u_indptr[i];
+      offs[e + 1] = u_indptr[i + 1] - u_indptr[i];
+    }
+    __syncthreads();
+    if (!threadIdx.x) {
+      offs[0] = 0;
+      for (int64_t e = 0; e < ny; ++e) offs[e + 1] += offs[e];
+    }
+    __syncthreads();
+    fits = offs[ny] <= kProjCap;
+  }
+  if (fits) {
+    for (int64_t e = 0; e < ny; ++e) {  // all loads issued back to back, no barrier between rows
+      const int64_t s0 = starts[e], o0 = offs[e], len = offs[e + 1] - o0;
+      for (int64_t t = threadIdx.x; t < len; t += blockDim.x) {
+        ec[o0 + t] = u_indices[s0 + t];
+        ev[o0 + t] = u_values[s0 + t];
+      }
+    }
+    __syncthreads();
+    for (int64_t e = 0; e < ny; ++e) {
+      const T v = y_val[y0 + e];
+      for (int64_t t = offs[e] + threadIdx.x; t < offs[e + 1]; t += blockDim.x) {
+        const int32_t c = ec[t];
+        z[c] = fsr::mul_add_rn(z[c], ev[t], v);
+      }
+      __syncthreads();
+    }
+  } else {
+    __syncthreads();
+    for (int64_t e = 0; e < ny; ++e) {
+      const int64_t i = y_idx[y0 + e];
+      const T v = y_val[y0 + e];
+      for (int64_t s = u_indptr[i] + threadIdx.x; s < u_indptr[i + 1]; s += blockDim.x) {
+        const int32_t c = u_indices[s];
+        z[c] = fsr::mul_add_rn(z[c], u_values[s], v);
+      }
+      __syncthreads();
+    }
+  }
+  for (int64_t c = threadIdx.x; c < r; c += blockDim.x) {
+    const T s = w[c] * z[c];
+    Zt[j * r + c] = s;
+    if (Zs) Zs[c * b + j] = s;
+  }
+}
+
 template <typename T>
 __global__ void transpose_kernel(int64_t rows, int64_t cols, const T* __restrict__ in, T* __restrict__ out) {
   // in: rows x cols row-major -> out: cols x rows row-major
@@ -105,7 +180,17 @@ int filter_impl(fsr_ctx* ctx, int64_t n, int64_t r, int u_sparse, const int64_t*
 
   {
   fsr::StageTimer timer(ctx, FSR_STAGE_PROJECT);
-  if (u_sparse)
+  const size_t psmem = ((size_t)r * sizeof(T) + 15) / 16 * 16 + (size_t)kProjCap * (sizeof(T) + 4);
+  if (u_sparse && psmem <= 160 * 1024) {
+    static size_t configured[2] = {0, 0};
+    if (configured[sizeof(T) == 8] < psmem) {
+      FSR_CUDA(ctx, cudaFuncSetAttribute(project_smem_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)psmem));
+      configured[sizeof(T) == 8] = psmem;
+    }
+    project_smem_kernel<T><<<(unsigned)b, 256, psmem, ctx->stream>>>(r, b, u_indptr, u_indices, u_values, w, y_ptr,
+                                                                     y_idx, y_val, Zt, Zs);
+  } else if (u_sparse)
     project_kernel<T, true><<<(unsigned)b, 256, 0, ctx->stream>>>(r, b, u_indptr, u_indices, u_values, nullptr, 0, w,
                                                                   y_ptr, y_idx, y_val, Zt, Zs);
   else

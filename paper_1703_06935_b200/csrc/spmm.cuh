@@ -197,29 +197,32 @@ __global__ void __launch_bounds__(256) spmv_kernel(int64_t n_rows, const int64_t
                                                    const int32_t* __restrict__ indices,
                                                    const T* __restrict__ vals, const T* __restrict__ x,
                                                    T* __restrict__ y, int64_t ldy) {
-  // 4 nonzeros per lane in flight (128 per warp iteration): the index/value
-  // streams are the HBM traffic, the gathers of x hit L1/L2.
-  const int lane = threadIdx.x & 31;
-  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < n_rows; i += nwarps) {
+  // Half-warp per row (two rows in flight per warp), 4 nonzeros per lane per
+  // iteration: the index/value streams are the HBM traffic, the gathers of x
+  // hit L1/L2; short load chains keep many rows in flight per SM.
+  const int lane = threadIdx.x & 31, half = lane >> 4, hl = lane & 15;
+  const int64_t nhalves = ((int64_t)gridDim.x * blockDim.x) >> 4;
+  for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 4; i - half < n_rows; i += nhalves) {
     T acc = T(0);
-    const int64_t e0 = __ldg(indptr + i), e1 = __ldg(indptr + i + 1);
-    for (int64_t base = e0 + lane; base < e1; base += 128) {
-      int c[4];
-      T a[4];
+    if (i < n_rows) {
+      const int64_t e0 = __ldg(indptr + i), e1 = __ldg(indptr + i + 1);
+      for (int64_t base = e0 + hl; base < e1; base += 64) {
+        int c[4];
+        T a[4];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int64_t e = base + 32 * u;
-        c[u] = e < e1 ? __ldg(indices + e) : -1;
-        a[u] = e < e1 ? __ldg(vals + e) : T(0);
+        for (int u = 0; u < 4; ++u) {
+          const int64_t e = base + 16 * u;
+          c[u] = e < e1 ? __ldg(indices + e) : -1;
+          a[u] = e < e1 ? __ldg(vals + e) : T(0);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (c[u] >= 0) acc = axpy1(acc, a[u], __ldg(x + c[u]));
       }
-#pragma unroll
-      for (int u = 0; u < 4; ++u)
-        if (c[u] >= 0) acc = axpy1(acc, a[u], __ldg(x + c[u]));
     }
 #pragma unroll
-    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    if (!lane) y[i * ldy] = acc;
+    for (int o = 8; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (!hl && i < n_rows) y[i * ldy] = acc;
   }
 }
 
