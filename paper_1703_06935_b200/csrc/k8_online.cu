@@ -202,7 +202,10 @@ int filter_impl(fsr_ctx* ctx, int64_t n, int64_t r, int u_sparse, const int64_t*
   if (u_sparse) {
     if (b == 1) {
       fsr::StageTimer timer(ctx, FSR_STAGE_FILTER_SPMM);
-      FSR_TRY(fsr::launch_spmm<T>(ctx, n, u_indptr, u_indices, u_values, 1, Zs, 1, Xout, 1));
+      if ((size_t)r * sizeof(T) <= 160 * 1024)
+        FSR_TRY(fsr::launch_spmv_smem<T>(ctx, n, u_indptr, u_indices, u_values, Zs, r, Xout));
+      else
+        FSR_TRY(fsr::launch_spmm<T>(ctx, n, u_indptr, u_indices, u_values, 1, Zs, 1, Xout, 1));
     } else {
       // K9 writes X (b x n) directly: smem-staged transposed tiles, no separate pass
       fsr::StageTimer timer(ctx, FSR_STAGE_FILTER_SPMM);

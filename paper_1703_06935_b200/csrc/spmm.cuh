@@ -12,6 +12,8 @@
 // sum are rounded separately, so the result is bitwise equal to scipy's.
 #pragma once
 
+#include <algorithm>
+
 #include "fsr_common.cuh"
 
 namespace fsr {
@@ -299,7 +301,59 @@ __global__ void __launch_bounds__(256) spmm_narrow_T_kernel(int64_t n_rows, cons
   }
 }
 
+// SpMV with the dense vector staged in shared memory: random 4-byte gathers
+// from L1 cost one wavefront per distinct 128B line (~32 per warp access);
+// from shared memory they cost a few bank cycles.  Warp per row, 4 nonzeros
+// per lane in flight.
+template <typename T>
+__global__ void __launch_bounds__(256) spmv_smem_kernel(int64_t n_rows, const int64_t* __restrict__ indptr,
+                                                        const int32_t* __restrict__ indices,
+                                                        const T* __restrict__ vals, const T* __restrict__ x,
+                                                        int64_t x_len, T* __restrict__ y) {
+  extern __shared__ __align__(16) unsigned char dyn[];
+  T* xs = (T*)dyn;
+  for (int64_t c = threadIdx.x; c < x_len; c += blockDim.x) xs[c] = x[c];
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < n_rows; i += nwarps) {
+    T acc = T(0);
+    const int64_t e0 = __ldg(indptr + i), e1 = __ldg(indptr + i + 1);
+    for (int64_t base = e0 + lane; base < e1; base += 128) {
+      int c[4];
+      T a[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int64_t e = base + 32 * u;
+        c[u] = e < e1 ? __ldg(indices + e) : -1;
+        a[u] = e < e1 ? __ldg(vals + e) : T(0);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (c[u] >= 0) acc = axpy1(acc, a[u], xs[c[u]]);
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (!lane) y[i] = acc;
+  }
+}
+
 inline bool aligned(const void* p, int bytes) { return ((uintptr_t)p % bytes) == 0; }
+
+template <typename T>
+int launch_spmv_smem(fsr_ctx* ctx, int64_t n_rows, const int64_t* indptr, const int32_t* indices, const T* vals,
+                     const T* x, int64_t x_len, T* y) {
+  const size_t smem = (size_t)x_len * sizeof(T);
+  static size_t configured[2] = {0, 0};
+  if (configured[sizeof(T) == 8] < smem) {
+    FSR_CUDA(ctx, cudaFuncSetAttribute(spmv_smem_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    configured[sizeof(T) == 8] = smem;
+  }
+  // enough resident blocks to cover the SMs several times; each re-stages x (L2 hits)
+  const int grid = (int)std::min<int64_t>(ceil_div(n_rows * 32, 256), (int64_t)ctx->num_sms * 4);
+  spmv_smem_kernel<T><<<grid, 256, smem, ctx->stream>>>(n_rows, indptr, indices, vals, x, x_len, y);
+  return launched(ctx, "spmv_smem_kernel");
+}
 
 // Y^T (ncols x n_rows, ld = ldy) = A X for ncols >= 2 (online K9 output layout).
 template <typename T>
