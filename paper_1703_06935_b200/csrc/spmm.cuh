@@ -228,9 +228,11 @@ __global__ void __launch_bounds__(256) spmv_kernel(int64_t n_rows, const int64_t
   }
 }
 
-// Narrow dense blocks (ncols <= 16 * VEC): LPR lanes per row, 32/LPR rows per
-// warp, each sub-group broadcasting its row's (col, val) chunk with a width-LPR
-// shuffle.  Output Y^T (ldy = n) via a padded shared tile, like the wide kernel.
+// Narrow dense blocks (ncols <= LPR * VEC): one warp per row (no divergence
+// across rows of different lengths); the warp's lanes form 32/LPR groups of
+// LPR column lanes, group g taking nonzeros g, g+G, g+2G, ... of the row; the
+// G partial rows are summed by shuffles at the end.  Output Y^T (ldy = n) via
+// a padded shared tile, like the wide kernel.
 template <typename T, int VEC, int LPR>
 __global__ void __launch_bounds__(256) spmm_narrow_T_kernel(int64_t n_rows, const int64_t* __restrict__ indptr,
                                                             const int32_t* __restrict__ indices,
@@ -238,60 +240,57 @@ __global__ void __launch_bounds__(256) spmm_narrow_T_kernel(int64_t n_rows, cons
                                                             const T* __restrict__ X, int64_t ldx,
                                                             T* __restrict__ Yt, int64_t ldy) {
   constexpr int PW = LPR * VEC;
-  constexpr int RPW = 32 / LPR;  // rows per warp pass
+  constexpr int G = 32 / LPR;  // nonzero groups per row
   __shared__ T tile[64][PW + 1];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int sub = lane / LPR, sl = lane % LPR;
-  const unsigned mask = LPR == 32 ? 0xffffffffu : (((1u << LPR) - 1u) << (sub * LPR));
+  const int grp = lane / LPR, sl = lane % LPR;
   const int64_t row0 = (int64_t)blockIdx.x * 64;
   const int64_t c0 = (int64_t)sl * VEC;
   const bool live = c0 < ncols;
-  for (int rr = warp * RPW + sub; rr < 64; rr += 8 * RPW) {
+  for (int rr = warp; rr < 64; rr += 8) {
     const int64_t i = row0 + rr;
     T acc[VEC];
 #pragma unroll
     for (int q = 0; q < VEC; ++q) acc[q] = T(0);
     if (i < n_rows) {
       const int64_t e0 = __ldg(indptr + i), e1 = __ldg(indptr + i + 1);
-      for (int64_t base = e0; base < e1; base += LPR) {
-        const int m = (e1 - base) < LPR ? (int)(e1 - base) : LPR;
+      for (int64_t base = e0; base < e1; base += 32) {
+        const int m = (e1 - base) < 32 ? (int)(e1 - base) : 32;
         int my_col = 0;
         T my_val = T(0);
-        if (sl < m) {
-          my_col = __ldg(indices + base + sl);
-          my_val = __ldg(vals + base + sl);
+        if (lane < m) {
+          my_col = __ldg(indices + base + lane);
+          my_val = __ldg(vals + base + lane);
         }
-        int j = 0;
-        for (; j + 4 <= m; j += 4) {
+        // group grp consumes chunk entries grp, grp+G, ... (4 in flight)
+        for (int j0 = 0; j0 < m; j0 += 4 * G) {
           int c[4];
           T a[4], v[4][VEC];
 #pragma unroll
-          for (int g = 0; g < 4; ++g) {
-            c[g] = __shfl_sync(mask, my_col, j + g, LPR);
-            a[g] = __shfl_sync(mask, my_val, j + g, LPR);
+          for (int u = 0; u < 4; ++u) {
+            const int j = j0 + u * G + grp;
+            c[u] = __shfl_sync(0xffffffffu, my_col, j & 31);
+            a[u] = __shfl_sync(0xffffffffu, my_val, j & 31);
+            if (j >= m) a[u] = T(0), c[u] = -1;
           }
 #pragma unroll
-          for (int g = 0; g < 4; ++g)
-            if (live) load_vec<T, VEC>(X + (int64_t)c[g] * ldx + c0, v[g]);
+          for (int u = 0; u < 4; ++u)
+            if (live && c[u] >= 0) load_vec<T, VEC>(X + (int64_t)c[u] * ldx + c0, v[u]);
 #pragma unroll
-          for (int g = 0; g < 4; ++g)
+          for (int u = 0; u < 4; ++u)
+            if (c[u] >= 0)
 #pragma unroll
-            for (int q = 0; q < VEC; ++q) acc[q] = axpy1(acc[q], a[g], v[g][q]);
-        }
-        for (; j < m; ++j) {
-          const int c = __shfl_sync(mask, my_col, j, LPR);
-          const T a = __shfl_sync(mask, my_val, j, LPR);
-          if (live) {
-            T v[VEC];
-            load_vec<T, VEC>(X + (int64_t)c * ldx + c0, v);
-#pragma unroll
-            for (int q = 0; q < VEC; ++q) acc[q] = axpy1(acc[q], a, v[q]);
-          }
+              for (int q = 0; q < VEC; ++q) acc[q] = axpy1(acc[q], a[u], v[u][q]);
         }
       }
     }
 #pragma unroll
-    for (int q = 0; q < VEC; ++q) tile[rr][sl * VEC + q] = acc[q];
+    for (int q = 0; q < VEC; ++q)
+#pragma unroll
+      for (int o = LPR; o < 32; o <<= 1) acc[q] += __shfl_xor_sync(0xffffffffu, acc[q], o);
+    if (grp == 0)
+#pragma unroll
+      for (int q = 0; q < VEC; ++q) tile[rr][sl * VEC + q] = acc[q];
   }
   __syncthreads();
   for (int t = threadIdx.x; t < 64 * PW; t += blockDim.x) {
@@ -349,8 +348,8 @@ int launch_spmv_smem(fsr_ctx* ctx, int64_t n_rows, const int64_t* indptr, const 
     FSR_CUDA(ctx, cudaFuncSetAttribute(spmv_smem_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     configured[sizeof(T) == 8] = smem;
   }
-  // enough resident blocks to cover the SMs several times; each re-stages x (L2 hits)
-  const int grid = (int)std::min<int64_t>(ceil_div(n_rows * 32, 256), (int64_t)ctx->num_sms * 4);
+  // full occupancy (8 blocks x 8 warps per SM); each block re-stages x (L2 hits)
+  const int grid = (int)std::min<int64_t>(ceil_div(n_rows * 32, 256), (int64_t)ctx->num_sms * 8);
   spmv_smem_kernel<T><<<grid, 256, smem, ctx->stream>>>(n_rows, indptr, indices, vals, x, x_len, y);
   return launched(ctx, "spmv_smem_kernel");
 }
