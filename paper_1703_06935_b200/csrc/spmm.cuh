@@ -233,7 +233,7 @@ __global__ void __launch_bounds__(256) spmv_kernel(int64_t n_rows, const int64_t
 // LPR column lanes, group g taking nonzeros g, g+G, g+2G, ... of the row; the
 // G partial rows are summed by shuffles at the end.  Output Y^T (ldy = n) via
 // a padded shared tile, like the wide kernel.
-template <typename T, int VEC, int LPR>
+template <typename T, int VEC, int LPR, bool TRANS = true>
 __global__ void __launch_bounds__(256) spmm_narrow_T_kernel(int64_t n_rows, const int64_t* __restrict__ indptr,
                                                             const int32_t* __restrict__ indices,
                                                             const T* __restrict__ vals, int64_t ncols,
@@ -245,7 +245,8 @@ __global__ void __launch_bounds__(256) spmm_narrow_T_kernel(int64_t n_rows, cons
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int grp = lane / LPR, sl = lane % LPR;
   const int64_t row0 = (int64_t)blockIdx.x * 64;
-  const int64_t c0 = (int64_t)sl * VEC;
+  const int64_t p0 = (int64_t)blockIdx.y * PW;  // column panel (row-major output mode)
+  const int64_t c0 = p0 + (int64_t)sl * VEC;
   const bool live = c0 < ncols;
   for (int rr = warp; rr < 64; rr += 8) {
     const int64_t i = row0 + rr;
@@ -288,10 +289,15 @@ __global__ void __launch_bounds__(256) spmm_narrow_T_kernel(int64_t n_rows, cons
     for (int q = 0; q < VEC; ++q)
 #pragma unroll
       for (int o = LPR; o < 32; o <<= 1) acc[q] += __shfl_xor_sync(0xffffffffu, acc[q], o);
-    if (grp == 0)
+    if (TRANS) {
+      if (grp == 0)
 #pragma unroll
-      for (int q = 0; q < VEC; ++q) tile[rr][sl * VEC + q] = acc[q];
+        for (int q = 0; q < VEC; ++q) tile[rr][sl * VEC + q] = acc[q];
+    } else if (grp == 0 && live && i < n_rows) {
+      store_vec<T, VEC>(Yt + i * ldy + c0, acc);  // row-major Y, this panel's columns
+    }
   }
+  if (!TRANS) return;
   __syncthreads();
   for (int t = threadIdx.x; t < 64 * PW; t += blockDim.x) {
     const int c = t / 64, rr = t % 64;
@@ -403,6 +409,26 @@ int launch_spmm(fsr_ctx* ctx, int64_t n_rows, const int64_t* indptr, const int32
   }
   constexpr int VW = sizeof(T) == 4 ? 4 : 2;  // 16-byte vectors
   const bool vec_ok = ncols % VW == 0 && ldx % VW == 0 && ldy % VW == 0 && aligned(X, 16) && aligned(Y, 16);
+  // Large dense blocks: the wide panel (256 fp32 / 128 fp64 columns of all n
+  // rows) would not stay L2-resident while every row gathers from it, so use
+  // narrow panels (16 or 32 columns, warp per row) whose n x panel slice fits L2;
+  // W is re-streamed once per panel instead.
+  const int64_t l2_budget = (int64_t)80 << 20;
+  if (vec_ok && n_rows * 64 * (int64_t)sizeof(T) > l2_budget && ncols >= 16) {
+    const int64_t rows_x = n_rows;  // X has as many rows as W has columns (square W)
+    if (rows_x * 32 * (int64_t)sizeof(T) <= l2_budget) {
+      constexpr int LPR = 32 / VW;  // 32-column panels
+      dim3 grid((unsigned)ceil_div(n_rows, 64), (unsigned)ceil_div(ncols, LPR * VW));
+      spmm_narrow_T_kernel<T, VW, LPR, false><<<grid, block, 0, ctx->stream>>>(n_rows, indptr, indices, vals, ncols, X,
+                                                                               ldx, Y, ldy);
+    } else {
+      constexpr int LPR = 16 / VW;  // 16-column panels
+      dim3 grid((unsigned)ceil_div(n_rows, 64), (unsigned)ceil_div(ncols, LPR * VW));
+      spmm_narrow_T_kernel<T, VW, LPR, false><<<grid, block, 0, ctx->stream>>>(n_rows, indptr, indices, vals, ncols, X,
+                                                                               ldx, Y, ldy);
+    }
+    return launched(ctx, "spmm_narrow_rowmajor_kernel");
+  }
   if (vec_ok) {
     constexpr int NV = 2;
     constexpr int PW = 32 * VW * NV;
