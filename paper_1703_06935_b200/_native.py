@@ -39,7 +39,7 @@ _SIGS = {
     "fsr_synchronize": (_c_int, [_c_p]),
     "fsr_ctx_enable_timing": (_c_int, [_c_p, _c_int]),
     "fsr_ctx_set_option": (_c_int, [_c_p, _c_int, _c_i64]),
-    "fsr_gram_tf32": (_c_int, [_c_p, _c_i64, _c_i64, _c_p, _c_i64, _c_p, _c_int, _c_int]),
+    "fsr_gram_levels": (_c_int, [_c_p, _c_i64, _c_i64, _c_p, _c_i64, _c_p, _c_int, _c_int]),
     "fsr_stage_time": (_c_int, [_c_p, _c_int, _c_dp, ctypes.POINTER(_c_u64)]),
     "fsr_stage_reset": (_c_int, [_c_p]),
     "fsr_gaussian_block": (_c_int, [_c_p, _c_int, _c_i64, _c_i64, _c_i64, _c_i64, _c_u64, _c_u64, _c_p]),

@@ -143,13 +143,17 @@ __global__ void slice_rows_kernel(int64_t rows, int64_t cols, const T* __restric
 }
 
 // ------------------------------------------------------------------ kernel --
-template <int N, int STAGES>
+// LEVELS = 3: the full 6-product scheme (21 bits); LEVELS = 1: only s1 s1'
+// (7-bit slices, one plane) -- enough for the first CholeskyQR pass, whose R
+// only needs to precondition (span(B R^-1) = span(B) for any R).
+template <int N, int STAGES, int LEVELS>
 struct OzCfg {
+  static constexpr int PLANES = LEVELS == 1 ? 1 : kSlices;
   static constexpr int A_PLANE = 128 * kBK;  // 128 rows x 128 K bytes
   static constexpr int B_PLANE = N * kBK;
-  static constexpr int STAGE_BYTES = kSlices * (A_PLANE + B_PLANE);
+  static constexpr int STAGE_BYTES = PLANES * (A_PLANE + B_PLANE);
   static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
-  static constexpr uint32_t TMEM_COLS = 3 * N <= 128 ? 128 : (3 * N <= 256 ? 256 : 512);
+  static constexpr uint32_t TMEM_COLS = LEVELS * N <= 128 ? 128 : (LEVELS * N <= 256 ? 256 : 512);
 };
 
 // kind::i8, signed x signed, s32 accumulate, both K-major
@@ -178,13 +182,13 @@ __device__ __forceinline__ void tmem_ld32_i(uint32_t taddr, int (&v)[32]) {
 //   rows = output rows i (ka of them), B rows = output cols j; result added to
 //   the fp64 partial P[split] (ka x kb).
 // MODE 1 (apply): D[r, j] = sum_K A[r, :] B[j, :] over the full K; fp32 out.
-template <int MODE, int N, int STAGES>
+template <int MODE, int N, int STAGES, int LEVELS>
 __global__ void __launch_bounds__(kThreads, 1)
     oz_gemm_kernel(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUtensorMap mB, int rowsA,
                    int rowsB, int64_t planeA_rows, int64_t planeB_rows, int64_t K, int tiles_n, int64_t k_per_split,
                    const int* __restrict__ eA, const int* __restrict__ eB, int symmetric, double* __restrict__ P,
                    float* __restrict__ Out, int64_t ldo) {
-  using Cfg = OzCfg<N, STAGES>;
+  using Cfg = OzCfg<N, STAGES, LEVELS>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint64_t* full = (uint64_t*)(smem + STAGES * Cfg::STAGE_BYTES);
@@ -227,9 +231,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_expect_tx(&full[s], Cfg::STAGE_BYTES);
         const int kk = (int)(kb0 + (int64_t)it * kBK);
 #pragma unroll
-        for (int p = 0; p < kSlices; ++p) {
+        for (int p = 0; p < Cfg::PLANES; ++p) {
           tma_load_2d(st + p * Cfg::A_PLANE, &mA, &full[s], kk, (int)(p * planeA_rows + i0));
-          tma_load_2d(st + kSlices * Cfg::A_PLANE + p * Cfg::B_PLANE, &mB, &full[s], kk,
+          tma_load_2d(st + Cfg::PLANES * Cfg::A_PLANE + p * Cfg::B_PLANE, &mB, &full[s], kk,
                       (int)(p * planeB_rows + j0));
         }
       }
@@ -243,22 +247,24 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_after();
       if (lane == 0) {
         const uint32_t base = smem_u32(smem + s * Cfg::STAGE_BYTES);
-        const uint32_t bbase = base + kSlices * Cfg::A_PLANE;
+        const uint32_t bbase = base + Cfg::PLANES * Cfg::A_PLANE;
 #pragma unroll
         for (int ks = 0; ks < kBK / 32; ++ks) {
-          uint64_t a[kSlices], b[kSlices];
+          uint64_t a[Cfg::PLANES], b[Cfg::PLANES];
 #pragma unroll
-          for (int p = 0; p < kSlices; ++p) {
+          for (int p = 0; p < Cfg::PLANES; ++p) {
             a[p] = smem_desc_sw128(base + p * Cfg::A_PLANE + ks * 32, 16, 1024);
             b[p] = smem_desc_sw128(bbase + p * Cfg::B_PLANE + ks * 32, 16, 1024);
           }
           const uint32_t acc = (it == 0 && ks == 0) ? 0u : 1u;
           mma_i8(tmem + 0 * N, a[0], b[0], idesc, acc);  // L0: s1 s1'
-          mma_i8(tmem + 1 * N, a[0], b[1], idesc, acc);  // L1: s1 s2'
-          mma_i8(tmem + 1 * N, a[1], b[0], idesc, 1u);   //     s2 s1'
-          mma_i8(tmem + 2 * N, a[1], b[1], idesc, acc);  // L2: s2 s2'
-          mma_i8(tmem + 2 * N, a[0], b[2], idesc, 1u);   //     s1 s3'
-          mma_i8(tmem + 2 * N, a[2], b[0], idesc, 1u);   //     s3 s1'
+          if (LEVELS == 3) {
+            mma_i8(tmem + 1 * N, a[0], b[1 % Cfg::PLANES], idesc, acc);  // L1: s1 s2'
+            mma_i8(tmem + 1 * N, a[1 % Cfg::PLANES], b[0], idesc, 1u);   //     s2 s1'
+            mma_i8(tmem + 2 * N, a[1 % Cfg::PLANES], b[1 % Cfg::PLANES], idesc, acc);  // L2: s2 s2'
+            mma_i8(tmem + 2 * N, a[0], b[2 % Cfg::PLANES], idesc, 1u);                 //     s1 s3'
+            mma_i8(tmem + 2 * N, a[2 % Cfg::PLANES], b[0], idesc, 1u);                 //     s3 s1'
+          }
         }
         mma_commit(&empty[s]);
         if (it == iters - 1) mma_commit(&tfull[0]);
@@ -280,8 +286,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       int l0[32], l1[32], l2[32];
       if (iters > 0) {
         tmem_ld32_i(tl + 0 * N + cc * 32, l0);
-        tmem_ld32_i(tl + 1 * N + cc * 32, l1);
-        tmem_ld32_i(tl + 2 * N + cc * 32, l2);
+        if (LEVELS == 3) {
+          tmem_ld32_i(tl + 1 * N + cc * 32, l1);
+          tmem_ld32_i(tl + 2 * N + cc * 32, l2);
+        } else {
+#pragma unroll
+          for (int t = 0; t < 32; ++t) l1[t] = l2[t] = 0;
+        }
       } else {
 #pragma unroll
         for (int t = 0; t < 32; ++t) l0[t] = l1[t] = l2[t] = 0;
@@ -378,18 +389,19 @@ int set_smem(fsr_ctx* ctx, K kernel, int bytes) {
 constexpr int kStages = 2;
 constexpr size_t kChunkBudget = (size_t)6 << 30;  // bytes of slice staging per row chunk
 
-template <int MODE>
+template <int MODE, int LEVELS = 3>
 int launch_oz(fsr_ctx* ctx, dim3 grid, const CUtensorMap& mA, const CUtensorMap& mB, int rowsA, int rowsB,
               int64_t pA, int64_t pB, int64_t K, int tiles_n, int64_t kps, const int* eA, const int* eB, int sym,
               double* P, float* Out, int64_t ldo) {
   constexpr int N = MODE == 0 ? kNG : kNA;
-  using Cfg = OzCfg<N, kStages>;
+  constexpr int STAGES = LEVELS == 1 ? 5 : kStages;
+  using Cfg = OzCfg<N, STAGES, LEVELS>;
   static bool attr = false;
   if (!attr) {
-    FSR_TRY(set_smem(ctx, oz_gemm_kernel<MODE, N, kStages>, Cfg::SMEM));
+    FSR_TRY(set_smem(ctx, oz_gemm_kernel<MODE, N, STAGES, LEVELS>, Cfg::SMEM));
     attr = true;
   }
-  oz_gemm_kernel<MODE, N, kStages><<<grid, kThreads, Cfg::SMEM, ctx->stream>>>(
+  oz_gemm_kernel<MODE, N, STAGES, LEVELS><<<grid, kThreads, Cfg::SMEM, ctx->stream>>>(
       mA, mB, rowsA, rowsB, pA, pB, K, tiles_n, kps, eA, eB, sym, P, Out, ldo);
   return fsr::launched(ctx, MODE == 0 ? "oz_gram_kernel" : "oz_apply_kernel");
 }
@@ -400,7 +412,7 @@ namespace fsr {
 
 // C (ka x kb, fp64 row-major) (+)= A^T B over n rows of fp32 row-major blocks.
 int tc_gram(fsr_ctx* ctx, int64_t n, int64_t ka, const float* A, int64_t lda, int64_t kb, const float* B,
-            int64_t ldb, double* C, int accumulate, int /*nprod*/, int symmetric) {
+            int64_t ldb, double* C, int accumulate, int levels, int symmetric) {
   const bool same = (A == B) && lda == ldb && ka == kb;
   symmetric = symmetric && same;
   const int64_t per_row = kSlices * (ka + (same ? 0 : kb));
@@ -448,8 +460,12 @@ int tc_gram(fsr_ctx* ctx, int64_t n, int64_t ka, const float* A, int64_t lda, in
     FSR_TRY(make_map_u8(ctx, &mB, sB, kSlices * kb, ldT, ldT, kNG));
     const int64_t kps = pad_to(ceil_div(ldT, splits), kBK);
     dim3 grid((unsigned)(tiles_m * tiles_n), (unsigned)ceil_div(ldT, kps));
-    FSR_TRY(launch_oz<0>(ctx, grid, mA, mB, (int)ka, (int)kb, ka, kb, ldT, tiles_n, kps, eA, eB, symmetric, P,
-                         nullptr, 0));
+    if (levels == 1)
+      FSR_TRY((launch_oz<0, 1>(ctx, grid, mA, mB, (int)ka, (int)kb, ka, kb, ldT, tiles_n, kps, eA, eB, symmetric,
+                               P, nullptr, 0)));
+    else
+      FSR_TRY((launch_oz<0, 3>(ctx, grid, mA, mB, (int)ka, (int)kb, ka, kb, ldT, tiles_n, kps, eA, eB, symmetric,
+                               P, nullptr, 0)));
     const int acc = (s0 > 0) || accumulate;
     gram_reduce_kernel<<<grid_for(ka * kb, 256, ctx, 8), 256, 0, ctx->stream>>>(
         (int)ka, (int)kb, (int)grid.y, P, C, acc, symmetric);

@@ -155,10 +155,13 @@ class CudaOps:
                       N.ptr(A_local.values), X_full.shape[1], N.ptr(X_full), X_full.stride(0), N.ptr(Y), Y.stride(0))
         return Y
 
-    def gram(self, Y):
+    def gram(self, Y, fast=False):
         k = Y.shape[1]
         G = self.torch.empty(k, k, dtype=self.torch.float64, device=self.device)
-        self.ctx.call("gram", self.dt, Y.shape[0], k, N.ptr(Y), Y.stride(0), N.ptr(G), 0)
+        if fast and self.dt == N.F32:  # first CholeskyQR pass: one-slice Gram (spectral._cholqr_pass)
+            self.ctx.call("gram_levels", Y.shape[0], k, N.ptr(Y), Y.stride(0), N.ptr(G), 0, 1)
+        else:
+            self.ctx.call("gram", self.dt, Y.shape[0], k, N.ptr(Y), Y.stride(0), N.ptr(G), 0)
         return G
 
     def max_dev(self, G) -> float:
@@ -246,8 +249,8 @@ def sharded_orthonormalize(comm: Comm, ops, Y, shard: Shard, dt_code: int, stats
     """CholeskyQR2 over row shards; Householder on the gathered block as fallback."""
     ok = True
     last_dev = np.inf
-    for _ in range(2):
-        G = comm.sum_ordered(ops.gram(Y))
+    for pass_ in range(2):
+        G = comm.sum_ordered(ops.gram(Y, fast=(pass_ == 0)))
         last_dev = ops.max_dev(G)
         R = ops.cholesky(G)
         if R is None:

@@ -37,7 +37,7 @@ ORTH_TOL = {N.F64: 1e-8, N.F32: 1e-4}
 # CholeskyQR2 is orthogonal to O(eps) when the second Gram is this close to I
 # (Yamamoto et al. 2015); beyond it an explicit check runs (spectral.py:167).
 CHOLQR2_SAFE = 0.1
-# first CholeskyQR pass of a float32 block with a 1xTF32 Gram (see _cholqr_pass)
+# first CholeskyQR pass of a float32 block with a one-slice Gram (see _cholqr_pass)
 FAST_FIRST_GRAM = True
 
 _MASK64 = (1 << 64) - 1
@@ -203,13 +203,14 @@ def _max_dev(ctx, G) -> float:
 def _cholqr_pass(ctx, dt, Y, G, gram_hook=None, fast_gram=False) -> tuple[bool, float]:
     """One CholeskyQR pass in place: Y <- Y R^-1.  Returns (ok, max|G - I|).
 
-    ``fast_gram`` (float32 blocks only): a single-TF32-product Gram.  The first
-    pass of CholeskyQR2 only needs R to be a decent preconditioner -- span(Y R^-1)
-    equals span(Y) whatever R is -- so its Gram can skip the 3xTF32 split.
+    ``fast_gram`` (float32 blocks only): a one-slice (7-bit) int8 Gram.  The
+    first pass of CholeskyQR2 only needs R to be a decent preconditioner --
+    span(Y R^-1) equals span(Y) whatever R is -- so its Gram can skip the
+    full 6-product Ozaki scheme.
     """
     if fast_gram and dt == N.F32:
         n, k = Y.shape
-        ctx.call("gram_tf32", n, k, N.ptr(Y), Y.stride(0), N.ptr(G), 0, 1)
+        ctx.call("gram_levels", n, k, N.ptr(Y), Y.stride(0), N.ptr(G), 0, 1)
     else:
         _gram(ctx, dt, Y, G)
     if gram_hook is not None:

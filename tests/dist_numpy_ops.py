@@ -28,7 +28,7 @@ class NumpyOps:
     def spmm(self, A_local, X_full):
         return _t(A_local @ _np(X_full))
 
-    def gram(self, Y):
+    def gram(self, Y, fast=False):
         y = _np(Y)
         return _t(y.T @ y)
 

@@ -63,9 +63,9 @@ def test_gram_fast(n, k):
     A = rng.standard_normal((n, k)).astype(np.float32)
     Ad = torch.as_tensor(A).cuda()
     G = torch.empty(k, k, dtype=torch.float64, device="cuda")
-    ctx.call("gram_tf32", n, k, N.ptr(Ad), k, N.ptr(G), 0, 1)
+    ctx.call("gram_levels", n, k, N.ptr(Ad), k, N.ptr(G), 0, 1)
     ref = A.astype(np.float64).T @ A.astype(np.float64)
-    assert rel(G.cpu().numpy(), ref) < 2e-3
+    assert rel(G.cpu().numpy(), ref) < 5e-2  # one 7-bit slice: a preconditioner, not a Gram
 
 
 @pytest.mark.parametrize("n,k", SHAPES)
