@@ -13,6 +13,7 @@
 #pragma once
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "fsr_common.cuh"
 
@@ -413,24 +414,28 @@ int launch_spmm(fsr_ctx* ctx, int64_t n_rows, const int64_t* indptr, const int32
   // rows) would not stay L2-resident while every row gathers from it, so use
   // narrow panels (16 or 32 columns, warp per row) whose n x panel slice fits L2;
   // W is re-streamed once per panel instead.
-  // Measured on B200 at C3 (n = 1e6, r_hat = 5500): 241 ms per SpMM vs 107 ms
-  // for the wide kernel (which streams its gathers at ~6.5 TB/s of DRAM), so the
-  // narrow-panel path is kept only behind kUseNarrowPanels for experiments.
-  constexpr bool kUseNarrowPanels = false;
-  const int64_t l2_budget = (int64_t)80 << 20;
-  if (kUseNarrowPanels && vec_ok && n_rows * 64 * (int64_t)sizeof(T) > l2_budget && ncols >= 16) {
-    const int64_t rows_x = n_rows;  // X has as many rows as W has columns (square W)
-    if (rows_x * 32 * (int64_t)sizeof(T) <= l2_budget) {
-      constexpr int LPR = 32 / VW;  // 32-column panels
-      dim3 grid((unsigned)ceil_div(n_rows, 64), (unsigned)ceil_div(ncols, LPR * VW));
-      spmm_narrow_T_kernel<T, VW, LPR, false><<<grid, block, 0, ctx->stream>>>(n_rows, indptr, indices, vals, ncols, X,
-                                                                               ldx, Y, ldy);
-    } else {
-      constexpr int LPR = 16 / VW;  // 16-column panels
-      dim3 grid((unsigned)ceil_div(n_rows, 64), (unsigned)ceil_div(ncols, LPR * VW));
-      spmm_narrow_T_kernel<T, VW, LPR, false><<<grid, block, 0, ctx->stream>>>(n_rows, indptr, indices, vals, ncols, X,
-                                                                               ldx, Y, ldy);
-    }
+  // Narrow row-major panels (warp per row, nonzero groups): an experiment knob
+  // (FSR_K2_PANEL = 16 | 32 | 64 | 128 columns).  Measured on B200 at C3
+  // (n = 1e6, r_hat = 5500): 16/32-column panels 241 ms vs 107 ms for the wide
+  // kernel, which streams its gathers at ~6.5 TB/s of DRAM; the default stays wide.
+  static const int k2_panel = [] {
+    const char* e = getenv("FSR_K2_PANEL");
+    return e ? atoi(e) : 0;
+  }();
+  if (k2_panel > 0 && vec_ok && ncols >= 16) {
+    dim3 grid((unsigned)ceil_div(n_rows, 64), (unsigned)ceil_div(ncols, k2_panel));
+    if (k2_panel == 16)
+      spmm_narrow_T_kernel<T, VW, 16 / VW, false><<<grid, block, 0, ctx->stream>>>(n_rows, indptr, indices, vals, ncols,
+                                                                                   X, ldx, Y, ldy);
+    else if (k2_panel == 32)
+      spmm_narrow_T_kernel<T, VW, 32 / VW, false><<<grid, block, 0, ctx->stream>>>(n_rows, indptr, indices, vals, ncols,
+                                                                                   X, ldx, Y, ldy);
+    else if (k2_panel == 64 && VW == 4)
+      spmm_narrow_T_kernel<T, 4, 16, false><<<grid, block, 0, ctx->stream>>>(n_rows, indptr, indices, vals, ncols, X,
+                                                                             ldx, Y, ldy);
+    else
+      spmm_narrow_T_kernel<T, VW, 32, false><<<dim3(grid.x, (unsigned)ceil_div(ncols, 32 * VW)), block, 0,
+                                                ctx->stream>>>(n_rows, indptr, indices, vals, ncols, X, ldx, Y, ldy);
     return launched(ctx, "spmm_narrow_rowmajor_kernel");
   }
   if (vec_ok) {
