@@ -430,9 +430,9 @@ int launch_spmm(fsr_ctx* ctx, int64_t n_rows, const int64_t* indptr, const int32
     else if (k2_panel == 32)
       spmm_narrow_T_kernel<T, VW, 32 / VW, false><<<grid, block, 0, ctx->stream>>>(n_rows, indptr, indices, vals, ncols,
                                                                                    X, ldx, Y, ldy);
-    else if (k2_panel == 64 && VW == 4)
-      spmm_narrow_T_kernel<T, 4, 16, false><<<grid, block, 0, ctx->stream>>>(n_rows, indptr, indices, vals, ncols, X,
-                                                                             ldx, Y, ldy);
+    else if (k2_panel == 64)
+      spmm_narrow_T_kernel<T, VW, 64 / VW, false><<<grid, block, 0, ctx->stream>>>(n_rows, indptr, indices, vals, ncols,
+                                                                                   X, ldx, Y, ldy);
     else
       spmm_narrow_T_kernel<T, VW, 32, false><<<dim3(grid.x, (unsigned)ceil_div(ncols, 32 * VW)), block, 0,
                                                 ctx->stream>>>(n_rows, indptr, indices, vals, ncols, X, ldx, Y, ldy);
