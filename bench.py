@@ -319,7 +319,8 @@ def max_over_ranks(x, world):
     import torch
     import torch.distributed as dist
 
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dev = "cpu" if dist.get_backend() == "gloo" else "cuda"
+    t = torch.tensor([x], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -533,7 +534,9 @@ def main():
         import torch.distributed as dist
 
         torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl")
+        # FSR_DIST_BACKEND=gloo runs the multi-rank path with host-staged
+        # collectives (e.g. two ranks sharing one GPU for a functional check)
+        dist.init_process_group(os.environ.get("FSR_DIST_BACKEND", "nccl"))
     try:
         run_fsr(args, cfg, n, rank, world, local_rank)
     finally:
