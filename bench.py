@@ -533,6 +533,8 @@ def main():
         import torch
         import torch.distributed as dist
 
+        if os.environ.get("FSR_DIST_BACKEND") == "gloo":
+            local_rank %= max(1, torch.cuda.device_count())  # functional check: ranks may share a GPU
         torch.cuda.set_device(local_rank)
         # FSR_DIST_BACKEND=gloo runs the multi-rank path with host-staged
         # collectives (e.g. two ranks sharing one GPU for a functional check)
