@@ -101,6 +101,78 @@ __device__ __forceinline__ void slice3(double x, int e, int8_t& s1, int8_t& s2, 
   s3 = (int8_t)c;
 }
 
+__device__ __forceinline__ uint32_t pack4(int8_t a, int8_t b, int8_t c, int8_t d) {
+  return (uint32_t)(uint8_t)a | ((uint32_t)(uint8_t)b << 8) | ((uint32_t)(uint8_t)c << 16) | ((uint32_t)(uint8_t)d << 24);
+}
+
+// Gram operand, HBM-friendly: a 128-row x 32-column tile is read coalesced,
+// transposed through shared memory, and every thread emits 16 consecutive
+// rows of one column as one 16-byte store per slice plane.  Requires
+// ld_out % 16 == 0 (rows beyond `rows` are written as zero slices).
+__global__ void __launch_bounds__(256) slice_T_packed_kernel(int64_t rows, int64_t cols, const float* __restrict__ in,
+                                                             int64_t ld_in, const int* __restrict__ ecol,
+                                                             int8_t* __restrict__ S, int64_t ld_out) {
+  __shared__ float tile[32][129];
+  const int64_t r0 = (int64_t)blockIdx.x * 128, c0 = (int64_t)blockIdx.y * 32;
+#pragma unroll 4
+  for (int k = 0; k < 16; ++k) {
+    const int idx = threadIdx.x + k * 256;
+    const int r = idx >> 5, c = idx & 31;
+    const int64_t gr = r0 + r, gc = c0 + c;
+    tile[c][r] = (gr < rows && gc < cols) ? __ldg(in + gr * ld_in + gc) : 0.f;
+  }
+  __syncthreads();
+  const int c = threadIdx.x >> 3, g = threadIdx.x & 7;
+  const int64_t gc = c0 + c;
+  const int64_t gr = r0 + 16 * g;
+  if (gc >= cols || gr >= ld_out) return;
+  const int e = ecol[gc] - 2048;
+  uint32_t w[3][4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    int8_t s[3][4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) slice3((double)tile[c][16 * g + 4 * q + u], e, s[0][u], s[1][u], s[2][u]);
+#pragma unroll
+    for (int p = 0; p < 3; ++p) w[p][q] = pack4(s[p][0], s[p][1], s[p][2], s[p][3]);
+  }
+  const int64_t plane = cols * ld_out;
+#pragma unroll
+  for (int p = 0; p < 3; ++p)
+    *reinterpret_cast<uint4*>(S + p * plane + gc * ld_out + gr) = make_uint4(w[p][0], w[p][1], w[p][2], w[p][3]);
+}
+
+// Apply operand, fused: warp per row, pass 1 finds the row exponent, pass 2
+// (row still in L1/L2) slices four values per lane into packed 4-byte stores.
+// Requires ld_out % 4 == 0; columns in [cols, ld_out) are zero slices.
+__global__ void __launch_bounds__(256) slice_rows_fused_kernel(int64_t rows, int64_t cols, const float* __restrict__ in,
+                                                               int64_t ld_in, int* __restrict__ erow,
+                                                               int8_t* __restrict__ S, int64_t ld_out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t plane = rows * ld_out;
+  for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < rows; r += nwarps) {
+    const float* row = in + r * ld_in;
+    float m = 0.f;
+    for (int64_t c = lane; c < cols; c += 32) m = fmaxf(m, fabsf(row[c]));
+#pragma unroll
+    for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    const int e = exp_above((double)m);
+    if (!lane) erow[r] = e + 2048;
+    for (int64_t c = 4 * lane; c < ld_out; c += 128) {
+      int8_t s[3][4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const float x = (c + u < cols) ? row[c + u] : 0.f;
+        slice3((double)x, e, s[0][u], s[1][u], s[2][u]);
+      }
+#pragma unroll
+      for (int p = 0; p < 3; ++p)
+        *reinterpret_cast<uint32_t*>(S + p * plane + r * ld_out + c) = pack4(s[p][0], s[p][1], s[p][2], s[p][3]);
+    }
+  }
+}
+
 // Gram operand: transpose + slice.  in: rows x cols (row-major, ld_in) ->
 // plane p (p = 0..2): cols x ld_out int8 with the rows (reduction index) contiguous.
 __global__ void slice_T_kernel(int64_t rows, int64_t cols, const float* __restrict__ in, int64_t ld_in,
@@ -443,17 +515,17 @@ int tc_gram(fsr_ctx* ctx, int64_t n, int64_t ka, const float* A, int64_t lda, in
       dim3 g((unsigned)ceil_div(ka, 32), (unsigned)std::min<int64_t>(ceil_div(rows, 8), 256)), b(32, 8);
       exp_of_cols_kernel<float><<<g, b, 0, ctx->stream>>>(rows, ka, A + s0 * lda, lda, eA);
       FSR_TRY(launched(ctx, "exp_of_cols_kernel"));
-      dim3 gs((unsigned)ceil_div(ldT, 32), (unsigned)ceil_div(ka, 32)), bs(32, 8);
-      slice_T_kernel<<<gs, bs, 0, ctx->stream>>>(rows, ka, A + s0 * lda, lda, eA, sA, ldT);
-      FSR_TRY(launched(ctx, "slice_T_kernel"));
+      dim3 gs((unsigned)ceil_div(ldT, 128), (unsigned)ceil_div(ka, 32));
+      slice_T_packed_kernel<<<gs, 256, 0, ctx->stream>>>(rows, ka, A + s0 * lda, lda, eA, sA, ldT);
+      FSR_TRY(launched(ctx, "slice_T_packed_kernel"));
     }
     if (!same) {
       dim3 g((unsigned)ceil_div(kb, 32), (unsigned)std::min<int64_t>(ceil_div(rows, 8), 256)), b(32, 8);
       exp_of_cols_kernel<float><<<g, b, 0, ctx->stream>>>(rows, kb, B + s0 * ldb, ldb, eB);
       FSR_TRY(launched(ctx, "exp_of_cols_kernel"));
-      dim3 gs((unsigned)ceil_div(ldT, 32), (unsigned)ceil_div(kb, 32)), bs(32, 8);
-      slice_T_kernel<<<gs, bs, 0, ctx->stream>>>(rows, kb, B + s0 * ldb, ldb, eB, sB, ldT);
-      FSR_TRY(launched(ctx, "slice_T_kernel"));
+      dim3 gs((unsigned)ceil_div(ldT, 128), (unsigned)ceil_div(kb, 32));
+      slice_T_packed_kernel<<<gs, 256, 0, ctx->stream>>>(rows, kb, B + s0 * ldb, ldb, eB, sB, ldT);
+      FSR_TRY(launched(ctx, "slice_T_packed_kernel"));
     }
     CUtensorMap mA, mB;
     FSR_TRY(make_map_u8(ctx, &mA, sA, kSlices * ka, ldT, ldT, 128));
@@ -501,12 +573,9 @@ int tc_apply(fsr_ctx* ctx, int64_t n, int64_t K, const float* A, int64_t lda, in
   const int tiles_n = (int)ceil_div(N2, kNA);
   for (int64_t s0 = 0; s0 < n; s0 += chunk) {
     const int64_t rows = std::min(chunk, n - s0);
-    exp_of_rows_kernel<float><<<grid_for(rows * 32, 256, ctx, 8), 256, 0, ctx->stream>>>(rows, K, A + s0 * lda, lda, 0,
-                                                                                         eR);
-    FSR_TRY(launched(ctx, "exp_of_rows_kernel"));
-    slice_rows_kernel<float><<<grid_for(rows * pk, 256, ctx, 16), 256, 0, ctx->stream>>>(rows, K, A + s0 * lda, lda,
-                                                                                         0, eR, sR, pk);
-    FSR_TRY(launched(ctx, "slice_rows_kernel"));
+    slice_rows_fused_kernel<<<grid_for(rows * 32, 256, ctx, 8), 256, 0, ctx->stream>>>(rows, K, A + s0 * lda, lda, eR,
+                                                                                       sR, pk);
+    FSR_TRY(launched(ctx, "slice_rows_fused_kernel"));
     CUtensorMap mA;
     FSR_TRY(make_map_u8(ctx, &mA, sR, kSlices * rows, pk, pk, 128));
     dim3 grid((unsigned)(ceil_div(rows, 128) * tiles_n), 1);
