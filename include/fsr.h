@@ -117,8 +117,8 @@ int fsr_csr_spmm(fsr_ctx* ctx, int dtype, int64_t n_rows, const int64_t* indptr,
  * (accumulate != 0: G += A^T A). */
 int fsr_gram(fsr_ctx* ctx, int dtype, int64_t n_rows, int64_t k, const void* A, int64_t lda,
              double* G, int accumulate);
-/* F32 only: G (+)= A^T A on the tcgen05 int8 path with `levels` = 3 (three
- * 7-bit slices, 6 slice products: ~21-bit accurate, the default of fsr_gram)
+/* F32 only: G (+)= A^T A on the tcgen05 int8 path with `levels` = 4 (four
+ * 7-bit slices, 10 slice products: ~28-bit accurate, the default of fsr_gram)
  * or 1 (one slice, 1 product: ~7 bits -- enough for the first CholeskyQR pass,
  * whose R only needs to precondition; span(B R^-1) = span(B) for any R). */
 int fsr_gram_levels(fsr_ctx* ctx, int64_t n_rows, int64_t k, const float* A, int64_t lda, double* G,

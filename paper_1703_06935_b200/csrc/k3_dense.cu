@@ -190,7 +190,7 @@ int cross_impl(fsr_ctx* ctx, int dtype, int64_t n_rows, int64_t k, const void* A
     return dgemm_nt_accum(ctx, k, n_rows, (const double*)A, lda, (const double*)B, ldb, C, accumulate ? 1.0 : 0.0);
   const bool same = A == B && lda == ldb;
   if (ctx->dense_path == 0)
-    return fsr::tc_gram(ctx, n_rows, k, (const float*)A, lda, k, (const float*)B, ldb, C, accumulate, 3, same);
+    return fsr::tc_gram(ctx, n_rows, k, (const float*)A, lda, k, (const float*)B, ldb, C, accumulate, 4, same);
   const int64_t m = chunk_rows(n_rows, k, same ? 1 : 2);
   void* buf = nullptr;
   FSR_TRY(fsr::scratch(ctx, (size_t)m * k * 8 * (same ? 1 : 2), &buf));
@@ -222,7 +222,7 @@ int fsr_cross(fsr_ctx* ctx, int dtype, int64_t n_rows, int64_t k, const void* Q,
 
 int fsr_gram_levels(fsr_ctx* ctx, int64_t n_rows, int64_t k, const float* A, int64_t lda, double* G, int accumulate,
                     int levels) {
-  FSR_REQUIRE(ctx, n_rows >= 0 && k >= 1 && lda >= k && (levels == 1 || levels == 3), "gram_levels: bad args");
+  FSR_REQUIRE(ctx, n_rows >= 0 && k >= 1 && lda >= k && (levels == 1 || levels == 4), "gram_levels: bad args");
   fsr::StageTimer timer(ctx, FSR_STAGE_GRAM);
   if (n_rows == 0) {
     if (!accumulate) FSR_CUDA(ctx, cudaMemsetAsync(G, 0, k * k * 8, ctx->stream));

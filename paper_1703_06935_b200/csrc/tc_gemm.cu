@@ -12,23 +12,27 @@
 // in K; tools/tc_debug.cu), so a 1e6-row Gram cannot reach fp32 accuracy with
 // fp32 accumulation.  Integer accumulation is exact.
 //
-// Scheme: for a reduction over index r, every value x of operand X gets an
-// exponent e shared along r (per column of a Gram operand, per row of the
-// big apply operand, per column of the small matrix) with |x| < 2^e, and is
-// written as x = 2^(e-6) (s1 + s2/2^7 + s3/2^14 + eps), s_t = rint slices in
-// [-64, 64] (int8), |eps| <= 2^-15: 21 bits of fixed point below 2^e, rounding
-// unbiased.  A product keeps the 6 slice pairs with t+u <= 4, accumulated in
-// three int32 TMEM accumulators by level (L0 = s1s1', L1 = s1s2'+s2s1',
-// L2 = s2s2'+s1s3'+s3s1'); |term| <= 2^12, so int32 is exact for K < 174k.
-// The epilogue forms 2^(e+e'-12) (L0 + L1/2^7 + L2/2^14) in fp64.
+// Scheme: for a reduction over index r, every value x of an operand gets an
+// exponent e shared along r (per column of a Gram operand, per row of the big
+// apply operand, per column of the small matrix) with |x| < 2^e, and is written
+// as x = 2^(e-6) (s1 + s2/2^7 + s3/2^14 + s4/2^21 + eps), s_t = rint slices in
+// [-64, 64] (int8), |eps| <= 2^-22: 28 bits of fixed point below 2^e, rounding
+// unbiased.  A product keeps the 10 slice pairs with level t+u <= 3 (0-based),
+// each level summed in its own int32 TMEM accumulator (|term| <= 2^12 and at
+// most 4 terms per level, so int32 is exact for K <= 2^17); the epilogue forms
+// 2^(e+e'-12) sum_l L_l / 2^(7 l) in fp64.  21 bits (3 slices) were measured
+// NOT to be fp32-accurate on incoherent sums (C1 ranking vectors ~1e-4 vs
+// 9e-7 for cuBLAS fp32; tools/precision_probe.py).
+// LEVELS = 1 (one 7-bit slice, one product) serves the first CholeskyQR pass,
+// whose R only preconditions (span(B R^-1) = span(B) for any R).
 //
 // Kernel (one CTA per SM, 192 threads: warp 0 = TMA producer, warp 1 = MMA
 // issuer + TMEM owner, warps 2-5 = epilogue): D[128 x N] over a K range, both
-// operands K-major int8 slice planes staged by TMA (SWIZZLE_128B, 128 bytes of
-// K per row per stage) through an mbarrier ring; tcgen05.commit frees stages
-// and hands the accumulators to the epilogue.  Gram mode writes a per-split
-// fp64 partial (reduced later in fixed order: deterministic); apply mode
-// writes fp32 output rows.
+// operands K-major int8 slice planes staged by TMA (SWIZZLE_64B, 64 bytes of K
+// per row per stage) through an mbarrier ring; tcgen05.commit frees stages and
+// hands the accumulators to the epilogue.  Gram mode writes a per-split fp64
+// partial (reduced later in fixed order: deterministic); apply mode writes
+// fp32 output rows.
 #include <cuda.h>
 
 #include <algorithm>
@@ -42,15 +46,13 @@ namespace {
 using namespace fsr::tc;
 
 constexpr int kThreads = 192;
-constexpr int kBK = 128;      // K bytes (int8 elements) per stage = one 128B swizzle atom
-constexpr int kSlices = 3;
-constexpr int kNG = 160;      // N tile of the Gram kernel (3 x 160 TMEM columns)
-constexpr int kNA = 160;      // N tile of the apply kernel
-constexpr int64_t kMaxK = 131072;  // int32-exact reduction length per launch (bound 174k)
+constexpr int kBK = 64;            // K bytes (int8 elements) per stage = one 64B swizzle atom
+constexpr int kSlices = 4;         // slice planes produced
+constexpr int64_t kMaxK = 65536;   // reduction length per launch (int32-exact bound: 131072)
 
 // --------------------------------------------------------------- exponents --
 __device__ __forceinline__ int exp_above(double m) {
-  // smallest e with m < 2^e (m >= 0); zero columns get 0
+  // smallest e with m < 2^e (m >= 0); zero vectors get 0
   if (!(m > 0.0)) return 0;
   int e;
   frexp(m, &e);  // m = f 2^e, f in [0.5, 1)
@@ -89,26 +91,26 @@ __global__ void exp_of_rows_kernel(int64_t rows, int64_t cols, const T* __restri
   }
 }
 
-__device__ __forceinline__ void slice3(double x, int e, int8_t& s1, int8_t& s2, int8_t& s3) {
+__device__ __forceinline__ void slice4(double x, int e, int8_t (&s)[kSlices]) {
   double y = ldexp(x, 6 - e);  // |y| < 64
-  const double a = rint(y);
-  y = (y - a) * 128.0;
-  const double b = rint(y);
-  y = (y - b) * 128.0;
-  const double c = rint(y);
-  s1 = (int8_t)a;
-  s2 = (int8_t)b;
-  s3 = (int8_t)c;
+#pragma unroll
+  for (int t = 0; t < kSlices; ++t) {
+    const double a = rint(y);
+    s[t] = (int8_t)a;
+    y = (y - a) * 128.0;
+  }
 }
 
 __device__ __forceinline__ uint32_t pack4(int8_t a, int8_t b, int8_t c, int8_t d) {
-  return (uint32_t)(uint8_t)a | ((uint32_t)(uint8_t)b << 8) | ((uint32_t)(uint8_t)c << 16) | ((uint32_t)(uint8_t)d << 24);
+  return (uint32_t)(uint8_t)a | ((uint32_t)(uint8_t)b << 8) | ((uint32_t)(uint8_t)c << 16) |
+         ((uint32_t)(uint8_t)d << 24);
 }
 
-// Gram operand, HBM-friendly: a 128-row x 32-column tile is read coalesced,
-// transposed through shared memory, and every thread emits 16 consecutive
-// rows of one column as one 16-byte store per slice plane.  Requires
-// ld_out % 16 == 0 (rows beyond `rows` are written as zero slices).
+// Gram operand: a 128-row x 32-column tile is read coalesced, transposed
+// through shared memory, and every thread emits 16 consecutive rows of one
+// column as one 16-byte store per slice plane.  Output plane p: cols x ld_out
+// int8, the rows (reduction index) contiguous (K-major for the MMA).
+// Requires ld_out % 16 == 0; rows beyond `rows` become zero slices.
 __global__ void __launch_bounds__(256) slice_T_packed_kernel(int64_t rows, int64_t cols, const float* __restrict__ in,
                                                              int64_t ld_in, const int* __restrict__ ecol,
                                                              int8_t* __restrict__ S, int64_t ld_out) {
@@ -127,18 +129,18 @@ __global__ void __launch_bounds__(256) slice_T_packed_kernel(int64_t rows, int64
   const int64_t gr = r0 + 16 * g;
   if (gc >= cols || gr >= ld_out) return;
   const int e = ecol[gc] - 2048;
-  uint32_t w[3][4];
+  uint32_t w[kSlices][4];
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
-    int8_t s[3][4];
+    int8_t s[4][kSlices];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) slice3((double)tile[c][16 * g + 4 * q + u], e, s[0][u], s[1][u], s[2][u]);
+    for (int u = 0; u < 4; ++u) slice4((double)tile[c][16 * g + 4 * q + u], e, s[u]);
 #pragma unroll
-    for (int p = 0; p < 3; ++p) w[p][q] = pack4(s[p][0], s[p][1], s[p][2], s[p][3]);
+    for (int p = 0; p < kSlices; ++p) w[p][q] = pack4(s[0][p], s[1][p], s[2][p], s[3][p]);
   }
   const int64_t plane = cols * ld_out;
 #pragma unroll
-  for (int p = 0; p < 3; ++p)
+  for (int p = 0; p < kSlices; ++p)
     *reinterpret_cast<uint4*>(S + p * plane + gc * ld_out + gr) = make_uint4(w[p][0], w[p][1], w[p][2], w[p][3]);
 }
 
@@ -160,45 +162,18 @@ __global__ void __launch_bounds__(256) slice_rows_fused_kernel(int64_t rows, int
     const int e = exp_above((double)m);
     if (!lane) erow[r] = e + 2048;
     for (int64_t c = 4 * lane; c < ld_out; c += 128) {
-      int8_t s[3][4];
+      int8_t s[4][kSlices];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const float x = (c + u < cols) ? row[c + u] : 0.f;
-        slice3((double)x, e, s[0][u], s[1][u], s[2][u]);
-      }
+      for (int u = 0; u < 4; ++u) slice4((double)((c + u < cols) ? row[c + u] : 0.f), e, s[u]);
 #pragma unroll
-      for (int p = 0; p < 3; ++p)
-        *reinterpret_cast<uint32_t*>(S + p * plane + r * ld_out + c) = pack4(s[p][0], s[p][1], s[p][2], s[p][3]);
+      for (int p = 0; p < kSlices; ++p)
+        *reinterpret_cast<uint32_t*>(S + p * plane + r * ld_out + c) = pack4(s[0][p], s[1][p], s[2][p], s[3][p]);
     }
   }
 }
 
-// Gram operand: transpose + slice.  in: rows x cols (row-major, ld_in) ->
-// plane p (p = 0..2): cols x ld_out int8 with the rows (reduction index) contiguous.
-__global__ void slice_T_kernel(int64_t rows, int64_t cols, const float* __restrict__ in, int64_t ld_in,
-                               const int* __restrict__ ecol, int8_t* __restrict__ S, int64_t ld_out) {
-  __shared__ float tile[32][33];
-  const int64_t r0 = (int64_t)blockIdx.x * 32, c0 = (int64_t)blockIdx.y * 32;
-  for (int k = threadIdx.y; k < 32; k += 8) {
-    const int64_t r = r0 + k, c = c0 + threadIdx.x;
-    tile[k][threadIdx.x] = (r < rows && c < cols) ? in[r * ld_in + c] : 0.f;
-  }
-  __syncthreads();
-  const int64_t plane = cols * ld_out;
-  for (int k = threadIdx.y; k < 32; k += 8) {
-    const int64_t c = c0 + k, r = r0 + threadIdx.x;
-    if (c < cols && r < ld_out) {
-      int8_t a, b, d;
-      slice3((double)tile[threadIdx.x][k], ecol[c] - 2048, a, b, d);
-      S[c * ld_out + r] = a;
-      S[plane + c * ld_out + r] = b;
-      S[2 * plane + c * ld_out + r] = d;
-    }
-  }
-}
-
-// Apply operands: logical rows x cols matrix (row-major or transposed read),
-// per-row exponent; planes rows x ld_out int8 (cols = reduction index, contiguous).
+// Small operands (the r_hat x r_hat / r_hat x r matrices, fp64): logical rows x
+// cols read row-major or transposed, per-row exponent, planes rows x ld_out.
 template <typename T>
 __global__ void slice_rows_kernel(int64_t rows, int64_t cols, const T* __restrict__ in, int64_t ld_in, int transposed,
                                   const int* __restrict__ erow, int8_t* __restrict__ S, int64_t ld_out) {
@@ -206,26 +181,24 @@ __global__ void slice_rows_kernel(int64_t rows, int64_t cols, const T* __restric
   for (int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; f < total;
        f += (int64_t)gridDim.x * blockDim.x) {
     const int64_t r = f / ld_out, c = f - r * ld_out;
-    int8_t a = 0, b = 0, d = 0;
-    if (c < cols) slice3((double)(transposed ? in[c * ld_in + r] : in[r * ld_in + c]), erow[r] - 2048, a, b, d);
-    S[f] = a;
-    S[plane + f] = b;
-    S[2 * plane + f] = d;
+    int8_t s[kSlices] = {0, 0, 0, 0};
+    if (c < cols) slice4((double)(transposed ? in[c * ld_in + r] : in[r * ld_in + c]), erow[r] - 2048, s);
+#pragma unroll
+    for (int p = 0; p < kSlices; ++p) S[p * plane + f] = s[p];
   }
 }
 
 // ------------------------------------------------------------------ kernel --
-// LEVELS = 3: the full 6-product scheme (21 bits); LEVELS = 1: only s1 s1'
-// (7-bit slices, one plane) -- enough for the first CholeskyQR pass, whose R
-// only needs to precondition (span(B R^-1) = span(B) for any R).
 template <int N, int STAGES, int LEVELS>
 struct OzCfg {
-  static constexpr int PLANES = LEVELS == 1 ? 1 : kSlices;
-  static constexpr int A_PLANE = 128 * kBK;  // 128 rows x 128 K bytes
+  static constexpr int PLANES = LEVELS;      // level l needs slices 0..l
+  static constexpr int A_PLANE = 128 * kBK;  // 128 rows x 64 K bytes
   static constexpr int B_PLANE = N * kBK;
   static constexpr int STAGE_BYTES = PLANES * (A_PLANE + B_PLANE);
   static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
   static constexpr uint32_t TMEM_COLS = LEVELS * N <= 128 ? 128 : (LEVELS * N <= 256 ? 256 : 512);
+  static_assert(LEVELS * N <= 512, "accumulators exceed TMEM");
+  static_assert(SMEM <= 227 * 1024, "stages exceed shared memory");
 };
 
 // kind::i8, signed x signed, s32 accumulate, both K-major
@@ -243,6 +216,17 @@ __device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t adesc, uint64_t
       : "memory");
 }
 
+// K-major SWIZZLE_64B matrix descriptor: 8-row x 64-byte atoms (SBO = 512 B).
+__device__ __forceinline__ uint64_t desc_sw64(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+  d |= (uint64_t)1 << 16;           // LBO (ignored for swizzled K-major) = 16 B
+  d |= (uint64_t)(512 >> 4) << 32;  // SBO
+  d |= (uint64_t)1 << 46;           // descriptor version (sm_100)
+  d |= (uint64_t)4 << 61;           // SWIZZLE_64B
+  return d;
+}
+
 __device__ __forceinline__ void tmem_ld32_i(uint32_t taddr, int (&v)[32]) {
   float f[32];
   tmem_ld32(taddr, f);
@@ -251,8 +235,8 @@ __device__ __forceinline__ void tmem_ld32_i(uint32_t taddr, int (&v)[32]) {
 }
 
 // MODE 0 (Gram/cross): D[i, j] over K rows [k_begin, k_end) of the split, A
-//   rows = output rows i (ka of them), B rows = output cols j; result added to
-//   the fp64 partial P[split] (ka x kb).
+//   rows = output rows i (ka of them), B rows = output cols j; result written
+//   to the fp64 partial P[split] (ka x kb).
 // MODE 1 (apply): D[r, j] = sum_K A[r, :] B[j, :] over the full K; fp32 out.
 template <int MODE, int N, int STAGES, int LEVELS>
 __global__ void __launch_bounds__(kThreads, 1)
@@ -325,18 +309,15 @@ __global__ void __launch_bounds__(kThreads, 1)
           uint64_t a[Cfg::PLANES], b[Cfg::PLANES];
 #pragma unroll
           for (int p = 0; p < Cfg::PLANES; ++p) {
-            a[p] = smem_desc_sw128(base + p * Cfg::A_PLANE + ks * 32, 16, 1024);
-            b[p] = smem_desc_sw128(bbase + p * Cfg::B_PLANE + ks * 32, 16, 1024);
+            a[p] = desc_sw64(base + p * Cfg::A_PLANE + ks * 32);
+            b[p] = desc_sw64(bbase + p * Cfg::B_PLANE + ks * 32);
           }
           const uint32_t acc = (it == 0 && ks == 0) ? 0u : 1u;
-          mma_i8(tmem + 0 * N, a[0], b[0], idesc, acc);  // L0: s1 s1'
-          if (LEVELS == 3) {
-            mma_i8(tmem + 1 * N, a[0], b[1 % Cfg::PLANES], idesc, acc);  // L1: s1 s2'
-            mma_i8(tmem + 1 * N, a[1 % Cfg::PLANES], b[0], idesc, 1u);   //     s2 s1'
-            mma_i8(tmem + 2 * N, a[1 % Cfg::PLANES], b[1 % Cfg::PLANES], idesc, acc);  // L2: s2 s2'
-            mma_i8(tmem + 2 * N, a[0], b[2 % Cfg::PLANES], idesc, 1u);                 //     s1 s3'
-            mma_i8(tmem + 2 * N, a[2 % Cfg::PLANES], b[0], idesc, 1u);                 //     s3 s1'
-          }
+          // level l accumulates the slice pairs (t, l - t)
+#pragma unroll
+          for (int l = 0; l < LEVELS; ++l)
+#pragma unroll
+            for (int t = 0; t <= l; ++t) mma_i8(tmem + l * N, a[t], b[l - t], idesc, t == 0 ? acc : 1u);
         }
         mma_commit(&empty[s]);
         if (it == iters - 1) mma_commit(&tfull[0]);
@@ -355,19 +336,19 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
 #pragma unroll 1
     for (int cc = 0; cc < N / 32; ++cc) {
-      int l0[32], l1[32], l2[32];
+      double v[32];
+#pragma unroll
+      for (int t = 0; t < 32; ++t) v[t] = 0.0;
       if (iters > 0) {
-        tmem_ld32_i(tl + 0 * N + cc * 32, l0);
-        if (LEVELS == 3) {
-          tmem_ld32_i(tl + 1 * N + cc * 32, l1);
-          tmem_ld32_i(tl + 2 * N + cc * 32, l2);
-        } else {
+        double scale = 1.0;
 #pragma unroll
-          for (int t = 0; t < 32; ++t) l1[t] = l2[t] = 0;
+        for (int l = 0; l < LEVELS; ++l) {
+          int acc[32];
+          tmem_ld32_i(tl + l * N + cc * 32, acc);
+#pragma unroll
+          for (int t = 0; t < 32; ++t) v[t] += (double)acc[t] * scale;
+          scale *= 0x1p-7;
         }
-      } else {
-#pragma unroll
-        for (int t = 0; t < 32; ++t) l0[t] = l1[t] = l2[t] = 0;
       }
       if (!row_ok) continue;
       const int cbase = j0 + cc * 32;
@@ -376,20 +357,14 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int t = 0; t < 32; ++t) {
           const int col = cbase + t;
-          if (col < rowsB) {
-            const double v = (double)l0[t] + (double)l1[t] * 0x1p-7 + (double)l2[t] * 0x1p-14;
-            prow[col] = ldexp(v, ea + eB[col] - 2048 - 12);
-          }
+          if (col < rowsB) prow[col] = ldexp(v[t], ea + eB[col] - 2048 - 12);
         }
       } else {
         float* orow = Out + (int64_t)row * ldo;
 #pragma unroll
         for (int t = 0; t < 32; ++t) {
           const int col = cbase + t;
-          if (col < rowsB) {
-            const double v = (double)l0[t] + (double)l1[t] * 0x1p-7 + (double)l2[t] * 0x1p-14;
-            orow[col] = (float)ldexp(v, ea + eB[col] - 2048 - 12);
-          }
+          if (col < rowsB) orow[col] = (float)ldexp(v[t], ea + eB[col] - 2048 - 12);
         }
       }
     }
@@ -434,7 +409,7 @@ EncodeTiledFn encode_fn() {
   return fn;
 }
 
-// 2-D byte map over rows x cols int8 (row pitch ld bytes), box = 128 bytes x box_rows.
+// 2-D byte map over rows x cols int8 (row pitch ld bytes), box = 64 bytes x box_rows, 64B swizzle.
 int make_map_u8(fsr_ctx* ctx, CUtensorMap* m, const void* base, int64_t rows, int64_t cols, int64_t ld,
                 int box_rows) {
   EncodeTiledFn fn = encode_fn();
@@ -444,7 +419,7 @@ int make_map_u8(fsr_ctx* ctx, CUtensorMap* m, const void* base, int64_t rows, in
   cuuint32_t box[2] = {kBK, (cuuint32_t)box_rows};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, (void*)base, dims, strides, box, estr,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fsr::set_error(ctx, FSR_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
   return FSR_OK;
@@ -458,15 +433,25 @@ int set_smem(fsr_ctx* ctx, K kernel, int bytes) {
   return FSR_OK;
 }
 
-constexpr int kStages = 2;
 constexpr size_t kChunkBudget = (size_t)6 << 30;  // bytes of slice staging per row chunk
 
-template <int MODE, int LEVELS = 3>
+// tile width / pipeline depth per variant
+template <int LEVELS>
+struct Variant;
+template <>
+struct Variant<4> {  // 4 x 128 TMEM columns; 3 stages of 4 x (128 + 128) x 64 B
+  static constexpr int N = 128, STAGES = 3;
+};
+template <>
+struct Variant<1> {  // 160 TMEM columns; 8 stages of (128 + 160) x 64 B
+  static constexpr int N = 160, STAGES = 8;
+};
+
+template <int MODE, int LEVELS>
 int launch_oz(fsr_ctx* ctx, dim3 grid, const CUtensorMap& mA, const CUtensorMap& mB, int rowsA, int rowsB,
               int64_t pA, int64_t pB, int64_t K, int tiles_n, int64_t kps, const int* eA, const int* eB, int sym,
               double* P, float* Out, int64_t ldo) {
-  constexpr int N = MODE == 0 ? kNG : kNA;
-  constexpr int STAGES = LEVELS == 1 ? 5 : kStages;
+  constexpr int N = Variant<LEVELS>::N, STAGES = Variant<LEVELS>::STAGES;
   using Cfg = OzCfg<N, STAGES, LEVELS>;
   static bool attr = false;
   if (!attr) {
@@ -483,19 +468,21 @@ int launch_oz(fsr_ctx* ctx, dim3 grid, const CUtensorMap& mA, const CUtensorMap&
 namespace fsr {
 
 // C (ka x kb, fp64 row-major) (+)= A^T B over n rows of fp32 row-major blocks.
+// levels == 1: one-slice preconditioner Gram; otherwise the full 28-bit scheme.
 int tc_gram(fsr_ctx* ctx, int64_t n, int64_t ka, const float* A, int64_t lda, int64_t kb, const float* B,
             int64_t ldb, double* C, int accumulate, int levels, int symmetric) {
   const bool same = (A == B) && lda == ldb && ka == kb;
   symmetric = symmetric && same;
+  const int NT = levels == 1 ? Variant<1>::N : Variant<4>::N;
   const int64_t per_row = kSlices * (ka + (same ? 0 : kb));
-  int64_t chunk = std::max<int64_t>(kBK, std::min<int64_t>({n, kMaxK, (int64_t)(kChunkBudget / per_row)}));
-  chunk = pad_to(chunk, kBK);
-  const int tiles_m = (int)ceil_div(ka, 128), tiles_n = (int)ceil_div(kb, kNG);
+  int64_t chunk = std::max<int64_t>(128, std::min<int64_t>({n, kMaxK, (int64_t)(kChunkBudget / per_row)}));
+  chunk = pad_to(chunk, 128);
+  const int tiles_m = (int)ceil_div(ka, 128), tiles_n = (int)ceil_div(kb, NT);
   int tiles_eff = 0;
   for (int ti = 0; ti < tiles_m; ++ti)
-    for (int tj = 0; tj < tiles_n; ++tj) tiles_eff += !(symmetric && tj * kNG + kNG - 1 < ti * 128);
+    for (int tj = 0; tj < tiles_n; ++tj) tiles_eff += !(symmetric && tj * NT + NT - 1 < ti * 128);
   int splits = (int)std::max<int64_t>(1, ceil_div(2 * ctx->num_sms, tiles_eff));
-  splits = (int)std::min<int64_t>(splits, std::max<int64_t>(1, chunk / (4 * kBK)));
+  splits = (int)std::min<int64_t>(splits, std::max<int64_t>(1, chunk / (8 * kBK)));
   const size_t p_bytes = (size_t)splits * ka * kb * 8;
   const size_t e_bytes = (size_t)(ka + kb) * 4 + 256;
   const size_t s_bytes = (size_t)chunk * per_row;
@@ -508,7 +495,7 @@ int tc_gram(fsr_ctx* ctx, int64_t n, int64_t ka, const float* A, int64_t lda, in
   int8_t* sB = same ? sA : sA + kSlices * ka * chunk;
   for (int64_t s0 = 0; s0 < n; s0 += chunk) {
     const int64_t rows = std::min(chunk, n - s0);
-    const int64_t ldT = pad_to(rows, kBK);
+    const int64_t ldT = pad_to(rows, 128);
     // exponents per column over this chunk, then transposed slice planes
     FSR_CUDA(ctx, cudaMemsetAsync(eA, 0, (ka + (same ? 0 : kb)) * 4, ctx->stream));
     {
@@ -529,28 +516,30 @@ int tc_gram(fsr_ctx* ctx, int64_t n, int64_t ka, const float* A, int64_t lda, in
     }
     CUtensorMap mA, mB;
     FSR_TRY(make_map_u8(ctx, &mA, sA, kSlices * ka, ldT, ldT, 128));
-    FSR_TRY(make_map_u8(ctx, &mB, sB, kSlices * kb, ldT, ldT, kNG));
+    FSR_TRY(make_map_u8(ctx, &mB, sB, kSlices * kb, ldT, ldT, NT));
     const int64_t kps = pad_to(ceil_div(ldT, splits), kBK);
     dim3 grid((unsigned)(tiles_m * tiles_n), (unsigned)ceil_div(ldT, kps));
     if (levels == 1)
       FSR_TRY((launch_oz<0, 1>(ctx, grid, mA, mB, (int)ka, (int)kb, ka, kb, ldT, tiles_n, kps, eA, eB, symmetric,
                                P, nullptr, 0)));
     else
-      FSR_TRY((launch_oz<0, 3>(ctx, grid, mA, mB, (int)ka, (int)kb, ka, kb, ldT, tiles_n, kps, eA, eB, symmetric,
+      FSR_TRY((launch_oz<0, 4>(ctx, grid, mA, mB, (int)ka, (int)kb, ka, kb, ldT, tiles_n, kps, eA, eB, symmetric,
                                P, nullptr, 0)));
     const int acc = (s0 > 0) || accumulate;
-    gram_reduce_kernel<<<grid_for(ka * kb, 256, ctx, 8), 256, 0, ctx->stream>>>(
-        (int)ka, (int)kb, (int)grid.y, P, C, acc, symmetric);
+    gram_reduce_kernel<<<grid_for(ka * kb, 256, ctx, 8), 256, 0, ctx->stream>>>((int)ka, (int)kb, (int)grid.y, P,
+                                                                                C, acc, symmetric);
     FSR_TRY(launched(ctx, "gram_reduce_kernel"));
   }
   return FSR_OK;
 }
 
 // Out (n x N2 fp32) = A (n x K fp32) * M (K x N2, fp64; column-major if m_col_major).
+// Out may alias A (row chunks are sliced before they are overwritten).
 int tc_apply(fsr_ctx* ctx, int64_t n, int64_t K, const float* A, int64_t lda, int64_t N2, const double* M,
              int64_t ldm, int m_col_major, float* Out, int64_t ldo) {
   if (K > kMaxK) return set_error(ctx, FSR_EINVAL, "tc_apply: K=%lld exceeds the int32-exact bound", (long long)K);
-  const int64_t pk = pad_to(K, kBK);
+  constexpr int NT = Variant<4>::N;
+  const int64_t pk = pad_to(K, 128);
   const size_t m_bytes = (size_t)kSlices * N2 * pk;
   const int64_t per_row = kSlices * pk;
   int64_t chunk = std::max<int64_t>(128, std::min<int64_t>(n, (int64_t)(kChunkBudget / per_row)));
@@ -569,18 +558,18 @@ int tc_apply(fsr_ctx* ctx, int64_t n, int64_t K, const float* A, int64_t lda, in
   slice_rows_kernel<double><<<grid_for(N2 * pk, 256, ctx, 16), 256, 0, ctx->stream>>>(N2, K, M, ldm, tr, eM, sM, pk);
   FSR_TRY(launched(ctx, "slice_rows_kernel"));
   CUtensorMap mB;
-  FSR_TRY(make_map_u8(ctx, &mB, sM, kSlices * N2, pk, pk, kNA));
-  const int tiles_n = (int)ceil_div(N2, kNA);
+  FSR_TRY(make_map_u8(ctx, &mB, sM, kSlices * N2, pk, pk, NT));
+  const int tiles_n = (int)ceil_div(N2, NT);
   for (int64_t s0 = 0; s0 < n; s0 += chunk) {
     const int64_t rows = std::min(chunk, n - s0);
-    slice_rows_fused_kernel<<<grid_for(rows * 32, 256, ctx, 8), 256, 0, ctx->stream>>>(rows, K, A + s0 * lda, lda, eR,
-                                                                                       sR, pk);
+    slice_rows_fused_kernel<<<grid_for(rows * 32, 256, ctx, 8), 256, 0, ctx->stream>>>(rows, K, A + s0 * lda, lda,
+                                                                                       eR, sR, pk);
     FSR_TRY(launched(ctx, "slice_rows_fused_kernel"));
     CUtensorMap mA;
     FSR_TRY(make_map_u8(ctx, &mA, sR, kSlices * rows, pk, pk, 128));
     dim3 grid((unsigned)(ceil_div(rows, 128) * tiles_n), 1);
-    FSR_TRY(launch_oz<1>(ctx, grid, mA, mB, (int)rows, (int)N2, rows, N2, pk, tiles_n, pk, eR, eM, 0, nullptr,
-                         Out + s0 * ldo, ldo));
+    FSR_TRY((launch_oz<1, 4>(ctx, grid, mA, mB, (int)rows, (int)N2, rows, N2, pk, tiles_n, pk, eR, eM, 0, nullptr,
+                             Out + s0 * ldo, ldo)));
   }
   return FSR_OK;
 }
