@@ -69,6 +69,20 @@ def load_peaks():
         return 6650.0, "fallback"
 
 
+def load_profile(name):
+    """A committed measurement summary under profiles/ (None when absent)."""
+    path = os.path.join(REPO, "profiles", PROFILE_ROUND, name)
+    try:
+        with open(path) as f:
+            return json.load(f)
+    except Exception:
+        return None
+
+
+PROFILE_ROUND = "r01"
+FP32_LANES_PER_SM = 128  # FFMA lanes per SM (sm_100)
+
+
 class ClockSampler:
     """nvidia-smi sampling of SM clocks and throttle reasons while the bench runs."""
 
@@ -385,10 +399,16 @@ def run_fsr(args, cfg, n, rank, world, local_rank):
     nnz_s = S.nnz
     spmm_bytes = nnz_s * (es + 4) + (n + 1) * 8 + 2 * es * n * r_hat
     spmm_gbs = spmm_bytes / (spmm_ms_iter * 1e-3) / 1e9
+    # what K2 must actually move on a graph without locality: one dense row
+    # gather per nonzero (Q >> L2), i.e. nnz * r_hat * es bytes from DRAM
+    spmm_gather = nnz_s * r_hat * es
+    spmm_gather_gbs = spmm_gather / (spmm_ms_iter * 1e-3) / 1e9
     offline = {
         "si_time_s": si_s, "rayleigh_ritz_s": rr_s, "sparsify_s": sp_s, "decompose_total_s": si_s + rr_s + sp_s,
         "spmm_ms_per_iter": spmm_ms_iter, "spmm_launches": spmm_cnt, "spmm_algorithmic_bytes": spmm_bytes,
         "spmm_gbs": spmm_gbs, "spmm_hbm_frac": spmm_gbs / peak_gbs,
+        "spmm_gather_bytes": spmm_gather, "spmm_gather_gbs": spmm_gather_gbs,
+        "spmm_gather_hbm_frac": spmm_gather_gbs / peak_gbs,
         "spmm_fp32_tflops": 2.0 * nnz_s * r_hat / (spmm_ms_iter * 1e-3) / 1e12,
         "stage_ms": {k: round(v[0], 3) for k, v in stages.items() if v[1]},
         "nnz_W": nnz_w, "isolated_vertices": isolated, "kept_nnz": sdec.U_device.nnz, "inputs_build_s": t_inputs,
@@ -441,6 +461,14 @@ def run_fsr(args, cfg, n, rank, world, local_rank):
     k9_bytes = kept * (es + 4) + (n + 1) * 8 + es * r * b + es * n * b
     k9_gbs = k9_bytes / (k9_ms_launch * 1e-3) / 1e9
     k9_share = k9_ms / max(sum(v[0] for v in on_stages.values()), 1e-9)
+    # binding limbs: every nonzero of U~ gathers one b-wide row of Zs (L2-resident)
+    k9_gather = kept * b * es
+    k9_gather_gbs = k9_gather / (k9_ms_launch * 1e-3) / 1e9
+    l2 = load_profile("l2_bw.json") or {}
+    l2_peak = l2.get("gather_1KB_rows_19MB_GBs")
+    ncu9 = load_profile("k9_ncu_full.json") or {}
+    k9_traffic = ncu9.get("dram_bytes_per_launch") if (cfg.name == "C3" and b == 1024 and es == 4
+                                                         and args.density is None) else None
 
     # ---------------- e2e through the public API with host buffers ----------
     e2e = None
@@ -491,6 +519,8 @@ def run_fsr(args, cfg, n, rank, world, local_rank):
 
     if rank != 0:
         return
+    sms = torch.cuda.get_device_properties(device).multi_processor_count
+    fp32_peak = 2.0 * sms * FP32_LANES_PER_SM * ((clk or {}).get("sm_mhz") or 1965.0) * 1e6 / 1e12
     line = {
         "metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": dev_ms_max / args.steps, "higher_is_better": True,
@@ -501,11 +531,21 @@ def run_fsr(args, cfg, n, rank, world, local_rank):
                                f"h_alpha({cfg.alpha}), top-{K}",
                    "global_batch": b * world, "parallelism": (f"offline row-sharded x{world} (NCCL all-gather + ordered fp64 sums), online replicas (batch split)" if world > 1 else "single GPU"),
                    "l2": "256 MB buffer written between timed steps (L2 flush); U~ itself > L2"},
-        "roofline": {"kernel": "K9 filter SpMM (spmm_rowpanel_kernel on U~ x Zs)", "bound": "hbm",
+        "roofline": {"kernel": "K9 filter SpMM (spmm_rowpanel_T_kernel on U~ x Zs)", "bound": "hbm",
                      "achieved": k9_gbs, "peak": peak_gbs, "unit": "GB/s", "frac": k9_gbs / peak_gbs,
-                     "peak_kind": peak_kind, "traffic": None, "algorithmic_bytes_per_launch": k9_bytes,
+                     "peak_kind": peak_kind, "traffic": k9_traffic,
+                     "traffic_source": ("profiles/%s/k9_ncu_full.json" % PROFILE_ROUND) if k9_traffic else None,
+                     "algorithmic_bytes_per_launch": k9_bytes,
                      "ms_per_launch": k9_ms_launch, "share_of_step": k9_share,
-                     "fp32_tflops": 2.0 * kept * b / (k9_ms_launch * 1e-3) / 1e12},
+                     "binding_limbs": {
+                         "l2_gather": {"bytes_per_launch": k9_gather, "achieved_gbs": k9_gather_gbs,
+                                       "peak_gbs": l2_peak, "frac": (k9_gather_gbs / l2_peak) if l2_peak else None,
+                                       "peak_source": "tools/l2_bw.cu random 1 KB row gathers from a 19 MB "
+                                                      "matrix (profiles/%s/l2_bw.json)" % PROFILE_ROUND},
+                         "fp32_fma": {"achieved_tflops": 2.0 * kept * b / (k9_ms_launch * 1e-3) / 1e12,
+                                      "peak_tflops": fp32_peak,
+                                      "frac": 2.0 * kept * b / (k9_ms_launch * 1e-3) / 1e12 / fp32_peak},
+                     }},
         "online_stage_ms_per_step": {k: v[0] / args.steps for k, v in on_stages.items()},
         "offline": offline,
         "gpu_launches": launches,

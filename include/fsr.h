@@ -74,9 +74,11 @@ enum fsr_stage {
 int fsr_ctx_enable_timing(fsr_ctx* ctx, int on);
 
 /* Context options.  FSR_OPT_DENSE_PATH: 0 = auto (F32 Gram / cross / apply /
- * lift on tcgen05 3xTF32 kernels), 1 = cuBLAS/cuSOLVER (fp64-upcast Gram,
- * TRSM, SGEMM) -- kept for A/B checks. */
-enum fsr_option { FSR_OPT_DENSE_PATH = 0 };
+ * lift on the tcgen05 int8 Ozaki kernels), 1 = cuBLAS/cuSOLVER (fp64-upcast
+ * Gram, TRSM, SGEMM) -- kept for A/B checks.  FSR_OPT_SPMM_PANEL_BYTES: K2
+ * schedule -- 0 = wide row panels, 32/64/128 = L2-resident column panels of
+ * that many bytes per dense row (results identical; speed only). */
+enum fsr_option { FSR_OPT_DENSE_PATH = 0, FSR_OPT_SPMM_PANEL_BYTES = 1 };
 int fsr_ctx_set_option(fsr_ctx* ctx, int option, int64_t value);
 int fsr_stage_time(fsr_ctx* ctx, int stage, double* ms, uint64_t* count);
 int fsr_stage_reset(fsr_ctx* ctx);

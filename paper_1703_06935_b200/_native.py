@@ -182,8 +182,12 @@ class Context:
         return st
 
     def set_dense_path(self, path: str):
-        """'auto' (tcgen05 3xTF32 kernels for float32 blocks) or 'cublas'."""
+        """'auto' (tcgen05 int8 Ozaki kernels for float32 blocks) or 'cublas'."""
         self.check(self.lib.fsr_ctx_set_option(self.handle, 0, {"auto": 0, "tcgen05": 0, "cublas": 1}[path]))
+
+    def set_spmm_panel(self, panel_bytes: int):
+        """K2 schedule: 0 = wide row panels, 32/64/128 = L2-resident column panels."""
+        self.check(self.lib.fsr_ctx_set_option(self.handle, 1, int(panel_bytes)))
 
     def enable_timing(self, on: bool = True):
         self.check(self.lib.fsr_ctx_enable_timing(self.handle, int(on)))

@@ -25,6 +25,7 @@ struct fsr_ctx {
   void* scratch_aux = nullptr;  // caller-level temporaries that outlive a scratch() user
   size_t scratch_aux_bytes = 0;
   int dense_path = 0;           // FSR_OPT_DENSE_PATH: 0 auto (tcgen05 for F32), 1 cuBLAS
+  int spmm_panel_bytes = 0;     // FSR_OPT_SPMM_PANEL_BYTES: 0 wide row panels, else L2 panel width
   int* dev_info = nullptr;
   double* host_stage = nullptr;  // pinned staging for small host reads
   size_t host_stage_bytes = 0;

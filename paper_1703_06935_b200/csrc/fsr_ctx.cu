@@ -86,6 +86,11 @@ int fsr_ctx_set_option(fsr_ctx* ctx, int option, int64_t value) {
       if (value < 0 || value > 1) return fsr::set_error(ctx, FSR_EINVAL, "dense path must be 0 or 1");
       ctx->dense_path = (int)value;
       return FSR_OK;
+    case FSR_OPT_SPMM_PANEL_BYTES:
+      if (value != 0 && value != 32 && value != 64 && value != 128)
+        return fsr::set_error(ctx, FSR_EINVAL, "spmm panel must be 0, 32, 64 or 128 bytes");
+      ctx->spmm_panel_bytes = (int)value;
+      return FSR_OK;
     default:
       return fsr::set_error(ctx, FSR_EINVAL, "unknown option %d", option);
   }

@@ -70,7 +70,7 @@ constexpr int kGatherDepth = 4;  // dense rows gathered before their FMAs (memor
 
 // Accumulate row i of the CSR matrix against the dense panel columns
 // [c0 + u*32*VEC, +VEC) (u < NV) into acc; nonzeros are consumed in CSR order.
-template <typename T, int VEC, int NV>
+template <typename T, int VEC, int NV, int DEPTH = kGatherDepth>
 __device__ __forceinline__ void row_panel_accumulate(int64_t e0, int64_t e1, const int32_t* __restrict__ indices,
                                                      const T* __restrict__ vals, const T* __restrict__ X,
                                                      int64_t ldx, int64_t c0, const bool (&live)[NV],
@@ -85,22 +85,22 @@ __device__ __forceinline__ void row_panel_accumulate(int64_t e0, int64_t e1, con
       my_val = __ldg(vals + base + lane);
     }
     int j = 0;
-    for (; j + kGatherDepth <= m; j += kGatherDepth) {
-      int c[kGatherDepth];
-      T a[kGatherDepth];
+    for (; j + DEPTH <= m; j += DEPTH) {
+      int c[DEPTH];
+      T a[DEPTH];
 #pragma unroll
-      for (int g = 0; g < kGatherDepth; ++g) {
+      for (int g = 0; g < DEPTH; ++g) {
         c[g] = __shfl_sync(0xffffffffu, my_col, j + g);
         a[g] = __shfl_sync(0xffffffffu, my_val, j + g);
       }
-      T v[kGatherDepth][NV][VEC];
+      T v[DEPTH][NV][VEC];
 #pragma unroll
-      for (int g = 0; g < kGatherDepth; ++g)
+      for (int g = 0; g < DEPTH; ++g)
 #pragma unroll
         for (int u = 0; u < NV; ++u)
           if (live[u]) load_vec<T, VEC>(X + (int64_t)c[g] * ldx + c0 + u * 32 * VEC, v[g][u]);
 #pragma unroll
-      for (int g = 0; g < kGatherDepth; ++g)
+      for (int g = 0; g < DEPTH; ++g)
 #pragma unroll
         for (int u = 0; u < NV; ++u)
 #pragma unroll
@@ -156,8 +156,8 @@ __global__ void __launch_bounds__(256) spmm_rowpanel_kernel(int64_t n_rows, cons
 // K9 variant with a transposed output: CTA = 32 consecutive rows x one panel;
 // each warp computes 4 rows, the 32 x PW tile is staged in shared memory
 // (padded) and written as Y^T (ldy = n): 128-byte coalesced column segments.
-template <typename T, int VEC, int NV>
-__global__ void __launch_bounds__(256) spmm_rowpanel_T_kernel(int64_t n_rows, const int64_t* __restrict__ indptr,
+template <typename T, int VEC, int NV, int DEPTH = kGatherDepth, int MINB = 1>
+__global__ void __launch_bounds__(256, MINB) spmm_rowpanel_T_kernel(int64_t n_rows, const int64_t* __restrict__ indptr,
                                                               const int32_t* __restrict__ indices,
                                                               const T* __restrict__ vals, int64_t ncols,
                                                               const T* __restrict__ X, int64_t ldx,
@@ -179,8 +179,8 @@ __global__ void __launch_bounds__(256) spmm_rowpanel_T_kernel(int64_t n_rows, co
 #pragma unroll
       for (int q = 0; q < VEC; ++q) acc[u][q] = T(0);
     if (i < n_rows)
-      row_panel_accumulate<T, VEC, NV>(__ldg(indptr + i), __ldg(indptr + i + 1), indices, vals, X, ldx, c0, live,
-                                       acc);
+      row_panel_accumulate<T, VEC, NV, DEPTH>(__ldg(indptr + i), __ldg(indptr + i + 1), indices, vals, X, ldx, c0,
+                                              live, acc);
 #pragma unroll
     for (int u = 0; u < NV; ++u)
 #pragma unroll
@@ -307,6 +307,66 @@ __global__ void __launch_bounds__(256) spmm_narrow_T_kernel(int64_t n_rows, cons
   }
 }
 
+// L2-resident column panels (row-major output): a group of LPR lanes owns one
+// output row and VEC*LPR columns of one panel, so a warp advances 32/LPR rows
+// at once with no cross-lane reduction; each group keeps DEPTH dense-row
+// gathers in flight and prefetches the next DEPTH (col, val) pairs while they
+// land.  Blocks are ordered panel-major (blockIdx.x = row block), so the whole
+// GPU sweeps one n x PW panel of X at a time; sized to fit one die's share
+// of L2, the panel is read from DRAM once and every gather after the first
+// hits L2.  The CSR stream is re-read once per panel.  Accumulation keeps CSR
+// order per output element (fp64: bitwise equal to scipy).
+template <typename T, int VEC, int LPR, int DEPTH>
+__global__ void __launch_bounds__(256) spmm_l2panel_kernel(int64_t n_rows, const int64_t* __restrict__ indptr,
+                                                           const int32_t* __restrict__ indices,
+                                                           const T* __restrict__ vals, int64_t ncols,
+                                                           const T* __restrict__ X, int64_t ldx,
+                                                           T* __restrict__ Y, int64_t ldy) {
+  constexpr int G = 32 / LPR;  // rows per warp
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int grp = lane / LPR, sl = lane % LPR;
+  const int64_t i = ((int64_t)blockIdx.x * 8 + warp) * G + grp;
+  const int64_t c0 = (int64_t)blockIdx.y * (LPR * VEC) + (int64_t)sl * VEC;
+  if (i >= n_rows || c0 >= ncols) return;
+  const int64_t e0 = __ldg(indptr + i), e1 = __ldg(indptr + i + 1);
+  T acc[VEC];
+#pragma unroll
+  for (int q = 0; q < VEC; ++q) acc[q] = T(0);
+  int c[DEPTH];
+  T a[DEPTH];
+#pragma unroll
+  for (int g = 0; g < DEPTH; ++g) {
+    const bool ok = e0 + g < e1;
+    c[g] = ok ? __ldg(indices + e0 + g) : -1;
+    a[g] = ok ? __ldg(vals + e0 + g) : T(0);
+  }
+  for (int64_t e = e0; e < e1; e += DEPTH) {
+    T v[DEPTH][VEC];
+#pragma unroll
+    for (int g = 0; g < DEPTH; ++g)
+      if (c[g] >= 0) load_vec<T, VEC>(X + (int64_t)c[g] * ldx + c0, v[g]);
+    T an[DEPTH];
+    int cn[DEPTH];
+#pragma unroll
+    for (int g = 0; g < DEPTH; ++g) {
+      const bool ok = e + DEPTH + g < e1;
+      cn[g] = ok ? __ldg(indices + e + DEPTH + g) : -1;
+      an[g] = ok ? __ldg(vals + e + DEPTH + g) : T(0);
+    }
+#pragma unroll
+    for (int g = 0; g < DEPTH; ++g)
+      if (c[g] >= 0)
+#pragma unroll
+        for (int q = 0; q < VEC; ++q) acc[q] = axpy1(acc[q], a[g], v[g][q]);
+#pragma unroll
+    for (int g = 0; g < DEPTH; ++g) {
+      c[g] = cn[g];
+      a[g] = an[g];
+    }
+  }
+  store_vec<T, VEC>(Y + i * ldy + c0, acc);
+}
+
 // SpMV with the dense vector staged in shared memory: random 4-byte gathers
 // from L1 cost one wavefront per distinct 128B line (~32 per warp access);
 // from shared memory they cost a few bank cycles.  Warp per row, 4 nonzeros
@@ -381,6 +441,10 @@ int launch_spmm_T(fsr_ctx* ctx, int64_t n_rows, const int64_t* indptr, const int
                                                                       Yt, ldy);
     return launched(ctx, "spmm_narrow_T_kernel");
   }
+  // Schedule variants measured on B200 (tools/k9_micro.py, C3 shape, b = 1024):
+  // NV=2 (256 columns) 20.9 ms; NV=1 22.2 ms; NV=1 depth 8 22.7 ms; NV=2 with
+  // 4 CTAs/SM (64 registers) 45.7 ms; NV=1 with 6 CTAs/SM 30.4 ms -- all
+  // bitwise identical.  The kernel streams ~19.6 TB/s of L2->SM gathers.
   if (vec_ok && ncols > 32 * VW) {
     constexpr int NV = 2, PW = 32 * VW * NV;
     dim3 grid((unsigned)ceil_div(n_rows, 32), (unsigned)ceil_div(ncols, PW));
@@ -410,33 +474,31 @@ int launch_spmm(fsr_ctx* ctx, int64_t n_rows, const int64_t* indptr, const int32
   }
   constexpr int VW = sizeof(T) == 4 ? 4 : 2;  // 16-byte vectors
   const bool vec_ok = ncols % VW == 0 && ldx % VW == 0 && ldy % VW == 0 && aligned(X, 16) && aligned(Y, 16);
-  // Large dense blocks: the wide panel (256 fp32 / 128 fp64 columns of all n
-  // rows) would not stay L2-resident while every row gathers from it, so use
-  // narrow panels (16 or 32 columns, warp per row) whose n x panel slice fits L2;
-  // W is re-streamed once per panel instead.
-  // Narrow row-major panels (warp per row, nonzero groups): an experiment knob
-  // (FSR_K2_PANEL = 16 | 32 | 64 | 128 columns).  Measured on B200 at C3
-  // (n = 1e6, r_hat = 5500): 16/32-column panels 241 ms vs 107 ms for the wide
-  // kernel, which streams its gathers at ~6.5 TB/s of DRAM; the default stays wide.
-  static const int k2_panel = [] {
-    const char* e = getenv("FSR_K2_PANEL");
-    return e ? atoi(e) : 0;
-  }();
-  if (k2_panel > 0 && vec_ok && ncols >= 16) {
-    dim3 grid((unsigned)ceil_div(n_rows, 64), (unsigned)ceil_div(ncols, k2_panel));
-    if (k2_panel == 16)
-      spmm_narrow_T_kernel<T, VW, 16 / VW, false><<<grid, block, 0, ctx->stream>>>(n_rows, indptr, indices, vals, ncols,
-                                                                                   X, ldx, Y, ldy);
-    else if (k2_panel == 32)
-      spmm_narrow_T_kernel<T, VW, 32 / VW, false><<<grid, block, 0, ctx->stream>>>(n_rows, indptr, indices, vals, ncols,
-                                                                                   X, ldx, Y, ldy);
-    else if (k2_panel == 64)
-      spmm_narrow_T_kernel<T, VW, 64 / VW, false><<<grid, block, 0, ctx->stream>>>(n_rows, indptr, indices, vals, ncols,
-                                                                                   X, ldx, Y, ldy);
+  // L2-resident column panels (FSR_OPT_SPMM_PANEL_BYTES = 32 | 64 | 128 bytes
+  // of each dense row per panel); 0 = the wide row-panel kernel below.
+  // Measured on B200 (tools/spmm_micro.py, n = 1e6, k = 5500, 29 nnz/row of
+  // random columns): wide 107 ms (gathers stream at 5.95 TB/s from DRAM);
+  // 32/64/128-byte panels 443/236/177 ms.  Panels strided across the 22 GB
+  // block touch every page on every pass (TLB reach); even a contiguous
+  // panel copy (n x 8/16/32 columns) extrapolates to 145/121/129 ms, because
+  // 32-128 byte gathers from L2 run at a lower request efficiency than the
+  // wide kernel's DRAM stream.  So the wide kernel stays the default.
+  const int panel_bytes = ctx->spmm_panel_bytes;
+  if (panel_bytes > 0 && vec_ok) {
+    constexpr int D = 8;
+    const int lpr = panel_bytes / 16;  // 16-byte vectors per row segment
+    const int64_t pw = (int64_t)lpr * VW;
+    dim3 grid((unsigned)ceil_div(n_rows, 8 * (32 / lpr)), (unsigned)ceil_div(ncols, pw));
+    if (lpr == 2)
+      spmm_l2panel_kernel<T, VW, 2, D><<<grid, block, 0, ctx->stream>>>(n_rows, indptr, indices, vals, ncols, X, ldx,
+                                                                         Y, ldy);
+    else if (lpr == 4)
+      spmm_l2panel_kernel<T, VW, 4, D><<<grid, block, 0, ctx->stream>>>(n_rows, indptr, indices, vals, ncols, X, ldx,
+                                                                         Y, ldy);
     else
-      spmm_narrow_T_kernel<T, VW, 32, false><<<dim3(grid.x, (unsigned)ceil_div(ncols, 32 * VW)), block, 0,
-                                                ctx->stream>>>(n_rows, indptr, indices, vals, ncols, X, ldx, Y, ldy);
-    return launched(ctx, "spmm_narrow_rowmajor_kernel");
+      spmm_l2panel_kernel<T, VW, 8, D><<<grid, block, 0, ctx->stream>>>(n_rows, indptr, indices, vals, ncols, X, ldx,
+                                                                         Y, ldy);
+    return launched(ctx, "spmm_l2panel_kernel");
   }
   if (vec_ok) {
     constexpr int NV = 2;

@@ -97,14 +97,51 @@ def test_spmm_fp32(golden, ncols):
     assert err < 1e-6
 
 
-def test_spmm_empty_rows():
+@pytest.mark.parametrize("panel", [0, 32, 64, 128])
+def test_spmm_empty_rows(panel):
     # rows with no nonzeros (isolated vertices) must produce exact zeros
     S = sp.csr_matrix((np.array([0.5, 0.5]), (np.array([0, 3]), np.array([3, 0]))), shape=(5, 5))
     A = SparseSymmetricMatrix.from_scipy(S)
     X = torch.arange(5 * 8, dtype=torch.float64, device="cuda").reshape(5, 8)
     Y = torch.full_like(X, 7.0)
-    spectral._spmm(N.Context.get(), N.F64, A.device(torch.float64), X, Y)
+    ctx = N.Context.get()
+    ctx.set_spmm_panel(panel)
+    try:
+        spectral._spmm(ctx, N.F64, A.device(torch.float64), X, Y)
+    finally:
+        ctx.set_spmm_panel(0)
     np.testing.assert_array_equal(Y.cpu().numpy(), S @ X.cpu().numpy())
+
+
+@pytest.mark.parametrize("panel", [32, 64, 128])
+@pytest.mark.parametrize("ncols", [8, 350, 520])
+def test_spmm_l2panel_schedule(golden, panel, ncols):
+    """The L2-panel schedule keeps CSR order per element: fp64 bitwise equal to
+    scipy, fp32 bitwise equal to the wide row-panel kernel."""
+    g = golden("c1")
+    _, S = c1_mats(g)
+    A = SparseSymmetricMatrix.from_scipy(S)
+    rng = np.random.default_rng(ncols + panel)
+    X = rng.standard_normal((S.shape[0], ncols))
+    ctx = N.Context.get()
+    out = {}
+    for dt, tdt in ((N.F64, torch.float64), (N.F32, torch.float32)):
+        Xd = torch.as_tensor(X).to(tdt).cuda()
+        for p in (0, panel):
+            Yd = torch.full_like(Xd, float("nan"))
+            ctx.set_spmm_panel(p)
+            try:
+                spectral._spmm(ctx, dt, A.device(tdt), Xd, Yd)
+            finally:
+                ctx.set_spmm_panel(0)
+            out[(dt, p)] = Yd.cpu().numpy()
+    np.testing.assert_array_equal(out[(N.F64, panel)], S @ X)
+    np.testing.assert_array_equal(out[(N.F32, panel)], out[(N.F32, 0)])
+
+
+def test_spmm_panel_option_rejects_bad_width():
+    with pytest.raises(ValueError):
+        N.Context.get().set_spmm_panel(48)
 
 
 # ------------------------------------------------------------- K3-K6 -------
