@@ -220,7 +220,7 @@ def build_inputs(cfg, n, n_queries, device, dtype):
 
     t0 = time.perf_counter()
     X, Qv, _ = workloads.device_cluster_descriptors(cfg, device, n=n, queries=n_queries)
-    W = knn.mutual_knn_graph_device(X, cfg.k, cfg.gamma)
+    W = knn.mutual_knn_graph_device(X, cfg.k, cfg.gamma, gemm_dtype=torch.bfloat16)  # bf16 candidates, fp32 re-score
     deg = graph.degrees_device(W, device)
     S = graph.normalize_adjacency(W, deg, dtype=dtype, device=device)
     y_ptr, y_idx, y_val = knn.observation_batch_device(Qv, X, cfg.y_top, cfg.gamma)

@@ -156,8 +156,8 @@ __global__ void __launch_bounds__(256) spmm_rowpanel_kernel(int64_t n_rows, cons
 // K9 variant with a transposed output: CTA = 32 consecutive rows x one panel;
 // each warp computes 4 rows, the 32 x PW tile is staged in shared memory
 // (padded) and written as Y^T (ldy = n): 128-byte coalesced column segments.
-template <typename T, int VEC, int NV, int DEPTH = kGatherDepth, int MINB = 1>
-__global__ void __launch_bounds__(256, MINB) spmm_rowpanel_T_kernel(int64_t n_rows, const int64_t* __restrict__ indptr,
+template <typename T, int VEC, int NV, int DEPTH = kGatherDepth>
+__global__ void __launch_bounds__(256) spmm_rowpanel_T_kernel(int64_t n_rows, const int64_t* __restrict__ indptr,
                                                               const int32_t* __restrict__ indices,
                                                               const T* __restrict__ vals, int64_t ncols,
                                                               const T* __restrict__ X, int64_t ldx,
@@ -442,9 +442,11 @@ int launch_spmm_T(fsr_ctx* ctx, int64_t n_rows, const int64_t* indptr, const int
     return launched(ctx, "spmm_narrow_T_kernel");
   }
   // Schedule variants measured on B200 (tools/k9_micro.py, C3 shape, b = 1024):
-  // NV=2 (256 columns) 20.9 ms; NV=1 22.2 ms; NV=1 depth 8 22.7 ms; NV=2 with
-  // 4 CTAs/SM (64 registers) 45.7 ms; NV=1 with 6 CTAs/SM 30.4 ms -- all
-  // bitwise identical.  The kernel streams ~19.6 TB/s of L2->SM gathers.
+  // NV=2 (256 columns, 80 registers, 3 CTAs/SM) 20.9 ms; NV=1 22.2 ms; NV=1
+  // depth 8 22.7 ms; NV=2 capped at 64 registers (4 CTAs/SM) 45.7 ms; NV=1 at
+  // 6 CTAs/SM 30.4 ms -- all bitwise identical.  Letting NV=2 grow to 96
+  // registers (2 CTAs/SM) cost 30% on the bench's U~ (skewed row lengths).
+  // The kernel streams ~19.6 TB/s of L2->SM gathers.
   if (vec_ok && ncols > 32 * VW) {
     constexpr int NV = 2, PW = 32 * VW * NV;
     dim3 grid((unsigned)ceil_div(n_rows, 32), (unsigned)ceil_div(ncols, PW));
