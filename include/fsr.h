@@ -206,6 +206,36 @@ int fsr_filter_batch(fsr_ctx* ctx, int dtype, int64_t n, int64_t r, int u_sparse
 /* Top-k of every row of X (b x n): indices/values ordered by (-x, index). */
 int fsr_topk_rows(fsr_ctx* ctx, int dtype, int64_t b, int64_t n, const void* X, int64_t ldx,
                   int64_t topk, int64_t* top_idx, void* top_val);
+/* K8 alone: Zt (b x r, ld r) row j = w .* U[supp y_j]^T y_j (ranking.py:219-226
+ * _project; w may be NULL for no scaling).  Used by filter_pooled and the
+ * embedding (ranking.py:337-387). */
+int fsr_project_batch(fsr_ctx* ctx, int dtype, int64_t n, int64_t r, int u_sparse,
+                      const int64_t* u_indptr, const int32_t* u_indices, const void* u_values,
+                      const void* u_dense, int64_t ldu, const void* w, int64_t b,
+                      const int64_t* y_ptr, const int64_t* y_idx, const void* y_val, void* Zt);
+
+/* ---- K10: epilogues --------------------------------
+ * FSRw (ranking.py:256-274): X[j, :] += (1 - eta) .* (V Qsum[j, :]^T) for b
+ * score rows; V (n x d, ld ldv) the dataset vectors, Qsum (b x d, ld ldq) the
+ * per-query sums of region vectors, eta fp64 (n). */
+int fsr_fsrw_correct(fsr_ctx* ctx, int dtype, int64_t b, int64_t n, int64_t d, const void* V,
+                     int64_t ldv, const void* Qsum, int64_t ldq, const double* eta, void* X,
+                     int64_t ldx);
+/* pooled_basis (ranking.py:329-334): U_bar (N x r, ld ldb) = P U with P the
+ * (N x n) pooling CSR (values in dtype) and U dense or CSR as in
+ * fsr_filter_batch.  Accumulation in CSR order (scipy's). */
+int fsr_pool_rows(fsr_ctx* ctx, int dtype, int64_t N, const int64_t* p_indptr,
+                  const int32_t* p_indices, const void* p_values, int64_t n, int64_t r,
+                  int u_sparse, const int64_t* u_indptr, const int32_t* u_indices,
+                  const void* u_values, const void* u_dense, int64_t ldu, void* Ubar, int64_t ldb);
+/* pool (ranking.py:322-326) for b score rows: Xp (b x N, ld ldp) = X P^T. */
+int fsr_pool_scores(fsr_ctx* ctx, int dtype, int64_t b, int64_t N, const int64_t* p_indptr,
+                    const int32_t* p_indices, const void* p_values, const void* X, int64_t ldx,
+                    void* Xp, int64_t ldp);
+/* filter_pooled (ranking.py:337-353): Out (b x N, ld ldo) = Z A^T with A =
+ * U_bar (N x k, ld lda) and Z the scaled projections (b x k, ld ldz). */
+int fsr_dense_scores(fsr_ctx* ctx, int dtype, int64_t N, int64_t k, const void* A, int64_t lda,
+                     int64_t b, const void* Z, int64_t ldz, void* Out, int64_t ldo);
 
 #ifdef __cplusplus
 }

@@ -300,3 +300,68 @@ def observation_vector(regions: np.ndarray, data: np.ndarray, k: int, gamma: flo
 def rank(x: np.ndarray) -> np.ndarray:
     """Descending scores, ties by ascending index (``ranking.py:390-395``)."""
     return np.lexsort((np.arange(x.size), -x)).astype(np.int64)
+
+
+# ---------------------------------------------------------------------------
+# epilogues (SURVEY.md 8(f) row 3)
+# ---------------------------------------------------------------------------
+
+def project(U, w, y_idx: np.ndarray, y_val: np.ndarray) -> np.ndarray:
+    """w * U[supp y]^T y (``ranking.py:219-226`` scaled as in ``:244-246``)."""
+    r = U.shape[1]
+    if y_idx.size == 0:
+        z = np.zeros(r)
+    else:
+        z = np.asarray(U[y_idx].T @ y_val).ravel()
+    return z if w is None else w * z
+
+
+def fsrw_correct(x: np.ndarray, eta: np.ndarray, vectors: np.ndarray, regions: np.ndarray) -> np.ndarray:
+    """x + (1 - eta) * (V . sum of the query's region vectors) (``ranking.py:256-274``)."""
+    regions = np.atleast_2d(regions)
+    euclid = vectors @ regions.sum(axis=0)
+    return np.asarray(x, dtype=np.float64) + (1.0 - eta) * euclid
+
+
+def pooling_from_region_map(region_to_image: np.ndarray, n_images: int | None = None,
+                            weights: np.ndarray | None = None) -> sp.csr_matrix:
+    """(N, n) pooling CSR, one owning image per region (``ranking.py:300-311``)."""
+    r2i = np.asarray(region_to_image, dtype=np.int64)
+    n = r2i.size
+    n_images = int(r2i.max()) + 1 if n_images is None else n_images
+    data = np.ones(n) if weights is None else np.asarray(weights, dtype=np.float64)
+    return sp.csr_matrix(sp.csr_matrix((data, (r2i, np.arange(n))), shape=(n_images, n)), dtype=np.float64)
+
+
+def pool(P: sp.csr_matrix, x: np.ndarray) -> np.ndarray:
+    """Image scores P x (``ranking.py:322-326``)."""
+    return np.asarray(P @ np.asarray(x, dtype=np.float64)).ravel()
+
+
+def pooled_basis(P: sp.csr_matrix, U) -> np.ndarray:
+    """U_bar = P U as a dense (N, r) array (``ranking.py:329-334``)."""
+    Ub = P @ U
+    return Ub.toarray() if sp.issparse(Ub) else np.asarray(Ub)
+
+
+def filter_pooled(U, w: np.ndarray, y_idx: np.ndarray, y_val: np.ndarray, U_bar: np.ndarray) -> np.ndarray:
+    """U_bar (w * U[supp y]^T y), no uncovered copy (``ranking.py:337-353``)."""
+    return U_bar @ project(U, w, y_idx, y_val)
+
+
+def embedding(U, w: np.ndarray):
+    """Phi = h(lam)^{1/2} U^T (``ranking.py:356-365``)."""
+    if np.any(w < 0.0):
+        raise ValueError("transfer values must be nonnegative to take a square root")
+    scale = np.sqrt(w)
+    if sp.issparse(U):
+        return sp.diags(scale) @ U.T.tocsr()
+    return scale[:, None] * U.T
+
+
+def out_of_sample_similarity(z1: np.ndarray, z2: np.ndarray, phi, data: np.ndarray, k: int,
+                             gamma: float) -> float:
+    """(Phi psi(z1)) . (Phi psi(z2)), psi(z)_i = s(v_i | z) (``ranking.py:368-387``)."""
+    e1 = np.asarray(phi @ neighbor_similarities(z1, data, k, gamma)).ravel()
+    e2 = np.asarray(phi @ neighbor_similarities(z2, data, k, gamma)).ravel()
+    return float(e1 @ e2)

@@ -66,6 +66,14 @@ _SIGS = {
     "fsr_filter_batch": (_c_int, [_c_p, _c_int, _c_i64, _c_i64, _c_int, _c_p, _c_p, _c_p, _c_p, _c_i64, _c_p, _c_p,
                                   _c_i64, _c_p, _c_p, _c_p, _c_int, _c_p, _c_p, _c_i64, _c_p, _c_p]),
     "fsr_topk_rows": (_c_int, [_c_p, _c_int, _c_i64, _c_i64, _c_p, _c_i64, _c_i64, _c_p, _c_p]),
+    "fsr_project_batch": (_c_int, [_c_p, _c_int, _c_i64, _c_i64, _c_int, _c_p, _c_p, _c_p, _c_p, _c_i64, _c_p,
+                                   _c_i64, _c_p, _c_p, _c_p, _c_p]),
+    "fsr_fsrw_correct": (_c_int, [_c_p, _c_int, _c_i64, _c_i64, _c_i64, _c_p, _c_i64, _c_p, _c_i64, _c_p, _c_p,
+                                  _c_i64]),
+    "fsr_pool_rows": (_c_int, [_c_p, _c_int, _c_i64, _c_p, _c_p, _c_p, _c_i64, _c_i64, _c_int, _c_p, _c_p, _c_p,
+                               _c_p, _c_i64, _c_p, _c_i64]),
+    "fsr_pool_scores": (_c_int, [_c_p, _c_int, _c_i64, _c_i64, _c_p, _c_p, _c_p, _c_p, _c_i64, _c_p, _c_i64]),
+    "fsr_dense_scores": (_c_int, [_c_p, _c_int, _c_i64, _c_i64, _c_p, _c_i64, _c_i64, _c_p, _c_i64, _c_p, _c_i64]),
 }
 
 EXPORTED = tuple(_SIGS)

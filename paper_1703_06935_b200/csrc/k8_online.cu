@@ -51,7 +51,7 @@ __global__ void __launch_bounds__(256) project_kernel(int64_t r, int64_t b, cons
     __syncthreads();
   }
   for (int64_t c = threadIdx.x; c < r; c += blockDim.x) {
-    const T s = w[c] * z[c];
+    const T s = w ? w[c] * z[c] : z[c];
     z[c] = s;
     if (Zs) Zs[c * b + j] = s;
   }
@@ -126,7 +126,7 @@ __global__ void __launch_bounds__(256) project_smem_kernel(int64_t r, int64_t b,
     }
   }
   for (int64_t c = threadIdx.x; c < r; c += blockDim.x) {
-    const T s = w[c] * z[c];
+    const T s = w ? w[c] * z[c] : z[c];
     Zt[j * r + c] = s;
     if (Zs) Zs[c * b + j] = s;
   }
@@ -159,6 +159,32 @@ __global__ void copy_uncovered_kernel(int64_t n, const int64_t* __restrict__ y_p
   }
 }
 
+// K8 for b queries: Zt (b x r) = w .* U[supp y_j]^T y_j (w may be NULL: no
+// scaling); also Zs = Zt^T (r x b) when Zs != NULL (sparse U only).
+template <typename T>
+int launch_project(fsr_ctx* ctx, int64_t r, int64_t b, int u_sparse, const int64_t* u_indptr,
+                   const int32_t* u_indices, const T* u_values, const T* u_dense, int64_t ldu, const T* w,
+                   const int64_t* y_ptr, const int64_t* y_idx, const T* y_val, T* Zt, T* Zs) {
+  fsr::StageTimer timer(ctx, FSR_STAGE_PROJECT);
+  const size_t psmem = ((size_t)r * sizeof(T) + 15) / 16 * 16 + (size_t)kProjCap * (sizeof(T) + 4);
+  if (u_sparse && psmem <= 160 * 1024) {
+    static size_t configured[2] = {0, 0};
+    if (configured[sizeof(T) == 8] < psmem) {
+      FSR_CUDA(ctx, cudaFuncSetAttribute(project_smem_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)psmem));
+      configured[sizeof(T) == 8] = psmem;
+    }
+    project_smem_kernel<T><<<(unsigned)b, 256, psmem, ctx->stream>>>(r, b, u_indptr, u_indices, u_values, w, y_ptr,
+                                                                     y_idx, y_val, Zt, Zs);
+  } else if (u_sparse)
+    project_kernel<T, true><<<(unsigned)b, 256, 0, ctx->stream>>>(r, b, u_indptr, u_indices, u_values, nullptr, 0, w,
+                                                                  y_ptr, y_idx, y_val, Zt, Zs);
+  else
+    project_kernel<T, false><<<(unsigned)b, 256, 0, ctx->stream>>>(r, b, nullptr, nullptr, nullptr, u_dense, ldu, w,
+                                                                   y_ptr, y_idx, y_val, Zt, nullptr);
+  return fsr::launched(ctx, "project_kernel");
+}
+
 inline size_t align256(size_t x) { return (x + 255) / 256 * 256; }
 
 template <typename T>
@@ -178,26 +204,8 @@ int filter_impl(fsr_ctx* ctx, int64_t n, int64_t r, int u_sparse, const int64_t*
   T* Xout = X;
   if (!Xout) Xout = (T*)ws;
 
-  {
-  fsr::StageTimer timer(ctx, FSR_STAGE_PROJECT);
-  const size_t psmem = ((size_t)r * sizeof(T) + 15) / 16 * 16 + (size_t)kProjCap * (sizeof(T) + 4);
-  if (u_sparse && psmem <= 160 * 1024) {
-    static size_t configured[2] = {0, 0};
-    if (configured[sizeof(T) == 8] < psmem) {
-      FSR_CUDA(ctx, cudaFuncSetAttribute(project_smem_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)psmem));
-      configured[sizeof(T) == 8] = psmem;
-    }
-    project_smem_kernel<T><<<(unsigned)b, 256, psmem, ctx->stream>>>(r, b, u_indptr, u_indices, u_values, w, y_ptr,
-                                                                     y_idx, y_val, Zt, Zs);
-  } else if (u_sparse)
-    project_kernel<T, true><<<(unsigned)b, 256, 0, ctx->stream>>>(r, b, u_indptr, u_indices, u_values, nullptr, 0, w,
-                                                                  y_ptr, y_idx, y_val, Zt, Zs);
-  else
-    project_kernel<T, false><<<(unsigned)b, 256, 0, ctx->stream>>>(r, b, nullptr, nullptr, nullptr, u_dense, ldu, w,
-                                                                   y_ptr, y_idx, y_val, Zt, nullptr);
-  FSR_TRY(fsr::launched(ctx, "project_kernel"));
-  }
+  FSR_TRY(launch_project<T>(ctx, r, b, u_sparse, u_indptr, u_indices, u_values, u_dense, ldu, w, y_ptr, y_idx,
+                            y_val, Zt, Zs));
 
   if (u_sparse) {
     if (b == 1) {
@@ -277,4 +285,22 @@ int fsr_topk_rows(fsr_ctx* ctx, int dtype, int64_t b, int64_t n, const void* X, 
   return fsr::topk::launch<float>(ctx, b, n, (const float*)X, ldx, topk, top_idx, (float*)top_val);
 }
 
+int fsr_project_batch(fsr_ctx* ctx, int dtype, int64_t n, int64_t r, int u_sparse, const int64_t* u_indptr,
+                      const int32_t* u_indices, const void* u_values, const void* u_dense, int64_t ldu,
+                      const void* w, int64_t b, const int64_t* y_ptr, const int64_t* y_idx, const void* y_val,
+                      void* Zt) {
+  FSR_REQUIRE(ctx, n >= 1 && r >= 1 && b >= 0 && Zt, "project_batch: bad shape");
+  FSR_REQUIRE(ctx, u_sparse ? (u_indptr && u_indices && u_values) : (u_dense && ldu >= r),
+              "project_batch: missing U");
+  if (!b) return FSR_OK;
+  if (dtype == FSR_F64)
+    return launch_project<double>(ctx, r, b, u_sparse, u_indptr, u_indices, (const double*)u_values,
+                                  (const double*)u_dense, ldu, (const double*)w, y_ptr, y_idx, (const double*)y_val,
+                                  (double*)Zt, nullptr);
+  return launch_project<float>(ctx, r, b, u_sparse, u_indptr, u_indices, (const float*)u_values,
+                               (const float*)u_dense, ldu, (const float*)w, y_ptr, y_idx, (const float*)y_val,
+                               (float*)Zt, nullptr);
+}
+
 }  // extern "C"
+

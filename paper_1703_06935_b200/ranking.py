@@ -319,3 +319,307 @@ def top_k(dec, h: TransferFunction, ys, k: int = 100, copy_uncovered: bool | Non
 def empty_query_warning(y: ObservationVector) -> None:
     if y.is_empty:
         warnings.warn("query has no positive similarity to the dataset; empty observation")
+
+
+# ---------------------------------------------------------------------------
+# Epilogues around the online path (reference ranking.py:256-411, SURVEY.md
+# 8(f) row 3): FSRw, region->image pooling, the explicit embedding.  Device
+# kernels K10 (csrc/k10_epilogue.cu) and the K8 projection.
+# ---------------------------------------------------------------------------
+
+def _check_query_regions(query_regions, d: int) -> np.ndarray:
+    """Same validation as the reference (``ranking.py:156-165``)."""
+    regions = np.atleast_2d(np.asarray(query_regions, dtype=np.float64))
+    if regions.size == 0:
+        raise ValueError("query must contain at least one region vector")
+    if regions.shape[1] != d:
+        raise ValueError(f"query dimension {regions.shape[1]} != dataset dimension {d}")
+    norms = np.linalg.norm(regions, axis=1)
+    if np.any(np.abs(norms - 1.0) > NORM_TOL):
+        raise ValueError("query vectors must be unit-norm")
+    return regions
+
+
+def _host_vectors(data) -> np.ndarray:
+    """Dataset vectors of a reference ``DescriptorSet`` (``.vectors``) or an array."""
+    v = getattr(data, "vectors", data)
+    if hasattr(v, "detach"):
+        return v
+    return np.asarray(v, dtype=np.float64)
+
+
+def _device_vectors(data, dtype, device):
+    import torch
+
+    v = _host_vectors(data)
+    if hasattr(v, "detach"):
+        return v.to(device=device, dtype=dtype).contiguous()
+    cache = _device_vectors.__dict__.setdefault("_cache", {})
+    key = (id(data), dtype, str(device))
+    hit = cache.get(key)
+    if hit is None or hit[0] is not data:
+        hit = cache[key] = (data, torch.as_tensor(v).to(device=device, dtype=dtype).contiguous())
+    return hit[1]
+
+
+def fsrw_correct_device(X, dec: SpectralDecomposition, V, Qsum):
+    """In place: X[j] += (1 - eta) * (V Qsum[j]) for the (b x n) device scores X."""
+    ctx = N.Context.get(X.device)
+    b, n = X.shape
+    if V.shape[0] != n or dec.n != n or Qsum.shape != (b, V.shape[1]):
+        raise ValueError("score rows, dataset and decomposition sizes must agree")
+    ctx.call("fsrw_correct", N.dtype_code(X.dtype), b, n, V.shape[1], N.ptr(V), V.stride(0), N.ptr(Qsum),
+             Qsum.stride(0), N.ptr(dec.eta_device), N.ptr(X), X.stride(0))
+    return X
+
+
+def fsrw_correct(x, dec, data, query_regions) -> np.ndarray:
+    """x + (1 - eta) * (V . sum of query regions) (``ranking.py:256-274``), on the device."""
+    import torch
+
+    dec = _as_device_dec(dec)
+    V_host = _host_vectors(data)
+    n, d = V_host.shape
+    regions = _check_query_regions(query_regions, d)
+    x = np.asarray(x, dtype=np.float64)
+    if x.shape != (n,) or dec.n != n:
+        raise ValueError("score vector, dataset and decomposition sizes must agree")
+    dev = dec.eta_device.device
+    V = _device_vectors(data, dec.dtype, dev)
+    X = torch.as_tensor(x).to(device=dev, dtype=dec.dtype).reshape(1, n).contiguous()
+    Qs = torch.as_tensor(regions.sum(axis=0)).to(device=dev, dtype=dec.dtype).reshape(1, d)
+    fsrw_correct_device(X, dec, V, Qs)
+    return X[0].double().cpu().numpy()
+
+
+@dataclass(frozen=True, eq=False)
+class PoolingMatrix:
+    """Sparse (N, n) region->image map (``ranking.py:277-319``): every region
+    column owned by exactly one image row, finite nonnegative weights."""
+
+    csr: object
+
+    def __post_init__(self):
+        import scipy.sparse as sp
+
+        mat = sp.csr_matrix(self.csr, dtype=np.float64)
+        counts = np.asarray((mat != 0).sum(axis=0)).ravel()
+        if np.any(counts != 1):
+            raise ValueError("each region must belong to exactly one image")
+        if not np.all(np.isfinite(mat.data)) or (mat.nnz and mat.data.min() < 0.0):
+            raise ValueError("pooling weights must be finite and nonnegative")
+        object.__setattr__(self, "csr", mat)
+
+    @classmethod
+    def identity(cls, n: int) -> "PoolingMatrix":
+        import scipy.sparse as sp
+
+        return cls(sp.identity(n, dtype=np.float64, format="csr"))
+
+    @classmethod
+    def from_region_map(cls, region_to_image, n_images: int | None = None, weights=None) -> "PoolingMatrix":
+        import scipy.sparse as sp
+
+        r2i = np.asarray(region_to_image, dtype=np.int64)
+        n = r2i.size
+        n_images = int(r2i.max()) + 1 if n_images is None else n_images
+        data = np.ones(n) if weights is None else np.asarray(weights, dtype=np.float64)
+        return cls(sp.csr_matrix((data, (r2i, np.arange(n))), shape=(n_images, n)))
+
+    @property
+    def n_images(self) -> int:
+        return self.csr.shape[0]
+
+    @property
+    def n_regions(self) -> int:
+        return self.csr.shape[1]
+
+    def device(self, dtype, device):
+        """(indptr int64, indices int32, values dtype) of the CSR on the device (cached)."""
+        import torch
+
+        cache = self.__dict__.setdefault("_dev", {})
+        key = (dtype, str(device))
+        if key not in cache:
+            m = self.csr
+            m.sort_indices()
+            cache[key] = (torch.as_tensor(m.indptr.astype(np.int64)).to(device),
+                          torch.as_tensor(m.indices.astype(np.int32)).to(device),
+                          torch.as_tensor(m.data).to(device=device, dtype=dtype))
+        return cache[key]
+
+
+def pool_device(pooling: PoolingMatrix, X):
+    """(b x N) image scores of the (b x n_regions) device scores X."""
+    import torch
+
+    b, n = X.shape
+    if n != pooling.n_regions:
+        raise ValueError(f"score vector length {n} != {pooling.n_regions} regions")
+    ip, ix, pv = pooling.device(X.dtype, X.device)
+    out = torch.empty(b, pooling.n_images, dtype=X.dtype, device=X.device)
+    N.Context.get(X.device).call("pool_scores", N.dtype_code(X.dtype), b, pooling.n_images, N.ptr(ip), N.ptr(ix),
+                                 N.ptr(pv), N.ptr(X), X.stride(0), N.ptr(out), out.stride(0))
+    return out
+
+
+def pool(pooling: PoolingMatrix, x) -> np.ndarray:
+    """Image scores P x (``ranking.py:322-326``), on the device."""
+    import torch
+
+    x = np.asarray(x, dtype=np.float64)
+    if x.shape != (pooling.n_regions,):
+        raise ValueError(f"score vector length {x.shape} != {pooling.n_regions} regions")
+    dev = torch.device("cuda", torch.cuda.current_device())
+    X = torch.as_tensor(x).to(dev).reshape(1, -1)
+    return pool_device(pooling, X)[0].cpu().numpy()
+
+
+def pooled_basis_device(pooling: PoolingMatrix, dec: SpectralDecomposition):
+    """U_bar = P U (N x r) on the device (``ranking.py:329-334``)."""
+    import torch
+
+    if pooling.n_regions != dec.n:
+        raise ValueError("pooling width does not match the decomposition")
+    dev = dec.eta_device.device
+    ip, ix, pv = pooling.device(dec.dtype, dev)
+    Ub = torch.empty(pooling.n_images, dec.r, dtype=dec.dtype, device=dev)
+    U = dec.U_device
+    if dec.is_sparse:
+        uargs = (1, N.ptr(U.indptr), N.ptr(U.indices), N.ptr(U.values), N.ptr(None), 0)
+    else:
+        uargs = (0, N.ptr(None), N.ptr(None), N.ptr(None), N.ptr(U), U.stride(0))
+    N.Context.get(dev).call("pool_rows", N.dtype_code(dec.dtype), pooling.n_images, N.ptr(ip), N.ptr(ix), N.ptr(pv),
+                            dec.n, dec.r, *uargs, N.ptr(Ub), Ub.stride(0))
+    return Ub
+
+
+def pooled_basis(pooling: PoolingMatrix, dec) -> np.ndarray:
+    """Precomputed (N, r) pooled basis (``ranking.py:329-334``), as a host array."""
+    dec = _as_device_dec(dec)
+    return pooled_basis_device(pooling, dec).double().cpu().numpy()
+
+
+def _project_device(dec: SpectralDecomposition, w, queries: DeviceQueries):
+    import torch
+
+    dev = dec.eta_device.device
+    Zt = torch.empty(queries.b, dec.r, dtype=dec.dtype, device=dev)
+    U = dec.U_device
+    if dec.is_sparse:
+        uargs = (1, N.ptr(U.indptr), N.ptr(U.indices), N.ptr(U.values), N.ptr(None), 0)
+    else:
+        uargs = (0, N.ptr(None), N.ptr(None), N.ptr(None), N.ptr(U), U.stride(0))
+    N.Context.get(dev).call("project_batch", N.dtype_code(dec.dtype), dec.n, dec.r, *uargs, N.ptr(w), queries.b,
+                            N.ptr(queries.y_ptr), N.ptr(queries.y_idx), N.ptr(queries.y_val), N.ptr(Zt))
+    return Zt
+
+
+def filter_pooled_device(dec: SpectralDecomposition, h: TransferFunction, queries: DeviceQueries, U_bar):
+    """(b x N) image scores U_bar h(Lambda) U^T y_j; no uncovered copy (``ranking.py:337-353``)."""
+    import torch
+
+    if queries.batch.size != dec.n:
+        raise ValueError(f"observation size {queries.batch.size} != decomposition size {dec.n}")
+    if U_bar.shape[1] != dec.r:
+        raise ValueError("pooled basis width does not match the decomposition")
+    Zt = _project_device(dec, _weights_device(dec, h), queries)
+    out = torch.empty(queries.b, U_bar.shape[0], dtype=dec.dtype, device=Zt.device)
+    N.Context.get(Zt.device).call("dense_scores", N.dtype_code(dec.dtype), U_bar.shape[0], dec.r, N.ptr(U_bar),
+                                  U_bar.stride(0), queries.b, N.ptr(Zt), Zt.stride(0), N.ptr(out), out.stride(0))
+    return out
+
+
+def filter_pooled(dec, h: TransferFunction, y: ObservationVector, U_bar) -> np.ndarray:
+    """Image scores directly, U_bar h(Lambda) U^T y (``ranking.py:337-353``), on the device."""
+    import torch
+
+    dec = _as_device_dec(dec)
+    if y.size != dec.n:
+        raise ValueError(f"observation size {y.size} != decomposition size {dec.n}")
+    dev = dec.eta_device.device
+    Ub = U_bar if hasattr(U_bar, "detach") else torch.as_tensor(np.asarray(U_bar, dtype=np.float64))
+    Ub = Ub.to(device=dev, dtype=dec.dtype).contiguous()
+    q = DeviceQueries(QueryBatch.from_vectors([y]), dec.dtype, dev)
+    return filter_pooled_device(dec, h, q, Ub)[0].double().cpu().numpy()
+
+
+@dataclass(frozen=True, eq=False)
+class RankingResult:
+    """Region scores, pooled image scores and the image order (``ranking.py:398-411``)."""
+
+    x: np.ndarray
+    x_pooled: np.ndarray
+    order: np.ndarray
+
+    @classmethod
+    def from_scores(cls, x, pooling: PoolingMatrix | None = None) -> "RankingResult":
+        x = np.asarray(x, dtype=np.float64)
+        x_pooled = pool(pooling, x) if pooling is not None else x
+        return cls(x=x, x_pooled=x_pooled, order=rank(x_pooled))
+
+
+class Embedding:
+    """Phi = h(Lambda)^{1/2} U^T (``ranking.py:356-365``) bound to a device
+    decomposition: ``phi @ psi`` runs the K8 projection with weights sqrt(w);
+    ``matrix()`` materialises the reference's object (scipy CSR or ndarray)."""
+
+    def __init__(self, dec: SpectralDecomposition, h: TransferFunction):
+        import torch
+
+        w = transfer_values(h, dec.eigenvalues)
+        if np.any(w < 0.0):
+            raise ValueError("transfer values must be nonnegative to take a square root")
+        self.dec = dec
+        self.scale = np.sqrt(w)
+        self.scale_device = torch.as_tensor(self.scale).to(device=dec.eta_device.device, dtype=dec.dtype)
+
+    @property
+    def shape(self):
+        return (self.dec.r, self.dec.n)
+
+    def __matmul__(self, psi) -> np.ndarray:
+        y = psi if isinstance(psi, ObservationVector) else ObservationVector.from_dense(psi)
+        if y.size != self.dec.n:
+            raise ValueError(f"vector size {y.size} != {self.dec.n}")
+        q = DeviceQueries(QueryBatch.from_vectors([y]), self.dec.dtype, self.dec.eta_device.device)
+        return _project_device(self.dec, self.scale_device, q)[0].double().cpu().numpy()
+
+    def matrix(self):
+        import scipy.sparse as sp
+
+        if self.dec.is_sparse:
+            U = self.dec.U_device
+            vals = (U.values.double() * self.scale_device.double()[U.indices.long()]).cpu().numpy()
+            m = sp.csr_matrix((vals, U.indices.cpu().numpy(), U.indptr.cpu().numpy()), shape=(self.dec.n, self.dec.r))
+            return m.T.tocsr()
+        U = self.dec.U_device.double() * self.scale_device.double()[None, :]
+        return U.T.contiguous().cpu().numpy()
+
+
+def embedding(dec, h: TransferFunction) -> Embedding:
+    """Explicit feature map Phi = h(Lambda)^{1/2} U^T (``ranking.py:356-365``)."""
+    return Embedding(_as_device_dec(dec), h)
+
+
+def out_of_sample_similarity(z1, z2, phi, data, k: int, gamma: float) -> float:
+    """(Phi psi(z1)) . (Phi psi(z2)) with psi(z)_i = s(v_i | z) on the k-NN of z
+    (``ranking.py:368-387``); psi on the device (knn.observation_batch_device)."""
+    import torch
+
+    from .knn import observation_batch_device
+
+    V_host = _host_vectors(data)
+    n = V_host.shape[0]
+    if k < 1 or k > n:
+        raise ValueError(f"k must lie in [1, n], got {k}")
+    if gamma <= 0:
+        raise ValueError("gamma must be positive")
+    dev = phi.dec.eta_device.device if isinstance(phi, Embedding) else torch.device("cuda", torch.cuda.current_device())
+    V = _device_vectors(data, torch.float64, dev)
+    Z = torch.as_tensor(np.stack([np.asarray(z1, dtype=np.float64), np.asarray(z2, dtype=np.float64)])).to(dev)
+    ptr, idx, val = observation_batch_device(Z, V, k, gamma, cap=k)
+    psis = [ObservationVector(n, idx[ptr[j]:ptr[j + 1]], val[ptr[j]:ptr[j + 1]], cap=max(1, k)) for j in (0, 1)]
+    e1 = np.asarray(phi @ psis[0] if isinstance(phi, Embedding) else phi @ psis[0].to_dense()).ravel()
+    e2 = np.asarray(phi @ psis[1] if isinstance(phi, Embedding) else phi @ psis[1].to_dense()).ravel()
+    return float(e1 @ e2)

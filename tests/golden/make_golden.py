@@ -165,8 +165,55 @@ def c1_case(n_x: int = 20):
     )
 
 
+def epilogue_case(n_q: int = 5, region_per_image: int = 4):
+    """FSRw, pooling and the embedding on the C1 decomposition."""
+    cfg = CONFIGS["C1"]
+    data, queries, _ = cluster_descriptors(cfg)
+    ds = DescriptorSet(data)
+    W = graph.build_mutual_knn_graph(ds, cfg.k, cfg.gamma)
+    S = graph.normalize_adjacency(W, graph.degrees(W))
+    dec = spectral.decompose(S, cfg.r, p=cfg.p, q=cfg.q, seed=0)
+    sdec = spectral.sparsify(dec, cfg.tau)
+    h = ranking.h_alpha(cfg.alpha)
+    n = cfg.n
+    rng = np.random.default_rng(11)
+    r2i = np.arange(n) // region_per_image
+    wts = rng.uniform(0.5, 1.5, n)
+    P = ranking.PoolingMatrix.from_region_map(r2i, weights=wts)
+    out = {"r2i": r2i, "pool_w": wts}
+    for tag, d in (("a", dec), ("s", sdec)):
+        xs, xw, xp, xf, order = [], [], [], [], []
+        Ub = ranking.pooled_basis(P, d)
+        for j in range(n_q):
+            y = ranking.observation_vector(queries[j], ds, cfg.y_top, cfg.gamma)
+            x = ranking.filter(d, h, y)
+            xs.append(x)
+            xw.append(ranking.fsrw_correct(x, d, ds, queries[j]))
+            xp.append(ranking.pool(P, x))
+            xf.append(ranking.filter_pooled(d, h, y, Ub))
+            order.append(ranking.RankingResult.from_scores(x, P).order[:100])
+        out[f"{tag}_fsrw"] = np.array(xw)
+        out[f"{tag}_pool"] = np.array(xp)
+        out[f"{tag}_filter_pooled"] = np.array(xf)
+        out[f"{tag}_pooled_order"] = np.array(order)
+        out[f"{tag}_ubar_head"] = Ub[:200].copy()
+        out[f"{tag}_ubar_rowsum"] = Ub.sum(axis=1)
+        out[f"{tag}_ubar_colsum"] = Ub.sum(axis=0)
+        phi = ranking.embedding(d, h)
+        sims = [ranking.out_of_sample_similarity(queries[a], queries[b], phi, ds, cfg.y_top, cfg.gamma)
+                for a, b in ((0, 1), (2, 3), (4, 4), (5, 9))]
+        out[f"{tag}_oos"] = np.array(sims)
+    np.savez_compressed(os.path.join(HERE, "epi.npz"), **out)
+
+
 if __name__ == "__main__":
-    gaussian_cases()
-    kat_cases()
-    c1_case()
+    which = sys.argv[1:] or ["gaussian", "kat", "c1", "epi"]
+    if "gaussian" in which:
+        gaussian_cases()
+    if "kat" in which:
+        kat_cases()
+    if "c1" in which:
+        c1_case()
+    if "epi" in which:
+        epilogue_case()
     print("ok")

@@ -105,3 +105,41 @@ def test_c1_oracle_matches_reference(golden):
     assert flat.size == int(g["sparse_nnz"])
     import hashlib
     assert hashlib.sha256(flat.astype(np.int64).tobytes()).hexdigest() == str(g["sparse_hash"])
+
+
+def test_c1_oracle_epilogues_match_reference(golden):
+    """FSRw, pooling, filter_pooled and the embedding similarity (ranking.py:256-387)
+    restated by the oracle on its own C1 decomposition vs the reference's outputs."""
+    import os
+    import sys
+
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    from paper_1703_06935_b200.workloads import CONFIGS, cluster_descriptors
+
+    g, e = golden("c1"), golden("epi")
+    cfg = CONFIGS["C1"]
+    data, queries, _ = cluster_descriptors(cfg)
+    _, S = c1_matrices(g)
+    n, r, p, q, tau, seed = (int(v) for v in g["params"])
+    U, lam, eta = O.decompose(S, r, p=p, q=q, seed=seed)
+    Us, eta_s = O.sparsify(U, tau)
+    w = O.transfer_values(O.h_alpha(float(g["alpha"])), lam)
+    P = O.pooling_from_region_map(e["r2i"], weights=e["pool_w"])
+    for tag, UU, et in (("a", U, eta), ("s", Us, eta_s)):
+        Ub = O.pooled_basis(P, UU)
+        np.testing.assert_allclose(Ub[:200], e[f"{tag}_ubar_head"], rtol=1e-8, atol=1e-12)
+        np.testing.assert_allclose(Ub.sum(axis=1), e[f"{tag}_ubar_rowsum"], rtol=1e-8, atol=1e-11)
+        for j in range(e[f"{tag}_fsrw"].shape[0]):
+            yi, yv = O.observation_vector(queries[j], data, cfg.y_top, cfg.gamma)
+            x = O.filter_scores(UU, lam, et, w, yi, yv)
+            np.testing.assert_allclose(O.fsrw_correct(x, et, data, queries[j]), e[f"{tag}_fsrw"][j],
+                                       rtol=1e-8, atol=1e-12)
+            xp = O.pool(P, x)
+            np.testing.assert_allclose(xp, e[f"{tag}_pool"][j], rtol=1e-8, atol=1e-12)
+            np.testing.assert_array_equal(O.rank(xp)[:100], e[f"{tag}_pooled_order"][j])
+            np.testing.assert_allclose(O.filter_pooled(UU, w, yi, yv, Ub), e[f"{tag}_filter_pooled"][j],
+                                       rtol=1e-8, atol=1e-12)
+        phi = O.embedding(UU, w)
+        sims = [O.out_of_sample_similarity(queries[a], queries[b], phi, data, cfg.y_top, cfg.gamma)
+                for a, b in ((0, 1), (2, 3), (4, 4), (5, 9))]
+        np.testing.assert_allclose(sims, e[f"{tag}_oos"], rtol=1e-8)
