@@ -214,6 +214,13 @@ int fsr_project_batch(fsr_ctx* ctx, int dtype, int64_t n, int64_t r, int u_spars
                       const void* u_dense, int64_t ldu, const void* w, int64_t b,
                       const int64_t* y_ptr, const int64_t* y_idx, const void* y_val, void* Zt);
 
+/* ---- K11: connected components  (graph.py:215-250) ----------------------
+ * root[i] = the smallest vertex index of i's connected component, every
+ * stored entry counting as an edge.  Host-synchronous (iterates to a fixed
+ * point); *rounds_host (may be NULL) = hook/jump rounds used. */
+int fsr_connected_components(fsr_ctx* ctx, int64_t n, const int64_t* indptr, const int32_t* indices,
+                             int64_t* root, int64_t* rounds_host);
+
 /* ---- K10: epilogues --------------------------------
  * FSRw (ranking.py:256-274): X[j, :] += (1 - eta) .* (V Qsum[j, :]^T) for b
  * score rows; V (n x d, ld ldv) the dataset vectors, Qsum (b x d, ld ldq) the

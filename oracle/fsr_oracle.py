@@ -365,3 +365,83 @@ def out_of_sample_similarity(z1: np.ndarray, z2: np.ndarray, phi, data: np.ndarr
     e1 = np.asarray(phi @ neighbor_similarities(z1, data, k, gamma)).ravel()
     e2 = np.asarray(phi @ neighbor_similarities(z2, data, k, gamma)).ravel()
     return float(e1 @ e2)
+
+
+# ---------------------------------------------------------------------------
+# components and the blockwise decomposition
+# ---------------------------------------------------------------------------
+
+def mix_seed(seed: int, salt: int) -> int:
+    """splitmix64 finalizer of (seed, salt) (``spectral.py:47-52``)."""
+    z = (seed ^ ((salt + 1) * 0x9E3779B97F4A7C15)) & MASK64
+    z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & MASK64
+    z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & MASK64
+    return (z ^ (z >> 31)) & MASK64
+
+
+def connected_components(W: sp.csr_matrix):
+    """(labels, sizes, order) by union-find, components by size desc then
+    smallest vertex (``graph.py:215-250``)."""
+    n = W.shape[0]
+    parent = np.arange(n, dtype=np.int64)
+
+    def find(i):
+        root = i
+        while parent[root] != root:
+            root = parent[root]
+        while parent[i] != root:
+            parent[i], i = root, parent[i]
+        return root
+
+    coo = W.tocoo()
+    for i, j in zip(coo.row.tolist(), coo.col.tolist()):
+        if i < j:
+            ri, rj = find(i), find(j)
+            if ri != rj:
+                parent[max(ri, rj)] = min(ri, rj)
+    roots = np.array([find(i) for i in range(n)], dtype=np.int64)
+    uniq, inverse, counts = np.unique(roots, return_inverse=True, return_counts=True)
+    rank = np.lexsort((uniq, -counts))
+    label_of = np.empty_like(rank)
+    label_of[rank] = np.arange(rank.size)
+    labels = label_of[inverse]
+    return labels, counts[rank], np.argsort(labels, kind="stable")
+
+
+def exact_eigenpairs(A: sp.csr_matrix, r: int | None = None):
+    """Dense eigh, top r descending (stable), sign rule (``spectral.py:200-243``)."""
+    vals, vecs = np.linalg.eigh(A.toarray())
+    r = vals.size if r is None else r
+    idx = np.argsort(-vals, kind="stable")[:r]
+    U = sign_fix(vecs[:, idx])
+    return U, vals[idx], row_norms(U)
+
+
+def decompose_blockwise(A: sp.csr_matrix, labels: np.ndarray, r: int, rho: int, p: int = 10, q: int = 4,
+                        seed: int = 0, dense_guard: int = 4096):
+    """Per-component decomposition with a global top-r merge (``spectral.py:312-390``).
+    Returns (U dense, eigenvalues, eta, all_exact, truncated)."""
+    import math
+
+    n = A.shape[0]
+    blocks = []
+    all_exact = True
+    for comp in range(int(labels.max()) + 1):
+        v = np.flatnonzero(labels == comp)
+        sub = sp.csr_matrix(A[v][:, v])
+        if v.size <= rho:
+            U, lam, _ = exact_eigenpairs(sub)
+        else:
+            r_l = min(max(rho, math.ceil(r * v.size / n)), v.size)
+            U, lam, _ = decompose(sub, r_l, p=p, q=q, seed=seed if comp == 0 else mix_seed(seed, comp))
+            all_exact = False
+        blocks.append((v, U, lam))
+    lams = np.concatenate([b[2] for b in blocks])
+    comps = np.concatenate([np.full(b[2].size, c) for c, b in enumerate(blocks)])
+    cols = np.concatenate([np.arange(b[2].size) for b in blocks])
+    keep = np.lexsort((cols, comps, -lams))[: min(r, lams.size)]
+    U = np.zeros((n, keep.size))
+    for out_col, cand in enumerate(keep):
+        v, Ub, _ = blocks[comps[cand]]
+        U[v, out_col] = Ub[:, cols[cand]]
+    return U, lams[keep], row_norms(U), all_exact, keep.size < lams.size

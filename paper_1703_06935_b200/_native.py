@@ -73,6 +73,7 @@ _SIGS = {
     "fsr_pool_rows": (_c_int, [_c_p, _c_int, _c_i64, _c_p, _c_p, _c_p, _c_i64, _c_i64, _c_int, _c_p, _c_p, _c_p,
                                _c_p, _c_i64, _c_p, _c_i64]),
     "fsr_pool_scores": (_c_int, [_c_p, _c_int, _c_i64, _c_i64, _c_p, _c_p, _c_p, _c_p, _c_i64, _c_p, _c_i64]),
+    "fsr_connected_components": (_c_int, [_c_p, _c_i64, _c_p, _c_p, _c_p, _c_p]),
     "fsr_dense_scores": (_c_int, [_c_p, _c_int, _c_i64, _c_i64, _c_p, _c_i64, _c_i64, _c_p, _c_i64, _c_p, _c_i64]),
 }
 

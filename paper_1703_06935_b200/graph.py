@@ -6,8 +6,9 @@ S_ij = (w_ij s_i) s_j with s = 1/sqrt(d), 0 where d == 0 -- the same
 operation order as the reference, so S is bitwise equal in fp64.
 
 ``ComponentLabeling`` mirrors the reference container (``graph.py:168-212``)
-because every ``SpectralDecomposition`` carries one; the hot path only uses
-the trivial labeling.
+because every ``SpectralDecomposition`` carries one; ``connected_components``
+(``graph.py:215-250``) labels an adjacency on the device (kernel K11) for
+``spectral.decompose_blockwise``.
 """
 
 from __future__ import annotations
@@ -98,3 +99,29 @@ def normalize_adjacency(adjacency, degree, dtype="float64", device=None) -> Spar
     ctx.call("csr_normalize", N.dtype_code(dt), A.n, 0, N.ptr(W.indptr), N.ptr(W.indices), N.ptr(W.values),
              N.ptr(deg), N.ptr(out))
     return SparseSymmetricMatrix.from_device(DeviceCSR(W.indptr, W.indices, out, W.shape))
+
+
+def connected_components(adjacency) -> ComponentLabeling:
+    """Connected components ordered by decreasing size, ties by the smallest
+    vertex index (``graph.py:215-250``); isolated vertices are singletons.
+
+    The roots (smallest vertex of each component) come from the K11 kernel;
+    numbering, sizes and the block order follow the reference's rules.
+    """
+    import torch
+
+    A = SparseSymmetricMatrix.coerce(adjacency)
+    if A._csr is not None:
+        A.require_adjacency()
+    W = A.device(torch.float64)
+    n = A.n
+    roots = torch.empty(n, dtype=torch.int64, device=W.device)
+    N.Context.get(W.device).call("connected_components", n, N.ptr(W.indptr), N.ptr(W.indices), N.ptr(roots),
+                                 N.ptr(None))
+    uniq, inverse, counts = torch.unique(roots, sorted=True, return_inverse=True, return_counts=True)
+    rank = torch.argsort(-counts, stable=True)          # size desc, then smallest root (uniq is ascending)
+    label_of = torch.empty_like(rank)
+    label_of[rank] = torch.arange(rank.numel(), device=rank.device)
+    labels = label_of[inverse]
+    order = torch.argsort(labels, stable=True)          # ascending vertex index inside each block
+    return ComponentLabeling(labels.cpu().numpy(), counts[rank].cpu().numpy(), order.cpu().numpy())

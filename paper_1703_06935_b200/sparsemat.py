@@ -177,6 +177,30 @@ class SparseSymmetricMatrix:
     def diagonal(self) -> np.ndarray:
         return self.csr.diagonal()
 
+    def submatrix(self, index) -> "SparseSymmetricMatrix":
+        """Principal submatrix on the given sorted vertex indices (``sparsemat.py:82-86``),
+        extracted on the device (fp64 values); canonical CSR, device-resident."""
+        import torch
+
+        W = self.device(torch.float64)
+        dev = W.device
+        idx = torch.as_tensor(np.asarray(index, dtype=np.int64)).to(dev)
+        m = int(idx.numel())
+        newid = torch.full((self.n,), -1, dtype=torch.int64, device=dev)
+        newid[idx] = torch.arange(m, device=dev)
+        starts = W.indptr[idx]
+        lens = W.indptr[idx + 1] - starts
+        total = int(lens.sum())
+        rows = torch.repeat_interleave(torch.arange(m, device=dev), lens)
+        first = torch.cumsum(lens, 0) - lens
+        pos = torch.repeat_interleave(starts - first, lens) + torch.arange(total, device=dev)
+        cols = newid[W.indices[pos].long()]
+        keep = cols >= 0
+        rows, cols, vals = rows[keep], cols[keep], W.values[pos][keep]
+        indptr = torch.zeros(m + 1, dtype=torch.int64, device=dev)
+        indptr[1:] = torch.cumsum(torch.bincount(rows, minlength=m), 0)
+        return SparseSymmetricMatrix.from_device(DeviceCSR(indptr, cols.to(torch.int32), vals.contiguous(), (m, m)))
+
     def require_adjacency(self) -> None:
         if np.any(self.diagonal() != 0.0):
             raise ValueError("adjacency must have a zero diagonal")

@@ -337,6 +337,159 @@ def decompose(A, r: int, p: int = DEFAULT_OVERSAMPLING, q: int = DEFAULT_POWER_I
     return dec
 
 
+def mix_seed(seed: int, salt: int) -> int:
+    """Decorrelated 64-bit stream seed, splitmix64 finalizer (``spectral.py:47-52``)."""
+    z = (seed ^ ((salt + 1) * 0x9E3779B97F4A7C15)) & _MASK64
+    z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & _MASK64
+    z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & _MASK64
+    return (z ^ (z >> 31)) & _MASK64
+
+
+def _signfix_eta(ctx, dt, U):
+    """In place: sign rule of spectral.py:133-138 on U's columns; returns eta (row norms)."""
+    import torch
+
+    n, r = U.shape
+    best_abs = torch.empty(r, dtype=torch.float64, device=U.device)
+    best_row = torch.empty(r, dtype=torch.int64, device=U.device)
+    best_val = torch.empty(r, dtype=torch.float64, device=U.device)
+    ctx.call("col_absmax", dt, n, r, N.ptr(U), U.stride(0), 0, N.ptr(best_abs), N.ptr(best_row), N.ptr(best_val))
+    eta = torch.empty(n, dtype=torch.float64, device=U.device)
+    ctx.call("apply_signs_rownorm", dt, n, r, N.ptr(U), U.stride(0), N.ptr(best_val), N.ptr(eta))
+    return eta
+
+
+def _dense_eigenpairs(A: SparseSymmetricMatrix, r: int, dtype, device=None):
+    """Top-r eigenpairs of the dense A on the device (cuSOLVER syevd, fp64),
+    descending with the stable order of spectral.py:141-144, sign-fixed."""
+    import torch
+
+    W = A.device(torch.float64, device)
+    n = A.n
+    dev = W.device
+    ctx = N.Context.get(dev)
+    D = torch.zeros(n, n, dtype=torch.float64, device=dev)
+    if W.nnz:
+        rows = torch.repeat_interleave(torch.arange(n, device=dev), W.indptr[1:] - W.indptr[:-1])
+        D[rows, W.indices.long()] = W.values
+    lam = np.empty(r, dtype=np.float64)
+    V = torch.empty(n, r, dtype=torch.float64, device=dev)
+    ctx.call("eigh_desc", n, N.ptr(D), r, lam.ctypes.data_as(N._c_dp), N.ptr(V))
+    del D
+    dt_t = N.torch_dtype(dtype)
+    U = V if dt_t == torch.float64 else V.to(dt_t)
+    eta = _signfix_eta(ctx, N.dtype_code(dt_t), U)
+    return U, lam, eta
+
+
+def exact_eigendecomposition(A, max_n: int = DENSE_GUARD, dtype="float64", device=None) -> SpectralDecomposition:
+    """Full dense symmetric eigendecomposition (``spectral.py:200-220``), on the device."""
+    A = SparseSymmetricMatrix.coerce(A)
+    n = A.n
+    if n > max_n:
+        raise NumericalError(f"dense decomposition guarded at n <= {max_n} (got n={n}); "
+                             "use the randomized path instead")
+    U, lam, eta = _dense_eigenpairs(A, n, dtype, device)
+    return SpectralDecomposition(U, lam, eta, ComponentLabeling.trivial(n), Variant.EXACT, Provenance(r=n))
+
+
+def rank_r_decomposition(A, r: int, max_n: int = DENSE_GUARD, dtype="float64", device=None) -> SpectralDecomposition:
+    """Exact decomposition truncated to the r algebraically largest pairs (``spectral.py:223-243``)."""
+    A = SparseSymmetricMatrix.coerce(A)
+    n = A.n
+    if r < 1 or r > n:
+        raise ValueError(f"r must lie in [1, n], got {r} for n={n}")
+    if n > max_n:
+        raise NumericalError(f"dense decomposition guarded at n <= {max_n} (got n={n}); "
+                             "use the randomized path instead")
+    U, lam, eta = _dense_eigenpairs(A, r, dtype, device)
+    return SpectralDecomposition(U, lam, eta, ComponentLabeling.trivial(n),
+                                 Variant.EXACT if r == n else Variant.RANK_R, Provenance(r=r))
+
+
+def truncate_rank(dec: SpectralDecomposition, r: int) -> SpectralDecomposition:
+    """Drop trailing eigenpairs (``spectral.py:246-266``)."""
+    import torch
+
+    if dec.variant is Variant.SPARSE:
+        raise ValueError("cannot truncate a sparsified decomposition")
+    if r < 1 or r > dec.r:
+        raise ValueError(f"r must lie in [1, {dec.r}], got {r}")
+    if r == dec.r:
+        return dec
+    U = dec.U_device[:, :r].contiguous()
+    eta = torch.empty(dec.n, dtype=torch.float64, device=U.device)
+    N.Context.get(U.device).call("row_norms", N.dtype_code(U.dtype), dec.n, r, N.ptr(U), U.stride(0), N.ptr(eta))
+    variant = Variant.RANK_R if dec.variant is Variant.EXACT else dec.variant
+    return SpectralDecomposition(U, dec.eigenvalues[:r], eta, dec.components, variant, replace(dec.provenance, r=r))
+
+
+def decompose_blockwise(A, labeling: ComponentLabeling, r: int, rho: int, p: int = DEFAULT_OVERSAMPLING,
+                        q: int = DEFAULT_POWER_ITERATIONS, seed: int = 0, dtype="float64",
+                        device=None) -> SpectralDecomposition:
+    """Per-component decomposition with a global top-r selection (``spectral.py:312-390``).
+
+    Components of at most rho vertices are decomposed exactly (dense eigh on
+    the device), larger ones by the randomized path at rank
+    max(rho, ceil(r n_l / n)); the r algebraically largest pairs over all
+    components are kept (ties by component, then column).  Component 0 uses
+    ``seed``, later ones ``mix_seed(seed, comp)``.
+    """
+    import torch
+
+    A = SparseSymmetricMatrix.coerce(A)
+    n = A.n
+    if labeling.n != n:
+        raise ValueError("labeling does not match the matrix dimension")
+    if r < 1:
+        raise ValueError("r must be positive")
+    if rho < 1:
+        raise ValueError("rho must be positive")
+    if p < 0 or q < 1:
+        raise ValueError("need p >= 0 and q >= 1")
+    blocks = []
+    all_exact = True
+    for comp in range(labeling.count):
+        vertices = labeling.vertices_of(comp)
+        n_l = vertices.size
+        sub = A.submatrix(vertices)
+        if n_l <= rho:
+            part = exact_eigendecomposition(sub, max_n=max(DENSE_GUARD, n_l), dtype=dtype, device=device)
+        else:
+            r_l = min(max(rho, math.ceil(r * n_l / n)), n_l)
+            comp_seed = seed if comp == 0 else mix_seed(seed, comp)
+            part = decompose(sub, r_l, p=p, q=q, seed=comp_seed, dtype=dtype, device=device)
+            all_exact = False
+        blocks.append((vertices, part))
+
+    lams = np.concatenate([part.eigenvalues for _, part in blocks])
+    comps = np.concatenate([np.full(part.r, c, dtype=np.int64) for c, (_, part) in enumerate(blocks)])
+    cols = np.concatenate([np.arange(part.r, dtype=np.int64) for _, part in blocks])
+    order = np.lexsort((cols, comps, -lams))
+    keep = order[: min(r, lams.size)]
+    kept = keep.size
+    dev = blocks[0][1].U_device.device
+    dt_t = blocks[0][1].U_device.dtype
+    U = torch.zeros(n, kept, dtype=dt_t, device=dev)
+    out_cols = np.arange(kept)
+    for c, (vertices, part) in enumerate(blocks):
+        mine = comps[keep] == c
+        if not mine.any():
+            continue
+        src = torch.as_tensor(cols[keep][mine], device=dev)
+        dst = torch.as_tensor(out_cols[mine], device=dev)
+        rows = torch.as_tensor(vertices, device=dev)
+        U[rows[:, None], dst[None, :]] = part.U_device[:, src]
+    eta = torch.empty(n, dtype=torch.float64, device=dev)
+    N.Context.get(dev).call("row_norms", N.dtype_code(dt_t), n, kept, N.ptr(U), U.stride(0), N.ptr(eta))
+    truncated = kept < lams.size
+    if all_exact:
+        variant = Variant.RANK_R if truncated else Variant.EXACT
+    else:
+        variant = Variant.APPROX
+    return SpectralDecomposition(U, lams[keep], eta, labeling, variant, Provenance(r=r, p=p, q=q, seed=seed))
+
+
 # ---------------------------------------------------------------------------
 # K7: sparsify
 # ---------------------------------------------------------------------------

@@ -17,6 +17,7 @@ import sys
 import time
 
 import numpy as np
+import scipy.sparse as sp
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 REPO = os.path.dirname(os.path.dirname(HERE))
@@ -206,8 +207,65 @@ def epilogue_case(n_q: int = 5, region_per_image: int = 4):
     np.savez_compressed(os.path.join(HERE, "epi.npz"), **out)
 
 
+def block_graph(sizes, seed: int, density: float = 0.08):
+    """Symmetric nonnegative adjacency whose components have the given sizes
+    (each block connected: a random spanning path plus random edges), vertices
+    randomly permuted so the labeling is not trivial."""
+    rng = np.random.default_rng(seed)
+    n = int(sum(sizes))
+    perm = rng.permutation(n)
+    rows, cols = [], []
+    start = 0
+    for m in sizes:
+        v = perm[start:start + m]
+        start += m
+        if m == 1:
+            continue
+        for a in range(m - 1):  # spanning path keeps the block connected
+            rows.append(v[a]), cols.append(v[a + 1])
+        extra = rng.random((m, m)) < density
+        ii, jj = np.nonzero(np.triu(extra, 1))
+        rows.extend(v[ii].tolist()), cols.extend(v[jj].tolist())
+    rows, cols = np.array(rows, dtype=np.int64), np.array(cols, dtype=np.int64)
+    vals = rng.uniform(0.1, 1.0, rows.size)
+    W = sp.coo_matrix((np.r_[vals, vals], (np.r_[rows, cols], np.r_[cols, rows])), shape=(n, n)).tocsr()
+    W.sum_duplicates()
+    W.sort_indices()
+    return W
+
+
+def blockwise_case():
+    """connected_components + decompose_blockwise + exact/rank-r decompositions."""
+    W = block_graph([300, 120, 45, 30, 2, 2, 1, 1, 1], seed=21)
+    A = SparseSymmetricMatrix(W)
+    lab = graph.connected_components(A)
+    S = graph.normalize_adjacency(A, graph.degrees(A))
+    out = {"W_indptr": W.indptr.astype(np.int64), "W_indices": W.indices.astype(np.int32), "W_data": W.data,
+           "S_data": S.csr.data, "labels": lab.labels, "sizes": lab.sizes, "order": lab.order}
+    for tag, rho, r in (("mixed", 50, 60), ("exact", 400, 60)):
+        # step r down until the r-th and (r+1)-th candidates are well separated
+        while True:
+            dec = spectral.decompose_blockwise(S, lab, r=r, rho=rho, p=10, q=4, seed=7)
+            full = spectral.decompose_blockwise(S, lab, r=10 ** 6, rho=rho, p=10, q=4, seed=7)
+            lam_all = full.eigenvalues
+            if r >= lam_all.size or lam_all[r - 1] - lam_all[r] > 1e-6:
+                break
+            r -= 1
+        out[f"{tag}_r"] = np.array(r)
+        out[f"{tag}_lam"] = dec.eigenvalues
+        out[f"{tag}_U"] = dec.dense_u()
+        out[f"{tag}_eta"] = dec.eta
+        out[f"{tag}_variant"] = np.array(dec.variant.value)
+    sub = A.submatrix(lab.vertices_of(2))
+    ex = spectral.exact_eigendecomposition(graph.normalize_adjacency(sub, graph.degrees(sub)))
+    out["exact_sub_lam"], out["exact_sub_U"] = ex.eigenvalues, ex.U
+    rr = spectral.rank_r_decomposition(S.submatrix(lab.vertices_of(1)), 17)
+    out["rankr_lam"], out["rankr_U"], out["rankr_eta"] = rr.eigenvalues, rr.U, rr.eta
+    np.savez_compressed(os.path.join(HERE, "blockwise.npz"), **out)
+
+
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["gaussian", "kat", "c1", "epi"]
+    which = sys.argv[1:] or ["gaussian", "kat", "c1", "epi", "blockwise"]
     if "gaussian" in which:
         gaussian_cases()
     if "kat" in which:
@@ -216,4 +274,6 @@ if __name__ == "__main__":
         c1_case()
     if "epi" in which:
         epilogue_case()
+    if "blockwise" in which:
+        blockwise_case()
     print("ok")

@@ -143,3 +143,33 @@ def test_c1_oracle_epilogues_match_reference(golden):
         sims = [O.out_of_sample_similarity(queries[a], queries[b], phi, data, cfg.y_top, cfg.gamma)
                 for a, b in ((0, 1), (2, 3), (4, 4), (5, 9))]
         np.testing.assert_allclose(sims, e[f"{tag}_oos"], rtol=1e-8)
+
+
+def _blockwise_mats(b):
+    n = b["labels"].size
+    W = sp.csr_matrix((b["W_data"], b["W_indices"], b["W_indptr"]), shape=(n, n))
+    S = sp.csr_matrix((b["S_data"], b["W_indices"], b["W_indptr"]), shape=(n, n))
+    return W, S
+
+
+def _assert_same_spectral_operator(U, lam, U_ref, lam_ref, tol):
+    """Invariant to column order among equal eigenvalues and to signs."""
+    np.testing.assert_allclose(np.sort(lam)[::-1], np.sort(lam_ref)[::-1], atol=tol)
+    np.testing.assert_allclose((U * lam) @ U.T, (U_ref * lam_ref) @ U_ref.T, atol=tol)
+    np.testing.assert_allclose(U @ U.T, U_ref @ U_ref.T, atol=tol)
+
+
+def test_oracle_components_and_blockwise_match_reference(golden):
+    b = golden("blockwise")
+    W, S = _blockwise_mats(b)
+    labels, sizes, order = O.connected_components(W)
+    np.testing.assert_array_equal(labels, b["labels"])
+    np.testing.assert_array_equal(sizes, b["sizes"])
+    np.testing.assert_array_equal(order, b["order"])
+    for tag, rho in (("mixed", 50), ("exact", 400)):
+        U, lam, eta, all_exact, truncated = O.decompose_blockwise(S, labels, int(b[f"{tag}_r"]), rho, p=10, q=4,
+                                                                  seed=7)
+        variant = ("rank_r" if truncated else "exact") if all_exact else "approx"
+        assert variant == str(b[f"{tag}_variant"])
+        _assert_same_spectral_operator(U, lam, b[f"{tag}_U"], b[f"{tag}_lam"], 1e-9)
+        np.testing.assert_allclose(eta, b[f"{tag}_eta"], atol=1e-9)
