@@ -41,7 +41,8 @@ enum fsr_status {
   FSR_ECUDA = 3,
   FSR_ENOMEM = 4,
   FSR_ELIBRARY = 5,    /* cuBLAS / cuSOLVER failure                          */
-  FSR_ENOTSPD = 6      /* Cholesky breakdown: caller falls back to Householder */
+  FSR_ENOTSPD = 6,     /* Cholesky breakdown: caller falls back to Householder */
+  FSR_EIO = 7          /* file I/O or checksum failure (FSRX persistence)     */
 };
 
 enum fsr_dtype { FSR_F32 = 0, FSR_F64 = 1 };
@@ -243,6 +244,31 @@ int fsr_pool_scores(fsr_ctx* ctx, int dtype, int64_t b, int64_t N, const int64_t
  * U_bar (N x k, ld lda) and Z the scaled projections (b x k, ld ldz). */
 int fsr_dense_scores(fsr_ctx* ctx, int dtype, int64_t N, int64_t k, const void* A, int64_t lda,
                      int64_t b, const void* Z, int64_t ldz, void* Out, int64_t ldo);
+
+/* ---- FSRX decomposition files ---------
+ * Host buffers only.  variant: 0 exact, 1 rank_r, 2 approx, 3 sparse;
+ * storage: 0 dense U (n x r float32, row-major), 1 CSR (n+1 u64 offsets, nnz
+ * u32 columns, nnz float32 values).  A CRC-32 trailer covers every byte;
+ * fsr_fsrx_read returns FSR_EIO on a truncated file or checksum mismatch. */
+typedef struct fsr_fsrx_header {
+  uint64_t n;
+  uint32_t r;
+  uint8_t variant;
+  uint8_t storage;
+  uint64_t seed;
+  double alpha_hint;
+  uint64_t nnz;
+  uint64_t components;
+} fsr_fsrx_header;
+int fsr_fsrx_write(fsr_ctx* ctx, const char* path, const fsr_fsrx_header* h, const double* eigenvalues,
+                   const float* U_dense, const uint64_t* indptr, const uint32_t* indices,
+                   const float* values, const float* eta, const uint64_t* sizes,
+                   const uint64_t* permutation);
+/* Header only (sizes for the caller's buffers); no checksum verification. */
+int fsr_fsrx_read_header(fsr_ctx* ctx, const char* path, fsr_fsrx_header* h);
+int fsr_fsrx_read(fsr_ctx* ctx, const char* path, fsr_fsrx_header* h, double* eigenvalues,
+                  float* U_dense, uint64_t* indptr, uint32_t* indices, float* values, float* eta,
+                  uint64_t* sizes, uint64_t* permutation);
 
 #ifdef __cplusplus
 }

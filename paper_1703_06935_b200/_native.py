@@ -18,7 +18,7 @@ F32, F64 = 0, 1
 STAGES = {name: i for i, name in enumerate((
     "gaussian", "normalize", "spmm", "gram", "cholesky", "apply", "eigh", "lift", "signs", "histogram",
     "compact", "project", "filter_spmm", "transpose", "copy_uncovered", "topk", "householder"))}
-OK, EINVAL, ENUMERICAL, ECUDA, ENOMEM, ELIBRARY, ENOTSPD = range(7)
+OK, EINVAL, ENUMERICAL, ECUDA, ENOMEM, ELIBRARY, ENOTSPD, EIO = range(8)
 
 _c_i64 = ctypes.c_int64
 _c_u64 = ctypes.c_uint64
@@ -74,6 +74,9 @@ _SIGS = {
                                _c_p, _c_i64, _c_p, _c_i64]),
     "fsr_pool_scores": (_c_int, [_c_p, _c_int, _c_i64, _c_i64, _c_p, _c_p, _c_p, _c_p, _c_i64, _c_p, _c_i64]),
     "fsr_connected_components": (_c_int, [_c_p, _c_i64, _c_p, _c_p, _c_p, _c_p]),
+    "fsr_fsrx_write": (_c_int, [_c_p, ctypes.c_char_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p]),
+    "fsr_fsrx_read_header": (_c_int, [_c_p, ctypes.c_char_p, _c_p]),
+    "fsr_fsrx_read": (_c_int, [_c_p, ctypes.c_char_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p]),
     "fsr_dense_scores": (_c_int, [_c_p, _c_int, _c_i64, _c_i64, _c_p, _c_i64, _c_i64, _c_p, _c_i64, _c_p, _c_i64]),
 }
 
@@ -81,6 +84,14 @@ EXPORTED = tuple(_SIGS)
 
 _lib = None
 _lock = threading.Lock()
+
+
+class FsrxHeader(ctypes.Structure):
+    """fsr_fsrx_header of include/fsr.h."""
+
+    _fields_ = [("n", ctypes.c_uint64), ("r", ctypes.c_uint32), ("variant", ctypes.c_uint8),
+                ("storage", ctypes.c_uint8), ("seed", ctypes.c_uint64), ("alpha_hint", ctypes.c_double),
+                ("nnz", ctypes.c_uint64), ("components", ctypes.c_uint64)]
 
 
 class FsrError(RuntimeError):
@@ -177,6 +188,8 @@ class Context:
         msg = self.lib.fsr_last_error(self.handle).decode(errors="replace")
         if status == EINVAL:
             raise ValueError(msg)
+        if status == EIO:
+            raise OSError(msg)
         if status == ENUMERICAL:
             from .spectral import NumericalError
 
