@@ -20,6 +20,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <type_traits>
 
 #include "fsr_common.cuh"
 
@@ -212,6 +213,41 @@ __device__ void select_exact(const Range<T, EXPLICIT>& R, int64_t K, Shared& sh,
   bitonic_sort(ckey, cidx, (int)K);
 }
 
+// Visit element values of a range with 16-byte vector loads, U vectors in
+// flight per thread (fp32 rows are HBM-streamed: one CTA per row must keep
+// enough bytes in flight); f(e, v) is called for every element e in [0, m).
+// Falls back to scalar loads when the range start is not 16-byte aligned.
+template <typename T, int U, typename F>
+__device__ __forceinline__ void for_each_vec(const T* __restrict__ v, int64_t m, F&& f) {
+  constexpr int W = 16 / sizeof(T);
+  using V = typename std::conditional<sizeof(T) == 4, float4, double2>::type;
+  if (((uintptr_t)v & 15) != 0) {
+    for (int64_t e = threadIdx.x; e < m; e += blockDim.x) f(e, v[e]);
+    return;
+  }
+  const V* vv = reinterpret_cast<const V*>(v);
+  const int64_t mv = m / W;
+  const int64_t step = (int64_t)blockDim.x * U;
+  for (int64_t base = threadIdx.x; base < mv; base += step) {
+    V x[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = base + (int64_t)u * blockDim.x;
+      if (i < mv) x[u] = __ldg(vv + i);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = base + (int64_t)u * blockDim.x;
+      if (i < mv) {
+        const T* xs = reinterpret_cast<const T*>(&x[u]);
+#pragma unroll
+        for (int c = 0; c < W; ++c) f(i * W + c, xs[c]);
+      }
+    }
+  }
+  for (int64_t e = mv * W + threadIdx.x; e < m; e += blockDim.x) f(e, v[e]);
+}
+
 // Sampled single-pass selection; returns false when the caller must fall back.
 template <typename T>
 __device__ bool select_sampled(const Range<T, false>& R, int64_t K, Shared& sh, uint64_t* ckey, int64_t* cidx) {
@@ -227,13 +263,13 @@ __device__ bool select_sampled(const Range<T, false>& R, int64_t K, Shared& sh, 
     __syncthreads();
     for (int64_t b = 0; b < nblk; b += kSampleEvery) {
       const int64_t e0 = b * kSampleChunk, e1 = min(R.m, e0 + kSampleChunk);
-      for (int64_t e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
-        const uint64_t k = order_key(R.v[e]);
+      for_each_vec<T, 1>(R.v + e0, e1 - e0, [&](int64_t, T x) {
+        const uint64_t k = order_key(x);
         if (level == 0)
           atomicAdd(&sh.hist[k >> (KB - kHistBits)], 1u);
         else if ((k >> (KB - kHistBits)) == prefix)
           atomicAdd(&sh.hist[(k >> (KB - 2 * kHistBits)) & (nb - 1)], 1u);
-      }
+      });
     }
     __syncthreads();
     find_bin(sh, nb, level == 0 ? target : target - above0);
@@ -244,16 +280,17 @@ __device__ bool select_sampled(const Range<T, false>& R, int64_t K, Shared& sh, 
   const uint64_t T_lo = prefix << (KB - 2 * kHistBits);  // candidates: key >= T_lo
   if (!threadIdx.x) sh.count = 0;
   __syncthreads();
-  for (int64_t e = threadIdx.x; e < R.m; e += blockDim.x) {
-    const uint64_t k = order_key(R.v[e]);
+  const int64_t base = R.base;
+  for_each_vec<T, 4>(R.v, R.m, [&](int64_t e, T x) {
+    const uint64_t k = order_key(x);
     if (k >= T_lo) {
       const unsigned slot = atomicAdd(&sh.count, 1u);
       if (slot < (unsigned)kCap) {
         ckey[slot] = k;
-        cidx[slot] = R.base + e;
+        cidx[slot] = base + e;
       }
     }
-  }
+  });
   __syncthreads();
   const unsigned c = sh.count;
   if (c < (unsigned)K || c > (unsigned)kCap) return false;
