@@ -370,7 +370,11 @@ __global__ void __launch_bounds__(256) spmm_l2panel_kernel(int64_t n_rows, const
 // SpMV with the dense vector staged in shared memory: random 4-byte gathers
 // from L1 cost one wavefront per distinct 128B line (~32 per warp access);
 // from shared memory they cost a few bank cycles.  Warp per row, 4 nonzeros
-// per lane in flight.
+// per lane in flight.  (Tried: a warp owning 32 consecutive rows with one
+// coalesced row-pointer load and 1-4 rows in flight -- faster on uniform
+// rows, but 3-25% slower on the bench's U~, whose row lengths are very
+// skewed: rows of small clusters keep hundreds of entries, rows of large
+// clusters few.  Grid-stride warp-per-row balances that best.)
 template <typename T>
 __global__ void __launch_bounds__(256) spmv_smem_kernel(int64_t n_rows, const int64_t* __restrict__ indptr,
                                                         const int32_t* __restrict__ indices,

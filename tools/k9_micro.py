@@ -83,7 +83,10 @@ def main():
 
     ref = None
     res = {"n": n, "r": r, "tau": tau, "b": b}
-    for v in range(a.runs):
+    variants = os.environ.get("MICRO_VARIANTS", "").split(",") if os.environ.get("MICRO_VARIANTS") else [None]
+    for v in range(a.runs * len(variants)):
+        if variants[0] is not None:
+            os.environ[os.environ.get("MICRO_VARIANT_ENV", "FSR_SPMV_VARIANT")] = variants[v % len(variants)]
         run()
         torch.cuda.synchronize()
         ctx.enable_timing(True)
@@ -96,7 +99,7 @@ def main():
         if ref is None:
             ref = X.clone()
         err = float((X - ref).abs().max() / ref.abs().max())
-        out = {"run": v, "check_rel_l2": check(), "k9_ms": ms, "tflops": 2 * tau * b / ms / 1e9,
+        out = {"run": v, "variant": variants[v % len(variants)], "check_rel_l2": check(), "k9_ms": ms, "tflops": 2 * tau * b / ms / 1e9,
                "l2_gather_tbs": 4 * tau * b / ms / 1e9, "max_rel_diff_vs_first": err}
         res[f"run{v}"] = out
         print(json.dumps(out), flush=True)
