@@ -131,8 +131,8 @@ class ClockSampler:
         if not sm:
             return None
         loaded = [s for s in sm if mx and s >= 0.5 * mx] or sm
-        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm)}
+        return {"sm_mhz": statistics.median(loaded), "sm_min_mhz": min(loaded), "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
 
 
 # ---------------------------------------------------------------------------
@@ -371,6 +371,7 @@ def run_fsr(args, cfg, n, rank, world, local_rank):
     # ---------------- offline: SI + Rayleigh-Ritz + sparsify (timed once) ----
     ctx.enable_timing(True)
     ctx.stage_reset()
+    off_clocks = ClockSampler(local_rank)
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
     torch.cuda.synchronize()
     torch.cuda.nvtx.range_push("fsr:offline")
@@ -389,6 +390,7 @@ def run_fsr(args, cfg, n, rank, world, local_rank):
         sdec = sharded_offline(S, r, r_hat, q, tau, dt, device, ev)
     torch.cuda.synchronize()
     torch.cuda.nvtx.range_pop()
+    off_clk = off_clocks.stop()
     stages = {name: ctx.stage_time(name) for name in N.STAGES}
     torch.cuda.empty_cache()
     si_s = ev[0].elapsed_time(ev[1]) / 1e3
@@ -412,6 +414,7 @@ def run_fsr(args, cfg, n, rank, world, local_rank):
         "spmm_fp32_tflops": 2.0 * nnz_s * r_hat / (spmm_ms_iter * 1e-3) / 1e12,
         "stage_ms": {k: round(v[0], 3) for k, v in stages.items() if v[1]},
         "nnz_W": nnz_w, "isolated_vertices": isolated, "kept_nnz": sdec.U_device.nnz, "inputs_build_s": t_inputs,
+        "clocks": off_clk,
     }
 
     # ---------------- online: device-resident batches ------------------------

@@ -132,6 +132,13 @@ int fsr_cholesky(fsr_ctx* ctx, int64_t k, double* G);
 /* A <- A R^-1 for the R produced by fsr_cholesky (row-major A, n_rows x k). */
 int fsr_apply_rinv(fsr_ctx* ctx, int dtype, int64_t n_rows, int64_t k, const double* R, void* A,
                    int64_t lda);
+/* F32 tcgen05 path: A <- A M' with M' = R^-1 kept to m_slices = 1 (7-bit) or
+ * 4 (28-bit) slices; 1 is the first CholeskyQR pass (span(A M') = span(A)
+ * for any invertible M'; 4 products instead of 10), used only when every
+ * diagonal entry of R^-1 is >= 2^-4 of its column's maximum (else 4).  Other
+ * dtypes / paths ignore m_slices. */
+int fsr_apply_rinv_levels(fsr_ctx* ctx, int dtype, int64_t n_rows, int64_t k, const double* R, void* A,
+                          int64_t lda, int m_slices);
 /* Householder QR (single device): A <- Q, the reduced orthonormal factor.
  * Fallback for rank-deficient blocks, mirroring spectral.py:165. */
 int fsr_householder_qr(fsr_ctx* ctx, int dtype, int64_t n_rows, int64_t k, void* A, int64_t lda);

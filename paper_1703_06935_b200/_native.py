@@ -77,6 +77,7 @@ _SIGS = {
     "fsr_fsrx_write": (_c_int, [_c_p, ctypes.c_char_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p]),
     "fsr_fsrx_read_header": (_c_int, [_c_p, ctypes.c_char_p, _c_p]),
     "fsr_fsrx_read": (_c_int, [_c_p, ctypes.c_char_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p]),
+    "fsr_apply_rinv_levels": (_c_int, [_c_p, _c_int, _c_i64, _c_i64, _c_p, _c_p, _c_i64, _c_int]),
     "fsr_dense_scores": (_c_int, [_c_p, _c_int, _c_i64, _c_i64, _c_p, _c_i64, _c_i64, _c_p, _c_i64, _c_p, _c_i64]),
 }
 

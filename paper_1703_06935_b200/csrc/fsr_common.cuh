@@ -127,7 +127,7 @@ inline int scratch_aux(fsr_ctx* ctx, size_t bytes, void** out) {
 int tc_gram(fsr_ctx* ctx, int64_t n, int64_t ka, const float* A, int64_t lda, int64_t kb, const float* B,
             int64_t ldb, double* C, int accumulate, int levels, int symmetric);
 int tc_apply(fsr_ctx* ctx, int64_t n, int64_t K, const float* A, int64_t lda, int64_t N2, const double* M,
-             int64_t ldm, int m_col_major, float* Out, int64_t ldo);
+             int64_t ldm, int m_col_major, float* Out, int64_t ldo, int m_slices = 4);
 
 inline int host_stage(fsr_ctx* ctx, size_t bytes, void** out) {
   if (bytes > ctx->host_stage_bytes) {

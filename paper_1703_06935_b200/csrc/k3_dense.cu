@@ -18,6 +18,8 @@
 #include <algorithm>
 #include <vector>
 
+#include <cstring>
+
 #include "fsr_common.cuh"
 
 namespace {
@@ -67,6 +69,22 @@ __global__ void gather_cols_kernel(int64_t k, int64_t r, const double* __restric
        f += (int64_t)gridDim.x * blockDim.x) {
     const int64_t a = f / r, j = f - a * r;
     V[f] = Vc[perm[j] * k + a];
+  }
+}
+
+// min over columns j of |R^-1_jj| / max_i |R^-1_ij| (column-major upper-triangular R^-1),
+// as float bits (nonnegative floats order like unsigned ints)
+__global__ void diag_ratio_kernel(int64_t k, const double* __restrict__ Rinv, unsigned* __restrict__ worst) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t j = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; j < k; j += nwarps) {
+    double m = 0.0;
+    for (int64_t i = lane; i <= j; i += 32) m = fmax(m, fabs(Rinv[j * k + i]));
+    for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (!lane) {
+      const float r = m > 0.0 ? (float)(fabs(Rinv[j * k + j]) / m) : 0.0f;
+      atomicMin(worst, __float_as_uint(r));
+    }
   }
 }
 
@@ -250,7 +268,13 @@ int fsr_cholesky(fsr_ctx* ctx, int64_t k, double* G) {
 }
 
 int fsr_apply_rinv(fsr_ctx* ctx, int dtype, int64_t n_rows, int64_t k, const double* R, void* A, int64_t lda) {
+  return fsr_apply_rinv_levels(ctx, dtype, n_rows, k, R, A, lda, 4);
+}
+
+int fsr_apply_rinv_levels(fsr_ctx* ctx, int dtype, int64_t n_rows, int64_t k, const double* R, void* A, int64_t lda,
+                          int m_slices) {
   FSR_REQUIRE(ctx, n_rows >= 0 && k >= 1 && lda >= k, "apply_rinv: bad shape");
+  FSR_REQUIRE(ctx, m_slices == 1 || m_slices == 4, "apply_rinv: m_slices must be 1 or 4");
   if (!n_rows) return FSR_OK;
   fsr::StageTimer timer(ctx, FSR_STAGE_APPLY);
   // (A R^-1)^T = R^-T A^T: solve R^T X = A_c with A_c the column-major k x n view
@@ -271,7 +295,22 @@ int fsr_apply_rinv(fsr_ctx* ctx, int dtype, int64_t n_rows, int64_t k, const dou
     const double done = 1.0;
     FSR_BLAS(ctx, cublasDtrsm_64(ctx->blas, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_N,
                                  CUBLAS_DIAG_NON_UNIT, k, k, &done, R, k, Rinv, k));
-    return fsr::tc_apply(ctx, n_rows, k, (const float*)A, lda, k, Rinv, k, 1, (float*)A, lda);
+    if (m_slices == 1) {
+      // the 7-bit R^-1 must stay a good preconditioner: every diagonal entry
+      // (triangular: its determinant) within 2^-4 of its column's maximum
+      unsigned* worst = (unsigned*)ctx->dev_info;  // 4 device bytes, free between solver calls
+      const unsigned one_bits = 0x3f800000u;
+      FSR_CUDA(ctx, cudaMemcpyAsync(worst, &one_bits, sizeof(unsigned), cudaMemcpyHostToDevice, ctx->stream));
+      diag_ratio_kernel<<<fsr::grid_for(k * 32, 256, ctx, 8), 256, 0, ctx->stream>>>(k, Rinv, worst);
+      FSR_TRY(fsr::launched(ctx, "diag_ratio_kernel"));
+      unsigned h = 0;
+      FSR_CUDA(ctx, cudaMemcpyAsync(&h, worst, sizeof(unsigned), cudaMemcpyDeviceToHost, ctx->stream));
+      FSR_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+      float ratio;
+      memcpy(&ratio, &h, 4);
+      if (!(ratio >= 0.0625f)) m_slices = 4;
+    }
+    return fsr::tc_apply(ctx, n_rows, k, (const float*)A, lda, k, Rinv, k, 1, (float*)A, lda, m_slices);
   }
   void* buf = nullptr;
   FSR_TRY(fsr::scratch(ctx, (size_t)k * k * 4, &buf));

@@ -189,12 +189,13 @@ __global__ void slice_rows_kernel(int64_t rows, int64_t cols, const T* __restric
 }
 
 // ------------------------------------------------------------------ kernel --
-template <int N, int STAGES, int LEVELS>
+template <int N, int STAGES, int LEVELS, int BPL = LEVELS>
 struct OzCfg {
-  static constexpr int PLANES = LEVELS;      // level l needs slices 0..l
+  static constexpr int APLANES = LEVELS;     // level l needs A slices 0..l
+  static constexpr int BPLANES = BPL;        // B slices kept (1: B is a 7-bit matrix)
   static constexpr int A_PLANE = 128 * kBK;  // 128 rows x 64 K bytes
   static constexpr int B_PLANE = N * kBK;
-  static constexpr int STAGE_BYTES = PLANES * (A_PLANE + B_PLANE);
+  static constexpr int STAGE_BYTES = APLANES * A_PLANE + BPLANES * B_PLANE;
   static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
   static constexpr uint32_t TMEM_COLS = LEVELS * N <= 128 ? 128 : (LEVELS * N <= 256 ? 256 : 512);
   static_assert(LEVELS * N <= 512, "accumulators exceed TMEM");
@@ -238,13 +239,13 @@ __device__ __forceinline__ void tmem_ld32_i(uint32_t taddr, int (&v)[32]) {
 //   rows = output rows i (ka of them), B rows = output cols j; result written
 //   to the fp64 partial P[split] (ka x kb).
 // MODE 1 (apply): D[r, j] = sum_K A[r, :] B[j, :] over the full K; fp32 out.
-template <int MODE, int N, int STAGES, int LEVELS>
+template <int MODE, int N, int STAGES, int LEVELS, int BPL>
 __global__ void __launch_bounds__(kThreads, 1)
     oz_gemm_kernel(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUtensorMap mB, int rowsA,
                    int rowsB, int64_t planeA_rows, int64_t planeB_rows, int64_t K, int tiles_n, int64_t k_per_split,
                    const int* __restrict__ eA, const int* __restrict__ eB, int symmetric, double* __restrict__ P,
                    float* __restrict__ Out, int64_t ldo) {
-  using Cfg = OzCfg<N, STAGES, LEVELS>;
+  using Cfg = OzCfg<N, STAGES, LEVELS, BPL>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint64_t* full = (uint64_t*)(smem + STAGES * Cfg::STAGE_BYTES);
@@ -287,11 +288,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_expect_tx(&full[s], Cfg::STAGE_BYTES);
         const int kk = (int)(kb0 + (int64_t)it * kBK);
 #pragma unroll
-        for (int p = 0; p < Cfg::PLANES; ++p) {
+        for (int p = 0; p < Cfg::APLANES; ++p)
           tma_load_2d(st + p * Cfg::A_PLANE, &mA, &full[s], kk, (int)(p * planeA_rows + i0));
-          tma_load_2d(st + Cfg::PLANES * Cfg::A_PLANE + p * Cfg::B_PLANE, &mB, &full[s], kk,
+#pragma unroll
+        for (int p = 0; p < Cfg::BPLANES; ++p)
+          tma_load_2d(st + Cfg::APLANES * Cfg::A_PLANE + p * Cfg::B_PLANE, &mB, &full[s], kk,
                       (int)(p * planeB_rows + j0));
-        }
       }
       __syncwarp();
     }
@@ -303,21 +305,23 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_after();
       if (lane == 0) {
         const uint32_t base = smem_u32(smem + s * Cfg::STAGE_BYTES);
-        const uint32_t bbase = base + Cfg::PLANES * Cfg::A_PLANE;
+        const uint32_t bbase = base + Cfg::APLANES * Cfg::A_PLANE;
 #pragma unroll
         for (int ks = 0; ks < kBK / 32; ++ks) {
-          uint64_t a[Cfg::PLANES], b[Cfg::PLANES];
+          uint64_t a[Cfg::APLANES], b[Cfg::BPLANES];
 #pragma unroll
-          for (int p = 0; p < Cfg::PLANES; ++p) {
-            a[p] = desc_sw64(base + p * Cfg::A_PLANE + ks * 32);
-            b[p] = desc_sw64(bbase + p * Cfg::B_PLANE + ks * 32);
-          }
+          for (int p = 0; p < Cfg::APLANES; ++p) a[p] = desc_sw64(base + p * Cfg::A_PLANE + ks * 32);
+#pragma unroll
+          for (int p = 0; p < Cfg::BPLANES; ++p) b[p] = desc_sw64(bbase + p * Cfg::B_PLANE + ks * 32);
           const uint32_t acc = (it == 0 && ks == 0) ? 0u : 1u;
-          // level l accumulates the slice pairs (t, l - t)
+          // level l accumulates the slice pairs (t, l - t) that are kept; the
+          // first product issued into each accumulator starts it (acc == 0)
 #pragma unroll
-          for (int l = 0; l < LEVELS; ++l)
+          for (int l = 0; l < LEVELS; ++l) {
+            const int t0 = l - (Cfg::BPLANES - 1) > 0 ? l - (Cfg::BPLANES - 1) : 0;
 #pragma unroll
-            for (int t = 0; t <= l; ++t) mma_i8(tmem + l * N, a[t], b[l - t], idesc, t == 0 ? acc : 1u);
+            for (int t = t0; t <= l; ++t) mma_i8(tmem + l * N, a[t], b[l - t], idesc, t == t0 ? acc : 1u);
+          }
         }
         mma_commit(&empty[s]);
         if (it == iters - 1) mma_commit(&tfull[0]);
@@ -435,30 +439,34 @@ int set_smem(fsr_ctx* ctx, K kernel, int bytes) {
 
 constexpr size_t kChunkBudget = (size_t)6 << 30;  // bytes of slice staging per row chunk
 
-// tile width / pipeline depth per variant
-template <int LEVELS>
+// tile width / pipeline depth per variant (A slice planes = LEVELS, B planes = BPL)
+template <int LEVELS, int BPL>
 struct Variant;
 template <>
-struct Variant<4> {  // 4 x 128 TMEM columns; 3 stages of 4 x (128 + 128) x 64 B
+struct Variant<4, 4> {  // 4 x 128 TMEM columns; 3 stages of 4 x (128 + 128) x 64 B
   static constexpr int N = 128, STAGES = 3;
 };
 template <>
-struct Variant<1> {  // 160 TMEM columns; 8 stages of (128 + 160) x 64 B
+struct Variant<4, 1> {  // 4 x 128 TMEM columns; 5 stages of (4 x 128 + 128) x 64 B
+  static constexpr int N = 128, STAGES = 5;
+};
+template <>
+struct Variant<1, 1> {  // 160 TMEM columns; 8 stages of (128 + 160) x 64 B
   static constexpr int N = 160, STAGES = 8;
 };
 
-template <int MODE, int LEVELS>
+template <int MODE, int LEVELS, int BPL = LEVELS>
 int launch_oz(fsr_ctx* ctx, dim3 grid, const CUtensorMap& mA, const CUtensorMap& mB, int rowsA, int rowsB,
               int64_t pA, int64_t pB, int64_t K, int tiles_n, int64_t kps, const int* eA, const int* eB, int sym,
               double* P, float* Out, int64_t ldo) {
-  constexpr int N = Variant<LEVELS>::N, STAGES = Variant<LEVELS>::STAGES;
-  using Cfg = OzCfg<N, STAGES, LEVELS>;
+  constexpr int N = Variant<LEVELS, BPL>::N, STAGES = Variant<LEVELS, BPL>::STAGES;
+  using Cfg = OzCfg<N, STAGES, LEVELS, BPL>;
   static bool attr = false;
   if (!attr) {
-    FSR_TRY(set_smem(ctx, oz_gemm_kernel<MODE, N, STAGES, LEVELS>, Cfg::SMEM));
+    FSR_TRY(set_smem(ctx, oz_gemm_kernel<MODE, N, STAGES, LEVELS, BPL>, Cfg::SMEM));
     attr = true;
   }
-  oz_gemm_kernel<MODE, N, STAGES, LEVELS><<<grid, kThreads, Cfg::SMEM, ctx->stream>>>(
+  oz_gemm_kernel<MODE, N, STAGES, LEVELS, BPL><<<grid, kThreads, Cfg::SMEM, ctx->stream>>>(
       mA, mB, rowsA, rowsB, pA, pB, K, tiles_n, kps, eA, eB, sym, P, Out, ldo);
   return fsr::launched(ctx, MODE == 0 ? "oz_gram_kernel" : "oz_apply_kernel");
 }
@@ -473,7 +481,7 @@ int tc_gram(fsr_ctx* ctx, int64_t n, int64_t ka, const float* A, int64_t lda, in
             int64_t ldb, double* C, int accumulate, int levels, int symmetric) {
   const bool same = (A == B) && lda == ldb && ka == kb;
   symmetric = symmetric && same;
-  const int NT = levels == 1 ? Variant<1>::N : Variant<4>::N;
+  const int NT = levels == 1 ? Variant<1, 1>::N : Variant<4, 4>::N;
   const int64_t per_row = kSlices * (ka + (same ? 0 : kb));
   int64_t chunk = std::max<int64_t>(128, std::min<int64_t>({n, kMaxK, (int64_t)(kChunkBudget / per_row)}));
   chunk = pad_to(chunk, 128);
@@ -535,10 +543,15 @@ int tc_gram(fsr_ctx* ctx, int64_t n, int64_t ka, const float* A, int64_t lda, in
 
 // Out (n x N2 fp32) = A (n x K fp32) * M (K x N2, fp64; column-major if m_col_major).
 // Out may alias A (row chunks are sliced before they are overwritten).
+// m_slices = 1: M enters as its 7-bit first slice M' (4 products instead of
+// 10); the product A M' is still 28-bit accurate in A.  For the first
+// CholeskyQR pass that is all that matters: span(A M') = span(A) for any
+// invertible M', and the second pass orthonormalises A M' exactly.
 int tc_apply(fsr_ctx* ctx, int64_t n, int64_t K, const float* A, int64_t lda, int64_t N2, const double* M,
-             int64_t ldm, int m_col_major, float* Out, int64_t ldo) {
+             int64_t ldm, int m_col_major, float* Out, int64_t ldo, int m_slices) {
   if (K > kMaxK) return set_error(ctx, FSR_EINVAL, "tc_apply: K=%lld exceeds the int32-exact bound", (long long)K);
-  constexpr int NT = Variant<4>::N;
+  constexpr int NT = Variant<4, 4>::N;
+  static_assert(Variant<4, 1>::N == NT, "apply variants share the output tile width");
   const int64_t pk = pad_to(K, 128);
   const size_t m_bytes = (size_t)kSlices * N2 * pk;
   const int64_t per_row = kSlices * pk;
@@ -568,8 +581,12 @@ int tc_apply(fsr_ctx* ctx, int64_t n, int64_t K, const float* A, int64_t lda, in
     CUtensorMap mA;
     FSR_TRY(make_map_u8(ctx, &mA, sR, kSlices * rows, pk, pk, 128));
     dim3 grid((unsigned)(ceil_div(rows, 128) * tiles_n), 1);
-    FSR_TRY((launch_oz<1, 4>(ctx, grid, mA, mB, (int)rows, (int)N2, rows, N2, pk, tiles_n, pk, eR, eM, 0, nullptr,
-                             Out + s0 * ldo, ldo)));
+    if (m_slices == 1)
+      FSR_TRY((launch_oz<1, 4, 1>(ctx, grid, mA, mB, (int)rows, (int)N2, rows, N2, pk, tiles_n, pk, eR, eM, 0,
+                                  nullptr, Out + s0 * ldo, ldo)));
+    else
+      FSR_TRY((launch_oz<1, 4>(ctx, grid, mA, mB, (int)rows, (int)N2, rows, N2, pk, tiles_n, pk, eR, eM, 0, nullptr,
+                               Out + s0 * ldo, ldo)));
   }
   return FSR_OK;
 }

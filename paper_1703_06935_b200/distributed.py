@@ -176,8 +176,12 @@ class CudaOps:
         st = self.ctx.call("cholesky", R.shape[0], N.ptr(R))
         return None if st == N.ENOTSPD else R
 
-    def apply_rinv(self, R, Y):
-        self.ctx.call("apply_rinv", self.dt, Y.shape[0], Y.shape[1], N.ptr(R), N.ptr(Y), Y.stride(0))
+    def apply_rinv(self, R, Y, fast=False):
+        # first CholeskyQR pass: R^-1 may enter as a 7-bit matrix (spectral._cholqr_pass)
+        from .spectral import FAST_FIRST_APPLY
+
+        self.ctx.call("apply_rinv_levels", self.dt, Y.shape[0], Y.shape[1], N.ptr(R), N.ptr(Y), Y.stride(0),
+                      1 if (fast and FAST_FIRST_APPLY) else 4)
         return Y
 
     def householder(self, Yfull):
@@ -256,7 +260,7 @@ def sharded_orthonormalize(comm: Comm, ops, Y, shard: Shard, dt_code: int, stats
         if R is None:
             ok = False
             break
-        Y = ops.apply_rinv(R, Y)
+        Y = ops.apply_rinv(R, Y, fast=(pass_ == 0))
     method = "cholqr2"
     if ok and last_dev > 0.1:
         G = comm.sum_ordered(ops.gram(Y))

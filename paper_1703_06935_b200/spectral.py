@@ -18,6 +18,7 @@ from __future__ import annotations
 
 import enum
 import math
+import os
 from dataclasses import dataclass, replace
 
 import numpy as np
@@ -37,8 +38,10 @@ ORTH_TOL = {N.F64: 1e-8, N.F32: 1e-4}
 # CholeskyQR2 is orthogonal to O(eps) when the second Gram is this close to I
 # (Yamamoto et al. 2015); beyond it an explicit check runs (spectral.py:167).
 CHOLQR2_SAFE = 0.1
-# first CholeskyQR pass of a float32 block with a one-slice Gram (see _cholqr_pass)
+# first CholeskyQR pass of a float32 block with a one-slice Gram and a one-slice
+# R^-1 (see _cholqr_pass / fsr_apply_rinv_levels)
 FAST_FIRST_GRAM = True
+FAST_FIRST_APPLY = os.environ.get("FSR_FAST_FIRST_APPLY", "1") != "0"
 
 _MASK64 = (1 << 64) - 1
 
@@ -219,7 +222,10 @@ def _cholqr_pass(ctx, dt, Y, G, gram_hook=None, fast_gram=False) -> tuple[bool, 
     st = ctx.call("cholesky", G.shape[0], N.ptr(G))
     if st == N.ENOTSPD:
         return False, dev
-    ctx.call("apply_rinv", dt, Y.shape[0], Y.shape[1], N.ptr(G), N.ptr(Y), Y.stride(0))
+    # the preconditioning pass may also apply R^-1 as a 7-bit matrix: only
+    # span(Y R'^-1) = span(Y) matters there (see fsr_apply_rinv_levels)
+    ctx.call("apply_rinv_levels", dt, Y.shape[0], Y.shape[1], N.ptr(G), N.ptr(Y), Y.stride(0),
+             1 if (fast_gram and FAST_FIRST_APPLY) else 4)
     return True, dev
 
 

@@ -42,7 +42,7 @@ class NumpyOps:
         except np.linalg.LinAlgError:
             return None
 
-    def apply_rinv(self, R, Y):
+    def apply_rinv(self, R, Y, fast=False):
         return _t(sla.solve_triangular(_np(R), _np(Y).T, trans="T", lower=False).T)
 
     def householder(self, Yfull):

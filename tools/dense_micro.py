@@ -36,6 +36,7 @@ def main():
     ap.add_argument("--r", type=int, default=5000)
     ap.add_argument("--path", default="auto")
     ap.add_argument("--only", default="gram,cross,apply,lift")
+    ap.add_argument("--apply-slices", type=int, default=4, help="R^-1 slices in apply (1 = first CholQR pass)")
     a = ap.parse_args()
     dev = torch.device("cuda", 0)
     ctx = N.Context.get(dev)
@@ -62,7 +63,9 @@ def main():
         R = torch.linalg.cholesky(Gs).T.contiguous()  # upper
         Rc = R.T.contiguous()  # column-major storage of R
         Bw = B.clone()
-        ms = timed(lambda: ctx.call("apply_rinv", N.F32, n, k, N.ptr(Rc), N.ptr(Bw), k), reps=1)
+        ms = timed(lambda: ctx.call("apply_rinv_levels", N.F32, n, k, N.ptr(Rc), N.ptr(Bw), k, a.apply_slices),
+                   reps=1)
+        out["apply_slices"] = a.apply_slices
         out["apply_ms"] = ms
         out["apply_tflops"] = 2 * n * k * k / (ms * 1e-3) / 1e12
         del Bw

@@ -35,6 +35,7 @@ def main():
         for rr in ("auto", "cublas"):
             for fast in fast_opts:
                 spectral.FAST_FIRST_GRAM = fast
+                spectral.FAST_FIRST_APPLY = fast
                 ctx.set_dense_path(rf)
                 basis = spectral.range_finder(S, r + p, q, seed, dtype="float32")
                 Qd = basis.Q.double().cpu().numpy()
@@ -50,6 +51,7 @@ def main():
                             "ritz_err": lam_err, "x_err_max": max(xerr), "x_err_median": float(np.median(xerr))})
                 print(json.dumps(out[-1]), flush=True)
     spectral.FAST_FIRST_GRAM = True
+    spectral.FAST_FIRST_APPLY = True
 
 
 if __name__ == "__main__":
