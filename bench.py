@@ -341,16 +341,56 @@ def online_sweep(dec, sdec_default, density_default, cfg, n, r, queries, device,
                 k9_ms, k9_cnt = ctx.stage_time("filter_spmm")
                 kept = sd.U_device.nnz
                 k9_bytes = kept * (es + 4) + (n + 1) * 8 + es * r * b + es * n * b
-                out.append({"density": d, "b": b, "h": name, "queries_per_s": b * steps / (ms / 1e3),
-                            "ms_per_batch": ms / steps, "k9_ms": k9_ms / max(k9_cnt, 1),
-                            "k9_algorithmic_gbs": k9_bytes / (k9_ms / max(k9_cnt, 1) * 1e-3) / 1e9,
-                            "k9_fp32_tflops": 2.0 * kept * b / (k9_ms / max(k9_cnt, 1) * 1e-3) / 1e12})
+                row = {"density": d, "b": b, "h": name, "queries_per_s": b * steps / (ms / 1e3),
+                       "ms_per_batch": ms / steps, "k9_ms": k9_ms / max(k9_cnt, 1),
+                       "k9_algorithmic_gbs": k9_bytes / (k9_ms / max(k9_cnt, 1) * 1e-3) / 1e9,
+                       "k9_fp32_tflops": 2.0 * kept * b / (k9_ms / max(k9_cnt, 1) * 1e-3) / 1e12}
+                if b <= 64 and name == "h_alpha(0.99)":
+                    row.update(graph_sweep_row(sd, h, qb, b, steps, warmup, flush, ctx))
+                out.append(row)
                 del res
             del dq
         if sd is not sdec_default:
             del sd
         torch.cuda.empty_cache()
     return out
+
+
+def graph_sweep_row(sd, h, qb, b, steps, warmup, flush, ctx):
+    """Same step through ranking.FilterGraph (one CUDA-graph launch per batch):
+    device time per replay, and host-to-host latency (stage + replay + top-k D2H)."""
+    import torch
+
+    from paper_1703_06935_b200 import ranking
+
+    timing = ctx._timing
+    fg = ranking.FilterGraph(sd, h, b=b, nnz_cap=int(qb.y_ptr[-1]), topk=100)
+    fg.stage(qb)
+    for _ in range(warmup):
+        fg.replay()
+    torch.cuda.synchronize()
+    ms = 0.0
+    for _ in range(steps):
+        flush.zero_()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        fg.replay()
+        e1.record()
+        torch.cuda.synchronize()
+        ms += e0.elapsed_time(e1)
+    lat = []
+    for _ in range(steps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        res = fg.run(qb)
+        res.top_idx.cpu()
+        res.top_val.cpu()
+        lat.append(time.perf_counter() - t0)
+    ctx.enable_timing(timing)
+    del fg
+    return {"graph_ms_per_batch": ms / steps, "graph_queries_per_s": b * steps / (ms / 1e3),
+            "graph_e2e_latency_ms": 1e3 * min(lat)}
 
 
 def _repeat_batch(queries, reps, b):

@@ -160,6 +160,7 @@ class Context:
             raise FsrError(st, "fsr_ctx_create failed")
         self.handle = h
         self._stream = None
+        self._timing = False
 
     @classmethod
     def get(cls, device=None) -> "Context":
@@ -214,6 +215,7 @@ class Context:
 
     def enable_timing(self, on: bool = True):
         self.check(self.lib.fsr_ctx_enable_timing(self.handle, int(on)))
+        self._timing = bool(on)
 
     def stage_time(self, stage: str):
         """(total ms, launches) accumulated for one stage since the last reset."""

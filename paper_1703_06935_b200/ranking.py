@@ -623,3 +623,115 @@ def out_of_sample_similarity(z1, z2, phi, data, k: int, gamma: float) -> float:
     e1 = np.asarray(phi @ psis[0] if isinstance(phi, Embedding) else phi @ psis[0].to_dense()).ravel()
     e2 = np.asarray(phi @ psis[1] if isinstance(phi, Embedding) else phi @ psis[1].to_dense()).ravel()
     return float(e1 @ e2)
+
+
+# ---------------------------------------------------------------------------
+# CUDA-graph replay of the online step (small batches are launch-bound)
+# ---------------------------------------------------------------------------
+
+class _StaticQueries:
+    """DeviceQueries-shaped view of fixed device buffers (graph-capturable)."""
+
+    def __init__(self, size, b, y_ptr, y_idx, y_val):
+        self.batch = QueryBatch(size, np.zeros(b + 1, np.int64), np.zeros(0, np.int64), np.zeros(0))
+        self.b = b
+        self.y_ptr, self.y_idx, self.y_val = y_ptr, y_idx, y_val
+
+
+class FilterGraph:
+    """One CUDA graph for ``filter_device`` over a fixed query capacity.
+
+    The graph holds the pinned-host -> device copies of (y_ptr, y_idx,
+    y_val), K8 projection, K9, copy-uncovered and the exact top-k; ``run``
+    only refreshes the pinned staging buffers and replays it, so a query
+    batch costs one graph launch instead of ~6 kernel launches and the
+    Python/ctypes work between them.  Batches smaller than ``b`` are padded
+    with empty queries.  Results are identical to ``filter_device`` (same
+    kernels, same arguments).
+    """
+
+    def __init__(self, dec: SpectralDecomposition, h: TransferFunction, b: int, nnz_cap: int, topk: int = 100,
+                 copy_uncovered: bool | None = None):
+        import torch
+
+        if b < 1 or nnz_cap < 0 or topk < 1:
+            raise ValueError("need b >= 1, nnz_cap >= 0, topk >= 1")
+        self.dec, self.h, self.b, self.nnz_cap, self.topk = dec, h, b, nnz_cap, topk
+        dev = dec.eta_device.device
+        dt = dec.dtype
+        cap = max(1, nnz_cap)
+        self.h_ptr = torch.zeros(b + 1, dtype=torch.int64).pin_memory()
+        self.h_idx = torch.zeros(cap, dtype=torch.int64).pin_memory()
+        self.h_val = torch.zeros(cap, dtype=dt).pin_memory()
+        self.d_ptr = torch.zeros(b + 1, dtype=torch.int64, device=dev)
+        self.d_idx = torch.zeros(cap, dtype=torch.int64, device=dev)
+        self.d_val = torch.zeros(cap, dtype=dt, device=dev)
+        self.queries = _StaticQueries(dec.n, b, self.d_ptr, self.d_idx, self.d_val)
+        self.res = FilterResult(top_idx=torch.empty(b, topk, dtype=torch.int64, device=dev),
+                                top_val=torch.empty(b, topk, dtype=dt, device=dev))
+        ctx = N.Context.get(dev)
+        need = int(ctx.lib.fsr_filter_workspace_bytes(N.dtype_code(dt), dec.n, dec.r, b, 1))
+        self.ws = torch.empty(need, dtype=torch.uint8, device=dev)
+        self.copy_uncovered = copy_uncovered
+        self._done = None
+        _weights_device(dec, h)  # cache h(Lambda) on the device before capture
+        timing = bool(getattr(ctx, "_timing", False))
+        side = torch.cuda.Stream(dev)
+        side.wait_stream(torch.cuda.current_stream(dev))
+        with torch.cuda.stream(side):  # warm-up: sizes libfsr scratch, sets kernel attributes
+            for _ in range(2):
+                self._body()
+        torch.cuda.current_stream(dev).wait_stream(side)
+        torch.cuda.synchronize(dev)
+        ctx.enable_timing(False)
+        self.graph = torch.cuda.CUDAGraph()
+        try:
+            with torch.cuda.graph(self.graph, stream=side):
+                self._body()
+        finally:
+            ctx.enable_timing(timing)
+            N.Context.get(dev)  # re-bind libfsr to the current stream
+
+    def _body(self):
+        self.d_ptr.copy_(self.h_ptr, non_blocking=True)
+        self.d_idx.copy_(self.h_idx, non_blocking=True)
+        self.d_val.copy_(self.h_val, non_blocking=True)
+        filter_device(self.dec, self.h, self.queries, copy_uncovered=self.copy_uncovered, topk=self.topk,
+                      want_x=False, out=self.res, workspace=self.ws)
+
+    def stage(self, batch: QueryBatch) -> None:
+        """Copy a host batch into the pinned staging buffers (host-only work;
+        waits until the previous replay has consumed them)."""
+        if self._done is not None:
+            self._done.synchronize()
+        if batch.size != self.dec.n:
+            raise ValueError(f"observation size {batch.size} != decomposition size {self.dec.n}")
+        if batch.b > self.b or int(batch.y_ptr[-1]) > self.nnz_cap:
+            raise ValueError(f"batch ({batch.b} queries, {int(batch.y_ptr[-1])} nonzeros) exceeds the graph's "
+                             f"capacity ({self.b}, {self.nnz_cap})")
+        ptr = self.h_ptr.numpy()
+        ptr[: batch.b + 1] = batch.y_ptr
+        ptr[batch.b + 1:] = batch.y_ptr[-1]
+        nz = int(batch.y_ptr[-1])
+        self.h_idx.numpy()[:nz] = batch.y_idx
+        self.h_val[:nz] = torch_from_numpy_cast(batch.y_val, self.h_val.dtype)
+
+    def replay(self):
+        """Launch the captured step on the current stream (after ``stage``)."""
+        import torch
+
+        self.graph.replay()
+        self._done = torch.cuda.Event()
+        self._done.record()
+        return self.res
+
+    def run(self, batch: QueryBatch):
+        """stage + replay; returns the device FilterResult (top_idx / top_val, b x topk)."""
+        self.stage(batch)
+        return self.replay()
+
+
+def torch_from_numpy_cast(a, dtype):
+    import torch
+
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).to(dtype)

@@ -142,3 +142,33 @@ def test_batch_widths_agree_with_single_queries(c1, decs, b):
         x = ranking.filter(sdec, h, sub.column(j))
         assert rel_l2(X[j], x) <= tol
         np.testing.assert_array_equal(idx[j], ranking.rank(X[j])[:100])
+
+
+@pytest.mark.parametrize("b", [1, 7, 64])
+def test_filter_graph_matches_filter_device(c1, decs, b):
+    """CUDA-graph replay of the online step gives the same top-k as the eager
+    path, for full and partially filled batches, across repeated replays."""
+    g, A, batch, P = c1
+    dtype, dec, sdec = decs
+    h = ranking.h_alpha(float(g["alpha"]))
+    cap = int(batch.y_ptr[b])
+    fg = ranking.FilterGraph(sdec, h, b=b, nnz_cap=cap, topk=100)
+    for start in (0, b, 2 * b):
+        if start >= batch.b:
+            continue
+        stop = min(start + b, batch.b)
+        s, e = batch.y_ptr[start], batch.y_ptr[stop]
+        sub = ranking.QueryBatch(batch.size, batch.y_ptr[start:stop + 1] - s, batch.y_idx[s:e], batch.y_val[s:e])
+        if int(sub.y_ptr[-1]) > cap:
+            continue
+        res = fg.run(sub)
+        ti = res.top_idx[: sub.b].cpu().numpy()
+        tv = res.top_val[: sub.b].cpu().numpy()
+        ref_i, ref_v = ranking.top_k(sdec, h, sub, k=100)
+        np.testing.assert_array_equal(ti, ref_i)
+        np.testing.assert_array_equal(tv, ref_v.astype(tv.dtype))
+    # partially filled batch: trailing queries are empty
+    one = ranking.QueryBatch(batch.size, batch.y_ptr[:2], batch.y_idx[: batch.y_ptr[1]], batch.y_val[: batch.y_ptr[1]])
+    res = fg.run(one)
+    ref_i, _ = ranking.top_k(sdec, h, one, k=100)
+    np.testing.assert_array_equal(res.top_idx[:1].cpu().numpy(), ref_i)
