@@ -49,6 +49,7 @@ constexpr int kThreads = 192;
 constexpr int kBK = 64;            // K bytes (int8 elements) per stage = one 64B swizzle atom
 constexpr int kSlices = 4;         // slice planes produced
 constexpr int64_t kMaxK = 65536;   // reduction length per launch (int32-exact bound: 131072)
+constexpr int kApplyGroup = 32;    // column tiles per L2-resident group in the apply raster
 
 // --------------------------------------------------------------- exponents --
 __device__ __forceinline__ int exp_above(double m) {
@@ -228,6 +229,13 @@ __device__ __forceinline__ uint64_t desc_sw64(uint32_t saddr) {
   return d;
 }
 
+// x * 2^k: an exact multiply by a constructed power of two in the normal
+// range, ldexp (with its range handling) otherwise
+__device__ __forceinline__ double scale_pow2(double x, int k) {
+  if (k >= -1022 && k <= 1023) return x * __hiloint2double((k + 1023) << 20, 0);
+  return ldexp(x, k);
+}
+
 __device__ __forceinline__ void tmem_ld32_i(uint32_t taddr, int (&v)[32]) {
   float f[32];
   tmem_ld32(taddr, f);
@@ -244,7 +252,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     oz_gemm_kernel(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUtensorMap mB, int rowsA,
                    int rowsB, int64_t planeA_rows, int64_t planeB_rows, int64_t K, int tiles_n, int64_t k_per_split,
                    const int* __restrict__ eA, const int* __restrict__ eB, int symmetric, double* __restrict__ P,
-                   float* __restrict__ Out, int64_t ldo) {
+                   float* __restrict__ Out, int64_t ldo, int vec_out) {
   using Cfg = OzCfg<N, STAGES, LEVELS, BPL>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
@@ -253,7 +261,22 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* tfull = empty + STAGES;
   uint32_t* tmem_slot = (uint32_t*)(tfull + 1);
 
-  const int ti = (int)(blockIdx.x / tiles_n), tj = (int)(blockIdx.x % tiles_n);
+  int ti, tj;
+  if (MODE == 1) {
+    // apply: column tiles in groups of kApplyGroup, all row tiles swept per
+    // group -- the group's B slices (kApplyGroup x 2.8 MB at k = 5500) stay
+    // L2-resident while A row blocks stream; tj fastest inside a group so an
+    // A block is reused by consecutive CTAs
+    const int tiles_m = (int)((rowsA + 127) / 128);
+    const int per_group = tiles_m * kApplyGroup;
+    const int g = (int)blockIdx.x / per_group, rr = (int)blockIdx.x % per_group;
+    const int gw = min(kApplyGroup, tiles_n - g * kApplyGroup);
+    ti = rr / gw;
+    tj = g * kApplyGroup + rr % gw;
+  } else {
+    ti = (int)(blockIdx.x / tiles_n);
+    tj = (int)(blockIdx.x % tiles_n);
+  }
   const int i0 = ti * 128, j0 = tj * N;
   if (MODE == 0 && symmetric && j0 + N - 1 < i0) return;  // strictly below the diagonal: mirrored later
   const int64_t kb0 = (int64_t)blockIdx.y * k_per_split;
@@ -356,19 +379,35 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       if (!row_ok) continue;
       const int cbase = j0 + cc * 32;
-      if (MODE == 0) {
-        double* prow = P + ((int64_t)blockIdx.y * rowsA + row) * (int64_t)rowsB;
 #pragma unroll
-        for (int t = 0; t < 32; ++t) {
-          const int col = cbase + t;
-          if (col < rowsB) prow[col] = ldexp(v[t], ea + eB[col] - 2048 - 12);
+      for (int t = 0; t < 32; ++t) {
+        const int col = cbase + t < rowsB ? cbase + t : rowsB - 1;
+        v[t] = scale_pow2(v[t], ea + eB[col] - 2048 - 12);
+      }
+      // 16-byte stores when the whole 32-column chunk is in range and aligned
+      // (a warp writes 32 different rows: wide stores cut sector traffic 4x/2x)
+      const bool full = vec_out && cbase + 32 <= rowsB;
+      if (MODE == 0) {
+        double* prow = P + ((int64_t)blockIdx.y * rowsA + row) * (int64_t)rowsB + cbase;
+        if (full) {
+#pragma unroll
+          for (int t = 0; t < 32; t += 2) *reinterpret_cast<double2*>(prow + t) = make_double2(v[t], v[t + 1]);
+        } else {
+#pragma unroll
+          for (int t = 0; t < 32; ++t)
+            if (cbase + t < rowsB) prow[t] = v[t];
         }
       } else {
-        float* orow = Out + (int64_t)row * ldo;
+        float* orow = Out + (int64_t)row * ldo + cbase;
+        if (full) {
 #pragma unroll
-        for (int t = 0; t < 32; ++t) {
-          const int col = cbase + t;
-          if (col < rowsB) orow[col] = (float)ldexp(v[t], ea + eB[col] - 2048 - 12);
+          for (int t = 0; t < 32; t += 4)
+            *reinterpret_cast<float4*>(orow + t) =
+                make_float4((float)v[t], (float)v[t + 1], (float)v[t + 2], (float)v[t + 3]);
+        } else {
+#pragma unroll
+          for (int t = 0; t < 32; ++t)
+            if (cbase + t < rowsB) orow[t] = (float)v[t];
         }
       }
     }
@@ -466,8 +505,11 @@ int launch_oz(fsr_ctx* ctx, dim3 grid, const CUtensorMap& mA, const CUtensorMap&
     FSR_TRY(set_smem(ctx, oz_gemm_kernel<MODE, N, STAGES, LEVELS, BPL>, Cfg::SMEM));
     attr = true;
   }
+  // 16-byte epilogue stores need 16-byte aligned rows
+  const int vec_out = MODE == 0 ? (rowsB % 2 == 0 && ((uintptr_t)P & 15) == 0)
+                                : (ldo % 4 == 0 && ((uintptr_t)Out & 15) == 0);
   oz_gemm_kernel<MODE, N, STAGES, LEVELS, BPL><<<grid, kThreads, Cfg::SMEM, ctx->stream>>>(
-      mA, mB, rowsA, rowsB, pA, pB, K, tiles_n, kps, eA, eB, sym, P, Out, ldo);
+      mA, mB, rowsA, rowsB, pA, pB, K, tiles_n, kps, eA, eB, sym, P, Out, ldo, vec_out);
   return fsr::launched(ctx, MODE == 0 ? "oz_gram_kernel" : "oz_apply_kernel");
 }
 
