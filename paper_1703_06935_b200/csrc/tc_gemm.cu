@@ -259,30 +259,35 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* full = (uint64_t*)(smem + STAGES * Cfg::STAGE_BYTES);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
-  uint32_t* tmem_slot = (uint32_t*)(tfull + 1);
+  uint64_t* tempty = tfull + 1;
+  uint32_t* tmem_slot = (uint32_t*)(tempty + 1);
 
-  int ti, tj;
-  if (MODE == 1) {
-    // apply: column tiles in groups of kApplyGroup, all row tiles swept per
-    // group -- the group's B slices (kApplyGroup x 2.8 MB at k = 5500) stay
-    // L2-resident while A row blocks stream; tj fastest inside a group so an
-    // A block is reused by consecutive CTAs
-    const int tiles_m = (int)((rowsA + 127) / 128);
-    const int per_group = tiles_m * kApplyGroup;
-    const int g = (int)blockIdx.x / per_group, rr = (int)blockIdx.x % per_group;
-    const int gw = min(kApplyGroup, tiles_n - g * kApplyGroup);
-    ti = rr / gw;
-    tj = g * kApplyGroup + rr % gw;
-  } else {
-    ti = (int)(blockIdx.x / tiles_n);
-    tj = (int)(blockIdx.x % tiles_n);
-  }
-  const int i0 = ti * 128, j0 = tj * N;
-  if (MODE == 0 && symmetric && j0 + N - 1 < i0) return;  // strictly below the diagonal: mirrored later
+  // Persistent over output tiles (MODE 1: grid = #SMs; MODE 0: one tile per
+  // CTA): the TMA warp runs ahead into the next tile while the epilogue
+  // drains TMEM, and setup is paid once per CTA.
+  const int tiles_m = (int)((rowsA + 127) / 128);
+  const int total = tiles_m * tiles_n;
   const int64_t kb0 = (int64_t)blockIdx.y * k_per_split;
   const int64_t kb1 = min(K, kb0 + k_per_split);
   const int iters = kb1 > kb0 ? (int)((kb1 - kb0 + kBK - 1) / kBK) : 0;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // tile index -> (row tile, column tile); false if the tile is skipped
+  auto tile_of = [&](int idx, int& ti, int& tj) -> bool {
+    if (MODE == 1) {
+      // column tiles in groups of kApplyGroup, all row tiles swept per group:
+      // the group's B slices stay L2-resident while A row blocks stream; tj
+      // fastest inside a group so an A block is reused by neighbouring tiles
+      const int per_group = tiles_m * kApplyGroup;
+      const int g = idx / per_group, rr = idx % per_group;
+      const int gw = min(kApplyGroup, tiles_n - g * kApplyGroup);
+      ti = rr / gw;
+      tj = g * kApplyGroup + rr % gw;
+      return true;
+    }
+    ti = idx / tiles_n;
+    tj = idx % tiles_n;
+    return !(symmetric && tj * N + N - 1 < ti * 128);  // strictly below the diagonal: mirrored later
+  };
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -290,6 +295,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&empty[s], 1);
     }
     mbar_init(&tfull[0], 1);
+    mbar_init(&tempty[0], 4);  // one arrive per epilogue warp
     fence_barrier_init();
   }
   if (warp == 0 && lane == 0) {
@@ -303,115 +309,144 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tmem = *tmem_slot;
 
   if (warp == 0) {
-    for (int it = 0; it < iters; ++it) {
-      const int s = it % STAGES;
-      mbar_wait(&empty[s], ((it / STAGES) & 1) ^ 1);
-      if (lane == 0) {
-        uint8_t* st = smem + s * Cfg::STAGE_BYTES;
-        mbar_expect_tx(&full[s], Cfg::STAGE_BYTES);
-        const int kk = (int)(kb0 + (int64_t)it * kBK);
+    int g = 0;  // stage-ring position across tiles
+    for (int idx = blockIdx.x; idx < total; idx += gridDim.x) {
+      int ti, tj;
+      if (!tile_of(idx, ti, tj)) continue;
+      const int i0 = ti * 128, j0 = tj * N;
+      for (int it = 0; it < iters; ++it, ++g) {
+        const int s = g % STAGES;
+        mbar_wait(&empty[s], ((g / STAGES) & 1) ^ 1);
+        if (lane == 0) {
+          uint8_t* st = smem + s * Cfg::STAGE_BYTES;
+          mbar_expect_tx(&full[s], Cfg::STAGE_BYTES);
+          const int kk = (int)(kb0 + (int64_t)it * kBK);
 #pragma unroll
-        for (int p = 0; p < Cfg::APLANES; ++p)
-          tma_load_2d(st + p * Cfg::A_PLANE, &mA, &full[s], kk, (int)(p * planeA_rows + i0));
+          for (int p = 0; p < Cfg::APLANES; ++p)
+            tma_load_2d(st + p * Cfg::A_PLANE, &mA, &full[s], kk, (int)(p * planeA_rows + i0));
 #pragma unroll
-        for (int p = 0; p < Cfg::BPLANES; ++p)
-          tma_load_2d(st + Cfg::APLANES * Cfg::A_PLANE + p * Cfg::B_PLANE, &mB, &full[s], kk,
-                      (int)(p * planeB_rows + j0));
+          for (int p = 0; p < Cfg::BPLANES; ++p)
+            tma_load_2d(st + Cfg::APLANES * Cfg::A_PLANE + p * Cfg::B_PLANE, &mB, &full[s], kk,
+                        (int)(p * planeB_rows + j0));
+        }
+        __syncwarp();
       }
-      __syncwarp();
     }
   } else if (warp == 1) {
     constexpr uint32_t idesc = idesc_i8(128, N);
-    for (int it = 0; it < iters; ++it) {
-      const int s = it % STAGES;
-      mbar_wait(&full[s], (it / STAGES) & 1);
-      tc_fence_after();
-      if (lane == 0) {
-        const uint32_t base = smem_u32(smem + s * Cfg::STAGE_BYTES);
-        const uint32_t bbase = base + Cfg::APLANES * Cfg::A_PLANE;
-#pragma unroll
-        for (int ks = 0; ks < kBK / 32; ++ks) {
-          uint64_t a[Cfg::APLANES], b[Cfg::BPLANES];
-#pragma unroll
-          for (int p = 0; p < Cfg::APLANES; ++p) a[p] = desc_sw64(base + p * Cfg::A_PLANE + ks * 32);
-#pragma unroll
-          for (int p = 0; p < Cfg::BPLANES; ++p) b[p] = desc_sw64(bbase + p * Cfg::B_PLANE + ks * 32);
-          const uint32_t acc = (it == 0 && ks == 0) ? 0u : 1u;
-          // level l accumulates the slice pairs (t, l - t) that are kept; the
-          // first product issued into each accumulator starts it (acc == 0)
-#pragma unroll
-          for (int l = 0; l < LEVELS; ++l) {
-            const int t0 = l - (Cfg::BPLANES - 1) > 0 ? l - (Cfg::BPLANES - 1) : 0;
-#pragma unroll
-            for (int t = t0; t <= l; ++t) mma_i8(tmem + l * N, a[t], b[l - t], idesc, t == t0 ? acc : 1u);
-          }
-        }
-        mma_commit(&empty[s]);
-        if (it == iters - 1) mma_commit(&tfull[0]);
+    int g = 0, tcount = 0;
+    for (int idx = blockIdx.x; idx < total; idx += gridDim.x) {
+      int ti, tj;
+      if (!tile_of(idx, ti, tj)) continue;
+      if (tcount > 0) {  // the epilogue has drained the previous tile's accumulators
+        mbar_wait(&tempty[0], (tcount - 1) & 1);
+        tc_fence_after();
       }
-      __syncwarp();
+      for (int it = 0; it < iters; ++it, ++g) {
+        const int s = g % STAGES;
+        mbar_wait(&full[s], (g / STAGES) & 1);
+        tc_fence_after();
+        // descriptors are warp-uniform (computed by the whole warp, so they can
+        // live in uniform registers); one elected lane issues the MMAs.  A
+        // descriptor's start-address field is addr >> 4, so an offset is a
+        // 64-bit add of (offset >> 4) while the field does not overflow.
+        const uint64_t d0 = desc_sw64(smem_u32(smem + s * Cfg::STAGE_BYTES));
+        if (lane == 0) {
+#pragma unroll
+          for (int ks = 0; ks < kBK / 32; ++ks) {
+            uint64_t a[Cfg::APLANES], b[Cfg::BPLANES];
+#pragma unroll
+            for (int p = 0; p < Cfg::APLANES; ++p) a[p] = d0 + (uint64_t)((p * Cfg::A_PLANE + ks * 32) >> 4);
+#pragma unroll
+            for (int p = 0; p < Cfg::BPLANES; ++p)
+              b[p] = d0 + (uint64_t)((Cfg::APLANES * Cfg::A_PLANE + p * Cfg::B_PLANE + ks * 32) >> 4);
+            const uint32_t acc = (it == 0 && ks == 0) ? 0u : 1u;
+            // level l accumulates the kept slice pairs (t, l - t); the first
+            // product issued into each accumulator starts it (acc == 0)
+#pragma unroll
+            for (int l = 0; l < LEVELS; ++l) {
+              const int t0 = l - (Cfg::BPLANES - 1) > 0 ? l - (Cfg::BPLANES - 1) : 0;
+#pragma unroll
+              for (int t = t0; t <= l; ++t) mma_i8(tmem + l * N, a[t], b[l - t], idesc, t == t0 ? acc : 1u);
+            }
+          }
+          mma_commit(&empty[s]);
+          if (it == iters - 1) mma_commit(&tfull[0]);
+        }
+        __syncwarp();
+      }
+      ++tcount;
     }
   } else {
     const int q = warp & 3;
-    const int row = i0 + 32 * q + lane;
-    const bool row_ok = row < rowsA;
-    const int ea = row_ok ? eA[row] - 2048 : 0;
     const uint32_t tl = tmem + ((uint32_t)(32 * q) << 16);
-    if (iters > 0) {
-      mbar_wait(&tfull[0], 0);
-      tc_fence_after();
-    }
-#pragma unroll 1
-    for (int cc = 0; cc < N / 32; ++cc) {
-      double v[32];
-#pragma unroll
-      for (int t = 0; t < 32; ++t) v[t] = 0.0;
+    int tcount = 0;
+    for (int idx = blockIdx.x; idx < total; idx += gridDim.x) {
+      int ti, tj;
+      if (!tile_of(idx, ti, tj)) continue;
+      const int i0 = ti * 128, j0 = tj * N;
+      const int row = i0 + 32 * q + lane;
+      const bool row_ok = row < rowsA;
+      const int ea = row_ok ? eA[row] - 2048 : 0;
       if (iters > 0) {
-        double scale = 1.0;
+        mbar_wait(&tfull[0], tcount & 1);
+        tc_fence_after();
+      }
+#pragma unroll 1
+      for (int cc = 0; cc < N / 32; ++cc) {
+        double v[32];
 #pragma unroll
-        for (int l = 0; l < LEVELS; ++l) {
-          int acc[32];
-          tmem_ld32_i(tl + l * N + cc * 32, acc);
+        for (int t = 0; t < 32; ++t) v[t] = 0.0;
+        if (iters > 0) {
+          double scale = 1.0;
 #pragma unroll
-          for (int t = 0; t < 32; ++t) v[t] += (double)acc[t] * scale;
-          scale *= 0x1p-7;
+          for (int l = 0; l < LEVELS; ++l) {
+            int acc[32];
+            tmem_ld32_i(tl + l * N + cc * 32, acc);
+#pragma unroll
+            for (int t = 0; t < 32; ++t) v[t] += (double)acc[t] * scale;
+            scale *= 0x1p-7;
+          }
         }
-      }
-      if (!row_ok) continue;
-      const int cbase = j0 + cc * 32;
+        if (!row_ok) continue;
+        const int cbase = j0 + cc * 32;
 #pragma unroll
-      for (int t = 0; t < 32; ++t) {
-        const int col = cbase + t < rowsB ? cbase + t : rowsB - 1;
-        v[t] = scale_pow2(v[t], ea + eB[col] - 2048 - 12);
-      }
-      // 16-byte stores when the whole 32-column chunk is in range and aligned
-      // (a warp writes 32 different rows: wide stores cut sector traffic 4x/2x)
-      const bool full = vec_out && cbase + 32 <= rowsB;
-      if (MODE == 0) {
-        double* prow = P + ((int64_t)blockIdx.y * rowsA + row) * (int64_t)rowsB + cbase;
-        if (full) {
+        for (int t = 0; t < 32; ++t) {
+          const int col = cbase + t < rowsB ? cbase + t : rowsB - 1;
+          v[t] = scale_pow2(v[t], ea + eB[col] - 2048 - 12);
+        }
+        // 16-byte stores when the whole 32-column chunk is in range and aligned
+        // (a warp writes 32 different rows: wide stores cut sector traffic 4x/2x)
+        const bool full_chunk = vec_out && cbase + 32 <= rowsB;
+        if (MODE == 0) {
+          double* prow = P + ((int64_t)blockIdx.y * rowsA + row) * (int64_t)rowsB + cbase;
+          if (full_chunk) {
 #pragma unroll
-          for (int t = 0; t < 32; t += 2) *reinterpret_cast<double2*>(prow + t) = make_double2(v[t], v[t + 1]);
+            for (int t = 0; t < 32; t += 2) *reinterpret_cast<double2*>(prow + t) = make_double2(v[t], v[t + 1]);
+          } else {
+#pragma unroll
+            for (int t = 0; t < 32; ++t)
+              if (cbase + t < rowsB) prow[t] = v[t];
+          }
         } else {
+          float* orow = Out + (int64_t)row * ldo + cbase;
+          if (full_chunk) {
 #pragma unroll
-          for (int t = 0; t < 32; ++t)
-            if (cbase + t < rowsB) prow[t] = v[t];
-        }
-      } else {
-        float* orow = Out + (int64_t)row * ldo + cbase;
-        if (full) {
+            for (int t = 0; t < 32; t += 4)
+              *reinterpret_cast<float4*>(orow + t) =
+                  make_float4((float)v[t], (float)v[t + 1], (float)v[t + 2], (float)v[t + 3]);
+          } else {
 #pragma unroll
-          for (int t = 0; t < 32; t += 4)
-            *reinterpret_cast<float4*>(orow + t) =
-                make_float4((float)v[t], (float)v[t + 1], (float)v[t + 2], (float)v[t + 3]);
-        } else {
-#pragma unroll
-          for (int t = 0; t < 32; ++t)
-            if (cbase + t < rowsB) orow[t] = (float)v[t];
+            for (int t = 0; t < 32; ++t)
+              if (cbase + t < rowsB) orow[t] = (float)v[t];
+          }
         }
       }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[0]);
+      ++tcount;
     }
-    tc_fence_before();
   }
   __syncthreads();
   if (warp == 1) {
@@ -622,7 +657,8 @@ int tc_apply(fsr_ctx* ctx, int64_t n, int64_t K, const float* A, int64_t lda, in
     FSR_TRY(launched(ctx, "slice_rows_fused_kernel"));
     CUtensorMap mA;
     FSR_TRY(make_map_u8(ctx, &mA, sR, kSlices * rows, pk, pk, 128));
-    dim3 grid((unsigned)(ceil_div(rows, 128) * tiles_n), 1);
+    // persistent: one CTA per SM walks the tiles (see oz_gemm_kernel)
+    dim3 grid((unsigned)std::min<int64_t>(ceil_div(rows, 128) * tiles_n, ctx->num_sms), 1);
     if (m_slices == 1)
       FSR_TRY((launch_oz<1, 4, 1>(ctx, grid, mA, mB, (int)rows, (int)N2, rows, N2, pk, tiles_n, pk, eR, eM, 0,
                                   nullptr, Out + s0 * ldo, ldo)));
