@@ -730,6 +730,28 @@ class FilterGraph:
         self.stage(batch)
         return self.replay()
 
+    def submit(self, batch: QueryBatch):
+        """Asynchronous step: stage, replay and start the top-k D2H into pinned
+        host buffers; ``fetch`` returns them.  Alternating two FilterGraphs
+        overlaps one batch's host work with the other's device work."""
+        import torch
+
+        if not hasattr(self, "_h_idx"):
+            self._h_idx = torch.empty(self.res.top_idx.shape, dtype=torch.int64).pin_memory()
+            self._h_val = torch.empty(self.res.top_val.shape, dtype=self.res.top_val.dtype).pin_memory()
+        self.run(batch)
+        self._h_idx.copy_(self.res.top_idx, non_blocking=True)
+        self._h_val.copy_(self.res.top_val, non_blocking=True)
+        self._fetched = torch.cuda.Event()
+        self._fetched.record()
+        self._done = self._fetched  # staging buffers are reusable once the copies are done too
+        self._nb = batch.b
+
+    def fetch(self):
+        """Wait for the last ``submit`` and return host (top_idx, top_val) of its queries."""
+        self._fetched.synchronize()
+        return self._h_idx[: self._nb].numpy(), self._h_val[: self._nb].numpy()
+
 
 def torch_from_numpy_cast(a, dtype):
     import torch

@@ -172,3 +172,15 @@ def test_filter_graph_matches_filter_device(c1, decs, b):
     res = fg.run(one)
     ref_i, _ = ranking.top_k(sdec, h, one, k=100)
     np.testing.assert_array_equal(res.top_idx[:1].cpu().numpy(), ref_i)
+    # asynchronous submit / fetch with two graphs in flight
+    fg2 = ranking.FilterGraph(sdec, h, b=b, nnz_cap=cap, topk=100)
+    sub0 = ranking.QueryBatch(batch.size, batch.y_ptr[: b + 1], batch.y_idx[: batch.y_ptr[b]],
+                              batch.y_val[: batch.y_ptr[b]])
+    fg.submit(one)
+    fg2.submit(sub0)
+    i1, _ = fg.fetch()
+    i0, v0 = fg2.fetch()
+    np.testing.assert_array_equal(i1, ref_i)
+    ref0_i, ref0_v = ranking.top_k(sdec, h, sub0, k=100)
+    np.testing.assert_array_equal(i0, ref0_i)
+    np.testing.assert_array_equal(v0, ref0_v.astype(v0.dtype))
