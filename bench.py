@@ -473,11 +473,13 @@ def run_fsr(args, cfg, n, rank, world, local_rank):
     off_clk = off_clocks.stop()
     stages = {name: ctx.stage_time(name) for name in N.STAGES}
     torch.cuda.empty_cache()
-    si_s = ev[0].elapsed_time(ev[1]) / 1e3
-    rr_s = ev[1].elapsed_time(ev[2]) / 1e3
-    sp_s = ev[2].elapsed_time(ev[3]) / 1e3
+    si_s = max_over_ranks(ev[0].elapsed_time(ev[1]) / 1e3, world)
+    rr_s = max_over_ranks(ev[1].elapsed_time(ev[2]) / 1e3, world)
+    sp_s = max_over_ranks(ev[2].elapsed_time(ev[3]) / 1e3, world)
     spmm_ms, spmm_cnt = stages["spmm"]
-    spmm_ms_iter = spmm_ms / max(spmm_cnt, 1)
+    # per-iteration time of the slowest rank; the byte counts below are whole-matrix,
+    # so the GB/s figures are job aggregates and the fractions are over world x peak
+    spmm_ms_iter = max_over_ranks(spmm_ms / max(spmm_cnt, 1), world)
     nnz_s = S.nnz
     spmm_bytes = nnz_s * (es + 4) + (n + 1) * 8 + 2 * es * n * r_hat
     spmm_gbs = spmm_bytes / (spmm_ms_iter * 1e-3) / 1e9
@@ -488,9 +490,9 @@ def run_fsr(args, cfg, n, rank, world, local_rank):
     offline = {
         "si_time_s": si_s, "rayleigh_ritz_s": rr_s, "sparsify_s": sp_s, "decompose_total_s": si_s + rr_s + sp_s,
         "spmm_ms_per_iter": spmm_ms_iter, "spmm_launches": spmm_cnt, "spmm_algorithmic_bytes": spmm_bytes,
-        "spmm_gbs": spmm_gbs, "spmm_hbm_frac": spmm_gbs / peak_gbs,
+        "spmm_gbs": spmm_gbs, "spmm_hbm_frac": spmm_gbs / (world * peak_gbs),
         "spmm_gather_bytes": spmm_gather, "spmm_gather_gbs": spmm_gather_gbs,
-        "spmm_gather_hbm_frac": spmm_gather_gbs / peak_gbs,
+        "spmm_gather_hbm_frac": spmm_gather_gbs / (world * peak_gbs),
         "spmm_fp32_tflops": 2.0 * nnz_s * r_hat / (spmm_ms_iter * 1e-3) / 1e12,
         "stage_ms": {k: round(v[0], 3) for k, v in stages.items() if v[1]},
         "nnz_W": nnz_w, "isolated_vertices": isolated, "kept_nnz": sdec.U_device.nnz, "inputs_build_s": t_inputs,
