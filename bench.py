@@ -534,8 +534,7 @@ def run_fsr(args, cfg, n, rank, world, local_rank):
     barrier(world)
     launches = ctx.launches - launches0
     dev_ms = sum(s.elapsed_time(e) for s, e in zip(starts, ends))
-    on_stages = {name: ctx.stage_time(name) for name in ("project", "filter_spmm", "transpose",
-                                                          "copy_uncovered", "topk")}
+    on_stages = {name: ctx.stage_time(name) for name in ("project", "filter_spmm", "copy_uncovered", "topk")}
     dev_ms_max = max_over_ranks(dev_ms, world)
     value = world * b * args.steps / (dev_ms_max / 1e3)
 

@@ -69,7 +69,7 @@ enum fsr_stage {
   FSR_STAGE_GAUSSIAN = 0, FSR_STAGE_NORMALIZE = 1, FSR_STAGE_SPMM = 2, FSR_STAGE_GRAM = 3,
   FSR_STAGE_CHOLESKY = 4, FSR_STAGE_APPLY = 5, FSR_STAGE_EIGH = 6, FSR_STAGE_LIFT = 7,
   FSR_STAGE_SIGNS = 8, FSR_STAGE_HISTOGRAM = 9, FSR_STAGE_COMPACT = 10, FSR_STAGE_PROJECT = 11,
-  FSR_STAGE_FILTER_SPMM = 12, FSR_STAGE_TRANSPOSE = 13, FSR_STAGE_COPY_UNCOVERED = 14,
+  FSR_STAGE_FILTER_SPMM = 12, FSR_STAGE_TRANSPOSE = 13 /* reserved */, FSR_STAGE_COPY_UNCOVERED = 14,
   FSR_STAGE_TOPK = 15, FSR_STAGE_HOUSEHOLDER = 16, FSR_NUM_STAGES = 17
 };
 int fsr_ctx_enable_timing(fsr_ctx* ctx, int on);

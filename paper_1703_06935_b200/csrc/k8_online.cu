@@ -133,22 +133,6 @@ __global__ void __launch_bounds__(256) project_smem_kernel(int64_t r, int64_t b,
 }
 
 template <typename T>
-__global__ void transpose_kernel(int64_t rows, int64_t cols, const T* __restrict__ in, T* __restrict__ out) {
-  // in: rows x cols row-major -> out: cols x rows row-major
-  __shared__ T tile[32][33];
-  const int64_t c0 = (int64_t)blockIdx.x * 32, r0 = (int64_t)blockIdx.y * 32;
-  for (int k = threadIdx.y; k < 32; k += 8) {
-    const int64_t rr = r0 + k, cc = c0 + threadIdx.x;
-    if (rr < rows && cc < cols) tile[k][threadIdx.x] = in[rr * cols + cc];
-  }
-  __syncthreads();
-  for (int k = threadIdx.y; k < 32; k += 8) {
-    const int64_t cc = c0 + k, rr = r0 + threadIdx.x;
-    if (rr < rows && cc < cols) out[cc * rows + rr] = tile[threadIdx.x][k];
-  }
-}
-
-template <typename T>
 __global__ void copy_uncovered_kernel(int64_t n, const int64_t* __restrict__ y_ptr, const int64_t* __restrict__ y_idx,
                                       const T* __restrict__ y_val, const double* __restrict__ eta, T* __restrict__ X,
                                       int64_t ldx) {
