@@ -279,6 +279,7 @@ def _as_device_dec(dec) -> SpectralDecomposition:
 
 def filter(dec, h: TransferFunction, y: ObservationVector, copy_uncovered: bool | None = None) -> np.ndarray:
     """x = U h(Lambda) U^T y (``ranking.py:229-255``) for one query, on the device."""
+    dec = _as_device_dec(dec)
     if y.size != dec.n:
         raise ValueError(f"observation size {y.size} != decomposition size {dec.n}")
     return filter_batch(dec, h, [y], copy_uncovered=copy_uncovered)[0]
