@@ -207,6 +207,47 @@ def epilogue_case(n_q: int = 5, region_per_image: int = 4):
     np.savez_compressed(os.path.join(HERE, "epi.npz"), **out)
 
 
+def c2_reduced_case(n: int = 20_000, queries: int = 50, r: int = 400, p: int = 40, n_x: int = 5):
+    """C2's generator (d=512, 1000 Zipf clusters, k=50, gamma=3, tau=5%) at n=20k
+    (reduced C2), r=400, p=40, q=3."""
+    from dataclasses import replace
+
+    cfg = replace(CONFIGS["C2"], n=n, queries=queries, r=r, p=p)
+    t0 = time.perf_counter()
+    data, qv, _ = cluster_descriptors(cfg)
+    ds = DescriptorSet(data)
+    W = graph.build_mutual_knn_graph(ds, cfg.k, cfg.gamma)
+    S = graph.normalize_adjacency(W, graph.degrees(W))
+    t1 = time.perf_counter()
+    dec = spectral.decompose(S, cfg.r, p=cfg.p, q=cfg.q, seed=0)
+    sdec = spectral.sparsify(dec, cfg.tau)
+    h = ranking.h_alpha(cfg.alpha)
+    ys = [ranking.observation_vector(q, ds, cfg.y_top, cfg.gamma) for q in qv]
+    y_ptr = np.zeros(len(ys) + 1, dtype=np.int64)
+    y_ptr[1:] = np.cumsum([y.nnz for y in ys])
+    xa, xs, ta, ts = [], [], [], []
+    for j, y in enumerate(ys):
+        x = ranking.filter(dec, h, y)
+        x2 = ranking.filter(sdec, h, y)
+        ta.append(ranking.rank(x)[:100])
+        ts.append(ranking.rank(x2)[:100])
+        if j < n_x:
+            xa.append(x)
+            xs.append(x2)
+    flat = csr_support(sdec.U)
+    print(f"C2r: graph {t1 - t0:.1f}s total {time.perf_counter() - t0:.1f}s nnz(W)={W.nnz}")
+    np.savez_compressed(
+        os.path.join(HERE, "c2r.npz"),
+        W_indptr=W.csr.indptr.astype(np.int64), W_indices=W.csr.indices.astype(np.int32),
+        S_data=S.csr.data, lam=dec.eigenvalues, eta=dec.eta, sparse_eta=sdec.eta,
+        sparse_nnz=np.array(sdec.U.nnz), sparse_hash=np.array(support_hash(flat)),
+        y_ptr=y_ptr, y_idx=np.concatenate([y.indices for y in ys]), y_val=np.concatenate([y.values for y in ys]),
+        x_approx=np.array(xa), x_sparse=np.array(xs),
+        top_approx=np.array(ta, dtype=np.int32), top_sparse=np.array(ts, dtype=np.int32),
+        params=np.array([cfg.n, cfg.r, cfg.p, cfg.q, cfg.tau, 0]), alpha=np.array(cfg.alpha),
+    )
+
+
 def block_graph(sizes, seed: int, density: float = 0.08):
     """Symmetric nonnegative adjacency whose components have the given sizes
     (each block connected: a random spanning path plus random edges), vertices
@@ -265,7 +306,7 @@ def blockwise_case():
 
 
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["gaussian", "kat", "c1", "epi", "blockwise"]
+    which = sys.argv[1:] or ["gaussian", "kat", "c1", "epi", "blockwise", "c2r"]
     if "gaussian" in which:
         gaussian_cases()
     if "kat" in which:
@@ -276,4 +317,6 @@ if __name__ == "__main__":
         epilogue_case()
     if "blockwise" in which:
         blockwise_case()
+    if "c2r" in which:
+        c2_reduced_case()
     print("ok")

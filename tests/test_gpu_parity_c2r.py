@@ -1,0 +1,75 @@
+"""End-to-end parity on a reduced C2: C2's
+generator (d=512, 1000 Zipf-sized clusters, mutual kNN k=50, gamma=3, 5%
+sparsification) at n=20k with r=400, p=40, q=3, against the reference's own
+outputs (tests/golden/c2r.npz).  Same contract as the C1 test: Ritz values
+normwise 1e-5 (fp32) / 1e-10 (fp64), ranking vectors 1e-4 / 1e-9 relative
+L2, top-100 overlap >= 99%, exact sparse support in fp64.
+"""
+
+import hashlib
+
+import numpy as np
+import pytest
+import scipy.sparse as sp
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from paper_1703_06935_b200 import ranking, spectral  # noqa: E402
+from paper_1703_06935_b200.sparsemat import SparseSymmetricMatrix  # noqa: E402
+
+
+def rel_l2(a, b):
+    return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300)
+
+
+def overlap(a, b):
+    return len(set(a.tolist()) & set(b.tolist())) / len(b)
+
+
+@pytest.fixture(scope="module")
+def c2r(golden):
+    g = golden("c2r")
+    n, r, p, q, tau, seed = (int(v) for v in g["params"])
+    S = sp.csr_matrix((g["S_data"], g["W_indices"], g["W_indptr"]), shape=(n, n))
+    batch = ranking.QueryBatch(n, g["y_ptr"], g["y_idx"], g["y_val"])
+    return g, SparseSymmetricMatrix(S), batch, dict(n=n, r=r, p=p, q=q, tau=tau, seed=seed)
+
+
+@pytest.fixture(scope="module", params=["float64", "float32"])
+def decs(request, c2r):
+    g, A, batch, P = c2r
+    dec = spectral.decompose(A, P["r"], p=P["p"], q=P["q"], seed=P["seed"], dtype=request.param)
+    return request.param, dec, spectral.sparsify(dec, P["tau"])
+
+
+def test_c2r_ritz_and_eta(c2r, decs):
+    g, *_ = c2r
+    dtype, dec, _ = decs
+    err = np.abs(dec.eigenvalues - g["lam"]).max() / np.abs(g["lam"]).max()
+    assert err <= (1e-10 if dtype == "float64" else 1e-5), err
+    assert np.abs(dec.eta - g["eta"]).max() < (1e-8 if dtype == "float64" else 1e-4)
+
+
+def test_c2r_ranking(c2r, decs):
+    g, A, batch, P = c2r
+    dtype, dec, sdec = decs
+    h = ranking.h_alpha(float(g["alpha"]))
+    X = ranking.filter_batch(dec, h, batch)
+    tol = 1e-9 if dtype == "float64" else 1e-4
+    xa = g["x_approx"]
+    assert max(rel_l2(X[j], xa[j]) for j in range(xa.shape[0])) <= tol
+    ov = [overlap(ranking.rank(X[j])[:100], g["top_approx"][j]) for j in range(batch.b)]
+    assert np.mean(ov) >= 0.99 and min(ov) >= 0.95
+    Xs = ranking.filter_batch(sdec, h, batch)
+    ovs = [overlap(ranking.rank(Xs[j])[:100], g["top_sparse"][j]) for j in range(batch.b)]
+    assert np.mean(ovs) >= 0.99
+    if dtype == "float64":
+        coo = sdec.U.tocoo()
+        flat = np.sort(coo.row.astype(np.int64) * P["r"] + coo.col)
+        assert hashlib.sha256(flat.tobytes()).hexdigest() == str(g["sparse_hash"])
+        xs = g["x_sparse"]
+        assert max(rel_l2(Xs[j], xs[j]) for j in range(xs.shape[0])) <= 1e-9

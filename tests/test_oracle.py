@@ -173,3 +173,18 @@ def test_oracle_components_and_blockwise_match_reference(golden):
         assert variant == str(b[f"{tag}_variant"])
         _assert_same_spectral_operator(U, lam, b[f"{tag}_U"], b[f"{tag}_lam"], 1e-9)
         np.testing.assert_allclose(eta, b[f"{tag}_eta"], atol=1e-9)
+
+
+def test_c2_reduced_oracle_matches_reference(golden):
+    g = golden("c2r")
+    n, r, p, q, tau, seed = (int(v) for v in g["params"])
+    S = sp.csr_matrix((g["S_data"], g["W_indices"], g["W_indptr"]), shape=(n, n))
+    U, lam, eta = O.decompose(S, r, p=p, q=q, seed=seed)
+    np.testing.assert_allclose(lam, g["lam"], rtol=0, atol=1e-12)
+    w = O.transfer_values(O.h_alpha(float(g["alpha"])), lam)
+    sl = slice(g["y_ptr"][0], g["y_ptr"][1])
+    x = O.filter_scores(U, lam, eta, w, g["y_idx"][sl], g["y_val"][sl])
+    np.testing.assert_allclose(x, g["x_approx"][0], rtol=1e-8, atol=1e-12)
+    import hashlib
+    flat = O.sparsify_support(U, tau)
+    assert hashlib.sha256(flat.astype(np.int64).tobytes()).hexdigest() == str(g["sparse_hash"])
