@@ -42,6 +42,10 @@ CHOLQR2_SAFE = 0.1
 # R^-1 (see _cholqr_pass / fsr_apply_rinv_levels)
 FAST_FIRST_GRAM = True
 FAST_FIRST_APPLY = os.environ.get("FSR_FAST_FIRST_APPLY", "1") != "0"
+# float32 simultaneous iteration: intermediate rounds keep a well-conditioned
+# basis (max|Q^T Q - I| <= PRECOND_TOL) instead of an orthonormal one; see range_finder
+SI_SPAN_ONLY = os.environ.get("FSR_SI_SPAN_ONLY", "1") != "0"
+PRECOND_TOL = 0.25
 
 _MASK64 = (1 << 64) - 1
 
@@ -287,11 +291,43 @@ def range_finder(A, r_hat: int, q: int, seed: int, dtype="float64", device=None,
     dt = N.dtype_code(dt_t)
     Y = gaussian_block(n, r_hat, seed, dtype=dt_t, device=Ad.device)
     Q = torch.empty_like(Y)
-    for _ in range(q):
-        orthonormalize(Y, ctx, stats)
-        Q, Y = Y, Q  # Y now holds the orthonormal block
+    for t in range(q):
+        if SI_SPAN_ONLY and dt == N.F32 and t < q - 1:
+            # Only span(Q) of the intermediate rounds reaches the output (the
+            # last round is orthonormalised in full before Rayleigh-Ritz), so
+            # they need a well-conditioned basis, not an orthonormal one.  The
+            # Gaussian start block already is one when r_hat <= n / 4.
+            if t > 0 or 4 * r_hat > n:
+                _precondition(Y, ctx, stats)
+            elif stats is not None:
+                stats.append("start")
+        else:
+            orthonormalize(Y, ctx, stats)
+        Q, Y = Y, Q  # Y now holds the (orthonormal or well-conditioned) block
         _spmm(ctx, dt, Ad, Q, Y)
     return RangeBasis(Q=Q, B=Y, iterations_used=q, seed=seed)
+
+
+def _precondition(Y, ctx, stats=None):
+    """In place: Y <- Y R'^-1 with span(Y) kept and max|Y^T Y - I| <= PRECOND_TOL.
+
+    One CholeskyQR pass on 7-bit Gram and 7-bit R^-1 (span(Y M) = span(Y) for
+    any invertible M; Y's own slices stay 28-bit), then a 7-bit Gram checks
+    the conditioning; a full ``orthonormalize`` runs if the check fails.
+    """
+    import torch
+
+    dt = N.dtype_code(Y.dtype)
+    n, k = Y.shape
+    G = torch.empty(k, k, dtype=torch.float64, device=Y.device)
+    ok, _ = _cholqr_pass(ctx, dt, Y, G, fast_gram=True)
+    if ok:
+        ctx.call("gram_levels", n, k, N.ptr(Y), Y.stride(0), N.ptr(G), 0, 1)
+        if _max_dev(ctx, G) <= PRECOND_TOL:
+            if stats is not None:
+                stats.append("precond")
+            return Y
+    return orthonormalize(Y, ctx, stats)
 
 
 def _rayleigh_ritz(ctx, dt, Q, B, r):
