@@ -283,14 +283,36 @@ def sharded_range_finder(comm: Comm, ops, A_local, shard: Shard, r_hat: int, q: 
         raise ValueError(f"r_hat must lie in [1, n], got {r_hat} for n={shard.n}")
     if q < 1:
         raise ValueError("q must be at least 1")
+    from .spectral import SI_SPAN_ONLY
+
     Y = ops.gaussian(shard.n, r_hat, seed, shard.r0, shard.r1)
     Q = None
-    for _ in range(q):
-        Q = sharded_orthonormalize(comm, ops, Y, shard, dt_code, stats)
+    for t in range(q):
+        if SI_SPAN_ONLY and dt_code == N.F32 and t < q - 1:
+            # intermediate rounds: a well-conditioned basis suffices (spectral.range_finder)
+            Q = Y if (t == 0 and 4 * r_hat <= shard.n) else sharded_precondition(comm, ops, Y, shard, dt_code, stats)
+        else:
+            Q = sharded_orthonormalize(comm, ops, Y, shard, dt_code, stats)
         Qfull = comm.all_gather_rows(Q, shard.counts)
         Y = ops.spmm(A_local, Qfull)
         del Qfull
     return Q, Y
+
+
+def sharded_precondition(comm: Comm, ops, Y, shard: Shard, dt_code: int, stats=None):
+    """spectral._precondition over row shards: one 7-bit CholeskyQR pass, a 7-bit
+    Gram check, full CholeskyQR2 if the basis is not within PRECOND_TOL of orthonormal."""
+    from .spectral import PRECOND_TOL
+
+    R = ops.cholesky(comm.sum_ordered(ops.gram(Y, fast=True)))
+    if R is not None:
+        Y1 = ops.apply_rinv(R, Y, fast=True)
+        if ops.max_dev(comm.sum_ordered(ops.gram(Y1, fast=True))) <= PRECOND_TOL:
+            if stats is not None:
+                stats.append("precond")
+            return Y1
+        Y = Y1
+    return sharded_orthonormalize(comm, ops, Y, shard, dt_code, stats)
 
 
 def sharded_rayleigh_ritz(comm: Comm, ops, Q, B, r: int, shard: Shard):
