@@ -457,7 +457,9 @@ def run_fsr(args, cfg, n, rank, world, local_rank):
     torch.cuda.nvtx.range_push("fsr:offline")
     if world == 1:
         ev[0].record()
-        basis = spectral.range_finder(S, r_hat, q, 0, dtype=dt, device=device)
+        # the same schedule as spectral.decompose (timed in two parts)
+        basis = spectral.range_finder(S, r_hat, q, 0, dtype=dt, device=device,
+                                      _orthonormal_last=not spectral.fused_rr_enabled(dt))
         ev[1].record()
         dec = spectral.approx_eigendecomposition(S, basis, r)
         del basis

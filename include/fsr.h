@@ -154,6 +154,10 @@ int fsr_cross(fsr_ctx* ctx, int dtype, int64_t n_rows, int64_t k, const void* Q,
  * eigenvalues (host-synchronous), V (k x r, fp64, row-major) the eigenvectors.
  * C is destroyed. */
 int fsr_eigh_desc(fsr_ctx* ctx, int64_t k, double* C, int64_t r, double* lam_host, double* V);
+/* Generalised form for a non-orthonormal basis Q~ (C = Q~^T A Q~, G = Q~^T Q~,
+ * both destroyed): C v = lambda G v, top r by the same stable descending rule,
+ * V (k x r fp64) G-orthonormal so U = Q~ V is orthonormal.  cuSOLVER sygvd. */
+int fsr_eigh_gen_desc(fsr_ctx* ctx, int64_t k, double* C, double* G, int64_t r, double* lam_host, double* V);
 /* U (n_rows x r, dtype) = Q (n_rows x k) V (k x r). */
 int fsr_lift(fsr_ctx* ctx, int dtype, int64_t n_rows, int64_t k, int64_t r, const void* Q,
              int64_t ldq, const double* V, void* U, int64_t ldu);

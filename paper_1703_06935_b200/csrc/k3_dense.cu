@@ -386,29 +386,45 @@ int fsr_max_offdiag_error(fsr_ctx* ctx, int64_t k, const double* G, double* err_
   return FSR_OK;
 }
 
-int fsr_eigh_desc(fsr_ctx* ctx, int64_t k, double* C, int64_t r, double* lam_host, double* V) {
+// Shared by fsr_eigh_desc (C v = lambda v) and fsr_eigh_gen_desc (C v = lambda G v).
+static int eigh_impl(fsr_ctx* ctx, int64_t k, double* C, double* G, int64_t r, double* lam_host, double* V) {
   FSR_REQUIRE(ctx, k >= 1 && r >= 1 && r <= k && lam_host, "eigh_desc: bad shape");
   FSR_REQUIRE(ctx, k < (1 << 20), "eigh_desc: k too large");
   fsr::StageTimer timer(ctx, FSR_STAGE_EIGH);
   symmetrize_kernel<<<fsr::grid_for(k * k, 256, ctx, 8), 256, 0, ctx->stream>>>(k, C);
   FSR_TRY(fsr::launched(ctx, "symmetrize_kernel"));
+  if (G) {
+    symmetrize_kernel<<<fsr::grid_for(k * k, 256, ctx, 8), 256, 0, ctx->stream>>>(k, G);
+    FSR_TRY(fsr::launched(ctx, "symmetrize_kernel"));
+  }
   int lwork = 0;
   void* buf = nullptr;
-  FSR_SOLVER(ctx, cusolverDnDsyevd_bufferSize(ctx->solver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_UPPER, (int)k,
-                                              C, (int)k, C, &lwork));
+  if (G)
+    FSR_SOLVER(ctx, cusolverDnDsygvd_bufferSize(ctx->solver, CUSOLVER_EIG_TYPE_1, CUSOLVER_EIG_MODE_VECTOR,
+                                                CUBLAS_FILL_MODE_UPPER, (int)k, C, (int)k, G, (int)k, C, &lwork));
+  else
+    FSR_SOLVER(ctx, cusolverDnDsyevd_bufferSize(ctx->solver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_UPPER, (int)k,
+                                                C, (int)k, C, &lwork));
   const size_t bytes = ((size_t)lwork + k) * 8 + (size_t)r * 8 + 256;
   FSR_TRY(fsr::scratch(ctx, bytes, &buf));
   double* W = (double*)buf;
   int64_t* perm_dev = (int64_t*)(W + k);
   double* work = (double*)(perm_dev + r);
-  FSR_SOLVER(ctx, cusolverDnDsyevd(ctx->solver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_UPPER, (int)k, C, (int)k,
-                                   W, work, lwork, ctx->dev_info));
+  if (G)
+    FSR_SOLVER(ctx, cusolverDnDsygvd(ctx->solver, CUSOLVER_EIG_TYPE_1, CUSOLVER_EIG_MODE_VECTOR,
+                                     CUBLAS_FILL_MODE_UPPER, (int)k, C, (int)k, G, (int)k, W, work, lwork,
+                                     ctx->dev_info));
+  else
+    FSR_SOLVER(ctx, cusolverDnDsyevd(ctx->solver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_UPPER, (int)k, C,
+                                     (int)k, W, work, lwork, ctx->dev_info));
   std::vector<double> lam(k);
   int info = 0;
   FSR_CUDA(ctx, cudaMemcpyAsync(lam.data(), W, k * 8, cudaMemcpyDeviceToHost, ctx->stream));
   FSR_CUDA(ctx, cudaMemcpyAsync(&info, ctx->dev_info, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
   FSR_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
-  if (info != 0) return fsr::set_error(ctx, FSR_ENUMERICAL, "syevd failed to converge (info=%d)", info);
+  if (info != 0)
+    return fsr::set_error(ctx, FSR_ENUMERICAL, "%s failed (info=%d)%s", G ? "sygvd" : "syevd", info,
+                          G && info > k ? ": G not positive definite" : "");
   for (int64_t i = 0; i < k; ++i)
     if (!(lam[i] == lam[i])) return fsr::set_error(ctx, FSR_ENUMERICAL, "syevd produced NaN eigenvalues");
   // argsort(-lambda, kind="stable")[:r]
@@ -423,6 +439,15 @@ int fsr_eigh_desc(fsr_ctx* ctx, int64_t k, double* C, int64_t r, double* lam_hos
   // perm_dev lives in scratch: make sure the gather consumed it before reuse
   FSR_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
   return FSR_OK;
+}
+
+int fsr_eigh_desc(fsr_ctx* ctx, int64_t k, double* C, int64_t r, double* lam_host, double* V) {
+  return eigh_impl(ctx, k, C, nullptr, r, lam_host, V);
+}
+
+int fsr_eigh_gen_desc(fsr_ctx* ctx, int64_t k, double* C, double* G, int64_t r, double* lam_host, double* V) {
+  FSR_REQUIRE(ctx, G != nullptr, "eigh_gen_desc: missing G");
+  return eigh_impl(ctx, k, C, G, r, lam_host, V);
 }
 
 int fsr_lift(fsr_ctx* ctx, int dtype, int64_t n_rows, int64_t k, int64_t r, const void* Q, int64_t ldq,

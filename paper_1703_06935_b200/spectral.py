@@ -46,6 +46,9 @@ FAST_FIRST_APPLY = os.environ.get("FSR_FAST_FIRST_APPLY", "1") != "0"
 # basis (max|Q^T Q - I| <= PRECOND_TOL) instead of an orthonormal one; see range_finder
 SI_SPAN_ONLY = os.environ.get("FSR_SI_SPAN_ONLY", "1") != "0"
 PRECOND_TOL = 0.25
+# decompose (fp32): the last round is preconditioned too and Rayleigh-Ritz
+# solves the generalised problem with G = Q^T Q (see _rayleigh_ritz)
+FUSED_RR = os.environ.get("FSR_FUSED_RR", "1") != "0"
 
 _MASK64 = (1 << 64) - 1
 
@@ -271,7 +274,8 @@ def _spmm(ctx, dt, Ad: DeviceCSR, X, Y):
              N.ptr(X), X.stride(0), N.ptr(Y), Y.stride(0))
 
 
-def range_finder(A, r_hat: int, q: int, seed: int, dtype="float64", device=None, stats=None) -> RangeBasis:
+def range_finder(A, r_hat: int, q: int, seed: int, dtype="float64", device=None, stats=None,
+                 _orthonormal_last: bool = True) -> RangeBasis:
     """Simultaneous iteration (``spectral.py:147-171``) on the device.
 
     Start block from the seeded counter stream (K0); q rounds of
@@ -291,8 +295,13 @@ def range_finder(A, r_hat: int, q: int, seed: int, dtype="float64", device=None,
     dt = N.dtype_code(dt_t)
     Y = gaussian_block(n, r_hat, seed, dtype=dt_t, device=Ad.device)
     Q = torch.empty_like(Y)
+    gram_last = None
     for t in range(q):
-        if SI_SPAN_ONLY and dt == N.F32 and t < q - 1:
+        if t == q - 1 and not _orthonormal_last:
+            # decompose's fused path: one preconditioning CholeskyQR pass plus the
+            # exact Gram G of the result, which Rayleigh-Ritz then absorbs
+            Y, gram_last = _precondition_with_gram(Y, ctx, stats)
+        elif SI_SPAN_ONLY and dt == N.F32 and t < q - 1:
             # Only span(Q) of the intermediate rounds reaches the output (the
             # last round is orthonormalised in full before Rayleigh-Ritz), so
             # they need a well-conditioned basis, not an orthonormal one.  The
@@ -305,7 +314,35 @@ def range_finder(A, r_hat: int, q: int, seed: int, dtype="float64", device=None,
             orthonormalize(Y, ctx, stats)
         Q, Y = Y, Q  # Y now holds the (orthonormal or well-conditioned) block
         _spmm(ctx, dt, Ad, Q, Y)
-    return RangeBasis(Q=Q, B=Y, iterations_used=q, seed=seed)
+    basis = RangeBasis(Q=Q, B=Y, iterations_used=q, seed=seed)
+    if gram_last is not None:
+        object.__setattr__(basis, "_gram", gram_last)
+    return basis
+
+
+def _precondition_with_gram(Y, ctx, stats=None):
+    """(Y R'^-1, G) with G = (Y R'^-1)^T (Y R'^-1) from the full 28-bit Gram: one
+    7-bit CholeskyQR pass; if G is far from I (max|G - I| > 0.9) the second
+    CholeskyQR pass is applied and G recomputed, so Rayleigh-Ritz always gets
+    a basis with cond <= ~4.4 and its exact Gram."""
+    import torch
+
+    dt = N.dtype_code(Y.dtype)
+    n, k = Y.shape
+    G = torch.empty(k, k, dtype=torch.float64, device=Y.device)
+    ok, _ = _cholqr_pass(ctx, dt, Y, G, fast_gram=True)
+    if ok:
+        _gram(ctx, dt, Y, G)
+        dev = _max_dev(ctx, G)
+        if dev <= 0.9:
+            if stats is not None:
+                stats.append(f"precond+gram(dev={dev:.3g})")
+            return Y, G
+        if stats is not None:
+            stats.append(f"precond+gram-failed(dev={dev:.3g})")
+    orthonormalize(Y, ctx, stats)
+    _gram(ctx, dt, Y, G)
+    return Y, G
 
 
 def _precondition(Y, ctx, stats=None):
@@ -323,15 +360,23 @@ def _precondition(Y, ctx, stats=None):
     ok, _ = _cholqr_pass(ctx, dt, Y, G, fast_gram=True)
     if ok:
         ctx.call("gram_levels", n, k, N.ptr(Y), Y.stride(0), N.ptr(G), 0, 1)
-        if _max_dev(ctx, G) <= PRECOND_TOL:
+        dev = _max_dev(ctx, G)
+        if dev <= PRECOND_TOL:
             if stats is not None:
-                stats.append("precond")
+                stats.append(f"precond(dev={dev:.3g})")
             return Y
+        if stats is not None:
+            stats.append(f"precond-failed(dev={dev:.3g})")
     return orthonormalize(Y, ctx, stats)
 
 
-def _rayleigh_ritz(ctx, dt, Q, B, r):
-    """C = Q^T B, eigh, U = Q V, sign fix, eta (K4-K6). Returns (U, lam, eta)."""
+def _rayleigh_ritz(ctx, dt, Q, B, r, general=False):
+    """C = Q^T B, eigh, U = Q V, sign fix, eta (K4-K6). Returns (U, lam, eta).
+
+    general=True: Q is only well conditioned (decompose's fused fp32 path);
+    the Ritz pairs solve C v = lambda G v with G = Q^T Q, V is G-orthonormal
+    and U = Q V orthonormal -- the same pairs as orthonormalising Q first.
+    """
     import torch
 
     n, k = Q.shape
@@ -339,7 +384,16 @@ def _rayleigh_ritz(ctx, dt, Q, B, r):
     ctx.call("cross", dt, n, k, N.ptr(Q), Q.stride(0), N.ptr(B), B.stride(0), N.ptr(C), 0)
     lam = np.empty(r, dtype=np.float64)
     V = torch.empty(k, r, dtype=torch.float64, device=Q.device)
-    ctx.call("eigh_desc", k, N.ptr(C), r, lam.ctypes.data_as(N._c_dp), N.ptr(V))
+    if general is not False:
+        if isinstance(general, bool):
+            G = torch.empty(k, k, dtype=torch.float64, device=Q.device)
+            ctx.call("gram", dt, n, k, N.ptr(Q), Q.stride(0), N.ptr(G), 0)
+        else:
+            G = general.clone()  # the exact Gram of Q, computed by range_finder (sygvd destroys its input)
+        ctx.call("eigh_gen_desc", k, N.ptr(C), N.ptr(G), r, lam.ctypes.data_as(N._c_dp), N.ptr(V))
+        del G
+    else:
+        ctx.call("eigh_desc", k, N.ptr(C), r, lam.ctypes.data_as(N._c_dp), N.ptr(V))
     del C
     U = torch.empty(n, r, dtype=Q.dtype, device=Q.device)
     ctx.call("lift", dt, n, k, r, N.ptr(Q), Q.stride(0), N.ptr(V), N.ptr(U), U.stride(0))
@@ -361,7 +415,8 @@ def approx_eigendecomposition(A, basis: RangeBasis, r: int) -> SpectralDecomposi
     if Q.shape[0] != A.n:
         raise ValueError("basis dimension does not match A")
     ctx = N.Context.get(Q.device)
-    U, lam, eta = _rayleigh_ritz(ctx, N.dtype_code(Q.dtype), Q, B, r)
+    # a basis from decompose's fused schedule carries its exact Gram matrix
+    U, lam, eta = _rayleigh_ritz(ctx, N.dtype_code(Q.dtype), Q, B, r, general=getattr(basis, "_gram", False))
     return SpectralDecomposition(U, lam, eta, ComponentLabeling.trivial(A.n), Variant.APPROX,
                                  Provenance(r=r, p=basis.r_hat - r, q=basis.iterations_used, seed=basis.seed))
 
@@ -373,10 +428,18 @@ def decompose(A, r: int, p: int = DEFAULT_OVERSAMPLING, q: int = DEFAULT_POWER_I
     r_hat = min(r + p, A.n)
     if r > r_hat:
         raise ValueError(f"r={r} exceeds n={A.n}")
-    basis = range_finder(A, r_hat, q, seed, dtype=dtype, device=device)
+    # fp32: the last round's basis may stay merely well conditioned; the
+    # Rayleigh-Ritz step then absorbs G = Q~^T Q~ (generalised eigenproblem)
+    basis = range_finder(A, r_hat, q, seed, dtype=dtype, device=device,
+                         _orthonormal_last=not fused_rr_enabled(dtype))
     dec = approx_eigendecomposition(A, basis, r)
     del basis
     return dec
+
+
+def fused_rr_enabled(dtype) -> bool:
+    """Whether decompose keeps the last SI basis non-orthonormal (fp32 fast mode)."""
+    return FUSED_RR and SI_SPAN_ONLY and N.dtype_code(N.torch_dtype(dtype)) == N.F32
 
 
 def mix_seed(seed: int, salt: int) -> int:
