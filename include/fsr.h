@@ -149,6 +149,12 @@ int fsr_max_offdiag_error(fsr_ctx* ctx, int64_t k, const double* G, double* err_
  * C (k x k fp64) (+)= Q^T B over n_rows rows. */
 int fsr_cross(fsr_ctx* ctx, int dtype, int64_t n_rows, int64_t k, const void* Q, int64_t ldq,
               const void* B, int64_t ldb, double* C, int accumulate);
+/* Rayleigh-Ritz form: C = Q^T B where Q^T B is symmetric up to rounding
+ * (B = A Q, A symmetric).  F32 tensor-core path computes the upper triangle
+ * and mirrors it (half the work; the reference averages C and C^T, the two
+ * differ at rounding level); other dtypes/paths compute the full product. */
+int fsr_cross_sym(fsr_ctx* ctx, int dtype, int64_t n_rows, int64_t k, const void* Q, int64_t ldq,
+                  const void* B, int64_t ldb, double* C, int accumulate);
 /* C <- (C + C^T)/2; eigh; keep the r algebraically largest pairs in
  * argsort(-lambda, stable) order (spectral.py:141-144).  lam_host[r] gets the
  * eigenvalues (host-synchronous), V (k x r, fp64, row-major) the eigenvectors.

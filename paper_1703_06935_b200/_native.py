@@ -53,6 +53,7 @@ _SIGS = {
     "fsr_householder_qr": (_c_int, [_c_p, _c_int, _c_i64, _c_i64, _c_p, _c_i64]),
     "fsr_max_offdiag_error": (_c_int, [_c_p, _c_i64, _c_p, _c_dp]),
     "fsr_cross": (_c_int, [_c_p, _c_int, _c_i64, _c_i64, _c_p, _c_i64, _c_p, _c_i64, _c_p, _c_int]),
+    "fsr_cross_sym": (_c_int, [_c_p, _c_int, _c_i64, _c_i64, _c_p, _c_i64, _c_p, _c_i64, _c_p, _c_int]),
     "fsr_eigh_desc": (_c_int, [_c_p, _c_i64, _c_p, _c_i64, _c_dp, _c_p]),
     "fsr_eigh_gen_desc": (_c_int, [_c_p, _c_i64, _c_p, _c_p, _c_i64, _c_dp, _c_p]),
     "fsr_lift": (_c_int, [_c_p, _c_int, _c_i64, _c_i64, _c_i64, _c_p, _c_i64, _c_p, _c_p, _c_i64]),

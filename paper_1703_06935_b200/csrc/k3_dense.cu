@@ -197,7 +197,7 @@ int dgemm_nt_accum(fsr_ctx* ctx, int64_t k, int64_t rows, const double* A, int64
 
 // C (k x k) (+)= A^T B over n_rows rows (A, B row-major); B may alias A.
 int cross_impl(fsr_ctx* ctx, int dtype, int64_t n_rows, int64_t k, const void* A, int64_t lda, const void* B,
-               int64_t ldb, double* C, int accumulate) {
+               int64_t ldb, double* C, int accumulate, bool sym_hint = false) {
   FSR_REQUIRE(ctx, n_rows >= 0 && k >= 1 && lda >= k && ldb >= k, "gram/cross: bad shape");
   fsr::StageTimer timer(ctx, FSR_STAGE_GRAM);
   if (n_rows == 0) {
@@ -208,7 +208,8 @@ int cross_impl(fsr_ctx* ctx, int dtype, int64_t n_rows, int64_t k, const void* A
     return dgemm_nt_accum(ctx, k, n_rows, (const double*)A, lda, (const double*)B, ldb, C, accumulate ? 1.0 : 0.0);
   const bool same = A == B && lda == ldb;
   if (ctx->dense_path == 0)
-    return fsr::tc_gram(ctx, n_rows, k, (const float*)A, lda, k, (const float*)B, ldb, C, accumulate, 4, same);
+    return fsr::tc_gram(ctx, n_rows, k, (const float*)A, lda, k, (const float*)B, ldb, C, accumulate, 4,
+                        same || sym_hint);
   const int64_t m = chunk_rows(n_rows, k, same ? 1 : 2);
   void* buf = nullptr;
   FSR_TRY(fsr::scratch(ctx, (size_t)m * k * 8 * (same ? 1 : 2), &buf));
@@ -236,6 +237,12 @@ int fsr_gram(fsr_ctx* ctx, int dtype, int64_t n_rows, int64_t k, const void* A, 
 int fsr_cross(fsr_ctx* ctx, int dtype, int64_t n_rows, int64_t k, const void* Q, int64_t ldq, const void* B,
               int64_t ldb, double* C, int accumulate) {
   return cross_impl(ctx, dtype, n_rows, k, Q, ldq, B, ldb, C, accumulate);
+}
+
+int fsr_cross_sym(fsr_ctx* ctx, int dtype, int64_t n_rows, int64_t k, const void* Q, int64_t ldq, const void* B,
+                  int64_t ldb, double* C, int accumulate) {
+  // F32 tensor-core path: upper triangle only, mirrored; other paths: full product
+  return cross_impl(ctx, dtype, n_rows, k, Q, ldq, B, ldb, C, accumulate, dtype == FSR_F32);
 }
 
 int fsr_gram_levels(fsr_ctx* ctx, int64_t n_rows, int64_t k, const float* A, int64_t lda, double* G, int accumulate,

@@ -557,7 +557,9 @@ namespace fsr {
 int tc_gram(fsr_ctx* ctx, int64_t n, int64_t ka, const float* A, int64_t lda, int64_t kb, const float* B,
             int64_t ldb, double* C, int accumulate, int levels, int symmetric) {
   const bool same = (A == B) && lda == ldb && ka == kb;
-  symmetric = symmetric && same;
+  // symmetric: compute the upper triangle only and mirror it (A == B, or a
+  // caller that knows A^T B is symmetric up to rounding, fsr_cross_sym)
+  symmetric = symmetric && ka == kb;
   const int NT = levels == 1 ? Variant<1, 1>::N : Variant<4, 4>::N;
   const int64_t per_row = kSlices * (ka + (same ? 0 : kb));
   int64_t chunk = std::max<int64_t>(128, std::min<int64_t>({n, kMaxK, (int64_t)(kChunkBudget / per_row)}));

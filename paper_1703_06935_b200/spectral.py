@@ -381,7 +381,8 @@ def _rayleigh_ritz(ctx, dt, Q, B, r, general=False):
 
     n, k = Q.shape
     C = torch.empty(k, k, dtype=torch.float64, device=Q.device)
-    ctx.call("cross", dt, n, k, N.ptr(Q), Q.stride(0), N.ptr(B), B.stride(0), N.ptr(C), 0)
+    # C = Q^T A Q is symmetric: the fp32 tensor-core path computes one triangle
+    ctx.call("cross_sym", dt, n, k, N.ptr(Q), Q.stride(0), N.ptr(B), B.stride(0), N.ptr(C), 0)
     lam = np.empty(r, dtype=np.float64)
     V = torch.empty(k, r, dtype=torch.float64, device=Q.device)
     if general is not False:
