@@ -374,7 +374,10 @@ __global__ void __launch_bounds__(256) spmm_l2panel_kernel(int64_t n_rows, const
 // coalesced row-pointer load and 1-4 rows in flight -- faster on uniform
 // rows, but 3-25% slower on the bench's U~, whose row lengths are very
 // skewed: rows of small clusters keep hundreds of entries, rows of large
-// clusters few.  Grid-stride warp-per-row balances that best.)
+// clusters few.  Grid-stride warp-per-row balances that best.  A software-
+// pipelined version -- next row's pointers and first 128 entries in flight
+// while the current row is summed -- measured 10-15% slower on that U~:
+// 0.171/0.217/0.401 vs 0.150/0.189/0.377 ms at 1/2/5%, tools/b1_probe.py.)
 template <typename T>
 __global__ void __launch_bounds__(256) spmv_smem_kernel(int64_t n_rows, const int64_t* __restrict__ indptr,
                                                         const int32_t* __restrict__ indices,
