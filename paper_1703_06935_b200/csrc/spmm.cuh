@@ -164,6 +164,7 @@ __global__ void __launch_bounds__(256) spmm_rowpanel_T_kernel(int64_t n_rows, co
                                                               T* __restrict__ Yt, int64_t ldy) {
   constexpr int PW = 32 * VEC * NV;
   __shared__ T tile[32][PW + 1];
+  __shared__ int next_row;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t row0 = (int64_t)blockIdx.x * 32;
   const int64_t p0 = (int64_t)blockIdx.y * PW;
@@ -171,7 +172,11 @@ __global__ void __launch_bounds__(256) spmm_rowpanel_T_kernel(int64_t n_rows, co
   bool live[NV];
 #pragma unroll
   for (int u = 0; u < NV; ++u) live[u] = c0 + u * 32 * VEC < ncols;
-  for (int rr = warp; rr < 32; rr += 8) {
+  if (threadIdx.x == 0) next_row = 8;
+  __syncthreads();
+  // rows are handed out dynamically: U~'s row lengths are skewed (median 54,
+  // max > 2000 at C3), so a static 4-rows-per-warp split leaves warps idle
+  for (int rr = warp; rr < 32;) {
     const int64_t i = row0 + rr;
     T acc[NV][VEC];
 #pragma unroll
@@ -185,6 +190,9 @@ __global__ void __launch_bounds__(256) spmm_rowpanel_T_kernel(int64_t n_rows, co
     for (int u = 0; u < NV; ++u)
 #pragma unroll
       for (int q = 0; q < VEC; ++q) tile[rr][lane * VEC + u * 32 * VEC + q] = acc[u][q];
+    int nr = 0;
+    if (lane == 0) nr = atomicAdd(&next_row, 1);
+    rr = __shfl_sync(0xffffffffu, nr, 0);
   }
   __syncthreads();
   const int64_t i = row0 + lane;
