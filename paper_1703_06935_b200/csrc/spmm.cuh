@@ -153,20 +153,22 @@ __global__ void __launch_bounds__(256) spmm_rowpanel_kernel(int64_t n_rows, cons
   }
 }
 
-// K9 variant with a transposed output: CTA = 32 consecutive rows x one panel;
-// each warp computes 4 rows, the 32 x PW tile is staged in shared memory
-// (padded) and written as Y^T (ldy = n): 128-byte coalesced column segments.
-template <typename T, int VEC, int NV, int DEPTH = kGatherDepth>
+// K9 variant with a transposed output: CTA = ROWS consecutive rows x one panel;
+// warps take the rows one at a time from a shared counter, the ROWS x PW tile
+// is staged in shared memory (padded) and written as Y^T (ldy = n): 128-byte
+// coalesced column segments.
+template <typename T, int VEC, int NV, int DEPTH = kGatherDepth, int ROWS = 32>
 __global__ void __launch_bounds__(256) spmm_rowpanel_T_kernel(int64_t n_rows, const int64_t* __restrict__ indptr,
                                                               const int32_t* __restrict__ indices,
                                                               const T* __restrict__ vals, int64_t ncols,
                                                               const T* __restrict__ X, int64_t ldx,
                                                               T* __restrict__ Yt, int64_t ldy) {
   constexpr int PW = 32 * VEC * NV;
-  __shared__ T tile[32][PW + 1];
+  extern __shared__ __align__(16) unsigned char dyn_tile[];
+  T(*tile)[PW + 1] = reinterpret_cast<T(*)[PW + 1]>(dyn_tile);  // ROWS x (PW + 1)
   __shared__ int next_row;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t row0 = (int64_t)blockIdx.x * 32;
+  const int64_t row0 = (int64_t)blockIdx.x * ROWS;
   const int64_t p0 = (int64_t)blockIdx.y * PW;
   const int64_t c0 = p0 + (int64_t)lane * VEC;
   bool live[NV];
@@ -176,7 +178,7 @@ __global__ void __launch_bounds__(256) spmm_rowpanel_T_kernel(int64_t n_rows, co
   __syncthreads();
   // rows are handed out dynamically: U~'s row lengths are skewed (median 54,
   // max > 2000 at C3), so a static 4-rows-per-warp split leaves warps idle
-  for (int rr = warp; rr < 32;) {
+  for (int rr = warp; rr < ROWS;) {
     const int64_t i = row0 + rr;
     T acc[NV][VEC];
 #pragma unroll
@@ -195,10 +197,13 @@ __global__ void __launch_bounds__(256) spmm_rowpanel_T_kernel(int64_t n_rows, co
     rr = __shfl_sync(0xffffffffu, nr, 0);
   }
   __syncthreads();
-  const int64_t i = row0 + lane;
   for (int c = warp; c < PW; c += 8) {
     const int64_t col = p0 + c;
-    if (col < ncols && i < n_rows) Yt[col * ldy + i] = tile[lane][c];
+#pragma unroll
+    for (int h = 0; h < ROWS / 32; ++h) {
+      const int64_t i = row0 + h * 32 + lane;
+      if (col < ncols && i < n_rows) Yt[col * ldy + i] = tile[h * 32 + lane][c];
+    }
   }
 }
 
@@ -436,6 +441,23 @@ int launch_spmv_smem(fsr_ctx* ctx, int64_t n_rows, const int64_t* indptr, const 
   return launched(ctx, "spmv_smem_kernel");
 }
 
+template <typename T, int VEC, int NV, int ROWS>
+int launch_rowpanel_T(fsr_ctx* ctx, int64_t n_rows, const int64_t* indptr, const int32_t* indices, const T* vals,
+                      int64_t ncols, const T* X, int64_t ldx, T* Yt, int64_t ldy) {
+  constexpr int PW = 32 * VEC * NV;
+  const size_t smem = (size_t)ROWS * (PW + 1) * sizeof(T);
+  static bool configured = false;
+  if (!configured) {
+    FSR_CUDA(ctx, cudaFuncSetAttribute(spmm_rowpanel_T_kernel<T, VEC, NV, kGatherDepth, ROWS>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    configured = true;
+  }
+  dim3 grid((unsigned)ceil_div(n_rows, ROWS), (unsigned)ceil_div(ncols, PW));
+  spmm_rowpanel_T_kernel<T, VEC, NV, kGatherDepth, ROWS><<<grid, 256, smem, ctx->stream>>>(
+      n_rows, indptr, indices, vals, ncols, X, ldx, Yt, ldy);
+  return FSR_OK;
+}
+
 // Y^T (ncols x n_rows, ld = ldy) = A X for ncols >= 2 (online K9 output layout).
 template <typename T>
 int launch_spmm_T(fsr_ctx* ctx, int64_t n_rows, const int64_t* indptr, const int32_t* indices, const T* vals,
@@ -463,18 +485,13 @@ int launch_spmm_T(fsr_ctx* ctx, int64_t n_rows, const int64_t* indptr, const int
   // registers (2 CTAs/SM) cost 30% on the bench's U~ (skewed row lengths).
   // The kernel streams ~19.6 TB/s of L2->SM gathers.
   if (vec_ok && ncols > 32 * VW) {
-    constexpr int NV = 2, PW = 32 * VW * NV;
-    dim3 grid((unsigned)ceil_div(n_rows, 32), (unsigned)ceil_div(ncols, PW));
-    spmm_rowpanel_T_kernel<T, VW, NV><<<grid, block, 0, ctx->stream>>>(n_rows, indptr, indices, vals, ncols, X, ldx,
-                                                                        Yt, ldy);
+    // 32-row blocks: 64-row blocks (same occupancy) measured 22.4 vs 21.0 ms at C3
+    constexpr int NV = 2;
+    FSR_TRY((launch_rowpanel_T<T, VW, NV, 32>(ctx, n_rows, indptr, indices, vals, ncols, X, ldx, Yt, ldy)));
   } else if (vec_ok) {
-    dim3 grid((unsigned)ceil_div(n_rows, 32), (unsigned)ceil_div(ncols, 32 * VW));
-    spmm_rowpanel_T_kernel<T, VW, 1><<<grid, block, 0, ctx->stream>>>(n_rows, indptr, indices, vals, ncols, X, ldx,
-                                                                       Yt, ldy);
+    FSR_TRY((launch_rowpanel_T<T, VW, 1, 32>(ctx, n_rows, indptr, indices, vals, ncols, X, ldx, Yt, ldy)));
   } else {
-    dim3 grid((unsigned)ceil_div(n_rows, 32), (unsigned)ceil_div(ncols, 32));
-    spmm_rowpanel_T_kernel<T, 1, 1><<<grid, block, 0, ctx->stream>>>(n_rows, indptr, indices, vals, ncols, X, ldx,
-                                                                      Yt, ldy);
+    FSR_TRY((launch_rowpanel_T<T, 1, 1, 32>(ctx, n_rows, indptr, indices, vals, ncols, X, ldx, Yt, ldy)));
   }
   return launched(ctx, "spmm_rowpanel_T_kernel");
 }
