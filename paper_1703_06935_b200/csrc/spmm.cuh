@@ -262,7 +262,12 @@ __global__ void __launch_bounds__(256) spmm_narrow_T_kernel(int64_t n_rows, cons
   const int64_t p0 = (int64_t)blockIdx.y * PW;  // column panel (row-major output mode)
   const int64_t c0 = p0 + (int64_t)sl * VEC;
   const bool live = c0 < ncols;
-  for (int rr = warp; rr < 64; rr += 8) {
+  // rows are handed out dynamically (as in the wide kernel): a warp that
+  // drew short rows takes more of them instead of idling at the barrier
+  __shared__ int next_row;
+  if (threadIdx.x == 0) next_row = 8;
+  __syncthreads();
+  for (int rr = warp; rr < 64;) {
     const int64_t i = row0 + rr;
     T acc[VEC];
 #pragma unroll
@@ -310,6 +315,9 @@ __global__ void __launch_bounds__(256) spmm_narrow_T_kernel(int64_t n_rows, cons
     } else if (grp == 0 && live && i < n_rows) {
       store_vec<T, VEC>(Yt + i * ldy + c0, acc);  // row-major Y, this panel's columns
     }
+    int nr = 0;
+    if (lane == 0) nr = atomicAdd(&next_row, 1);
+    rr = __shfl_sync(0xffffffffu, nr, 0);
   }
   if (!TRANS) return;
   __syncthreads();

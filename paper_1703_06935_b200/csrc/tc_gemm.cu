@@ -46,10 +46,17 @@ namespace {
 using namespace fsr::tc;
 
 constexpr int kThreads = 192;
-constexpr int kBK = 64;            // K bytes (int8 elements) per stage = one 64B swizzle atom
+// K bytes (int8 elements) per stage = one 64B swizzle atom.  Measured
+// alternative (tools/dense_micro.py, C3 shapes): 32-byte stages (SWIZZLE_32B)
+// with twice the stages were 20-30% slower on every dense stage.
+constexpr int kBK = 64;
 constexpr int kSlices = 4;         // slice planes produced
 constexpr int64_t kMaxK = 65536;   // reduction length per launch (int32-exact bound: 131072)
-constexpr int kApplyGroup = 32;    // column tiles per L2-resident group in the apply raster
+// column tiles per L2-resident group in the apply raster.  Measured at C3
+// (k = 5500): 4 .. 43 all within 3% (apply 239-246 ms) although DRAM reads
+// differ ~5x: the int8 MMA stream runs at the board power limit (ncu: Gram
+// 94% tensor-busy at 1.55 GHz, apply 74% at 1.85 GHz), not at a feed limit.
+constexpr int kApplyGroup = 32;
 
 // --------------------------------------------------------------- exponents --
 __device__ __forceinline__ int exp_above(double m) {
@@ -190,14 +197,14 @@ __global__ void slice_rows_kernel(int64_t rows, int64_t cols, const T* __restric
 }
 
 // ------------------------------------------------------------------ kernel --
-template <int N, int STAGES, int LEVELS, int BPL = LEVELS>
+template <int N, int STAGES, int LEVELS, int BPL, int BK>
 struct OzCfg {
-  static constexpr int APLANES = LEVELS;     // level l needs A slices 0..l
-  static constexpr int BPLANES = BPL;        // B slices kept (1: B is a 7-bit matrix)
-  static constexpr int A_PLANE = 128 * kBK;  // 128 rows x 64 K bytes
-  static constexpr int B_PLANE = N * kBK;
+  static constexpr int APLANES = LEVELS;    // level l needs A slices 0..l
+  static constexpr int BPLANES = BPL;       // B slices kept (1: B is a 7-bit matrix)
+  static constexpr int A_PLANE = 128 * BK;  // 128 rows x BK K bytes
+  static constexpr int B_PLANE = N * BK;
   static constexpr int STAGE_BYTES = APLANES * A_PLANE + BPLANES * B_PLANE;
-  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 512;  // alignment slack + barriers
   static constexpr uint32_t TMEM_COLS = LEVELS * N <= 128 ? 128 : (LEVELS * N <= 256 ? 256 : 512);
   static_assert(LEVELS * N <= 512, "accumulators exceed TMEM");
   static_assert(SMEM <= 227 * 1024, "stages exceed shared memory");
@@ -218,14 +225,17 @@ __device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t adesc, uint64_t
       : "memory");
 }
 
-// K-major SWIZZLE_64B matrix descriptor: 8-row x 64-byte atoms (SBO = 512 B).
-__device__ __forceinline__ uint64_t desc_sw64(uint32_t saddr) {
+// K-major swizzled matrix descriptor: 8-row x BK-byte atoms (SBO = 8 * BK),
+// SWIZZLE_64B for BK = 64, SWIZZLE_32B for BK = 32.
+template <int BK>
+__device__ __forceinline__ uint64_t desc_kmajor(uint32_t saddr) {
+  static_assert(BK == 64 || BK == 32, "one swizzle atom of K per stage");
   uint64_t d = 0;
   d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
-  d |= (uint64_t)1 << 16;           // LBO (ignored for swizzled K-major) = 16 B
-  d |= (uint64_t)(512 >> 4) << 32;  // SBO
-  d |= (uint64_t)1 << 46;           // descriptor version (sm_100)
-  d |= (uint64_t)4 << 61;           // SWIZZLE_64B
+  d |= (uint64_t)1 << 16;                // LBO (ignored for swizzled K-major) = 16 B
+  d |= (uint64_t)((8 * BK) >> 4) << 32;  // SBO
+  d |= (uint64_t)1 << 46;                // descriptor version (sm_100)
+  d |= (uint64_t)(BK == 64 ? 4 : 6) << 61;
   return d;
 }
 
@@ -247,13 +257,14 @@ __device__ __forceinline__ void tmem_ld32_i(uint32_t taddr, int (&v)[32]) {
 //   rows = output rows i (ka of them), B rows = output cols j; result written
 //   to the fp64 partial P[split] (ka x kb).
 // MODE 1 (apply): D[r, j] = sum_K A[r, :] B[j, :] over the full K; fp32 out.
-template <int MODE, int N, int STAGES, int LEVELS, int BPL>
+template <int MODE, int N, int STAGES, int LEVELS, int BPL, bool WIDE, int BK>
 __global__ void __launch_bounds__(kThreads, 1)
     oz_gemm_kernel(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUtensorMap mB, int rowsA,
                    int rowsB, int64_t planeA_rows, int64_t planeB_rows, int64_t K, int tiles_n, int64_t k_per_split,
                    const int* __restrict__ eA, const int* __restrict__ eB, int symmetric, double* __restrict__ P,
-                   float* __restrict__ Out, int64_t ldo, int vec_out) {
-  using Cfg = OzCfg<N, STAGES, LEVELS, BPL>;
+                   float* __restrict__ Out, int64_t ldo, int vec_out, int group) {
+  using Cfg = OzCfg<N, STAGES, LEVELS, BPL, BK>;
+  static_assert(!WIDE || (LEVELS == 4 && BPL == 4 && N == 128), "wide MMAs pair 128-column levels");
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint64_t* full = (uint64_t*)(smem + STAGES * Cfg::STAGE_BYTES);
@@ -269,7 +280,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int total = tiles_m * tiles_n;
   const int64_t kb0 = (int64_t)blockIdx.y * k_per_split;
   const int64_t kb1 = min(K, kb0 + k_per_split);
-  const int iters = kb1 > kb0 ? (int)((kb1 - kb0 + kBK - 1) / kBK) : 0;
+  const int iters = kb1 > kb0 ? (int)((kb1 - kb0 + BK - 1) / BK) : 0;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // tile index -> (row tile, column tile); false if the tile is skipped
   auto tile_of = [&](int idx, int& ti, int& tj) -> bool {
@@ -277,11 +288,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       // column tiles in groups of kApplyGroup, all row tiles swept per group:
       // the group's B slices stay L2-resident while A row blocks stream; tj
       // fastest inside a group so an A block is reused by neighbouring tiles
-      const int per_group = tiles_m * kApplyGroup;
+      const int per_group = tiles_m * group;
       const int g = idx / per_group, rr = idx % per_group;
-      const int gw = min(kApplyGroup, tiles_n - g * kApplyGroup);
+      const int gw = min(group, tiles_n - g * group);
       ti = rr / gw;
-      tj = g * kApplyGroup + rr % gw;
+      tj = g * group + rr % gw;
       return true;
     }
     ti = idx / tiles_n;
@@ -320,7 +331,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (lane == 0) {
           uint8_t* st = smem + s * Cfg::STAGE_BYTES;
           mbar_expect_tx(&full[s], Cfg::STAGE_BYTES);
-          const int kk = (int)(kb0 + (int64_t)it * kBK);
+          const int kk = (int)(kb0 + (int64_t)it * BK);
 #pragma unroll
           for (int p = 0; p < Cfg::APLANES; ++p)
             tma_load_2d(st + p * Cfg::A_PLANE, &mA, &full[s], kk, (int)(p * planeA_rows + i0));
@@ -334,6 +345,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp == 1) {
     constexpr uint32_t idesc = idesc_i8(128, N);
+    constexpr uint32_t idesc_w = idesc_i8(128, WIDE ? 2 * N : N);
     int g = 0, tcount = 0;
     for (int idx = blockIdx.x; idx < total; idx += gridDim.x) {
       int ti, tj;
@@ -350,10 +362,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         // live in uniform registers); one elected lane issues the MMAs.  A
         // descriptor's start-address field is addr >> 4, so an offset is a
         // 64-bit add of (offset >> 4) while the field does not overflow.
-        const uint64_t d0 = desc_sw64(smem_u32(smem + s * Cfg::STAGE_BYTES));
+        const uint64_t d0 = desc_kmajor<BK>(smem_u32(smem + s * Cfg::STAGE_BYTES));
         if (lane == 0) {
 #pragma unroll
-          for (int ks = 0; ks < kBK / 32; ++ks) {
+          for (int ks = 0; ks < BK / 32; ++ks) {
             uint64_t a[Cfg::APLANES], b[Cfg::BPLANES];
 #pragma unroll
             for (int p = 0; p < Cfg::APLANES; ++p) a[p] = d0 + (uint64_t)((p * Cfg::A_PLANE + ks * 32) >> 4);
@@ -361,13 +373,27 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int p = 0; p < Cfg::BPLANES; ++p)
               b[p] = d0 + (uint64_t)((Cfg::APLANES * Cfg::A_PLANE + p * Cfg::B_PLANE + ks * 32) >> 4);
             const uint32_t acc = (it == 0 && ks == 0) ? 0u : 1u;
-            // level l accumulates the kept slice pairs (t, l - t); the first
-            // product issued into each accumulator starts it (acc == 0)
+            if (WIDE) {
+              // 4 x 4 planes: B planes u, u+1 are adjacent in shared memory
+              // (one 2N-row operand) and levels l, l+1 are adjacent in TMEM,
+              // so A_t [B_u | B_u+1] is ONE N = 2*128 MMA into levels t+u and
+              // t+u+1: the 10 slice pairs become 4 wide + 2 narrow MMAs, and
+              // the A tile is read from shared memory 6 times instead of 10.
+              mma_i8(tmem + 0 * N, a[0], b[0], idesc_w, acc);  // L0 += A0B0, L1 += A0B1
+              mma_i8(tmem + 2 * N, a[0], b[2], idesc_w, acc);  // L2 += A0B2, L3 += A0B3
+              mma_i8(tmem + 1 * N, a[1], b[0], idesc_w, 1u);   // L1 += A1B0, L2 += A1B1
+              mma_i8(tmem + 3 * N, a[1], b[2], idesc, 1u);     // L3 += A1B2
+              mma_i8(tmem + 2 * N, a[2], b[0], idesc_w, 1u);   // L2 += A2B0, L3 += A2B1
+              mma_i8(tmem + 3 * N, a[3], b[0], idesc, 1u);     // L3 += A3B0
+            } else {
+              // level l accumulates the kept slice pairs (t, l - t); the first
+              // product issued into each accumulator starts it (acc == 0)
 #pragma unroll
-            for (int l = 0; l < LEVELS; ++l) {
-              const int t0 = l - (Cfg::BPLANES - 1) > 0 ? l - (Cfg::BPLANES - 1) : 0;
+              for (int l = 0; l < LEVELS; ++l) {
+                const int t0 = l - (Cfg::BPLANES - 1) > 0 ? l - (Cfg::BPLANES - 1) : 0;
 #pragma unroll
-              for (int t = t0; t <= l; ++t) mma_i8(tmem + l * N, a[t], b[l - t], idesc, t == t0 ? acc : 1u);
+                for (int t = t0; t <= l; ++t) mma_i8(tmem + l * N, a[t], b[l - t], idesc, t == t0 ? acc : 1u);
+              }
             }
           }
           mma_commit(&empty[s]);
@@ -487,17 +513,18 @@ EncodeTiledFn encode_fn() {
   return fn;
 }
 
-// 2-D byte map over rows x cols int8 (row pitch ld bytes), box = 64 bytes x box_rows, 64B swizzle.
+// 2-D byte map over rows x cols int8 (row pitch ld bytes), box = bk bytes x box_rows, bk-byte swizzle.
 int make_map_u8(fsr_ctx* ctx, CUtensorMap* m, const void* base, int64_t rows, int64_t cols, int64_t ld,
-                int box_rows) {
+                int box_rows, int bk) {
   EncodeTiledFn fn = encode_fn();
   if (!fn) return fsr::set_error(ctx, FSR_ECUDA, "cuTensorMapEncodeTiled unavailable");
   cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
   cuuint64_t strides[1] = {(cuuint64_t)ld};
-  cuuint32_t box[2] = {kBK, (cuuint32_t)box_rows};
+  cuuint32_t box[2] = {(cuuint32_t)bk, (cuuint32_t)box_rows};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, (void*)base, dims, strides, box, estr,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, bk == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fsr::set_error(ctx, FSR_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
   return FSR_OK;
@@ -514,18 +541,18 @@ int set_smem(fsr_ctx* ctx, K kernel, int bytes) {
 constexpr size_t kChunkBudget = (size_t)6 << 30;  // bytes of slice staging per row chunk
 
 // tile width / pipeline depth per variant (A slice planes = LEVELS, B planes = BPL)
-template <int LEVELS, int BPL>
+template <int LEVELS, int BPL, int BK>
 struct Variant;
 template <>
-struct Variant<4, 4> {  // 4 x 128 TMEM columns; 3 stages of 4 x (128 + 128) x 64 B
+struct Variant<4, 4, 64> {  // 4 x 128 TMEM columns; 3 stages of 4 x (128 + 128) x 64 B
   static constexpr int N = 128, STAGES = 3;
 };
 template <>
-struct Variant<4, 1> {  // 4 x 128 TMEM columns; 5 stages of (4 x 128 + 128) x 64 B
+struct Variant<4, 1, 64> {  // 4 x 128 TMEM columns; 5 stages of (4 x 128 + 128) x 64 B
   static constexpr int N = 128, STAGES = 5;
 };
 template <>
-struct Variant<1, 1> {  // 160 TMEM columns; 8 stages of (128 + 160) x 64 B
+struct Variant<1, 1, 64> {  // 160 TMEM columns; 8 stages of (128 + 160) x 64 B
   static constexpr int N = 160, STAGES = 8;
 };
 
@@ -533,18 +560,20 @@ template <int MODE, int LEVELS, int BPL = LEVELS>
 int launch_oz(fsr_ctx* ctx, dim3 grid, const CUtensorMap& mA, const CUtensorMap& mB, int rowsA, int rowsB,
               int64_t pA, int64_t pB, int64_t K, int tiles_n, int64_t kps, const int* eA, const int* eB, int sym,
               double* P, float* Out, int64_t ldo) {
-  constexpr int N = Variant<LEVELS, BPL>::N, STAGES = Variant<LEVELS, BPL>::STAGES;
-  using Cfg = OzCfg<N, STAGES, LEVELS, BPL>;
+  constexpr int BK = kBK;
+  constexpr int N = Variant<LEVELS, BPL, BK>::N, STAGES = Variant<LEVELS, BPL, BK>::STAGES;
+  constexpr bool kWide = LEVELS == 4 && BPL == 4;
+  using Cfg = OzCfg<N, STAGES, LEVELS, BPL, BK>;
   static bool attr = false;
   if (!attr) {
-    FSR_TRY(set_smem(ctx, oz_gemm_kernel<MODE, N, STAGES, LEVELS, BPL>, Cfg::SMEM));
+    FSR_TRY(set_smem(ctx, oz_gemm_kernel<MODE, N, STAGES, LEVELS, BPL, kWide, BK>, Cfg::SMEM));
     attr = true;
   }
   // 16-byte epilogue stores need 16-byte aligned rows
   const int vec_out = MODE == 0 ? (rowsB % 2 == 0 && ((uintptr_t)P & 15) == 0)
                                 : (ldo % 4 == 0 && ((uintptr_t)Out & 15) == 0);
-  oz_gemm_kernel<MODE, N, STAGES, LEVELS, BPL><<<grid, kThreads, Cfg::SMEM, ctx->stream>>>(
-      mA, mB, rowsA, rowsB, pA, pB, K, tiles_n, kps, eA, eB, sym, P, Out, ldo, vec_out);
+  oz_gemm_kernel<MODE, N, STAGES, LEVELS, BPL, kWide, BK><<<grid, kThreads, Cfg::SMEM, ctx->stream>>>(
+      mA, mB, rowsA, rowsB, pA, pB, K, tiles_n, kps, eA, eB, sym, P, Out, ldo, vec_out, kApplyGroup);
   return fsr::launched(ctx, MODE == 0 ? "oz_gram_kernel" : "oz_apply_kernel");
 }
 
@@ -560,7 +589,7 @@ int tc_gram(fsr_ctx* ctx, int64_t n, int64_t ka, const float* A, int64_t lda, in
   // symmetric: compute the upper triangle only and mirror it (A == B, or a
   // caller that knows A^T B is symmetric up to rounding, fsr_cross_sym)
   symmetric = symmetric && ka == kb;
-  const int NT = levels == 1 ? Variant<1, 1>::N : Variant<4, 4>::N;
+  const int NT = levels == 1 ? Variant<1, 1, 64>::N : Variant<4, 4, 64>::N;
   const int64_t per_row = kSlices * (ka + (same ? 0 : kb));
   int64_t chunk = std::max<int64_t>(128, std::min<int64_t>({n, kMaxK, (int64_t)(kChunkBudget / per_row)}));
   chunk = pad_to(chunk, 128);
@@ -602,8 +631,8 @@ int tc_gram(fsr_ctx* ctx, int64_t n, int64_t ka, const float* A, int64_t lda, in
       FSR_TRY(launched(ctx, "slice_T_packed_kernel"));
     }
     CUtensorMap mA, mB;
-    FSR_TRY(make_map_u8(ctx, &mA, sA, kSlices * ka, ldT, ldT, 128));
-    FSR_TRY(make_map_u8(ctx, &mB, sB, kSlices * kb, ldT, ldT, NT));
+    FSR_TRY(make_map_u8(ctx, &mA, sA, kSlices * ka, ldT, ldT, 128, kBK));
+    FSR_TRY(make_map_u8(ctx, &mB, sB, kSlices * kb, ldT, ldT, NT, kBK));
     const int64_t kps = pad_to(ceil_div(ldT, splits), kBK);
     dim3 grid((unsigned)(tiles_m * tiles_n), (unsigned)ceil_div(ldT, kps));
     if (levels == 1)
@@ -629,8 +658,8 @@ int tc_gram(fsr_ctx* ctx, int64_t n, int64_t ka, const float* A, int64_t lda, in
 int tc_apply(fsr_ctx* ctx, int64_t n, int64_t K, const float* A, int64_t lda, int64_t N2, const double* M,
              int64_t ldm, int m_col_major, float* Out, int64_t ldo, int m_slices) {
   if (K > kMaxK) return set_error(ctx, FSR_EINVAL, "tc_apply: K=%lld exceeds the int32-exact bound", (long long)K);
-  constexpr int NT = Variant<4, 4>::N;
-  static_assert(Variant<4, 1>::N == NT, "apply variants share the output tile width");
+  constexpr int NT = Variant<4, 4, 64>::N;
+  static_assert(Variant<4, 1, 64>::N == NT, "apply variants share the output tile width");
   const int64_t pk = pad_to(K, 128);
   const size_t m_bytes = (size_t)kSlices * N2 * pk;
   const int64_t per_row = kSlices * pk;
@@ -650,7 +679,7 @@ int tc_apply(fsr_ctx* ctx, int64_t n, int64_t K, const float* A, int64_t lda, in
   slice_rows_kernel<double><<<grid_for(N2 * pk, 256, ctx, 16), 256, 0, ctx->stream>>>(N2, K, M, ldm, tr, eM, sM, pk);
   FSR_TRY(launched(ctx, "slice_rows_kernel"));
   CUtensorMap mB;
-  FSR_TRY(make_map_u8(ctx, &mB, sM, kSlices * N2, pk, pk, NT));
+  FSR_TRY(make_map_u8(ctx, &mB, sM, kSlices * N2, pk, pk, NT, kBK));
   const int tiles_n = (int)ceil_div(N2, NT);
   for (int64_t s0 = 0; s0 < n; s0 += chunk) {
     const int64_t rows = std::min(chunk, n - s0);
@@ -658,7 +687,7 @@ int tc_apply(fsr_ctx* ctx, int64_t n, int64_t K, const float* A, int64_t lda, in
                                                                                        eR, sR, pk);
     FSR_TRY(launched(ctx, "slice_rows_fused_kernel"));
     CUtensorMap mA;
-    FSR_TRY(make_map_u8(ctx, &mA, sR, kSlices * rows, pk, pk, 128));
+    FSR_TRY(make_map_u8(ctx, &mA, sR, kSlices * rows, pk, pk, 128, kBK));
     // persistent: one CTA per SM walks the tiles (see oz_gemm_kernel)
     dim3 grid((unsigned)std::min<int64_t>(ceil_div(rows, 128) * tiles_n, ctx->num_sms), 1);
     if (m_slices == 1)
