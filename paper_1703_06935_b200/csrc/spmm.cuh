@@ -398,7 +398,12 @@ __global__ void __launch_bounds__(256) spmm_l2panel_kernel(int64_t n_rows, const
 // clusters few.  Grid-stride warp-per-row balances that best.  A software-
 // pipelined version -- next row's pointers and first 128 entries in flight
 // while the current row is summed -- measured 10-15% slower on that U~:
-// 0.171/0.217/0.401 vs 0.150/0.189/0.377 ms at 1/2/5%, tools/b1_probe.py.)
+// 0.171/0.217/0.401 vs 0.150/0.189/0.377 ms at 1/2/5%, tools/b1_probe.py.
+// A merge-style streaming SpMV -- warp per 32-row group streaming the group's
+// entries in 256-entry windows of 16-byte loads, per-row sums by a thread-
+// local pass plus a segmented warp scan, next window prefetched -- measured
+// 0.142/0.225/0.479 ms: the per-entry row-boundary bookkeeping makes it
+// issue-bound before it is HBM-bound.)
 template <typename T>
 __global__ void __launch_bounds__(256) spmv_smem_kernel(int64_t n_rows, const int64_t* __restrict__ indptr,
                                                         const int32_t* __restrict__ indices,

@@ -300,3 +300,41 @@ def test_topk_matches_rank(dtype):
     N.Context.get().call("topk_rows", N.dtype_code(dt), b, n, N.ptr(Xd), n, K, N.ptr(idx), N.ptr(val))
     for j in range(b):
         np.testing.assert_array_equal(idx[j].cpu().numpy(), O.rank(Xr[j])[:K])
+
+
+# ------------------------------------------------------- K9 at b = 1 -------
+def _skewed_sparse_dec(n, r, seed):
+    """Sparse U with skewed rows for the b = 1 SpMV (K9): empty rows, runs of
+    empty rows, rows of 1 .. r entries around the 32/128-entry load widths."""
+    from types import SimpleNamespace
+
+    rng = np.random.default_rng(seed)
+    lens = rng.choice([0, 1, 3, 31, 32, 33, 54, 255, 256, 257, 600], size=n,
+                      p=[.15, .1, .1, .05, .05, .05, .3, .05, .05, .05, .05])
+    lens[64:160] = 0                       # three empty groups
+    lens[5] = r                            # a full row
+    lens = np.minimum(lens, r)
+    indptr = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    cols = np.concatenate([np.sort(rng.choice(r, size=k, replace=False)) for k in lens]).astype(np.int32)
+    vals = rng.standard_normal(indptr[-1])
+    U = sp.csr_matrix((vals, cols, indptr), shape=(n, r))
+    eta = np.sqrt(np.asarray(U.multiply(U).sum(axis=1)).ravel())
+    lam = np.sort(rng.uniform(-0.5, 1.0, r))[::-1].copy()
+    return SimpleNamespace(U=U, eigenvalues=lam, eta=eta, variant="sparse", provenance=None, components=None)
+
+
+@pytest.mark.parametrize("dtype,tol", [("float64", 1e-12), ("float32", 1e-5)])
+def test_filter_b1_spmv_skewed_rows(dtype, tol):
+    n, r = 3001, 700
+    host = _skewed_sparse_dec(n, r, 11)
+    dec = spectral.SpectralDecomposition.from_host(host, dtype=dtype)
+    h = ranking.h_alpha(0.9)
+    w = O.transfer_values(O.h_alpha(0.9), host.eigenvalues)
+    for yi in ([5], [0, 7, 100, 2999], [64, 65]):
+        y = ranking.ObservationVector(n, np.array(yi), np.linspace(1.0, 0.5, len(yi)), cap=len(yi))
+        x = ranking.filter_batch(dec, h, [y])[0]
+        ref = O.filter_scores(host.U, host.eigenvalues, host.eta, w, y.indices, y.values)
+        err = np.linalg.norm(x - ref) / max(np.linalg.norm(ref), 1e-300)
+        assert err <= tol, (yi, err)
+        rows = np.flatnonzero(np.diff(host.U.indptr) == 0)
+        np.testing.assert_array_equal(x[rows[~np.isin(rows, yi)]], 0.0)
