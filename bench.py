@@ -58,6 +58,7 @@ def parse_args():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--skip-e2e", action="store_true")
     ap.add_argument("--no-sweep", action="store_true", help="skip the C5 online sweep")
+    ap.add_argument("--no-parity", action="store_true", help="skip the full-size parity checks")
     ap.add_argument("--cpu-procs", type=int, default=64, help="processes for the CPU oracle arms (capped at nproc)")
     return ap.parse_args()
 
@@ -296,6 +297,75 @@ def sharded_offline(S, r, r_hat, q, tau, dt, device, ev):
     return spectral.SpectralDecomposition(full, lam, eta, ComponentLabeling.trivial(shard.n),
                                           spectral.Variant.SPARSE, spectral.Provenance(r=r, p=r_hat - r, q=q,
                                                                                        tau=tau, seed=0))
+
+
+def offline_properties(S, dec, sdec, tau, device, ctx, m=64):
+    """Size-independent checks of the full-size decomposition (untimed, N=1):
+    Ritz identity lambda_i = u_i^T W u_i and u_i^T u_j = delta_ij on m sampled
+    columns, and the sparsify contract (U~ keeps exactly tau entries, all
+    at least as large in |u| as every dropped one)."""
+    import torch
+
+    from paper_1703_06935_b200 import _native as N
+    from paper_1703_06935_b200 import spectral
+
+    U = dec.U_device
+    n, r = U.shape
+    cols = torch.as_tensor(np.unique(np.linspace(0, r - 1, m).round().astype(np.int64)), device=device)
+    Us = U.index_select(1, cols).contiguous()
+    Bs = torch.empty_like(Us)
+    Ad = S.device(Us.dtype, device)
+    spectral._spmm(ctx, N.dtype_code(Us.dtype), Ad, Us, Bs)
+    U64, B64 = Us.double(), Bs.double()
+    rho = (U64 * B64).sum(0).cpu().numpy()
+    lam = dec.eigenvalues[cols.cpu().numpy()]
+    G = (U64.T @ U64).cpu().numpy()
+    res = torch.linalg.vector_norm(B64 - U64 * torch.as_tensor(lam, device=device), dim=0).cpu().numpy()
+    del Us, Bs, U64, B64
+    kept = sdec.U_device.values.abs()
+    t = float(kept.min())
+    gt = ge = 0
+    for i0 in range(0, n, 65536):
+        blk = U[i0:i0 + 65536].abs()
+        gt += int((blk > t).sum())
+        ge += int((blk >= t).sum())
+    scale = float(np.max(np.abs(dec.eigenvalues)))
+    return {"sample_columns": int(cols.numel()),
+            "ritz_identity_max_rel": float(np.max(np.abs(rho - lam)) / scale), "ritz_tol": 1e-5,
+            "orthonormality_max_abs": float(np.max(np.abs(G - np.eye(G.shape[0])))),
+            "residual_norm_top1": float(res[0]), "residual_norm_median": float(np.median(res)),
+            "sparsify_kept": int(sdec.U_device.nnz), "tau": int(tau),
+            "sparsify_count_above_min_kept": gt, "sparsify_count_at_least_min_kept": ge,
+            "sparsify_support_is_top_tau": bool(gt <= tau <= ge) and int(sdec.U_device.nnz) == int(tau)}
+
+
+def online_parity(sdec, Uh, eta, queries, alpha, K, device, nq=8):
+    """GPU scores / top-K vs the oracle port (scipy CSR f64) on the same
+    GPU-produced U~ for nq full-size queries (north_star: x <= 1e-4 rel-L2,
+    top-100 overlap >= 99%)."""
+    from oracle import fsr_oracle as O
+    from paper_1703_06935_b200 import ranking
+
+    nq = min(nq, queries.b)
+    e = int(queries.y_ptr[nq])
+    qb = ranking.QueryBatch(queries.size, queries.y_ptr[:nq + 1], queries.y_idx[:e], queries.y_val[:e])
+    h = ranking.h_alpha(alpha)
+    dq = ranking.DeviceQueries(qb, sdec.dtype, device)
+    res = ranking.filter_device(sdec, h, dq, topk=K, want_x=True)
+    X = res.X.double().cpu().numpy()
+    top = res.top_idx.cpu().numpy()
+    w = O.transfer_values(O.h_alpha(alpha), sdec.eigenvalues)
+    errs, overlaps, same = [], [], 0
+    for j in range(nq):
+        idx = qb.y_idx[qb.y_ptr[j]:qb.y_ptr[j + 1]]
+        val = qb.y_val[qb.y_ptr[j]:qb.y_ptr[j + 1]]
+        x = O.filter_scores(Uh, sdec.eigenvalues, eta, w, idx, val)
+        errs.append(float(np.linalg.norm(X[j] - x) / np.linalg.norm(x)))
+        ref_top = O.rank(x)[:K]
+        overlaps.append(len(np.intersect1d(ref_top, top[j])) / K)
+        same += int(np.array_equal(ref_top, top[j]))
+    return {"queries": nq, "x_rel_l2_max": max(errs), "x_tol": 1e-4, "topk_overlap_min": min(overlaps),
+            "topk_identical_order": same, "oracle": "oracle/fsr_oracle.py filter_scores + rank (scipy CSR f64)"}
 
 
 def online_sweep(dec, sdec_default, density_default, cfg, n, r, queries, device, ctx, es, steps=3, warmup=2):
@@ -610,6 +680,11 @@ def run_fsr(args, cfg, n, rank, world, local_rank):
         del fgs
     clk = clocks.stop()
 
+    # ---------------- full-size parity (untimed, N=1) -------------------------
+    parity = None
+    if world == 1 and not args.no_parity:
+        parity = {"offline": offline_properties(S, dec, sdec, tau, device, ctx) if not args.no_sweep else None}
+
     # ---------------- C5 online sweep (BASELINE config 5) ----------------------
     sweep = None
     if world == 1 and not args.no_sweep:
@@ -628,6 +703,8 @@ def run_fsr(args, cfg, n, rank, world, local_rank):
               for j in range(min(all_queries.b, 8 * procs))]
         done, secs, procs = parallel_oracle_qps(Uh, sdec.eigenvalues, eta, ys, cfg.alpha, args.cpu_seconds, K,
                                                 procs)
+        if parity is not None:
+            parity["online"] = online_parity(sdec, Uh, eta, all_queries, cfg.alpha, K, device)
         cpu = {"value": done / secs, "unit": "queries/s", "cores": procs, "kind": "port",
                "sample": f"{done} queries of this workload on the GPU-produced U~ (scipy CSR f64), oracle filter + "
                          f"rank, {procs} forked processes, {secs:.1f} s wall"}
@@ -669,6 +746,7 @@ def run_fsr(args, cfg, n, rank, world, local_rank):
         "cpu_baseline": cpu,
         "clocks": clk,
         "c5_sweep": sweep,
+        "parity": parity,
     }
     print(json.dumps(line), flush=True)
 
