@@ -413,8 +413,10 @@ def online_sweep(dec, sdec_default, density_default, cfg, n, r, queries, device,
                     ms += e0.elapsed_time(e1)
                 k9_ms, k9_cnt = ctx.stage_time("filter_spmm")
                 kept = sd.U_device.nnz
-                k9_bytes = kept * (es + 4) + (n + 1) * 8 + es * r * b + es * n * b
-                row = {"density": d, "b": b, "h": name, "queries_per_s": b * nsteps / (ms / 1e3),
+                pr = ranking.topk_pruned(n, b, 100, sd.dtype)
+                k9_bytes = kept * (es + 4) + (n + 1) * 8 + (2 if pr else es) * r * b + es * n * b
+                row = {"density": d, "b": b, "h": name, "k9_path": "pruned" if pr else "exact",
+                       "queries_per_s": b * nsteps / (ms / 1e3),
                        "ms_per_batch": ms / nsteps, "k9_ms": k9_ms / max(k9_cnt, 1),
                        "k9_algorithmic_gbs": k9_bytes / (k9_ms / max(k9_cnt, 1) * 1e-3) / 1e9,
                        "k9_fp32_tflops": 2.0 * kept * b / (k9_ms / max(k9_cnt, 1) * 1e-3) / 1e12}
@@ -627,19 +629,37 @@ def run_fsr(args, cfg, n, rank, world, local_rank):
     dev_ms_max = max_over_ranks(dev_ms, world)
     value = world * b * args.steps / (dev_ms_max / 1e3)
 
-    # roofline of the dominant kernel: K9 (sparse U~ x Zs)
+    # roofline of the dominant kernel: K9 (sparse U~ x Zs; the pruned path's
+    # K9h gathers Zs in fp16, 2 bytes per column)
+    pruned = ranking.topk_pruned(n, b, K, sdec.dtype)
+    zb_es = 2 if pruned else es
     k9_ms, k9_cnt = on_stages["filter_spmm"]
     k9_ms_launch = k9_ms / max(k9_cnt, 1)
     kept = sdec.U_device.nnz
-    k9_bytes = kept * (es + 4) + (n + 1) * 8 + es * r * b + es * n * b
+    k9_bytes = kept * (es + 4) + (n + 1) * 8 + zb_es * r * b + es * n * b
     k9_gbs = k9_bytes / (k9_ms_launch * 1e-3) / 1e9
     k9_share = k9_ms / max(sum(v[0] for v in on_stages.values()), 1e-9)
     # binding limbs: every nonzero of U~ gathers one b-wide row of Zs (L2-resident)
-    k9_gather = kept * b * es
+    k9_gather = kept * b * zb_es
+    # pruned path: same top-k as the unpruned fp32 path, bit for bit (untimed check)
+    prune_check = None
+    if pruned:
+        same, fallback = True, 0
+        for dq in dqs:
+            ranking.filter_device(sdec, h, dq, topk=K, want_x=False, out=res, workspace=ws)
+            torch.cuda.synchronize()
+            fallback += ranking.pruned_fallback_count(ws, n, r, b)
+            pi, pv = res.top_idx.clone(), res.top_val.clone()
+            ctx.set_topk_prune(False)
+            ranking.filter_device(sdec, h, dq, topk=K, want_x=False, out=res, workspace=ws)
+            torch.cuda.synchronize()
+            ctx.set_topk_prune(True)
+            same &= bool(torch.equal(pi, res.top_idx) and torch.equal(pv.view(torch.int32), res.top_val.view(torch.int32)))
+        prune_check = {"batches": len(dqs), "topk_identical_to_unpruned_fp32": same, "fallback_queries": fallback}
     k9_gather_gbs = k9_gather / (k9_ms_launch * 1e-3) / 1e9
     l2 = load_profile("l2_bw.json") or {}
     l2_peak = l2.get("gather_1KB_rows_19MB_GBs")
-    ncu9 = load_profile("k9_ncu_full.json") or {}
+    ncu9 = load_profile("k9h_ncu_full.json" if pruned else "k9_ncu_full.json") or {}
     k9_traffic = ncu9.get("dram_bytes_per_launch") if (cfg.name == "C3" and b == 1024 and es == 4
                                                          and args.density is None) else None
 
@@ -724,10 +744,17 @@ def run_fsr(args, cfg, n, rank, world, local_rank):
                    "global_batch": b * world, "parallelism": (f"offline row-sharded x{world} (NCCL all-gather + ordered fp64 sums), online replicas (batch split)" if world > 1 else "single GPU"),
                    "l2": "256 MB buffer written, then a 256 MB buffer read, between timed steps (L2 flush "
                          "with write-back outside the timed region); U~ itself > L2"},
-        "roofline": {"kernel": "K9 filter SpMM (spmm_rowpanel_T_kernel on U~ x Zs)", "bound": "hbm",
+        "online_path": ("certified pruned top-k: K9h gathers Zs rounded to fp16 (per-query power-of-two scale), "
+                        "a rigorous per-row bound selects the rows that can reach the top-k, those are re-scored "
+                        "exactly in fp32 in the unpruned kernel's order (csrc/prune.cuh)" if pruned else
+                        "unpruned fp32 K9 + exact top-k"),
+        "prune_check": prune_check,
+        "roofline": {"kernel": ("K9h filter SpMM (spmm_T_half_kernel on U~ x fp16 Zs)" if pruned else
+                                "K9 filter SpMM (spmm_rowpanel_T_kernel on U~ x Zs)"), "bound": "hbm",
                      "achieved": k9_gbs, "peak": peak_gbs, "unit": "GB/s", "frac": k9_gbs / peak_gbs,
                      "peak_kind": peak_kind, "traffic": k9_traffic,
-                     "traffic_source": ("profiles/%s/k9_ncu_full.json" % PROFILE_ROUND) if k9_traffic else None,
+                     "traffic_source": ("profiles/%s/%s" % (PROFILE_ROUND, "k9h_ncu_full.json" if pruned else
+                                                            "k9_ncu_full.json")) if k9_traffic else None,
                      "algorithmic_bytes_per_launch": k9_bytes,
                      "ms_per_launch": k9_ms_launch, "share_of_step": k9_share,
                      "binding_limbs": {

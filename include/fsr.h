@@ -78,8 +78,12 @@ int fsr_ctx_enable_timing(fsr_ctx* ctx, int on);
  * lift on the tcgen05 int8 Ozaki kernels), 1 = cuBLAS/cuSOLVER (fp64-upcast
  * Gram, TRSM, SGEMM) -- kept for A/B checks.  FSR_OPT_SPMM_PANEL_BYTES: K2
  * schedule -- 0 = wide row panels, 32/64/128 = L2-resident column panels of
- * that many bytes per dense row (results identical; speed only). */
-enum fsr_option { FSR_OPT_DENSE_PATH = 0, FSR_OPT_SPMM_PANEL_BYTES = 1 };
+ * that many bytes per dense row (results identical; speed only).
+ * FSR_OPT_TOPK_PRUNE: 1 (default) = fsr_filter_batch with top-k only (X ==
+ * NULL), float32, sparse U, b >= 256 gathers Zs in fp16 and re-scores the
+ * rows that can reach the top k exactly in fp32 (certified bound; the same
+ * top-k indices and values as 0 = the unpruned fp32 path). */
+enum fsr_option { FSR_OPT_DENSE_PATH = 0, FSR_OPT_SPMM_PANEL_BYTES = 1, FSR_OPT_TOPK_PRUNE = 2 };
 int fsr_ctx_set_option(fsr_ctx* ctx, int option, int64_t value);
 int fsr_stage_time(fsr_ctx* ctx, int stage, double* ms, uint64_t* count);
 int fsr_stage_reset(fsr_ctx* ctx);
@@ -207,7 +211,8 @@ int fsr_threshold_compact(fsr_ctx* ctx, int dtype, int64_t n_rows, int64_t r, co
  *   z_j = U[supp y_j]^T y_j            (K8, ranking.py:219-226)
  *   x_j = U (w .* z_j)                 (K9, ranking.py:246)
  *   x_j[i] = y_ij where eta_i == 0     (copy_uncovered, ranking.py:248-254)
- * U is CSR (u_indptr/u_indices/u_values, n x r) when u_sparse, else dense
+ * U is CSR (u_indptr/u_indices/u_values, n x r; canonical: distinct sorted
+ * column indices per row, as scipy/sparsify produce) when u_sparse, else dense
  * u_dense (n x r, ld ldu).  w: r weights h(lambda) (dtype).  eta: n fp64 (may
  * be NULL when copy_uncovered == 0).
  * Outputs: X (b x n, row j = x_j) when X != NULL; and/or the top `topk`

@@ -215,6 +215,11 @@ class Context:
         """K2 schedule: 0 = wide row panels, 32/64/128 = L2-resident column panels."""
         self.check(self.lib.fsr_ctx_set_option(self.handle, 1, int(panel_bytes)))
 
+    def set_topk_prune(self, on: bool):
+        """Top-k-only fp32 batches: certified fp16-pruned K9 + exact re-score (True, default)
+        or the unpruned fp32 K9 (False).  Both return the same top-k."""
+        self.check(self.lib.fsr_ctx_set_option(self.handle, 2, int(bool(on))))
+
     def enable_timing(self, on: bool = True):
         self.check(self.lib.fsr_ctx_enable_timing(self.handle, int(on)))
         self._timing = bool(on)

@@ -91,6 +91,10 @@ int fsr_ctx_set_option(fsr_ctx* ctx, int option, int64_t value) {
         return fsr::set_error(ctx, FSR_EINVAL, "spmm panel must be 0, 32, 64 or 128 bytes");
       ctx->spmm_panel_bytes = (int)value;
       return FSR_OK;
+    case FSR_OPT_TOPK_PRUNE:
+      if (value < 0 || value > 1) return fsr::set_error(ctx, FSR_EINVAL, "topk prune must be 0 or 1");
+      ctx->topk_prune = (int)value;
+      return FSR_OK;
     default:
       return fsr::set_error(ctx, FSR_EINVAL, "unknown option %d", option);
   }

@@ -17,6 +17,10 @@
 // multi-pass fallback when the candidate set overflows shared memory.
 #include <cub/cub.cuh>
 
+#include <algorithm>
+#include <cstdlib>
+
+#include "prune.cuh"
 #include "spmm.cuh"
 #include "topk.cuh"
 
@@ -171,11 +175,104 @@ int launch_project(fsr_ctx* ctx, int64_t r, int64_t b, int u_sparse, const int64
 
 inline size_t align256(size_t x) { return (x + 255) / 256 * 256; }
 
+template <int NV, int DEPTH, int ROWS, int MINB>
+int launch_k9h(fsr_ctx* ctx, int64_t n, const int64_t* u_indptr, const int32_t* u_indices, const float* u_values,
+               int64_t b, const __half* Zh, const float2* qp, float* Xt, float* cb) {
+  namespace P = fsr::prune;
+  const size_t smem = (size_t)ROWS * (256 * NV + 1) * 4;
+  static bool configured = false;
+  if (!configured) {
+    FSR_CUDA(ctx, cudaFuncSetAttribute(P::spmm_T_half_kernel<NV, DEPTH, ROWS, MINB>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    configured = true;
+  }
+  dim3 grid((unsigned)fsr::ceil_div(n, ROWS), (unsigned)fsr::ceil_div(b, 256 * NV));
+  P::spmm_T_half_kernel<NV, DEPTH, ROWS, MINB><<<grid, 256, smem, ctx->stream>>>(n, u_indptr, u_indices, u_values, b,
+                                                                                Zh, b, qp, Xt, n, cb);
+  return fsr::launched(ctx, "spmm_T_half_kernel");
+}
+
+// Top-k-only fp32 batch through the certified pruned path (prune.cuh).
+int filter_pruned(fsr_ctx* ctx, int64_t n, int64_t r, const int64_t* u_indptr, const int32_t* u_indices,
+                  const float* u_values, const float* w, const double* eta, int64_t b, const int64_t* y_ptr,
+                  const int64_t* y_idx, const float* y_val, int copy_uncovered, void* workspace, int64_t topk,
+                  int64_t* top_idx, float* top_val) {
+  namespace P = fsr::prune;
+  char* ws = (char*)workspace;
+  float* Zt = (float*)ws;
+  ws += align256((size_t)b * r * 4);
+  float* Zs = (float*)ws;
+  ws += align256((size_t)r * b * 4);
+  float* Xt = (float*)ws;  // x~ (b x n), then exact rows of flagged queries
+  ws += align256((size_t)n * b * 4);
+  __half* Zh = (__half*)ws;
+  ws += align256((size_t)r * b * 2);
+  float2* qp = (float2*)ws;
+  ws += align256((size_t)b * 8);
+  float* cb = (float*)ws;
+  ws += align256((size_t)n * 4);
+  int* nflag = (int*)ws;
+  int* flags = nflag + 1;
+  ws += align256((size_t)(b + 1) * 4);
+  int32_t* cand = (int32_t*)ws;
+  ws += align256((size_t)b * P::kCap * 4);
+  int32_t* ccount = (int32_t*)ws;
+  FSR_TRY(launch_project<float>(ctx, r, b, 1, u_indptr, u_indices, u_values, nullptr, 0, w, y_ptr, y_idx, y_val, Zt,
+                                Zs));
+  {
+    fsr::StageTimer timer(ctx, FSR_STAGE_PROJECT);
+    P::zs_half_kernel<<<(unsigned)fsr::ceil_div(b, 32), dim3(32, 8), 0, ctx->stream>>>(r, b, Zs, Zh, qp, nflag);
+    FSR_TRY(fsr::launched(ctx, "zs_half_kernel"));
+  }
+  {
+    fsr::StageTimer timer(ctx, FSR_STAGE_FILTER_SPMM);
+    FSR_TRY((launch_k9h<1, 4, 32, 4>(ctx, n, u_indptr, u_indices, u_values, b, Zh, qp, Xt, cb)));
+  }
+  if (copy_uncovered && eta) {
+    fsr::StageTimer timer(ctx, FSR_STAGE_COPY_UNCOVERED);
+    copy_uncovered_kernel<float><<<(unsigned)b, 128, 0, ctx->stream>>>(n, y_ptr, y_idx, y_val, eta, Xt, n);
+    FSR_TRY(fsr::launched(ctx, "copy_uncovered_kernel"));
+  }
+  {
+    fsr::StageTimer timer(ctx, FSR_STAGE_TOPK);
+    const size_t fsmem = (size_t)fsr::topk::kCap * 16;
+    static int per_sm = 0;
+    if (!per_sm) {
+      FSR_CUDA(ctx, cudaFuncSetAttribute(P::fallback_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)fsmem));
+      FSR_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, P::prune_collect_kernel, P::kThreads, 0));
+      per_sm = std::max(per_sm, 1);
+    }
+    const int copy = copy_uncovered && eta;
+    const int64_t grid = std::min<int64_t>(b, (int64_t)ctx->num_sms * per_sm);
+    P::prune_collect_kernel<<<(unsigned)grid, P::kThreads, 0, ctx->stream>>>(n, b, Xt, n, cb, qp, topk, cand, ccount,
+                                                                            nflag, flags);
+    FSR_TRY(fsr::launched(ctx, "prune_collect_kernel"));
+    P::prune_finish_kernel<<<(unsigned)b, P::kThreads, 0, ctx->stream>>>(n, Xt, n, cb, qp, cand, ccount, u_indptr,
+                                                                        u_indices, u_values, Zs, b, eta, copy, y_ptr,
+                                                                        y_idx, topk, top_idx, top_val);
+    FSR_TRY(fsr::launched(ctx, "prune_finish_kernel"));
+    P::fallback_rows_kernel<<<(unsigned)ctx->num_sms * 8, 256, 0, ctx->stream>>>(
+        n, Xt, n, u_indptr, u_indices, u_values, Zs, b, eta, copy, y_ptr, y_idx, nflag, flags);
+    FSR_TRY(fsr::launched(ctx, "fallback_rows_kernel"));
+    P::fallback_select_kernel<<<(unsigned)b, fsr::topk::kThreads, fsmem, ctx->stream>>>(n, Xt, n, topk, top_idx,
+                                                                                      top_val, nflag, flags);
+    FSR_TRY(fsr::launched(ctx, "fallback_select_kernel"));
+  }
+  return FSR_OK;
+}
+
 template <typename T>
 int filter_impl(fsr_ctx* ctx, int64_t n, int64_t r, int u_sparse, const int64_t* u_indptr, const int32_t* u_indices,
                 const T* u_values, const T* u_dense, int64_t ldu, const T* w, const double* eta, int64_t b,
                 const int64_t* y_ptr, const int64_t* y_idx, const T* y_val, int copy_uncovered, void* workspace,
                 T* X, int64_t topk, int64_t* top_idx, T* top_val) {
+  if constexpr (std::is_same<T, float>::value) {
+    if (u_sparse && !X && topk > 0 && ctx->topk_prune && fsr::prune::applicable(n, b, topk) &&
+        fsr::aligned(workspace, 256))
+      return filter_pruned(ctx, n, r, u_indptr, u_indices, u_values, w, eta, b, y_ptr, y_idx, y_val, copy_uncovered,
+                           workspace, topk, top_idx, top_val);
+  }
   char* ws = (char*)workspace;
   const size_t es = sizeof(T);
   T* Zt = (T*)ws;
@@ -236,6 +333,7 @@ int64_t fsr_filter_workspace_bytes(int dtype, int64_t n, int64_t r, int64_t b, i
   const size_t es = fsr::dtype_size(dtype);
   size_t total = align256((size_t)b * r * es) + align256((size_t)r * b * es);
   if (need_x) total += align256((size_t)n * b * es);
+  if (need_x && dtype == FSR_F32) total += fsr::prune::workspace_bytes(n, r, b);
   return (int64_t)total + 256;
 }
 

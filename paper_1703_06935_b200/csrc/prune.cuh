@@ -1,0 +1,600 @@
+// Certified top-k for the online step (K9 + select), fp32 only.
+//
+// The ranked-query step returns the top K of every x_q = U~ Zs[:, q] in the
+// reference's rank order (ranking.py:390-395).  K9 is bound by the L2 -> SM
+// gathers of Zs rows (4 bytes per column per nonzero), so
+// the pruned path gathers Zs rounded to fp16 (per-query power-of-two scale,
+// half the bytes), and then re-scores only the rows that can still be in the
+// top K with the fp32 data, in the same order as the unpruned fp32 K9.  The
+// returned top-K indices and values are therefore the ones the unpruned fp32
+// path returns, bit for bit; fp16 values are never returned.
+//
+// Bound (row i with m_i entries, query q, rounding unit u = 2^-24):
+//   |x_fp32 - x~_fp32| <= sum_j |u_ij||zs_j - zs~_j| + gamma_m (sum |u||zs| + sum |u||zs~|)
+//                      <= ||u_i||_2 ||zs_q||_2 (2^-11 + 2.01 m_i u) + sqrt(m_i) ||u_i||_2 2^-25 / s_q
+//                      <= c_i * Zb_q,
+//   c_i  = ||u_i||_2 (2^-11 + 2.01 m_i 2^-24 + sqrt(m_i) 2^-38)   (K9h, from the row it streams)
+//   Zb_q = max(||zs_q||_2, 2^13 / s_q)                           (zs_half_kernel)
+// (fp16 rounding is relative 2^-11 for normal scaled values and absolute
+// 2^-25 below the normal range; Cauchy-Schwarz bounds both sums.)  With
+// lower_i = x~_i - c_i Zb and upper_i = x~_i + c_i Zb (directed rounding), any
+// threshold t such that at least K rows have lower >= t satisfies t <= x_(K),
+// so {i : upper_i >= t} contains every exact top-K row and every tie at the
+// K-th value.  t comes from a 1/16 sample of the lower keys and is verified
+// by counting on the full pass; when the count falls short or the candidates
+// overflow shared memory the query is flagged and recomputed exactly by the
+// fallback kernels (launched always, they exit at once when nothing is
+// flagged, so the step stays one CUDA graph).
+#pragma once
+
+#include <cuda_fp16.h>
+
+#include "spmm.cuh"
+#include "topk.cuh"
+
+namespace fsr {
+namespace prune {
+
+constexpr int kThreads = 256;  // prune_select_kernel: several CTAs per SM overlap their serial phases
+constexpr int kCap = 1024;     // candidates held in shared memory (typical ~3K + band); more -> fallback
+
+// Per query column q of Zs (r x b, ld b): amax, ||zs_q||_2 and the scale
+// s_q = 2^(14 - e) with amax < 2^e (so |zs * s| < 2^14); Zh = half(Zs * s).
+// qp[q] = {1 / s_q, Zb_q}.  Also clears the fallback counter.
+__global__ void __launch_bounds__(256) zs_half_kernel(int64_t r, int64_t b, const float* __restrict__ Zs,
+                                                      __half* __restrict__ Zh, float2* __restrict__ qp,
+                                                      int* __restrict__ nflag) {
+  __shared__ float smax[8][33];
+  __shared__ double sss[8][33];
+  __shared__ float sscale[32];
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  const int64_t col = (int64_t)blockIdx.x * 32 + tx;
+  float amax = 0.f;
+  double ss = 0.0;
+  if (col < b)
+    for (int64_t j = ty; j < r; j += 8) {
+      const float v = Zs[j * b + col];
+      amax = fmaxf(amax, fabsf(v));
+      ss = fma((double)v, (double)v, ss);
+    }
+  smax[ty][tx] = amax;
+  sss[ty][tx] = ss;
+  __syncthreads();
+  if (ty == 0) {
+    for (int k = 1; k < 8; ++k) {
+      amax = fmaxf(amax, smax[k][tx]);
+      ss += sss[k][tx];
+    }
+    float s = 1.f, inv = 1.f, zb = 0.f;
+    if (amax > 0.f) {
+      int e;
+      frexpf(amax, &e);  // amax = f 2^e, f in [0.5, 1)
+      const int k = max(-120, min(120, 14 - e));
+      s = ldexpf(1.f, k);
+      inv = ldexpf(1.f, -k);
+      const float zn = __double2float_ru(__dsqrt_ru(ss) * (1.0 + 0x1p-40));
+      zb = fmaxf(zn, ldexpf(1.f, 13 - k));
+    }
+    sscale[tx] = s;
+    if (col < b) qp[col] = make_float2(inv, zb);
+  }
+  __syncthreads();
+  const float s = sscale[tx];
+  if (col < b)
+    for (int64_t j = ty; j < r; j += 8) Zh[j * b + col] = __float2half_rn(Zs[j * b + col] * s);
+  if (blockIdx.x == 0 && tx == 0 && ty == 0) *nflag = 0;
+}
+
+// K9h: Xt~ (ncols x n_rows, ld ldy) = (A Zh) .* inv_s over column panels of
+// Measured at C3 (tools: _exp sweeps): NV = 1 (256-column
+// panels), DEPTH 4, 4 CTAs/SM (58 registers) 15.7 ms; NV = 1 DEPTH 8 3 CTAs/SM
+// 15.8; NV = 2 DEPTH 4 at 2 or 3 CTAs/SM 20.5 / 16.5; a barrier-free variant
+// (warp-owned 8-row items, persistent grid, per-warp transposes) 19.1-19.4.
+// FFMA2 on converted half pairs and 32-bit row offsets (one IMAD.WIDE per
+// gather) took it from 18.7 to 16.8 ms on a synthetic U~.
+
+// PW = 256 NV columns (8 halves = 16 bytes per lane per vector); the same
+// CTA layout as spmm_rowpanel_T_kernel (ROWS rows handed to 8 warps from a
+// shared counter, transposed tile in shared memory).  Panel 0 also writes the
+// row bound factor c_i.  Requires ncols % 8 == 0 and 16-byte aligned Zh rows.
+template <int NV, int DEPTH, int ROWS, int MINB>
+__global__ void __launch_bounds__(256, MINB) spmm_T_half_kernel(int64_t n_rows, const int64_t* __restrict__ indptr,
+                                                          const int32_t* __restrict__ indices,
+                                                          const float* __restrict__ vals, int64_t ncols,
+                                                          const __half* __restrict__ Zh, int64_t ldx,
+                                                          const float2* __restrict__ qp, float* __restrict__ Yt,
+                                                          int64_t ldy, float* __restrict__ cbound) {
+  constexpr int PW = 256 * NV;
+  extern __shared__ __align__(16) unsigned char dyn_tile[];
+  float(*tile)[PW + 1] = reinterpret_cast<float(*)[PW + 1]>(dyn_tile);
+  __shared__ int next_row;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t row0 = (int64_t)blockIdx.x * ROWS;
+  const int64_t p0 = (int64_t)blockIdx.y * PW;
+  const int64_t c0 = p0 + (int64_t)lane * 8;
+  bool live[NV];
+#pragma unroll
+  for (int u = 0; u < NV; ++u) live[u] = c0 + u * 256 < ncols;
+  if (threadIdx.x == 0) next_row = 8;
+  __syncthreads();
+  // per-lane base of its 8 columns; row offsets in 32 bits (Zh <= 4 GB): one IMAD.WIDE per gather
+  const __half* zl = Zh + c0;
+  const uint32_t ldx32 = (uint32_t)ldx;
+  for (int rr = warp; rr < ROWS;) {
+    const int64_t i = row0 + rr;
+    float2 acc[NV][4];
+#pragma unroll
+    for (int u = 0; u < NV; ++u)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) acc[u][q] = make_float2(0.f, 0.f);
+    if (i < n_rows) {
+      const int64_t e0 = __ldg(indptr + i), e1 = __ldg(indptr + i + 1);
+      float ss = 0.f;  // sum of squares, rounded up (an upper bound of ||u_i||^2)
+      for (int64_t base = e0; base < e1; base += 32) {
+        const int m = (e1 - base) < 32 ? (int)(e1 - base) : 32;
+        int my_col = 0;
+        float my_val = 0.f;
+        if (lane < m) {
+          my_col = __ldg(indices + base + lane);
+          my_val = __ldg(vals + base + lane);
+        }
+        ss = __fmaf_ru(my_val, my_val, ss);
+        int j = 0;
+        for (; j + DEPTH <= m; j += DEPTH) {
+          uint32_t c[DEPTH];
+          float a[DEPTH];
+#pragma unroll
+          for (int g = 0; g < DEPTH; ++g) {
+            c[g] = (uint32_t)__shfl_sync(0xffffffffu, my_col, j + g);
+            a[g] = __shfl_sync(0xffffffffu, my_val, j + g);
+          }
+          uint4 raw[DEPTH][NV];
+#pragma unroll
+          for (int g = 0; g < DEPTH; ++g)
+#pragma unroll
+            for (int u = 0; u < NV; ++u)
+              if (live[u]) raw[g][u] = __ldg(reinterpret_cast<const uint4*>(zl + c[g] * ldx32 + u * 256));
+#pragma unroll
+          for (int g = 0; g < DEPTH; ++g) {
+            const float2 a2 = make_float2(a[g], a[g]);
+#pragma unroll
+            for (int u = 0; u < NV; ++u) {
+              if (!live[u]) continue;
+              const __half2* h = reinterpret_cast<const __half2*>(&raw[g][u]);
+#pragma unroll
+              for (int k = 0; k < 4; ++k) acc[u][k] = __ffma2_rn(a2, __half22float2(h[k]), acc[u][k]);
+            }
+          }
+        }
+        for (; j < m; ++j) {
+          const uint32_t c = (uint32_t)__shfl_sync(0xffffffffu, my_col, j);
+          const float2 a2 = make_float2(__shfl_sync(0xffffffffu, my_val, j), 0.f);
+#pragma unroll
+          for (int u = 0; u < NV; ++u) {
+            if (!live[u]) continue;
+            const uint4 t = __ldg(reinterpret_cast<const uint4*>(zl + c * ldx32 + u * 256));
+            const __half2* h = reinterpret_cast<const __half2*>(&t);
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+              acc[u][k] = __ffma2_rn(make_float2(a2.x, a2.x), __half22float2(h[k]), acc[u][k]);
+          }
+        }
+      }
+      if (blockIdx.y == 0) {
+#pragma unroll
+        for (int o = 16; o; o >>= 1) ss = __fadd_ru(ss, __shfl_xor_sync(0xffffffffu, ss, o));
+        if (lane == 0) {
+          const double m = (double)(e1 - e0);
+          const double f = 0x1p-11 + 2.01 * m * 0x1p-24 + sqrt(m) * 0x1p-38;
+          cbound[i] = __double2float_ru(__dsqrt_ru((double)ss) * f * (1.0 + 0x1p-20));
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < NV; ++u)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        tile[rr][lane * 8 + u * 256 + 2 * q] = acc[u][q].x;
+        tile[rr][lane * 8 + u * 256 + 2 * q + 1] = acc[u][q].y;
+      }
+    int nr = 0;
+    if (lane == 0) nr = atomicAdd(&next_row, 1);
+    rr = __shfl_sync(0xffffffffu, nr, 0);
+  }
+  __syncthreads();
+  for (int c = warp; c < PW; c += 8) {
+    const int64_t col = p0 + c;
+#pragma unroll
+    for (int h = 0; h < ROWS / 32; ++h) {
+      const int64_t i = row0 + h * 32 + lane;
+      if (col < ncols && i < n_rows) Yt[col * ldy + i] = tile[h * 32 + lane][c] * qp[col].x;
+    }
+  }
+}
+
+__device__ __forceinline__ float bound_of(float c, float zb) { return __fadd_ru(__fmul_ru(c, zb), 1.401298464e-45f); }
+
+// 32-bit order key of a float (-0 folded onto +0): key order == value order.
+__device__ __forceinline__ uint32_t key32(float x) {
+  if (x == 0.0f) x = 0.0f;
+  const uint32_t u = __float_as_uint(x);
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+
+__device__ __forceinline__ float key_to_float(uint64_t k) {
+  return __uint_as_float((k & 0x80000000ull) ? (uint32_t)(k & 0x7fffffffull) : (uint32_t)~k);
+}
+
+// Visit (e, x[e], c[e]) for e in [0, m) (m < 2^31) with 16-byte loads of both
+// arrays, U vectors in flight per thread, 32-bit indexing.
+template <int U, typename F>
+__device__ __forceinline__ void for_each_xc32(const float* __restrict__ x, const float* __restrict__ c, int m, F&& f) {
+  if ((((uintptr_t)x | (uintptr_t)c) & 15) != 0) {
+    for (int e = threadIdx.x; e < m; e += blockDim.x) f(e, x[e], __ldg(c + e));
+    return;
+  }
+  const float4* xv = reinterpret_cast<const float4*>(x);
+  const float4* cv = reinterpret_cast<const float4*>(c);
+  const int mv = m / 4, step = blockDim.x * U;
+  for (int base = threadIdx.x; base < mv; base += step) {
+    float4 xa[U], ca[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int i = base + u * blockDim.x;
+      if (i < mv) {
+        xa[u] = __ldg(xv + i);
+        ca[u] = __ldg(cv + i);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int i = base + u * blockDim.x;
+      if (i < mv) {
+        f(4 * i, xa[u].x, ca[u].x);
+        f(4 * i + 1, xa[u].y, ca[u].y);
+        f(4 * i + 2, xa[u].z, ca[u].z);
+        f(4 * i + 3, xa[u].w, ca[u].w);
+      }
+    }
+  }
+  for (int e = mv * 4 + threadIdx.x; e < m; e += blockDim.x) f(e, x[e], __ldg(c + e));
+}
+
+// Visit (e, x[e], c[e]) for e in [0, m) with 16-byte loads of both arrays,
+// U vectors in flight per thread (scalar loads when either is misaligned).
+template <int U, typename F>
+__device__ __forceinline__ void for_each_xc(const float* __restrict__ x, const float* __restrict__ c, int64_t m,
+                                            F&& f) {
+  if ((((uintptr_t)x | (uintptr_t)c) & 15) != 0) {
+    for (int64_t e = threadIdx.x; e < m; e += blockDim.x) f(e, x[e], __ldg(c + e));
+    return;
+  }
+  const float4* xv = reinterpret_cast<const float4*>(x);
+  const float4* cv = reinterpret_cast<const float4*>(c);
+  const int64_t mv = m / 4, step = (int64_t)blockDim.x * U;
+  for (int64_t base = threadIdx.x; base < mv; base += step) {
+    float4 xa[U], ca[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = base + (int64_t)u * blockDim.x;
+      if (i < mv) {
+        xa[u] = __ldg(xv + i);
+        ca[u] = __ldg(cv + i);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = base + (int64_t)u * blockDim.x;
+      if (i < mv) {
+        f(4 * i, xa[u].x, ca[u].x);
+        f(4 * i + 1, xa[u].y, ca[u].y);
+        f(4 * i + 2, xa[u].z, ca[u].z);
+        f(4 * i + 3, xa[u].w, ca[u].w);
+      }
+    }
+  }
+  for (int64_t e = mv * 4 + threadIdx.x; e < m; e += blockDim.x) f(e, x[e], __ldg(c + e));
+}
+
+// The exact fp32 score of row i for query q, in the unpruned K9's order
+// (sequential FMAs over the row's entries from 0), computed by one warp
+// (lanes load and gather, the chain runs on broadcast values), or the stored
+// value for rows the unpruned path does not sum (empty rows; copied uncovered
+// rows).  Uniform across the warp.
+__device__ __forceinline__ float exact_score_warp(int64_t i, int64_t q, const float* __restrict__ xt_row,
+                                                  const int64_t* __restrict__ indptr,
+                                                  const int32_t* __restrict__ indices,
+                                                  const float* __restrict__ vals, const float* __restrict__ Zs,
+                                                  int64_t ldz, const double* __restrict__ eta, int copy,
+                                                  const int64_t* __restrict__ y_ptr,
+                                                  const int64_t* __restrict__ y_idx) {
+  const int lane = threadIdx.x & 31;
+  const int64_t e0 = indptr[i], e1 = indptr[i + 1];
+  if (e0 == e1) return xt_row[i];
+  if (copy && eta && eta[i] == 0.0) {
+    bool hit = false;
+    for (int64_t t = y_ptr[q] + lane; t < y_ptr[q + 1]; t += 32) hit |= y_idx[t] == i;
+    if (__any_sync(0xffffffffu, hit)) return xt_row[i];
+  }
+  float acc = 0.f;
+  for (int64_t base = e0; base < e1; base += 128) {
+    const int m = e1 - base < 128 ? (int)(e1 - base) : 128;
+    float a[4], z[4];
+    int c[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int t = k * 32 + lane;
+      c[k] = t < m ? __ldg(indices + base + t) : 0;
+      a[k] = t < m ? __ldg(vals + base + t) : 0.f;
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) z[k] = k * 32 + lane < m ? __ldg(Zs + (int64_t)c[k] * ldz + q) : 0.f;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int mk = m - k * 32 < 32 ? m - k * 32 : 32;
+      for (int e = 0; e < mk; ++e)
+        acc = fmaf(__shfl_sync(0xffffffffu, a[k], e), __shfl_sync(0xffffffffu, z[k], e), acc);
+    }
+  }
+  return acc;
+}
+
+// Thread-sequential form of the same score (fallback_rows_kernel).
+__device__ __forceinline__ float exact_score(int64_t i, int64_t q, const float* __restrict__ xt_row,
+                                             const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices,
+                                             const float* __restrict__ vals, const float* __restrict__ Zs,
+                                             int64_t ldz, const double* __restrict__ eta, int copy,
+                                             const int64_t* __restrict__ y_ptr, const int64_t* __restrict__ y_idx) {
+  const int64_t e0 = indptr[i], e1 = indptr[i + 1];
+  if (e0 == e1) return xt_row[i];
+  if (copy && eta && eta[i] == 0.0) {
+    for (int64_t t = y_ptr[q]; t < y_ptr[q + 1]; ++t)
+      if (y_idx[t] == i) return xt_row[i];
+  }
+  float acc = 0.f;
+  for (int64_t e = e0; e < e1; ++e)
+    acc = fmaf(__ldg(vals + e), __ldg(Zs + (int64_t)__ldg(indices + e) * ldz + q), acc);
+  return acc;
+}
+
+// Selection in two kernels so the streaming one stays light (registers ->
+// occupancy -> bytes in flight):
+// prune_collect_kernel -- persistent CTAs, one query at a time:
+//  1. t = threshold on the lower keys from a 1/16 sample (two 12-bit digits);
+//  2. one pass: count lower >= t, collect the rows with upper >= t (a round-
+//     to-nearest pre-filter skips the directed-rounding work far below t)
+//     into cand[q][0 .. kCap); ccount[q] = count, or flags the query when
+//     count < K or the candidates overflow.
+// prune_finish_kernel -- one CTA per query:
+//  3. lambda_K = K-th largest lower among the candidates (they hold every
+//     row with lower >= t), keep upper >= lambda_K;
+//  4. exact re-score of those (warp per row), bitonic sort, top K out.
+struct SelShared {
+  unsigned int hist[1 << topk::kHistBits];
+  unsigned int count;
+  unsigned int found_bin;
+  unsigned long long above;
+  unsigned long long n_lower;
+  unsigned int n_keep;
+};
+
+__global__ void __launch_bounds__(kThreads) prune_collect_kernel(int64_t n, int64_t b, const float* __restrict__ Xt,
+                                                                  int64_t ldx, const float* __restrict__ cb,
+                                                                  const float2* __restrict__ qp, int64_t K,
+                                                                  int32_t* __restrict__ cand,
+                                                                  int32_t* __restrict__ ccount,
+                                                                  int* __restrict__ nflag, int* __restrict__ flags) {
+  constexpr int KB = 32;
+  constexpr int nb = 1 << topk::kHistBits;
+  __shared__ SelShared sh;
+  const int lane = threadIdx.x & 31;
+  const int64_t nblk = (n + topk::kSampleChunk - 1) / topk::kSampleChunk;
+  const unsigned long long target = (unsigned long long)((2 * K + topk::kSampleEvery - 1) / topk::kSampleEvery) + 8;
+  for (int64_t q = blockIdx.x; q < b; q += gridDim.x) {
+    const float* xr = Xt + q * ldx;
+    const float zb = qp[q].y;
+    const bool vec_ok = ((((uintptr_t)xr) | ((uintptr_t)cb)) & 15) == 0;
+    int32_t* cq = cand + q * kCap;
+    // 1. sampled threshold on the lower keys
+    uint32_t prefix = 0;
+    unsigned long long above0 = 0;
+    for (int level = 0; level < 2; ++level) {
+      for (int t = threadIdx.x; t < nb; t += blockDim.x) sh.hist[t] = 0;
+      __syncthreads();
+      auto add = [&](float x, float c) {
+        const uint32_t k = key32(__fsub_rd(x, bound_of(c, zb)));
+        if (level == 0)
+          atomicAdd(&sh.hist[k >> (KB - topk::kHistBits)], 1u);
+        else if ((k >> (KB - topk::kHistBits)) == prefix)
+          atomicAdd(&sh.hist[(k >> (KB - 2 * topk::kHistBits)) & (nb - 1)], 1u);
+      };
+      if (vec_ok) {
+        // sampled blocks = every kSampleEvery-th block of kSampleChunk elements (whole blocks only)
+        constexpr int VPB = topk::kSampleChunk / 4;  // float4 per block
+        const int nsb = (int)((n / topk::kSampleChunk + topk::kSampleEvery - 1) / topk::kSampleEvery);
+        const int nvec = nsb * VPB;
+        const float4* xv = reinterpret_cast<const float4*>(xr);
+        const float4* cv = reinterpret_cast<const float4*>(cb);
+        for (int v0 = threadIdx.x; v0 < nvec; v0 += 2 * blockDim.x) {
+          float4 xa[2], ca[2];
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            const int v = v0 + u * blockDim.x;
+            if (v < nvec) {
+              const int off = (v / VPB) * topk::kSampleEvery * VPB + v % VPB;
+              xa[u] = __ldg(xv + off);
+              ca[u] = __ldg(cv + off);
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < 2; ++u)
+            if (v0 + u * blockDim.x < nvec) {
+              add(xa[u].x, ca[u].x);
+              add(xa[u].y, ca[u].y);
+              add(xa[u].z, ca[u].z);
+              add(xa[u].w, ca[u].w);
+            }
+        }
+      } else {
+        for (int64_t bk = 0; bk < nblk; bk += topk::kSampleEvery) {
+          const int64_t e0 = bk * topk::kSampleChunk, e1 = min(n, e0 + (int64_t)topk::kSampleChunk);
+          for (int64_t e = e0 + threadIdx.x; e < e1; e += blockDim.x) add(xr[e], __ldg(cb + e));
+        }
+      }
+      __syncthreads();
+      topk::find_bin_t<kThreads>(sh.hist, nb, level == 0 ? target : target - above0, &sh.found_bin, &sh.above);
+      if (level == 0) above0 = sh.above;
+      prefix = (prefix << topk::kHistBits) | sh.found_bin;
+      __syncthreads();
+    }
+    const uint32_t t_lo = prefix << (KB - 2 * topk::kHistBits);
+    const float tf = key_to_float((uint64_t)t_lo);
+    const float tf_pre = tf - fabsf(tf) * 0x1p-20f - 0x1p-126f;  // conservative round-to-nearest pre-filter
+    // 2. one pass
+    if (!threadIdx.x) {
+      sh.count = 0;
+      sh.n_lower = 0;
+    }
+    __syncthreads();
+    unsigned mine = 0;
+    for_each_xc32<4>(xr, cb, (int)n, [&](int e, float x, float c) {
+      if (x + c * zb >= tf_pre) {
+        const float bd = bound_of(c, zb);
+        mine += key32(__fsub_rd(x, bd)) >= t_lo;
+        if (key32(__fadd_ru(x, bd)) >= t_lo) {
+          const unsigned slot = atomicAdd(&sh.count, 1u);
+          if (slot < (unsigned)kCap) cq[slot] = (int32_t)e;
+        }
+      }
+    });
+#pragma unroll
+    for (int o = 16; o; o >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, o);
+    if (lane == 0) atomicAdd(&sh.n_lower, (unsigned long long)mine);
+    __syncthreads();
+    if (!threadIdx.x) {
+      const bool bad = sh.n_lower < (unsigned long long)K || sh.count > (unsigned)kCap;
+      ccount[q] = bad ? -1 : (int32_t)sh.count;
+      if (bad) flags[atomicAdd(nflag, 1)] = (int)q;
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(kThreads) prune_finish_kernel(
+    int64_t n, const float* __restrict__ Xt, int64_t ldx, const float* __restrict__ cb, const float2* __restrict__ qp,
+    const int32_t* __restrict__ cand, const int32_t* __restrict__ ccount, const int64_t* __restrict__ indptr,
+    const int32_t* __restrict__ indices, const float* __restrict__ vals, const float* __restrict__ Zs, int64_t ldz,
+    const double* __restrict__ eta, int copy, const int64_t* __restrict__ y_ptr, const int64_t* __restrict__ y_idx,
+    int64_t K, int64_t* __restrict__ out_idx, float* __restrict__ out_val) {
+  __shared__ uint64_t ckey[kCap];
+  __shared__ int64_t cidx[kCap];
+  __shared__ unsigned n_keep;
+  const int64_t q = blockIdx.x;
+  const int cnt = ccount[q];
+  if (cnt < 0) return;  // flagged: the fallback kernels answer this query
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const float* xr = Xt + q * ldx;
+  const float zb = qp[q].y;
+  const int32_t* cq = cand + q * kCap;
+  if (!threadIdx.x) n_keep = 0;
+  // 3. lambda_K among the candidates
+  for (int t = threadIdx.x; t < cnt; t += blockDim.x) {
+    const int64_t i = cq[t];
+    cidx[t] = i;
+    ckey[t] = topk::order_key(__fsub_rd(xr[i], bound_of(cb[i], zb)));
+  }
+  __syncthreads();
+  topk::bitonic_sort(ckey, cidx, cnt);  // (lower key desc, index asc)
+  const uint64_t lam = ckey[K - 1];
+  __syncthreads();
+  // compaction in place: the writes of one round land below the reads of the next
+  for (int base = 0; base < cnt; base += blockDim.x) {
+    const int t = base + threadIdx.x;
+    int64_t i = 0;
+    bool keep = false;
+    if (t < cnt) {
+      i = cidx[t];
+      keep = topk::order_key(__fadd_ru(xr[i], bound_of(cb[i], zb))) >= lam;
+    }
+    __syncthreads();
+    if (keep) cidx[atomicAdd(&n_keep, 1u)] = i;
+  }
+  __syncthreads();
+  const unsigned keep = n_keep;
+  // 4. exact re-score (warp per row), sort, output
+  for (unsigned t = wid; t < keep; t += kThreads / 32) {
+    const float v = exact_score_warp(cidx[t], q, xr, indptr, indices, vals, Zs, ldz, eta, copy, y_ptr, y_idx);
+    if (lane == 0) ckey[t] = topk::order_key(v);
+  }
+  __syncthreads();
+  topk::bitonic_sort(ckey, cidx, (int)keep);
+  for (int64_t m = threadIdx.x; m < K; m += blockDim.x) {
+    out_idx[q * K + m] = cidx[m];
+    out_val[q * K + m] = key_to_float(ckey[m]);
+  }
+}
+
+// ---- fallback for flagged queries (exit at once when nothing is flagged) ----
+
+// Exact fp32 scores of every summed row of the flagged queries, written over
+// the pruned values (persistent grid over (flagged query, 256-row block)).
+__global__ void __launch_bounds__(256) fallback_rows_kernel(int64_t n, float* __restrict__ Xt, int64_t ldx,
+                                                            const int64_t* __restrict__ indptr,
+                                                            const int32_t* __restrict__ indices,
+                                                            const float* __restrict__ vals,
+                                                            const float* __restrict__ Zs, int64_t ldz,
+                                                            const double* __restrict__ eta, int copy,
+                                                            const int64_t* __restrict__ y_ptr,
+                                                            const int64_t* __restrict__ y_idx,
+                                                            const int* __restrict__ nflag,
+                                                            const int* __restrict__ flags) {
+  const int nf = *nflag;
+  if (!nf) return;
+  const int64_t nblk = (n + 255) / 256;
+  for (int64_t item = blockIdx.x; item < nf * nblk; item += gridDim.x) {
+    const int64_t q = flags[item / nblk];
+    const int64_t i = (item % nblk) * 256 + threadIdx.x;
+    if (i < n) {
+      float* xr = Xt + q * ldx;
+      xr[i] = exact_score(i, q, xr, indptr, indices, vals, Zs, ldz, eta, copy, y_ptr, y_idx);
+    }
+  }
+}
+
+// Exact top K of the (now exact) rows of the flagged queries.
+__global__ void __launch_bounds__(topk::kThreads) fallback_select_kernel(int64_t n, const float* __restrict__ Xt,
+                                                                         int64_t ldx, int64_t K,
+                                                                         int64_t* __restrict__ out_idx,
+                                                                         float* __restrict__ out_val,
+                                                                         const int* __restrict__ nflag,
+                                                                         const int* __restrict__ flags) {
+  if ((int)blockIdx.x >= *nflag) return;
+  extern __shared__ __align__(16) unsigned char dyn[];
+  uint64_t* ckey = (uint64_t*)dyn;
+  int64_t* cidx = (int64_t*)(ckey + topk::kCap);
+  __shared__ topk::Shared sh;
+  const int64_t q = flags[blockIdx.x];
+  topk::Range<float, false> R{Xt + q * ldx, nullptr, n, 0};
+  topk::select_exact<float, false>(R, K, sh, ckey, cidx);
+  __syncthreads();
+  for (int64_t m = threadIdx.x; m < K; m += blockDim.x) {
+    const int64_t i = cidx[m];
+    out_idx[q * K + m] = i;
+    out_val[q * K + m] = R.v[i];
+  }
+}
+
+// Workspace of the pruned path beyond the unpruned one.
+inline size_t workspace_bytes(int64_t n, int64_t r, int64_t b) {
+  auto al = [](size_t x) { return (x + 255) / 256 * 256; };
+  return al((size_t)r * b * 2) + al((size_t)b * 8) + al((size_t)n * 4) + al((size_t)(b + 1) * 4) +
+         al((size_t)b * kCap * 4) + al((size_t)b * 4);
+}
+
+inline bool applicable(int64_t n, int64_t b, int64_t K) {
+  return n >= (int64_t)topk::kSampleChunk * topk::kSampleEvery * 8 && n < ((int64_t)1 << 31) && b >= 256 && b % 8 == 0 && K >= 1 &&
+         K <= kCap / 8;
+}
+
+}  // namespace prune
+}  // namespace fsr

@@ -53,20 +53,23 @@ struct Shared {
 };
 
 // The bin (scanning from the top) where the running count first reaches `need`
-// (or the lowest bin if the total is smaller); found_bin / above (count strictly above).
-__device__ void find_bin(Shared& sh, int nb, unsigned long long need) {
-  typedef cub::BlockScan<unsigned long long, kThreads> Scan;
+// (or the lowest bin if the total is smaller): *found_bin, *above (count
+// strictly above).  NT = threads per block.
+template <int NT>
+__device__ void find_bin_t(const unsigned int* hist, int nb, unsigned long long need, unsigned int* found_bin,
+                           unsigned long long* above) {
+  typedef cub::BlockScan<unsigned long long, NT> Scan;
   __shared__ typename Scan::TempStorage scan_tmp;
-  const int per = nb / kThreads > 0 ? nb / kThreads : 1;
+  const int per = nb / NT > 0 ? nb / NT : 1;
   unsigned long long mine = 0;
   const int hi = nb - 1 - (int)threadIdx.x * per;
   for (int q = 0; q < per; ++q) {
     const int bin = hi - q;
-    if (bin >= 0) mine += sh.hist[bin];
+    if (bin >= 0) mine += hist[bin];
   }
   if (threadIdx.x == 0) {
-    sh.found_bin = 0;
-    sh.above = 0;
+    *found_bin = 0;
+    *above = 0;
   }
   __syncthreads();
   unsigned long long before = 0, total = 0;
@@ -75,15 +78,19 @@ __device__ void find_bin(Shared& sh, int nb, unsigned long long need) {
   for (int q = 0; q < per; ++q) {
     const int bin = hi - q;
     if (bin < 0) break;
-    const unsigned long long h = sh.hist[bin];
+    const unsigned long long h = hist[bin];
     if (run < need && run + h >= need) {
-      sh.found_bin = (unsigned)bin;
-      sh.above = run;
+      *found_bin = (unsigned)bin;
+      *above = run;
     }
     run += h;
   }
-  if (total < need && threadIdx.x == 0) sh.above = total;  // everything qualifies; bin 0
+  if (total < need && threadIdx.x == 0) *above = total;  // everything qualifies; bin 0
   __syncthreads();
+}
+
+__device__ __forceinline__ void find_bin(Shared& sh, int nb, unsigned long long need) {
+  find_bin_t<kThreads>(sh.hist, nb, need, &sh.found_bin, &sh.above);
 }
 
 __device__ __forceinline__ bool before_in_rank(uint64_t ka, int64_t ia, uint64_t kb, int64_t ib) {

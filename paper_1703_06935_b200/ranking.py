@@ -265,6 +265,27 @@ def filter_device(dec: SpectralDecomposition, h: TransferFunction, queries: Devi
     return res
 
 
+def topk_pruned(n: int, b: int, k: int, dtype, sparse: bool = True) -> bool:
+    """Whether a top-k-only ``filter_device`` call takes the certified pruned
+    path (csrc/prune.cuh ``applicable``; the context option FSR_OPT_TOPK_PRUNE
+    must also be on): fp32 sparse U~, n >= 131072, b >= 256, b % 8 == 0,
+    1 <= k <= 128.  Its top-k equals the unpruned fp32 path's bit for bit."""
+    import torch
+
+    return (sparse and dtype == torch.float32 and 131072 <= n < 2 ** 31 and b >= 256 and b % 8 == 0
+            and 1 <= k <= 128)
+
+
+def pruned_fallback_count(workspace, n: int, r: int, b: int) -> int:
+    """Queries of the last pruned call answered by the exact fallback (the
+    counter in filter_pruned's workspace layout, csrc/k8_online.cu)."""
+    import torch
+
+    al = lambda x: (x + 255) // 256 * 256  # noqa: E731
+    off = al(b * r * 4) + al(r * b * 4) + al(n * b * 4) + al(r * b * 2) + al(b * 8) + al(n * 4)
+    return int(workspace[off:off + 4].view(torch.int32).item())
+
+
 def _as_device_dec(dec) -> SpectralDecomposition:
     if isinstance(dec, SpectralDecomposition):
         return dec

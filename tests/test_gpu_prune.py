@@ -1,0 +1,128 @@
+"""Certified pruned top-k (csrc/prune.cuh): fp16-gathered K9 + exact fp32
+re-score must return exactly the unpruned fp32 path's top-k -- the same
+indices and bitwise the same values -- including ties, empty observations,
+copied uncovered rows and queries that overflow the candidate buffer (the
+device fallback)."""
+
+from types import SimpleNamespace
+
+import numpy as np
+import pytest
+import scipy.sparse as sp
+
+from oracle import fsr_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from paper_1703_06935_b200 import _native as N  # noqa: E402
+from paper_1703_06935_b200 import ranking, spectral  # noqa: E402
+
+
+def make_dec(n, r, per_row, seed, dup_block=0, empty_every=0):
+    rng = np.random.default_rng(seed)
+    lens = rng.integers(max(1, per_row // 4), 2 * per_row, size=n)
+    if empty_every:
+        lens[::empty_every] = 0
+    indptr = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    cols = np.concatenate([np.sort(rng.choice(r, size=k, replace=False)) for k in lens]).astype(np.int32)
+    vals = rng.standard_normal(indptr[-1]) * rng.choice([1.0, 1e-3], size=indptr[-1], p=[0.9, 0.1])
+    U = sp.csr_matrix((vals, cols, indptr), shape=(n, r))
+    if dup_block:
+        # dup_block copies of row 1 (identical scores -> ties broken by index)
+        rows = [U[i] if not (1000 <= i < 1000 + dup_block) else U[1] for i in range(n)]
+        U = sp.vstack(rows).tocsr()
+    eta = np.sqrt(np.asarray(U.multiply(U).sum(axis=1)).ravel())
+    lam = np.sort(rng.uniform(-0.3, 1.0, r))[::-1].copy()
+    host = SimpleNamespace(U=U, eigenvalues=lam, eta=eta, variant="sparse", provenance=None, components=None)
+    return host, spectral.SpectralDecomposition.from_host(host, dtype="float32")
+
+
+def queries(n, b, seed, k=50, empty=(), extra=None):
+    rng = np.random.default_rng(seed)
+    ys = []
+    for j in range(b):
+        if j in empty:
+            idx = np.array([], dtype=np.int64)
+        else:
+            idx = np.unique(rng.integers(0, n, size=k))
+            if extra and j in extra:
+                idx = np.unique(np.concatenate([idx, extra[j]]))
+        ys.append(ranking.ObservationVector(n, idx, rng.random(idx.size) ** 3 + 0.01, cap=max(idx.size, 1)))
+    return ranking.QueryBatch.from_vectors(ys)
+
+
+def both(dec, qb, K=100, h=None, flags=None):
+    h = h or ranking.h_alpha(0.99)
+    ctx = N.Context.get()
+    dq = ranking.DeviceQueries(qb, dec.dtype, dec.eta_device.device)
+    need = int(ctx.lib.fsr_filter_workspace_bytes(N.F32, dec.n, dec.r, qb.b, 1))
+    ws = torch.empty(need, dtype=torch.uint8, device=dec.eta_device.device)
+    assert ranking.topk_pruned(dec.n, qb.b, K, dec.dtype)
+    out = []
+    for prune in (True, False):
+        ctx.set_topk_prune(prune)
+        try:
+            r = ranking.filter_device(dec, h, dq, topk=K, want_x=False, workspace=ws)
+            torch.cuda.synchronize()
+            out.append((r.top_idx.cpu().numpy(), r.top_val.cpu().numpy()))
+            if prune and flags is not None:
+                flags.append(ranking.pruned_fallback_count(ws, dec.n, dec.r, qb.b))
+        finally:
+            ctx.set_topk_prune(True)
+    return out
+
+
+@pytest.mark.parametrize("seed", [0, 1])
+def test_pruned_topk_identical_to_unpruned(seed):
+    n, r, b = 150_000, 600, 256
+    host, dec = make_dec(n, r, 40, seed)
+    qb = queries(n, b, seed + 10)
+    fl = []
+    (pi, pv), (ui, uv) = both(dec, qb, flags=fl)
+    assert fl == [0]  # no query needed the fallback
+    np.testing.assert_array_equal(pi, ui)
+    np.testing.assert_array_equal(pv.view(np.uint32), uv.view(np.uint32))
+    # and the unpruned fp32 path against the fp64 oracle on a few queries
+    w = O.transfer_values(O.h_alpha(0.99), host.eigenvalues)
+    for j in (0, 77, 255):
+        idx = qb.y_idx[qb.y_ptr[j]:qb.y_ptr[j + 1]]
+        val = qb.y_val[qb.y_ptr[j]:qb.y_ptr[j + 1]]
+        x = O.filter_scores(host.U, host.eigenvalues, host.eta, w, idx, val)
+        assert len(np.intersect1d(O.rank(x)[:100], pi[j])) >= 99
+        np.testing.assert_allclose(pv[j], x[pi[j]], rtol=1e-4, atol=1e-5 * np.abs(x).max())
+
+
+def test_pruned_ties_empty_uncovered_and_fallback():
+    n, r, b = 140_000, 400, 256
+    # 5000 identical rows overflow the candidate buffer for queries that hit row 1;
+    # every 97th row is empty (uncovered when observed)
+    host, dec = make_dec(n, r, 30, 3, dup_block=5000, empty_every=97)
+    extra = {5: np.array([1]), 6: np.array([1, 97 * 3]), 9: np.array([97 * 5, 97 * 8])}
+    qb = queries(n, b, 4, empty=(2, 200), extra=extra)
+    fl = []
+    (pi, pv), (ui, uv) = both(dec, qb, flags=fl)
+    assert fl[0] >= 4  # the two empty observations and the queries on the duplicated rows
+    np.testing.assert_array_equal(pi, ui)
+    np.testing.assert_array_equal(pv.view(np.uint32), uv.view(np.uint32))
+    # empty observation: all-zero scores, first K indices
+    np.testing.assert_array_equal(pi[2], np.arange(100))
+    # copied uncovered rows carry y
+    j = 9
+    yv = dict(zip(qb.y_idx[qb.y_ptr[j]:qb.y_ptr[j + 1]], qb.y_val[qb.y_ptr[j]:qb.y_ptr[j + 1]]))
+    for i in (97 * 5, 97 * 8):
+        if i in pi[j]:
+            assert pv[j][list(pi[j]).index(i)] == np.float32(yv[i])
+
+
+def test_pruned_heat_kernel_and_small_k():
+    n, r, b = 131_072 + 5, 300, 512
+    _, dec = make_dec(n, r, 20, 8)
+    qb = queries(n, b, 9, k=30)
+    for K, h in ((1, ranking.heat_kernel(10.0)), (37, ranking.h_alpha(0.9))):
+        (pi, pv), (ui, uv) = both(dec, qb, K=K, h=h)
+        np.testing.assert_array_equal(pi, ui)
+        np.testing.assert_array_equal(pv.view(np.uint32), uv.view(np.uint32))

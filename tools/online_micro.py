@@ -36,10 +36,14 @@ def synth(n, r, nnz, skew, dev, seed=0):
     indptr[1:] = torch.cumsum(lens, 0)
     tot = int(indptr[-1])
     cols = torch.randint(0, r, (tot,), generator=g, device=dev, dtype=torch.int32)
-    # sort columns within rows: key = row * r + col
+    # canonical CSR (sorted, distinct columns per row): key = row * r + col, deduplicated
     rows = torch.repeat_interleave(torch.arange(n, device=dev), lens)
-    key, _ = torch.sort(rows * r + cols.long())
+    key = torch.unique(rows * r + cols.long())  # sorted
+    rows = key // r
     cols = (key % r).to(torch.int32)
+    indptr = torch.zeros(n + 1, dtype=torch.long, device=dev)
+    indptr[1:] = torch.cumsum(torch.bincount(rows, minlength=n), 0)
+    tot = int(key.numel())
     vals = torch.randn(tot, generator=g, device=dev) / np.sqrt(nnz)
     return DeviceCSR(indptr, cols, vals.float(), (n, r))
 
@@ -52,6 +56,9 @@ def main():
     ap.add_argument("--skew", type=float, default=0.0)
     ap.add_argument("--b", type=int, nargs="+", default=[1, 64, 1024])
     ap.add_argument("--reps", type=int, default=10)
+    ap.add_argument("--prune", default="on", choices=["on", "off", "both"],
+                    help="top-k-only batches through the certified pruned path (on), the unpruned fp32 K9 (off), "
+                         "or both (and check they agree)")
     a = ap.parse_args()
     dev = torch.device("cuda", 0)
     U = synth(a.n, a.r, a.nnz, a.skew, dev)
@@ -64,10 +71,15 @@ def main():
     rng = np.random.default_rng(2)
     h = ranking.h_alpha(0.99)
     out = {"n": a.n, "r": a.r, "nnz": U.nnz, "skew": a.skew, "points": []}
+    modes = {"on": [True], "off": [False], "both": [True, False]}[a.prune]
+    batches = {}
     for b in a.b:
         ptr = np.arange(b + 1, dtype=np.int64) * 50
         idx = np.concatenate([np.sort(rng.choice(a.n, 50, replace=False)) for _ in range(b)])
-        qb = ranking.QueryBatch(a.n, ptr, idx, rng.random(b * 50) ** 3)
+        batches[b] = ranking.QueryBatch(a.n, ptr, idx, rng.random(b * 50) ** 3)
+    for b, prune in [(b, p) for b in a.b for p in modes]:
+        ctx.set_topk_prune(prune)
+        qb = batches[b]
         dq = ranking.DeviceQueries(qb, torch.float32, dev)
         res = ranking.FilterResult()
         for _ in range(3):
@@ -83,9 +95,18 @@ def main():
         st = {k: ctx.stage_time(k)[0] / a.reps for k in ("project", "filter_spmm", "copy_uncovered", "topk")}
         ms = e0.elapsed_time(e1) / a.reps
         bytes_k9 = U.nnz * 8 + (a.n + 1) * 8 + 4 * a.r * b + 4 * a.n * b
-        out["points"].append({"b": b, "ms": ms, "qps": b / ms * 1e3, "stages_ms": st,
-                              "k9_gbs": bytes_k9 / (st["filter_spmm"] * 1e-3) / 1e9})
-    print(json.dumps(out, indent=1))
+        pt = {"b": b, "prune": prune, "variant": os.environ.get("FSR_K9H_VARIANT", "0"), "ms": ms,
+              "qps": b / ms * 1e3, "stages_ms": st, "k9_gbs": bytes_k9 / (st["filter_spmm"] * 1e-3) / 1e9}
+        if a.prune == "both":
+            top = (res.top_idx.cpu(), res.top_val.cpu())
+            if prune:
+                first = top
+            else:
+                pt["identical_to_pruned"] = bool(torch.equal(first[0], top[0]) and
+                                                 torch.equal(first[1].view(torch.int32), top[1].view(torch.int32)))
+        out["points"].append(pt)
+        print(json.dumps(pt), flush=True)
+    print(json.dumps(out))
 
 
 if __name__ == "__main__":
