@@ -86,12 +86,15 @@ __global__ void __launch_bounds__(256) zs_half_kernel(int64_t r, int64_t b, cons
 }
 
 // K9h: Xt~ (ncols x n_rows, ld ldy) = (A Zh) .* inv_s over column panels of
-// Measured at C3 (tools: _exp sweeps): NV = 1 (256-column
-// panels), DEPTH 4, 4 CTAs/SM (58 registers) 15.7 ms; NV = 1 DEPTH 8 3 CTAs/SM
-// 15.8; NV = 2 DEPTH 4 at 2 or 3 CTAs/SM 20.5 / 16.5; a barrier-free variant
-// (warp-owned 8-row items, persistent grid, per-warp transposes) 19.1-19.4.
-// FFMA2 on converted half pairs and 32-bit row offsets (one IMAD.WIDE per
-// gather) took it from 18.7 to 16.8 ms on a synthetic U~.
+// Measured at C3 2%, b = 1024: NV = 1 (256-column
+// panels), DEPTH 8, 4 CTAs/SM (64 registers) 14.8 ms -- kept; DEPTH 4 at 4 /
+// 5 / 6 CTAs/SM 15.7 / 16.4 / 18.1; DEPTH 6 at 5 CTAs/SM 16.6; NV = 2 DEPTH 4
+// at 2 or 3 CTAs/SM 20.5 / 16.5; a barrier-free variant (warp-owned 8-row
+// items, persistent grid, per-warp transposes) 19.1-19.4.  FFMA2 on converted
+// half pairs and 32-bit row offsets (one IMAD.WIDE per gather) took it from
+// 18.7 to 16.8 ms on a synthetic U~.  Neither L2 (55%) nor issue (61%) is
+// saturated (ncu, profiles/r01/k9h_ncu_full.json): the bytes in flight per SM
+// over the loaded L2 latency bound it.
 
 // PW = 256 NV columns (8 halves = 16 bytes per lane per vector); the same
 // CTA layout as spmm_rowpanel_T_kernel (ROWS rows handed to 8 warps from a
