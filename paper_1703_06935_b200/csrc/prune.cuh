@@ -123,86 +123,99 @@ __global__ void __launch_bounds__(256, MINB) spmm_T_half_kernel(int64_t n_rows, 
   // per-lane base of its 8 columns; row offsets in 32 bits (Zh <= 4 GB): one IMAD.WIDE per gather
   const __half* zl = Zh + c0;
   const uint32_t ldx32 = (uint32_t)ldx;
-  for (int rr = warp; rr < ROWS;) {
+  // Rows are handed out from a shared counter (skewed row lengths); within a
+  // row the next 32 entries are in flight while the current 32 are summed.
+  static_assert(NV == 1, "row loop is written for one 256-column vector per lane");
+  int rr = warp;
+  int64_t e0 = 0, e1 = 0;
+  if (row0 + rr < n_rows) {
+    e0 = __ldg(indptr + row0 + rr);
+    e1 = __ldg(indptr + row0 + rr + 1);
+  }
+  int cc = 0;
+  float cv = 0.f;
+  if (lane < e1 - e0) {
+    cc = __ldg(indices + e0 + lane);
+    cv = __ldg(vals + e0 + lane);
+  }
+  while (rr < ROWS) {
     const int64_t i = row0 + rr;
-    float2 acc[NV][4];
+    float2 acc[4];
 #pragma unroll
-    for (int u = 0; u < NV; ++u)
+    for (int q = 0; q < 4; ++q) acc[q] = make_float2(0.f, 0.f);
+    float ss = 0.f;  // sum of squares, rounded up (an upper bound of ||u_i||^2)
+    for (int64_t base = e0; base < e1; base += 32) {
+      const int m = (e1 - base) < 32 ? (int)(e1 - base) : 32;
+      int pc = 0;
+      float pv = 0.f;
+      if (lane < e1 - base - 32) {
+        pc = __ldg(indices + base + 32 + lane);
+        pv = __ldg(vals + base + 32 + lane);
+      }
+      ss = __fmaf_ru(cv, cv, ss);
+      int j = 0;
+      for (; j + DEPTH <= m; j += DEPTH) {
+        uint32_t c[DEPTH];
+        float a[DEPTH];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) acc[u][q] = make_float2(0.f, 0.f);
-    if (i < n_rows) {
-      const int64_t e0 = __ldg(indptr + i), e1 = __ldg(indptr + i + 1);
-      float ss = 0.f;  // sum of squares, rounded up (an upper bound of ||u_i||^2)
-      for (int64_t base = e0; base < e1; base += 32) {
-        const int m = (e1 - base) < 32 ? (int)(e1 - base) : 32;
-        int my_col = 0;
-        float my_val = 0.f;
-        if (lane < m) {
-          my_col = __ldg(indices + base + lane);
-          my_val = __ldg(vals + base + lane);
+        for (int g = 0; g < DEPTH; ++g) {
+          c[g] = (uint32_t)__shfl_sync(0xffffffffu, cc, j + g);
+          a[g] = __shfl_sync(0xffffffffu, cv, j + g);
         }
-        ss = __fmaf_ru(my_val, my_val, ss);
-        int j = 0;
-        for (; j + DEPTH <= m; j += DEPTH) {
-          uint32_t c[DEPTH];
-          float a[DEPTH];
+        uint4 raw[DEPTH];
 #pragma unroll
-          for (int g = 0; g < DEPTH; ++g) {
-            c[g] = (uint32_t)__shfl_sync(0xffffffffu, my_col, j + g);
-            a[g] = __shfl_sync(0xffffffffu, my_val, j + g);
-          }
-          uint4 raw[DEPTH][NV];
+        for (int g = 0; g < DEPTH; ++g)
+          if (live[0]) raw[g] = __ldg(reinterpret_cast<const uint4*>(zl + c[g] * ldx32));
 #pragma unroll
-          for (int g = 0; g < DEPTH; ++g)
+        for (int g = 0; g < DEPTH; ++g) {
+          if (!live[0]) continue;
+          const float2 a2 = make_float2(a[g], a[g]);
+          const __half2* h = reinterpret_cast<const __half2*>(&raw[g]);
 #pragma unroll
-            for (int u = 0; u < NV; ++u)
-              if (live[u]) raw[g][u] = __ldg(reinterpret_cast<const uint4*>(zl + c[g] * ldx32 + u * 256));
-#pragma unroll
-          for (int g = 0; g < DEPTH; ++g) {
-            const float2 a2 = make_float2(a[g], a[g]);
-#pragma unroll
-            for (int u = 0; u < NV; ++u) {
-              if (!live[u]) continue;
-              const __half2* h = reinterpret_cast<const __half2*>(&raw[g][u]);
-#pragma unroll
-              for (int k = 0; k < 4; ++k) acc[u][k] = __ffma2_rn(a2, __half22float2(h[k]), acc[u][k]);
-            }
-          }
-        }
-        for (; j < m; ++j) {
-          const uint32_t c = (uint32_t)__shfl_sync(0xffffffffu, my_col, j);
-          const float2 a2 = make_float2(__shfl_sync(0xffffffffu, my_val, j), 0.f);
-#pragma unroll
-          for (int u = 0; u < NV; ++u) {
-            if (!live[u]) continue;
-            const uint4 t = __ldg(reinterpret_cast<const uint4*>(zl + c * ldx32 + u * 256));
-            const __half2* h = reinterpret_cast<const __half2*>(&t);
-#pragma unroll
-            for (int k = 0; k < 4; ++k)
-              acc[u][k] = __ffma2_rn(make_float2(a2.x, a2.x), __half22float2(h[k]), acc[u][k]);
-          }
+          for (int k = 0; k < 4; ++k) acc[k] = __ffma2_rn(a2, __half22float2(h[k]), acc[k]);
         }
       }
-      if (blockIdx.y == 0) {
+      for (; j < m; ++j) {
+        const uint32_t c = (uint32_t)__shfl_sync(0xffffffffu, cc, j);
+        const float a = __shfl_sync(0xffffffffu, cv, j);
+        if (live[0]) {
+          const uint4 t = __ldg(reinterpret_cast<const uint4*>(zl + c * ldx32));
+          const __half2* h = reinterpret_cast<const __half2*>(&t);
 #pragma unroll
-        for (int o = 16; o; o >>= 1) ss = __fadd_ru(ss, __shfl_xor_sync(0xffffffffu, ss, o));
-        if (lane == 0) {
-          const double m = (double)(e1 - e0);
-          const double f = 0x1p-11 + 2.01 * m * 0x1p-24 + sqrt(m) * 0x1p-38;
-          cbound[i] = __double2float_ru(__dsqrt_ru((double)ss) * f * (1.0 + 0x1p-20));
+          for (int k = 0; k < 4; ++k) acc[k] = __ffma2_rn(make_float2(a, a), __half22float2(h[k]), acc[k]);
         }
+      }
+      cc = pc;
+      cv = pv;
+    }
+    if (blockIdx.y == 0 && i < n_rows) {
+#pragma unroll
+      for (int o = 16; o; o >>= 1) ss = __fadd_ru(ss, __shfl_xor_sync(0xffffffffu, ss, o));
+      if (lane == 0) {
+        const double m = (double)(e1 - e0);
+        const double f = 0x1p-11 + 2.01 * m * 0x1p-24 + sqrt(m) * 0x1p-38;
+        cbound[i] = __double2float_ru(__dsqrt_ru((double)ss) * f * (1.0 + 0x1p-20));
       }
     }
 #pragma unroll
-    for (int u = 0; u < NV; ++u)
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        tile[rr][lane * 8 + u * 256 + 2 * q] = acc[u][q].x;
-        tile[rr][lane * 8 + u * 256 + 2 * q + 1] = acc[u][q].y;
-      }
+    for (int q = 0; q < 4; ++q) {
+      tile[rr][lane * 8 + 2 * q] = acc[q].x;
+      tile[rr][lane * 8 + 2 * q + 1] = acc[q].y;
+    }
     int nr = 0;
     if (lane == 0) nr = atomicAdd(&next_row, 1);
     rr = __shfl_sync(0xffffffffu, nr, 0);
+    e0 = e1 = 0;
+    if (rr < ROWS && row0 + rr < n_rows) {
+      e0 = __ldg(indptr + row0 + rr);
+      e1 = __ldg(indptr + row0 + rr + 1);
+    }
+    cc = 0;
+    cv = 0.f;
+    if (rr < ROWS && lane < e1 - e0) {
+      cc = __ldg(indices + e0 + lane);
+      cv = __ldg(vals + e0 + lane);
+    }
   }
   __syncthreads();
   for (int c = warp; c < PW; c += 8) {
