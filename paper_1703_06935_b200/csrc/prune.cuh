@@ -85,6 +85,10 @@ __global__ void __launch_bounds__(256) zs_half_kernel(int64_t r, int64_t b, cons
   if (blockIdx.x == 0 && tx == 0 && ty == 0) *nflag = 0;
 }
 
+// 16-byte gather of an fp16 Zs row segment (read-only path; L1-allocating:
+// ld.global.nc.L1::no_allocate measured 10% slower, 16.0 vs 14.5 ms at C3).
+__device__ __forceinline__ uint4 ld_gather(const __half* p) { return __ldg(reinterpret_cast<const uint4*>(p)); }
+
 // K9h: Xt~ (ncols x n_rows, ld ldy) = (A Zh) .* inv_s over column panels of
 // Measured at C3 2%, b = 1024: NV = 1 (256-column
 // panels), DEPTH 8, 4 CTAs/SM (64 registers) 14.8 ms -- kept; DEPTH 4 at 4 /
@@ -165,7 +169,7 @@ __global__ void __launch_bounds__(256, MINB) spmm_T_half_kernel(int64_t n_rows, 
         uint4 raw[DEPTH];
 #pragma unroll
         for (int g = 0; g < DEPTH; ++g)
-          if (live[0]) raw[g] = __ldg(reinterpret_cast<const uint4*>(zl + c[g] * ldx32));
+          if (live[0]) raw[g] = ld_gather(zl + c[g] * ldx32);
 #pragma unroll
         for (int g = 0; g < DEPTH; ++g) {
           if (!live[0]) continue;
@@ -179,7 +183,7 @@ __global__ void __launch_bounds__(256, MINB) spmm_T_half_kernel(int64_t n_rows, 
         const uint32_t c = (uint32_t)__shfl_sync(0xffffffffu, cc, j);
         const float a = __shfl_sync(0xffffffffu, cv, j);
         if (live[0]) {
-          const uint4 t = __ldg(reinterpret_cast<const uint4*>(zl + c * ldx32));
+          const uint4 t = ld_gather(zl + c * ldx32);
           const __half2* h = reinterpret_cast<const __half2*>(&t);
 #pragma unroll
           for (int k = 0; k < 4; ++k) acc[k] = __ffma2_rn(make_float2(a, a), __half22float2(h[k]), acc[k]);
