@@ -96,7 +96,9 @@ __device__ __forceinline__ uint4 ld_gather(const __half* p) { return __ldg(reint
 // at 2 or 3 CTAs/SM 20.5 / 16.5; a barrier-free variant (warp-owned 8-row
 // items, persistent grid, per-warp transposes) 19.1-19.4.  FFMA2 on converted
 // half pairs and 32-bit row offsets (one IMAD.WIDE per gather) took it from
-// 18.7 to 16.8 ms on a synthetic U~.  Neither L2 (55%) nor issue (61%) is
+// 18.7 to 16.8 ms on a synthetic U~.  Landing the gathers in shared memory
+// instead (cp.async, a per-warp ring of 16-32 512-byte slots, 4-byte direct
+// output writes; up to 224 KB in flight per SM) measured 33-41 ms.  Neither L2 (55%) nor issue (61%) is
 // saturated (ncu, profiles/r01/k9h_ncu_full.json): the bytes in flight per SM
 // over the loaded L2 latency bound it.
 
