@@ -177,7 +177,7 @@ inline size_t align256(size_t x) { return (x + 255) / 256 * 256; }
 
 template <int NV, int DEPTH, int ROWS, int MINB>
 int launch_k9h(fsr_ctx* ctx, int64_t n, const int64_t* u_indptr, const int32_t* u_indices, const float* u_values,
-               int64_t b, const __half* Zh, const float2* qp, float* Xt, float* cb) {
+               int64_t b, const __half* Zh, const float2* qp, float* Xt, float* cb, int* cmax_bits) {
   namespace P = fsr::prune;
   const size_t smem = (size_t)ROWS * (256 * NV + 1) * 4;
   static bool configured = false;
@@ -188,7 +188,7 @@ int launch_k9h(fsr_ctx* ctx, int64_t n, const int64_t* u_indptr, const int32_t* 
   }
   dim3 grid((unsigned)fsr::ceil_div(n, ROWS), (unsigned)fsr::ceil_div(b, 256 * NV));
   P::spmm_T_half_kernel<NV, DEPTH, ROWS, MINB><<<grid, 256, smem, ctx->stream>>>(n, u_indptr, u_indices, u_values, b,
-                                                                                Zh, b, qp, Xt, n, cb);
+                                                                                Zh, b, qp, Xt, n, cb, cmax_bits);
   return fsr::launched(ctx, "spmm_T_half_kernel");
 }
 
@@ -213,7 +213,8 @@ int filter_pruned(fsr_ctx* ctx, int64_t n, int64_t r, const int64_t* u_indptr, c
   ws += align256((size_t)n * 4);
   int* nflag = (int*)ws;
   int* flags = nflag + 1;
-  ws += align256((size_t)(b + 1) * 4);
+  int* cmax_bits = nflag + b + 1;
+  ws += align256((size_t)(b + 2) * 4);
   int32_t* cand = (int32_t*)ws;
   ws += align256((size_t)b * P::kCap * 4);
   int32_t* ccount = (int32_t*)ws;
@@ -226,7 +227,7 @@ int filter_pruned(fsr_ctx* ctx, int64_t n, int64_t r, const int64_t* u_indptr, c
   }
   {
     fsr::StageTimer timer(ctx, FSR_STAGE_FILTER_SPMM);
-    FSR_TRY((launch_k9h<1, 8, 32, 4>(ctx, n, u_indptr, u_indices, u_values, b, Zh, qp, Xt, cb)));
+    FSR_TRY((launch_k9h<1, 8, 32, 4>(ctx, n, u_indptr, u_indices, u_values, b, Zh, qp, Xt, cb, cmax_bits)));
   }
   if (copy_uncovered && eta) {
     fsr::StageTimer timer(ctx, FSR_STAGE_COPY_UNCOVERED);
@@ -245,8 +246,8 @@ int filter_pruned(fsr_ctx* ctx, int64_t n, int64_t r, const int64_t* u_indptr, c
     }
     const int copy = copy_uncovered && eta;
     const int64_t grid = std::min<int64_t>(b, (int64_t)ctx->num_sms * per_sm);
-    P::prune_collect_kernel<<<(unsigned)grid, P::kThreads, 0, ctx->stream>>>(n, b, Xt, n, cb, qp, topk, cand, ccount,
-                                                                            nflag, flags);
+    P::prune_collect_kernel<<<(unsigned)grid, P::kThreads, 0, ctx->stream>>>(n, b, Xt, n, cb, cmax_bits, qp, topk,
+                                                                            cand, ccount, nflag, flags);
     FSR_TRY(fsr::launched(ctx, "prune_collect_kernel"));
     P::prune_finish_kernel<<<(unsigned)b, P::kThreads, 0, ctx->stream>>>(n, Xt, n, cb, qp, cand, ccount, u_indptr,
                                                                         u_indices, u_values, Zs, b, eta, copy, y_ptr,

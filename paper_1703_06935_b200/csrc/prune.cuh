@@ -40,7 +40,7 @@ constexpr int kCap = 1024;     // candidates held in shared memory (typical ~3K 
 
 // Per query column q of Zs (r x b, ld b): amax, ||zs_q||_2 and the scale
 // s_q = 2^(14 - e) with amax < 2^e (so |zs * s| < 2^14); Zh = half(Zs * s).
-// qp[q] = {1 / s_q, Zb_q}.  Also clears the fallback counter.
+// qp[q] = {1 / s_q, Zb_q}.  Also clears the fallback counter and max c_i.
 __global__ void __launch_bounds__(256) zs_half_kernel(int64_t r, int64_t b, const float* __restrict__ Zs,
                                                       __half* __restrict__ Zh, float2* __restrict__ qp,
                                                       int* __restrict__ nflag) {
@@ -82,7 +82,10 @@ __global__ void __launch_bounds__(256) zs_half_kernel(int64_t r, int64_t b, cons
   const float s = sscale[tx];
   if (col < b)
     for (int64_t j = ty; j < r; j += 8) Zh[j * b + col] = __float2half_rn(Zs[j * b + col] * s);
-  if (blockIdx.x == 0 && tx == 0 && ty == 0) *nflag = 0;
+  if (blockIdx.x == 0 && tx == 0 && ty == 0) {
+    nflag[0] = 0;
+    nflag[b + 1] = 0;  // max_i c_i (float bits), raised by K9h
+  }
 }
 
 // 16-byte gather of an fp16 Zs row segment (read-only path; L1-allocating:
@@ -112,14 +115,17 @@ __global__ void __launch_bounds__(256, MINB) spmm_T_half_kernel(int64_t n_rows, 
                                                           const float* __restrict__ vals, int64_t ncols,
                                                           const __half* __restrict__ Zh, int64_t ldx,
                                                           const float2* __restrict__ qp, float* __restrict__ Yt,
-                                                          int64_t ldy, float* __restrict__ cbound) {
+                                                          int64_t ldy, float* __restrict__ cbound,
+                                                          int* __restrict__ cmax_bits) {
   constexpr int PW = 256 * NV;
   extern __shared__ __align__(16) unsigned char dyn_tile[];
   float(*tile)[PW + 1] = reinterpret_cast<float(*)[PW + 1]>(dyn_tile);
   __shared__ int next_row;
+  __shared__ int cmax_s;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t row0 = (int64_t)blockIdx.x * ROWS;
   const int64_t p0 = (int64_t)blockIdx.y * PW;
+  if (threadIdx.x == 0) cmax_s = 0;
   const int64_t c0 = p0 + (int64_t)lane * 8;
   bool live[NV];
 #pragma unroll
@@ -200,7 +206,9 @@ __global__ void __launch_bounds__(256, MINB) spmm_T_half_kernel(int64_t n_rows, 
       if (lane == 0) {
         const double m = (double)(e1 - e0);
         const double f = 0x1p-11 + 2.01 * m * 0x1p-24 + sqrt(m) * 0x1p-38;
-        cbound[i] = __double2float_ru(__dsqrt_ru((double)ss) * f * (1.0 + 0x1p-20));
+        const float c = __double2float_ru(__dsqrt_ru((double)ss) * f * (1.0 + 0x1p-20));
+        cbound[i] = c;
+        atomicMax(&cmax_s, __float_as_int(c));  // c >= 0: int order == float order
       }
     }
 #pragma unroll
@@ -224,6 +232,7 @@ __global__ void __launch_bounds__(256, MINB) spmm_T_half_kernel(int64_t n_rows, 
     }
   }
   __syncthreads();
+  if (threadIdx.x == 0 && blockIdx.y == 0) atomicMax(cmax_bits, cmax_s);
   for (int c = warp; c < PW; c += 8) {
     const int64_t col = p0 + c;
 #pragma unroll
@@ -245,6 +254,37 @@ __device__ __forceinline__ uint32_t key32(float x) {
 
 __device__ __forceinline__ float key_to_float(uint64_t k) {
   return __uint_as_float((k & 0x80000000ull) ? (uint32_t)(k & 0x7fffffffull) : (uint32_t)~k);
+}
+
+// Visit (e, x[e]) for e in [0, m) (m < 2^31) with 16-byte loads, U vectors in
+// flight per thread, 32-bit indexing.
+template <int U, typename F>
+__device__ __forceinline__ void for_each_x32(const float* __restrict__ x, int m, F&& f) {
+  if (((uintptr_t)x & 15) != 0) {
+    for (int e = threadIdx.x; e < m; e += blockDim.x) f(e, x[e]);
+    return;
+  }
+  const float4* xv = reinterpret_cast<const float4*>(x);
+  const int mv = m / 4, step = blockDim.x * U;
+  for (int base = threadIdx.x; base < mv; base += step) {
+    float4 xa[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int i = base + u * blockDim.x;
+      if (i < mv) xa[u] = __ldg(xv + i);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int i = base + u * blockDim.x;
+      if (i < mv) {
+        f(4 * i, xa[u].x);
+        f(4 * i + 1, xa[u].y);
+        f(4 * i + 2, xa[u].z);
+        f(4 * i + 3, xa[u].w);
+      }
+    }
+  }
+  for (int e = mv * 4 + threadIdx.x; e < m; e += blockDim.x) f(e, x[e]);
 }
 
 // Visit (e, x[e], c[e]) for e in [0, m) (m < 2^31) with 16-byte loads of both
@@ -402,6 +442,7 @@ struct SelShared {
 
 __global__ void __launch_bounds__(kThreads) prune_collect_kernel(int64_t n, int64_t b, const float* __restrict__ Xt,
                                                                   int64_t ldx, const float* __restrict__ cb,
+                                                                  const int* __restrict__ cmax_bits,
                                                                   const float2* __restrict__ qp, int64_t K,
                                                                   int32_t* __restrict__ cand,
                                                                   int32_t* __restrict__ ccount,
@@ -479,9 +520,11 @@ __global__ void __launch_bounds__(kThreads) prune_collect_kernel(int64_t n, int6
     }
     __syncthreads();
     unsigned mine = 0;
-    for_each_xc32<4>(xr, cb, (int)n, [&](int e, float x, float c) {
-      if (x + c * zb >= tf_pre) {
-        const float bd = bound_of(c, zb);
+    // rows with x~ + max_i(c_i) Zb below the threshold cannot qualify: c_i is read only for the rest
+    const float cz_max = __int_as_float(*cmax_bits) * zb * (1.f + 0x1p-20f);
+    for_each_x32<8>(xr, (int)n, [&](int e, float x) {
+      if (x + cz_max >= tf_pre) {
+        const float bd = bound_of(__ldg(cb + e), zb);
         mine += key32(__fsub_rd(x, bd)) >= t_lo;
         if (key32(__fadd_ru(x, bd)) >= t_lo) {
           const unsigned slot = atomicAdd(&sh.count, 1u);
@@ -609,7 +652,7 @@ __global__ void __launch_bounds__(topk::kThreads) fallback_select_kernel(int64_t
 // Workspace of the pruned path beyond the unpruned one.
 inline size_t workspace_bytes(int64_t n, int64_t r, int64_t b) {
   auto al = [](size_t x) { return (x + 255) / 256 * 256; };
-  return al((size_t)r * b * 2) + al((size_t)b * 8) + al((size_t)n * 4) + al((size_t)(b + 1) * 4) +
+  return al((size_t)r * b * 2) + al((size_t)b * 8) + al((size_t)n * 4) + al((size_t)(b + 2) * 4) +
          al((size_t)b * kCap * 4) + al((size_t)b * 4);
 }
 
