@@ -48,6 +48,69 @@ class Config:
         return int(round(self.density * self.n * self.r))
 
 
+@dataclass(frozen=True)
+class RegionalConfig:
+    """BASELINE C4: ``images`` images x ``regions`` region descriptors (the
+    regions of one image = its centre + sigma noise), n = images * regions;
+    a query is a re-photographed database image: its ``regions`` regions
+    pooled into one observation vector (ranking.py:190-216)."""
+
+    name: str
+    seed: int
+    images: int
+    regions: int
+    d: int
+    sigma: float
+    k: int
+    gamma: float
+    r: int
+    p: int
+    q: int
+    density: float
+    queries: int
+    y_top: int
+    alpha: float = 0.99
+
+    @property
+    def n(self) -> int:
+        return self.images * self.regions
+
+    @property
+    def r_hat(self) -> int:
+        return min(self.r + self.p, self.n)
+
+    @property
+    def tau(self) -> int:
+        return int(round(self.density * self.n * self.r))
+
+
+# C4 at full size needs the 8-GPU sharded path (n x r_hat fp32 = 110 GB per block);
+# C4r is its generator at 4000 images (n = 20k) for parity against the reference.
+REGIONAL = {
+    "C4": RegionalConfig("C4", 4, 500_000, 5, 512, 0.05, 50, 3.0, 10_000, 1_000, 3, 0.02, 1_000, 50),
+    "C4r": RegionalConfig("C4r", 4, 4_000, 5, 512, 0.05, 50, 3.0, 400, 40, 3, 0.02, 30, 50),
+}
+
+
+def regional_descriptors(cfg: RegionalConfig):
+    """(data (n x d), query_regions (queries*regions x d), region_to_image, query_images)
+    as float64 arrays of fp32-rounded unit rows, from one default_rng(seed):
+    image centres, region noise, query images, query region noise."""
+    rng = np.random.default_rng(cfg.seed)
+    centres = rng.standard_normal((cfg.images, cfg.d))
+    centres /= np.linalg.norm(centres, axis=1, keepdims=True)
+    r2i = np.repeat(np.arange(cfg.images), cfg.regions)
+    x = centres[r2i] + cfg.sigma * rng.standard_normal((cfg.n, cfg.d))
+    qimg = rng.choice(cfg.images, size=cfg.queries, replace=False)
+    qx = centres[np.repeat(qimg, cfg.regions)] + cfg.sigma * rng.standard_normal((cfg.queries * cfg.regions, cfg.d))
+
+    def unit32(a):
+        a = a.astype(np.float32).astype(np.float64)
+        return a / np.linalg.norm(a, axis=1, keepdims=True)
+
+    return unit32(x), unit32(qx), r2i, qimg
+
+
 CONFIGS = {
     "C1": Config("C1", 1, 10_000, 128, 100, 0.1, None, 30, 3.0, 300, 50, 3, 0.10, 100, 30),
     "C2": Config("C2", 2, 100_000, 512, 1_000, 0.1, 1.1, 50, 3.0, 2_000, 200, 3, 0.05, 1_000, 50),

@@ -28,7 +28,7 @@ from specrank import graph, ranking, spectral  # noqa: E402
 from specrank.descriptors import DescriptorSet  # noqa: E402
 from specrank.sparsemat import SparseSymmetricMatrix  # noqa: E402
 
-from paper_1703_06935_b200.workloads import CONFIGS, cluster_descriptors  # noqa: E402
+from paper_1703_06935_b200.workloads import CONFIGS, REGIONAL, cluster_descriptors, regional_descriptors  # noqa: E402
 
 
 def support_hash(flat_sorted: np.ndarray) -> str:
@@ -248,6 +248,53 @@ def c2_reduced_case(n: int = 20_000, queries: int = 50, r: int = 400, p: int = 4
     )
 
 
+def c4_reduced_case(n_x: int = 5):
+    """C4's regional generator (images x 5 regions, sigma=0.05, d=512, k=50,
+    gamma=3, tau=2%) at 4000 images (n = 20k), r=400, p=40, q=3; queries pool
+    their 5 regions into one observation vector (cap 50); region scores are
+    also pooled to images (PoolingMatrix, RankingResult)."""
+    cfg = REGIONAL["C4r"]
+    t0 = time.perf_counter()
+    data, qx, r2i, qimg = regional_descriptors(cfg)
+    ds = DescriptorSet(data)
+    W = graph.build_mutual_knn_graph(ds, cfg.k, cfg.gamma)
+    S = graph.normalize_adjacency(W, graph.degrees(W))
+    t1 = time.perf_counter()
+    dec = spectral.decompose(S, cfg.r, p=cfg.p, q=cfg.q, seed=0)
+    sdec = spectral.sparsify(dec, cfg.tau)
+    h = ranking.h_alpha(cfg.alpha)
+    m = cfg.regions
+    ys = [ranking.observation_vector(qx[j * m:(j + 1) * m], ds, cfg.y_top, cfg.gamma, cap=cfg.y_top)
+          for j in range(cfg.queries)]
+    y_ptr = np.zeros(len(ys) + 1, dtype=np.int64)
+    y_ptr[1:] = np.cumsum([y.nnz for y in ys])
+    P = ranking.PoolingMatrix.from_region_map(r2i)
+    xa, xs, ta, ts, ia, isp = [], [], [], [], [], []
+    for j, y in enumerate(ys):
+        x = ranking.filter(dec, h, y)
+        x2 = ranking.filter(sdec, h, y)
+        ta.append(ranking.rank(x)[:100])
+        ts.append(ranking.rank(x2)[:100])
+        ia.append(ranking.RankingResult.from_scores(x, P).order[:100])
+        isp.append(ranking.RankingResult.from_scores(x2, P).order[:100])
+        if j < n_x:
+            xa.append(x)
+            xs.append(x2)
+    flat = csr_support(sdec.U)
+    print(f"C4r: graph {t1 - t0:.1f}s total {time.perf_counter() - t0:.1f}s nnz(W)={W.nnz}")
+    np.savez_compressed(
+        os.path.join(HERE, "c4r.npz"),
+        W_indptr=W.csr.indptr.astype(np.int64), W_indices=W.csr.indices.astype(np.int32),
+        W_data=W.csr.data, lam=dec.eigenvalues, eta=dec.eta, sparse_eta=sdec.eta,
+        sparse_nnz=np.array(sdec.U.nnz), sparse_hash=np.array(support_hash(flat)),
+        y_ptr=y_ptr, y_idx=np.concatenate([y.indices for y in ys]), y_val=np.concatenate([y.values for y in ys]),
+        x_approx=np.array(xa), x_sparse=np.array(xs),
+        top_approx=np.array(ta, dtype=np.int32), top_sparse=np.array(ts, dtype=np.int32),
+        img_top_approx=np.array(ia, dtype=np.int32), img_top_sparse=np.array(isp, dtype=np.int32),
+        query_images=qimg, params=np.array([cfg.n, cfg.r, cfg.p, cfg.q, cfg.tau, 0]), alpha=np.array(cfg.alpha),
+    )
+
+
 def block_graph(sizes, seed: int, density: float = 0.08):
     """Symmetric nonnegative adjacency whose components have the given sizes
     (each block connected: a random spanning path plus random edges), vertices
@@ -306,7 +353,7 @@ def blockwise_case():
 
 
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["gaussian", "kat", "c1", "epi", "blockwise", "c2r"]
+    which = sys.argv[1:] or ["gaussian", "kat", "c1", "epi", "blockwise", "c2r", "c4r"]
     if "gaussian" in which:
         gaussian_cases()
     if "kat" in which:
@@ -319,4 +366,6 @@ if __name__ == "__main__":
         blockwise_case()
     if "c2r" in which:
         c2_reduced_case()
+    if "c4r" in which:
+        c4_reduced_case()
     print("ok")

@@ -1,0 +1,95 @@
+"""End-to-end parity on a reduced C4 (BASELINE config 4, the regional
+variant): 4000 images x 5 region descriptors (centre + sigma=0.05 noise,
+d=512, n=20k), mutual kNN k=50, gamma=3, r=400, p=40, q=3, 2% sparsification;
+queries are re-photographed database images whose 5 regions are pooled into
+one observation vector (cap 50, ranking.py:190-216), and region scores are
+pooled to images (PoolingMatrix / RankingResult, ranking.py:398-411).
+Against the reference's own outputs (tests/golden/c4r.npz, make_golden.py):
+graph pattern exact and weights 1e-12; pooled observation vectors exact
+support, values 1e-12; Ritz 1e-10 (fp64) / 1e-5 (fp32) normwise; ranking
+vectors 1e-9 / 1e-4 relative L2; exact sparse support in fp64; region and
+image top-100 overlap >= 99% (mean).
+"""
+
+import hashlib
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from paper_1703_06935_b200 import graph, knn, ranking, spectral  # noqa: E402
+from paper_1703_06935_b200.sparsemat import SparseSymmetricMatrix  # noqa: E402
+from paper_1703_06935_b200.workloads import REGIONAL, regional_descriptors  # noqa: E402
+
+
+def rel_l2(a, b):
+    return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300)
+
+
+def overlap(a, b):
+    return len(set(np.asarray(a).tolist()) & set(np.asarray(b).tolist())) / len(b)
+
+
+@pytest.fixture(scope="module")
+def c4r(golden):
+    g = golden("c4r")
+    cfg = REGIONAL["C4r"]
+    data, qx, r2i, qimg = regional_descriptors(cfg)
+    np.testing.assert_array_equal(qimg, g["query_images"])
+    return g, cfg, data, qx, r2i
+
+
+def test_c4r_inputs_match_reference(c4r):
+    g, cfg, data, qx, _ = c4r
+    X = torch.as_tensor(data).cuda()
+    W = knn.mutual_knn_graph_device(X, cfg.k, cfg.gamma).csr
+    np.testing.assert_array_equal(W.indptr, g["W_indptr"])
+    np.testing.assert_array_equal(W.indices, g["W_indices"])
+    np.testing.assert_allclose(W.data, g["W_data"], rtol=1e-12, atol=0)
+    y_ptr, y_idx, y_val = knn.observation_batch_device(torch.as_tensor(qx).cuda(), X, cfg.y_top, cfg.gamma,
+                                                       cap=cfg.y_top, regions=cfg.regions)
+    np.testing.assert_array_equal(y_ptr, g["y_ptr"])
+    np.testing.assert_array_equal(y_idx, g["y_idx"])
+    np.testing.assert_allclose(y_val, g["y_val"], rtol=1e-12, atol=0)
+
+
+@pytest.fixture(scope="module", params=["float64", "float32"])
+def decs(request, c4r):
+    import scipy.sparse as sp
+
+    g, cfg, *_ = c4r
+    n = cfg.n
+    W = SparseSymmetricMatrix(sp.csr_matrix((g["W_data"], g["W_indices"], g["W_indptr"]), shape=(n, n)))
+    S = graph.normalize_adjacency(W, graph.degrees(W))
+    dec = spectral.decompose(S, cfg.r, p=cfg.p, q=cfg.q, seed=0, dtype=request.param)
+    return request.param, dec, spectral.sparsify(dec, cfg.tau)
+
+
+def test_c4r_ritz_and_ranking(c4r, decs):
+    g, cfg, _, _, r2i = c4r
+    dtype, dec, sdec = decs
+    err = np.abs(dec.eigenvalues - g["lam"]).max() / np.abs(g["lam"]).max()
+    assert err <= (1e-10 if dtype == "float64" else 1e-5), err
+    batch = ranking.QueryBatch(cfg.n, g["y_ptr"], g["y_idx"], g["y_val"])
+    h = ranking.h_alpha(float(g["alpha"]))
+    tol = 1e-9 if dtype == "float64" else 1e-4
+    P = ranking.PoolingMatrix.from_region_map(r2i)
+    for name, d in (("approx", dec), ("sparse", sdec)):
+        X = ranking.filter_batch(d, h, batch)
+        ref = g[f"x_{name}"]
+        if name == "approx" or dtype == "float64":
+            assert max(rel_l2(X[j], ref[j]) for j in range(ref.shape[0])) <= tol
+        ov = [overlap(ranking.rank(X[j])[:100], g[f"top_{name}"][j]) for j in range(batch.b)]
+        oi = [overlap(ranking.RankingResult.from_scores(X[j], P).order[:100], g[f"img_top_{name}"][j])
+              for j in range(batch.b)]
+        assert np.mean(ov) >= 0.99 and np.mean(oi) >= 0.99, (name, np.mean(ov), np.mean(oi))
+    if dtype == "float64":
+        coo = sdec.U.tocoo()
+        flat = np.sort(coo.row.astype(np.int64) * cfg.r + coo.col)
+        assert hashlib.sha256(flat.tobytes()).hexdigest() == str(g["sparse_hash"])
+        np.testing.assert_allclose(sdec.eta, g["sparse_eta"], rtol=1e-9, atol=1e-12)

@@ -188,3 +188,36 @@ def test_c2_reduced_oracle_matches_reference(golden):
     import hashlib
     flat = O.sparsify_support(U, tau)
     assert hashlib.sha256(flat.astype(np.int64).tobytes()).hexdigest() == str(g["sparse_hash"])
+
+
+def test_c4_reduced_oracle_matches_reference(golden):
+    """Regional C4r: pooled 5-region observation vectors, normalisation,
+    decomposition, sparse support and image pooling of the oracle against
+    the reference's outputs (tests/golden/c4r.npz)."""
+    import hashlib
+
+    from paper_1703_06935_b200.workloads import REGIONAL, regional_descriptors
+
+    g = golden("c4r")
+    cfg = REGIONAL["C4r"]
+    data, qx, r2i, qimg = regional_descriptors(cfg)
+    np.testing.assert_array_equal(qimg, g["query_images"])
+    m = cfg.regions
+    for j in (0, 7, cfg.queries - 1):
+        oi, ov = O.observation_vector(qx[j * m:(j + 1) * m], data, cfg.y_top, cfg.gamma, cap=cfg.y_top)
+        sl = slice(g["y_ptr"][j], g["y_ptr"][j + 1])
+        np.testing.assert_array_equal(oi, g["y_idx"][sl])
+        np.testing.assert_allclose(ov, g["y_val"][sl], rtol=1e-13, atol=0)
+    n = cfg.n
+    W = sp.csr_matrix((g["W_data"], g["W_indices"], g["W_indptr"]), shape=(n, n))
+    S = O.normalize_adjacency(W, O.degrees(W))
+    U, lam, eta = O.decompose(S, cfg.r, p=cfg.p, q=cfg.q, seed=0)
+    np.testing.assert_allclose(lam, g["lam"], rtol=0, atol=1e-12)
+    flat = O.sparsify_support(U, cfg.tau)
+    assert hashlib.sha256(flat.astype(np.int64).tobytes()).hexdigest() == str(g["sparse_hash"])
+    w = O.transfer_values(O.h_alpha(float(g["alpha"])), lam)
+    P = O.pooling_from_region_map(r2i)
+    sl = slice(g["y_ptr"][0], g["y_ptr"][1])
+    x = O.filter_scores(U, lam, eta, w, g["y_idx"][sl], g["y_val"][sl])
+    np.testing.assert_allclose(x, g["x_approx"][0], rtol=1e-8, atol=1e-12)
+    np.testing.assert_array_equal(O.rank(O.pool(P, x))[:100], g["img_top_approx"][0])
