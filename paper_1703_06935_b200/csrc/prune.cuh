@@ -130,27 +130,49 @@ __global__ void __launch_bounds__(256, MINB) spmm_T_half_kernel(int64_t n_rows, 
   bool live[NV];
 #pragma unroll
   for (int u = 0; u < NV; ++u) live[u] = c0 + u * 256 < ncols;
+  // Rows are handed out from a shared counter longest first (row lengths are
+  // skewed; handing out the short rows last keeps the warps' finishing times
+  // close -- the end-of-block barrier held 21% of the stall samples with the
+  // rows in index order).  Within a row the next 32 entries are in flight
+  // while the current 32 are summed.
+  static_assert(NV == 1, "row loop is written for one 256-column vector per lane");
+  static_assert(ROWS == 32, "one lane per row ranks the block's rows");
+  __shared__ int order_s[ROWS];
+  __shared__ int64_t start_s[ROWS];
+  __shared__ int len_s[ROWS];
+  if (warp == 0) {
+    const int64_t i = row0 + lane;
+    int64_t a = 0, z = 0;
+    if (i < n_rows) {
+      a = __ldg(indptr + i);
+      z = __ldg(indptr + i + 1);
+    }
+    const int len = (int)(z - a);
+    start_s[lane] = a;
+    len_s[lane] = len;
+    int rank = 0;
+#pragma unroll
+    for (int k = 0; k < 32; ++k) {
+      const int lk = __shfl_sync(0xffffffffu, len, k);
+      rank += (lk > len) || (lk == len && k < lane);
+    }
+    order_s[rank] = lane;
+  }
   if (threadIdx.x == 0) next_row = 8;
   __syncthreads();
   // per-lane base of its 8 columns; row offsets in 32 bits (Zh <= 4 GB): one IMAD.WIDE per gather
   const __half* zl = Zh + c0;
   const uint32_t ldx32 = (uint32_t)ldx;
-  // Rows are handed out from a shared counter (skewed row lengths); within a
-  // row the next 32 entries are in flight while the current 32 are summed.
-  static_assert(NV == 1, "row loop is written for one 256-column vector per lane");
-  int rr = warp;
-  int64_t e0 = 0, e1 = 0;
-  if (row0 + rr < n_rows) {
-    e0 = __ldg(indptr + row0 + rr);
-    e1 = __ldg(indptr + row0 + rr + 1);
-  }
+  int pos = warp;
+  int rr = order_s[pos];
+  int64_t e0 = start_s[rr], e1 = e0 + len_s[rr];
   int cc = 0;
   float cv = 0.f;
   if (lane < e1 - e0) {
     cc = __ldg(indices + e0 + lane);
     cv = __ldg(vals + e0 + lane);
   }
-  while (rr < ROWS) {
+  while (pos < ROWS) {
     const int64_t i = row0 + rr;
     float2 acc[4];
 #pragma unroll
@@ -218,15 +240,16 @@ __global__ void __launch_bounds__(256, MINB) spmm_T_half_kernel(int64_t n_rows, 
     }
     int nr = 0;
     if (lane == 0) nr = atomicAdd(&next_row, 1);
-    rr = __shfl_sync(0xffffffffu, nr, 0);
+    pos = __shfl_sync(0xffffffffu, nr, 0);
     e0 = e1 = 0;
-    if (rr < ROWS && row0 + rr < n_rows) {
-      e0 = __ldg(indptr + row0 + rr);
-      e1 = __ldg(indptr + row0 + rr + 1);
+    if (pos < ROWS) {
+      rr = order_s[pos];
+      e0 = start_s[rr];
+      e1 = e0 + len_s[rr];
     }
     cc = 0;
     cv = 0.f;
-    if (rr < ROWS && lane < e1 - e0) {
+    if (pos < ROWS && lane < e1 - e0) {
       cc = __ldg(indices + e0 + lane);
       cv = __ldg(vals + e0 + lane);
     }

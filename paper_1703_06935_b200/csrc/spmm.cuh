@@ -174,11 +174,27 @@ __global__ void __launch_bounds__(256) spmm_rowpanel_T_kernel(int64_t n_rows, co
   bool live[NV];
 #pragma unroll
   for (int u = 0; u < NV; ++u) live[u] = c0 + u * 32 * VEC < ncols;
+  // rows are handed out dynamically, longest first: U~'s row lengths are
+  // skewed (median 54, max > 2000 at C3), so a static 4-rows-per-warp split
+  // leaves warps idle, and short rows handed out last keep the warps'
+  // finishing times close (fewer idle warps at the end-of-block barrier)
+  static_assert(ROWS == 32, "one lane per row ranks the block's rows");
+  __shared__ int order_s[ROWS];
+  if (warp == 0) {
+    const int64_t i = row0 + lane;
+    const int64_t len = i < n_rows ? __ldg(indptr + i + 1) - __ldg(indptr + i) : 0;
+    int rank = 0;
+#pragma unroll
+    for (int k = 0; k < 32; ++k) {
+      const int64_t lk = __shfl_sync(0xffffffffu, len, k);
+      rank += (lk > len) || (lk == len && k < lane);
+    }
+    order_s[rank] = lane;
+  }
   if (threadIdx.x == 0) next_row = 8;
   __syncthreads();
-  // rows are handed out dynamically: U~'s row lengths are skewed (median 54,
-  // max > 2000 at C3), so a static 4-rows-per-warp split leaves warps idle
-  for (int rr = warp; rr < ROWS;) {
+  for (int pos = warp; pos < ROWS;) {
+    const int rr = order_s[pos];
     const int64_t i = row0 + rr;
     T acc[NV][VEC];
 #pragma unroll
@@ -194,7 +210,7 @@ __global__ void __launch_bounds__(256) spmm_rowpanel_T_kernel(int64_t n_rows, co
       for (int q = 0; q < VEC; ++q) tile[rr][lane * VEC + u * 32 * VEC + q] = acc[u][q];
     int nr = 0;
     if (lane == 0) nr = atomicAdd(&next_row, 1);
-    rr = __shfl_sync(0xffffffffu, nr, 0);
+    pos = __shfl_sync(0xffffffffu, nr, 0);
   }
   __syncthreads();
   for (int c = warp; c < PW; c += 8) {
