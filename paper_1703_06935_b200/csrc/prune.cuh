@@ -576,7 +576,7 @@ __global__ void __launch_bounds__(kThreads) prune_finish_kernel(
     int64_t K, int64_t* __restrict__ out_idx, float* __restrict__ out_val) {
   __shared__ uint64_t ckey[kCap];
   __shared__ int64_t cidx[kCap];
-  __shared__ unsigned n_keep;
+  __shared__ unsigned n_keep, n_next;
   const int64_t q = blockIdx.x;
   const int cnt = ccount[q];
   if (cnt < 0) return;  // flagged: the fallback kernels answer this query
@@ -609,10 +609,18 @@ __global__ void __launch_bounds__(kThreads) prune_finish_kernel(
   }
   __syncthreads();
   const unsigned keep = n_keep;
-  // 4. exact re-score (warp per row), sort, output
-  for (unsigned t = wid; t < keep; t += kThreads / 32) {
+  // 4. exact re-score (warp per row; rows handed out from a counter, their
+  //    lengths differ by 10x and more), sort, output
+  if (threadIdx.x == 0) n_next = kThreads / 32;
+  __syncthreads();
+  for (unsigned t = wid; t < keep;) {
     const float v = exact_score_warp(cidx[t], q, xr, indptr, indices, vals, Zs, ldz, eta, copy, y_ptr, y_idx);
-    if (lane == 0) ckey[t] = topk::order_key(v);
+    unsigned nt = 0;
+    if (lane == 0) {
+      ckey[t] = topk::order_key(v);
+      nt = atomicAdd(&n_next, 1u);
+    }
+    t = __shfl_sync(0xffffffffu, nt, 0);
   }
   __syncthreads();
   topk::bitonic_sort(ckey, cidx, (int)keep);
