@@ -93,22 +93,24 @@ __global__ void __launch_bounds__(256) zs_half_kernel(int64_t r, int64_t b, cons
 __device__ __forceinline__ uint4 ld_gather(const __half* p) { return __ldg(reinterpret_cast<const uint4*>(p)); }
 
 // K9h: Xt~ (ncols x n_rows, ld ldy) = (A Zh) .* inv_s over column panels of
-// Measured at C3 2%, b = 1024 (DESIGN.md section 4): NV = 1 (256-column
-// panels), DEPTH 8, 4 CTAs/SM (64 registers) 14.8 ms -- kept; DEPTH 4 at 4 /
-// 5 / 6 CTAs/SM 15.7 / 16.4 / 18.1; DEPTH 6 at 5 CTAs/SM 16.6; NV = 2 DEPTH 4
-// at 2 or 3 CTAs/SM 20.5 / 16.5; a barrier-free variant (warp-owned 8-row
-// items, persistent grid, per-warp transposes) 19.1-19.4.  FFMA2 on converted
-// half pairs and 32-bit row offsets (one IMAD.WIDE per gather) took it from
-// 18.7 to 16.8 ms on a synthetic U~.  Landing the gathers in shared memory
-// instead (cp.async, a per-warp ring of 16-32 512-byte slots, 4-byte direct
-// output writes; up to 224 KB in flight per SM) measured 33-41 ms.  Neither L2 (55%) nor issue (61%) is
-// saturated (ncu, profiles/r01/k9h_ncu_full.json): the bytes in flight per SM
-// over the loaded L2 latency bound it.
-
 // PW = 256 NV columns (8 halves = 16 bytes per lane per vector); the same
 // CTA layout as spmm_rowpanel_T_kernel (ROWS rows handed to 8 warps from a
-// shared counter, transposed tile in shared memory).  Panel 0 also writes the
-// row bound factor c_i.  Requires ncols % 8 == 0 and 16-byte aligned Zh rows.
+// shared counter, longest first; transposed tile in shared memory).  Panel 0
+// also writes the row bound factor c_i and raises max_i c_i.  Requires
+// ncols % 8 == 0 and 16-byte aligned Zh rows.
+// Measured at C3 2%, b = 1024 (DESIGN.md section 4): NV = 1 (256-column
+// panels), DEPTH 8, 4 CTAs/SM (64 registers) 14.8 ms, then 14.5 with the next
+// 32 entries prefetched and 13.7 with the rows handed out longest first --
+// kept; DEPTH 4 at 4 / 5 / 6 CTAs/SM 15.7 / 16.4 / 18.1; DEPTH 6 at 5 CTAs/SM
+// 16.6; NV = 2 DEPTH 4 at 2 or 3 CTAs/SM 20.5 / 16.5; a barrier-free variant
+// (warp-owned 8-row items, persistent grid, per-warp transposes) 19.1-19.4;
+// a one-row lookahead in the hand-out 16.5; gathers landing in shared memory
+// (cp.async, per-warp rings of 16-32 512-byte slots, up to 224 KB in flight
+// per SM, 4-byte direct output writes) 33-41.  FFMA2 on converted half pairs
+// and 32-bit row offsets (one IMAD.WIDE per gather) took it from 18.7 to 16.8
+// ms on a synthetic U~.  Neither L2 (62%) nor issue (68%) is saturated (ncu,
+// profiles/r01/k9h_ncu_full.json): the bytes in flight per SM over the loaded
+// L2 latency bound it.
 template <int NV, int DEPTH, int ROWS, int MINB>
 __global__ void __launch_bounds__(256, MINB) spmm_T_half_kernel(int64_t n_rows, const int64_t* __restrict__ indptr,
                                                           const int32_t* __restrict__ indices,
@@ -310,77 +312,6 @@ __device__ __forceinline__ void for_each_x32(const float* __restrict__ x, int m,
   for (int e = mv * 4 + threadIdx.x; e < m; e += blockDim.x) f(e, x[e]);
 }
 
-// Visit (e, x[e], c[e]) for e in [0, m) (m < 2^31) with 16-byte loads of both
-// arrays, U vectors in flight per thread, 32-bit indexing.
-template <int U, typename F>
-__device__ __forceinline__ void for_each_xc32(const float* __restrict__ x, const float* __restrict__ c, int m, F&& f) {
-  if ((((uintptr_t)x | (uintptr_t)c) & 15) != 0) {
-    for (int e = threadIdx.x; e < m; e += blockDim.x) f(e, x[e], __ldg(c + e));
-    return;
-  }
-  const float4* xv = reinterpret_cast<const float4*>(x);
-  const float4* cv = reinterpret_cast<const float4*>(c);
-  const int mv = m / 4, step = blockDim.x * U;
-  for (int base = threadIdx.x; base < mv; base += step) {
-    float4 xa[U], ca[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int i = base + u * blockDim.x;
-      if (i < mv) {
-        xa[u] = __ldg(xv + i);
-        ca[u] = __ldg(cv + i);
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int i = base + u * blockDim.x;
-      if (i < mv) {
-        f(4 * i, xa[u].x, ca[u].x);
-        f(4 * i + 1, xa[u].y, ca[u].y);
-        f(4 * i + 2, xa[u].z, ca[u].z);
-        f(4 * i + 3, xa[u].w, ca[u].w);
-      }
-    }
-  }
-  for (int e = mv * 4 + threadIdx.x; e < m; e += blockDim.x) f(e, x[e], __ldg(c + e));
-}
-
-// Visit (e, x[e], c[e]) for e in [0, m) with 16-byte loads of both arrays,
-// U vectors in flight per thread (scalar loads when either is misaligned).
-template <int U, typename F>
-__device__ __forceinline__ void for_each_xc(const float* __restrict__ x, const float* __restrict__ c, int64_t m,
-                                            F&& f) {
-  if ((((uintptr_t)x | (uintptr_t)c) & 15) != 0) {
-    for (int64_t e = threadIdx.x; e < m; e += blockDim.x) f(e, x[e], __ldg(c + e));
-    return;
-  }
-  const float4* xv = reinterpret_cast<const float4*>(x);
-  const float4* cv = reinterpret_cast<const float4*>(c);
-  const int64_t mv = m / 4, step = (int64_t)blockDim.x * U;
-  for (int64_t base = threadIdx.x; base < mv; base += step) {
-    float4 xa[U], ca[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int64_t i = base + (int64_t)u * blockDim.x;
-      if (i < mv) {
-        xa[u] = __ldg(xv + i);
-        ca[u] = __ldg(cv + i);
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int64_t i = base + (int64_t)u * blockDim.x;
-      if (i < mv) {
-        f(4 * i, xa[u].x, ca[u].x);
-        f(4 * i + 1, xa[u].y, ca[u].y);
-        f(4 * i + 2, xa[u].z, ca[u].z);
-        f(4 * i + 3, xa[u].w, ca[u].w);
-      }
-    }
-  }
-  for (int64_t e = mv * 4 + threadIdx.x; e < m; e += blockDim.x) f(e, x[e], __ldg(c + e));
-}
-
 // The exact fp32 score of row i for query q, in the unpruned K9's order
 // (sequential FMAs over the row's entries from 0), computed by one warp
 // (lanes load and gather, the chain runs on broadcast values), or the stored
@@ -453,7 +384,7 @@ __device__ __forceinline__ float exact_score(int64_t i, int64_t q, const float* 
 // prune_finish_kernel -- one CTA per query:
 //  3. lambda_K = K-th largest lower among the candidates (they hold every
 //     row with lower >= t), keep upper >= lambda_K;
-//  4. exact re-score of those (warp per row), bitonic sort, top K out.
+//  4. exact re-score of those (warp per row, from a counter), bitonic sort, top K out.
 struct SelShared {
   unsigned int hist[1 << topk::kHistBits];
   unsigned int count;
