@@ -175,20 +175,19 @@ int launch_project(fsr_ctx* ctx, int64_t r, int64_t b, int u_sparse, const int64
 
 inline size_t align256(size_t x) { return (x + 255) / 256 * 256; }
 
-template <int NV, int DEPTH, int ROWS, int MINB>
+template <int NV, int DEPTH, int ROWS, int MINB, int WARPS = 8>
 int launch_k9h(fsr_ctx* ctx, int64_t n, const int64_t* u_indptr, const int32_t* u_indices, const float* u_values,
                int64_t b, const __half* Zh, const float2* qp, float* Xt, float* cb, int* cmax_bits) {
   namespace P = fsr::prune;
+  auto kern = P::spmm_T_half_kernel<NV, DEPTH, ROWS, MINB, WARPS>;
   const size_t smem = (size_t)ROWS * (256 * NV + 1) * 4;
   static bool configured = false;
   if (!configured) {
-    FSR_CUDA(ctx, cudaFuncSetAttribute(P::spmm_T_half_kernel<NV, DEPTH, ROWS, MINB>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    FSR_CUDA(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     configured = true;
   }
   dim3 grid((unsigned)fsr::ceil_div(n, ROWS), (unsigned)fsr::ceil_div(b, 256 * NV));
-  P::spmm_T_half_kernel<NV, DEPTH, ROWS, MINB><<<grid, 256, smem, ctx->stream>>>(n, u_indptr, u_indices, u_values, b,
-                                                                                Zh, b, qp, Xt, n, cb, cmax_bits);
+  kern<<<grid, 32 * WARPS, smem, ctx->stream>>>(n, u_indptr, u_indices, u_values, b, Zh, b, qp, Xt, n, cb, cmax_bits);
   return fsr::launched(ctx, "spmm_T_half_kernel");
 }
 

@@ -110,9 +110,10 @@ __device__ __forceinline__ uint4 ld_gather(const __half* p) { return __ldg(reint
 // and 32-bit row offsets (one IMAD.WIDE per gather) took it from 18.7 to 16.8
 // ms on a synthetic U~.  Neither L2 (62%) nor issue (68%) is saturated (ncu,
 // profiles/r01/k9h_ncu_full.json): the bytes in flight per SM over the loaded
-// L2 latency bound it.
-template <int NV, int DEPTH, int ROWS, int MINB>
-__global__ void __launch_bounds__(256, MINB) spmm_T_half_kernel(int64_t n_rows, const int64_t* __restrict__ indptr,
+// L2 latency bound it.  64-row blocks (8 or 16 warps) and 4-warp blocks at 6
+// CTAs/SM measured 14.7-15.0 ms.
+template <int NV, int DEPTH, int ROWS, int MINB, int WARPS = 8>
+__global__ void __launch_bounds__(32 * WARPS, MINB) spmm_T_half_kernel(int64_t n_rows, const int64_t* __restrict__ indptr,
                                                           const int32_t* __restrict__ indices,
                                                           const float* __restrict__ vals, int64_t ncols,
                                                           const __half* __restrict__ Zh, int64_t ldx,
@@ -138,29 +139,41 @@ __global__ void __launch_bounds__(256, MINB) spmm_T_half_kernel(int64_t n_rows, 
   // rows in index order).  Within a row the next 32 entries are in flight
   // while the current 32 are summed.
   static_assert(NV == 1, "row loop is written for one 256-column vector per lane");
-  static_assert(ROWS == 32, "one lane per row ranks the block's rows");
+  static_assert(ROWS % 32 == 0 && ROWS <= 128, "lanes of warp 0 rank the block's rows, ROWS / 32 each");
+  constexpr int RPL = ROWS / 32;
   __shared__ int order_s[ROWS];
   __shared__ int64_t start_s[ROWS];
   __shared__ int len_s[ROWS];
   if (warp == 0) {
-    const int64_t i = row0 + lane;
-    int64_t a = 0, z = 0;
-    if (i < n_rows) {
-      a = __ldg(indptr + i);
-      z = __ldg(indptr + i + 1);
-    }
-    const int len = (int)(z - a);
-    start_s[lane] = a;
-    len_s[lane] = len;
-    int rank = 0;
+    int len[RPL];
 #pragma unroll
-    for (int k = 0; k < 32; ++k) {
-      const int lk = __shfl_sync(0xffffffffu, len, k);
-      rank += (lk > len) || (lk == len && k < lane);
+    for (int h = 0; h < RPL; ++h) {
+      const int64_t i = row0 + h * 32 + lane;
+      int64_t a = 0, z = 0;
+      if (i < n_rows) {
+        a = __ldg(indptr + i);
+        z = __ldg(indptr + i + 1);
+      }
+      len[h] = (int)(z - a);
+      start_s[h * 32 + lane] = a;
+      len_s[h * 32 + lane] = len[h];
     }
-    order_s[rank] = lane;
+    int rank[RPL];
+#pragma unroll
+    for (int h = 0; h < RPL; ++h) rank[h] = 0;
+#pragma unroll
+    for (int g = 0; g < RPL; ++g)
+#pragma unroll 8
+      for (int k = 0; k < 32; ++k) {
+        const int lk = __shfl_sync(0xffffffffu, len[g], k);
+#pragma unroll
+        for (int h = 0; h < RPL; ++h)
+          rank[h] += (lk > len[h]) || (lk == len[h] && g * 32 + k < h * 32 + lane);
+      }
+#pragma unroll
+    for (int h = 0; h < RPL; ++h) order_s[rank[h]] = h * 32 + lane;
   }
-  if (threadIdx.x == 0) next_row = 8;
+  if (threadIdx.x == 0) next_row = WARPS;
   __syncthreads();
   // per-lane base of its 8 columns; row offsets in 32 bits (Zh <= 4 GB): one IMAD.WIDE per gather
   const __half* zl = Zh + c0;
@@ -258,7 +271,7 @@ __global__ void __launch_bounds__(256, MINB) spmm_T_half_kernel(int64_t n_rows, 
   }
   __syncthreads();
   if (threadIdx.x == 0 && blockIdx.y == 0) atomicMax(cmax_bits, cmax_s);
-  for (int c = warp; c < PW; c += 8) {
+  for (int c = warp; c < PW; c += WARPS) {
     const int64_t col = p0 + c;
 #pragma unroll
     for (int h = 0; h < ROWS / 32; ++h) {
