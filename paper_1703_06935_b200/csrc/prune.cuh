@@ -35,6 +35,7 @@
 namespace fsr {
 namespace prune {
 
+constexpr int kExactRows = 1 << 30;  // flag bit: the query's x~ row is exact (z = 0), no recompute
 constexpr int kThreads = 256;  // prune_select_kernel: several CTAs per SM overlap their serial phases
 constexpr int kCap = 1024;     // candidates held in shared memory (typical ~3K + band); more -> fallback
 
@@ -423,6 +424,13 @@ __global__ void __launch_bounds__(kThreads) prune_collect_kernel(int64_t n, int6
   for (int64_t q = blockIdx.x; q < b; q += gridDim.x) {
     const float* xr = Xt + q * ldx;
     const float zb = qp[q].y;
+    if (zb == 0.f) {  // z = 0 (empty observation): x~ is exact (zeros and copied y); exact select only
+      if (!threadIdx.x) {
+        ccount[q] = -1;
+        flags[atomicAdd(nflag, 1)] = (int)q | kExactRows;
+      }
+      continue;
+    }
     const bool vec_ok = ((((uintptr_t)xr) | ((uintptr_t)cb)) & 15) == 0;
     int32_t* cq = cand + q * kCap;
     // 1. sampled threshold on the lower keys
@@ -592,7 +600,9 @@ __global__ void __launch_bounds__(256) fallback_rows_kernel(int64_t n, float* __
   if (!nf) return;
   const int64_t nblk = (n + 255) / 256;
   for (int64_t item = blockIdx.x; item < nf * nblk; item += gridDim.x) {
-    const int64_t q = flags[item / nblk];
+    const int f = flags[item / nblk];
+    if (f & kExactRows) continue;  // x~ is already exact for this query
+    const int64_t q = f;
     const int64_t i = (item % nblk) * 256 + threadIdx.x;
     if (i < n) {
       float* xr = Xt + q * ldx;
@@ -613,7 +623,7 @@ __global__ void __launch_bounds__(topk::kThreads) fallback_select_kernel(int64_t
   uint64_t* ckey = (uint64_t*)dyn;
   int64_t* cidx = (int64_t*)(ckey + topk::kCap);
   __shared__ topk::Shared sh;
-  const int64_t q = flags[blockIdx.x];
+  const int64_t q = flags[blockIdx.x] & ~kExactRows;
   topk::Range<float, false> R{Xt + q * ldx, nullptr, n, 0};
   topk::select_exact<float, false>(R, K, sh, ckey, cidx);
   __syncthreads();
