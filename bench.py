@@ -655,7 +655,25 @@ def run_fsr(args, cfg, n, rank, world, local_rank):
             torch.cuda.synchronize()
             ctx.set_topk_prune(True)
             same &= bool(torch.equal(pi, res.top_idx) and torch.equal(pv.view(torch.int32), res.top_val.view(torch.int32)))
-        prune_check = {"batches": len(dqs), "topk_identical_to_unpruned_fp32": same, "fallback_queries": fallback}
+        # the same timed protocol on the unpruned fp32 path, for reference
+        ctx.set_topk_prune(False)
+        for i in range(args.warmup):
+            step(i)
+        torch.cuda.synchronize()
+        ums = 0.0
+        for i in range(args.steps):
+            flush()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            step(i)
+            e1.record()
+            torch.cuda.synchronize()
+            ums += e0.elapsed_time(e1)
+        ctx.set_topk_prune(True)
+        ums = max_over_ranks(ums, world)
+        prune_check = {"batches": len(dqs), "topk_identical_to_unpruned_fp32": same, "fallback_queries": fallback,
+                       "unpruned_fp32": {"value": world * b * args.steps / (ums / 1e3), "unit": "queries/s",
+                                         "ms_per_step": ums / args.steps}}
     k9_gather_gbs = k9_gather / (k9_ms_launch * 1e-3) / 1e9
     l2 = load_profile("l2_bw.json") or {}
     l2_peak = l2.get("gather_1KB_rows_19MB_GBs")
