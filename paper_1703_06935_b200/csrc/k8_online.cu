@@ -386,3 +386,4 @@ int fsr_project_batch(fsr_ctx* ctx, int dtype, int64_t n, int64_t r, int u_spars
 
 }  // extern "C"
 
+

@@ -29,6 +29,7 @@
 
 #include <cuda_fp16.h>
 
+
 #include "spmm.cuh"
 #include "topk.cuh"
 
@@ -347,24 +348,39 @@ __device__ __forceinline__ float exact_score_warp(int64_t i, int64_t q, const fl
     for (int64_t t = y_ptr[q] + lane; t < y_ptr[q + 1]; t += 32) hit |= y_idx[t] == i;
     if (__any_sync(0xffffffffu, hit)) return xt_row[i];
   }
+  // R entries per lane per round: all loads of a round in flight together
+  // (R = 8 / 16 measured no faster: the rounds are bound by the dependent
+  // DRAM latencies indptr -> entries -> Zs of the candidate's row)
+  constexpr int R = 4;
   float acc = 0.f;
-  for (int64_t base = e0; base < e1; base += 128) {
-    const int m = e1 - base < 128 ? (int)(e1 - base) : 128;
-    float a[4], z[4];
-    int c[4];
+  for (int64_t base = e0; base < e1; base += 32 * R) {
+    const int m = e1 - base < 32 * R ? (int)(e1 - base) : 32 * R;
+    float a[R], z[R];
+    int c[R];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
+    for (int k = 0; k < R; ++k) {
       const int t = k * 32 + lane;
       c[k] = t < m ? __ldg(indices + base + t) : 0;
       a[k] = t < m ? __ldg(vals + base + t) : 0.f;
     }
 #pragma unroll
-    for (int k = 0; k < 4; ++k) z[k] = k * 32 + lane < m ? __ldg(Zs + (int64_t)c[k] * ldz + q) : 0.f;
+    for (int k = 0; k < R; ++k) z[k] = k * 32 + lane < m ? __ldg(Zs + (int64_t)c[k] * ldz + q) : 0.f;
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
+    for (int k = 0; k < R; ++k) {
       const int mk = m - k * 32 < 32 ? m - k * 32 : 32;
-      for (int e = 0; e < mk; ++e)
-        acc = fmaf(__shfl_sync(0xffffffffu, a[k], e), __shfl_sync(0xffffffffu, z[k], e), acc);
+      int e = 0;
+      // groups of 8: the 16 shuffles are issued ahead of the dependent FMA chain
+      for (; e + 8 <= mk; e += 8) {
+        float av[8], zv[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          av[u] = __shfl_sync(0xffffffffu, a[k], e + u);
+          zv[u] = __shfl_sync(0xffffffffu, z[k], e + u);
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) acc = fmaf(av[u], zv[u], acc);
+      }
+      for (; e < mk; ++e) acc = fmaf(__shfl_sync(0xffffffffu, a[k], e), __shfl_sync(0xffffffffu, z[k], e), acc);
     }
   }
   return acc;
