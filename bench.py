@@ -59,6 +59,8 @@ def parse_args():
     ap.add_argument("--skip-e2e", action="store_true")
     ap.add_argument("--no-sweep", action="store_true", help="skip the C5 online sweep")
     ap.add_argument("--no-parity", action="store_true", help="skip the full-size parity checks")
+    ap.add_argument("--no-offline-warmup", action="store_true",
+                    help="time the offline decomposition on its first (cold) run")
     ap.add_argument("--cpu-procs", type=int, default=64, help="processes for the CPU oracle arms (capped at nproc)")
     return ap.parse_args()
 
@@ -537,7 +539,23 @@ def run_fsr(args, cfg, n, rank, world, local_rank):
     all_queries = ranking.QueryBatch(n, y_ptr, y_idx, y_val)
     ctx = N.Context.get(device)
 
-    # ---------------- offline: SI + Rayleigh-Ritz + sparsify (timed once) ----
+    # ---------------- offline: SI + Rayleigh-Ritz + sparsify ------------------
+    # One untimed pass first: it sizes libfsr's scratch arena and torch's
+    # allocator pools (multi-GB first-touch cudaMalloc/cudaFree inside the
+    # dense stages made single-shot timings swing by up to 2x), then the timed pass.
+    if not args.no_offline_warmup:
+        if world == 1:
+            _b = spectral.range_finder(S, r_hat, q, 0, dtype=dt, device=device,
+                                       _orthonormal_last=not spectral.fused_rr_enabled(dt))
+            _d = spectral.approx_eigendecomposition(S, _b, r)
+            del _b
+            _s = spectral.sparsify(_d, tau)
+            del _d, _s
+        else:
+            _s = sharded_offline(S, r, r_hat, q, tau, dt, device,
+                                 [torch.cuda.Event(enable_timing=True) for _ in range(4)])
+            del _s
+        torch.cuda.synchronize()
     ctx.enable_timing(True)
     ctx.stage_reset()
     off_clocks = ClockSampler(local_rank)
@@ -588,6 +606,8 @@ def run_fsr(args, cfg, n, rank, world, local_rank):
         "stage_ms": {k: round(v[0], 3) for k, v in stages.items() if v[1]},
         "nnz_W": nnz_w, "isolated_vertices": isolated, "kept_nnz": sdec.U_device.nnz, "inputs_build_s": t_inputs,
         "clocks": off_clk,
+        "timed_run": "second of two identical runs (the first sizes allocations)" if not args.no_offline_warmup
+                     else "first run",
     }
 
     # ---------------- online: device-resident batches ------------------------
