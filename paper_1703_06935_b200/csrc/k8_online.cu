@@ -75,7 +75,9 @@ __global__ void __launch_bounds__(256) project_smem_kernel(int64_t r, int64_t b,
                                                            const int64_t* __restrict__ y_ptr,
                                                            const int64_t* __restrict__ y_idx,
                                                            const T* __restrict__ y_val, T* __restrict__ Zt,
-                                                           T* __restrict__ Zs) {
+                                                           T* __restrict__ Zs, __half* __restrict__ Zh = nullptr,
+                                                           float2* __restrict__ qp = nullptr,
+                                                           int* __restrict__ nflag = nullptr) {
   extern __shared__ __align__(16) unsigned char dyn[];
   T* z = (T*)dyn;
   T* ev = (T*)(dyn + ((r * sizeof(T) + 15) / 16) * 16);
@@ -129,10 +131,53 @@ __global__ void __launch_bounds__(256) project_smem_kernel(int64_t r, int64_t b,
       __syncthreads();
     }
   }
+  float amax = 0.f;
+  double ss = 0.0;
   for (int64_t c = threadIdx.x; c < r; c += blockDim.x) {
     const T s = w ? w[c] * z[c] : z[c];
     Zt[j * r + c] = s;
     if (Zs) Zs[c * b + j] = s;
+    if (Zh) {
+      z[c] = s;
+      amax = fmaxf(amax, fabsf((float)s));
+      ss = fma((double)s, (double)s, ss);
+    }
+  }
+  if constexpr (std::is_same<T, float>::value) {
+    // fp16 copy of column j of Zs for the pruned path (prune.cuh zs_half_kernel, fused)
+    if (Zh) {
+      __shared__ float red_a[8];
+      __shared__ double red_s[8];
+      __shared__ float sc_s;
+      const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+        ss += __shfl_xor_sync(0xffffffffu, ss, o);
+      }
+      if (lane == 0) {
+        red_a[wid] = amax;
+        red_s[wid] = ss;
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        for (int k = 1; k < (int)(blockDim.x >> 5); ++k) {
+          amax = fmaxf(amax, red_a[k]);
+          ss += red_s[k];
+        }
+        float sc = 1.f, inv = 1.f, zb = 0.f;
+        fsr::prune::query_scale(amax, ss, &sc, &inv, &zb);
+        sc_s = sc;
+        qp[j] = make_float2(inv, zb);
+        if (j == 0) {
+          nflag[0] = 0;
+          nflag[b + 1] = 0;
+        }
+      }
+      __syncthreads();
+      const float sc = sc_s;
+      for (int64_t c = threadIdx.x; c < r; c += blockDim.x) Zh[c * b + j] = __float2half_rn(z[c] * sc);
+    }
   }
 }
 
@@ -152,9 +197,11 @@ __global__ void copy_uncovered_kernel(int64_t n, const int64_t* __restrict__ y_p
 template <typename T>
 int launch_project(fsr_ctx* ctx, int64_t r, int64_t b, int u_sparse, const int64_t* u_indptr,
                    const int32_t* u_indices, const T* u_values, const T* u_dense, int64_t ldu, const T* w,
-                   const int64_t* y_ptr, const int64_t* y_idx, const T* y_val, T* Zt, T* Zs) {
+                   const int64_t* y_ptr, const int64_t* y_idx, const T* y_val, T* Zt, T* Zs,
+                   __half* Zh = nullptr, float2* qp = nullptr, int* nflag = nullptr, bool* fused = nullptr) {
   fsr::StageTimer timer(ctx, FSR_STAGE_PROJECT);
   const size_t psmem = ((size_t)r * sizeof(T) + 15) / 16 * 16 + (size_t)kProjCap * (sizeof(T) + 4);
+  if (fused) *fused = u_sparse && psmem <= 160 * 1024;
   if (u_sparse && psmem <= 160 * 1024) {
     static size_t configured[2] = {0, 0};
     if (configured[sizeof(T) == 8] < psmem) {
@@ -163,7 +210,7 @@ int launch_project(fsr_ctx* ctx, int64_t r, int64_t b, int u_sparse, const int64
       configured[sizeof(T) == 8] = psmem;
     }
     project_smem_kernel<T><<<(unsigned)b, 256, psmem, ctx->stream>>>(r, b, u_indptr, u_indices, u_values, w, y_ptr,
-                                                                     y_idx, y_val, Zt, Zs);
+                                                                     y_idx, y_val, Zt, Zs, Zh, qp, nflag);
   } else if (u_sparse)
     project_kernel<T, true><<<(unsigned)b, 256, 0, ctx->stream>>>(r, b, u_indptr, u_indices, u_values, nullptr, 0, w,
                                                                   y_ptr, y_idx, y_val, Zt, Zs);
@@ -217,9 +264,10 @@ int filter_pruned(fsr_ctx* ctx, int64_t n, int64_t r, const int64_t* u_indptr, c
   int32_t* cand = (int32_t*)ws;
   ws += align256((size_t)b * P::kCap * 4);
   int32_t* ccount = (int32_t*)ws;
+  bool fused = false;
   FSR_TRY(launch_project<float>(ctx, r, b, 1, u_indptr, u_indices, u_values, nullptr, 0, w, y_ptr, y_idx, y_val, Zt,
-                                Zs));
-  {
+                                Zs, Zh, qp, nflag, &fused));
+  if (!fused) {
     fsr::StageTimer timer(ctx, FSR_STAGE_PROJECT);
     P::zs_half_kernel<<<(unsigned)fsr::ceil_div(b, 32), dim3(32, 8), 0, ctx->stream>>>(r, b, Zs, Zh, qp, nflag);
     FSR_TRY(fsr::launched(ctx, "zs_half_kernel"));

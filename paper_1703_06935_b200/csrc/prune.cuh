@@ -40,6 +40,24 @@ constexpr int kExactRows = 1 << 30;  // flag bit: the query's x~ row is exact (z
 constexpr int kThreads = 256;  // prune_select_kernel: several CTAs per SM overlap their serial phases
 constexpr int kCap = 1024;     // candidates held in shared memory (typical ~3K + band); more -> fallback
 
+// Scale of one query column from its max |zs| and sum of squares:
+// s = 2^(14 - e) with amax < 2^e, 1/s, and Zb = max(||zs||_2 rounded up, 2^13 / s);
+// an all-zero column keeps s = 1 and Zb = 0 (its x~ is exact).
+__device__ __forceinline__ void query_scale(float amax, double ss, float* s, float* inv, float* zb) {
+  *s = 1.f;
+  *inv = 1.f;
+  *zb = 0.f;
+  if (amax > 0.f) {
+    int e;
+    frexpf(amax, &e);  // amax = f 2^e, f in [0.5, 1)
+    const int k = max(-120, min(120, 14 - e));
+    *s = ldexpf(1.f, k);
+    *inv = ldexpf(1.f, -k);
+    const float zn = __double2float_ru(__dsqrt_ru(ss) * (1.0 + 0x1p-40));
+    *zb = fmaxf(zn, ldexpf(1.f, 13 - k));
+  }
+}
+
 // Per query column q of Zs (r x b, ld b): amax, ||zs_q||_2 and the scale
 // s_q = 2^(14 - e) with amax < 2^e (so |zs * s| < 2^14); Zh = half(Zs * s).
 // qp[q] = {1 / s_q, Zb_q}.  Also clears the fallback counter and max c_i.
@@ -68,15 +86,7 @@ __global__ void __launch_bounds__(256) zs_half_kernel(int64_t r, int64_t b, cons
       ss += sss[k][tx];
     }
     float s = 1.f, inv = 1.f, zb = 0.f;
-    if (amax > 0.f) {
-      int e;
-      frexpf(amax, &e);  // amax = f 2^e, f in [0.5, 1)
-      const int k = max(-120, min(120, 14 - e));
-      s = ldexpf(1.f, k);
-      inv = ldexpf(1.f, -k);
-      const float zn = __double2float_ru(__dsqrt_ru(ss) * (1.0 + 0x1p-40));
-      zb = fmaxf(zn, ldexpf(1.f, 13 - k));
-    }
+    query_scale(amax, ss, &s, &inv, &zb);
     sscale[tx] = s;
     if (col < b) qp[col] = make_float2(inv, zb);
   }
