@@ -264,6 +264,10 @@ int filter_pruned(fsr_ctx* ctx, int64_t n, int64_t r, const int64_t* u_indptr, c
   int32_t* cand = (int32_t*)ws;
   ws += align256((size_t)b * P::kCap * 4);
   int32_t* ccount = (int32_t*)ws;
+  ws += align256((size_t)b * 4);
+  uint32_t* thr = (uint32_t*)ws;
+  ws += align256((size_t)b * 4);
+  unsigned* nlow = (unsigned*)ws;
   bool fused = false;
   FSR_TRY(launch_project<float>(ctx, r, b, 1, u_indptr, u_indices, u_values, nullptr, 0, w, y_ptr, y_idx, y_val, Zt,
                                 Zs, Zh, qp, nflag, &fused));
@@ -288,17 +292,24 @@ int filter_pruned(fsr_ctx* ctx, int64_t n, int64_t r, const int64_t* u_indptr, c
     if (!per_sm) {
       FSR_CUDA(ctx, cudaFuncSetAttribute(P::fallback_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)fsmem));
-      FSR_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, P::prune_collect_kernel, P::kThreads, 0));
+      FSR_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, P::prune_threshold_kernel, P::kThreads, 0));
       per_sm = std::max(per_sm, 1);
     }
     const int copy = copy_uncovered && eta;
     const int64_t grid = std::min<int64_t>(b, (int64_t)ctx->num_sms * per_sm);
-    P::prune_collect_kernel<<<(unsigned)grid, P::kThreads, 0, ctx->stream>>>(n, b, Xt, n, cb, cmax_bits, qp, topk,
-                                                                            cand, ccount, nflag, flags);
-    FSR_TRY(fsr::launched(ctx, "prune_collect_kernel"));
-    P::prune_finish_kernel<<<(unsigned)b, P::kThreads, 0, ctx->stream>>>(n, Xt, n, cb, qp, cand, ccount, u_indptr,
-                                                                        u_indices, u_values, Zs, b, eta, copy, y_ptr,
-                                                                        y_idx, topk, top_idx, top_val);
+    P::prune_threshold_kernel<<<(unsigned)grid, P::kThreads, 0, ctx->stream>>>(n, b, Xt, n, cb, qp, topk, thr, ccount,
+                                                                              nlow, nflag, flags);
+    FSR_TRY(fsr::launched(ctx, "prune_threshold_kernel"));
+    // segments of the streaming pass: enough CTAs to keep every SM streaming
+    const int segs = (int)std::max<int64_t>(1, std::min<int64_t>(16, fsr::ceil_div(4 * ctx->num_sms * 8, b)));
+    const int64_t seg_len = fsr::ceil_div(fsr::ceil_div(n, segs), 1024) * 1024;
+    P::prune_scan_kernel<<<(unsigned)(b * segs), P::kThreads, 0, ctx->stream>>>(n, segs, seg_len, Xt, n, cb, cmax_bits,
+                                                                               qp, thr, cand, ccount, nlow);
+    FSR_TRY(fsr::launched(ctx, "prune_scan_kernel"));
+    P::prune_finish_kernel<<<(unsigned)b, P::kThreads, 0, ctx->stream>>>(n, Xt, n, cb, qp, cand, ccount, nlow,
+                                                                        u_indptr, u_indices, u_values, Zs, b, eta,
+                                                                        copy, y_ptr, y_idx, topk, top_idx, top_val,
+                                                                        nflag, flags);
     FSR_TRY(fsr::launched(ctx, "prune_finish_kernel"));
     P::fallback_rows_kernel<<<(unsigned)ctx->num_sms * 8, 256, 0, ctx->stream>>>(
         n, Xt, n, u_indptr, u_indices, u_values, Zs, b, eta, copy, y_ptr, y_idx, nflag, flags);

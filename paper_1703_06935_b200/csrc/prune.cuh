@@ -415,18 +415,19 @@ __device__ __forceinline__ float exact_score(int64_t i, int64_t q, const float* 
   return acc;
 }
 
-// Selection in two kernels so the streaming one stays light (registers ->
-// occupancy -> bytes in flight):
-// prune_collect_kernel -- persistent CTAs, one query at a time:
-//  1. t = threshold on the lower keys from a 1/16 sample (two 12-bit digits);
-//  2. one pass: count lower >= t, collect the rows with upper >= t (a round-
-//     to-nearest pre-filter skips the directed-rounding work far below t)
-//     into cand[q][0 .. kCap); ccount[q] = count, or flags the query when
-//     count < K or the candidates overflow.
-// prune_finish_kernel -- one CTA per query:
-//  3. lambda_K = K-th largest lower among the candidates (they hold every
-//     row with lower >= t), keep upper >= lambda_K;
-//  4. exact re-score of those (8-lane group per row, from a counter), bitonic sort, top K out.
+// Selection in three kernels:
+// prune_threshold_kernel -- per query (persistent CTAs): t = threshold on the
+//    lower keys from a 1/16 sample (two 12-bit digits); zeroes the query's
+//    counters; z = 0 queries are flagged for the exact select at once.
+// prune_scan_kernel -- per (query, segment), b x segs CTAs so every SM keeps
+//    streaming (one persistent CTA per query left the DRAM at 53%): one pass
+//    counts lower >= t and collects the rows with upper >= t into cand[q]
+//    through per-query global counters.
+// prune_finish_kernel -- per query: flags the query when count < K or the
+//    candidates overflow; else lambda_K = K-th largest lower among the
+//    candidates (they hold every row with lower >= t), keep upper >= lambda_K,
+//    exact re-score of those (8-lane group per row, from a counter), bitonic
+//    sort, top K out.
 struct SelShared {
   unsigned int hist[1 << topk::kHistBits];
   unsigned int count;
@@ -436,13 +437,13 @@ struct SelShared {
   unsigned int n_keep;
 };
 
-__global__ void __launch_bounds__(kThreads) prune_collect_kernel(int64_t n, int64_t b, const float* __restrict__ Xt,
-                                                                  int64_t ldx, const float* __restrict__ cb,
-                                                                  const int* __restrict__ cmax_bits,
-                                                                  const float2* __restrict__ qp, int64_t K,
-                                                                  int32_t* __restrict__ cand,
-                                                                  int32_t* __restrict__ ccount,
-                                                                  int* __restrict__ nflag, int* __restrict__ flags) {
+__global__ void __launch_bounds__(kThreads) prune_threshold_kernel(int64_t n, int64_t b, const float* __restrict__ Xt,
+                                                                    int64_t ldx, const float* __restrict__ cb,
+                                                                    const float2* __restrict__ qp, int64_t K,
+                                                                    uint32_t* __restrict__ thr,
+                                                                    int32_t* __restrict__ ccount,
+                                                                    unsigned* __restrict__ nlow,
+                                                                    int* __restrict__ nflag, int* __restrict__ flags) {
   constexpr int KB = 32;
   constexpr int nb = 1 << topk::kHistBits;
   __shared__ SelShared sh;
@@ -460,7 +461,6 @@ __global__ void __launch_bounds__(kThreads) prune_collect_kernel(int64_t n, int6
       continue;
     }
     const bool vec_ok = ((((uintptr_t)xr) | ((uintptr_t)cb)) & 15) == 0;
-    int32_t* cq = cand + q * kCap;
     // 1. sampled threshold on the lower keys
     uint32_t prefix = 0;
     unsigned long long above0 = 0;
@@ -514,52 +514,78 @@ __global__ void __launch_bounds__(kThreads) prune_collect_kernel(int64_t n, int6
       __syncthreads();
     }
     const uint32_t t_lo = prefix << (KB - 2 * topk::kHistBits);
-    const float tf = key_to_float((uint64_t)t_lo);
-    const float tf_pre = tf - fabsf(tf) * 0x1p-20f - 0x1p-126f;  // conservative round-to-nearest pre-filter
-    // 2. one pass
     if (!threadIdx.x) {
-      sh.count = 0;
-      sh.n_lower = 0;
-    }
-    __syncthreads();
-    unsigned mine = 0;
-    // rows with x~ + max_i(c_i) Zb below the threshold cannot qualify: c_i is read only for the rest
-    const float cz_max = __int_as_float(*cmax_bits) * zb * (1.f + 0x1p-20f);
-    for_each_x32<8>(xr, (int)n, [&](int e, float x) {
-      if (x + cz_max >= tf_pre) {
-        const float bd = bound_of(__ldg(cb + e), zb);
-        mine += key32(__fsub_rd(x, bd)) >= t_lo;
-        if (key32(__fadd_ru(x, bd)) >= t_lo) {
-          const unsigned slot = atomicAdd(&sh.count, 1u);
-          if (slot < (unsigned)kCap) cq[slot] = (int32_t)e;
-        }
-      }
-    });
-#pragma unroll
-    for (int o = 16; o; o >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, o);
-    if (lane == 0) atomicAdd(&sh.n_lower, (unsigned long long)mine);
-    __syncthreads();
-    if (!threadIdx.x) {
-      const bool bad = sh.n_lower < (unsigned long long)K || sh.count > (unsigned)kCap;
-      ccount[q] = bad ? -1 : (int32_t)sh.count;
-      if (bad) flags[atomicAdd(nflag, 1)] = (int)q;
+      thr[q] = t_lo;
+      ccount[q] = 0;
+      nlow[q] = 0;
     }
     __syncthreads();
   }
 }
 
+// One streaming pass over a segment of one query's x~ row (grid = b x segs):
+// count lower >= t and collect the rows with upper >= t into cand[q] through
+// per-query global counters (a round-to-nearest pre-filter with max_i c_i
+// skips the directed-rounding work, and the read of c_i, far below t).
+__global__ void __launch_bounds__(kThreads) prune_scan_kernel(int64_t n, int segs, int64_t seg_len,
+                                                               const float* __restrict__ Xt, int64_t ldx,
+                                                               const float* __restrict__ cb,
+                                                               const int* __restrict__ cmax_bits,
+                                                               const float2* __restrict__ qp,
+                                                               const uint32_t* __restrict__ thr,
+                                                               int32_t* __restrict__ cand, int32_t* __restrict__ ccount,
+                                                               unsigned* __restrict__ nlow) {
+  __shared__ unsigned red[kThreads / 32];
+  const int64_t q = blockIdx.x / segs;
+  const int64_t s0 = (blockIdx.x % segs) * seg_len, s1 = min(n, s0 + seg_len);
+  if (ccount[q] < 0 || s0 >= s1) return;  // z = 0: answered by the exact select
+  const uint32_t t_lo = thr[q];
+  const float zb = qp[q].y;
+  const float tf = key_to_float((uint64_t)t_lo);
+  const float tf_pre = tf - fabsf(tf) * 0x1p-20f - 0x1p-126f;  // conservative round-to-nearest pre-filter
+  const float cz_max = __int_as_float(*cmax_bits) * zb * (1.f + 0x1p-20f);
+  const float* xr = Xt + q * ldx + s0;
+  int32_t* cq = cand + q * kCap;
+  unsigned mine = 0;
+  for_each_x32<8>(xr, (int)(s1 - s0), [&](int e, float x) {
+    if (x + cz_max >= tf_pre) {
+      const int64_t i = s0 + e;
+      const float bd = bound_of(__ldg(cb + i), zb);
+      mine += key32(__fsub_rd(x, bd)) >= t_lo;
+      if (key32(__fadd_ru(x, bd)) >= t_lo) {
+        const int slot = atomicAdd(ccount + q, 1);
+        if (slot < kCap) cq[slot] = (int32_t)i;
+      }
+    }
+  });
+#pragma unroll
+  for (int o = 16; o; o >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mine;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned tot = 0;
+    for (int w = 0; w < kThreads / 32; ++w) tot += red[w];
+    if (tot) atomicAdd(nlow + q, tot);
+  }
+}
+
 __global__ void __launch_bounds__(kThreads) prune_finish_kernel(
     int64_t n, const float* __restrict__ Xt, int64_t ldx, const float* __restrict__ cb, const float2* __restrict__ qp,
-    const int32_t* __restrict__ cand, const int32_t* __restrict__ ccount, const int64_t* __restrict__ indptr,
-    const int32_t* __restrict__ indices, const float* __restrict__ vals, const float* __restrict__ Zs, int64_t ldz,
-    const double* __restrict__ eta, int copy, const int64_t* __restrict__ y_ptr, const int64_t* __restrict__ y_idx,
-    int64_t K, int64_t* __restrict__ out_idx, float* __restrict__ out_val) {
+    const int32_t* __restrict__ cand, const int32_t* __restrict__ ccount, const unsigned* __restrict__ nlow,
+    const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices, const float* __restrict__ vals,
+    const float* __restrict__ Zs, int64_t ldz, const double* __restrict__ eta, int copy,
+    const int64_t* __restrict__ y_ptr, const int64_t* __restrict__ y_idx, int64_t K, int64_t* __restrict__ out_idx,
+    float* __restrict__ out_val, int* __restrict__ nflag, int* __restrict__ flags) {
   __shared__ uint64_t ckey[kCap];
   __shared__ int64_t cidx[kCap];
   __shared__ unsigned n_keep, n_next;
   const int64_t q = blockIdx.x;
   const int cnt = ccount[q];
-  if (cnt < 0) return;  // flagged: the fallback kernels answer this query
+  if (cnt < 0) return;  // z = 0: flagged by the threshold kernel, answered by the exact select
+  if (nlow[q] < (unsigned long long)K || cnt > kCap) {  // sampled threshold too high, or overflow
+    if (threadIdx.x == 0) flags[atomicAdd(nflag, 1)] = (int)q;
+    return;
+  }
   const int lane = threadIdx.x & 31;
   const float* xr = Xt + q * ldx;
   const float zb = qp[q].y;
@@ -672,7 +698,7 @@ __global__ void __launch_bounds__(topk::kThreads) fallback_select_kernel(int64_t
 inline size_t workspace_bytes(int64_t n, int64_t r, int64_t b) {
   auto al = [](size_t x) { return (x + 255) / 256 * 256; };
   return al((size_t)r * b * 2) + al((size_t)b * 8) + al((size_t)n * 4) + al((size_t)(b + 2) * 4) +
-         al((size_t)b * kCap * 4) + al((size_t)b * 4);
+         al((size_t)b * kCap * 4) + al((size_t)b * 4) + al((size_t)b * 4) + al((size_t)b * 4);
 }
 
 inline bool applicable(int64_t n, int64_t b, int64_t K) {
