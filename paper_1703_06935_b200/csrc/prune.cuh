@@ -362,7 +362,7 @@ __device__ __forceinline__ float exact_score_group(int64_t i, int64_t q, const f
   // R entries per lane per round: all loads of a round in flight together
   // (larger rounds measured no faster: a round is bound by the dependent
   // DRAM latencies indptr -> entries -> Zs of the candidate's row)
-  constexpr int R = 128 / G;
+  constexpr int R = 64 / G;
   float acc = 0.f;
   for (int64_t base = e0; base < e1; base += G * R) {
     const int m = e1 - base < G * R ? (int)(e1 - base) : G * R;
