@@ -278,12 +278,34 @@ __global__ void __launch_bounds__(256) spmm_narrow_T_kernel(int64_t n_rows, cons
   const int64_t p0 = (int64_t)blockIdx.y * PW;  // column panel (row-major output mode)
   const int64_t c0 = p0 + (int64_t)sl * VEC;
   const bool live = c0 < ncols;
-  // rows are handed out dynamically (as in the wide kernel): a warp that
-  // drew short rows takes more of them instead of idling at the barrier
+  // rows are handed out dynamically (as in the wide kernel), longest first:
+  // a warp that drew short rows takes more of them instead of idling at the
+  // barrier, and the rows handed out last are the short ones
   __shared__ int next_row;
+  __shared__ int order_s[64];
+  if (warp == 0) {
+    int64_t len[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int64_t i = row0 + h * 32 + lane;
+      len[h] = i < n_rows ? __ldg(indptr + i + 1) - __ldg(indptr + i) : 0;
+    }
+    int rank[2] = {0, 0};
+#pragma unroll
+    for (int g = 0; g < 2; ++g)
+#pragma unroll 8
+      for (int k = 0; k < 32; ++k) {
+        const int64_t lk = __shfl_sync(0xffffffffu, len[g], k);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) rank[h] += (lk > len[h]) || (lk == len[h] && g * 32 + k < h * 32 + lane);
+      }
+    order_s[rank[0]] = lane;
+    order_s[rank[1]] = 32 + lane;
+  }
   if (threadIdx.x == 0) next_row = 8;
   __syncthreads();
-  for (int rr = warp; rr < 64;) {
+  for (int pos = warp; pos < 64;) {
+    const int rr = order_s[pos];
     const int64_t i = row0 + rr;
     T acc[VEC];
 #pragma unroll
@@ -333,7 +355,7 @@ __global__ void __launch_bounds__(256) spmm_narrow_T_kernel(int64_t n_rows, cons
     }
     int nr = 0;
     if (lane == 0) nr = atomicAdd(&next_row, 1);
-    rr = __shfl_sync(0xffffffffu, nr, 0);
+    pos = __shfl_sync(0xffffffffu, nr, 0);
   }
   if (!TRANS) return;
   __syncthreads();
