@@ -152,6 +152,7 @@ __global__ void __launch_bounds__(32 * WARPS, MINB) spmm_T_half_kernel(int64_t n
   // rows in index order).  Within a row the next 32 entries are in flight
   // while the current 32 are summed.
   static_assert(NV == 1, "row loop is written for one 256-column vector per lane");
+  static_assert(DEPTH % 2 == 0, "entries are read in pairs");
   static_assert(ROWS % 32 == 0 && ROWS <= 128, "lanes of warp 0 rank the block's rows, ROWS / 32 each");
   constexpr int RPL = ROWS / 32;
   __shared__ int order_s[ROWS];
@@ -191,6 +192,8 @@ __global__ void __launch_bounds__(32 * WARPS, MINB) spmm_T_half_kernel(int64_t n
   // per-lane base of its 8 columns; row offsets in 32 bits (Zh <= 4 GB): one IMAD.WIDE per gather
   const __half* zl = Zh + c0;
   const uint32_t ldx32 = (uint32_t)ldx;
+  __shared__ __align__(16) int2 ent_s[32 * WARPS];
+  int2* ent = ent_s + warp * 32;
   int pos = warp;
   int rr = order_s[pos];
   int64_t e0 = start_s[rr], e1 = e0 + len_s[rr];
@@ -215,14 +218,22 @@ __global__ void __launch_bounds__(32 * WARPS, MINB) spmm_T_half_kernel(int64_t n
         pv = __ldg(vals + base + 32 + lane);
       }
       ss = __fmaf_ru(cv, cv, ss);
+      // the chunk's (column, value) pairs go through shared memory: one
+      // broadcast LDS.128 yields two entries (instead of four shuffles)
+      __syncwarp();
+      ent[lane] = make_int2(cc, __float_as_int(cv));
+      __syncwarp();
       int j = 0;
       for (; j + DEPTH <= m; j += DEPTH) {
         uint32_t c[DEPTH];
         float a[DEPTH];
 #pragma unroll
-        for (int g = 0; g < DEPTH; ++g) {
-          c[g] = (uint32_t)__shfl_sync(0xffffffffu, cc, j + g);
-          a[g] = __shfl_sync(0xffffffffu, cv, j + g);
+        for (int g = 0; g < DEPTH; g += 2) {
+          const int4 p2 = *reinterpret_cast<const int4*>(&ent[j + g]);
+          c[g] = (uint32_t)p2.x;
+          a[g] = __int_as_float(p2.y);
+          c[g + 1] = (uint32_t)p2.z;
+          a[g + 1] = __int_as_float(p2.w);
         }
         uint4 raw[DEPTH];
 #pragma unroll
