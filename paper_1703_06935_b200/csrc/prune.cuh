@@ -124,7 +124,8 @@ __device__ __forceinline__ uint4 ld_gather(const __half* p) { return __ldg(reint
 // profiles/r01/k9h_ncu_full.json): the bytes in flight per SM over the loaded
 // L2 latency bound it.  64-row blocks (8 or 16 warps) and 4-warp blocks at 6
 // CTAs/SM measured 14.7-15.0 ms; DEPTH 10 / 12 / 16 at 3 CTAs/SM 15.3 / 17.4 /
-// 14.6 ms.
+// 14.6 ms; a predicated last round per chunk (instead of single gathers) spilled
+// at 64 registers: 22.5 ms.
 template <int NV, int DEPTH, int ROWS, int MINB, int WARPS = 8>
 __global__ void __launch_bounds__(32 * WARPS, MINB) spmm_T_half_kernel(int64_t n_rows, const int64_t* __restrict__ indptr,
                                                           const int32_t* __restrict__ indices,
