@@ -9,14 +9,18 @@
 // returned top-K indices and values are therefore the ones the unpruned fp32
 // path returns, bit for bit; fp16 values are never returned.
 //
-// Bound (row i with m_i entries, query q, rounding unit u = 2^-24):
-//   |x_fp32 - x~_fp32| <= sum_j |u_ij||zs_j - zs~_j| + gamma_m (sum |u||zs| + sum |u||zs~|)
-//                      <= ||u_i||_2 ||zs_q||_2 (2^-11 + 2.01 m_i u) + sqrt(m_i) ||u_i||_2 2^-25 / s_q
+// Bound (row i with m_i entries, query q, rounding unit u = 2^-24): K9h
+// multiplies u~ = fp16(u) by zs~ = fp16(zs s_q) / s_q with fp32 accumulation
+// (FHFMA), so with du = u~ - u, dz = zs~ - zs,
+//   |x_fp32 - x~_fp32| <= sum_j (|u_ij||dz_j| + |du_ij||zs~_j|) + gamma_m (sum |u||zs| + sum |u~||zs~|)
+//                      <= ||u_i||_2 ||zs_q||_2 (2 * 2^-11 + 2.01 m_i u) + sqrt(m_i) ||u_i||_2 2^-25 / s_q
+//                         + sqrt(m_i) 2^-25 ||zs~_q||_2                        (all to first order)
 //                      <= c_i * Zb_q,
-//   c_i  = ||u_i||_2 (2^-11 + 2.01 m_i 2^-24 + sqrt(m_i) 2^-38)   (K9h, from the row it streams)
-//   Zb_q = max(||zs_q||_2, 2^13 / s_q)                           (zs_half_kernel)
-// (fp16 rounding is relative 2^-11 for normal scaled values and absolute
-// 2^-25 below the normal range; Cauchy-Schwarz bounds both sums.)  With
+//   c_i  = (||u_i||_2 (2^-10 + 2.01 m_i 2^-24 + sqrt(m_i) 2^-38) + sqrt(m_i) 2^-25) * 1.01
+//          (K9h, from the row it streams; 1.01 covers the second-order terms)
+//   Zb_q = max(||zs_q||_2, 2^13 / s_q)                           (K8 / zs_half_kernel)
+// (fp16 rounding is relative 2^-11 for normal values and absolute 2^-25 below
+// the normal range; Cauchy-Schwarz bounds every sum.)  With
 // lower_i = x~_i - c_i Zb and upper_i = x~_i + c_i Zb (directed rounding), any
 // threshold t such that at least K rows have lower >= t satisfies t <= x_(K),
 // so {i : upper_i >= t} contains every exact top-K row and every tie at the
@@ -38,7 +42,7 @@ namespace prune {
 
 constexpr int kExactRows = 1 << 30;  // flag bit: the query's x~ row is exact (z = 0), no recompute
 constexpr int kThreads = 256;  // prune_select_kernel: several CTAs per SM overlap their serial phases
-constexpr int kCap = 1024;     // candidates held in shared memory (typical ~3K + band); more -> fallback
+constexpr int kCap = 2048;     // candidates per query (typical ~3.7K + band, max seen 844 at C3); more -> fallback
 
 // Scale of one query column from its max |zs| and sum of squares:
 // s = 2^(14 - e) with amax < 2^e, 1/s, and Zb = max(||zs||_2 rounded up, 2^13 / s);
@@ -98,6 +102,15 @@ __global__ void __launch_bounds__(256) zs_half_kernel(int64_t r, int64_t b, cons
     nflag[0] = 0;
     nflag[b + 1] = 0;  // max_i c_i (float bits), raised by K9h
   }
+}
+
+// acc0 += a * lo(pair), acc1 += a * hi(pair): fp32 accumulation of fp16
+// products (FHFMA, one instruction per column; no fp16 -> fp32 conversions).
+__device__ __forceinline__ void fhfma2(uint32_t pair, uint16_t a, float& acc0, float& acc1) {
+  asm("{ .reg .f16 lo, hi, ah; mov.b32 {lo, hi}, %2; mov.b16 ah, %3;\n\t"
+      "fma.rn.f32.f16 %0, ah, lo, %0; fma.rn.f32.f16 %1, ah, hi, %1; }"
+      : "+f"(acc0), "+f"(acc1)
+      : "r"(pair), "h"(a));
 }
 
 // 16-byte gather of an fp16 Zs row segment (read-only path; L1-allocating:
@@ -206,9 +219,9 @@ __global__ void __launch_bounds__(32 * WARPS, MINB) spmm_T_half_kernel(int64_t n
   }
   while (pos < ROWS) {
     const int64_t i = row0 + rr;
-    float2 acc[4];
+    float acc[8];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) acc[q] = make_float2(0.f, 0.f);
+    for (int q = 0; q < 8; ++q) acc[q] = 0.f;
     float ss = 0.f;  // sum of squares, rounded up (an upper bound of ||u_i||^2)
     for (int64_t base = e0; base < e1; base += 32) {
       const int m = (e1 - base) < 32 ? (int)(e1 - base) : 32;
@@ -222,19 +235,19 @@ __global__ void __launch_bounds__(32 * WARPS, MINB) spmm_T_half_kernel(int64_t n
       // the chunk's (column, value) pairs go through shared memory: one
       // broadcast LDS.128 yields two entries (instead of four shuffles)
       __syncwarp();
-      ent[lane] = make_int2(cc, __float_as_int(cv));
+      ent[lane] = make_int2(cc, (int)__half_as_ushort(__float2half_rn(cv)));  // u~ = fp16(u)
       __syncwarp();
       int j = 0;
       for (; j + DEPTH <= m; j += DEPTH) {
         uint32_t c[DEPTH];
-        float a[DEPTH];
+        uint16_t a[DEPTH];
 #pragma unroll
         for (int g = 0; g < DEPTH; g += 2) {
           const int4 p2 = *reinterpret_cast<const int4*>(&ent[j + g]);
           c[g] = (uint32_t)p2.x;
-          a[g] = __int_as_float(p2.y);
+          a[g] = (uint16_t)p2.y;
           c[g + 1] = (uint32_t)p2.z;
-          a[g + 1] = __int_as_float(p2.w);
+          a[g + 1] = (uint16_t)p2.w;
         }
         uint4 raw[DEPTH];
 #pragma unroll
@@ -243,20 +256,22 @@ __global__ void __launch_bounds__(32 * WARPS, MINB) spmm_T_half_kernel(int64_t n
 #pragma unroll
         for (int g = 0; g < DEPTH; ++g) {
           if (!live[0]) continue;
-          const float2 a2 = make_float2(a[g], a[g]);
-          const __half2* h = reinterpret_cast<const __half2*>(&raw[g]);
-#pragma unroll
-          for (int k = 0; k < 4; ++k) acc[k] = __ffma2_rn(a2, __half22float2(h[k]), acc[k]);
+          fhfma2(raw[g].x, a[g], acc[0], acc[1]);
+          fhfma2(raw[g].y, a[g], acc[2], acc[3]);
+          fhfma2(raw[g].z, a[g], acc[4], acc[5]);
+          fhfma2(raw[g].w, a[g], acc[6], acc[7]);
         }
       }
       for (; j < m; ++j) {
-        const uint32_t c = (uint32_t)__shfl_sync(0xffffffffu, cc, j);
-        const float a = __shfl_sync(0xffffffffu, cv, j);
+        const int2 p1 = ent[j];
+        const uint32_t c = (uint32_t)p1.x;
+        const uint16_t ah = (uint16_t)p1.y;
         if (live[0]) {
           const uint4 t = ld_gather(zl + c * ldx32);
-          const __half2* h = reinterpret_cast<const __half2*>(&t);
-#pragma unroll
-          for (int k = 0; k < 4; ++k) acc[k] = __ffma2_rn(make_float2(a, a), __half22float2(h[k]), acc[k]);
+          fhfma2(t.x, ah, acc[0], acc[1]);
+          fhfma2(t.y, ah, acc[2], acc[3]);
+          fhfma2(t.z, ah, acc[4], acc[5]);
+          fhfma2(t.w, ah, acc[6], acc[7]);
         }
       }
       cc = pc;
@@ -267,17 +282,15 @@ __global__ void __launch_bounds__(32 * WARPS, MINB) spmm_T_half_kernel(int64_t n
       for (int o = 16; o; o >>= 1) ss = __fadd_ru(ss, __shfl_xor_sync(0xffffffffu, ss, o));
       if (lane == 0) {
         const double m = (double)(e1 - e0);
-        const double f = 0x1p-11 + 2.01 * m * 0x1p-24 + sqrt(m) * 0x1p-38;
-        const float c = __double2float_ru(__dsqrt_ru((double)ss) * f * (1.0 + 0x1p-20));
+        // u and zs both rounded to fp16 (2^-11 relative each), fp32 sums, subnormal fp16 u
+        const double f = 2.0 * 0x1p-11 + 2.01 * m * 0x1p-24 + sqrt(m) * 0x1p-38;
+        const float c = __double2float_ru((__dsqrt_ru((double)ss) * f + sqrt(m) * 0x1p-25) * 1.01);
         cbound[i] = c;
         atomicMax(&cmax_s, __float_as_int(c));  // c >= 0: int order == float order
       }
     }
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      tile[rr][lane * 8 + 2 * q] = acc[q].x;
-      tile[rr][lane * 8 + 2 * q + 1] = acc[q].y;
-    }
+    for (int q = 0; q < 8; ++q) tile[rr][lane * 8 + q] = acc[q];
     int nr = 0;
     if (lane == 0) nr = atomicAdd(&next_row, 1);
     pos = __shfl_sync(0xffffffffu, nr, 0);
