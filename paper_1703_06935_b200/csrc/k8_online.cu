@@ -278,7 +278,7 @@ int filter_pruned(fsr_ctx* ctx, int64_t n, int64_t r, const int64_t* u_indptr, c
   }
   {
     fsr::StageTimer timer(ctx, FSR_STAGE_FILTER_SPMM);
-    FSR_TRY((launch_k9h<1, 8, 32, 3>(ctx, n, u_indptr, u_indices, u_values, b, Zh, qp, Xt, cb, cmax_bits)));
+    FSR_TRY((launch_k9h<1, 4, 32, 4>(ctx, n, u_indptr, u_indices, u_values, b, Zh, qp, Xt, cb, cmax_bits)));
   }
   if (copy_uncovered && eta) {
     fsr::StageTimer timer(ctx, FSR_STAGE_COPY_UNCOVERED);

@@ -126,8 +126,10 @@ __device__ __forceinline__ uint4 ld_gather(const __half* p) { return __ldg(reint
 // Measured at C3 2%, b = 1024: NV = 1 (256-column
 // panels), DEPTH 8, 4 CTAs/SM (64 registers) 14.8 ms, then 14.5 with the next
 // 32 entries prefetched, 13.7 with the rows handed out longest first, 13.1
-// with the entries broadcast from shared memory, 11.9 with FHFMA (fp16 u) at
-// 3 CTAs/SM (80 registers; at 4 CTAs/SM it spills: 14.7) -- kept; DEPTH 4 at 4 / 5 / 6 CTAs/SM 15.7 / 16.4 / 18.1; DEPTH 6 at 5 CTAs/SM
+// with the entries broadcast from shared memory, 11.9 with FHFMA (fp16 u):
+// DEPTH 4 at 4 CTAs/SM (64 registers, no spills) 11.90 -- kept -- and DEPTH 8
+// at 3 CTAs/SM 11.92; DEPTH 8 / 10 / 12 spilling at 64-80 registers 14.7 /
+// 15.2 / 23.3, DEPTH 16 at 2 CTAs/SM 13.8; DEPTH 4 at 4 / 5 / 6 CTAs/SM 15.7 / 16.4 / 18.1; DEPTH 6 at 5 CTAs/SM
 // 16.6; NV = 2 DEPTH 4 at 2 or 3 CTAs/SM 20.5 / 16.5; a barrier-free variant
 // (warp-owned 8-row items, persistent grid, per-warp transposes) 19.1-19.4;
 // a one-row lookahead in the hand-out 16.5; gathers landing in shared memory
