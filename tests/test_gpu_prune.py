@@ -126,3 +126,25 @@ def test_pruned_heat_kernel_k_range_ragged_batch():
         (pi, pv), (ui, uv) = both(dec, qb, K=K, h=h)
         np.testing.assert_array_equal(pi, ui)
         np.testing.assert_array_equal(pv.view(np.uint32), uv.view(np.uint32))
+
+
+def test_filter_graph_partial_batch_on_pruned_path():
+    """A CUDA-graph step over a partial batch (the padding queries are empty
+    observations) returns the unpruned fp32 top-k for the real queries."""
+    n, r, b = 140_000, 300, 256
+    _, dec = make_dec(n, r, 20, 21)
+    qb = queries(n, 100, 22)
+    h = ranking.h_alpha(0.99)
+    fg = ranking.FilterGraph(dec, h, b=b, nnz_cap=int(qb.y_ptr[-1]), topk=50)
+    fg.submit(qb)
+    gi, gv = fg.fetch()
+    ctx = N.Context.get()
+    ctx.set_topk_prune(False)
+    try:
+        r_ = ranking.filter_device(dec, h, ranking.DeviceQueries(qb, dec.dtype, dec.eta_device.device), topk=50,
+                                   want_x=False)
+        torch.cuda.synchronize()
+    finally:
+        ctx.set_topk_prune(True)
+    np.testing.assert_array_equal(gi, r_.top_idx.cpu().numpy())
+    np.testing.assert_array_equal(gv.view(np.uint32), r_.top_val.cpu().numpy().view(np.uint32))
