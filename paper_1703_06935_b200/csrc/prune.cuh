@@ -729,6 +729,10 @@ inline size_t workspace_bytes(int64_t n, int64_t r, int64_t b) {
          al((size_t)b * kCap * 4) + al((size_t)b * 4) + al((size_t)b * 4) + al((size_t)b * 4);
 }
 
+// b >= 256: a narrow variant for 64 <= b < 256 (64-column panels, 8-lane
+// groups per row) measured K9 1.95 vs 2.05 ms at b = 64 but 0.40 vs 0.17 ms of
+// selection -- slower overall -- and b <= 64's exact kernel sums a row in two
+// interleaved halves, so its values are not the sequential order re-scored here.
 inline bool applicable(int64_t n, int64_t b, int64_t K) {
   return n >= (int64_t)topk::kSampleChunk * topk::kSampleEvery * 8 && n < ((int64_t)1 << 31) && b >= 256 && b % 8 == 0 && K >= 1 &&
          K <= kCap / 8;
