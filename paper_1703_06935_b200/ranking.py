@@ -269,11 +269,11 @@ def topk_pruned(n: int, b: int, k: int, dtype, sparse: bool = True) -> bool:
     """Whether a top-k-only ``filter_device`` call takes the certified pruned
     path (csrc/prune.cuh ``applicable``; the context option FSR_OPT_TOPK_PRUNE
     must also be on): fp32 sparse U~, n >= 131072, b >= 256, b % 8 == 0,
-    1 <= k <= 128.  Its top-k equals the unpruned fp32 path's bit for bit."""
+    1 <= k <= 256 (csrc/prune.cuh `applicable`).  Its top-k equals the unpruned fp32 path's bit for bit."""
     import torch
 
     return (sparse and dtype == torch.float32 and 131072 <= n < 2 ** 31 and b >= 256 and b % 8 == 0
-            and 1 <= k <= 128)
+            and 1 <= k <= 256)
 
 
 def pruned_fallback_count(workspace, n: int, r: int, b: int) -> int:

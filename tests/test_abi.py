@@ -51,3 +51,23 @@ def test_no_cuda_device_fails_loudly():
         pytest.skip("GPU present")
     with pytest.raises(RuntimeError):
         _native.Context.get(0)
+
+
+def test_topk_pruned_conditions():
+    """Host mirror of csrc/prune.cuh `applicable`: which filter calls take the
+    certified pruned path (fp32, sparse, n >= 131072, b >= 256 and b % 8 == 0,
+    1 <= k <= 256)."""
+    import torch
+
+    from paper_1703_06935_b200 import ranking
+
+    f32, f64 = torch.float32, torch.float64
+    assert ranking.topk_pruned(1_000_000, 1024, 100, f32)
+    assert ranking.topk_pruned(131_072, 256, 256, f32)
+    assert not ranking.topk_pruned(131_071, 1024, 100, f32)
+    assert not ranking.topk_pruned(1_000_000, 255, 100, f32)
+    assert not ranking.topk_pruned(1_000_000, 260, 100, f32)
+    assert not ranking.topk_pruned(1_000_000, 1024, 257, f32)
+    assert not ranking.topk_pruned(1_000_000, 1024, 0, f32)
+    assert not ranking.topk_pruned(1_000_000, 1024, 100, f64)
+    assert not ranking.topk_pruned(1_000_000, 1024, 100, f32, sparse=False)

@@ -122,7 +122,7 @@ def test_pruned_heat_kernel_k_range_ragged_batch():
     n, r, b = 131_072 + 5, 300, 264  # n not a multiple of 4, b not a multiple of the 256-column panel
     _, dec = make_dec(n, r, 20, 8)
     qb = queries(n, b, 9, k=30)
-    for K, h in ((1, ranking.heat_kernel(10.0)), (37, ranking.h_alpha(0.9)), (128, ranking.h_alpha(0.99))):
+    for K, h in ((1, ranking.heat_kernel(10.0)), (37, ranking.h_alpha(0.9)), (128, ranking.h_alpha(0.99)), (256, ranking.h_alpha(0.99))):
         (pi, pv), (ui, uv) = both(dec, qb, K=K, h=h)
         np.testing.assert_array_equal(pi, ui)
         np.testing.assert_array_equal(pv.view(np.uint32), uv.view(np.uint32))
