@@ -116,6 +116,12 @@ __device__ __forceinline__ void fhfma2(uint32_t pair, uint16_t a, float& acc0, f
 // 16-byte gather of an fp16 Zs row segment (read-only path; L1-allocating:
 // ld.global.nc.L1::no_allocate measured 10% slower, 16.0 vs 14.5 ms at C3).
 __device__ __forceinline__ uint4 ld_gather(const __half* p) { return __ldg(reinterpret_cast<const uint4*>(p)); }
+// The same at base + c * ldxb bytes: one IMAD.WIDE.U32 per address (a 32-bit
+// element offset scaled by sizeof(half) afterwards compiled to six integer
+// instructions per gather).
+__device__ __forceinline__ uint4 ld_gather(const char* base, uint32_t c, uint32_t ldxb) {
+  return __ldg(reinterpret_cast<const uint4*>(base + (uint64_t)c * ldxb));
+}
 
 // K9h: Xt~ (ncols x n_rows, ld ldy) = (A Zh) .* inv_s over column panels of
 // PW = 256 NV columns (8 halves = 16 bytes per lane per vector); the same
@@ -128,7 +134,9 @@ __device__ __forceinline__ uint4 ld_gather(const __half* p) { return __ldg(reint
 // 32 entries prefetched, 13.7 with the rows handed out longest first, 13.1
 // with the entries broadcast from shared memory, 11.9 with FHFMA (fp16 u):
 // DEPTH 4 at 4 CTAs/SM (64 registers, no spills) 11.90 -- kept -- and DEPTH 8
-// at 3 CTAs/SM 11.92; DEPTH 8 / 10 / 12 spilling at 64-80 registers 14.7 /
+// at 3 CTAs/SM 11.92, then 11.64 with one IMAD.WIDE.U32 per gather address
+// (6 -> 2 integer instructions; 17.6 TB/s of gathers, 88% of the random-row
+// L2 probe, so fewer L2 bytes is the remaining lever); DEPTH 8 / 10 / 12 spilling at 64-80 registers 14.7 /
 // 15.2 / 23.3, DEPTH 16 at 2 CTAs/SM 13.8; DEPTH 4 at 4 / 5 / 6 CTAs/SM 15.7 / 16.4 / 18.1; DEPTH 6 at 5 CTAs/SM
 // 16.6; NV = 2 DEPTH 4 at 2 or 3 CTAs/SM 20.5 / 16.5; a barrier-free variant
 // (warp-owned 8-row items, persistent grid, per-warp transposes) 19.1-19.4;
@@ -206,9 +214,9 @@ __global__ void __launch_bounds__(32 * WARPS, MINB) spmm_T_half_kernel(int64_t n
   }
   if (threadIdx.x == 0) next_row = WARPS;
   __syncthreads();
-  // per-lane base of its 8 columns; row offsets in 32 bits (Zh <= 4 GB): one IMAD.WIDE per gather
-  const __half* zl = Zh + c0;
-  const uint32_t ldx32 = (uint32_t)ldx;
+  // per-lane base of its 8 columns; 32-bit column index times the byte stride: one IMAD.WIDE.U32 per gather
+  const char* zl = reinterpret_cast<const char*>(Zh + c0);
+  const uint32_t ldxb = (uint32_t)ldx * (uint32_t)sizeof(__half);
   __shared__ __align__(16) int2 ent_s[32 * WARPS];
   int2* ent = ent_s + warp * 32;
   int pos = warp;
@@ -255,7 +263,7 @@ __global__ void __launch_bounds__(32 * WARPS, MINB) spmm_T_half_kernel(int64_t n
         uint4 raw[DEPTH];
 #pragma unroll
         for (int g = 0; g < DEPTH; ++g)
-          if (live[0]) raw[g] = ld_gather(zl + c[g] * ldx32);
+          if (live[0]) raw[g] = ld_gather(zl, c[g], ldxb);
 #pragma unroll
         for (int g = 0; g < DEPTH; ++g) {
           if (!live[0]) continue;
@@ -270,7 +278,7 @@ __global__ void __launch_bounds__(32 * WARPS, MINB) spmm_T_half_kernel(int64_t n
         const uint32_t c = (uint32_t)p1.x;
         const uint16_t ah = (uint16_t)p1.y;
         if (live[0]) {
-          const uint4 t = ld_gather(zl + c * ldx32);
+          const uint4 t = ld_gather(zl, c, ldxb);
           fhfma2(t.x, ah, acc[0], acc[1]);
           fhfma2(t.y, ah, acc[2], acc[3]);
           fhfma2(t.z, ah, acc[4], acc[5]);
