@@ -136,7 +136,8 @@ __device__ __forceinline__ uint4 ld_gather(const char* base, uint32_t c, uint32_
 // DEPTH 4 at 4 CTAs/SM (64 registers, no spills) 11.90 -- kept -- and DEPTH 8
 // at 3 CTAs/SM 11.92, then 11.64 with one IMAD.WIDE.U32 per gather address
 // (6 -> 2 integer instructions; 17.6 TB/s of gathers, 88% of the random-row
-// L2 probe, so fewer L2 bytes is the remaining lever); DEPTH 8 / 10 / 12 spilling at 64-80 registers 14.7 /
+// L2 probe, so fewer L2 bytes is the remaining lever; with it DEPTH 6 / 8 at
+// 4 CTAs/SM still spill, DEPTH 8 at 3 CTAs/SM spills 64 B: 13.74); DEPTH 8 / 10 / 12 spilling at 64-80 registers 14.7 /
 // 15.2 / 23.3, DEPTH 16 at 2 CTAs/SM 13.8; DEPTH 4 at 4 / 5 / 6 CTAs/SM 15.7 / 16.4 / 18.1; DEPTH 6 at 5 CTAs/SM
 // 16.6; NV = 2 DEPTH 4 at 2 or 3 CTAs/SM 20.5 / 16.5; a barrier-free variant
 // (warp-owned 8-row items, persistent grid, per-warp transposes) 19.1-19.4;
