@@ -15,9 +15,13 @@ Under torchrun each rank builds the same inputs, runs the offline pipeline as
 a replica and answers its own query batches (weak scaling: b queries per GPU
 per step); `value` = all ranks' queries / max-over-ranks device time.
 
-`--impl reference` times the reference's CPU path (the oracle port of
-``ranking.filter`` + ``rank``, /root/reference is absent on the GPU box) on a
-structure-equivalent synthetic decomposition (same n, r, tau) on host cores.
+`--impl reference` times the reference's CPU path -- the stock
+``specrank.ranking.filter`` + ``rank`` installed into baseline/_ref (the
+oracle port only when that is absent) -- on a structure-equivalent synthetic
+decomposition (same n, r, tau) on host cores.  The offline half of the
+metric gets a CPU baseline too (``offline.cpu_baseline``): the reference's
+own numpy/scipy calls timed on samples and extrapolated at C3, and the full
+stock ``decompose`` + ``sparsify`` at C1/C2.
 """
 
 from __future__ import annotations
@@ -62,6 +66,9 @@ def parse_args():
     ap.add_argument("--no-offline-warmup", action="store_true",
                     help="time the offline decomposition on its first (cold) run")
     ap.add_argument("--cpu-procs", type=int, default=64, help="processes for the CPU oracle arms (capped at nproc)")
+    ap.add_argument("--offline-cpu-full", dest="offline_cpu_full", action="store_true", default=None,
+                    help="also time the full stock reference decompose + sparsify (default at C1/C2)")
+    ap.add_argument("--no-offline-cpu-full", dest="offline_cpu_full", action="store_false")
     return ap.parse_args()
 
 
@@ -170,8 +177,54 @@ def synthetic_queries(n, b, k, seed=11):
     return ys
 
 
-def time_oracle_queries(U, lam, eta, ys, alpha, budget_s, topk):
-    """Reference per-query path: filter (ranking.py:229-255) + rank[:topk] (ranking.py:390-395)."""
+def load_reference():
+    """The stock reference package ``specrank`` installed into baseline/_ref
+    (``pip install --no-index --no-deps --target baseline/_ref`` of
+    /root/reference/pkg; pure Python, so it travels to the GPU box with the
+    repo snapshot).  None when it is absent."""
+    ref = os.path.join(REPO, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "specrank")):
+        return None
+    if ref not in sys.path:
+        sys.path.insert(0, ref)
+    try:
+        from specrank import graph as rgraph  # noqa: F401
+        from specrank import ranking as rranking
+        from specrank import spectral as rspectral
+    except Exception:
+        return None
+    return {"ranking": rranking, "spectral": rspectral, "graph": rgraph, "path": ref}
+
+
+def reference_decomposition(ref, U, lam, eta, r, tau):
+    """Wrap a host CSR U~ (float64) as the reference's own SparseDecomposition."""
+    S, G = ref["spectral"], ref["graph"]
+    return S.SpectralDecomposition(U=U, eigenvalues=np.asarray(lam, dtype=np.float64),
+                                   eta=np.asarray(eta, dtype=np.float64),
+                                   components=G.ComponentLabeling.trivial(U.shape[0]), variant=S.Variant.SPARSE,
+                                   provenance=S.Provenance(r=r, tau=tau, seed=0))
+
+
+def time_oracle_queries(U, lam, eta, ys, alpha, budget_s, topk, ref=None):
+    """Reference per-query path: filter (ranking.py:229-255) + rank[:topk]
+    (ranking.py:390-395) -- the stock ``specrank`` functions when ``ref`` is
+    given (U, lam, eta then describe a reference SpectralDecomposition),
+    else the oracle port of the same lines."""
+    if ref is not None:
+        R = ref["ranking"]
+        dec = reference_decomposition(ref, U, lam, eta, U.shape[1], U.nnz)
+        h = R.h_alpha(alpha)
+        n = U.shape[0]
+        done, t0 = 0, time.perf_counter()
+        while done < len(ys):
+            idx, val = ys[done % len(ys)]
+            y = R.ObservationVector(n, idx, val, cap=max(1, idx.size))
+            x = R.filter(dec, h, y)
+            R.rank(x)[:topk]
+            done += 1
+            if time.perf_counter() - t0 > budget_s and done >= 2:
+                break
+        return done, time.perf_counter() - t0
     from oracle import fsr_oracle as O
 
     w = O.transfer_values(O.h_alpha(alpha), lam)
@@ -193,12 +246,14 @@ def _oracle_worker(args):
     """One process of the parallel CPU arm: queries [lo, hi) of the shared list, within a budget."""
     lo, hi, budget_s, topk = args
     st = _POOL_STATE
-    done, secs = time_oracle_queries(st["U"], st["lam"], st["eta"], st["ys"][lo:hi], st["alpha"], budget_s, topk)
+    done, secs = time_oracle_queries(st["U"], st["lam"], st["eta"], st["ys"][lo:hi], st["alpha"], budget_s, topk,
+                                     st.get("ref"))
     return done, secs
 
 
-def parallel_oracle_qps(U, lam, eta, ys, alpha, budget_s, topk, procs):
-    """Queries/s of the oracle port over `procs` forked processes (U shared copy-on-write).
+def parallel_oracle_qps(U, lam, eta, ys, alpha, budget_s, topk, procs, ref=None):
+    """Queries/s of the reference's per-query path over `procs` forked
+    processes (U shared copy-on-write).
 
     The reference's filter is single-threaded scipy (csr_matvec), so the CPU's
     best throughput comes from answering independent queries in parallel.
@@ -206,9 +261,9 @@ def parallel_oracle_qps(U, lam, eta, ys, alpha, budget_s, topk, procs):
     import multiprocessing as mp
 
     if procs <= 1:
-        done, secs = time_oracle_queries(U, lam, eta, ys, alpha, budget_s, topk)
+        done, secs = time_oracle_queries(U, lam, eta, ys, alpha, budget_s, topk, ref)
         return done, secs, 1
-    _POOL_STATE.update(U=U, lam=lam, eta=eta, ys=ys, alpha=alpha)
+    _POOL_STATE.update(U=U, lam=lam, eta=eta, ys=ys, alpha=alpha, ref=ref)
     per = max(1, len(ys) // procs)
     chunks = [(i * per, (i + 1) * per if i < procs - 1 else len(ys), budget_s, topk) for i in range(procs)]
     chunks = [c for c in chunks if c[1] > c[0]]
@@ -221,6 +276,11 @@ def parallel_oracle_qps(U, lam, eta, ys, alpha, budget_s, topk, procs):
     return sum(d for d, _ in res), wall, len(chunks)
 
 
+def cpu_kind(ref):
+    return ("reference (stock specrank.ranking.filter + rank from baseline/_ref)" if ref is not None
+            else "port (oracle/fsr_oracle.py restatement; baseline/_ref absent)")
+
+
 def run_reference(args, cfg, n, rank, world):
     if rank != 0:
         return
@@ -228,28 +288,137 @@ def run_reference(args, cfg, n, rank, world):
     density = args.density if args.density is not None else cfg.density
     tau = int(round(density * n * r))
     U, lam, eta = synthetic_sparse_decomposition(n, r, tau)
+    ref = load_reference()
     procs = max(1, min(os.cpu_count() or 1, args.cpu_procs))
     # one step = one query per process, all processes in parallel (the reference has no batch API)
     ys = synthetic_queries(n, max((args.steps + args.warmup) * procs, 4), cfg.y_top)
-    time_oracle_queries(U, lam, eta, ys[:args.warmup], cfg.alpha, 1e9, args.topk)  # warm-up, untimed
-    done, secs, procs = parallel_oracle_qps(U, lam, eta, ys[args.warmup * procs:], cfg.alpha, 1e9, args.topk, procs)
+    time_oracle_queries(U, lam, eta, ys[:args.warmup], cfg.alpha, 1e9, args.topk, ref)  # warm-up, untimed
+    done, secs, procs = parallel_oracle_qps(U, lam, eta, ys[args.warmup * procs:], cfg.alpha, 1e9, args.topk, procs,
+                                            ref)
     qps = done / secs
     cores = procs
+    kind = "reference" if ref is not None else "port"
     line = {
         "metric": METRIC, "value": qps, "unit": "queries/s", "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * secs / max(args.steps, 1), "queries": done,
         "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
-        "config": {"workload": f"{cfg.name}/C5 online: oracle port of ranking.filter + rank on a synthetic "
-                               f"U~ with n={n}, r={r}, tau={tau} (density {density}), k={cfg.y_top}-sparse y, "
-                               f"h_alpha({cfg.alpha}), top-{args.topk}",
+        "config": {"workload": f"{cfg.name}/C5 online: {cpu_kind(ref)} on a synthetic U~ with n={n}, r={r}, "
+                               f"tau={tau} (density {density}), k={cfg.y_top}-sparse y, h_alpha({cfg.alpha}), "
+                               f"top-{args.topk}",
                    "step": f"one query per process on {cores} processes (reference has no batch API)"},
-        "cpu_baseline": {"value": qps, "unit": "queries/s", "cores": cores, "kind": "port",
+        "cpu_baseline": {"value": qps, "unit": "queries/s", "cores": cores, "kind": kind,
                          "sample": f"{done} queries, {secs:.1f} s wall, {cores} forked processes x scipy "
-                                   f"csr_matvec (single-threaded each)"},
+                                   f"csr_matvec (single-threaded each)" +
+                                   (f"; specrank imported from {ref['path']}" if ref else "")},
         "e2e": {"value": qps, "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def offline_cpu_baseline(S, n, r, r_hat, q, tau, panel_cols=256, panel_rows=16384, sort_rows=2048):
+    """The reference's offline path timed per operation on this host's cores
+    and extrapolated to the full config (the full CPU run is
+    infeasible at C3 -- fp64 n x r_hat = 44 GB per array, QR hours).  Each
+    timed call is the reference's own numpy/scipy call on a sample:
+      SpMM  ``A.csr @ Q`` (spectral.py:170 -> sparsemat.py:63-64) on all n
+            rows x ``panel_cols`` columns; scales with nnz * r_hat;
+      QR    ``np.linalg.qr(block)`` (spectral.py:165) on ``panel_rows`` x r_hat;
+            scales with the Householder count 4 m r_hat^2 - 4/3 r_hat^3
+            (geqrf + orgqr);
+      QtB   ``basis.Q.T @ basis.B`` (spectral.py:186) on panel_rows rows; linear in n;
+      eigh  ``np.linalg.eigh(C)`` (spectral.py:188) on the full r_hat x r_hat: measured, no extrapolation;
+      QV    ``basis.Q @ vecs`` (spectral.py:190) on panel_rows rows; linear in n;
+      sparsify ``np.lexsort`` of the (-|u|, row, col) keys (spectral.py:281) on
+            panel_rows x r entries; scales with N log N, N = n r.
+    The orthogonality check after each QR (spectral.py:166-167, a Gram of Q)
+    is counted as one more Q^T B-sized GEMM per round."""
+    import scipy.sparse as sp
+
+    ncpu = os.cpu_count() or 1
+    t = {}
+    A = sp.csr_matrix(S.csr, dtype=np.float64)
+    rng = np.random.default_rng(0)
+    Q = rng.standard_normal((n, panel_cols))
+    t0 = time.perf_counter()
+    A @ Q
+    t["spmm_panel_s"] = time.perf_counter() - t0
+    del Q
+    m = min(panel_rows, n)
+    P = rng.standard_normal((m, r_hat))
+    t0 = time.perf_counter()
+    np.linalg.qr(P)
+    t["qr_panel_s"] = time.perf_counter() - t0
+    P2 = rng.standard_normal((m, r_hat))
+    t0 = time.perf_counter()
+    P.T @ P2
+    t["qtb_panel_s"] = time.perf_counter() - t0
+    V = rng.standard_normal((r_hat, r))
+    t0 = time.perf_counter()
+    P @ V
+    t["qv_panel_s"] = time.perf_counter() - t0
+    del P2, V
+    C = P.T @ P / m
+    t0 = time.perf_counter()
+    np.linalg.eigh(C)
+    t["eigh_s"] = time.perf_counter() - t0
+    del P, C
+    ms = min(sort_rows, n)
+    N_s = ms * r
+    u = rng.standard_normal(N_s)
+    rows = np.repeat(np.arange(ms), r)
+    cols = np.tile(np.arange(r), ms)
+    t0 = time.perf_counter()
+    np.lexsort((cols, rows, -np.abs(u)))
+    t["lexsort_panel_s"] = time.perf_counter() - t0
+    del u, rows, cols
+
+    def hh(rows_):
+        return 4.0 * rows_ * r_hat ** 2 - 4.0 / 3.0 * r_hat ** 3
+
+    spmm_s = t["spmm_panel_s"] * r_hat / panel_cols
+    qr_s = t["qr_panel_s"] * hh(n) / hh(m)
+    qtb_s = t["qtb_panel_s"] * n / m
+    qv_s = t["qv_panel_s"] * n / m
+    N = n * r
+    sparsify_s = t["lexsort_panel_s"] * (N * math.log(N)) / (N_s * math.log(N_s))
+    si_s = q * (qr_s + qtb_s + spmm_s)
+    rr_s = qtb_s + t["eigh_s"] + qv_s
+    spmm_bytes = A.nnz * 12 + (n + 1) * 4 + 2 * 8 * n * r_hat
+    return {"kind": "extrapolated", "cores": ncpu,
+            "threads": {"openblas": os.environ.get("OPENBLAS_NUM_THREADS", f"default ({ncpu})"),
+                        "scipy_spmm": 1},
+            "sample": f"reference calls on samples: A.csr @ Q[:, :{panel_cols}] (all {n} rows, nnz={A.nnz}); "
+                      f"np.linalg.qr / Q^T B / Q V on {m} x {r_hat} row panels; eigh on the full {r_hat}^2; "
+                      f"lexsort on {ms} x {r} entries",
+            "measured_s": t,
+            "si_time_s": si_s, "rayleigh_ritz_s": rr_s, "sparsify_s": sparsify_s,
+            "decompose_total_s": si_s + rr_s + sparsify_s,
+            "spmm_s_per_iter": spmm_s, "spmm_gbs": spmm_bytes / spmm_s / 1e9,
+            "qr_s_per_iter": qr_s,
+            "model": "SpMM x r_hat/panel_cols; QR x (4 n r_hat^2 - 4/3 r_hat^3)/(same at m rows); GEMMs x n/m; "
+                     "sparsify x N log N; SI = q (QR + orthogonality Gram + SpMM)"}
+
+
+def offline_cpu_full(S, r, p, q, tau):
+    """The stock reference ``decompose`` + ``sparsify`` timed once in full
+    (feasible at C2: n = 1e5).  Needs baseline/_ref."""
+    import scipy.sparse as sp
+
+    ref = load_reference()
+    if ref is None:
+        return None
+    from specrank.sparsemat import SparseSymmetricMatrix as RefSSM
+
+    A = RefSSM(sp.csr_matrix(S.csr, dtype=np.float64))
+    t0 = time.perf_counter()
+    dec = ref["spectral"].decompose(A, r, p=p, q=q, seed=0)
+    t1 = time.perf_counter()
+    ref["spectral"].sparsify(dec, tau)
+    t2 = time.perf_counter()
+    return {"kind": "reference", "cores": os.cpu_count() or 1, "decompose_s": t1 - t0, "sparsify_s": t2 - t1,
+            "decompose_total_s": t2 - t0,
+            "sample": "full stock specrank.spectral.decompose + sparsify on this config's W (fp64)"}
 
 
 # ---------------------------------------------------------------------------
@@ -759,13 +928,32 @@ def run_fsr(args, cfg, n, rank, world, local_rank):
         ys = [(all_queries.y_idx[all_queries.y_ptr[j]:all_queries.y_ptr[j + 1]],
                all_queries.y_val[all_queries.y_ptr[j]:all_queries.y_ptr[j + 1]])
               for j in range(min(all_queries.b, 8 * procs))]
+        ref = load_reference()
         done, secs, procs = parallel_oracle_qps(Uh, sdec.eigenvalues, eta, ys, cfg.alpha, args.cpu_seconds, K,
-                                                procs)
+                                                procs, ref)
         if parity is not None:
             parity["online"] = online_parity(sdec, Uh, eta, all_queries, cfg.alpha, K, device)
-        cpu = {"value": done / secs, "unit": "queries/s", "cores": procs, "kind": "port",
-               "sample": f"{done} queries of this workload on the GPU-produced U~ (scipy CSR f64), oracle filter + "
-                         f"rank, {procs} forked processes, {secs:.1f} s wall"}
+        cpu = {"value": done / secs, "unit": "queries/s", "cores": procs, "kind": "reference" if ref else "port",
+               "sample": f"{done} queries of this workload on the GPU-produced U~ (scipy CSR f64), "
+                         f"{cpu_kind(ref)}, {procs} forked processes, {secs:.1f} s wall"}
+
+    # offline half of the metric: the reference's offline path on this host,
+    # per operation and extrapolated (C3), or in full at C2 (rank 0, N=1)
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            ocpu = offline_cpu_baseline(S, n, r, r_hat, q, tau)
+            for k in ("si_time_s", "rayleigh_ritz_s", "sparsify_s", "decompose_total_s"):
+                ocpu["speedup_" + k[:-2]] = ocpu[k] / max(offline[k], 1e-12)
+            ocpu["speedup_spmm_per_iter"] = ocpu["spmm_s_per_iter"] / max(offline["spmm_ms_per_iter"] / 1e3, 1e-12)
+            if args.offline_cpu_full or (args.offline_cpu_full is None and cfg.name in ("C1", "C2")):
+                full = offline_cpu_full(S, r, r_hat - r, q, tau)
+                if full is not None:
+                    full["speedup_decompose_total"] = full["decompose_total_s"] / max(offline["decompose_total_s"],
+                                                                                      1e-12)
+                ocpu["full_run"] = full
+        except Exception as exc:  # a host that cannot hold the samples must not lose the GPU line
+            ocpu = {"error": f"{type(exc).__name__}: {exc}"}
+        offline["cpu_baseline"] = ocpu
 
     if rank != 0:
         return

@@ -8,7 +8,10 @@
 #include <cstdarg>
 #include <cstdint>
 #include <cstdio>
+#include <map>
+#include <mutex>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "../../include/fsr.h"
@@ -141,6 +144,26 @@ inline int host_stage(fsr_ctx* ctx, size_t bytes, void** out) {
   }
   *out = ctx->host_stage;
   return FSR_OK;
+}
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) applies to the CURRENT
+// device only, so the "already configured" state is kept per (kernel, device):
+// a process driving two GPUs (one fsr_ctx each) configures each of them.
+inline int ensure_smem(fsr_ctx* ctx, const void* kernel, size_t bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, size_t> done;
+  std::lock_guard<std::mutex> lock(mu);
+  size_t& have = done[{kernel, ctx->device}];
+  if (have >= bytes) return FSR_OK;
+  const cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e != cudaSuccess) return cuda_status(ctx, e, "cudaFuncSetAttribute(MaxDynamicSharedMemorySize)");
+  have = bytes;
+  return FSR_OK;
+}
+
+template <typename K>
+inline int ensure_smem(fsr_ctx* ctx, K* kernel, size_t bytes) {
+  return ensure_smem(ctx, reinterpret_cast<const void*>(kernel), bytes);
 }
 
 inline size_t dtype_size(int dtype) { return dtype == FSR_F64 ? 8 : 4; }

@@ -203,12 +203,7 @@ int launch_project(fsr_ctx* ctx, int64_t r, int64_t b, int u_sparse, const int64
   const size_t psmem = ((size_t)r * sizeof(T) + 15) / 16 * 16 + (size_t)kProjCap * (sizeof(T) + 4);
   if (fused) *fused = u_sparse && psmem <= 160 * 1024;
   if (u_sparse && psmem <= 160 * 1024) {
-    static size_t configured[2] = {0, 0};
-    if (configured[sizeof(T) == 8] < psmem) {
-      FSR_CUDA(ctx, cudaFuncSetAttribute(project_smem_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)psmem));
-      configured[sizeof(T) == 8] = psmem;
-    }
+    FSR_TRY(fsr::ensure_smem(ctx, project_smem_kernel<T>, psmem));
     project_smem_kernel<T><<<(unsigned)b, 256, psmem, ctx->stream>>>(r, b, u_indptr, u_indices, u_values, w, y_ptr,
                                                                      y_idx, y_val, Zt, Zs, Zh, qp, nflag);
   } else if (u_sparse)
@@ -228,11 +223,7 @@ int launch_k9h(fsr_ctx* ctx, int64_t n, const int64_t* u_indptr, const int32_t* 
   namespace P = fsr::prune;
   auto kern = P::spmm_T_half_kernel<NV, DEPTH, ROWS, MINB, WARPS>;
   const size_t smem = (size_t)ROWS * (256 * NV + 1) * 4;
-  static bool configured = false;
-  if (!configured) {
-    FSR_CUDA(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    configured = true;
-  }
+  FSR_TRY(fsr::ensure_smem(ctx, kern, smem));
   dim3 grid((unsigned)fsr::ceil_div(n, ROWS), (unsigned)fsr::ceil_div(b, 256 * NV));
   kern<<<grid, 32 * WARPS, smem, ctx->stream>>>(n, u_indptr, u_indices, u_values, b, Zh, b, qp, Xt, n, cb, cmax_bits);
   return fsr::launched(ctx, "spmm_T_half_kernel");
@@ -288,10 +279,9 @@ int filter_pruned(fsr_ctx* ctx, int64_t n, int64_t r, const int64_t* u_indptr, c
   {
     fsr::StageTimer timer(ctx, FSR_STAGE_TOPK);
     const size_t fsmem = (size_t)fsr::topk::kCap * 16;
-    static int per_sm = 0;
+    FSR_TRY(fsr::ensure_smem(ctx, P::fallback_select_kernel, fsmem));
+    static int per_sm = 0;  // occupancy of a smem-free kernel: the same on every B200
     if (!per_sm) {
-      FSR_CUDA(ctx, cudaFuncSetAttribute(P::fallback_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)fsmem));
       FSR_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, P::prune_threshold_kernel, P::kThreads, 0));
       per_sm = std::max(per_sm, 1);
     }

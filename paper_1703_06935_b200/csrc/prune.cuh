@@ -33,6 +33,8 @@
 
 #include <cuda_fp16.h>
 
+#include <cfloat>
+
 
 #include "spmm.cuh"
 #include "topk.cuh"
@@ -51,6 +53,10 @@ __device__ __forceinline__ void query_scale(float amax, double ss, float* s, flo
   *s = 1.f;
   *inv = 1.f;
   *zb = 0.f;
+  if (!(amax <= FLT_MAX) || !(ss <= DBL_MAX)) {  // inf / NaN in zs: no bound, exact fallback
+    *zb = __int_as_float(0x7fffffff);
+    return;
+  }
   if (amax > 0.f) {
     int e;
     frexpf(amax, &e);  // amax = f 2^e, f in [0.5, 1)
@@ -497,6 +503,13 @@ __global__ void __launch_bounds__(kThreads) prune_threshold_kernel(int64_t n, in
       }
       continue;
     }
+    if (!(zb <= FLT_MAX)) {  // non-finite zs: no bound; exact recompute + select (as the unpruned path)
+      if (!threadIdx.x) {
+        ccount[q] = -1;
+        flags[atomicAdd(nflag, 1)] = (int)q;
+      }
+      continue;
+    }
     const bool vec_ok = ((((uintptr_t)xr) | ((uintptr_t)cb)) & 15) == 0;
     // 1. sampled threshold on the lower keys
     uint32_t prefix = 0;
@@ -675,7 +688,11 @@ __global__ void __launch_bounds__(kThreads) prune_finish_kernel(
   topk::bitonic_sort(ckey, cidx, (int)keep);
   for (int64_t m = threadIdx.x; m < K; m += blockDim.x) {
     out_idx[q * K + m] = cidx[m];
-    out_val[q * K + m] = key_to_float(ckey[m]);
+    float v = key_to_float(ckey[m]);
+    // the key folds -0 onto +0 (they tie); return the score's own bits, as the
+    // unpruned path does (the thread-sequential sum is bitwise the group's)
+    if (v == 0.f) v = exact_score(cidx[m], q, xr, indptr, indices, vals, Zs, ldz, eta, copy, y_ptr, y_idx);
+    out_val[q * K + m] = v;
   }
 }
 

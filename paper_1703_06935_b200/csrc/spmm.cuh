@@ -484,11 +484,7 @@ template <typename T>
 int launch_spmv_smem(fsr_ctx* ctx, int64_t n_rows, const int64_t* indptr, const int32_t* indices, const T* vals,
                      const T* x, int64_t x_len, T* y) {
   const size_t smem = (size_t)x_len * sizeof(T);
-  static size_t configured[2] = {0, 0};
-  if (configured[sizeof(T) == 8] < smem) {
-    FSR_CUDA(ctx, cudaFuncSetAttribute(spmv_smem_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    configured[sizeof(T) == 8] = smem;
-  }
+  FSR_TRY(fsr::ensure_smem(ctx, spmv_smem_kernel<T>, smem));
   // full occupancy (8 blocks x 8 warps per SM); each block re-stages x (L2 hits)
   const int grid = (int)std::min<int64_t>(ceil_div(n_rows * 32, 256), (int64_t)ctx->num_sms * 8);
   spmv_smem_kernel<T><<<grid, 256, smem, ctx->stream>>>(n_rows, indptr, indices, vals, x, x_len, y);
@@ -500,12 +496,7 @@ int launch_rowpanel_T(fsr_ctx* ctx, int64_t n_rows, const int64_t* indptr, const
                       int64_t ncols, const T* X, int64_t ldx, T* Yt, int64_t ldy) {
   constexpr int PW = 32 * VEC * NV;
   const size_t smem = (size_t)ROWS * (PW + 1) * sizeof(T);
-  static bool configured = false;
-  if (!configured) {
-    FSR_CUDA(ctx, cudaFuncSetAttribute(spmm_rowpanel_T_kernel<T, VEC, NV, kGatherDepth, ROWS>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    configured = true;
-  }
+  FSR_TRY(fsr::ensure_smem(ctx, spmm_rowpanel_T_kernel<T, VEC, NV, kGatherDepth, ROWS>, smem));
   dim3 grid((unsigned)ceil_div(n_rows, ROWS), (unsigned)ceil_div(ncols, PW));
   spmm_rowpanel_T_kernel<T, VEC, NV, kGatherDepth, ROWS><<<grid, 256, smem, ctx->stream>>>(
       n_rows, indptr, indices, vals, ncols, X, ldx, Yt, ldy);

@@ -535,11 +535,6 @@ int make_map_u8(fsr_ctx* ctx, CUtensorMap* m, const void* base, int64_t rows, in
 
 inline int64_t pad_to(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
 
-template <typename K>
-int set_smem(fsr_ctx* ctx, K kernel, int bytes) {
-  FSR_CUDA(ctx, cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-  return FSR_OK;
-}
 
 constexpr size_t kChunkBudget = (size_t)6 << 30;  // bytes of slice staging per row chunk
 
@@ -567,11 +562,7 @@ int launch_oz(fsr_ctx* ctx, dim3 grid, const CUtensorMap& mA, const CUtensorMap&
   constexpr int N = Variant<LEVELS, BPL, BK>::N, STAGES = Variant<LEVELS, BPL, BK>::STAGES;
   constexpr bool kWide = LEVELS == 4 && BPL == 4;
   using Cfg = OzCfg<N, STAGES, LEVELS, BPL, BK>;
-  static bool attr = false;
-  if (!attr) {
-    FSR_TRY(set_smem(ctx, oz_gemm_kernel<MODE, N, STAGES, LEVELS, BPL, kWide, BK>, Cfg::SMEM));
-    attr = true;
-  }
+  FSR_TRY(fsr::ensure_smem(ctx, oz_gemm_kernel<MODE, N, STAGES, LEVELS, BPL, kWide, BK>, Cfg::SMEM));
   // 16-byte epilogue stores need 16-byte aligned rows
   const int vec_out = MODE == 0 ? (rowsB % 2 == 0 && ((uintptr_t)P & 15) == 0)
                                 : (ldo % 4 == 0 && ((uintptr_t)Out & 15) == 0);

@@ -360,15 +360,8 @@ __global__ void __launch_bounds__(kThreads) select_kernel(const T* __restrict__ 
 template <typename T>
 int launch(fsr_ctx* ctx, int64_t b, int64_t n, const T* X, int64_t ldx, int64_t K, int64_t* top_idx, T* top_val) {
   const size_t smem = (size_t)kCap * 16;
-  static bool configured[2][2] = {{false, false}, {false, false}};
-  const int ti = sizeof(T) == 8;
-  if (!configured[ti][0]) {
-    FSR_CUDA(ctx, cudaFuncSetAttribute(select_kernel<T, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)smem));
-    FSR_CUDA(ctx, cudaFuncSetAttribute(select_kernel<T, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)smem));
-    configured[ti][0] = configured[ti][1] = true;
-  }
+  FSR_TRY(ensure_smem(ctx, select_kernel<T, false>, smem));
+  FSR_TRY(ensure_smem(ctx, select_kernel<T, true>, smem));
   int segs = 1;
   if (b < ctx->num_sms) {
     segs = (int)std::min<int64_t>(ceil_div(2 * ctx->num_sms, b), std::max<int64_t>(1, n / (8 * K)));

@@ -668,8 +668,13 @@ class FilterGraph:
     only refreshes the pinned staging buffers and replays it, so a query
     batch costs one graph launch instead of ~6 kernel launches and the
     Python/ctypes work between them.  Batches smaller than ``b`` are padded
-    with empty queries.  Results are identical to ``filter_device`` (same
-    kernels, same arguments).
+    with empty queries.  Results are identical to ``filter_device`` called
+    with a batch of the graph's capacity ``b`` (same kernels, same
+    arguments); the kernel path is chosen by ``b``, so a partial batch run
+    eagerly through ``filter_device`` with fewer queries may take a
+    different K9 variant (e.g. the narrow b <= 64 kernel, which sums a row
+    in two interleaved halves) and differ in the last bits of ``top_val``
+    and in the order of near-ties.
     """
 
     def __init__(self, dec: SpectralDecomposition, h: TransferFunction, b: int, nnz_cap: int, topk: int = 100,
@@ -770,9 +775,11 @@ class FilterGraph:
         self._nb = batch.b
 
     def fetch(self):
-        """Wait for the last ``submit`` and return host (top_idx, top_val) of its queries."""
+        """Wait for the last ``submit`` and return host (top_idx, top_val) of its
+        queries as fresh arrays (the pinned buffers are overwritten by the
+        next ``submit`` on this graph)."""
         self._fetched.synchronize()
-        return self._h_idx[: self._nb].numpy(), self._h_val[: self._nb].numpy()
+        return self._h_idx[: self._nb].numpy().copy(), self._h_val[: self._nb].numpy().copy()
 
 
 def torch_from_numpy_cast(a, dtype):

@@ -248,6 +248,91 @@ def c2_reduced_case(n: int = 20_000, queries: int = 50, r: int = 400, p: int = 4
     )
 
 
+def weight_digest(data: np.ndarray) -> np.ndarray:
+    """Size-independent digest of a CSR value array in its stored order:
+    [sum, sum of squares, sum weighted by seeded U(0,1) coefficients, max].
+    Two arrays whose entries agree to 1e-12 relative agree to ~1e-12 here;
+    a single wrong entry moves the weighted sum."""
+    c = np.random.default_rng(99).random(data.size)
+    return np.array([data.sum(), np.dot(data, data), np.dot(data, c), data.max() if data.size else 0.0])
+
+
+def pattern_hash(indptr: np.ndarray, indices: np.ndarray) -> str:
+    h = hashlib.sha256(np.ascontiguousarray(indptr, dtype=np.int64).tobytes())
+    h.update(np.ascontiguousarray(indices, dtype=np.int32).tobytes())
+    return h.hexdigest()
+
+
+def c2_full_case(n_x: int = 4, top: int = 100):
+    """BASELINE C2 at full size (n=1e5, d=512, 1000 Zipf clusters, k=50,
+    gamma=3, r=2000, p=200, q=3, tau=5% = 1e7, 1000 queries, y top-50,
+    h_alpha(0.99)), run through the reference.  Only outputs are stored (no
+    W: 2.7e6 fp64 weights); the GPU test regenerates W from the seeded
+    descriptors with the fp64 device builder and checks it against
+    ``W_pattern_hash`` / ``W_digest``.  Also records the reference's own
+    stage timings in this container (8 cores, OpenBLAS)."""
+    cfg = CONFIGS["C2"]
+    tm = {}
+    t0 = time.perf_counter()
+    data, qv, _ = cluster_descriptors(cfg)
+    ds = DescriptorSet(data)
+    W = graph.build_mutual_knn_graph(ds, cfg.k, cfg.gamma)
+    S = graph.normalize_adjacency(W, graph.degrees(W))
+    tm["graph"] = time.perf_counter() - t0
+    t = time.perf_counter()
+    basis = spectral.range_finder(S, cfg.r_hat, cfg.q, 0)
+    tm["range_finder"] = time.perf_counter() - t
+    t = time.perf_counter()
+    dec = spectral.approx_eigendecomposition(S, basis, cfg.r)
+    tm["approx_eig"] = time.perf_counter() - t
+    del basis
+    t = time.perf_counter()
+    sdec = spectral.sparsify(dec, cfg.tau)
+    tm["sparsify"] = time.perf_counter() - t
+    h = ranking.h_alpha(cfg.alpha)
+    t = time.perf_counter()
+    ys = [ranking.observation_vector(q, ds, cfg.y_top, cfg.gamma) for q in qv]
+    tm["observation_vectors"] = time.perf_counter() - t
+    y_ptr = np.zeros(len(ys) + 1, dtype=np.int64)
+    y_ptr[1:] = np.cumsum([y.nnz for y in ys])
+    xa, xs, ta, ts, va, vs = [], [], [], [], [], []
+    tf = [0.0, 0.0]
+    for j, y in enumerate(ys):
+        t = time.perf_counter()
+        x = ranking.filter(dec, h, y)
+        tf[0] += time.perf_counter() - t
+        t = time.perf_counter()
+        x2 = ranking.filter(sdec, h, y)
+        tf[1] += time.perf_counter() - t
+        oa, os_ = ranking.rank(x)[:top + 1], ranking.rank(x2)[:top + 1]
+        ta.append(oa[:top])
+        ts.append(os_[:top])
+        va.append(x[oa])
+        vs.append(x2[os_])
+        if j < n_x:
+            xa.append(x)
+            xs.append(x2)
+    tm["filter_dense_per_query"] = tf[0] / len(ys)
+    tm["filter_sparse_per_query"] = tf[1] / len(ys)
+    flat = csr_support(sdec.U)
+    print(f"C2: {tm} nnz(W)={W.nnz}")
+    np.savez_compressed(
+        os.path.join(HERE, "c2.npz"),
+        W_nnz=np.array(W.nnz), W_pattern_hash=np.array(pattern_hash(W.csr.indptr, W.csr.indices)),
+        W_digest=weight_digest(W.csr.data), S_digest=weight_digest(S.csr.data),
+        lam=dec.eigenvalues, eta=dec.eta, sparse_eta=sdec.eta,
+        U_colsum_abs=np.abs(dec.U).sum(axis=0),
+        sparse_nnz=np.array(sdec.U.nnz), sparse_hash=np.array(support_hash(flat)),
+        y_ptr=y_ptr, y_idx=np.concatenate([y.indices for y in ys]), y_val=np.concatenate([y.values for y in ys]),
+        x_approx=np.array(xa), x_sparse=np.array(xs),
+        top_approx=np.array(ta, dtype=np.int32), top_sparse=np.array(ts, dtype=np.int32),
+        topval_approx=np.array(va), topval_sparse=np.array(vs),
+        params=np.array([cfg.n, cfg.r, cfg.p, cfg.q, cfg.tau, 0]), alpha=np.array(cfg.alpha),
+        timings_keys=np.array(list(tm.keys())), timings=np.array(list(tm.values())),
+        host=np.array(f"{os.cpu_count()} cores, numpy {np.__version__}"),
+    )
+
+
 def c4_reduced_case(n_x: int = 5):
     """C4's regional generator (images x 5 regions, sigma=0.05, d=512, k=50,
     gamma=3, tau=2%) at 4000 images (n = 20k), r=400, p=40, q=3; queries pool
@@ -368,4 +453,6 @@ if __name__ == "__main__":
         c2_reduced_case()
     if "c4r" in which:
         c4_reduced_case()
+    if "c2" in which:  # full BASELINE C2: ~25 min on 8 cores, run explicitly
+        c2_full_case()
     print("ok")

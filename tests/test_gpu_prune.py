@@ -148,3 +148,45 @@ def test_filter_graph_partial_batch_on_pruned_path():
         ctx.set_topk_prune(True)
     np.testing.assert_array_equal(gi, r_.top_idx.cpu().numpy())
     np.testing.assert_array_equal(gv.view(np.uint32), r_.top_val.cpu().numpy().view(np.uint32))
+
+
+def test_pruned_nonfinite_projection_matches_unpruned():
+    """A query whose projection overflows fp32 (y values of 1e300 -> inf in the
+    fp32 batch) has no finite bound: the pruned path must hand it to the exact
+    fallback and return what the unpruned path returns (a NaN
+    bound used to sort above +inf and pick wrong rows)."""
+    n, r, b = 140_000, 300, 256
+    _, dec = make_dec(n, r, 20, 31)
+    qb = queries(n, b, 32)
+    y_val = qb.y_val.copy()
+    for j in (3, 70):
+        s, e = qb.y_ptr[j], qb.y_ptr[j + 1]
+        y_val[s:s + 3] = 1e300
+    qb = ranking.QueryBatch(n, qb.y_ptr, qb.y_idx, y_val)
+    fl = []
+    (pi, pv), (ui, uv) = both(dec, qb, flags=fl)
+    assert fl[0] >= 2
+    np.testing.assert_array_equal(pi, ui)
+    np.testing.assert_array_equal(pv.view(np.uint32), uv.view(np.uint32))
+    ok = [j for j in range(b) if j not in (3, 70)]
+    assert np.isfinite(pv[ok]).all()
+
+
+@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs two GPUs in one process")
+def test_two_devices_one_process():
+    """Kernel shared-memory attributes are per device: the pruned
+    step (64 KB fallback select, large-smem K8) runs on a second device of the
+    same process after the first."""
+    n, r, b = 140_000, 300, 256
+    host, _ = make_dec(n, r, 20, 41)
+    qb = queries(n, b, 42)
+    res = []
+    for d in (0, 1):
+        with torch.cuda.device(d):
+            dec = spectral.SpectralDecomposition.from_host(host, dtype="float32", device=torch.device("cuda", d))
+            dq = ranking.DeviceQueries(qb, dec.dtype, torch.device("cuda", d))
+            r_ = ranking.filter_device(dec, ranking.h_alpha(0.99), dq, topk=100, want_x=False)
+            torch.cuda.synchronize(d)
+            res.append((r_.top_idx.cpu().numpy(), r_.top_val.cpu().numpy()))
+    np.testing.assert_array_equal(res[0][0], res[1][0])
+    np.testing.assert_array_equal(res[0][1].view(np.uint32), res[1][1].view(np.uint32))
