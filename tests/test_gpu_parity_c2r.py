@@ -63,10 +63,13 @@ def test_c2r_ranking(c2r, decs):
     xa = g["x_approx"]
     assert max(rel_l2(X[j], xa[j]) for j in range(xa.shape[0])) <= tol
     ov = [overlap(ranking.rank(X[j])[:100], g["top_approx"][j]) for j in range(batch.b)]
-    assert np.mean(ov) >= 0.99 and min(ov) >= 0.95
+    assert min(ov) >= 0.99, min(ov)  # per query, both dtypes
     Xs = ranking.filter_batch(sdec, h, batch)
     ovs = [overlap(ranking.rank(Xs[j])[:100], g["top_sparse"][j]) for j in range(batch.b)]
-    assert np.mean(ovs) >= 0.99
+    if dtype == "float64":
+        assert min(ovs) >= 0.99, min(ovs)
+    else:  # fp32 end to end: own top-tau support, tau-boundary flips expected
+        assert np.mean(ovs) >= 0.99, (np.mean(ovs), min(ovs))
     if dtype == "float64":
         coo = sdec.U.tocoo()
         flat = np.sort(coo.row.astype(np.int64) * P["r"] + coo.col)

@@ -87,7 +87,12 @@ def test_c4r_ritz_and_ranking(c4r, decs):
         ov = [overlap(ranking.rank(X[j])[:100], g[f"top_{name}"][j]) for j in range(batch.b)]
         oi = [overlap(ranking.RankingResult.from_scores(X[j], P).order[:100], g[f"img_top_{name}"][j])
               for j in range(batch.b)]
-        assert np.mean(ov) >= 0.99 and np.mean(oi) >= 0.99, (name, np.mean(ov), np.mean(oi))
+        if name == "approx" or dtype == "float64":
+            # the contract per query: every query's region and image top-100 overlap >= 99%
+            assert min(ov) >= 0.99 and min(oi) >= 0.99, (name, min(ov), min(oi))
+        else:
+            # fp32 SPARSE end to end: own top-tau support, tau-boundary flips expected
+            assert np.mean(ov) >= 0.99 and np.mean(oi) >= 0.99, (name, np.mean(ov), np.mean(oi), min(ov))
     if dtype == "float64":
         coo = sdec.U.tocoo()
         flat = np.sort(coo.row.astype(np.int64) * cfg.r + coo.col)
