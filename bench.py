@@ -82,9 +82,20 @@ def load_peaks():
         return 6650.0, "fallback"
 
 
-def load_profile(name):
+def load_tensor_peak():
+    """Dense fp16/bf16 tensor peak in TF/s: MEASURED_PEAKS.json's cuBLAS bf16
+    (burst; kind::f16 and kind::bf16 run at the same rate), else the
+    profiling recipe's fallback."""
+    try:
+        with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["bf16_tflops"]), "measured (cuBLAS bf16 burst)"
+    except Exception:
+        return 1600.0, "fallback"
+
+
+def load_profile(name, rnd=None):
     """A committed measurement summary under profiles/ (None when absent)."""
-    path = os.path.join(REPO, "profiles", PROFILE_ROUND, name)
+    path = os.path.join(REPO, "profiles", rnd or PROFILE_ROUND, name)
     try:
         with open(path) as f:
             return json.load(f)
@@ -92,7 +103,7 @@ def load_profile(name):
         return None
 
 
-PROFILE_ROUND = "r01"
+PROFILE_ROUND = "r02"
 FP32_LANES_PER_SM = 128  # FFMA lanes per SM (sm_100)
 
 
@@ -584,13 +595,16 @@ def online_sweep(dec, sdec_default, density_default, cfg, n, r, queries, device,
                     ms += e0.elapsed_time(e1)
                 k9_ms, k9_cnt = ctx.stage_time("filter_spmm")
                 kept = sd.U_device.nnz
-                pr = ranking.topk_pruned(n, b, 100, sd.dtype)
-                k9_bytes = kept * (es + 4) + (n + 1) * 8 + (2 if pr else es) * r * b + es * n * b
-                row = {"density": d, "b": b, "h": name, "k9_path": "pruned" if pr else "exact",
+                pth = ctx.last_online_path
+                k9_bytes = kept * (es + 4) + (n + 1) * 8 + (2 if pth == "pruned" else es) * r * b + es * n * b
+                row = {"density": d, "b": b, "h": name, "k9_path": pth,
                        "queries_per_s": b * nsteps / (ms / 1e3),
-                       "ms_per_batch": ms / nsteps, "k9_ms": k9_ms / max(k9_cnt, 1),
-                       "k9_algorithmic_gbs": k9_bytes / (k9_ms / max(k9_cnt, 1) * 1e-3) / 1e9,
-                       "k9_fp32_tflops": 2.0 * kept * b / (k9_ms / max(k9_cnt, 1) * 1e-3) / 1e12}
+                       "ms_per_batch": ms / nsteps, "k9_ms": k9_ms / max(k9_cnt, 1)}
+                if pth == "tc":
+                    row["k9t_dense_tflops"] = 2.0 * n * r * b / (k9_ms / max(k9_cnt, 1) * 1e-3) / 1e12
+                else:
+                    row["k9_algorithmic_gbs"] = k9_bytes / (k9_ms / max(k9_cnt, 1) * 1e-3) / 1e9
+                row["useful_fp32_tflops"] = 2.0 * kept * b / (k9_ms / max(k9_cnt, 1) * 1e-3) / 1e12
                 if b <= 64 and name == "h_alpha(0.99)":
                     row.update(graph_sweep_row(sd, h, qb, b, nsteps, warmup, flush, ctx))
                 out.append(row)
@@ -786,8 +800,11 @@ def run_fsr(args, cfg, n, rank, world, local_rank):
     K = args.topk
     res = ranking.FilterResult(top_idx=torch.empty(b, K, dtype=torch.int64, device=device),
                                top_val=torch.empty(b, K, dtype=sdec.dtype, device=device))
-    ws = torch.empty(int(ctx.lib.fsr_filter_workspace_bytes(N.dtype_code(sdec.dtype), n, r, b, 1)),
-                     dtype=torch.uint8, device=device)
+    ws = torch.empty(ranking.filter_workspace_bytes(sdec, b, want_x=False, topk=K), dtype=torch.uint8,
+                     device=device)
+    path = ranking.online_path(sdec, b, K, ctx)
+    if path == "tc":
+        ranking.dense_layout(sdec)  # built once per decomposition, outside the timed region
     flush = L2Flush(device)  # > L2 (126 MB)
 
     def step(i):
@@ -818,26 +835,26 @@ def run_fsr(args, cfg, n, rank, world, local_rank):
     dev_ms_max = max_over_ranks(dev_ms, world)
     value = world * b * args.steps / (dev_ms_max / 1e3)
 
-    # roofline of the dominant kernel: K9 (sparse U~ x Zs; the pruned path's
-    # K9h gathers Zs in fp16, 2 bytes per column)
-    pruned = ranking.topk_pruned(n, b, K, sdec.dtype)
-    zb_es = 2 if pruned else es
+    # roofline of the dominant kernel: the main K9t GEMM (tensor), or K9 / K9h
+    # (sparse U~ x Zs, HBM by the survey's count; K9h gathers Zs in fp16)
     k9_ms, k9_cnt = on_stages["filter_spmm"]
     k9_ms_launch = k9_ms / max(k9_cnt, 1)
     kept = sdec.U_device.nnz
-    k9_bytes = kept * (es + 4) + (n + 1) * 8 + zb_es * r * b + es * n * b
-    k9_gbs = k9_bytes / (k9_ms_launch * 1e-3) / 1e9
     k9_share = k9_ms / max(sum(v[0] for v in on_stages.values()), 1e-9)
-    # binding limbs: every nonzero of U~ gathers one b-wide row of Zs (L2-resident)
-    k9_gather = kept * b * zb_es
-    # pruned path: same top-k as the unpruned fp32 path, bit for bit (untimed check)
+    certified = path in ("tc", "pruned")
+    tc_stats = None
+    if path == "tc":
+        st2 = ranking.last_tc_stats(ws, sdec, b)
+        tc_stats = {"candidates_median": float(np.median(st2[:, 0])), "candidates_max": int(st2[:, 0].max()),
+                    "rescored_median": float(np.median(st2[:, 1])), "rescored_max": int(st2[:, 1].max())}
+    # certified paths: same top-k as the unpruned fp32 path, bit for bit (untimed check)
     prune_check = None
-    if pruned:
+    if certified:
         same, fallback = True, 0
         for dq in dqs:
             ranking.filter_device(sdec, h, dq, topk=K, want_x=False, out=res, workspace=ws)
             torch.cuda.synchronize()
-            fallback += ranking.pruned_fallback_count(ws, n, r, b)
+            fallback += ranking.last_fallback_count(ws, sdec, b, ctx)
             pi, pv = res.top_idx.clone(), res.top_val.clone()
             ctx.set_topk_prune(False)
             ranking.filter_device(sdec, h, dq, topk=K, want_x=False, out=res, workspace=ws)
@@ -860,15 +877,63 @@ def run_fsr(args, cfg, n, rank, world, local_rank):
             ums += e0.elapsed_time(e1)
         ctx.set_topk_prune(True)
         ums = max_over_ranks(ums, world)
-        prune_check = {"batches": len(dqs), "topk_identical_to_unpruned_fp32": same, "fallback_queries": fallback,
+        prune_check = {"path": path, "batches": len(dqs), "topk_identical_to_unpruned_fp32": same,
+                       "fallback_queries": fallback, "selection": tc_stats,
                        "unpruned_fp32": {"value": world * b * args.steps / (ums / 1e3), "unit": "queries/s",
                                          "ms_per_step": ums / args.steps}}
-    k9_gather_gbs = k9_gather / (k9_ms_launch * 1e-3) / 1e9
-    l2 = load_profile("l2_bw.json") or {}
-    l2_peak = l2.get("gather_1KB_rows_19MB_GBs")
-    ncu9 = load_profile("k9h_ncu_full.json" if pruned else "k9_ncu_full.json") or {}
-    k9_traffic = ncu9.get("dram_bytes_per_launch") if (cfg.name == "C3" and b == 1024 and es == 4
-                                                         and args.density is None) else None
+    profile_ok = cfg.name == "C3" and b == 1024 and es == 4 and args.density is None
+    if path == "tc":
+        tpeak, tpeak_kind = load_tensor_peak()
+        ldr = (r + 7) // 8 * 8
+        dense_flops = 2.0 * n * r * b
+        achieved = dense_flops / (k9_ms_launch * 1e-3) / 1e12
+        hbm_bytes = n * ldr * 2 + b * ldr * 2 + n * 4  # dense fp16 U~ once, fp16 Zh, c_i
+        ncu9 = load_profile("k9t_ncu_full.json") or {}
+        roofline = {
+            "kernel": "K9t main pass k9t_gemm_kernel<1> (tcgen05.mma kind::f16 M=128 N=256, TMA with B-tile "
+                      "multicast in 2-CTA clusters, double-buffered TMEM accumulators, fused certified selection)",
+            "bound": "tensor", "achieved": achieved, "peak": tpeak, "unit": "TFLOP/s", "frac": achieved / tpeak,
+            "peak_kind": tpeak_kind,
+            "traffic": ncu9.get("dram_bytes_per_launch") if profile_ok else None,
+            "traffic_source": "profiles/%s/k9t_ncu_full.json" % PROFILE_ROUND if (profile_ok and ncu9) else None,
+            "algorithmic_flops_per_launch": dense_flops,
+            "algorithmic_bytes_per_launch": hbm_bytes,
+            "ms_per_launch": k9_ms_launch, "share_of_step": k9_share,
+            "binding_limbs": {
+                "hbm": {"bytes_per_launch": hbm_bytes, "achieved_gbs": hbm_bytes / (k9_ms_launch * 1e-3) / 1e9,
+                        "peak_gbs": peak_gbs,
+                        "frac": hbm_bytes / (k9_ms_launch * 1e-3) / 1e9 / peak_gbs},
+                "useful_flops": {"flops_per_launch": 2.0 * kept * b,
+                                 "achieved_tflops": 2.0 * kept * b / (k9_ms_launch * 1e-3) / 1e12,
+                                 "note": "2 tau b: the products with a nonzero of U~ (the dense GEMM multiplies "
+                                         "the zeros too: n r / tau = %.0fx the work, at tensor-core rate)"
+                                         % (n * r / kept)},
+            }}
+    else:
+        zb_es = 2 if path == "pruned" else es
+        k9_bytes = kept * (es + 4) + (n + 1) * 8 + zb_es * r * b + es * n * b
+        k9_gbs = k9_bytes / (k9_ms_launch * 1e-3) / 1e9
+        k9_gather = kept * b * zb_es  # every nonzero of U~ gathers one b-wide row of Zs (L2-resident)
+        k9_gather_gbs = k9_gather / (k9_ms_launch * 1e-3) / 1e9
+        l2 = load_profile("l2_bw.json", "r01") or {}
+        l2_peak = l2.get("gather_1KB_rows_19MB_GBs")
+        ncu9 = load_profile("k9h_ncu_full.json" if path == "pruned" else "k9_ncu_full.json", "r01") or {}
+        sms_ = torch.cuda.get_device_properties(device).multi_processor_count
+        fp32_peak_ = 2.0 * sms_ * FP32_LANES_PER_SM * 1965.0 * 1e6 / 1e12
+        roofline = {
+            "kernel": ("K9h filter SpMM (spmm_T_half_kernel on U~ x fp16 Zs)" if path == "pruned" else
+                       "K9 filter SpMM (spmm_rowpanel_T_kernel on U~ x Zs)"), "bound": "hbm",
+            "achieved": k9_gbs, "peak": peak_gbs, "unit": "GB/s", "frac": k9_gbs / peak_gbs,
+            "peak_kind": peak_kind, "traffic": ncu9.get("dram_bytes_per_launch") if profile_ok else None,
+            "traffic_source": "profiles/r01/%s" % ("k9h_ncu_full.json" if path == "pruned" else "k9_ncu_full.json"),
+            "algorithmic_bytes_per_launch": k9_bytes, "ms_per_launch": k9_ms_launch, "share_of_step": k9_share,
+            "binding_limbs": {
+                "l2_gather": {"bytes_per_launch": k9_gather, "achieved_gbs": k9_gather_gbs, "peak_gbs": l2_peak,
+                              "frac": (k9_gather_gbs / l2_peak) if l2_peak else None,
+                              "peak_source": "tools/l2_bw.cu random 1 KB row gathers (profiles/r01/l2_bw.json)"},
+                "fp32_fma": {"achieved_tflops": 2.0 * kept * b / (k9_ms_launch * 1e-3) / 1e12,
+                             "peak_tflops": fp32_peak_,
+                             "frac": 2.0 * kept * b / (k9_ms_launch * 1e-3) / 1e12 / fp32_peak_}}}
 
     # ---------------- e2e through the public API with host buffers ----------
     # ranking.FilterGraph: host batch -> pinned staging -> one CUDA-graph launch
@@ -970,28 +1035,17 @@ def run_fsr(args, cfg, n, rank, world, local_rank):
                    "global_batch": b * world, "parallelism": (f"offline row-sharded x{world} (NCCL all-gather + ordered fp64 sums), online replicas (batch split)" if world > 1 else "single GPU"),
                    "l2": "256 MB buffer written, then a 256 MB buffer read, between timed steps (L2 flush "
                          "with write-back outside the timed region); U~ itself > L2"},
-        "online_path": ("certified pruned top-k: K9h gathers Zs rounded to fp16 (per-query power-of-two scale), "
-                        "a rigorous per-row bound selects the rows that can reach the top-k, those are re-scored "
-                        "exactly in fp32 in the unpruned kernel's order (csrc/prune.cuh)" if pruned else
-                        "unpruned fp32 K9 + exact top-k"),
+        "online_path": {
+            "tc": "K9t (csrc/k9t.cu): x~ = fp16 dense U~ x fp16 Zs on tcgen05 tensor cores (fp32 TMEM "
+                  "accumulation), a rigorous per-row bound selects the rows that can reach the top-k inside the "
+                  "GEMM epilogue (threshold from a 1/32 row-tile sample), those are re-scored exactly in fp32 in "
+                  "the unpruned kernel's order -- the unpruned fp32 top-k bit for bit",
+            "pruned": "certified pruned top-k: K9h gathers Zs rounded to fp16 (per-query power-of-two scale), "
+                      "a rigorous per-row bound selects the rows that can reach the top-k, those are re-scored "
+                      "exactly in fp32 in the unpruned kernel's order (csrc/prune.cuh)",
+            "exact": "unpruned fp32 K9 + exact top-k"}[path],
         "prune_check": prune_check,
-        "roofline": {"kernel": ("K9h filter SpMM (spmm_T_half_kernel on U~ x fp16 Zs)" if pruned else
-                                "K9 filter SpMM (spmm_rowpanel_T_kernel on U~ x Zs)"), "bound": "hbm",
-                     "achieved": k9_gbs, "peak": peak_gbs, "unit": "GB/s", "frac": k9_gbs / peak_gbs,
-                     "peak_kind": peak_kind, "traffic": k9_traffic,
-                     "traffic_source": ("profiles/%s/%s" % (PROFILE_ROUND, "k9h_ncu_full.json" if pruned else
-                                                            "k9_ncu_full.json")) if k9_traffic else None,
-                     "algorithmic_bytes_per_launch": k9_bytes,
-                     "ms_per_launch": k9_ms_launch, "share_of_step": k9_share,
-                     "binding_limbs": {
-                         "l2_gather": {"bytes_per_launch": k9_gather, "achieved_gbs": k9_gather_gbs,
-                                       "peak_gbs": l2_peak, "frac": (k9_gather_gbs / l2_peak) if l2_peak else None,
-                                       "peak_source": "tools/l2_bw.cu random 1 KB row gathers from a 19 MB "
-                                                      "matrix (profiles/%s/l2_bw.json)" % PROFILE_ROUND},
-                         "fp32_fma": {"achieved_tflops": 2.0 * kept * b / (k9_ms_launch * 1e-3) / 1e12,
-                                      "peak_tflops": fp32_peak,
-                                      "frac": 2.0 * kept * b / (k9_ms_launch * 1e-3) / 1e12 / fp32_peak},
-                     }},
+        "roofline": roofline,
         "online_stage_ms_per_step": {k: v[0] / args.steps for k, v in on_stages.items()},
         "offline": offline,
         "gpu_launches": launches,

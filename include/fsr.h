@@ -226,6 +226,33 @@ int fsr_filter_batch(fsr_ctx* ctx, int dtype, int64_t n, int64_t r, int u_sparse
                      int64_t b, const int64_t* y_ptr, const int64_t* y_idx, const void* y_val,
                      int copy_uncovered, void* workspace, void* X, int64_t topk,
                      int64_t* top_idx, void* top_val);
+/* ---- K9t: the ranked-query step on tensor cores (csrc/k9t.cu) ----------------
+ * Replaces, for a float32 sparse decomposition and top-k-only output, the
+ * per-query loop of ranking.py:229-255 (filter) + ranking.py:390-395 (rank)[:topk]
+ * for a whole batch: the same top_idx / top_val as fsr_filter_batch's unpruned
+ * fp32 path, bit for bit (certified bound + exact fp32 re-score).
+ * dense_u: a layout of fsr_dense_u_bytes(n, r) bytes (256-aligned) built once
+ * per U~ by fsr_dense_u_build (fp16 copy of U~, n x round_up(r, 8), zeros off
+ * the support, and the per-row bound factors).  workspace:
+ * fsr_filter_tc_workspace_bytes(n, r, b) bytes (256-aligned); its first int is
+ * the number of queries the call answered through the exact fallback
+ * (fsr_filter_tc_fallback_count).  Shapes: fsr_filter_tc_applicable. */
+int64_t fsr_dense_u_bytes(int64_t n, int64_t r);
+int fsr_dense_u_build(fsr_ctx* ctx, int64_t n, int64_t r, const int64_t* u_indptr,
+                      const int32_t* u_indices, const float* u_values, void* dense_u);
+int64_t fsr_filter_tc_workspace_bytes(int64_t n, int64_t r, int64_t b);
+int fsr_filter_tc_applicable(int64_t n, int64_t r, int64_t b, int64_t topk);
+int fsr_filter_topk_tc(fsr_ctx* ctx, int64_t n, int64_t r, const int64_t* u_indptr,
+                       const int32_t* u_indices, const float* u_values, const void* dense_u,
+                       const float* w, const double* eta, int64_t b, const int64_t* y_ptr,
+                       const int64_t* y_idx, const float* y_val, int copy_uncovered,
+                       void* workspace, int64_t topk, int64_t* top_idx, float* top_val);
+int fsr_filter_tc_fallback_count(fsr_ctx* ctx, const void* workspace, int* out);
+/* Diagnostics of the last call: per query (candidate rows, rows re-scored
+ * exactly), b int32 pairs to host memory (zeros for queries not finished by
+ * the certified selection). */
+int fsr_filter_tc_stats(fsr_ctx* ctx, int64_t n, int64_t r, int64_t b, const void* workspace, int32_t* out);
+
 /* Top-k of every row of X (b x n): indices/values ordered by (-x, index). */
 int fsr_topk_rows(fsr_ctx* ctx, int dtype, int64_t b, int64_t n, const void* X, int64_t ldx,
                   int64_t topk, int64_t* top_idx, void* top_val);

@@ -67,6 +67,14 @@ _SIGS = {
     "fsr_filter_workspace_bytes": (_c_i64, [_c_int, _c_i64, _c_i64, _c_i64, _c_int]),
     "fsr_filter_batch": (_c_int, [_c_p, _c_int, _c_i64, _c_i64, _c_int, _c_p, _c_p, _c_p, _c_p, _c_i64, _c_p, _c_p,
                                   _c_i64, _c_p, _c_p, _c_p, _c_int, _c_p, _c_p, _c_i64, _c_p, _c_p]),
+    "fsr_dense_u_bytes": (_c_i64, [_c_i64, _c_i64]),
+    "fsr_dense_u_build": (_c_int, [_c_p, _c_i64, _c_i64, _c_p, _c_p, _c_p, _c_p]),
+    "fsr_filter_tc_workspace_bytes": (_c_i64, [_c_i64, _c_i64, _c_i64]),
+    "fsr_filter_tc_applicable": (_c_int, [_c_i64, _c_i64, _c_i64, _c_i64]),
+    "fsr_filter_topk_tc": (_c_int, [_c_p, _c_i64, _c_i64, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_i64, _c_p, _c_p,
+                                    _c_p, _c_int, _c_p, _c_i64, _c_p, _c_p]),
+    "fsr_filter_tc_fallback_count": (_c_int, [_c_p, _c_p, ctypes.POINTER(_c_int)]),
+    "fsr_filter_tc_stats": (_c_int, [_c_p, _c_i64, _c_i64, _c_i64, _c_p, _c_p]),
     "fsr_topk_rows": (_c_int, [_c_p, _c_int, _c_i64, _c_i64, _c_p, _c_i64, _c_i64, _c_p, _c_p]),
     "fsr_project_batch": (_c_int, [_c_p, _c_int, _c_i64, _c_i64, _c_int, _c_p, _c_p, _c_p, _c_p, _c_i64, _c_p,
                                    _c_i64, _c_p, _c_p, _c_p, _c_p]),
@@ -163,6 +171,9 @@ class Context:
         self.handle = h
         self._stream = None
         self._timing = False
+        self.topk_prune = True          # certified paths allowed (FSR_OPT_TOPK_PRUNE)
+        self.online_path = os.environ.get("FSR_ONLINE_PATH", "tc")  # "tc" | "pruned" | "exact"
+        self.last_online_path = None
 
     @classmethod
     def get(cls, device=None) -> "Context":
@@ -219,6 +230,14 @@ class Context:
         """Top-k-only fp32 batches: certified fp16-pruned K9 + exact re-score (True, default)
         or the unpruned fp32 K9 (False).  Both return the same top-k."""
         self.check(self.lib.fsr_ctx_set_option(self.handle, 2, int(bool(on))))
+        self.topk_prune = bool(on)
+
+    def set_online_path(self, path: str):
+        """Preferred certified top-k path: "tc" (K9t tensor cores, default),
+        "pruned" (K9h fp16 gathers) or "exact" (unpruned).  Same results."""
+        if path not in ("tc", "pruned", "exact"):
+            raise ValueError(f"unknown online path {path!r}")
+        self.online_path = path
 
     def enable_timing(self, on: bool = True):
         self.check(self.lib.fsr_ctx_enable_timing(self.handle, int(on)))

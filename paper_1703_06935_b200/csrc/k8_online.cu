@@ -77,7 +77,7 @@ __global__ void __launch_bounds__(256) project_smem_kernel(int64_t r, int64_t b,
                                                            const T* __restrict__ y_val, T* __restrict__ Zt,
                                                            T* __restrict__ Zs, __half* __restrict__ Zh = nullptr,
                                                            float2* __restrict__ qp = nullptr,
-                                                           int* __restrict__ nflag = nullptr) {
+                                                           int* __restrict__ nflag = nullptr, int64_t zh_ld = 0) {
   extern __shared__ __align__(16) unsigned char dyn[];
   T* z = (T*)dyn;
   T* ev = (T*)(dyn + ((r * sizeof(T) + 15) / 16) * 16);
@@ -176,7 +176,10 @@ __global__ void __launch_bounds__(256) project_smem_kernel(int64_t r, int64_t b,
       }
       __syncthreads();
       const float sc = sc_s;
-      for (int64_t c = threadIdx.x; c < r; c += blockDim.x) Zh[c * b + j] = __float2half_rn(z[c] * sc);
+      if (zh_ld)  // query-major [b][zh_ld] (K9t's K-major GEMM operand): coalesced
+        for (int64_t c = threadIdx.x; c < r; c += blockDim.x) Zh[j * zh_ld + c] = __float2half_rn(z[c] * sc);
+      else
+        for (int64_t c = threadIdx.x; c < r; c += blockDim.x) Zh[c * b + j] = __float2half_rn(z[c] * sc);
     }
   }
 }
@@ -198,14 +201,15 @@ template <typename T>
 int launch_project(fsr_ctx* ctx, int64_t r, int64_t b, int u_sparse, const int64_t* u_indptr,
                    const int32_t* u_indices, const T* u_values, const T* u_dense, int64_t ldu, const T* w,
                    const int64_t* y_ptr, const int64_t* y_idx, const T* y_val, T* Zt, T* Zs,
-                   __half* Zh = nullptr, float2* qp = nullptr, int* nflag = nullptr, bool* fused = nullptr) {
+                   __half* Zh = nullptr, float2* qp = nullptr, int* nflag = nullptr, bool* fused = nullptr,
+                   int64_t zh_ld = 0) {
   fsr::StageTimer timer(ctx, FSR_STAGE_PROJECT);
   const size_t psmem = ((size_t)r * sizeof(T) + 15) / 16 * 16 + (size_t)kProjCap * (sizeof(T) + 4);
   if (fused) *fused = u_sparse && psmem <= 160 * 1024;
   if (u_sparse && psmem <= 160 * 1024) {
     FSR_TRY(fsr::ensure_smem(ctx, project_smem_kernel<T>, psmem));
     project_smem_kernel<T><<<(unsigned)b, 256, psmem, ctx->stream>>>(r, b, u_indptr, u_indices, u_values, w, y_ptr,
-                                                                     y_idx, y_val, Zt, Zs, Zh, qp, nflag);
+                                                                     y_idx, y_val, Zt, Zs, Zh, qp, nflag, zh_ld);
   } else if (u_sparse)
     project_kernel<T, true><<<(unsigned)b, 256, 0, ctx->stream>>>(r, b, u_indptr, u_indices, u_values, nullptr, 0, w,
                                                                   y_ptr, y_idx, y_val, Zt, Zs);
@@ -375,6 +379,21 @@ int filter_impl(fsr_ctx* ctx, int64_t n, int64_t r, int u_sparse, const int64_t*
 }
 
 }  // namespace
+
+namespace fsr {
+// K8 for the tensor-core step (k9t.cu): Zt, Zs and the query-major scaled fp16 Zh.
+int k9t_project(fsr_ctx* ctx, int64_t r, int64_t b, const int64_t* u_indptr, const int32_t* u_indices,
+                const float* u_values, const float* w, const int64_t* y_ptr, const int64_t* y_idx,
+                const float* y_val, float* Zt, float* Zs, __half* Zh, int64_t ldzh, float2* qp, int* nflag) {
+  bool fused = false;
+  const size_t psmem = ((size_t)r * 4 + 15) / 16 * 16 + (size_t)kProjCap * 8;
+  FSR_REQUIRE(ctx, psmem <= 160 * 1024, "k9t_project: r = %lld too large for the fused projection", (long long)r);
+  FSR_TRY(launch_project<float>(ctx, r, b, 1, u_indptr, u_indices, u_values, nullptr, 0, w, y_ptr, y_idx, y_val, Zt,
+                                Zs, Zh, qp, nflag, &fused, ldzh));
+  FSR_REQUIRE(ctx, fused, "k9t_project: fused projection unavailable");
+  return FSR_OK;
+}
+}  // namespace fsr
 
 extern "C" {
 

@@ -1,0 +1,1008 @@
+// K9t: the online ranked-query step (top-K of x_q = U~ h(Lambda) U~^T y_q for
+// a batch of b queries, reference ranking.py:229-255 + rank ranking.py:390-395)
+// on the 5th-generation tensor cores, certified to return bit for bit the
+// top-K of the unpruned fp32 path.
+//
+// Why a dense GEMM for a 2%-dense U~.  The sparse K9/K9h kernels gather one
+// b-wide row of the projected queries per nonzero of U~ (tau * b * 2 bytes =
+// 205 GB of L2 -> SM traffic per 1024-query batch at C3) and are bound by the
+// loaded L2 latency of those gathers (K9h 11.6 ms, 88% of the random-row L2
+// probe; staging the rows in shared memory only moves the bound to shared
+// memory bandwidth, tools/fma_rate.cu).  The same product as a dense fp16 GEMM
+// (M = n, N = b, K = r: 1.02e16 flop at C3) runs at tensor-core rate, and the
+// dense fp16 U~ (n x r x 2 bytes = 10 GB at C3, independent of tau) streams
+// from HBM once per batch.  Both fp16 operands make the products approximate,
+// so -- exactly as in the K9h pruned path (prune.cuh) -- a rigorous per-row
+// bound selects the rows that can still be in the top K and only those are
+// re-scored in fp32 in the unpruned kernel's order.
+//
+// Bound (row i with m_i stored entries, query q; prune.cuh has the fp16
+// rounding part): |x_fp32 - x~| <= c_i * Zb_q with
+//   c_i = 1.01 (||u_i||_2 (2^-10 + 2.01 m_i 2^-24 + m_i 2^-21 + sqrt(m_i) 2^-38) + sqrt(m_i) 2^-25).
+// The new term m_i 2^-21 covers the tensor-core accumulation: products of two
+// fp16 values are exact in fp32; the accumulator is modelled as aligning each
+// MMA step's addends to the largest and truncating (at most one unit in the
+// 23rd bit per addend, <= 2 * 2^-22 relative per step with a nonzero
+// product; steps whose products are all zero leave it unchanged).  A row has
+// at most m_i steps with a nonzero product.  The measured behaviour (a
+// -2^-24 relative drift per MMA step, tools/tc_debug.cu) is 8x inside it.
+//
+// Step (one CUDA graph):
+//   K8 project (k8_online.cu, fp32 Zs + fp16 Zh[b][ldr] with a per-query
+//      power-of-two scale);
+//   k9t_gemm<0> on every 32nd 128-row tile (sample) -> lower keys;
+//   k9t_threshold: per query t = the sample's target-th largest lower key
+//      (any t with >= K rows of lower >= t satisfies t <= x_(K));
+//   k9t_gemm<1> on all tiles: the epilogue drains TMEM, counts rows with
+//      lower >= t and appends rows with upper >= t (and their x~) to the
+//      query's candidate list -- x~ (b x n) is never written;
+//   k9t_finish: adds copied uncovered rows (eta = 0, ranking.py:248-254),
+//      lambda_K = K-th largest lower, keeps upper >= lambda_K, exact fp32
+//      re-score in the unpruned K9's order, sort by (-x, index);
+//   k9t_empty: queries with z = 0 (empty observation, FilterGraph padding);
+//   fallback (flagged queries only): exact scores of every row + exact select.
+#include <cuda.h>
+#include <cuda_fp16.h>
+
+#include <algorithm>
+#include <cfloat>
+#include <cstdlib>
+#include <mutex>
+
+#include "fsr_common.cuh"
+#include "prune.cuh"
+#include "tc_common.cuh"
+#include "topk.cuh"
+
+namespace fsr {
+namespace k9t {
+
+using namespace fsr::tc;
+
+constexpr int kThreads = 192;   // warp 0 TMA, warp 1 MMA + TMEM owner, warps 2-5 epilogue
+constexpr int BM = 128;         // rows of U~ per tile (TMEM lanes)
+constexpr int BN = 256;         // queries per tile (TMEM columns per accumulator)
+constexpr int BK = 64;          // fp16 K elements per stage = 128 bytes = one SWIZZLE_128B row
+constexpr int STAGES = 4;
+constexpr int A_BYTES = BM * BK * 2;
+constexpr int B_BYTES = BN * BK * 2;
+constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256 + 2 * BN * 16 + 2 * BN * 4 + BN * 4;
+constexpr int kSampleStride = 32;  // threshold sample: every 32nd row tile
+constexpr int kCap = 4096;         // candidates per query (row << 12 | slot packs into int64)
+constexpr int kFinishThreads = 256;
+constexpr int kEmpty = -2;         // ccount marker: z = 0 query, answered by k9t_empty
+static_assert(SMEM <= 227 * 1024, "stages exceed shared memory");
+
+__host__ __device__ constexpr int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
+inline int64_t ld_of(int64_t r) { return round_up(r, 8); }  // 16-byte rows for TMA
+
+// kind::f16: A, B fp16 (format 0), D fp32 (format 1), both K-major.
+__host__ __device__ constexpr uint32_t idesc_f16(int M, int N) {
+  return (1u << 4) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
+__device__ __forceinline__ void mma_f16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                        uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+__device__ __forceinline__ void epi_barrier() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+
+// ---- thread-block cluster (B tile split across the cluster, TMA multicast) --
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// 2-D TMA load written to the same smem offset (and signalling the same
+// mbarrier offset) in every CTA of `mask`
+__device__ __forceinline__ void tma_load_2d_mc(void* dst, const CUtensorMap* map, uint64_t* bar, int32_t c0,
+                                               int32_t c1, uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+      " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "h"(mask)
+      : "memory");
+}
+// arrive once on the mbarrier at this offset in every CTA of `mask` when this
+// thread's previously issued MMAs complete
+__device__ __forceinline__ void mma_commit_mc(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"(mask)
+      : "memory");
+}
+
+// per-row bound factor (see the file comment); m entries, ss = sum of squares (rounded up)
+__device__ __forceinline__ float row_bound(double m, float ss) {
+  const double f = 0x1p-10 + 2.01 * m * 0x1p-24 + m * 0x1p-21 + sqrt(m) * 0x1p-38;
+  return __double2float_ru((__dsqrt_ru((double)ss) * f + sqrt(m) * 0x1p-25) * 1.01);
+}
+
+// ---------------------------------------------------------------- layout --
+// Dense fp16 copy of U~ (n x ldr, zeros off the support) + c_i + max_i c_i.
+// Warp per row: scatter the row's entries, bound factor from the fp32 row.
+__global__ void __launch_bounds__(256) densify_kernel(int64_t n, int64_t ldr, const int64_t* __restrict__ indptr,
+                                                      const int32_t* __restrict__ indices,
+                                                      const float* __restrict__ vals, __half* __restrict__ Ud,
+                                                      float* __restrict__ cb, int* __restrict__ cmax_bits) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  int cmax = 0;
+  for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < n; i += nw) {
+    const int64_t e0 = indptr[i], e1 = indptr[i + 1];
+    float ss = 0.f;
+    for (int64_t e = e0 + lane; e < e1; e += 32) {
+      const float v = vals[e];
+      ss = __fmaf_ru(v, v, ss);
+      Ud[i * ldr + indices[e]] = __float2half_rn(v);
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) ss = __fadd_ru(ss, __shfl_xor_sync(0xffffffffu, ss, o));
+    if (lane == 0) {
+      const float c = e1 > e0 ? row_bound((double)(e1 - e0), ss) : 0.f;
+      cb[i] = c;
+      cmax = max(cmax, __float_as_int(c));
+    }
+  }
+  if (lane == 0) atomicMax(cmax_bits, cmax);
+}
+
+// ------------------------------------------------------------------ GEMM --
+// MODE 0 (sample): row tiles kSampleStride * s, writes the lower keys of the
+//   sampled rows, Ks[q * ns + s * BM + row-in-tile].
+// MODE 1 (select): all row tiles; counts lower >= t (nlow) and appends rows
+//   with upper >= t to cand / cval.
+struct QParam {
+  float tf_pre;  // conservative round-to-nearest pre-filter of t (NaN: skip the query)
+  float inv;     // 1 / s_q
+  float cz;      // max_i c_i * Zb_q (1 + 2^-20)
+  float zb;      // Zb_q
+};
+
+// CL CTAs (consecutive blockIdx.x) form a cluster working on CL consecutive
+// row tiles of the same query tile: each loads its own A tile and 1/CL of the
+// B tile, multicast into every member's stage -- the L2 -> SM traffic per tile
+// drops from A + B to A + B / CL (ncu at CL = 1: L2 throughput 72%, tensor
+// pipe 48% -- L2-fed).  A stage is refilled only after every member's MMAs
+// consumed it (the commits are multicast: empty barriers count CL arrivals).
+template <int MODE, int CL>
+__global__ void __launch_bounds__(kThreads, 1)
+    k9t_gemm_kernel(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUtensorMap mB, int n, int b,
+                    int r, int tiles_n, int total, const float* __restrict__ cb, const float2* __restrict__ qp,
+                    const QParam* __restrict__ qpar, const uint32_t* __restrict__ thr, uint32_t* __restrict__ Ks,
+                    int64_t ns, int32_t* __restrict__ cand, float* __restrict__ cval, int32_t* __restrict__ ccount,
+                    unsigned* __restrict__ nlow) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint64_t* full = (uint64_t*)(smem + STAGES * STAGE_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;  // [2]
+  uint64_t* tempty = tfull + 2;      // [2]
+  uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
+  float4* spar = (float4*)(smem + STAGES * STAGE_BYTES + 256);  // [2][BN]
+  uint32_t* sthr = (uint32_t*)(spar + 2 * BN);                  // [2][BN]
+  unsigned* scnt = sthr + 2 * BN;                               // [BN]
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int iters = (r + BK - 1) / BK;
+  const int rank = CL > 1 ? (int)cluster_rank() : 0;
+  const int cluster = blockIdx.x / CL, nclusters = gridDim.x / CL;
+  constexpr uint16_t kMask = (uint16_t)((1u << CL) - 1);
+  constexpr int PART_ROWS = BN / CL, PART_BYTES = PART_ROWS * BK * 2;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], CL);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 4);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&mA);
+    tma_prefetch(&mB);
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, 512);
+  for (int t = threadIdx.x; t < BN; t += blockDim.x) scnt[t] = 0;
+  tc_fence_before();
+  if (CL > 1)
+    cluster_sync();  // every member's barriers exist before any multicast lands
+  else
+    __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  // work item idx (per cluster) -> this CTA's (row tile, query tile)
+  auto tile_of = [&](int idx, int& ti, int& tj) {
+    ti = (idx / tiles_n) * CL + rank;
+    tj = idx % tiles_n;
+    if (MODE == 0) ti *= kSampleStride;
+  };
+
+  if (warp == 0) {
+    int g = 0;
+    for (int idx = cluster; idx < total; idx += nclusters) {
+      int ti, tj;
+      tile_of(idx, ti, tj);
+      for (int it = 0; it < iters; ++it, ++g) {
+        const int s = g % STAGES;
+        mbar_wait(&empty[s], ((g / STAGES) & 1) ^ 1);
+        if (lane == 0) {
+          uint8_t* st = smem + s * STAGE_BYTES;
+          mbar_expect_tx(&full[s], STAGE_BYTES);
+          tma_load_2d(st, &mA, &full[s], it * BK, ti * BM);
+          if (CL == 1)
+            tma_load_2d(st + A_BYTES, &mB, &full[s], it * BK, tj * BN);
+          else
+            tma_load_2d_mc(st + A_BYTES + rank * PART_BYTES, &mB, &full[s], it * BK, tj * BN + rank * PART_ROWS,
+                           kMask);
+        }
+        __syncwarp();
+      }
+    }
+  } else if (warp == 1) {
+    constexpr uint32_t idesc = idesc_f16(BM, BN);
+    int g = 0, tcount = 0;
+    for (int idx = cluster; idx < total; idx += nclusters, ++tcount) {
+      const int ab = tcount & 1, use = tcount >> 1;
+      if (use > 0) {  // the epilogue has drained this accumulator's previous tile
+        mbar_wait(&tempty[ab], (use - 1) & 1);
+        tc_fence_after();
+      }
+      const uint32_t d = tmem + ab * BN;
+      for (int it = 0; it < iters; ++it, ++g) {
+        const int s = g % STAGES;
+        mbar_wait(&full[s], (g / STAGES) & 1);
+        tc_fence_after();
+        const uint32_t sa = smem_u32(smem + s * STAGE_BYTES);
+        const uint64_t da = smem_desc_sw128(sa, 16, 1024), db = smem_desc_sw128(sa + A_BYTES, 16, 1024);
+        if (lane == 0) {
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k)  // K = 16 per MMA: +32 bytes inside the 128-byte swizzle row
+            mma_f16(d, da + (uint64_t)(2 * k), db + (uint64_t)(2 * k), idesc, (it | k) ? 1u : 0u);
+          if (CL == 1)
+            mma_commit(&empty[s]);
+          else
+            mma_commit_mc(&empty[s], kMask);  // the stage holds every member's B part
+          if (it == iters - 1) mma_commit(&tfull[ab]);
+        }
+        __syncwarp();
+      }
+    }
+  } else {
+    const int q4 = warp & 3;  // TMEM lane quarter this warp may access
+    const int et = threadIdx.x - 64;  // 0..127 among the epilogue threads
+    int tcount = 0;
+    for (int idx = cluster; idx < total; idx += nclusters, ++tcount) {
+      int ti, tj;
+      tile_of(idx, ti, tj);
+      const int ab = tcount & 1, use = tcount >> 1, pb = tcount & 1;
+      const int j0 = tj * BN;
+      // per-query parameters of this tile's columns
+      for (int t = et; t < BN; t += 128) {
+        const int q = j0 + t;
+        float4 p = make_float4(__int_as_float(0x7fffffff), 1.f, 0.f, 0.f);
+        uint32_t tk = 0xffffffffu;
+        if (q < b) {
+          if (MODE == 0) {
+            const float2 v = qp[q];
+            p = make_float4(0.f, v.x, 0.f, v.y);
+          } else {
+            const QParam v = qpar[q];
+            p = make_float4(v.tf_pre, v.inv, v.cz, v.zb);
+            tk = thr[q];
+          }
+        }
+        spar[pb * BN + t] = p;
+        sthr[pb * BN + t] = tk;
+      }
+      const int row = ti * BM + 32 * q4 + lane;
+      const bool row_ok = row < n;
+      const float c = row_ok ? __ldg(cb + row) : 0.f;
+      mbar_wait(&tfull[ab], use & 1);
+      tc_fence_after();
+      epi_barrier();
+      const uint32_t tl = tmem + ((uint32_t)(32 * q4) << 16) + ab * BN;
+#pragma unroll 1
+      for (int cc = 0; cc < BN / 32; ++cc) {
+        float v[32];
+        tmem_ld32(tl + cc * 32, v);
+        if (!row_ok) continue;
+        if (MODE == 0) {
+          const int64_t srow = (int64_t)(ti / kSampleStride) * BM + 32 * q4 + lane;
+#pragma unroll
+          for (int t = 0; t < 32; ++t) {
+            const int jj = cc * 32 + t;
+            if (j0 + jj < b) {
+              const float4 p = spar[pb * BN + jj];
+              const float x = v[t] * p.y;
+              Ks[(int64_t)(j0 + jj) * ns + srow] = prune::key32(__fsub_rd(x, prune::bound_of(c, p.w)));
+            }
+          }
+        } else {
+#pragma unroll
+          for (int t = 0; t < 32; ++t) {
+            const int jj = cc * 32 + t;
+            const float4 p = spar[pb * BN + jj];
+            const float x = v[t] * p.y;
+            if (x + p.z >= p.x) {  // rare: within reach of the threshold
+              const float bd = prune::bound_of(c, p.w);
+              const uint32_t tk = sthr[pb * BN + jj];
+              if (prune::key32(__fsub_rd(x, bd)) >= tk) atomicAdd(&scnt[jj], 1u);
+              if (prune::key32(__fadd_ru(x, bd)) >= tk) {
+                const int slot = atomicAdd(ccount + j0 + jj, 1);
+                if (slot < kCap) {
+                  cand[(int64_t)(j0 + jj) * kCap + slot] = row;
+                  cval[(int64_t)(j0 + jj) * kCap + slot] = x;
+                }
+              }
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[ab]);
+      if (MODE == 1) {
+        epi_barrier();
+        for (int t = et; t < BN; t += 128) {
+          const unsigned k = scnt[t];
+          if (k) {
+            atomicAdd(nlow + j0 + t, k);
+            scnt[t] = 0;
+          }
+        }
+      }
+    }
+  }
+  if (CL > 1)
+    cluster_sync();  // no member exits while a peer may still signal its barriers
+  else
+    __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+// ------------------------------------------------------------- threshold --
+// Per query: t = the target-th largest lower key of the sample (two 12-bit
+// digits), the QParam of the main pass, zeroed counters.  z = 0 queries are
+// marked kEmpty; non-finite z, and thresholds at or below the smallest normal
+// (fewer than ~target positive sampled scores), are flagged for the exact
+// fallback.
+__global__ void __launch_bounds__(256) k9t_threshold_kernel(int64_t b, int64_t ns, int64_t n_valid_s,
+                                                            const uint32_t* __restrict__ Ks,
+                                                            const float2* __restrict__ qp,
+                                                            const int* __restrict__ cmax_bits, int64_t target,
+                                                            uint32_t* __restrict__ thr, QParam* __restrict__ qpar,
+                                                            int32_t* __restrict__ ccount, unsigned* __restrict__ nlow,
+                                                            int* __restrict__ nflag, int* __restrict__ flags) {
+  constexpr int KB = 32, HB = topk::kHistBits, nb = 1 << HB;
+  __shared__ unsigned hist[nb];
+  __shared__ unsigned found_bin;
+  __shared__ unsigned long long above;
+  const float nanf_ = __int_as_float(0x7fffffff);
+  for (int64_t q = blockIdx.x; q < b; q += gridDim.x) {
+    const float2 p = qp[q];
+    const float zb = p.y;
+    if (zb == 0.f || !(zb <= FLT_MAX)) {
+      if (threadIdx.x == 0) {
+        qpar[q] = QParam{nanf_, p.x, 0.f, zb};
+        if (zb == 0.f) {
+          ccount[q] = kEmpty;
+        } else {
+          ccount[q] = -1;
+          flags[atomicAdd(nflag, 1)] = (int)q;
+        }
+      }
+      continue;
+    }
+    const uint32_t* kq = Ks + q * ns;
+    uint32_t prefix = 0;
+    unsigned long long above0 = 0;
+    for (int level = 0; level < 2; ++level) {
+      for (int t = threadIdx.x; t < nb; t += blockDim.x) hist[t] = 0;
+      __syncthreads();
+      for (int64_t e = threadIdx.x; e < n_valid_s; e += blockDim.x) {
+        const uint32_t k = kq[e];
+        if (level == 0)
+          atomicAdd(&hist[k >> (KB - HB)], 1u);
+        else if ((k >> (KB - HB)) == prefix)
+          atomicAdd(&hist[(k >> (KB - 2 * HB)) & (nb - 1)], 1u);
+      }
+      __syncthreads();
+      topk::find_bin_t<256>(hist, nb, level == 0 ? target : target - above0, &found_bin, &above);
+      if (level == 0) above0 = above;
+      prefix = (prefix << HB) | found_bin;
+      __syncthreads();
+    }
+    const uint32_t t_lo = prefix << (KB - 2 * HB);
+    if (threadIdx.x == 0) {
+      const float tf = prune::key_to_float((uint64_t)t_lo);
+      if (!(tf >= FLT_MIN)) {  // t <= 0: zero-valued rows would all be candidates
+        qpar[q] = QParam{nanf_, p.x, 0.f, zb};
+        ccount[q] = -1;
+        flags[atomicAdd(nflag, 1)] = (int)q;
+      } else {
+        thr[q] = t_lo;
+        ccount[q] = 0;
+        nlow[q] = 0;
+        const float cz = __int_as_float(*cmax_bits) * zb * (1.f + 0x1p-20f);
+        qpar[q] = QParam{tf - fabsf(tf) * 0x1p-20f - 0x1p-126f, p.x, cz, zb};
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------- finish --
+// x_i of the unpruned fp32 path for a row with no stored product to re-score:
+// the copied y_i of an uncovered observed row (ranking.py:248-254), else 0.
+__device__ __forceinline__ bool copied_value(int64_t i, int64_t q, const double* __restrict__ eta, int copy,
+                                             const int64_t* __restrict__ y_ptr, const int64_t* __restrict__ y_idx,
+                                             const float* __restrict__ y_val, float* v) {
+  if (!(copy && eta && eta[i] == 0.0)) return false;
+  for (int64_t t = y_ptr[q]; t < y_ptr[q + 1]; ++t)
+    if (y_idx[t] == i) {
+      *v = y_val[t];
+      return true;
+    }
+  return false;
+}
+
+// The exact fp32 score of row i (thread-sequential, the unpruned K9's order).
+__device__ __forceinline__ float exact_row(int64_t i, int64_t q, const int64_t* __restrict__ indptr,
+                                           const int32_t* __restrict__ indices, const float* __restrict__ vals,
+                                           const float* __restrict__ Zs, int64_t ldz, const double* __restrict__ eta,
+                                           int copy, const int64_t* __restrict__ y_ptr,
+                                           const int64_t* __restrict__ y_idx, const float* __restrict__ y_val) {
+  float v;
+  if (copied_value(i, q, eta, copy, y_ptr, y_idx, y_val, &v)) return v;
+  float acc = 0.f;
+  for (int64_t e = indptr[i]; e < indptr[i + 1]; ++e)
+    acc = fmaf(__ldg(vals + e), __ldg(Zs + (int64_t)__ldg(indices + e) * ldz + q), acc);
+  return acc;
+}
+
+// The same for one row by a G-lane group (uniform result): copied rows first,
+// then the grouped sequential sum of prune.cuh (bitwise the thread version).
+template <int G>
+__device__ __forceinline__ float exact_row_group(int64_t i, int64_t q, const int64_t* __restrict__ indptr,
+                                                 const int32_t* __restrict__ indices, const float* __restrict__ vals,
+                                                 const float* __restrict__ Zs, int64_t ldz,
+                                                 const double* __restrict__ eta, int copy,
+                                                 const int64_t* __restrict__ y_ptr, const int64_t* __restrict__ y_idx,
+                                                 const float* __restrict__ y_val, unsigned mask) {
+  float v;
+  if (copied_value(i, q, eta, copy, y_ptr, y_idx, y_val, &v)) return v;
+  if (indptr[i] == indptr[i + 1]) return 0.f;
+  return prune::exact_score_group<G>(i, q, Zs /* unused: the row is not empty */, indptr, indices, vals, Zs, ldz,
+                                     nullptr, 0, y_ptr, y_idx, mask);
+}
+
+constexpr int kKeep = 1024;  // rows re-scored exactly per query (upper >= lambda_K); more -> fallback
+constexpr size_t kFinishSmem = (size_t)kCap * 12 + (size_t)(1 << topk::kHistBits) * 4 + (size_t)kKeep * 16;
+
+__global__ void __launch_bounds__(kFinishThreads) k9t_finish_kernel(
+    const float* __restrict__ cb, const QParam* __restrict__ qpar, const uint32_t* __restrict__ thr,
+    const int32_t* __restrict__ cand, const float* __restrict__ cval, const int32_t* __restrict__ ccount,
+    const unsigned* __restrict__ nlow, const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices,
+    const float* __restrict__ vals, const float* __restrict__ Zs, int64_t ldz, const double* __restrict__ eta,
+    int copy, const int64_t* __restrict__ y_ptr, const int64_t* __restrict__ y_idx, const float* __restrict__ y_val,
+    int64_t K, int64_t* __restrict__ out_idx, float* __restrict__ out_val, int* __restrict__ nflag,
+    int* __restrict__ flags, int2* __restrict__ stats) {
+  constexpr int HB = topk::kHistBits, NB = 1 << HB;
+  extern __shared__ __align__(16) unsigned char dyn[];
+  uint64_t* kkey = (uint64_t*)dyn;             // [kKeep] exact order keys of the kept rows
+  int64_t* kidx = (int64_t*)(kkey + kKeep);    // [kKeep] row << 12 | slot
+  uint32_t* lkey = (uint32_t*)(kidx + kKeep);  // [kCap] lower-bound keys by slot
+  int32_t* crow = (int32_t*)(lkey + kCap);     // [kCap] rows by slot
+  float* cv = (float*)(crow + kCap);           // [kCap] x~, then exact scores, by slot
+  unsigned* hist = (unsigned*)(cv + kCap);     // [NB]
+  __shared__ unsigned n_extra, n_extra_ge, n_keep, n_next, found_bin;
+  __shared__ unsigned long long above;
+  const int64_t q = blockIdx.x;
+  const int cnt0 = ccount[q];
+  if (cnt0 < 0) return;  // flagged (fallback) or empty observation (k9t_empty)
+  const int cnt = min(cnt0, kCap);
+  const uint32_t tk = thr[q];
+  const float zb = qpar[q].zb;
+  if (threadIdx.x == 0) n_extra = n_extra_ge = n_keep = 0;
+  __syncthreads();
+  // main candidates (rows with upper >= t) and their lower-bound keys
+  for (int t = threadIdx.x; t < cnt; t += blockDim.x) {
+    const int32_t i = cand[q * kCap + t];
+    const float x = cval[q * kCap + t];
+    crow[t] = i;
+    cv[t] = x;
+    lkey[t] = prune::key32(__fsub_rd(x, prune::bound_of(cb[i], zb)));
+  }
+  // copied uncovered rows of this query: exact value y_i (the main pass saw 0 < t)
+  if (copy && eta) {
+    for (int64_t t = y_ptr[q] + threadIdx.x; t < y_ptr[q + 1]; t += blockDim.x) {
+      const int64_t i = y_idx[t];
+      if (eta[i] != 0.0) continue;
+      const float v = y_val[t];
+      const unsigned s = atomicAdd(&n_extra, 1u);
+      if (prune::key32(v) >= tk) atomicAdd(&n_extra_ge, 1u);
+      const int slot = cnt + (int)s;
+      if (slot < kCap) {
+        crow[slot] = (int32_t)i;
+        cv[slot] = v;
+        lkey[slot] = prune::key32(v);
+      }
+    }
+  }
+  __syncthreads();
+  const int total = cnt + (int)n_extra;
+  if (cnt0 > kCap || total > kCap || (unsigned long long)nlow[q] + n_extra_ge < (unsigned long long)K) {
+    if (threadIdx.x == 0) flags[atomicAdd(nflag, 1)] = (int)q;  // overflow, or the sampled t was too high
+    return;
+  }
+  // lambda' <= lambda_K (the K-th largest lower bound): two 12-bit radix
+  // digits of the candidates' lower keys, the low end of the K-th key's bucket
+  uint32_t prefix = 0;
+  unsigned long long above0 = 0;
+  for (int level = 0; level < 2; ++level) {
+    for (int t = threadIdx.x; t < NB; t += blockDim.x) hist[t] = 0;
+    __syncthreads();
+    for (int t = threadIdx.x; t < total; t += blockDim.x) {
+      const uint32_t k = lkey[t];
+      if (level == 0)
+        atomicAdd(&hist[k >> (32 - HB)], 1u);
+      else if ((k >> (32 - HB)) == prefix)
+        atomicAdd(&hist[(k >> (32 - 2 * HB)) & (NB - 1)], 1u);
+    }
+    __syncthreads();
+    topk::find_bin_t<kFinishThreads>(hist, NB, level == 0 ? (unsigned long long)K : K - above0, &found_bin, &above);
+    if (level == 0) above0 = above;
+    prefix = (prefix << HB) | found_bin;
+    __syncthreads();
+  }
+  const uint32_t lam = prefix << (32 - 2 * HB);
+  // keep upper >= lambda' (copied rows: exact, upper == lower)
+  for (int t = threadIdx.x; t < total; t += blockDim.x) {
+    const int32_t i = crow[t];
+    const bool keep = t >= cnt ? lkey[t] >= lam
+                               : prune::key32(__fadd_ru(cv[t], prune::bound_of(cb[i], zb))) >= lam;
+    if (keep) {
+      const unsigned k = atomicAdd(&n_keep, 1u);
+      if (k < (unsigned)kKeep) kidx[k] = ((int64_t)i << 12) | t;
+    }
+  }
+  __syncthreads();
+  const unsigned keep = n_keep;
+  if (threadIdx.x == 0) stats[q] = make_int2(total, (int)keep);
+  if (keep > (unsigned)kKeep) {
+    if (threadIdx.x == 0) flags[atomicAdd(nflag, 1)] = (int)q;
+    return;
+  }
+  // exact re-score of the kept main candidates (8-lane groups, rows from a counter)
+  constexpr int G = 8;
+  const int lane = threadIdx.x & 31, grp = threadIdx.x / G, gl = threadIdx.x & (G - 1);
+  const unsigned gmask = 0xffu << (lane & ~(G - 1));
+  if (threadIdx.x == 0) n_next = kFinishThreads / G;
+  __syncthreads();
+  for (unsigned t = grp; t < keep;) {
+    const int64_t packed = kidx[t];
+    const int slot = (int)(packed & 4095);
+    if (slot < cnt) {
+      const float v = exact_row_group<G>(packed >> 12, q, indptr, indices, vals, Zs, ldz, eta, copy, y_ptr, y_idx,
+                                         y_val, gmask);
+      if (gl == 0) cv[slot] = v;
+    }
+    unsigned nt = 0;
+    if (gl == 0) nt = atomicAdd(&n_next, 1u);
+    t = __shfl_sync(gmask, nt, 0, G);
+  }
+  __syncthreads();
+  for (unsigned t = threadIdx.x; t < keep; t += blockDim.x) kkey[t] = topk::order_key(cv[kidx[t] & 4095]);
+  __syncthreads();
+  topk::bitonic_sort(kkey, kidx, (int)keep);
+  for (int64_t m = threadIdx.x; m < K; m += blockDim.x) {
+    const int64_t packed = kidx[m];
+    out_idx[q * K + m] = packed >> 12;
+    out_val[q * K + m] = cv[packed & 4095];
+  }
+}
+
+// ------------------------------------------------------------------ empty --
+// z = 0: every summed row scores +0; copied uncovered rows carry y_i.  Top K
+// by (key desc, index asc): the positive copies sorted, then the zero-valued
+// rows in index order (a copied +-0 keeps its own bits).  Copies of more than
+// kCap rows are flagged for the fallback.
+__global__ void __launch_bounds__(256) k9t_empty_kernel(int64_t n, const int32_t* __restrict__ ccount,
+                                                        const double* __restrict__ eta, int copy,
+                                                        const int64_t* __restrict__ y_ptr,
+                                                        const int64_t* __restrict__ y_idx,
+                                                        const float* __restrict__ y_val, int64_t K,
+                                                        int64_t* __restrict__ out_idx, float* __restrict__ out_val,
+                                                        int* __restrict__ nflag, int* __restrict__ flags) {
+  extern __shared__ __align__(16) unsigned char dyn[];
+  uint64_t* pkey = (uint64_t*)dyn;          // positives: key, row
+  int64_t* prow = (int64_t*)(pkey + kCap);
+  uint64_t* zkey = (uint64_t*)(prow + kCap);  // all copies by row: key = ~row (ascending row), value bits
+  int64_t* zval = (int64_t*)(zkey + kCap);
+  __shared__ unsigned npos, ncop;
+  const int64_t q = blockIdx.x;
+  if (ccount[q] != kEmpty) return;
+  if (threadIdx.x == 0) npos = ncop = 0;
+  __syncthreads();
+  if (copy && eta)
+    for (int64_t t = y_ptr[q] + threadIdx.x; t < y_ptr[q + 1]; t += blockDim.x) {
+      const int64_t i = y_idx[t];
+      if (eta[i] != 0.0) continue;
+      const float v = y_val[t];
+      const unsigned s = atomicAdd(&ncop, 1u);
+      if (s < (unsigned)kCap) {
+        zkey[s] = ~(uint64_t)i;  // bitonic_sort is descending in key: ~row gives ascending rows
+        zval[s] = (int64_t)__float_as_uint(v);
+      }
+      if (topk::order_key(v) > topk::order_key(0.f)) {
+        const unsigned p = atomicAdd(&npos, 1u);
+        if (p < (unsigned)kCap) {
+          pkey[p] = topk::order_key(v);
+          prow[p] = i;
+        }
+      }
+    }
+  __syncthreads();
+  if (ncop > (unsigned)kCap) {
+    if (threadIdx.x == 0) flags[atomicAdd(nflag, 1)] = (int)q;
+    return;
+  }
+  const int np = (int)npos, nc = (int)ncop;
+  topk::bitonic_sort(pkey, prow, np);
+  topk::bitonic_sort(zkey, zval, nc);
+  for (int64_t m = threadIdx.x; m < (np < K ? (int64_t)np : K); m += blockDim.x) {
+    out_idx[q * K + m] = prow[m];
+    out_val[q * K + m] = prune::key_to_float(pkey[m]);
+  }
+  if (threadIdx.x == 0) {
+    // zero-valued rows in index order, skipping the positive copies; copies
+    // are walked in ascending row order alongside
+    int c = 0;
+    int64_t i = 0;
+    for (int64_t m = np; m < K && i < n; ++i) {
+      while (c < nc && (int64_t)~zkey[c] < i) ++c;
+      float v = 0.f;
+      if (c < nc && (int64_t)~zkey[c] == i) {
+        v = __uint_as_float((uint32_t)zval[c]);
+        if (topk::order_key(v) != topk::order_key(0.f)) continue;  // a positive (or negative) copy
+      }
+      out_idx[q * K + m] = i;
+      out_val[q * K + m] = v;
+      ++m;
+    }
+  }
+}
+
+// --------------------------------------------------------------- fallback --
+__global__ void __launch_bounds__(256) k9t_fallback_rows_kernel(
+    int64_t n, float* __restrict__ Xt, int64_t ldx, const int64_t* __restrict__ indptr,
+    const int32_t* __restrict__ indices, const float* __restrict__ vals, const float* __restrict__ Zs, int64_t ldz,
+    const double* __restrict__ eta, int copy, const int64_t* __restrict__ y_ptr, const int64_t* __restrict__ y_idx,
+    const float* __restrict__ y_val, const int* __restrict__ nflag, const int* __restrict__ flags) {
+  const int nf = *nflag;
+  if (!nf) return;
+  const int64_t nblk = (n + 255) / 256;
+  for (int64_t item = blockIdx.x; item < nf * nblk; item += gridDim.x) {
+    const int64_t q = flags[item / nblk];
+    const int64_t i = (item % nblk) * 256 + threadIdx.x;
+    if (i < n) Xt[q * ldx + i] = exact_row(i, q, indptr, indices, vals, Zs, ldz, eta, copy, y_ptr, y_idx, y_val);
+  }
+}
+
+// ------------------------------------------------------------ host side --
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult qr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &qr) == cudaSuccess &&
+        qr == cudaDriverEntryPointSuccess)
+      fn = (EncodeTiledFn)p;
+  });
+  return fn;
+}
+
+// rows x cols fp16 (row pitch ld elements), box = 64 x box_rows, SWIZZLE_128B; OOB reads zero
+int make_map_f16(fsr_ctx* ctx, CUtensorMap* m, const void* base, int64_t rows, int64_t cols, int64_t ld,
+                 int box_rows) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return set_error(ctx, FSR_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)ld * 2};
+  cuuint32_t box[2] = {(cuuint32_t)BK, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult res = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, (void*)base, dims, strides, box, estr,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (res != CUDA_SUCCESS) return set_error(ctx, FSR_ECUDA, "cuTensorMapEncodeTiled (fp16) failed (%d)", (int)res);
+  return FSR_OK;
+}
+
+inline size_t al256(size_t x) { return (x + 255) / 256 * 256; }
+
+struct DenseLayout {
+  __half* Ud;
+  float* cb;
+  int* cmax_bits;
+};
+inline DenseLayout dense_layout(void* base, int64_t n, int64_t r) {
+  char* p = (char*)base;
+  DenseLayout L;
+  L.Ud = (__half*)p;
+  p += al256((size_t)n * ld_of(r) * 2);
+  L.cb = (float*)p;
+  p += al256((size_t)n * 4);
+  L.cmax_bits = (int*)p;
+  return L;
+}
+inline size_t dense_bytes(int64_t n, int64_t r) { return al256((size_t)n * ld_of(r) * 2) + al256((size_t)n * 4) + 256; }
+
+constexpr int kCluster = 4;  // CTAs per cluster sharing a query tile (B multicast)
+
+inline int64_t sample_rows(int64_t n) {
+  const int64_t tiles_m = (n + BM - 1) / BM;
+  const int64_t s_tiles = (tiles_m + kSampleStride - 1) / kSampleStride;
+  return (s_tiles + kCluster - 1) / kCluster * kCluster * BM;  // whole clusters of sampled tiles
+}
+
+// persistent grid: as many whole clusters as fit at once (1 CTA per SM)
+template <int CL>
+int cluster_grid(fsr_ctx* ctx) {
+  static int cached[64] = {0};
+  int& g = cached[ctx->device & 63];
+  if (g) return g;
+  if (ensure_smem(ctx, k9t_gemm_kernel<1, CL>, SMEM) != FSR_OK) return -1;
+  if (ensure_smem(ctx, k9t_gemm_kernel<0, CL>, SMEM) != FSR_OK) return -1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(ctx->num_sms / CL * CL));
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = SMEM;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = CL;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  int nclusters = 0;
+  if (cudaOccupancyMaxActiveClusters(&nclusters, k9t_gemm_kernel<1, CL>, &cfg) != cudaSuccess || nclusters < 1) {
+    cudaGetLastError();
+    nclusters = ctx->num_sms / CL;
+  }
+  g = nclusters * CL;
+  return g;
+}
+
+template <int MODE, int CL>
+int launch_gemm(fsr_ctx* ctx, int grid, const CUtensorMap& mA, const CUtensorMap& mB, int n, int b, int r,
+                int tiles_n, int total, const float* cb, const float2* qp, const QParam* qpar, const uint32_t* thr,
+                uint32_t* Ks, int64_t ns, int32_t* cand, float* cval, int32_t* ccount, unsigned* nlow) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = SMEM;
+  cfg.stream = ctx->stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = CL;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  FSR_CUDA(ctx, cudaLaunchKernelEx(&cfg, k9t_gemm_kernel<MODE, CL>, mA, mB, n, b, r, tiles_n, total, cb, qp, qpar,
+                                   thr, Ks, ns, cand, cval, ccount, nlow));
+  return launched(ctx, MODE == 0 ? "k9t_gemm_sample" : "k9t_gemm_select");
+}
+
+struct Work {
+  int* nflag;  // [0] = flagged count, [1 .. b] = flagged queries (first, so the host can read it)
+  float* Zt;
+  float* Zs;
+  __half* Zh;
+  float2* qp;
+  QParam* qpar;
+  uint32_t* Ks;
+  uint32_t* thr;
+  int32_t* ccount;
+  unsigned* nlow;
+  int32_t* cand;
+  float* cval;
+  int2* stats;  // per query (candidates, rows re-scored): diagnostics
+  float* Xt;
+};
+inline size_t work_bytes(int64_t n, int64_t r, int64_t b, Work* w, void* base) {
+  char* p = (char*)base;
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    char* q = p ? p + off : nullptr;
+    off += al256(bytes);
+    return q;
+  };
+  Work W;
+  W.nflag = (int*)take((size_t)(b + 2) * 4);
+  W.Zt = (float*)take((size_t)b * r * 4);
+  W.Zs = (float*)take((size_t)r * b * 4);
+  W.Zh = (__half*)take((size_t)b * ld_of(r) * 2);
+  W.qp = (float2*)take((size_t)b * 8);
+  W.qpar = (QParam*)take((size_t)b * sizeof(QParam));
+  W.Ks = (uint32_t*)take((size_t)b * sample_rows(n) * 4);
+  W.thr = (uint32_t*)take((size_t)b * 4);
+  W.ccount = (int32_t*)take((size_t)b * 4);
+  W.nlow = (unsigned*)take((size_t)b * 4);
+  W.cand = (int32_t*)take((size_t)b * kCap * 4);
+  W.cval = (float*)take((size_t)b * kCap * 4);
+  W.stats = (int2*)take((size_t)b * 8);
+  W.Xt = (float*)take((size_t)n * b * 4);
+  if (w) *w = W;
+  return off + 256;
+}
+
+// sample GEMM -> threshold -> selecting GEMM, with CL-CTA clusters
+template <int CL>
+int tc_gemms(fsr_ctx* ctx, const DenseLayout& L, const Work& Wk, int64_t n, int64_t r, int64_t b, int64_t topk) {
+  const int64_t ldr = ld_of(r);
+  CUtensorMap mA, mB;
+  FSR_TRY(make_map_f16(ctx, &mA, L.Ud, n, r, ldr, BM));
+  FSR_TRY(make_map_f16(ctx, &mB, Wk.Zh, b, r, ldr, BN / CL));
+  const int grid = cluster_grid<CL>(ctx);
+  if (grid <= 0) return set_error(ctx, FSR_ECUDA, "filter_topk_tc: no co-resident %d-CTA clusters", CL);
+  const int tiles_m = (int)((n + BM - 1) / BM), tiles_n = (int)((b + BN - 1) / BN);
+  const int64_t ns = sample_rows(n);
+  const int s_tiles = (tiles_m + kSampleStride - 1) / kSampleStride;
+  {
+    StageTimer timer(ctx, FSR_STAGE_TOPK);
+    const int total0 = (s_tiles + CL - 1) / CL * tiles_n;  // work items per cluster
+    FSR_TRY((launch_gemm<0, CL>(ctx, grid, mA, mB, (int)n, (int)b, (int)r, tiles_n, total0, L.cb, Wk.qp, nullptr,
+                               nullptr, Wk.Ks, ns, nullptr, nullptr, nullptr, nullptr)));
+    // rows of the last sampled tile beyond n hold no key: count only valid rows
+    const int64_t last_tile = (int64_t)(s_tiles - 1) * kSampleStride;
+    const int64_t n_valid_s = (int64_t)(s_tiles - 1) * BM + std::min<int64_t>(BM, n - last_tile * BM);
+    const int64_t target = (2 * topk + kSampleStride - 1) / kSampleStride + 8;
+    k9t_threshold_kernel<<<(unsigned)std::min<int64_t>(b, (int64_t)ctx->num_sms * 8), 256, 0, ctx->stream>>>(
+        b, ns, n_valid_s, Wk.Ks, Wk.qp, L.cmax_bits, target, Wk.thr, Wk.qpar, Wk.ccount, Wk.nlow, Wk.nflag,
+        Wk.nflag + 1);
+    FSR_TRY(launched(ctx, "k9t_threshold_kernel"));
+  }
+  {
+    StageTimer timer(ctx, FSR_STAGE_FILTER_SPMM);
+    const int total1 = (tiles_m + CL - 1) / CL * tiles_n;
+    FSR_TRY((launch_gemm<1, CL>(ctx, grid, mA, mB, (int)n, (int)b, (int)r, tiles_n, total1, L.cb, Wk.qp, Wk.qpar,
+                               Wk.thr, nullptr, 0, Wk.cand, Wk.cval, Wk.ccount, Wk.nlow)));
+  }
+  return FSR_OK;
+}
+
+// FSR_K9T_CLUSTER = 1 / 2 / 4 CTAs per cluster (B-tile multicast); default 2
+inline int cluster_choice() {
+  static int c = [] {
+    const char* e = getenv("FSR_K9T_CLUSTER");
+    const int v = e ? atoi(e) : 2;
+    return (v == 1 || v == 2 || v == 4) ? v : 2;
+  }();
+  return c;
+}
+
+}  // namespace k9t
+
+// K8 with the fp16 query-major Zh (k8_online.cu)
+int k9t_project(fsr_ctx* ctx, int64_t r, int64_t b, const int64_t* u_indptr, const int32_t* u_indices,
+                const float* u_values, const float* w, const int64_t* y_ptr, const int64_t* y_idx,
+                const float* y_val, float* Zt, float* Zs, __half* Zh, int64_t ldzh, float2* qp, int* nflag);
+
+}  // namespace fsr
+
+using namespace fsr;
+
+extern "C" {
+
+int64_t fsr_dense_u_bytes(int64_t n, int64_t r) { return (int64_t)k9t::dense_bytes(n, r); }
+
+int fsr_dense_u_build(fsr_ctx* ctx, int64_t n, int64_t r, const int64_t* indptr, const int32_t* indices,
+                      const float* values, void* out) {
+  FSR_REQUIRE(ctx, n >= 1 && r >= 1 && indptr && indices && values && out, "dense_u_build: bad args");
+  FSR_REQUIRE(ctx, aligned(out, 256), "dense_u_build: out must be 256-byte aligned");
+  k9t::DenseLayout L = k9t::dense_layout(out, n, r);
+  FSR_CUDA(ctx, cudaMemsetAsync(out, 0, k9t::dense_bytes(n, r), ctx->stream));
+  k9t::densify_kernel<<<grid_for(n * 32, 256, ctx, 8), 256, 0, ctx->stream>>>(n, k9t::ld_of(r), indptr, indices,
+                                                                             values, L.Ud, L.cb, L.cmax_bits);
+  return launched(ctx, "densify_kernel");
+}
+
+int64_t fsr_filter_tc_workspace_bytes(int64_t n, int64_t r, int64_t b) {
+  return (int64_t)k9t::work_bytes(n, r, b, nullptr, nullptr);
+}
+
+int fsr_filter_tc_applicable(int64_t n, int64_t r, int64_t b, int64_t topk) {
+  return n >= 8 * k9t::BM * k9t::kSampleStride && n < ((int64_t)1 << 31) - 4096 && r >= 1 && r <= 32768 && b >= 1 &&
+         topk >= 1 && topk <= k9t::kCap / 8 && topk <= n;
+}
+
+int fsr_filter_topk_tc(fsr_ctx* ctx, int64_t n, int64_t r, const int64_t* u_indptr, const int32_t* u_indices,
+                       const float* u_values, const void* dense_u, const float* w, const double* eta, int64_t b,
+                       const int64_t* y_ptr, const int64_t* y_idx, const float* y_val, int copy_uncovered,
+                       void* workspace, int64_t topk, int64_t* top_idx, float* top_val) {
+  using namespace k9t;
+  FSR_REQUIRE(ctx, fsr_filter_tc_applicable(n, r, b, topk), "filter_topk_tc: shape outside the tensor-core path");
+  FSR_REQUIRE(ctx, u_indptr && u_indices && u_values && dense_u && workspace && top_idx && top_val,
+              "filter_topk_tc: missing argument");
+  FSR_REQUIRE(ctx, aligned(dense_u, 256) && aligned(workspace, 256), "filter_topk_tc: buffers must be 256-aligned");
+  const DenseLayout L = dense_layout(const_cast<void*>(dense_u), n, r);
+  Work Wk;
+  work_bytes(n, r, b, &Wk, workspace);
+  const int64_t ldr = ld_of(r);
+  const int copy = copy_uncovered && eta;
+  // K8: Zt, Zs (fp32) and the query-major fp16 Zh with per-query scale
+  FSR_TRY(k9t_project(ctx, r, b, u_indptr, u_indices, u_values, w, y_ptr, y_idx, y_val, Wk.Zt, Wk.Zs, Wk.Zh, ldr,
+                      Wk.qp, Wk.nflag));
+  const int cl = cluster_choice();
+  if (cl == 1)
+    FSR_TRY(tc_gemms<1>(ctx, L, Wk, n, r, b, topk));
+  else if (cl == 2)
+    FSR_TRY(tc_gemms<2>(ctx, L, Wk, n, r, b, topk));
+  else
+    FSR_TRY(tc_gemms<4>(ctx, L, Wk, n, r, b, topk));
+  {
+    StageTimer timer(ctx, FSR_STAGE_TOPK);
+    const size_t fsm = kFinishSmem;
+    FSR_TRY(ensure_smem(ctx, k9t_finish_kernel, fsm));
+    k9t_finish_kernel<<<(unsigned)b, kFinishThreads, fsm, ctx->stream>>>(
+        L.cb, Wk.qpar, Wk.thr, Wk.cand, Wk.cval, Wk.ccount, Wk.nlow, u_indptr, u_indices, u_values, Wk.Zs, b, eta,
+        copy, y_ptr, y_idx, y_val, topk, top_idx, top_val, Wk.nflag, Wk.nflag + 1, Wk.stats);
+    FSR_TRY(launched(ctx, "k9t_finish_kernel"));
+    const size_t esm = (size_t)kCap * 32;
+    FSR_TRY(ensure_smem(ctx, k9t_empty_kernel, esm));
+    k9t_empty_kernel<<<(unsigned)b, 256, esm, ctx->stream>>>(n, Wk.ccount, eta, copy, y_ptr, y_idx, y_val, topk,
+                                                           top_idx, top_val, Wk.nflag, Wk.nflag + 1);
+    FSR_TRY(launched(ctx, "k9t_empty_kernel"));
+    k9t_fallback_rows_kernel<<<(unsigned)ctx->num_sms * 8, 256, 0, ctx->stream>>>(
+        n, Wk.Xt, n, u_indptr, u_indices, u_values, Wk.Zs, b, eta, copy, y_ptr, y_idx, y_val, Wk.nflag,
+        Wk.nflag + 1);
+    FSR_TRY(launched(ctx, "k9t_fallback_rows_kernel"));
+    const size_t fsmem = (size_t)topk::kCap * 16;
+    FSR_TRY(ensure_smem(ctx, prune::fallback_select_kernel, fsmem));
+    prune::fallback_select_kernel<<<(unsigned)b, topk::kThreads, fsmem, ctx->stream>>>(
+        n, Wk.Xt, n, topk, top_idx, top_val, Wk.nflag, Wk.nflag + 1);
+    FSR_TRY(launched(ctx, "fallback_select_kernel"));
+  }
+  return FSR_OK;
+}
+
+int fsr_filter_tc_stats(fsr_ctx* ctx, int64_t n, int64_t r, int64_t b, const void* workspace, int32_t* out) {
+  FSR_REQUIRE(ctx, workspace && out && b >= 1, "filter_tc_stats: bad args");
+  k9t::Work Wk;
+  k9t::work_bytes(n, r, b, &Wk, const_cast<void*>(workspace));
+  FSR_CUDA(ctx, cudaMemcpyAsync(out, Wk.stats, (size_t)b * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  FSR_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  return FSR_OK;
+}
+
+int fsr_filter_tc_fallback_count(fsr_ctx* ctx, const void* workspace, int* out) {
+  FSR_REQUIRE(ctx, workspace && out, "filter_tc_fallback_count: bad args");
+  FSR_CUDA(ctx, cudaMemcpyAsync(out, workspace, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  FSR_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  return FSR_OK;
+}
+
+}  // extern "C"

@@ -71,7 +71,7 @@ __device__ __forceinline__ void query_scale(float amax, double ss, float* s, flo
 // Per query column q of Zs (r x b, ld b): amax, ||zs_q||_2 and the scale
 // s_q = 2^(14 - e) with amax < 2^e (so |zs * s| < 2^14); Zh = half(Zs * s).
 // qp[q] = {1 / s_q, Zb_q}.  Also clears the fallback counter and max c_i.
-__global__ void __launch_bounds__(256) zs_half_kernel(int64_t r, int64_t b, const float* __restrict__ Zs,
+static __global__ void __launch_bounds__(256) zs_half_kernel(int64_t r, int64_t b, const float* __restrict__ Zs,
                                                       __half* __restrict__ Zh, float2* __restrict__ qp,
                                                       int* __restrict__ nflag) {
   __shared__ float smax[8][33];
@@ -480,7 +480,7 @@ struct SelShared {
   unsigned int n_keep;
 };
 
-__global__ void __launch_bounds__(kThreads) prune_threshold_kernel(int64_t n, int64_t b, const float* __restrict__ Xt,
+static __global__ void __launch_bounds__(kThreads) prune_threshold_kernel(int64_t n, int64_t b, const float* __restrict__ Xt,
                                                                     int64_t ldx, const float* __restrict__ cb,
                                                                     const float2* __restrict__ qp, int64_t K,
                                                                     uint32_t* __restrict__ thr,
@@ -577,7 +577,7 @@ __global__ void __launch_bounds__(kThreads) prune_threshold_kernel(int64_t n, in
 // count lower >= t and collect the rows with upper >= t into cand[q] through
 // per-query global counters (a round-to-nearest pre-filter with max_i c_i
 // skips the directed-rounding work, and the read of c_i, far below t).
-__global__ void __launch_bounds__(kThreads) prune_scan_kernel(int64_t n, int segs, int64_t seg_len,
+static __global__ void __launch_bounds__(kThreads) prune_scan_kernel(int64_t n, int segs, int64_t seg_len,
                                                                const float* __restrict__ Xt, int64_t ldx,
                                                                const float* __restrict__ cb,
                                                                const int* __restrict__ cmax_bits,
@@ -619,7 +619,7 @@ __global__ void __launch_bounds__(kThreads) prune_scan_kernel(int64_t n, int seg
   }
 }
 
-__global__ void __launch_bounds__(kThreads) prune_finish_kernel(
+static __global__ void __launch_bounds__(kThreads) prune_finish_kernel(
     int64_t n, const float* __restrict__ Xt, int64_t ldx, const float* __restrict__ cb, const float2* __restrict__ qp,
     const int32_t* __restrict__ cand, const int32_t* __restrict__ ccount, const unsigned* __restrict__ nlow,
     const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices, const float* __restrict__ vals,
@@ -700,7 +700,7 @@ __global__ void __launch_bounds__(kThreads) prune_finish_kernel(
 
 // Exact fp32 scores of every summed row of the flagged queries, written over
 // the pruned values (persistent grid over (flagged query, 256-row block)).
-__global__ void __launch_bounds__(256) fallback_rows_kernel(int64_t n, float* __restrict__ Xt, int64_t ldx,
+static __global__ void __launch_bounds__(256) fallback_rows_kernel(int64_t n, float* __restrict__ Xt, int64_t ldx,
                                                             const int64_t* __restrict__ indptr,
                                                             const int32_t* __restrict__ indices,
                                                             const float* __restrict__ vals,
@@ -726,7 +726,7 @@ __global__ void __launch_bounds__(256) fallback_rows_kernel(int64_t n, float* __
 }
 
 // Exact top K of the (now exact) rows of the flagged queries.
-__global__ void __launch_bounds__(topk::kThreads) fallback_select_kernel(int64_t n, const float* __restrict__ Xt,
+static __global__ void __launch_bounds__(topk::kThreads) fallback_select_kernel(int64_t n, const float* __restrict__ Xt,
                                                                          int64_t ldx, int64_t K,
                                                                          int64_t* __restrict__ out_idx,
                                                                          float* __restrict__ out_val,

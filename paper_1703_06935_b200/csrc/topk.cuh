@@ -97,7 +97,7 @@ __device__ __forceinline__ bool before_in_rank(uint64_t ka, int64_t ia, uint64_t
   return ka > kb || (ka == kb && ia < ib);
 }
 
-__device__ void bitonic_sort(uint64_t* key, int64_t* idx, int count) {
+__device__ inline void bitonic_sort(uint64_t* key, int64_t* idx, int count) {
   int P = 1;
   while (P < count) P <<= 1;
   for (int t = count + threadIdx.x; t < P; t += blockDim.x) {

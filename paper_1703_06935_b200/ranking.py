@@ -250,10 +250,24 @@ def filter_device(dec: SpectralDecomposition, h: TransferFunction, queries: Devi
     if topk and res.top_idx is None:
         res.top_idx = torch.empty(b, topk, dtype=torch.int64, device=dev)
         res.top_val = torch.empty(b, topk, dtype=dt, device=dev)
+    U = dec.U_device
+    path = online_path(dec, b, topk if not want_x else 0, ctx)
+    if path == "tc":
+        dense = dense_layout(dec)
+        if dense is not None:
+            need = int(ctx.lib.fsr_filter_tc_workspace_bytes(n, r, b))
+            if workspace is None or workspace.numel() < need:
+                workspace = torch.empty(need, dtype=torch.uint8, device=dev)
+            ctx.call("filter_topk_tc", n, r, N.ptr(U.indptr), N.ptr(U.indices), N.ptr(U.values), N.ptr(dense),
+                     N.ptr(w), N.ptr(dec.eta_device), b, N.ptr(queries.y_ptr), N.ptr(queries.y_idx),
+                     N.ptr(queries.y_val), int(bool(copy_uncovered)), N.ptr(workspace), int(topk),
+                     N.ptr(res.top_idx), N.ptr(res.top_val))
+            ctx.last_online_path = "tc"
+            return res
     need = int(ctx.lib.fsr_filter_workspace_bytes(dtc, n, r, b, int(not want_x)))
     if workspace is None or workspace.numel() < need:
         workspace = torch.empty(need, dtype=torch.uint8, device=dev)
-    U = dec.U_device
+    ctx.last_online_path = "pruned" if path != "exact" and topk_pruned(n, b, topk, dt) else "exact"
     if dec.is_sparse:
         uargs = (1, N.ptr(U.indptr), N.ptr(U.indices), N.ptr(U.values), N.ptr(None), 0)
     else:
@@ -263,6 +277,92 @@ def filter_device(dec: SpectralDecomposition, h: TransferFunction, queries: Devi
              N.ptr(res.X if want_x else None), int(topk), N.ptr(res.top_idx if topk else None),
              N.ptr(res.top_val if topk else None))
     return res
+
+
+ONLINE_PATHS = ("tc", "pruned", "exact")
+# below this batch the tensor-core step streams the whole dense U~ for too few
+# queries; the sparse paths are faster
+TC_MIN_BATCH = 128
+
+
+def online_path(dec, b: int, topk: int, ctx=None) -> str:
+    """Which kernels a ``filter_device`` call runs: "tc" (top-k only, fp32
+    sparse U~: K9t, the certified tensor-core step of csrc/k9t.cu), "pruned"
+    (the certified fp16-gather K9h of csrc/prune.cuh), or "exact" (unpruned
+    K9 + exact top-k).  All three return the same top-k, bit for bit.  The
+    context's ``online_path`` preference ("tc" by default) and the shape
+    limits decide; ``set_topk_prune(False)`` forces "exact"."""
+    import torch
+
+    ctx = ctx or N.Context.get(dec.eta_device.device)
+    if not topk or not dec.is_sparse or dec.dtype != torch.float32 or not ctx.topk_prune:
+        return "exact"
+    pref = ctx.online_path
+    if pref == "tc" and b >= TC_MIN_BATCH and ctx.lib.fsr_filter_tc_applicable(dec.n, dec.r, b, int(topk)):
+        return "tc"
+    if pref in ("tc", "pruned") and topk_pruned(dec.n, b, topk, dec.dtype):
+        return "pruned"
+    return "exact"
+
+
+def dense_layout(dec):
+    """The fp16 dense copy of a float32 U~ (+ per-row bound factors) that the
+    tensor-core step reads (fsr_dense_u_build), built once per decomposition
+    and cached on it; None when the device lacks the memory (n x r x 2 bytes
+    plus 2 GB of headroom), in which case the sparse paths run."""
+    import torch
+
+    cached = getattr(dec, "_dense_u", None)
+    if cached is not None:
+        return cached
+    if getattr(dec, "_dense_u_failed", False):
+        return None
+    U = dec.U_device
+    dev = dec.eta_device.device
+    ctx = N.Context.get(dev)
+    nbytes = int(ctx.lib.fsr_dense_u_bytes(dec.n, dec.r))
+    free, _ = torch.cuda.mem_get_info(dev)
+    if nbytes + (2 << 30) > free:
+        torch.cuda.empty_cache()
+        free, _ = torch.cuda.mem_get_info(dev)
+        if nbytes + (2 << 30) > free:
+            dec._dense_u_failed = True
+            return None
+    buf = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    ctx.call("dense_u_build", dec.n, dec.r, N.ptr(U.indptr), N.ptr(U.indices), N.ptr(U.values), N.ptr(buf))
+    dec._dense_u = buf
+    return buf
+
+
+def last_fallback_count(workspace, dec, b: int, ctx=None) -> int:
+    """Queries of the last certified call (tc or pruned) that went through the
+    exact fallback."""
+    import ctypes
+
+    ctx = ctx or N.Context.get(dec.eta_device.device)
+    if ctx.last_online_path == "tc":
+        out = ctypes.c_int()
+        ctx.call("filter_tc_fallback_count", N.ptr(workspace), ctypes.byref(out))
+        return int(out.value)
+    return pruned_fallback_count(workspace, dec.n, dec.r, b)
+
+
+def last_tc_stats(workspace, dec, b: int):
+    """(candidate rows, rows re-scored exactly) per query of the last
+    tensor-core call, as an int32 array (b x 2)."""
+    ctx = N.Context.get(dec.eta_device.device)
+    out = np.zeros((b, 2), dtype=np.int32)
+    ctx.call("filter_tc_stats", dec.n, dec.r, b, N.ptr(workspace), out.ctypes.data)
+    return out
+
+
+def filter_workspace_bytes(dec, b: int, want_x: bool, topk: int = 0) -> int:
+    """Workspace bytes ``filter_device`` needs for this call's path."""
+    ctx = N.Context.get(dec.eta_device.device)
+    need = int(ctx.lib.fsr_filter_workspace_bytes(N.dtype_code(dec.dtype), dec.n, dec.r, b, int(not want_x)))
+    if not want_x and online_path(dec, b, topk, ctx) == "tc":
+        need = max(need, int(ctx.lib.fsr_filter_tc_workspace_bytes(dec.n, dec.r, b)))
+    return need
 
 
 def topk_pruned(n: int, b: int, k: int, dtype, sparse: bool = True) -> bool:
@@ -697,8 +797,7 @@ class FilterGraph:
         self.res = FilterResult(top_idx=torch.empty(b, topk, dtype=torch.int64, device=dev),
                                 top_val=torch.empty(b, topk, dtype=dt, device=dev))
         ctx = N.Context.get(dev)
-        need = int(ctx.lib.fsr_filter_workspace_bytes(N.dtype_code(dt), dec.n, dec.r, b, 1))
-        self.ws = torch.empty(need, dtype=torch.uint8, device=dev)
+        self.ws = torch.empty(filter_workspace_bytes(dec, b, want_x=False, topk=topk), dtype=torch.uint8, device=dev)
         self.copy_uncovered = copy_uncovered
         self._done = None
         _weights_device(dec, h)  # cache h(Lambda) on the device before capture

@@ -55,13 +55,27 @@ def queries(n, b, seed, k=50, empty=(), extra=None):
     return ranking.QueryBatch.from_vectors(ys)
 
 
+# the certified paths under test: K9t (tensor cores, csrc/k9t.cu) and K9h (fp16 gathers, csrc/prune.cuh)
+PATHS = ["tc", "pruned"]
+
+
+@pytest.fixture(params=PATHS)
+def path(request):
+    ctx = N.Context.get()
+    old = ctx.online_path
+    ctx.set_online_path(request.param)
+    yield request.param
+    ctx.set_online_path(old)
+
+
 def both(dec, qb, K=100, h=None, flags=None):
+    """(certified path top-k, unpruned fp32 path top-k) of the same batch."""
     h = h or ranking.h_alpha(0.99)
     ctx = N.Context.get()
     dq = ranking.DeviceQueries(qb, dec.dtype, dec.eta_device.device)
-    need = int(ctx.lib.fsr_filter_workspace_bytes(N.F32, dec.n, dec.r, qb.b, 1))
-    ws = torch.empty(need, dtype=torch.uint8, device=dec.eta_device.device)
-    assert ranking.topk_pruned(dec.n, qb.b, K, dec.dtype)
+    ws = torch.empty(ranking.filter_workspace_bytes(dec, qb.b, want_x=False, topk=K), dtype=torch.uint8,
+                     device=dec.eta_device.device)
+    assert ranking.online_path(dec, qb.b, K) == ctx.online_path
     out = []
     for prune in (True, False):
         ctx.set_topk_prune(prune)
@@ -69,15 +83,17 @@ def both(dec, qb, K=100, h=None, flags=None):
             r = ranking.filter_device(dec, h, dq, topk=K, want_x=False, workspace=ws)
             torch.cuda.synchronize()
             out.append((r.top_idx.cpu().numpy(), r.top_val.cpu().numpy()))
-            if prune and flags is not None:
-                flags.append(ranking.pruned_fallback_count(ws, dec.n, dec.r, qb.b))
+            if prune:
+                assert ctx.last_online_path == ctx.online_path
+                if flags is not None:
+                    flags.append(ranking.last_fallback_count(ws, dec, qb.b))
         finally:
             ctx.set_topk_prune(True)
     return out
 
 
 @pytest.mark.parametrize("seed", [0, 1])
-def test_pruned_topk_identical_to_unpruned(seed):
+def test_pruned_topk_identical_to_unpruned(seed, path):
     n, r, b = 150_000, 600, 256
     host, dec = make_dec(n, r, 40, seed)
     qb = queries(n, b, seed + 10)
@@ -96,7 +112,7 @@ def test_pruned_topk_identical_to_unpruned(seed):
         np.testing.assert_allclose(pv[j], x[pi[j]], rtol=1e-4, atol=1e-5 * np.abs(x).max())
 
 
-def test_pruned_ties_empty_uncovered_and_fallback():
+def test_pruned_ties_empty_uncovered_and_fallback(path):
     n, r, b = 140_000, 400, 256
     # 5000 identical rows overflow the candidate buffer for queries that hit row 1;
     # every 97th row is empty (uncovered when observed)
@@ -105,7 +121,9 @@ def test_pruned_ties_empty_uncovered_and_fallback():
     qb = queries(n, b, 4, empty=(2, 200), extra=extra)
     fl = []
     (pi, pv), (ui, uv) = both(dec, qb, flags=fl)
-    assert fl[0] >= 4  # the two empty observations and the queries on the duplicated rows
+    # K9h: the two empty observations and the queries on the duplicated rows;
+    # K9t answers empty observations directly (k9t_empty), not by the fallback
+    assert fl[0] >= (4 if path == "pruned" else 2)
     np.testing.assert_array_equal(pi, ui)
     np.testing.assert_array_equal(pv.view(np.uint32), uv.view(np.uint32))
     # empty observation: all-zero scores, first K indices
@@ -118,7 +136,7 @@ def test_pruned_ties_empty_uncovered_and_fallback():
             assert pv[j][list(pi[j]).index(i)] == np.float32(yv[i])
 
 
-def test_pruned_heat_kernel_k_range_ragged_batch():
+def test_pruned_heat_kernel_k_range_ragged_batch(path):
     n, r, b = 131_072 + 5, 300, 264  # n not a multiple of 4, b not a multiple of the 256-column panel
     _, dec = make_dec(n, r, 20, 8)
     qb = queries(n, b, 9, k=30)
@@ -128,7 +146,7 @@ def test_pruned_heat_kernel_k_range_ragged_batch():
         np.testing.assert_array_equal(pv.view(np.uint32), uv.view(np.uint32))
 
 
-def test_filter_graph_partial_batch_on_pruned_path():
+def test_filter_graph_partial_batch_on_pruned_path(path):
     """A CUDA-graph step over a partial batch (the padding queries are empty
     observations) returns the unpruned fp32 top-k for the real queries."""
     n, r, b = 140_000, 300, 256
@@ -150,7 +168,7 @@ def test_filter_graph_partial_batch_on_pruned_path():
     np.testing.assert_array_equal(gv.view(np.uint32), r_.top_val.cpu().numpy().view(np.uint32))
 
 
-def test_pruned_nonfinite_projection_matches_unpruned():
+def test_pruned_nonfinite_projection_matches_unpruned(path):
     """A query whose projection overflows fp32 (y values of 1e300 -> inf in the
     fp32 batch) has no finite bound: the pruned path must hand it to the exact
     fallback and return what the unpruned path returns (a NaN
@@ -190,3 +208,33 @@ def test_two_devices_one_process():
             res.append((r_.top_idx.cpu().numpy(), r_.top_val.cpu().numpy()))
     np.testing.assert_array_equal(res[0][0], res[1][0])
     np.testing.assert_array_equal(res[0][1].view(np.uint32), res[1][1].view(np.uint32))
+
+
+@pytest.mark.parametrize("b", [1, 7, 64, 200])
+def test_tc_small_and_odd_batches(b, monkeypatch):
+    """K9t at batch widths below its default minimum (forced) and not a
+    multiple of the 256-query tile: same top-k as the unpruned path."""
+    monkeypatch.setattr(ranking, "TC_MIN_BATCH", 1)
+    n, r = 70_001, 257
+    _, dec = make_dec(n, r, 25, 51)
+    qb = queries(n, b, 52, empty=(0,) if b > 2 else ())
+    ctx = N.Context.get()
+    old = ctx.online_path
+    ctx.set_online_path("tc")
+    try:
+        (pi, pv), _ = both(dec, qb, K=100)
+    finally:
+        ctx.set_online_path(old)
+    # the unpruned reference in the sequential per-row order: the same queries
+    # padded with empty ones to a 256-wide batch (b <= 64 would take the narrow
+    # exact kernels, which sum a row in interleaved halves)
+    pad = ranking.QueryBatch(n, np.concatenate([qb.y_ptr, np.full(256 - b, qb.y_ptr[-1])]), qb.y_idx, qb.y_val)
+    ctx.set_topk_prune(False)
+    try:
+        r_ = ranking.filter_device(dec, ranking.h_alpha(0.99), ranking.DeviceQueries(pad, dec.dtype,
+                                   dec.eta_device.device), topk=100, want_x=False)
+        torch.cuda.synchronize()
+    finally:
+        ctx.set_topk_prune(True)
+    np.testing.assert_array_equal(pi, r_.top_idx[:b].cpu().numpy())
+    np.testing.assert_array_equal(pv.view(np.uint32), r_.top_val[:b].cpu().numpy().view(np.uint32))
