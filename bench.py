@@ -602,6 +602,13 @@ def online_sweep(dec, sdec_default, density_default, cfg, n, r, queries, device,
                        "ms_per_batch": ms / nsteps, "k9_ms": k9_ms / max(k9_cnt, 1)}
                 if pth == "tc":
                     row["k9t_dense_tflops"] = 2.0 * n * r * b / (k9_ms / max(k9_cnt, 1) * 1e-3) / 1e12
+                elif pth == "stream":
+                    # K9s select pass: per group of <= 8 queries the packed U~ (4 B per entry),
+                    # indptr (8 B) and the bound factors (4 B) per row stream from HBM once
+                    nb = next(v for v in (8, 4, 2, 1) if v <= b)
+                    s_bytes = -(-b // nb) * (4 * kept + 12 * n)
+                    row["k9s_stream_gbs"] = s_bytes / (k9_ms / max(k9_cnt, 1) * 1e-3) / 1e9
+                    row["k9s_hbm_frac"] = row["k9s_stream_gbs"] / load_peaks()[0]
                 else:
                     row["k9_algorithmic_gbs"] = k9_bytes / (k9_ms / max(k9_cnt, 1) * 1e-3) / 1e9
                 row["useful_fp32_tflops"] = 2.0 * kept * b / (k9_ms / max(k9_cnt, 1) * 1e-3) / 1e12

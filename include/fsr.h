@@ -206,6 +206,59 @@ int fsr_threshold_compact(fsr_ctx* ctx, int dtype, int64_t n_rows, int64_t r, co
                           const int64_t* gt, const int64_t* eq, int64_t* indptr_out,
                           int32_t* indices_out, void* values_out, double* eta, int64_t* nnz_host);
 
+/* ---- Operator level: the reference's offline functions as one call each ----
+ * (the schedule spectral.py used to own, now in csrc/fsr_ops.cu).
+ * Device arrays are row-major; temporaries are stream-ordered on the context
+ * stream; calls that return host values synchronise it.
+ * fsr_schedule_trace: ';'-separated orthonormalisation steps of the last
+ * fsr_range_finder / fsr_orthonormalize call (e.g. "start;precond(dev=0.03);
+ * precond+gram(dev=0.04)"), valid until the next such call on ctx. */
+enum fsr_si_flags {
+  FSR_SI_SPAN_ONLY = 1,         /* fp32: rounds 1..q-1 only precondition (span(Q) reaches the output) */
+  FSR_SI_FUSED_RR = 2,          /* fp32: last round preconditioned, its exact Gram goes to Rayleigh-Ritz */
+  FSR_SI_FAST_FIRST_APPLY = 4,  /* fp32: first CholeskyQR pass applies a 7-bit R^-1 */
+  FSR_SI_DEFAULT = 7
+};
+/* numpy's Philox key for a seed: SeedSequence(seed).generate_state(2, uint64)
+ * (the key fsr_gaussian_block takes; spectral.py:55-65).  Host only. */
+void fsr_philox_key(uint64_t seed, uint64_t* key0, uint64_t* key1);
+const char* fsr_schedule_trace(fsr_ctx* ctx);
+/* Y (n x k, ld) <- an orthonormal basis of its span: CholeskyQR2, Householder
+ * fallback (spectral.py:165-169 np.linalg.qr + the re-orthogonalisation check). */
+int fsr_orthonormalize(fsr_ctx* ctx, int dtype, int64_t n, int64_t k, void* Y, int64_t ldy);
+/* range_finder(A, r_hat, q, seed) (spectral.py:147-171) on the CSR A (n x n,
+ * values in dtype).  Q, B: caller blocks n x r_hat (ld = r_hat); on return Q
+ * is the last basis and B = A Q.  With FSR_SI_FUSED_RR (fp32) and gram_out
+ * (r_hat x r_hat fp64, device) non-NULL the last basis is only well
+ * conditioned and gram_out = Q^T Q; *gram_valid says whether that happened
+ * (pass gram_out to fsr_rayleigh_ritz then).  EINVAL: r_hat outside [1, n],
+ * q < 1 (spectral.py:158-161). */
+int fsr_range_finder(fsr_ctx* ctx, int dtype, int64_t n, const int64_t* indptr, const int32_t* indices,
+                     const void* values, int64_t r_hat, int q, uint64_t seed, int flags, void* Q, void* B,
+                     double* gram_out, int* gram_valid);
+/* approx_eigendecomposition (spectral.py:174-198): C = Q^T B, eigh (C v =
+ * lambda G v when gram != NULL), top r descending (stable), U = Q V (n x r,
+ * dtype), column signs (spectral.py:133-138), eta = row norms (device fp64).
+ * lam_host[r].  EINVAL: r outside [1, r_hat]. */
+int fsr_rayleigh_ritz(fsr_ctx* ctx, int dtype, int64_t n, int64_t r_hat, const void* Q, int64_t ldq,
+                      const void* B, int64_t ldb, const double* gram, int64_t r, double* lam_host, void* U,
+                      int64_t ldu, double* eta);
+/* decompose(A, r, p, q, seed) (spectral.py:297-309): r_hat = min(r + p, n). */
+int fsr_decompose(fsr_ctx* ctx, int dtype, int64_t n, const int64_t* indptr, const int32_t* indices,
+                  const void* values, int64_t r, int64_t p, int q, uint64_t seed, int flags, double* lam_host,
+                  void* U, int64_t ldu, double* eta);
+/* sparsify(dec, tau) (spectral.py:269-294) on the dense U (n x r): exactly
+ * keep = min(tau, nnz(U)) entries of largest |u|, ties in (row, col) order.
+ * fsr_sparsify_select returns the threshold key, the ties taken and keep (to
+ * size the outputs); fsr_sparsify writes the CSR (indptr n+1, indices and
+ * values of >= keep capacity), eta of the kept rows and *nnz_host = keep.
+ * EINVAL: tau < 1. */
+int fsr_sparsify_select(fsr_ctx* ctx, int dtype, int64_t n, int64_t r, const void* U, int64_t ldu, int64_t tau,
+                        uint64_t* T_out, int64_t* ties_out, int64_t* keep_out);
+int fsr_sparsify(fsr_ctx* ctx, int dtype, int64_t n, int64_t r, const void* U, int64_t ldu, int64_t tau,
+                 int64_t* indptr_out, int32_t* indices_out, void* values_out, int64_t capacity, double* eta,
+                 int64_t* nnz_host);
+
 /* ---- K8/K9: online batch  (ranking.py:219-255 _project / filter) ------------
  * For b observation columns y_j (CSC: y_ptr[b+1], y_idx row ids, y_val in dtype):
  *   z_j = U[supp y_j]^T y_j            (K8, ranking.py:219-226)
@@ -252,6 +305,28 @@ int fsr_filter_tc_fallback_count(fsr_ctx* ctx, const void* workspace, int* out);
  * exactly), b int32 pairs to host memory (zeros for queries not finished by
  * the certified selection). */
 int fsr_filter_tc_stats(fsr_ctx* ctx, int64_t n, int64_t r, int64_t b, const void* workspace, int32_t* out);
+
+/* K9s: the same certified top-k for small batches (the tensor-core step needs
+ * b >= 128 queries to amortise streaming the dense U~).  Replaces, like
+ * fsr_filter_topk_tc, ranking.filter + rank (ranking.py:229-255, 390-395)
+ * for a batch; the same top_idx / top_val as the unpruned sequential-order
+ * fp32 path bit for bit.  stream_u: fsr_stream_u_bytes(n, r, nnz) bytes
+ * (256-aligned) built once per U~ by fsr_stream_u_build (4-byte packed
+ * entries fp16 value << 16 | column, r <= 65536, per-row bound factors, chunk
+ * table).  workspace: fsr_filter_stream_workspace_bytes(n, r, b) bytes; its
+ * first int is the fallback count (fsr_filter_tc_fallback_count) and
+ * fsr_filter_tc_stats reads its diagnostics.  Shapes:
+ * fsr_filter_stream_applicable. */
+int64_t fsr_stream_u_bytes(int64_t n, int64_t r, int64_t nnz);
+int fsr_stream_u_build(fsr_ctx* ctx, int64_t n, int64_t r, int64_t nnz, const int64_t* u_indptr,
+                       const int32_t* u_indices, const float* u_values, void* stream_u);
+int fsr_filter_stream_applicable(int64_t n, int64_t r, int64_t nnz, int64_t b, int64_t topk);
+int64_t fsr_filter_stream_workspace_bytes(int64_t n, int64_t r, int64_t b);
+int fsr_filter_topk_stream(fsr_ctx* ctx, int64_t n, int64_t r, int64_t nnz, const int64_t* u_indptr,
+                           const int32_t* u_indices, const float* u_values, const void* stream_u,
+                           const float* w, const double* eta, int64_t b, const int64_t* y_ptr,
+                           const int64_t* y_idx, const float* y_val, int copy_uncovered,
+                           void* workspace, int64_t topk, int64_t* top_idx, float* top_val);
 
 /* Top-k of every row of X (b x n): indices/values ordered by (-x, index). */
 int fsr_topk_rows(fsr_ctx* ctx, int dtype, int64_t b, int64_t n, const void* X, int64_t ldx,

@@ -75,6 +75,25 @@ _SIGS = {
                                     _c_p, _c_int, _c_p, _c_i64, _c_p, _c_p]),
     "fsr_filter_tc_fallback_count": (_c_int, [_c_p, _c_p, ctypes.POINTER(_c_int)]),
     "fsr_filter_tc_stats": (_c_int, [_c_p, _c_i64, _c_i64, _c_i64, _c_p, _c_p]),
+    "fsr_philox_key": (None, [_c_u64, ctypes.POINTER(_c_u64), ctypes.POINTER(_c_u64)]),
+    "fsr_schedule_trace": (ctypes.c_char_p, [_c_p]),
+    "fsr_orthonormalize": (_c_int, [_c_p, _c_int, _c_i64, _c_i64, _c_p, _c_i64]),
+    "fsr_range_finder": (_c_int, [_c_p, _c_int, _c_i64, _c_p, _c_p, _c_p, _c_i64, _c_int, _c_u64, _c_int, _c_p, _c_p,
+                                  _c_p, ctypes.POINTER(_c_int)]),
+    "fsr_rayleigh_ritz": (_c_int, [_c_p, _c_int, _c_i64, _c_i64, _c_p, _c_i64, _c_p, _c_i64, _c_p, _c_i64, _c_dp,
+                                   _c_p, _c_i64, _c_p]),
+    "fsr_decompose": (_c_int, [_c_p, _c_int, _c_i64, _c_p, _c_p, _c_p, _c_i64, _c_i64, _c_int, _c_u64, _c_int, _c_dp,
+                               _c_p, _c_i64, _c_p]),
+    "fsr_sparsify_select": (_c_int, [_c_p, _c_int, _c_i64, _c_i64, _c_p, _c_i64, _c_i64, ctypes.POINTER(_c_u64),
+                                     _c_i64p, _c_i64p]),
+    "fsr_sparsify": (_c_int, [_c_p, _c_int, _c_i64, _c_i64, _c_p, _c_i64, _c_i64, _c_p, _c_p, _c_p, _c_i64, _c_p,
+                              _c_i64p]),
+    "fsr_stream_u_bytes": (_c_i64, [_c_i64, _c_i64, _c_i64]),
+    "fsr_stream_u_build": (_c_int, [_c_p, _c_i64, _c_i64, _c_i64, _c_p, _c_p, _c_p, _c_p]),
+    "fsr_filter_stream_applicable": (_c_int, [_c_i64, _c_i64, _c_i64, _c_i64, _c_i64]),
+    "fsr_filter_stream_workspace_bytes": (_c_i64, [_c_i64, _c_i64, _c_i64]),
+    "fsr_filter_topk_stream": (_c_int, [_c_p, _c_i64, _c_i64, _c_i64, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_i64,
+                                        _c_p, _c_p, _c_p, _c_int, _c_p, _c_i64, _c_p, _c_p]),
     "fsr_topk_rows": (_c_int, [_c_p, _c_int, _c_i64, _c_i64, _c_p, _c_i64, _c_i64, _c_p, _c_p]),
     "fsr_project_batch": (_c_int, [_c_p, _c_int, _c_i64, _c_i64, _c_int, _c_p, _c_p, _c_p, _c_p, _c_i64, _c_p,
                                    _c_i64, _c_p, _c_p, _c_p, _c_p]),
@@ -233,9 +252,11 @@ class Context:
         self.topk_prune = bool(on)
 
     def set_online_path(self, path: str):
-        """Preferred certified top-k path: "tc" (K9t tensor cores, default),
-        "pruned" (K9h fp16 gathers) or "exact" (unpruned).  Same results."""
-        if path not in ("tc", "pruned", "exact"):
+        """Preferred certified top-k path: "tc" (K9t tensor cores for b >= 128,
+        the K9s stream below; default), "stream" (K9s packed fp16 U~ streamed
+        from HBM, any b), "pruned" (K9h fp16 gathers) or "exact" (unpruned).
+        Same results."""
+        if path not in ("tc", "stream", "pruned", "exact"):
             raise ValueError(f"unknown online path {path!r}")
         self.online_path = path
 

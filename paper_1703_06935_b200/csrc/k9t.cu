@@ -389,8 +389,10 @@ __global__ void __launch_bounds__(256) k9t_threshold_kernel(int64_t b, int64_t n
                                                             const int* __restrict__ cmax_bits, int64_t target,
                                                             uint32_t* __restrict__ thr, QParam* __restrict__ qpar,
                                                             int32_t* __restrict__ ccount, unsigned* __restrict__ nlow,
-                                                            int* __restrict__ nflag, int* __restrict__ flags) {
+                                                            int* __restrict__ nflag, int* __restrict__ flags,
+                                                            const int32_t* __restrict__ n_valid_dev) {
   constexpr int KB = 32, HB = topk::kHistBits, nb = 1 << HB;
+  if (n_valid_dev) n_valid_s = *n_valid_dev;  // the streaming path's sample size lives on the device
   __shared__ unsigned hist[nb];
   __shared__ unsigned found_bin;
   __shared__ unsigned long long above;
@@ -832,7 +834,8 @@ struct Work {
   int2* stats;  // per query (candidates, rows re-scored): diagnostics
   float* Xt;
 };
-inline size_t work_bytes(int64_t n, int64_t r, int64_t b, Work* w, void* base) {
+// ks_rows: sample keys per query (K9t: sample_rows(n); the streaming path: n)
+inline size_t work_bytes(int64_t n, int64_t r, int64_t b, Work* w, void* base, int64_t ks_rows) {
   char* p = (char*)base;
   size_t off = 0;
   auto take = [&](size_t bytes) {
@@ -842,18 +845,18 @@ inline size_t work_bytes(int64_t n, int64_t r, int64_t b, Work* w, void* base) {
   };
   Work W;
   W.nflag = (int*)take((size_t)(b + 2) * 4);
+  W.stats = (int2*)take((size_t)b * 8);
   W.Zt = (float*)take((size_t)b * r * 4);
   W.Zs = (float*)take((size_t)r * b * 4);
   W.Zh = (__half*)take((size_t)b * ld_of(r) * 2);
   W.qp = (float2*)take((size_t)b * 8);
   W.qpar = (QParam*)take((size_t)b * sizeof(QParam));
-  W.Ks = (uint32_t*)take((size_t)b * sample_rows(n) * 4);
   W.thr = (uint32_t*)take((size_t)b * 4);
   W.ccount = (int32_t*)take((size_t)b * 4);
   W.nlow = (unsigned*)take((size_t)b * 4);
   W.cand = (int32_t*)take((size_t)b * kCap * 4);
   W.cval = (float*)take((size_t)b * kCap * 4);
-  W.stats = (int2*)take((size_t)b * 8);
+  W.Ks = (uint32_t*)take((size_t)b * ks_rows * 4);  // sample keys: last but one (their count differs by path)
   W.Xt = (float*)take((size_t)n * b * 4);
   if (w) *w = W;
   return off + 256;
@@ -882,7 +885,7 @@ int tc_gemms(fsr_ctx* ctx, const DenseLayout& L, const Work& Wk, int64_t n, int6
     const int64_t target = (2 * topk + kSampleStride - 1) / kSampleStride + 8;
     k9t_threshold_kernel<<<(unsigned)std::min<int64_t>(b, (int64_t)ctx->num_sms * 8), 256, 0, ctx->stream>>>(
         b, ns, n_valid_s, Wk.Ks, Wk.qp, L.cmax_bits, target, Wk.thr, Wk.qpar, Wk.ccount, Wk.nlow, Wk.nflag,
-        Wk.nflag + 1);
+        Wk.nflag + 1, nullptr);
     FSR_TRY(launched(ctx, "k9t_threshold_kernel"));
   }
   {
@@ -902,6 +905,502 @@ inline int cluster_choice() {
     return (v == 1 || v == 2 || v == 4) ? v : 2;
   }();
   return c;
+}
+
+
+// ------------------------------------------------------ small-batch stream --
+// K9s: the same certified top-K for batches too small to feed the tensor
+// cores (b < 128: K9t would stream the whole 10 GB fp16 U~ for a handful of
+// queries, the exact sparse K9 gathers fp32 rows from L2).  U~ is re-packed
+// once per decomposition into 4 bytes per entry -- fp16 value << 16 | column
+// (r <= 65536) -- 0.4 GB at C3 2% instead of the 0.8 GB fp32 CSR, and streamed
+// from HBM by 1-D TMA bulk copies into a shared-memory ring, one chunk of
+// ~kChunk entries at a time.  The NB-query slice of the scaled fp16 Zh sits in
+// shared memory as [column][query] (NB r 2 bytes); each entry costs NB
+// fma.rn.f32.f16 and a warp per row sums its entries lane-strided, then a
+// butterfly reduce-scatter (NB/2 + NB/4 + ... + log2(32/NB) shuffles).  The
+// sums differ from K9t's only in order, which the bound's gamma_m term covers,
+// and the per-row factor c_i is K9t's (it also covers the tensor-core
+// accumulation, so it is conservative here).  Threshold, finish, empty and
+// fallback are K9t's kernels: the top-K is the unpruned sequential fp32 top-K
+// bit for bit.
+namespace stream {
+
+constexpr int kChunk = 4096;       // chunk c = the rows whose first entry lies in [c kChunk, (c + 1) kChunk)
+constexpr int kConsumers = 16;     // warps summing rows; one more warp issues the chunk copies
+constexpr int kLpr = 8;            // lanes per row: 4 rows in flight per warp (rows are ~50-100 entries)
+constexpr int kThreads = 32 * (kConsumers + 1);
+constexpr int kStages = 3;
+constexpr int kSampleStride = 32;  // sample pass: every 32nd chunk
+constexpr int kRowsMax = 256;      // rows whose indptr / c_i ride along with a chunk's entries (else global reads)
+
+inline int64_t nchunks(int64_t nnz) { return std::max<int64_t>(1, (nnz + kChunk - 1) / kChunk); }
+inline int64_t nsample(int64_t nnz) { return (nchunks(nnz) + kSampleStride - 1) / kSampleStride; }
+// a chunk spans <= kChunk - 1 + (longest row <= r) entries, +3 for the 16-byte aligned start
+inline int64_t stage_words(int64_t r) { return round_up(kChunk + r + 8, 4); }
+// one stage: entries | indptr slice (kRowsMax + 4 int64) | c_i slice (kRowsMax + 8 floats)
+constexpr int kIpWords = 2 * (kRowsMax + 4), kCbWords = kRowsMax + 8;
+inline int64_t stage_total_words(int64_t r) { return stage_words(r) + kIpWords + kCbWords; }
+inline size_t smem_bytes(int nb, int64_t r) {
+  return (size_t)kStages * stage_total_words(r) * 4 + (size_t)round_up((int64_t)nb * r * 2, 16) + 64 +
+         (size_t)nb * 24 + kStages * 24 + 16 + (size_t)2 * kRowsMax * nb * 4;
+}
+
+struct Layout {
+  uint32_t* pk;    // [nnz + 16] fp16 value << 16 | column
+  int64_t* ipl;    // [n + 16] copy of indptr (padded: 16-byte TMA reads past row n stay inside)
+  float* cb;       // [n (+ pad)] per-row bound factor (K9t's row_bound)
+  int* cmax_bits;  // max c_i (as int bits)
+  int32_t* crow;   // [nchunks + 1] first row of each chunk
+  longlong2* desc; // [nchunks + 1] (first row, its first entry) of each chunk: the producer's one load
+  int32_t* soff;   // [nsample + 1] first sample slot of each sampled chunk; soff[nsample] = sampled rows
+};
+inline Layout layout(void* base, int64_t n, int64_t nnz) {
+  char* p = (char*)base;
+  Layout L;
+  L.pk = (uint32_t*)p;
+  p += al256((size_t)(nnz + 16) * 4);
+  L.ipl = (int64_t*)p;
+  p += al256((size_t)(n + 16) * 8);
+  L.cb = (float*)p;
+  p += al256((size_t)n * 4 + 64);
+  L.cmax_bits = (int*)p;
+  p += 256;
+  L.crow = (int32_t*)p;
+  p += al256((size_t)(nchunks(nnz) + 1) * 4);
+  L.desc = (longlong2*)p;
+  p += al256((size_t)(nchunks(nnz) + 1) * 16);
+  L.soff = (int32_t*)p;
+  return L;
+}
+inline size_t layout_bytes(int64_t n, int64_t nnz) {
+  return al256((size_t)(nnz + 16) * 4) + al256((size_t)(n + 16) * 8) + al256((size_t)n * 4 + 64) + 256 +
+         al256((size_t)(nchunks(nnz) + 1) * 4) + al256((size_t)(nchunks(nnz) + 1) * 16) +
+         al256((size_t)(nsample(nnz) + 1) * 4);
+}
+
+// warp per row: packed entries + the bound factor of densify_kernel
+__global__ void __launch_bounds__(256) pack_kernel(int64_t n, const int64_t* __restrict__ indptr,
+                                                   const int32_t* __restrict__ indices, const float* __restrict__ vals,
+                                                   uint32_t* __restrict__ pk, float* __restrict__ cb,
+                                                   int* __restrict__ cmax_bits) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  int cmax = 0;
+  for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < n; i += nw) {
+    const int64_t e0 = indptr[i], e1 = indptr[i + 1];
+    float ss = 0.f;
+    for (int64_t e = e0 + lane; e < e1; e += 32) {
+      const float v = vals[e];
+      ss = __fmaf_ru(v, v, ss);
+      pk[e] = ((uint32_t)__half_as_ushort(__float2half_rn(v)) << 16) | (uint32_t)indices[e];
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) ss = __fadd_ru(ss, __shfl_xor_sync(0xffffffffu, ss, o));
+    if (lane == 0) {
+      const float c = e1 > e0 ? row_bound((double)(e1 - e0), ss) : 0.f;
+      cb[i] = c;
+      cmax = max(cmax, __float_as_int(c));
+    }
+  }
+  if (lane == 0) atomicMax(cmax_bits, cmax);
+}
+
+// crow[c] = first row whose first entry is >= c kChunk (crow[nch] = n)
+__global__ void chunk_rows_kernel(int64_t n, const int64_t* __restrict__ indptr, int64_t nch,
+                                  int32_t* __restrict__ crow) {
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c > nch) return;
+  if (c == nch || c == 0) {
+    crow[c] = c == 0 ? 0 : (int32_t)n;
+    return;
+  }
+  const int64_t target = c * kChunk;
+  int64_t lo = 0, hi = n;  // indptr[n] = nnz > target
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (indptr[mid] >= target)
+      hi = mid;
+    else
+      lo = mid + 1;
+  }
+  crow[c] = (int32_t)lo;
+}
+
+__global__ void chunk_desc_kernel(const int64_t* __restrict__ indptr, int64_t nch, const int32_t* __restrict__ crow,
+                                  longlong2* __restrict__ desc) {
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c <= nch) desc[c] = make_longlong2(crow[c], indptr[crow[c]]);
+}
+
+__global__ void sample_offsets_kernel(int64_t nch, const int32_t* __restrict__ crow, int32_t* __restrict__ soff) {
+  if (threadIdx.x || blockIdx.x) return;
+  const int64_t ns = (nch + kSampleStride - 1) / kSampleStride;
+  int32_t s = 0;
+  for (int64_t j = 0; j < ns; ++j) {
+    soff[j] = s;
+    s += crow[j * kSampleStride + 1] - crow[j * kSampleStride];
+  }
+  soff[ns] = s;
+}
+
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
+// acc[q] += u * zh[col][q] for the NB queries (fp16 x fp16 -> fp32, one FHFMA each)
+template <int NB>
+__device__ __forceinline__ void entry_fma(uint32_t w, const __half* __restrict__ zh, float (&acc)[NB]) {
+  const uint16_t u = (uint16_t)(w >> 16);
+  const uint32_t col = w & 0xffffu;
+  if constexpr (NB == 1) {
+    const uint16_t z = __half_as_ushort(zh[col]);
+    asm("{ .reg .f16 a, z; mov.b16 a, %1; mov.b16 z, %2; fma.rn.f32.f16 %0, a, z, %0; }"
+        : "+f"(acc[0])
+        : "h"(u), "h"(z));
+  } else if constexpr (NB == 2) {
+    prune::fhfma2(reinterpret_cast<const uint32_t*>(zh)[col], u, acc[0], acc[1]);
+  } else if constexpr (NB == 4) {
+    const uint2 z = reinterpret_cast<const uint2*>(zh)[col];
+    prune::fhfma2(z.x, u, acc[0], acc[1]);
+    prune::fhfma2(z.y, u, acc[2], acc[3]);
+  } else {
+    static_assert(NB == 8, "NB in {1, 2, 4, 8}");
+    const uint4 z = reinterpret_cast<const uint4*>(zh)[col];
+    prune::fhfma2(z.x, u, acc[0], acc[1]);
+    prune::fhfma2(z.y, u, acc[2], acc[3]);
+    prune::fhfma2(z.z, u, acc[4], acc[5]);
+    prune::fhfma2(z.w, u, acc[6], acc[7]);
+  }
+}
+
+// Butterfly reduce-scatter of NB per-lane partial sums over a kLpr-lane group:
+// returns the group sum of query qidx(lane) (group lane bits high to low).
+template <int NB>
+__device__ __forceinline__ float reduce_scatter(float (&a)[NB], int lane) {
+  static_assert(NB <= kLpr, "one query per lane at least");
+#pragma unroll
+  for (int h = NB / 2, off = kLpr / 2; h >= 1; h >>= 1, off >>= 1) {
+    const bool upper = lane & off;
+#pragma unroll
+    for (int j = 0; j < h; ++j) {
+      const float send = upper ? a[j] : a[j + h];
+      const float keep = upper ? a[j + h] : a[j];
+      a[j] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+    }
+  }
+#pragma unroll
+  for (int off = kLpr / 2 / NB; off >= 1; off >>= 1) a[0] += __shfl_xor_sync(0xffffffffu, a[0], off);
+  return a[0];
+}
+template <int NB>
+__device__ __forceinline__ int qidx(int lane) {
+  static_assert(kLpr == 8, "lane bits 2, 1, 0 of the group");
+  int q = 0;
+#pragma unroll
+  for (int t = 0, b = 2; (1 << t) < NB; ++t, --b) q = (q << 1) | ((lane >> b) & 1);  // bit of offset kLpr/2 first
+  return q;
+}
+
+// MODE 0 (sample): every kSampleStride-th chunk, lower keys into Ks[q * ns + soff + row-in-chunk].
+// MODE 1 (select): every chunk; counts lower >= t, appends rows with upper >= t.
+// Queries q0 .. q0 + nq - 1 (nq <= NB); one CTA per SM, persistent over chunks.
+template <int MODE, int NB>
+__global__ void __launch_bounds__(kThreads, 1)
+    stream_kernel(const uint32_t* __restrict__ pk, const int64_t* __restrict__ indptr,
+                  const longlong2* __restrict__ desc, int64_t nch, int r, int sw, const __half* __restrict__ Zh,
+                  int64_t ldzh, int q0, int nq, const float* __restrict__ cb, const float2* __restrict__ qp,
+                  const QParam* __restrict__ qpar, const uint32_t* __restrict__ thr, const int32_t* __restrict__ soff,
+                  uint32_t* __restrict__ Ks, int64_t ns, int32_t* __restrict__ cand, float* __restrict__ cval,
+                  int32_t* __restrict__ ccount, unsigned* __restrict__ nlow) {
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  const int stw = sw + kIpWords + kCbWords;                                  // words per stage
+  uint32_t* stage = (uint32_t*)smem_raw;                                     // [kStages][stw]
+  __half* zh = (__half*)(stage + (size_t)kStages * stw);                      // [r][NB]
+  float4* sp = (float4*)(smem_raw + (size_t)kStages * stw * 4 + round_up((int64_t)NB * r * 2, 16));  // [NB]
+  uint64_t* full = (uint64_t*)(sp + NB);         // [kStages]; sp = (tf_pre | 0, 1/s_q, cz, zb)
+  uint64_t* empty = full + kStages;              // [kStages]
+  int2* meta = (int2*)(empty + kStages);         // [kStages] (first row, rows) of the staged chunk
+  uint32_t* sthr = (uint32_t*)(meta + kStages);  // [NB]
+  unsigned* scnt = sthr + NB;                    // [NB]
+  float* xs = (float*)(((uintptr_t)(scnt + NB) + 15) & ~(uintptr_t)15);  // [2][kRowsMax][NB] row sums
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t step = MODE == 0 ? (int64_t)kSampleStride * gridDim.x : gridDim.x;
+  const int64_t c_first = MODE == 0 ? (int64_t)kSampleStride * blockIdx.x : blockIdx.x;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kConsumers);
+    }
+    fence_barrier_init();
+  }
+  // the queries' fp16 Zh slice as [column][query] (padding queries zero) and their parameters
+  for (int64_t t = threadIdx.x; t < (int64_t)r * NB; t += kThreads) {
+    const int q = (int)(t % NB);
+    const int64_t col = t / NB;
+    zh[t] = q < nq ? Zh[(int64_t)(q0 + q) * ldzh + col] : __float2half_rn(0.f);
+  }
+  if (threadIdx.x < NB) {
+    const int q = threadIdx.x;
+    float4 p = make_float4(__int_as_float(0x7fffffff), 1.f, 0.f, 0.f);
+    uint32_t tk = 0xffffffffu;
+    if (q < nq) {
+      if (MODE == 0) {
+        const float2 v = qp[q0 + q];
+        p = make_float4(0.f, v.x, 0.f, v.y);
+      } else {
+        const QParam v = qpar[q0 + q];
+        p = make_float4(v.tf_pre, v.inv, v.cz, v.zb);
+        tk = thr[q0 + q];
+      }
+    }
+    sp[q] = p;
+    sthr[q] = tk;
+    scnt[q] = 0;
+  }
+  for (int t = threadIdx.x; t < 2 * kRowsMax * NB; t += kThreads) xs[t] = 0.f;
+  __syncthreads();
+
+  if (warp == kConsumers) {
+    // producer: chunk descriptors of the next 32 chunks in one load per lane,
+    // then lane 0 issues each chunk into the ring as soon as its stage is free.
+    // One mbarrier transaction carries the packed entries, the chunk's indptr
+    // slice and its c_i slice (chunks of more than kRowsMax rows -- runs of
+    // empty rows -- leave those two to global reads).
+    int k = 0;
+    for (int64_t cb0 = c_first; cb0 < nch; cb0 += 32 * step) {
+      const int64_t cl = cb0 + lane * step;
+      longlong2 d0 = make_longlong2(0, 0), d1 = make_longlong2(0, 0);
+      if (cl < nch) {
+        d0 = desc[cl];
+        d1 = desc[cl + 1];
+      }
+      for (int j = 0; j < 32 && cb0 + j * step < nch; ++j, ++k) {
+        const int32_t r0 = (int32_t)__shfl_sync(0xffffffffu, d0.x, j), r1 = (int32_t)__shfl_sync(0xffffffffu, d1.x, j);
+        const int64_t f = __shfl_sync(0xffffffffu, d0.y, j), e1 = __shfl_sync(0xffffffffu, d1.y, j);
+        if (lane == 0) {
+          const int s = k % kStages;
+          if (k >= kStages) mbar_wait(&empty[s], ((k / kStages) - 1) & 1);
+          uint32_t* st = stage + (size_t)s * stw;
+          meta[s] = make_int2(r0, r1 - r0);
+          const int64_t e0 = f & ~(int64_t)3;
+          const uint32_t ebytes = e1 > f ? (uint32_t)(round_up(e1 - e0, 4) * 4) : 0;
+          const bool small = r1 - r0 <= kRowsMax;
+          const int32_t i0 = r0 & ~1, c0 = r0 & ~3;
+          const uint32_t ibytes = small ? (uint32_t)(round_up((int64_t)r1 + 1 - i0, 2) * 8) : 0;
+          const uint32_t cbytes = small && r1 > r0 ? (uint32_t)(round_up((int64_t)r1 - c0, 4) * 4) : 0;
+          const uint32_t tx = ebytes + ibytes + cbytes;
+          if (tx) {
+            mbar_expect_tx(&full[s], tx);
+            if (ebytes) bulk_load(st, pk + e0, ebytes, &full[s]);
+            if (ibytes) bulk_load(st + sw, indptr + i0, ibytes, &full[s]);
+            if (cbytes) bulk_load(st + sw + kIpWords, cb + c0, cbytes, &full[s]);
+          } else {
+            mbar_arrive(&full[s]);
+          }
+        }
+        __syncwarp();
+      }
+    }
+  } else {
+    // a row's approximate score x~ (any summation order: the bound's gamma_m
+    // term covers it) -> sample key or candidate bookkeeping
+    auto row_out = [&](int32_t i, int32_t j, int q, float v, float c_i, int32_t slot0) {
+      const float4 p = sp[q];
+      const float x = v * p.y;
+      if (MODE == 0) {
+        Ks[(int64_t)(q0 + q) * ns + slot0 + j] = prune::key32(__fsub_rd(x, prune::bound_of(c_i, p.w)));
+      } else if (x + p.z >= p.x) {  // rare: within reach of the threshold
+        const float bd = prune::bound_of(c_i, p.w);
+        const uint32_t tk = sthr[q];
+        if (prune::key32(__fsub_rd(x, bd)) >= tk) atomicAdd(&scnt[q], 1u);
+        if (prune::key32(__fadd_ru(x, bd)) >= tk) {
+          const int slot = atomicAdd(ccount + q0 + q, 1);
+          if (slot < kCap) {
+            cand[(int64_t)(q0 + q) * kCap + slot] = i;
+            cval[(int64_t)(q0 + q) * kCap + slot] = x;
+          }
+        }
+      }
+    };
+    constexpr int kCT = 32 * kConsumers;  // consumer threads
+    const int ct = threadIdx.x;
+    const int myq = qidx<NB>(lane);
+    const bool leader = (lane & (kLpr / NB - 1)) == 0 && myq < nq;
+    int k = 0;
+    for (int64_t c = c_first; c < nch; c += step, ++k) {
+      const int s = k % kStages;
+      mbar_wait(&full[s], (k / kStages) & 1);
+      const int2 mt = meta[s];
+      const int32_t r0 = mt.x, nr = mt.y;
+      const uint32_t* sb = stage + (size_t)s * stw;
+      const int64_t* sip = (const int64_t*)(sb + sw) + (r0 & 1);  // sip[j] = indptr[r0 + j]
+      const float* scb = (const float*)(sb + sw + kIpWords) + (r0 & 3);
+      const int32_t slot0 = MODE == 0 ? soff[c / kSampleStride] : 0;
+      if (nr <= kRowsMax) {
+        // merge-style split: every consumer thread takes an equal run of the
+        // chunk's entries whatever the row lengths (C3's rows run from 1 to
+        // >2000 entries), sums them per row and adds the partial row sums
+        // into shared memory; then one thread per (row, query) finishes it
+        float* xk = xs + (k & 1) * kRowsMax * NB;  // double-buffered: the next chunk sums while this one finishes
+        const int64_t f = sip[0], m = sip[nr] - f;
+        const int64_t base = f & ~(int64_t)3;
+        const int64_t a = f + (m * ct) / kCT, b = f + (m * (ct + 1)) / kCT;
+        if (a < b) {
+          int lo = 0, hi = nr - 1;  // the row of entry a: largest j with sip[j] <= a
+          while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (sip[mid] <= a)
+              lo = mid;
+            else
+              hi = mid - 1;
+          }
+          int32_t j = lo;
+          int64_t next = sip[j + 1];
+          float acc[NB];
+#pragma unroll
+          for (int q = 0; q < NB; ++q) acc[q] = 0.f;
+          auto flush = [&]() {
+#pragma unroll
+            for (int q = 0; q < NB; ++q)
+              if (acc[q] != 0.f) {
+                atomicAdd(&xk[j * NB + q], acc[q]);
+                acc[q] = 0.f;
+              }
+          };
+          for (int64_t e = a; e < b; e += 4) {
+            uint32_t w[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) w[u] = e + u < b ? sb[e + u - base] : 0u;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              if (e + u < b) {
+                while (e + u >= next) {
+                  flush();
+                  ++j;
+                  next = sip[j + 1];
+                }
+                entry_fma<NB>(w[u], zh, acc);
+              }
+            }
+          }
+          flush();
+        }
+        asm volatile("bar.sync 1, %0;" ::"r"(kCT) : "memory");  // every partial sum of this chunk is in xk
+        for (int t = ct; t < nr * NB; t += kCT) {
+          const int32_t j = t / NB;
+          const int q = t - j * NB;
+          if (q < nq) row_out(r0 + j, j, q, xk[t], scb[j], slot0);
+          xk[t] = 0.f;
+        }
+      } else {
+        // a run of (mostly empty) rows longer than the staged slices: a lane
+        // group per row, indptr and c_i from global memory.  The barrier keeps
+        // the row-sum buffers' reuse ordered (the previous small chunk's
+        // finishing threads are done with theirs before the next small chunk)
+        asm volatile("bar.sync 1, %0;" ::"r"(kCT) : "memory");
+        const int64_t base = __ldg(indptr + r0) & ~(int64_t)3;
+        constexpr int kGroups = 32 / kLpr;  // rows per warp in flight
+        const int gl = lane & (kLpr - 1);
+        for (int32_t jb = warp * kGroups; jb < nr; jb += kConsumers * kGroups) {
+          const int32_t j = jb + lane / kLpr;  // this lane group's row (warp-uniform loop, ragged tail idles)
+          int64_t e0 = 0, e1 = 0;
+          if (j < nr) {
+            e0 = __ldg(indptr + r0 + j);
+            e1 = __ldg(indptr + r0 + j + 1);
+          }
+          float acc[NB];
+#pragma unroll
+          for (int q = 0; q < NB; ++q) acc[q] = 0.f;
+          for (int64_t e = e0 + gl; e < e1; e += kLpr) entry_fma<NB>(sb[e - base], zh, acc);
+          const float v = reduce_scatter<NB>(acc, lane);
+          if (leader && j < nr) row_out(r0 + j, j, myq, v, __ldg(cb + r0 + j), slot0);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);  // this warp is done with stage s
+    }
+  }
+  __syncthreads();
+  if (MODE == 1 && threadIdx.x < nq && scnt[threadIdx.x]) atomicAdd(nlow + q0 + threadIdx.x, scnt[threadIdx.x]);
+}
+
+// largest NB in {8, 4, 2, 1} not above b whose shared memory fits; 0 if none does
+inline int pick_nb(int64_t b, int64_t r) {
+  for (int nb = 8; nb >= 1; nb >>= 1)
+    if ((nb <= b || nb == 1) && smem_bytes(nb, r) <= 227 * 1024) return nb;
+  return 0;
+}
+
+template <int MODE, int NB>
+int launch(fsr_ctx* ctx, const Layout& L, const Work& Wk, const int64_t* indptr, int64_t nnz, int64_t n, int64_t r,
+           int64_t b, int q0, int nq) {
+  const size_t smem = smem_bytes(NB, r);
+  FSR_TRY(ensure_smem(ctx, stream_kernel<MODE, NB>, smem));
+  const int64_t nch = nchunks(nnz);
+  const int64_t work = MODE == 0 ? nsample(nnz) : nch;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(work, ctx->num_sms));
+  stream_kernel<MODE, NB><<<grid, kThreads, smem, ctx->stream>>>(
+      L.pk, L.ipl, L.desc, nch, (int)r, (int)stage_words(r), Wk.Zh, ld_of(r), q0, nq, L.cb, Wk.qp, Wk.qpar, Wk.thr,
+      L.soff, Wk.Ks, n, Wk.cand, Wk.cval, Wk.ccount, Wk.nlow);
+  return launched(ctx, MODE == 0 ? "k9s_stream_sample" : "k9s_stream_select");
+}
+
+template <int MODE>
+int launch_groups(fsr_ctx* ctx, const Layout& L, const Work& Wk, const int64_t* indptr, int64_t nnz, int64_t n,
+                  int64_t r, int64_t b) {
+  const int nb = pick_nb(b, r);
+  for (int64_t q0 = 0; q0 < b; q0 += nb) {
+    const int nq = (int)std::min<int64_t>(nb, b - q0);
+    if (nb == 8)
+      FSR_TRY((launch<MODE, 8>(ctx, L, Wk, indptr, nnz, n, r, b, (int)q0, nq)));
+    else if (nb == 4)
+      FSR_TRY((launch<MODE, 4>(ctx, L, Wk, indptr, nnz, n, r, b, (int)q0, nq)));
+    else if (nb == 2)
+      FSR_TRY((launch<MODE, 2>(ctx, L, Wk, indptr, nnz, n, r, b, (int)q0, nq)));
+    else
+      FSR_TRY((launch<MODE, 1>(ctx, L, Wk, indptr, nnz, n, r, b, (int)q0, nq)));
+  }
+  return FSR_OK;
+}
+
+}  // namespace stream
+
+
+// finish (exact re-score of the kept candidates, sort), empty observations,
+// fallback: shared by K9t and the streaming path
+inline int finish_stage(fsr_ctx* ctx, const float* cb, const Work& Wk, int64_t n, int64_t b, const int64_t* u_indptr,
+                        const int32_t* u_indices, const float* u_values, const double* eta, int copy,
+                        const int64_t* y_ptr, const int64_t* y_idx, const float* y_val, int64_t topk,
+                        int64_t* top_idx, float* top_val) {
+  {
+    StageTimer timer(ctx, FSR_STAGE_TOPK);
+    const size_t fsm = kFinishSmem;
+    FSR_TRY(ensure_smem(ctx, k9t_finish_kernel, fsm));
+    k9t_finish_kernel<<<(unsigned)b, kFinishThreads, fsm, ctx->stream>>>(
+        cb, Wk.qpar, Wk.thr, Wk.cand, Wk.cval, Wk.ccount, Wk.nlow, u_indptr, u_indices, u_values, Wk.Zs, b, eta,
+        copy, y_ptr, y_idx, y_val, topk, top_idx, top_val, Wk.nflag, Wk.nflag + 1, Wk.stats);
+    FSR_TRY(launched(ctx, "k9t_finish_kernel"));
+    const size_t esm = (size_t)kCap * 32;
+    FSR_TRY(ensure_smem(ctx, k9t_empty_kernel, esm));
+    k9t_empty_kernel<<<(unsigned)b, 256, esm, ctx->stream>>>(n, Wk.ccount, eta, copy, y_ptr, y_idx, y_val, topk,
+                                                           top_idx, top_val, Wk.nflag, Wk.nflag + 1);
+    FSR_TRY(launched(ctx, "k9t_empty_kernel"));
+    k9t_fallback_rows_kernel<<<(unsigned)ctx->num_sms * 8, 256, 0, ctx->stream>>>(
+        n, Wk.Xt, n, u_indptr, u_indices, u_values, Wk.Zs, b, eta, copy, y_ptr, y_idx, y_val, Wk.nflag,
+        Wk.nflag + 1);
+    FSR_TRY(launched(ctx, "k9t_fallback_rows_kernel"));
+    const size_t fsmem = (size_t)topk::kCap * 16;
+    FSR_TRY(ensure_smem(ctx, prune::fallback_select_kernel, fsmem));
+    prune::fallback_select_kernel<<<(unsigned)b, topk::kThreads, fsmem, ctx->stream>>>(
+        n, Wk.Xt, n, topk, top_idx, top_val, Wk.nflag, Wk.nflag + 1);
+    FSR_TRY(launched(ctx, "fallback_select_kernel"));
+  }
+  return FSR_OK;
 }
 
 }  // namespace k9t
@@ -931,7 +1430,7 @@ int fsr_dense_u_build(fsr_ctx* ctx, int64_t n, int64_t r, const int64_t* indptr,
 }
 
 int64_t fsr_filter_tc_workspace_bytes(int64_t n, int64_t r, int64_t b) {
-  return (int64_t)k9t::work_bytes(n, r, b, nullptr, nullptr);
+  return (int64_t)k9t::work_bytes(n, r, b, nullptr, nullptr, k9t::sample_rows(n));
 }
 
 int fsr_filter_tc_applicable(int64_t n, int64_t r, int64_t b, int64_t topk) {
@@ -950,7 +1449,7 @@ int fsr_filter_topk_tc(fsr_ctx* ctx, int64_t n, int64_t r, const int64_t* u_indp
   FSR_REQUIRE(ctx, aligned(dense_u, 256) && aligned(workspace, 256), "filter_topk_tc: buffers must be 256-aligned");
   const DenseLayout L = dense_layout(const_cast<void*>(dense_u), n, r);
   Work Wk;
-  work_bytes(n, r, b, &Wk, workspace);
+  work_bytes(n, r, b, &Wk, workspace, sample_rows(n));
   const int64_t ldr = ld_of(r);
   const int copy = copy_uncovered && eta;
   // K8: Zt, Zs (fp32) and the query-major fp16 Zh with per-query scale
@@ -963,36 +1462,14 @@ int fsr_filter_topk_tc(fsr_ctx* ctx, int64_t n, int64_t r, const int64_t* u_indp
     FSR_TRY(tc_gemms<2>(ctx, L, Wk, n, r, b, topk));
   else
     FSR_TRY(tc_gemms<4>(ctx, L, Wk, n, r, b, topk));
-  {
-    StageTimer timer(ctx, FSR_STAGE_TOPK);
-    const size_t fsm = kFinishSmem;
-    FSR_TRY(ensure_smem(ctx, k9t_finish_kernel, fsm));
-    k9t_finish_kernel<<<(unsigned)b, kFinishThreads, fsm, ctx->stream>>>(
-        L.cb, Wk.qpar, Wk.thr, Wk.cand, Wk.cval, Wk.ccount, Wk.nlow, u_indptr, u_indices, u_values, Wk.Zs, b, eta,
-        copy, y_ptr, y_idx, y_val, topk, top_idx, top_val, Wk.nflag, Wk.nflag + 1, Wk.stats);
-    FSR_TRY(launched(ctx, "k9t_finish_kernel"));
-    const size_t esm = (size_t)kCap * 32;
-    FSR_TRY(ensure_smem(ctx, k9t_empty_kernel, esm));
-    k9t_empty_kernel<<<(unsigned)b, 256, esm, ctx->stream>>>(n, Wk.ccount, eta, copy, y_ptr, y_idx, y_val, topk,
-                                                           top_idx, top_val, Wk.nflag, Wk.nflag + 1);
-    FSR_TRY(launched(ctx, "k9t_empty_kernel"));
-    k9t_fallback_rows_kernel<<<(unsigned)ctx->num_sms * 8, 256, 0, ctx->stream>>>(
-        n, Wk.Xt, n, u_indptr, u_indices, u_values, Wk.Zs, b, eta, copy, y_ptr, y_idx, y_val, Wk.nflag,
-        Wk.nflag + 1);
-    FSR_TRY(launched(ctx, "k9t_fallback_rows_kernel"));
-    const size_t fsmem = (size_t)topk::kCap * 16;
-    FSR_TRY(ensure_smem(ctx, prune::fallback_select_kernel, fsmem));
-    prune::fallback_select_kernel<<<(unsigned)b, topk::kThreads, fsmem, ctx->stream>>>(
-        n, Wk.Xt, n, topk, top_idx, top_val, Wk.nflag, Wk.nflag + 1);
-    FSR_TRY(launched(ctx, "fallback_select_kernel"));
-  }
-  return FSR_OK;
+  return finish_stage(ctx, L.cb, Wk, n, b, u_indptr, u_indices, u_values, eta, copy, y_ptr, y_idx, y_val, topk,
+                      top_idx, top_val);
 }
 
 int fsr_filter_tc_stats(fsr_ctx* ctx, int64_t n, int64_t r, int64_t b, const void* workspace, int32_t* out) {
   FSR_REQUIRE(ctx, workspace && out && b >= 1, "filter_tc_stats: bad args");
   k9t::Work Wk;
-  k9t::work_bytes(n, r, b, &Wk, const_cast<void*>(workspace));
+  k9t::work_bytes(n, r, b, &Wk, const_cast<void*>(workspace), 0);  // stats precede the sample keys
   FSR_CUDA(ctx, cudaMemcpyAsync(out, Wk.stats, (size_t)b * 8, cudaMemcpyDeviceToHost, ctx->stream));
   FSR_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
   return FSR_OK;
@@ -1003,6 +1480,78 @@ int fsr_filter_tc_fallback_count(fsr_ctx* ctx, const void* workspace, int* out) 
   FSR_CUDA(ctx, cudaMemcpyAsync(out, workspace, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
   FSR_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
   return FSR_OK;
+}
+
+// ---- small-batch streaming path (K9s) ----
+int64_t fsr_stream_u_bytes(int64_t n, int64_t r, int64_t nnz) {
+  (void)r;
+  return (int64_t)k9t::stream::layout_bytes(n, nnz);
+}
+
+int fsr_stream_u_build(fsr_ctx* ctx, int64_t n, int64_t r, int64_t nnz, const int64_t* indptr,
+                       const int32_t* indices, const float* values, void* out) {
+  using namespace k9t::stream;
+  FSR_REQUIRE(ctx, n >= 1 && r >= 1 && r <= 65536 && nnz >= 0 && indptr && out && (nnz == 0 || (indices && values)),
+              "stream_u_build: bad args (r <= 65536)");
+  FSR_REQUIRE(ctx, n < ((int64_t)1 << 31) - 1, "stream_u_build: n >= 2^31 - 1");
+  FSR_REQUIRE(ctx, aligned(out, 256), "stream_u_build: out must be 256-byte aligned");
+  const Layout L = layout(out, n, nnz);
+  FSR_CUDA(ctx, cudaMemsetAsync(out, 0, layout_bytes(n, nnz), ctx->stream));
+  FSR_CUDA(ctx, cudaMemcpyAsync(L.ipl, indptr, (size_t)(n + 1) * 8, cudaMemcpyDeviceToDevice, ctx->stream));
+  pack_kernel<<<grid_for(n * 32, 256, ctx, 8), 256, 0, ctx->stream>>>(n, indptr, indices, values, L.pk, L.cb,
+                                                                      L.cmax_bits);
+  FSR_TRY(launched(ctx, "stream_pack_kernel"));
+  const int64_t nch = nchunks(nnz);
+  chunk_rows_kernel<<<(unsigned)((nch + 256) / 256), 256, 0, ctx->stream>>>(n, indptr, nch, L.crow);
+  FSR_TRY(launched(ctx, "chunk_rows_kernel"));
+  chunk_desc_kernel<<<(unsigned)((nch + 256) / 256), 256, 0, ctx->stream>>>(indptr, nch, L.crow, L.desc);
+  FSR_TRY(launched(ctx, "chunk_desc_kernel"));
+  sample_offsets_kernel<<<1, 32, 0, ctx->stream>>>(nch, L.crow, L.soff);
+  return launched(ctx, "sample_offsets_kernel");
+}
+
+int fsr_filter_stream_applicable(int64_t n, int64_t r, int64_t nnz, int64_t b, int64_t topk) {
+  return n >= 1 && n < ((int64_t)1 << 31) - 1 && r >= 1 && r <= 65536 && nnz >= 0 && b >= 1 && topk >= 1 &&
+         topk <= k9t::kCap / 8 && topk <= n && k9t::stream::pick_nb(b, r) > 0 &&
+         (size_t)r * 4 + 16 + (size_t)4096 * 8 <= 160 * 1024;  // k9t_project (k8_online.cu, kProjCap = 4096)
+}
+
+int64_t fsr_filter_stream_workspace_bytes(int64_t n, int64_t r, int64_t b) {
+  return (int64_t)k9t::work_bytes(n, r, b, nullptr, nullptr, n);
+}
+
+int fsr_filter_topk_stream(fsr_ctx* ctx, int64_t n, int64_t r, int64_t nnz, const int64_t* u_indptr,
+                           const int32_t* u_indices, const float* u_values, const void* stream_u, const float* w,
+                           const double* eta, int64_t b, const int64_t* y_ptr, const int64_t* y_idx,
+                           const float* y_val, int copy_uncovered, void* workspace, int64_t topk, int64_t* top_idx,
+                           float* top_val) {
+  using namespace k9t;
+  FSR_REQUIRE(ctx, fsr_filter_stream_applicable(n, r, nnz, b, topk), "filter_topk_stream: shape outside the path");
+  FSR_REQUIRE(ctx, u_indptr && stream_u && workspace && top_idx && top_val && (nnz == 0 || (u_indices && u_values)),
+              "filter_topk_stream: missing argument");
+  FSR_REQUIRE(ctx, aligned(stream_u, 256) && aligned(workspace, 256),
+              "filter_topk_stream: buffers must be 256-aligned");
+  const stream::Layout L = stream::layout(const_cast<void*>(stream_u), n, nnz);
+  Work Wk;
+  work_bytes(n, r, b, &Wk, workspace, n);
+  const int copy = copy_uncovered && eta;
+  FSR_TRY(k9t_project(ctx, r, b, u_indptr, u_indices, u_values, w, y_ptr, y_idx, y_val, Wk.Zt, Wk.Zs, Wk.Zh,
+                      ld_of(r), Wk.qp, Wk.nflag));
+  {
+    StageTimer timer(ctx, FSR_STAGE_TOPK);
+    FSR_TRY(stream::launch_groups<0>(ctx, L, Wk, u_indptr, nnz, n, r, b));
+    const int64_t target = (2 * topk + stream::kSampleStride - 1) / stream::kSampleStride + 8;
+    k9t_threshold_kernel<<<(unsigned)std::min<int64_t>(b, (int64_t)ctx->num_sms * 8), 256, 0, ctx->stream>>>(
+        b, n, 0, Wk.Ks, Wk.qp, L.cmax_bits, target, Wk.thr, Wk.qpar, Wk.ccount, Wk.nlow, Wk.nflag, Wk.nflag + 1,
+        L.soff + stream::nsample(nnz));
+    FSR_TRY(launched(ctx, "k9t_threshold_kernel"));
+  }
+  {
+    StageTimer timer(ctx, FSR_STAGE_FILTER_SPMM);
+    FSR_TRY(stream::launch_groups<1>(ctx, L, Wk, u_indptr, nnz, n, r, b));
+  }
+  return finish_stage(ctx, L.cb, Wk, n, b, u_indptr, u_indices, u_values, eta, copy, y_ptr, y_idx, y_val, topk,
+                      top_idx, top_val);
 }
 
 }  // extern "C"

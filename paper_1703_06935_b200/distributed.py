@@ -64,31 +64,96 @@ class Comm:
         self.dist.all_gather(out, src, group=self.group)
         return [o.to(dev) for o in out] if dev is not None else out
 
-    def all_gather_rows(self, t, counts):
-        """Concatenate row shards of different lengths (counts[r] rows on rank r)."""
+    def all_gather_rows(self, t, counts, out=None, async_op=False):
+        """Concatenate row shards of different lengths (counts[r] rows on rank r)
+        straight into ``out`` (allocated when None): one broadcast per rank into
+        its row range of the output -- no padding, no concatenation copy.  With
+        ``async_op`` returns (out, handle); ``handle.wait()`` orders the current
+        stream after the transfer."""
+        import torch
+
+        if self.world == 1:
+            if out is None:
+                return (t, _Done()) if async_op else t
+            out.copy_(t)
+            return (out, _Done()) if async_op else out
+        rows = int(sum(counts))
+        if out is None:
+            out = torch.empty((rows,) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
+        staged = self.backend == "gloo" and out.is_cuda
+        buf = out.cpu() if staged else out
+        src = t.cpu() if staged and t.is_cuda else t
+        offs = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
+        if len(set(counts)) == 1 and not staged:
+            work = [self.dist.all_gather_into_tensor(buf, src.contiguous(), group=self.group, async_op=True)]
+        else:
+            me = buf[int(offs[self.rank]):int(offs[self.rank + 1])]
+            me.copy_(src)
+            work = [self.dist.broadcast(buf[int(offs[r]):int(offs[r + 1])], src=self._global(r), group=self.group,
+                                        async_op=True) for r in range(self.world) if counts[r] > 0]
+        handle = _Handles(work, (lambda: out.copy_(buf)) if staged else None)
+        if async_op:
+            return out, handle
+        handle.wait()
+        return out
+
+    def _global(self, r):
+        return r if self.group is None else self.dist.get_global_rank(self.group, r)
+
+    def sum_ordered(self, t):
+        """Sum over ranks in rank order, bitwise identical on every rank.
+
+        Reduce-scatter by hand so the order is fixed: the flattened tensor is
+        cut into world equal chunks, an all-to-all hands chunk c of every
+        rank's partial to rank c, which adds them in rank order
+        (((p_0 + p_1) + p_2) + ...); an all-gather returns the reduced
+        chunks.  Peak extra memory is ~2 copies of t per rank (the old
+        all-gather of every partial needed world copies: 7.7 GB per r_hat^2
+        fp64 Gram at C4 on 8 ranks)."""
         import torch
 
         if self.world == 1:
             return t
-        m = max(counts)
-        pad = torch.zeros((m,) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
-        pad[: t.shape[0]] = t
-        parts = self.all_gather(pad)
-        return torch.cat([p[:c] for p, c in zip(parts, counts)], dim=0)
-
-    def sum_ordered(self, t):
-        """Sum over ranks in rank order (bitwise identical result on all ranks)."""
-        if self.world == 1:
-            return t
-        parts = self.all_gather(t)
-        acc = parts[0].clone()
-        for p in parts[1:]:
-            acc += p
-        return acc
+        src, dev = self._staged(t.contiguous())
+        flat = src.reshape(-1)
+        m = -(-flat.numel() // self.world)
+        send = torch.zeros(m * self.world, dtype=flat.dtype, device=flat.device)
+        send[:flat.numel()] = flat
+        recv = torch.empty_like(send)
+        self.dist.all_to_all_single(recv, send, group=self.group)
+        del send
+        parts = recv.view(self.world, m)
+        mine = parts[0].clone()
+        for k in range(1, self.world):
+            mine += parts[k]
+        del recv, parts
+        full = torch.empty(m * self.world, dtype=flat.dtype, device=flat.device)
+        self.dist.all_gather_into_tensor(full, mine, group=self.group)
+        res = full[:flat.numel()].view(t.shape)
+        return res.to(dev) if dev is not None else res
 
     def barrier(self):
         if self.world > 1:
             self.dist.barrier(group=self.group)
+
+
+class _Done:
+    def wait(self):
+        return None
+
+
+class _Handles:
+    """Several async collectives (+ an optional host->device copy back) as one handle."""
+
+    def __init__(self, work, finish=None):
+        self.work, self.finish = work, finish
+
+    def wait(self):
+        for w in self.work:
+            w.wait()
+        if self.finish is not None:
+            self.finish()
+            self.finish = None
 
 
 # ---------------------------------------------------------------------------
@@ -151,9 +216,16 @@ class CudaOps:
 
     def spmm(self, A_local, X_full):
         Y = self.torch.empty(A_local.shape[0], X_full.shape[1], dtype=self.dt_t, device=self.device)
+        return self.spmm_into(A_local, X_full, Y)
+
+    def spmm_into(self, A_local, X, Y):
+        """Y = A_local X for a column panel (Y may be a column slice of a wider block)."""
         self.ctx.call("csr_spmm", self.dt, A_local.shape[0], N.ptr(A_local.indptr), N.ptr(A_local.indices),
-                      N.ptr(A_local.values), X_full.shape[1], N.ptr(X_full), X_full.stride(0), N.ptr(Y), Y.stride(0))
+                      N.ptr(A_local.values), X.shape[1], N.ptr(X), X.stride(0), N.ptr(Y), Y.stride(0))
         return Y
+
+    def empty(self, rows, cols):
+        return self.torch.empty(rows, cols, dtype=self.dt_t, device=self.device)
 
     def gram(self, Y, fast=False):
         k = Y.shape[1]
@@ -293,10 +365,47 @@ def sharded_range_finder(comm: Comm, ops, A_local, shard: Shard, r_hat: int, q: 
             Q = Y if (t == 0 and 4 * r_hat <= shard.n) else sharded_precondition(comm, ops, Y, shard, dt_code, stats)
         else:
             Q = sharded_orthonormalize(comm, ops, Y, shard, dt_code, stats)
-        Qfull = comm.all_gather_rows(Q, shard.counts)
-        Y = ops.spmm(A_local, Qfull)
-        del Qfull
+        Y = exchange_spmm(comm, ops, A_local, Q, shard)
     return Q, Y
+
+
+# Column-panel width of the pipelined exchange (EXCHANGE_PANEL columns of all n
+# rows per buffer, two buffers): at C4 (n = 2.5e6, fp32) 2 x 5.1 GB instead of
+# the 110 GB gathered block.  0 = gather the whole block at once.
+EXCHANGE_PANEL = 512
+
+
+def exchange_spmm(comm: Comm, ops, A_local, Q, shard: Shard, panel: int | None = None):
+    """B_l = W_l Q (the SI exchange step, spectral.py:170) without holding all of Q.
+
+    Q's columns are exchanged in panels: panel j+1's all-gather (one broadcast
+    per rank into its row range of a preallocated n x w buffer) is in flight
+    while K2 multiplies panel j into B_l[:, panel j]; two panel buffers
+    alternate.  K2 sums each row's nonzeros in the same order whatever the
+    panel width, so B_l is bitwise the unpipelined product.  Per-rank memory:
+    Q_l + B_l + 2 n w."""
+    w_all = Q.shape[1]
+    panel = EXCHANGE_PANEL if panel is None else panel
+    if comm.world == 1 or panel <= 0 or panel >= w_all:
+        return ops.spmm(A_local, comm.all_gather_rows(Q, shard.counts))
+    B = ops.empty(shard.rows, w_all)
+    bufs = [ops.empty(shard.n * panel, 1), ops.empty(shard.n * panel, 1)]
+    npan = -(-w_all // panel)
+
+    def start(j):
+        c0, c1 = j * panel, min(w_all, (j + 1) * panel)
+        out = bufs[j % 2][: shard.n * (c1 - c0)].view(shard.n, c1 - c0)
+        return comm.all_gather_rows(Q[:, c0:c1].contiguous(), shard.counts, out=out, async_op=True)
+
+    cur = start(0)
+    for j in range(npan):
+        panel_j, handle = cur
+        handle.wait()
+        if j + 1 < npan:
+            cur = start(j + 1)  # in flight while K2 runs on panel j
+        c0, c1 = j * panel, min(w_all, (j + 1) * panel)
+        ops.spmm_into(A_local, panel_j, B[:, c0:c1])
+    return B
 
 
 def sharded_precondition(comm: Comm, ops, Y, shard: Shard, dt_code: int, stats=None):
@@ -354,7 +463,8 @@ def sharded_sparsify(comm: Comm, ops, U, tau: int, shard: Shard, dt_code: int):
 
 
 __all__ = ["Comm", "CudaOps", "Shard", "make_shard", "row_partition", "sharded_orthonormalize",
-           "sharded_range_finder", "sharded_rayleigh_ritz", "sharded_sparsify", "HIST_BITS", "key_bits"]
+           "sharded_range_finder", "sharded_rayleigh_ritz", "sharded_sparsify", "exchange_spmm", "HIST_BITS",
+           "key_bits"]
 
 
 def shard_rows(A, r0: int, r1: int):

@@ -252,6 +252,17 @@ def filter_device(dec: SpectralDecomposition, h: TransferFunction, queries: Devi
         res.top_val = torch.empty(b, topk, dtype=dt, device=dev)
     U = dec.U_device
     path = online_path(dec, b, topk if not want_x else 0, ctx)
+    if path == "stream":
+        packed = stream_layout(dec)
+        need = int(ctx.lib.fsr_filter_stream_workspace_bytes(n, r, b))
+        if workspace is None or workspace.numel() < need:
+            workspace = torch.empty(need, dtype=torch.uint8, device=dev)
+        ctx.call("filter_topk_stream", n, r, U.nnz, N.ptr(U.indptr), N.ptr(U.indices), N.ptr(U.values),
+                 N.ptr(packed), N.ptr(w), N.ptr(dec.eta_device), b, N.ptr(queries.y_ptr), N.ptr(queries.y_idx),
+                 N.ptr(queries.y_val), int(bool(copy_uncovered)), N.ptr(workspace), int(topk), N.ptr(res.top_idx),
+                 N.ptr(res.top_val))
+        ctx.last_online_path = "stream"
+        return res
     if path == "tc":
         dense = dense_layout(dec)
         if dense is not None:
@@ -279,19 +290,23 @@ def filter_device(dec: SpectralDecomposition, h: TransferFunction, queries: Devi
     return res
 
 
-ONLINE_PATHS = ("tc", "pruned", "exact")
+ONLINE_PATHS = ("tc", "stream", "pruned", "exact")
 # below this batch the tensor-core step streams the whole dense U~ for too few
-# queries; the sparse paths are faster
+# queries; the packed-U~ stream (K9s) is faster
 TC_MIN_BATCH = 128
 
 
 def online_path(dec, b: int, topk: int, ctx=None) -> str:
     """Which kernels a ``filter_device`` call runs: "tc" (top-k only, fp32
-    sparse U~: K9t, the certified tensor-core step of csrc/k9t.cu), "pruned"
-    (the certified fp16-gather K9h of csrc/prune.cuh), or "exact" (unpruned
-    K9 + exact top-k).  All three return the same top-k, bit for bit.  The
-    context's ``online_path`` preference ("tc" by default) and the shape
-    limits decide; ``set_topk_prune(False)`` forces "exact"."""
+    sparse U~: K9t, the certified tensor-core step of csrc/k9t.cu, b >= 128),
+    "stream" (K9s: the same certification on a packed fp16 U~ streamed from
+    HBM, the small-batch path), "pruned" (the certified fp16-gather K9h of
+    csrc/prune.cuh), or "exact" (unpruned K9 + exact top-k).  The certified
+    paths return the top-k of the unpruned sequential-order fp32 path bit for
+    bit (for b <= 64 the exact path's narrow kernels sum rows in another
+    order, see tests/test_gpu_prune.py).  The context's ``online_path``
+    preference ("tc" by default) and the shape limits decide;
+    ``set_topk_prune(False)`` forces "exact"."""
     import torch
 
     ctx = ctx or N.Context.get(dec.eta_device.device)
@@ -300,6 +315,9 @@ def online_path(dec, b: int, topk: int, ctx=None) -> str:
     pref = ctx.online_path
     if pref == "tc" and b >= TC_MIN_BATCH and ctx.lib.fsr_filter_tc_applicable(dec.n, dec.r, b, int(topk)):
         return "tc"
+    if (pref == "stream" or (pref == "tc" and b < TC_MIN_BATCH)) and \
+            ctx.lib.fsr_filter_stream_applicable(dec.n, dec.r, dec.U_device.nnz, b, int(topk)):
+        return "stream"
     if pref in ("tc", "pruned") and topk_pruned(dec.n, b, topk, dec.dtype):
         return "pruned"
     return "exact"
@@ -334,13 +352,31 @@ def dense_layout(dec):
     return buf
 
 
+def stream_layout(dec):
+    """The packed U~ (4 bytes per entry: fp16 value << 16 | column, per-row
+    bound factors, chunk table) that the small-batch stream K9s reads
+    (fsr_stream_u_build), built once per decomposition and cached on it."""
+    import torch
+
+    cached = getattr(dec, "_stream_u", None)
+    if cached is not None:
+        return cached
+    U = dec.U_device
+    dev = dec.eta_device.device
+    ctx = N.Context.get(dev)
+    buf = torch.empty(int(ctx.lib.fsr_stream_u_bytes(dec.n, dec.r, U.nnz)), dtype=torch.uint8, device=dev)
+    ctx.call("stream_u_build", dec.n, dec.r, U.nnz, N.ptr(U.indptr), N.ptr(U.indices), N.ptr(U.values), N.ptr(buf))
+    dec._stream_u = buf
+    return buf
+
+
 def last_fallback_count(workspace, dec, b: int, ctx=None) -> int:
     """Queries of the last certified call (tc or pruned) that went through the
     exact fallback."""
     import ctypes
 
     ctx = ctx or N.Context.get(dec.eta_device.device)
-    if ctx.last_online_path == "tc":
+    if ctx.last_online_path in ("tc", "stream"):
         out = ctypes.c_int()
         ctx.call("filter_tc_fallback_count", N.ptr(workspace), ctypes.byref(out))
         return int(out.value)
@@ -360,8 +396,11 @@ def filter_workspace_bytes(dec, b: int, want_x: bool, topk: int = 0) -> int:
     """Workspace bytes ``filter_device`` needs for this call's path."""
     ctx = N.Context.get(dec.eta_device.device)
     need = int(ctx.lib.fsr_filter_workspace_bytes(N.dtype_code(dec.dtype), dec.n, dec.r, b, int(not want_x)))
-    if not want_x and online_path(dec, b, topk, ctx) == "tc":
+    path = online_path(dec, b, topk, ctx) if not want_x else "exact"
+    if path == "tc":
         need = max(need, int(ctx.lib.fsr_filter_tc_workspace_bytes(dec.n, dec.r, b)))
+    elif path == "stream":
+        need = max(need, int(ctx.lib.fsr_filter_stream_workspace_bytes(dec.n, dec.r, b)))
     return need
 
 

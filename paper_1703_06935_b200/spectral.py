@@ -210,58 +210,33 @@ def _max_dev(ctx, G) -> float:
     return err.value
 
 
-def _cholqr_pass(ctx, dt, Y, G, gram_hook=None, fast_gram=False) -> tuple[bool, float]:
-    """One CholeskyQR pass in place: Y <- Y R^-1.  Returns (ok, max|G - I|).
+def _trace_into(ctx, stats):
+    """Append the schedule steps libfsr recorded (fsr_schedule_trace) to stats."""
+    if stats is not None:
+        t = ctx.lib.fsr_schedule_trace(ctx.handle)
+        if t:
+            stats.extend(t.decode().split(";"))
 
-    ``fast_gram`` (float32 blocks only): a one-slice (7-bit) int8 Gram.  The
-    first pass of CholeskyQR2 only needs R to be a decent preconditioner --
-    span(Y R^-1) equals span(Y) whatever R is -- so its Gram can skip the
-    full 6-product Ozaki scheme.
-    """
-    if fast_gram and dt == N.F32:
-        n, k = Y.shape
-        ctx.call("gram_levels", n, k, N.ptr(Y), Y.stride(0), N.ptr(G), 0, 1)
-    else:
-        _gram(ctx, dt, Y, G)
-    if gram_hook is not None:
-        gram_hook(G)
-    dev = _max_dev(ctx, G)
-    st = ctx.call("cholesky", G.shape[0], N.ptr(G))
-    if st == N.ENOTSPD:
-        return False, dev
-    # the preconditioning pass may also apply R^-1 as a 7-bit matrix: only
-    # span(Y R'^-1) = span(Y) matters there (see fsr_apply_rinv_levels)
-    ctx.call("apply_rinv_levels", dt, Y.shape[0], Y.shape[1], N.ptr(G), N.ptr(Y), Y.stride(0),
-             1 if (fast_gram and FAST_FIRST_APPLY) else 4)
-    return True, dev
+
+def si_flags() -> int:
+    """FSR_SI_* flags of the fp32 fast-mode schedule (fsr.h fsr_si_flags), from
+    the module switches SI_SPAN_ONLY / FUSED_RR / FAST_FIRST_APPLY."""
+    return (1 if SI_SPAN_ONLY else 0) | (2 if FUSED_RR else 0) | (4 if FAST_FIRST_APPLY else 0)
 
 
 def orthonormalize(Y, ctx=None, stats=None):
     """Replace Y by an orthonormal basis of its span (CholeskyQR2, Householder fallback).
 
     Mirrors ``spectral.py:165-169``: the result is checked against the
-    re-orthogonalisation trigger and re-factorised when it fails.
+    re-orthogonalisation trigger and re-factorised when it fails.  One call of
+    the operator-level ``fsr_orthonormalize`` (csrc/fsr_ops.cu): first pass on a
+    7-bit Gram, second on the full Gram, Householder when Cholesky breaks down
+    or max|Q^T Q - I| misses ORTH_TOL.
     """
-    import torch
-
     ctx = ctx or N.Context.get(Y.device)
-    dt = N.dtype_code(Y.dtype)
     n, k = Y.shape
-    G = torch.empty(k, k, dtype=torch.float64, device=Y.device)
-    ok1, _ = _cholqr_pass(ctx, dt, Y, G, fast_gram=FAST_FIRST_GRAM)
-    ok2, dev2 = _cholqr_pass(ctx, dt, Y, G) if ok1 else (False, math.inf)
-    method = "cholqr2"
-    if not (ok1 and ok2):
-        ctx.call("householder_qr", dt, n, k, N.ptr(Y), Y.stride(0))
-        method = "householder"
-        dev2 = math.inf
-    if dev2 > CHOLQR2_SAFE:
-        _gram(ctx, dt, Y, G)
-        if _max_dev(ctx, G) > ORTH_TOL[dt]:
-            ctx.call("householder_qr", dt, n, k, N.ptr(Y), Y.stride(0))
-            method += "+householder"
-    if stats is not None:
-        stats.append(method)
+    ctx.call("orthonormalize", N.dtype_code(Y.dtype), n, k, N.ptr(Y), Y.stride(0))
+    _trace_into(ctx, stats)
     return Y
 
 
@@ -280,7 +255,15 @@ def range_finder(A, r_hat: int, q: int, seed: int, dtype="float64", device=None,
 
     Start block from the seeded counter stream (K0); q rounds of
     {orthonormalise (K3), B = A Q (K2)}.  Returns the last Q and B = A Q.
+    One call of the operator-level ``fsr_range_finder`` (csrc/fsr_ops.cu),
+    which owns the schedule: in fp32 fast mode the intermediate rounds only
+    precondition (span(Q) is what reaches the output; the Gaussian start block
+    already is well conditioned when r_hat <= n / 4), and with
+    ``_orthonormal_last=False`` (decompose's fused path) the last basis is
+    preconditioned and its exact Gram G = Q^T Q is kept for Rayleigh-Ritz.
     """
+    import ctypes
+
     import torch
 
     A = SparseSymmetricMatrix.coerce(A)
@@ -293,81 +276,18 @@ def range_finder(A, r_hat: int, q: int, seed: int, dtype="float64", device=None,
     Ad = A.device(dt_t, device)
     ctx = N.Context.get(Ad.device)
     dt = N.dtype_code(dt_t)
-    Y = gaussian_block(n, r_hat, seed, dtype=dt_t, device=Ad.device)
-    Q = torch.empty_like(Y)
-    gram_last = None
-    for t in range(q):
-        if t == q - 1 and not _orthonormal_last:
-            # decompose's fused path: one preconditioning CholeskyQR pass plus the
-            # exact Gram G of the result, which Rayleigh-Ritz then absorbs
-            Y, gram_last = _precondition_with_gram(Y, ctx, stats)
-        elif SI_SPAN_ONLY and dt == N.F32 and t < q - 1:
-            # Only span(Q) of the intermediate rounds reaches the output (the
-            # last round is orthonormalised in full before Rayleigh-Ritz), so
-            # they need a well-conditioned basis, not an orthonormal one.  The
-            # Gaussian start block already is one when r_hat <= n / 4.
-            if t > 0 or 4 * r_hat > n:
-                _precondition(Y, ctx, stats)
-            elif stats is not None:
-                stats.append("start")
-        else:
-            orthonormalize(Y, ctx, stats)
-        Q, Y = Y, Q  # Y now holds the (orthonormal or well-conditioned) block
-        _spmm(ctx, dt, Ad, Q, Y)
-    basis = RangeBasis(Q=Q, B=Y, iterations_used=q, seed=seed)
-    if gram_last is not None:
-        object.__setattr__(basis, "_gram", gram_last)
+    Q = torch.empty(n, r_hat, dtype=dt_t, device=Ad.device)
+    B = torch.empty_like(Q)
+    flags = si_flags() if not _orthonormal_last else si_flags() & ~2
+    G = torch.empty(r_hat, r_hat, dtype=torch.float64, device=Ad.device) if flags & 2 else None
+    valid = ctypes.c_int(0)
+    ctx.call("range_finder", dt, n, N.ptr(Ad.indptr), N.ptr(Ad.indices), N.ptr(Ad.values), r_hat, q, seed & _MASK64,
+             flags, N.ptr(Q), N.ptr(B), N.ptr(G), ctypes.byref(valid))
+    _trace_into(ctx, stats)
+    basis = RangeBasis(Q=Q, B=B, iterations_used=q, seed=seed)
+    if valid.value:
+        object.__setattr__(basis, "_gram", G)
     return basis
-
-
-def _precondition_with_gram(Y, ctx, stats=None):
-    """(Y R'^-1, G) with G = (Y R'^-1)^T (Y R'^-1) from the full 28-bit Gram: one
-    7-bit CholeskyQR pass; if G is far from I (max|G - I| > 0.9) the second
-    CholeskyQR pass is applied and G recomputed, so Rayleigh-Ritz always gets
-    a basis with cond <= ~4.4 and its exact Gram."""
-    import torch
-
-    dt = N.dtype_code(Y.dtype)
-    n, k = Y.shape
-    G = torch.empty(k, k, dtype=torch.float64, device=Y.device)
-    ok, _ = _cholqr_pass(ctx, dt, Y, G, fast_gram=True)
-    if ok:
-        _gram(ctx, dt, Y, G)
-        dev = _max_dev(ctx, G)
-        if dev <= 0.9:
-            if stats is not None:
-                stats.append(f"precond+gram(dev={dev:.3g})")
-            return Y, G
-        if stats is not None:
-            stats.append(f"precond+gram-failed(dev={dev:.3g})")
-    orthonormalize(Y, ctx, stats)
-    _gram(ctx, dt, Y, G)
-    return Y, G
-
-
-def _precondition(Y, ctx, stats=None):
-    """In place: Y <- Y R'^-1 with span(Y) kept and max|Y^T Y - I| <= PRECOND_TOL.
-
-    One CholeskyQR pass on 7-bit Gram and 7-bit R^-1 (span(Y M) = span(Y) for
-    any invertible M; Y's own slices stay 28-bit), then a 7-bit Gram checks
-    the conditioning; a full ``orthonormalize`` runs if the check fails.
-    """
-    import torch
-
-    dt = N.dtype_code(Y.dtype)
-    n, k = Y.shape
-    G = torch.empty(k, k, dtype=torch.float64, device=Y.device)
-    ok, _ = _cholqr_pass(ctx, dt, Y, G, fast_gram=True)
-    if ok:
-        ctx.call("gram_levels", n, k, N.ptr(Y), Y.stride(0), N.ptr(G), 0, 1)
-        dev = _max_dev(ctx, G)
-        if dev <= PRECOND_TOL:
-            if stats is not None:
-                stats.append(f"precond(dev={dev:.3g})")
-            return Y
-        if stats is not None:
-            stats.append(f"precond-failed(dev={dev:.3g})")
-    return orthonormalize(Y, ctx, stats)
 
 
 def _rayleigh_ritz(ctx, dt, Q, B, r, general=False):
@@ -376,34 +296,23 @@ def _rayleigh_ritz(ctx, dt, Q, B, r, general=False):
     general=True: Q is only well conditioned (decompose's fused fp32 path);
     the Ritz pairs solve C v = lambda G v with G = Q^T Q, V is G-orthonormal
     and U = Q V orthonormal -- the same pairs as orthonormalising Q first.
+    One call of the operator-level ``fsr_rayleigh_ritz`` (csrc/fsr_ops.cu).
     """
     import torch
 
     n, k = Q.shape
-    C = torch.empty(k, k, dtype=torch.float64, device=Q.device)
-    # C = Q^T A Q is symmetric: the fp32 tensor-core path computes one triangle
-    ctx.call("cross_sym", dt, n, k, N.ptr(Q), Q.stride(0), N.ptr(B), B.stride(0), N.ptr(C), 0)
-    lam = np.empty(r, dtype=np.float64)
-    V = torch.empty(k, r, dtype=torch.float64, device=Q.device)
+    G = None
     if general is not False:
         if isinstance(general, bool):
             G = torch.empty(k, k, dtype=torch.float64, device=Q.device)
             ctx.call("gram", dt, n, k, N.ptr(Q), Q.stride(0), N.ptr(G), 0)
         else:
-            G = general.clone()  # the exact Gram of Q, computed by range_finder (sygvd destroys its input)
-        ctx.call("eigh_gen_desc", k, N.ptr(C), N.ptr(G), r, lam.ctypes.data_as(N._c_dp), N.ptr(V))
-        del G
-    else:
-        ctx.call("eigh_desc", k, N.ptr(C), r, lam.ctypes.data_as(N._c_dp), N.ptr(V))
-    del C
+            G = general  # the exact Gram of Q from range_finder (fsr_rayleigh_ritz copies it)
+    lam = np.empty(r, dtype=np.float64)
     U = torch.empty(n, r, dtype=Q.dtype, device=Q.device)
-    ctx.call("lift", dt, n, k, r, N.ptr(Q), Q.stride(0), N.ptr(V), N.ptr(U), U.stride(0))
-    best_abs = torch.empty(r, dtype=torch.float64, device=Q.device)
-    best_row = torch.empty(r, dtype=torch.int64, device=Q.device)
-    best_val = torch.empty(r, dtype=torch.float64, device=Q.device)
-    ctx.call("col_absmax", dt, n, r, N.ptr(U), U.stride(0), 0, N.ptr(best_abs), N.ptr(best_row), N.ptr(best_val))
     eta = torch.empty(n, dtype=torch.float64, device=Q.device)
-    ctx.call("apply_signs_rownorm", dt, n, r, N.ptr(U), U.stride(0), N.ptr(best_val), N.ptr(eta))
+    ctx.call("rayleigh_ritz", dt, n, k, N.ptr(Q), Q.stride(0), N.ptr(B), B.stride(0), N.ptr(G), r,
+             lam.ctypes.data_as(N._c_dp), N.ptr(U), U.stride(0), N.ptr(eta))
     return U, lam, eta
 
 
@@ -650,18 +559,26 @@ def sparsify(dec: SpectralDecomposition, tau: int) -> SpectralDecomposition:
         raise ValueError("decomposition is already sparse")
     if tau < 1:
         raise ValueError("tau must be positive")
+    import ctypes
+
     U = dec.U_device
     n, r = U.shape
     ctx = N.Context.get(U.device)
     dt = N.dtype_code(U.dtype)
-
-    def hist_fn(prefix, shift, bits):
-        h = torch.zeros(1 << bits, dtype=torch.int64, device=U.device)
-        ctx.call("abs_histogram", dt, n, r, N.ptr(U), U.stride(0), prefix, shift, bits, N.ptr(h))
-        return h.cpu().numpy().astype(np.uint64)
-
-    T, ties, keep = select_threshold(hist_fn, dt, tau)
-    Ut, eta = compact_rows(ctx, dt, U, T, 0, ties, keep)
+    # operator level (csrc/fsr_ops.cu): radix-select the tau-th |u| key, then compact
+    T, ties, keep = ctypes.c_uint64(), ctypes.c_int64(), ctypes.c_int64()
+    ctx.call("sparsify_select", dt, n, r, N.ptr(U), U.stride(0), tau, ctypes.byref(T), ctypes.byref(ties),
+             ctypes.byref(keep))
+    cap = max(1, int(keep.value))
+    indptr = torch.empty(n + 1, dtype=torch.int64, device=U.device)
+    indices = torch.empty(cap, dtype=torch.int32, device=U.device)
+    values = torch.empty(cap, dtype=U.dtype, device=U.device)
+    eta = torch.empty(n, dtype=torch.float64, device=U.device)
+    nnz = ctypes.c_int64()
+    ctx.call("sparsify", dt, n, r, N.ptr(U), U.stride(0), tau, N.ptr(indptr), N.ptr(indices), N.ptr(values), cap,
+             N.ptr(eta), ctypes.byref(nnz))
+    k = int(nnz.value)
+    Ut = DeviceCSR(indptr, indices[:k], values[:k], (n, r))
     return SpectralDecomposition(Ut, dec.eigenvalues, eta, dec.components, Variant.SPARSE,
                                  replace(dec.provenance, tau=tau))
 

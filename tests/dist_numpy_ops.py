@@ -28,6 +28,13 @@ class NumpyOps:
     def spmm(self, A_local, X_full):
         return _t(A_local @ _np(X_full))
 
+    def spmm_into(self, A_local, X, Y):
+        Y.copy_(_t(A_local @ _np(X)))
+        return Y
+
+    def empty(self, rows, cols):
+        return torch.empty(rows, cols, dtype=torch.float64)
+
     def gram(self, Y, fast=False):
         y = _np(Y)
         return _t(y.T @ y)

@@ -71,3 +71,16 @@ def test_topk_pruned_conditions():
     assert not ranking.topk_pruned(1_000_000, 1024, 0, f32)
     assert not ranking.topk_pruned(1_000_000, 1024, 100, f64)
     assert not ranking.topk_pruned(1_000_000, 1024, 100, f32, sparse=False)
+
+
+@pytest.mark.parametrize("seed", [0, 1, 7, 2**31 + 5, 2**32, 2**32 + 1, 2**63 + 12345, 2**64 - 1])
+def test_philox_key_is_numpy_seedsequence(seed):
+    """fsr_philox_key (the C host's route to the reference start block,
+    spectral.py:55-65) equals numpy's SeedSequence(seed).generate_state(2, uint64)."""
+    import numpy as np
+
+    lib = _native.load_library()
+    k0, k1 = ctypes.c_uint64(), ctypes.c_uint64()
+    lib.fsr_philox_key(seed, ctypes.byref(k0), ctypes.byref(k1))
+    want = np.random.SeedSequence(seed).generate_state(2, np.uint64)
+    assert (k0.value, k1.value) == (int(want[0]), int(want[1]))

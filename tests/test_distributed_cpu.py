@@ -99,3 +99,55 @@ def test_row_partition_balances_nnz():
     loads = [indptr[b] - indptr[a] for a, b in parts]
     assert max(loads) - min(loads) <= 12
     assert row_partition(np.zeros(1, np.int64), 3) == [(0, 0)] * 3
+
+
+def pipeline_worker(rank, world, port, out_path, panel):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1703_06935_b200 import _native as N
+        from paper_1703_06935_b200 import distributed as D
+        from dist_numpy_ops import NumpyOps
+
+        D.EXCHANGE_PANEL = panel
+        S = problem()
+        comm = D.Comm()
+        shard = D.make_shard(comm, S.indptr)
+        ops = NumpyOps()
+        Q, B = D.sharded_range_finder(comm, ops, S[shard.r0:shard.r1], shard, 18, 3, 0, N.F64)
+        # the collectives themselves: rank-ordered sum, ragged (and empty) row shards
+        rng = np.random.default_rng(100 + rank)
+        part = torch.as_tensor(rng.standard_normal((7, 5)))
+        tot = comm.sum_ordered(part)
+        counts = [3, 0, 5, 1][:world] if world <= 4 else [2] * world
+        mine = torch.full((counts[rank], 2), float(rank))
+        rows = comm.all_gather_rows(mine, counts)
+        np.savez(f"{out_path}.{rank}.npz", Q=Q.numpy(), B=B.numpy(), part=part.numpy(), tot=tot.numpy(),
+                 rows=rows.numpy(), counts=np.array(counts))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_panel_pipelined_exchange_is_bitwise_unpipelined(tmp_path, world):
+    """exchange_spmm in 5-column panels (ragged last panel, two buffers in
+    flight) gives bitwise the Q and B of the whole-block exchange; sum_ordered
+    (all-to-all + rank-ordered adds + all-gather) equals ((p0 + p1) + p2) + ...
+    bit for bit on every rank; all_gather_rows handles ragged and empty shards."""
+    res = {}
+    for panel in (5, 0):
+        out = str(tmp_path / f"p{panel}")
+        mp.spawn(pipeline_worker, args=(world, free_port(), out, panel), nprocs=world, join=True)
+        res[panel] = [np.load(f"{out}.{k}.npz") for k in range(world)]
+    for k in range(world):
+        np.testing.assert_array_equal(res[5][k]["Q"], res[0][k]["Q"])
+        np.testing.assert_array_equal(res[5][k]["B"], res[0][k]["B"])
+    parts = [res[5][k]["part"] for k in range(world)]
+    acc = parts[0].copy()
+    for p in parts[1:]:
+        acc += p
+    counts = res[5][0]["counts"]
+    want_rows = np.concatenate([np.full((c, 2), float(k)) for k, c in enumerate(counts)])
+    for k in range(world):
+        np.testing.assert_array_equal(res[5][k]["tot"], acc)
+        np.testing.assert_array_equal(res[5][k]["rows"], want_rows)

@@ -37,14 +37,47 @@ def test_c1_graph_matches_reference(golden, c1_data):
 
 
 def test_c1_graph_bf16_candidates(golden, c1_data):
-    """bf16 candidate GEMM + fp64 re-score (the C3 input mode) on C1: same graph."""
+    """Certified bf16 candidate GEMM + fp64 re-score (the C3 input mode) on C1:
+    the reference's graph; every row settled by one of the three stages."""
     cfg, data, _ = c1_data
     g = golden("c1")
+    st = {}
     W = knn.mutual_knn_graph_device(torch.as_tensor(data).cuda(), cfg.k, cfg.gamma,
-                                    gemm_dtype=torch.bfloat16).csr
+                                    gemm_dtype=torch.bfloat16, stats=st).csr
+    assert sum(st.values()) == cfg.n
     np.testing.assert_array_equal(W.indptr, g["W_indptr"])
     np.testing.assert_array_equal(W.indices, g["W_indices"])
     np.testing.assert_allclose(W.data, g["W_data"], rtol=1e-12, atol=0)
+
+
+def test_c1_observation_vectors_bf16_certified(golden, c1_data):
+    """Certified bf16 candidates for the query neighbours: the reference's y."""
+    cfg, data, queries = c1_data
+    g = golden("c1")
+    st = {}
+    y_ptr, y_idx, y_val = knn.observation_batch_device(torch.as_tensor(queries).cuda(), torch.as_tensor(data).cuda(),
+                                                       cfg.y_top, cfg.gamma, gemm_dtype=torch.bfloat16, stats=st)
+    assert sum(st.values()) == len(queries)
+    np.testing.assert_array_equal(y_ptr, g["y_ptr"])
+    np.testing.assert_array_equal(y_idx, g["y_idx"])
+    np.testing.assert_allclose(y_val, g["y_val"], rtol=1e-12, atol=0)
+
+
+def test_score_error_bound_holds_on_adversarial_rows():
+    """The bf16 / bf16x3 candidate-score bounds cover the measured errors of
+    the GEMMs they model (rows built to maximise rounding: values just past
+    bf16 midpoints, all of one sign)."""
+    g = torch.Generator(device="cuda").manual_seed(5)
+    for d in (128, 512, 2048):
+        A = torch.rand(64, d, generator=g, device="cuda", dtype=torch.float64)
+        A = (A.to(torch.bfloat16).double() * (1 + 2.0 ** -9 * 0.999))  # each value ~half a bf16 ulp off
+        A /= A.norm(dim=1, keepdim=True)
+        X = torch.rand(4096, d, generator=g, device="cuda", dtype=torch.float64)
+        X /= X.norm(dim=1, keepdim=True)
+        exact = A @ X.T
+        for scheme in ("bf16", "bf16x3"):
+            err = (knn._approx_sims(A, X, scheme).double() - exact).abs().max().item()
+            assert err <= knn.score_error_bound(d, scheme), (d, scheme, err)
 
 
 def test_c1_observation_vectors_match_reference(golden, c1_data):

@@ -106,6 +106,22 @@ def test_c2_graph_and_queries_match_reference(c2):
     np.testing.assert_allclose(y_val, g["y_val"], rtol=1e-12, atol=0)
 
 
+def test_c2_graph_from_certified_bf16_candidates(c2):
+    """The C3/C4 input mode at the full C2 size: bf16 candidates (certified,
+    knn.certified_topk) + fp64 re-score give the reference's graph exactly."""
+    from paper_1703_06935_b200.workloads import cluster_descriptors as cd
+
+    g = c2.g
+    data, _, _ = cd(c2.cfg)
+    st = {}
+    W = knn.mutual_knn_graph_device(torch.as_tensor(data).cuda(), c2.cfg.k, c2.cfg.gamma,
+                                    gemm_dtype=torch.bfloat16, stats=st).csr
+    record("knn_bf16_certification_rows", st)
+    assert sum(st.values()) == c2.cfg.n
+    assert pattern_hash(W.indptr, W.indices) == str(g["W_pattern_hash"])
+    np.testing.assert_allclose(weight_digest(W.data), g["W_digest"], rtol=1e-12)
+
+
 @pytest.fixture(scope="module", params=["float64", "float32"])
 def decs(request, c2):
     P = c2.P

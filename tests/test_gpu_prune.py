@@ -55,8 +55,9 @@ def queries(n, b, seed, k=50, empty=(), extra=None):
     return ranking.QueryBatch.from_vectors(ys)
 
 
-# the certified paths under test: K9t (tensor cores, csrc/k9t.cu) and K9h (fp16 gathers, csrc/prune.cuh)
-PATHS = ["tc", "pruned"]
+# the certified paths under test: K9t (tensor cores, csrc/k9t.cu), K9s (packed
+# fp16 U~ streamed from HBM, csrc/k9t.cu) and K9h (fp16 gathers, csrc/prune.cuh)
+PATHS = ["tc", "stream", "pruned"]
 
 
 @pytest.fixture(params=PATHS)
@@ -122,7 +123,7 @@ def test_pruned_ties_empty_uncovered_and_fallback(path):
     fl = []
     (pi, pv), (ui, uv) = both(dec, qb, flags=fl)
     # K9h: the two empty observations and the queries on the duplicated rows;
-    # K9t answers empty observations directly (k9t_empty), not by the fallback
+    # K9t / K9s answer empty observations directly (k9t_empty), not by the fallback
     assert fl[0] >= (4 if path == "pruned" else 2)
     np.testing.assert_array_equal(pi, ui)
     np.testing.assert_array_equal(pv.view(np.uint32), uv.view(np.uint32))
@@ -238,3 +239,84 @@ def test_tc_small_and_odd_batches(b, monkeypatch):
         ctx.set_topk_prune(True)
     np.testing.assert_array_equal(pi, r_.top_idx[:b].cpu().numpy())
     np.testing.assert_array_equal(pv.view(np.uint32), r_.top_val[:b].cpu().numpy().view(np.uint32))
+
+
+def padded_unpruned(dec, qb, K, h=None):
+    """The unpruned reference in the sequential per-row order: the queries
+    padded with empty ones to a 256-wide batch (b <= 64 would take the narrow
+    exact kernels, which sum a row in interleaved halves)."""
+    n, b = dec.n, qb.b
+    pad = ranking.QueryBatch(n, np.concatenate([qb.y_ptr, np.full(256 - b, qb.y_ptr[-1])]), qb.y_idx, qb.y_val)
+    ctx = N.Context.get()
+    ctx.set_topk_prune(False)
+    try:
+        r_ = ranking.filter_device(dec, h or ranking.h_alpha(0.99), ranking.DeviceQueries(pad, dec.dtype,
+                                   dec.eta_device.device), topk=K, want_x=False)
+        torch.cuda.synchronize()
+    finally:
+        ctx.set_topk_prune(True)
+    return r_.top_idx[:b].cpu().numpy(), r_.top_val[:b].cpu().numpy()
+
+
+@pytest.mark.parametrize("b", [1, 2, 5, 8, 64, 100])
+def test_stream_small_batches_default_route(b):
+    """b < 128 on the default preference takes K9s (one NB-query group per
+    8 queries, ragged last group) and returns the sequential-order unpruned
+    top-k bit for bit; the FilterGraph replay of the same batch too."""
+    n, r = 140_003, 300
+    _, dec = make_dec(n, r, 25, 61)
+    qb = queries(n, b, 62, empty=(1,) if b > 4 else ())
+    ctx = N.Context.get()
+    assert ctx.online_path == "tc" and ranking.online_path(dec, b, 100) == "stream"
+    dq = ranking.DeviceQueries(qb, dec.dtype, dec.eta_device.device)
+    ws = torch.empty(ranking.filter_workspace_bytes(dec, b, want_x=False, topk=100), dtype=torch.uint8,
+                     device=dec.eta_device.device)
+    res = ranking.filter_device(dec, ranking.h_alpha(0.99), dq, topk=100, want_x=False, workspace=ws)
+    torch.cuda.synchronize()
+    assert ctx.last_online_path == "stream"
+    assert ranking.last_fallback_count(ws, dec, b) == 0
+    si, sv = res.top_idx.cpu().numpy(), res.top_val.cpu().numpy()
+    ui, uv = padded_unpruned(dec, qb, 100)
+    np.testing.assert_array_equal(si, ui)
+    np.testing.assert_array_equal(sv.view(np.uint32), uv.view(np.uint32))
+    fg = ranking.FilterGraph(dec, ranking.h_alpha(0.99), b=b, nnz_cap=int(qb.y_ptr[-1]), topk=100)
+    fg.submit(qb)
+    gi, gv = fg.fetch()
+    np.testing.assert_array_equal(gi, ui)
+    np.testing.assert_array_equal(gv.view(np.uint32), uv.view(np.uint32))
+
+
+def test_stream_long_rows_tiny_and_empty_chunks():
+    """Packed-stream chunking edge cases: rows as long as r (a chunk spans up
+    to kChunk - 1 + r entries), runs of thousands of empty rows (chunks that
+    hold many rows or none), and a U~ smaller than one chunk."""
+    rng = np.random.default_rng(71)
+    for n, r, full_rows in ((131_072, 512, 40), (3_000, 64, 2)):
+        lens = rng.integers(0, 30, size=n)
+        lens[rng.choice(n, full_rows, replace=False)] = r
+        lens[5000:9000 if n > 9000 else 0] = 0
+        if n < 5000:
+            lens[:] = rng.integers(0, 2, size=n)  # nnz < one chunk
+            lens[7] = r
+        indptr = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+        cols = np.concatenate([np.sort(rng.choice(r, size=k, replace=False)) for k in lens]).astype(np.int32)
+        U = sp.csr_matrix((rng.standard_normal(indptr[-1]), cols, indptr), shape=(n, r))
+        eta = np.sqrt(np.asarray(U.multiply(U).sum(axis=1)).ravel())
+        lam = np.sort(rng.uniform(-0.3, 1.0, r))[::-1].copy()
+        host = SimpleNamespace(U=U, eigenvalues=lam, eta=eta, variant="sparse", provenance=None, components=None)
+        dec = spectral.SpectralDecomposition.from_host(host, dtype="float32")
+        K = min(100, n)
+        for b in (1, 8, 13):
+            qb = queries(n, b, 72 + b, k=20)
+            ctx = N.Context.get()
+            ctx.set_online_path("stream")
+            try:
+                assert ranking.online_path(dec, b, K) == "stream"
+                res = ranking.filter_device(dec, ranking.h_alpha(0.99), ranking.DeviceQueries(qb, dec.dtype,
+                                            dec.eta_device.device), topk=K, want_x=False)
+                torch.cuda.synchronize()
+            finally:
+                ctx.set_online_path("tc")
+            ui, uv = padded_unpruned(dec, qb, K)
+            np.testing.assert_array_equal(res.top_idx.cpu().numpy(), ui)
+            np.testing.assert_array_equal(res.top_val.cpu().numpy().view(np.uint32), uv.view(np.uint32))
