@@ -436,6 +436,9 @@ def offline_cpu_full(S, r, p, q, tau):
 # FSR arm
 # ---------------------------------------------------------------------------
 
+KNN_STATS = {}  # rows of the last build_inputs settled by each certification stage (knn.certified_topk)
+
+
 def build_inputs(cfg, n, n_queries, device, dtype):
     import torch
 
@@ -443,7 +446,9 @@ def build_inputs(cfg, n, n_queries, device, dtype):
 
     t0 = time.perf_counter()
     X, Qv, _ = workloads.device_cluster_descriptors(cfg, device, n=n, queries=n_queries)
-    W = knn.mutual_knn_graph_device(X, cfg.k, cfg.gamma, gemm_dtype=torch.bfloat16)  # bf16 candidates, fp32 re-score
+    KNN_STATS.clear()
+    # certified bf16 candidates, fp32 re-score
+    W = knn.mutual_knn_graph_device(X, cfg.k, cfg.gamma, gemm_dtype=torch.bfloat16, stats=KNN_STATS)
     deg = graph.degrees_device(W, device)
     S = graph.normalize_adjacency(W, deg, dtype=dtype, device=device)
     y_ptr, y_idx, y_val = knn.observation_batch_device(Qv, X, cfg.y_top, cfg.gamma)
@@ -795,6 +800,7 @@ def run_fsr(args, cfg, n, rank, world, local_rank):
         "spmm_fp32_tflops": 2.0 * nnz_s * r_hat / (spmm_ms_iter * 1e-3) / 1e12,
         "stage_ms": {k: round(v[0], 3) for k, v in stages.items() if v[1]},
         "nnz_W": nnz_w, "isolated_vertices": isolated, "kept_nnz": sdec.U_device.nnz, "inputs_build_s": t_inputs,
+        "knn_certified_rows": dict(KNN_STATS),
         "clocks": off_clk,
         "timed_run": "second of two identical runs (the first sizes allocations)" if not args.no_offline_warmup
                      else "first run",

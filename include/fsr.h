@@ -258,6 +258,11 @@ int fsr_sparsify_select(fsr_ctx* ctx, int dtype, int64_t n, int64_t r, const voi
 int fsr_sparsify(fsr_ctx* ctx, int dtype, int64_t n, int64_t r, const void* U, int64_t ldu, int64_t tau,
                  int64_t* indptr_out, int32_t* indices_out, void* values_out, int64_t capacity, double* eta,
                  int64_t* nnz_host);
+/* The second half of fsr_sparsify for a threshold (T, ties) already chosen
+ * by fsr_sparsify_select (outputs must hold its `keep` entries). */
+int fsr_sparsify_apply(fsr_ctx* ctx, int dtype, int64_t n, int64_t r, const void* U, int64_t ldu, uint64_t T,
+                       int64_t ties, int64_t* indptr_out, int32_t* indices_out, void* values_out, double* eta,
+                       int64_t* nnz_host);
 
 /* ---- K8/K9: online batch  (ranking.py:219-255 _project / filter) ------------
  * For b observation columns y_j (CSC: y_ptr[b+1], y_idx row ids, y_val in dtype):

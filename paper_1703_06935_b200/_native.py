@@ -88,6 +88,8 @@ _SIGS = {
                                      _c_i64p, _c_i64p]),
     "fsr_sparsify": (_c_int, [_c_p, _c_int, _c_i64, _c_i64, _c_p, _c_i64, _c_i64, _c_p, _c_p, _c_p, _c_i64, _c_p,
                               _c_i64p]),
+    "fsr_sparsify_apply": (_c_int, [_c_p, _c_int, _c_i64, _c_i64, _c_p, _c_i64, _c_u64, _c_i64, _c_p, _c_p, _c_p,
+                                    _c_p, _c_i64p]),
     "fsr_stream_u_bytes": (_c_i64, [_c_i64, _c_i64, _c_i64]),
     "fsr_stream_u_build": (_c_int, [_c_p, _c_i64, _c_i64, _c_i64, _c_p, _c_p, _c_p, _c_p]),
     "fsr_filter_stream_applicable": (_c_int, [_c_i64, _c_i64, _c_i64, _c_i64, _c_i64]),

@@ -27,6 +27,16 @@ int fsr_ctx_create(int device, fsr_ctx** out) {
   }
   // Pure FP32/FP64 arithmetic: never let cuBLAS substitute TF32 tensor ops.
   cublasSetMathMode(ctx->blas, CUBLAS_PEDANTIC_MATH);
+  // The operator-level calls (fsr_ops.cu) take stream-ordered temporaries
+  // from the device's default memory pool; keep freed blocks in the pool
+  // instead of returning them at every synchronisation (re-mapping hundreds of
+  // MB per call cost ~0.2 s per sparsify at C3).
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+    uint64_t keep = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  }
+  cudaGetLastError();
   *out = ctx;
   return FSR_OK;
 }

@@ -352,6 +352,14 @@ int fsr_sparsify(fsr_ctx* ctx, int dtype, int64_t n, int64_t r, const void* U, i
   FSR_TRY(fsr_sparsify_select(ctx, dtype, n, r, U, ldu, tau, &T, &ties, &keep));
   FSR_REQUIRE(ctx, capacity >= keep, "sparsify: capacity %lld below the kept count %lld", (long long)capacity,
               (long long)keep);
+  return fsr_sparsify_apply(ctx, dtype, n, r, U, ldu, T, ties, indptr_out, indices_out, values_out, eta, nnz_host);
+}
+
+int fsr_sparsify_apply(fsr_ctx* ctx, int dtype, int64_t n, int64_t r, const void* U, int64_t ldu, uint64_t T,
+                       int64_t ties, int64_t* indptr_out, int32_t* indices_out, void* values_out, double* eta,
+                       int64_t* nnz_host) {
+  FSR_REQUIRE(ctx, n >= 1 && r >= 1 && U && ldu >= r && ties >= 0, "sparsify_apply: bad arguments");
+  FSR_REQUIRE(ctx, indptr_out && indices_out && values_out && eta && nnz_host, "sparsify_apply: missing outputs");
   ops::DevBuf cnt;
   FSR_TRY(cnt.alloc(ctx, (size_t)n * 16));
   int64_t* gt = cnt.as<int64_t>();

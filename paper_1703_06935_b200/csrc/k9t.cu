@@ -418,12 +418,24 @@ __global__ void __launch_bounds__(256) k9t_threshold_kernel(int64_t b, int64_t n
     for (int level = 0; level < 2; ++level) {
       for (int t = threadIdx.x; t < nb; t += blockDim.x) hist[t] = 0;
       __syncthreads();
-      for (int64_t e = threadIdx.x; e < n_valid_s; e += blockDim.x) {
-        const uint32_t k = kq[e];
-        if (level == 0)
-          atomicAdd(&hist[k >> (KB - HB)], 1u);
-        else if ((k >> (KB - HB)) == prefix)
-          atomicAdd(&hist[(k >> (KB - 2 * HB)) & (nb - 1)], 1u);
+      // 8 keys per thread in flight before their atomics (a small batch runs
+      // one CTA per query: a load-then-atomic loop was DRAM-latency bound)
+      for (int64_t e0 = (int64_t)threadIdx.x; e0 < n_valid_s; e0 += 8 * (int64_t)blockDim.x) {
+        uint32_t kk[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int64_t e = e0 + (int64_t)u * blockDim.x;
+          kk[u] = e < n_valid_s ? kq[e] : 0u;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          if (e0 + (int64_t)u * blockDim.x >= n_valid_s) break;
+          const uint32_t k = kk[u];
+          if (level == 0)
+            atomicAdd(&hist[k >> (KB - HB)], 1u);
+          else if ((k >> (KB - HB)) == prefix)
+            atomicAdd(&hist[(k >> (KB - 2 * HB)) & (nb - 1)], 1u);
+        }
       }
       __syncthreads();
       topk::find_bin_t<256>(hist, nb, level == 0 ? target : target - above0, &found_bin, &above);
@@ -495,8 +507,41 @@ __device__ __forceinline__ float exact_row_group(int64_t i, int64_t q, const int
                                      nullptr, 0, y_ptr, y_idx, mask);
 }
 
+// Small batches: the finish kernel is one CTA per query, so its exact
+// re-score (~100-400 rows of ~100 dependent entries) would run on a handful of
+// SMs.  This kernel re-scores every candidate of every query instead, one
+// 8-lane group per (query, slot), spread over the GPU; finish then only reads
+// the values.  Same sequential fp32 order (exact_row_group).
+__global__ void __launch_bounds__(256) k9t_rescore_kernel(
+    int64_t b, const int32_t* __restrict__ cand, const int32_t* __restrict__ ccount,
+    const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices, const float* __restrict__ vals,
+    const float* __restrict__ Zs, int64_t ldz, const double* __restrict__ eta, int copy,
+    const int64_t* __restrict__ y_ptr, const int64_t* __restrict__ y_idx, const float* __restrict__ y_val,
+    float* __restrict__ pre);
+
 constexpr int kKeep = 1024;  // rows re-scored exactly per query (upper >= lambda_K); more -> fallback
 constexpr size_t kFinishSmem = (size_t)kCap * 12 + (size_t)(1 << topk::kHistBits) * 4 + (size_t)kKeep * 16;
+
+__global__ void __launch_bounds__(256) k9t_rescore_kernel(
+    int64_t b, const int32_t* __restrict__ cand, const int32_t* __restrict__ ccount,
+    const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices, const float* __restrict__ vals,
+    const float* __restrict__ Zs, int64_t ldz, const double* __restrict__ eta, int copy,
+    const int64_t* __restrict__ y_ptr, const int64_t* __restrict__ y_idx, const float* __restrict__ y_val,
+    float* __restrict__ pre) {
+  constexpr int G = 8;
+  const int lane = threadIdx.x & 31, gl = threadIdx.x & (G - 1);
+  const unsigned gmask = 0xffu << (lane & ~(G - 1));
+  const int64_t ngroups = ((int64_t)gridDim.x * blockDim.x) / G;
+  for (int64_t g = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / G; g < b * kCap; g += ngroups) {
+    const int64_t q = g / kCap;
+    const int slot = (int)(g - q * kCap);
+    const int cnt = ccount[q];
+    if (cnt < 0 || cnt > kCap || slot >= cnt) continue;  // group-uniform
+    const float v = exact_row_group<G>(cand[g], q, indptr, indices, vals, Zs, ldz, eta, copy, y_ptr, y_idx, y_val,
+                                       gmask);
+    if (gl == 0) pre[g] = v;
+  }
+}
 
 __global__ void __launch_bounds__(kFinishThreads) k9t_finish_kernel(
     const float* __restrict__ cb, const QParam* __restrict__ qpar, const uint32_t* __restrict__ thr,
@@ -505,7 +550,7 @@ __global__ void __launch_bounds__(kFinishThreads) k9t_finish_kernel(
     const float* __restrict__ vals, const float* __restrict__ Zs, int64_t ldz, const double* __restrict__ eta,
     int copy, const int64_t* __restrict__ y_ptr, const int64_t* __restrict__ y_idx, const float* __restrict__ y_val,
     int64_t K, int64_t* __restrict__ out_idx, float* __restrict__ out_val, int* __restrict__ nflag,
-    int* __restrict__ flags, int2* __restrict__ stats) {
+    int* __restrict__ flags, int2* __restrict__ stats, const float* __restrict__ pre) {
   constexpr int HB = topk::kHistBits, NB = 1 << HB;
   extern __shared__ __align__(16) unsigned char dyn[];
   uint64_t* kkey = (uint64_t*)dyn;             // [kKeep] exact order keys of the kept rows
@@ -598,17 +643,24 @@ __global__ void __launch_bounds__(kFinishThreads) k9t_finish_kernel(
   const unsigned gmask = 0xffu << (lane & ~(G - 1));
   if (threadIdx.x == 0) n_next = kFinishThreads / G;
   __syncthreads();
-  for (unsigned t = grp; t < keep;) {
-    const int64_t packed = kidx[t];
-    const int slot = (int)(packed & 4095);
-    if (slot < cnt) {
-      const float v = exact_row_group<G>(packed >> 12, q, indptr, indices, vals, Zs, ldz, eta, copy, y_ptr, y_idx,
-                                         y_val, gmask);
-      if (gl == 0) cv[slot] = v;
+  if (pre) {  // small batches: every candidate was re-scored by k9t_rescore_kernel
+    for (unsigned t = threadIdx.x; t < keep; t += blockDim.x) {
+      const int slot = (int)(kidx[t] & 4095);
+      if (slot < cnt) cv[slot] = pre[q * kCap + slot];
     }
-    unsigned nt = 0;
-    if (gl == 0) nt = atomicAdd(&n_next, 1u);
-    t = __shfl_sync(gmask, nt, 0, G);
+  } else {
+    for (unsigned t = grp; t < keep;) {
+      const int64_t packed = kidx[t];
+      const int slot = (int)(packed & 4095);
+      if (slot < cnt) {
+        const float v = exact_row_group<G>(packed >> 12, q, indptr, indices, vals, Zs, ldz, eta, copy, y_ptr, y_idx,
+                                           y_val, gmask);
+        if (gl == 0) cv[slot] = v;
+      }
+      unsigned nt = 0;
+      if (gl == 0) nt = atomicAdd(&n_next, 1u);
+      t = __shfl_sync(gmask, nt, 0, G);
+    }
   }
   __syncthreads();
   for (unsigned t = threadIdx.x; t < keep; t += blockDim.x) kkey[t] = topk::order_key(cv[kidx[t] & 4095]);
@@ -831,9 +883,11 @@ struct Work {
   unsigned* nlow;
   int32_t* cand;
   float* cval;
+  float* cex;   // small batches: exact scores of every candidate, computed by k9t_rescore_kernel (else null)
   int2* stats;  // per query (candidates, rows re-scored): diagnostics
   float* Xt;
 };
+constexpr int64_t kPreScoreMaxB = 64;  // batches up to this size re-score all candidates on many CTAs
 // ks_rows: sample keys per query (K9t: sample_rows(n); the streaming path: n)
 inline size_t work_bytes(int64_t n, int64_t r, int64_t b, Work* w, void* base, int64_t ks_rows) {
   char* p = (char*)base;
@@ -856,6 +910,7 @@ inline size_t work_bytes(int64_t n, int64_t r, int64_t b, Work* w, void* base, i
   W.nlow = (unsigned*)take((size_t)b * 4);
   W.cand = (int32_t*)take((size_t)b * kCap * 4);
   W.cval = (float*)take((size_t)b * kCap * 4);
+  W.cex = b <= kPreScoreMaxB ? (float*)take((size_t)b * kCap * 4) : nullptr;
   W.Ks = (uint32_t*)take((size_t)b * ks_rows * 4);  // sample keys: last but one (their count differs by path)
   W.Xt = (float*)take((size_t)n * b * 4);
   if (w) *w = W;
@@ -911,73 +966,51 @@ inline int cluster_choice() {
 // ------------------------------------------------------ small-batch stream --
 // K9s: the same certified top-K for batches too small to feed the tensor
 // cores (b < 128: K9t would stream the whole 10 GB fp16 U~ for a handful of
-// queries, the exact sparse K9 gathers fp32 rows from L2).  U~ is re-packed
-// once per decomposition into 4 bytes per entry -- fp16 value << 16 | column
-// (r <= 65536) -- 0.4 GB at C3 2% instead of the 0.8 GB fp32 CSR, and streamed
-// from HBM by 1-D TMA bulk copies into a shared-memory ring, one chunk of
-// ~kChunk entries at a time.  The NB-query slice of the scaled fp16 Zh sits in
-// shared memory as [column][query] (NB r 2 bytes); each entry costs NB
-// fma.rn.f32.f16 and a warp per row sums its entries lane-strided, then a
-// butterfly reduce-scatter (NB/2 + NB/4 + ... + log2(32/NB) shuffles).  The
-// sums differ from K9t's only in order, which the bound's gamma_m term covers,
-// and the per-row factor c_i is K9t's (it also covers the tensor-core
-// accumulation, so it is conservative here).  Threshold, finish, empty and
-// fallback are K9t's kernels: the top-K is the unpruned sequential fp32 top-K
-// bit for bit.
+// queries; the exact sparse K9 gathers 4-byte fp32 Zs values).  U~ is
+// re-packed once per decomposition into 4 bytes per entry -- fp16 value << 16
+// | column (r <= 65536): 0.4 GB at C3 2% instead of the 0.8 GB fp32 CSR --
+// and streamed from HBM by warp-per-row passes at full occupancy (the b = 1
+// exact kernel's shape, spmv_smem_kernel, which reaches ~3 TB/s on the fp32
+// CSR).  The NB-query slice of the scaled fp16 Zh sits in shared memory as
+// [column][query] (NB r 2 bytes); each entry costs NB fma.rn.f32.f16, the
+// warp's partial sums meet in a butterfly reduce-scatter.  The sums differ
+// from K9t's only in order, which the bound's gamma_m term covers, and the
+// per-row factor c_i is K9t's (it also covers tensor-core accumulation, so it
+// is conservative here).  Threshold (on a 1/32 sample of 128-row tiles),
+// finish, empty and fallback are K9t's kernels: the top-K is the unpruned
+// sequential fp32 top-K bit for bit.
+// (A TMA-bulk chunk pipeline with a producer warp was measured slower here:
+// one CTA per SM cannot keep enough rows in flight.)
 namespace stream {
 
-constexpr int kChunk = 4096;       // chunk c = the rows whose first entry lies in [c kChunk, (c + 1) kChunk)
-constexpr int kConsumers = 16;     // warps summing rows; one more warp issues the chunk copies
-constexpr int kLpr = 8;            // lanes per row: 4 rows in flight per warp (rows are ~50-100 entries)
-constexpr int kThreads = 32 * (kConsumers + 1);
-constexpr int kStages = 3;
-constexpr int kSampleStride = 32;  // sample pass: every 32nd chunk
-constexpr int kRowsMax = 256;      // rows whose indptr / c_i ride along with a chunk's entries (else global reads)
+constexpr int kThreads = 256;
+constexpr int kTile = 128;         // sample unit: 128 consecutive rows
+constexpr int kSampleStride = 32;  // every 32nd tile
 
-inline int64_t nchunks(int64_t nnz) { return std::max<int64_t>(1, (nnz + kChunk - 1) / kChunk); }
-inline int64_t nsample(int64_t nnz) { return (nchunks(nnz) + kSampleStride - 1) / kSampleStride; }
-// a chunk spans <= kChunk - 1 + (longest row <= r) entries, +3 for the 16-byte aligned start
-inline int64_t stage_words(int64_t r) { return round_up(kChunk + r + 8, 4); }
-// one stage: entries | indptr slice (kRowsMax + 4 int64) | c_i slice (kRowsMax + 8 floats)
-constexpr int kIpWords = 2 * (kRowsMax + 4), kCbWords = kRowsMax + 8;
-inline int64_t stage_total_words(int64_t r) { return stage_words(r) + kIpWords + kCbWords; }
-inline size_t smem_bytes(int nb, int64_t r) {
-  return (size_t)kStages * stage_total_words(r) * 4 + (size_t)round_up((int64_t)nb * r * 2, 16) + 64 +
-         (size_t)nb * 24 + kStages * 24 + 16 + (size_t)2 * kRowsMax * nb * 4;
+inline int64_t sample_tiles(int64_t n) { return ((n + kTile - 1) / kTile + kSampleStride - 1) / kSampleStride; }
+inline int64_t sample_slots(int64_t n) { return sample_tiles(n) * kTile; }
+inline int64_t sample_valid(int64_t n) {
+  const int64_t st = sample_tiles(n), last = (st - 1) * kSampleStride;
+  return (st - 1) * kTile + std::min<int64_t>(kTile, n - last * kTile);
 }
+inline size_t smem_bytes(int nb, int64_t r) { return (size_t)round_up((int64_t)nb * r * 2, 16) + (size_t)nb * 24; }
 
 struct Layout {
   uint32_t* pk;    // [nnz + 16] fp16 value << 16 | column
-  int64_t* ipl;    // [n + 16] copy of indptr (padded: 16-byte TMA reads past row n stay inside)
-  float* cb;       // [n (+ pad)] per-row bound factor (K9t's row_bound)
+  float* cb;       // [n] per-row bound factor (K9t's row_bound)
   int* cmax_bits;  // max c_i (as int bits)
-  int32_t* crow;   // [nchunks + 1] first row of each chunk
-  longlong2* desc; // [nchunks + 1] (first row, its first entry) of each chunk: the producer's one load
-  int32_t* soff;   // [nsample + 1] first sample slot of each sampled chunk; soff[nsample] = sampled rows
 };
 inline Layout layout(void* base, int64_t n, int64_t nnz) {
   char* p = (char*)base;
   Layout L;
   L.pk = (uint32_t*)p;
   p += al256((size_t)(nnz + 16) * 4);
-  L.ipl = (int64_t*)p;
-  p += al256((size_t)(n + 16) * 8);
   L.cb = (float*)p;
-  p += al256((size_t)n * 4 + 64);
+  p += al256((size_t)n * 4);
   L.cmax_bits = (int*)p;
-  p += 256;
-  L.crow = (int32_t*)p;
-  p += al256((size_t)(nchunks(nnz) + 1) * 4);
-  L.desc = (longlong2*)p;
-  p += al256((size_t)(nchunks(nnz) + 1) * 16);
-  L.soff = (int32_t*)p;
   return L;
 }
-inline size_t layout_bytes(int64_t n, int64_t nnz) {
-  return al256((size_t)(nnz + 16) * 4) + al256((size_t)(n + 16) * 8) + al256((size_t)n * 4 + 64) + 256 +
-         al256((size_t)(nchunks(nnz) + 1) * 4) + al256((size_t)(nchunks(nnz) + 1) * 16) +
-         al256((size_t)(nsample(nnz) + 1) * 4);
-}
+inline size_t layout_bytes(int64_t n, int64_t nnz) { return al256((size_t)(nnz + 16) * 4) + al256((size_t)n * 4) + 256; }
 
 // warp per row: packed entries + the bound factor of densify_kernel
 __global__ void __launch_bounds__(256) pack_kernel(int64_t n, const int64_t* __restrict__ indptr,
@@ -1006,51 +1039,6 @@ __global__ void __launch_bounds__(256) pack_kernel(int64_t n, const int64_t* __r
   if (lane == 0) atomicMax(cmax_bits, cmax);
 }
 
-// crow[c] = first row whose first entry is >= c kChunk (crow[nch] = n)
-__global__ void chunk_rows_kernel(int64_t n, const int64_t* __restrict__ indptr, int64_t nch,
-                                  int32_t* __restrict__ crow) {
-  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (c > nch) return;
-  if (c == nch || c == 0) {
-    crow[c] = c == 0 ? 0 : (int32_t)n;
-    return;
-  }
-  const int64_t target = c * kChunk;
-  int64_t lo = 0, hi = n;  // indptr[n] = nnz > target
-  while (lo < hi) {
-    const int64_t mid = (lo + hi) >> 1;
-    if (indptr[mid] >= target)
-      hi = mid;
-    else
-      lo = mid + 1;
-  }
-  crow[c] = (int32_t)lo;
-}
-
-__global__ void chunk_desc_kernel(const int64_t* __restrict__ indptr, int64_t nch, const int32_t* __restrict__ crow,
-                                  longlong2* __restrict__ desc) {
-  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (c <= nch) desc[c] = make_longlong2(crow[c], indptr[crow[c]]);
-}
-
-__global__ void sample_offsets_kernel(int64_t nch, const int32_t* __restrict__ crow, int32_t* __restrict__ soff) {
-  if (threadIdx.x || blockIdx.x) return;
-  const int64_t ns = (nch + kSampleStride - 1) / kSampleStride;
-  int32_t s = 0;
-  for (int64_t j = 0; j < ns; ++j) {
-    soff[j] = s;
-    s += crow[j * kSampleStride + 1] - crow[j * kSampleStride];
-  }
-  soff[ns] = s;
-}
-
-__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                   smem_u32(dst)),
-               "l"(src), "r"(bytes), "r"(smem_u32(bar))
-               : "memory");
-}
-
 // acc[q] += u * zh[col][q] for the NB queries (fp16 x fp16 -> fp32, one FHFMA each)
 template <int NB>
 __device__ __forceinline__ void entry_fma(uint32_t w, const __half* __restrict__ zh, float (&acc)[NB]) {
@@ -1077,13 +1065,13 @@ __device__ __forceinline__ void entry_fma(uint32_t w, const __half* __restrict__
   }
 }
 
-// Butterfly reduce-scatter of NB per-lane partial sums over a kLpr-lane group:
-// returns the group sum of query qidx(lane) (group lane bits high to low).
-template <int NB>
-__device__ __forceinline__ float reduce_scatter(float (&a)[NB], int lane) {
-  static_assert(NB <= kLpr, "one query per lane at least");
+// Butterfly reduce-scatter of M per-lane partial sums over the warp: returns
+// the warp sum of output oidx(lane) (lane bits 4, 3, ... most significant first).
+template <int M>
+__device__ __forceinline__ float reduce_scatter(float (&a)[M], int lane) {
+  static_assert(M >= 1 && M <= 32 && (M & (M - 1)) == 0, "M a power of two <= 32");
 #pragma unroll
-  for (int h = NB / 2, off = kLpr / 2; h >= 1; h >>= 1, off >>= 1) {
+  for (int h = M / 2, off = 16; h >= 1; h >>= 1, off >>= 1) {
     const bool upper = lane & off;
 #pragma unroll
     for (int j = 0; j < h; ++j) {
@@ -1093,51 +1081,41 @@ __device__ __forceinline__ float reduce_scatter(float (&a)[NB], int lane) {
     }
   }
 #pragma unroll
-  for (int off = kLpr / 2 / NB; off >= 1; off >>= 1) a[0] += __shfl_xor_sync(0xffffffffu, a[0], off);
+  for (int off = 16 / M; off >= 1; off >>= 1) a[0] += __shfl_xor_sync(0xffffffffu, a[0], off);
   return a[0];
 }
-template <int NB>
-__device__ __forceinline__ int qidx(int lane) {
-  static_assert(kLpr == 8, "lane bits 2, 1, 0 of the group");
-  int q = 0;
+template <int M>
+__device__ __forceinline__ int oidx(int lane) {
+  int o = 0;
 #pragma unroll
-  for (int t = 0, b = 2; (1 << t) < NB; ++t, --b) q = (q << 1) | ((lane >> b) & 1);  // bit of offset kLpr/2 first
-  return q;
+  for (int t = 0, b = 4; (1 << t) < M; ++t, --b) o = (o << 1) | ((lane >> b) & 1);
+  return o;
 }
 
-// MODE 0 (sample): every kSampleStride-th chunk, lower keys into Ks[q * ns + soff + row-in-chunk].
-// MODE 1 (select): every chunk; counts lower >= t, appends rows with upper >= t.
-// Queries q0 .. q0 + nq - 1 (nq <= NB); one CTA per SM, persistent over chunks.
+// rows summed together per warp step (R rows x NB queries partial sums, one reduce-scatter)
+template <int NB>
+constexpr int rows_per_step() { return NB <= 2 ? 4 : 2; }  // R = 8 for NB = 1 measured slower (0.33 vs 0.23 ms)
+
+// MODE 0 (sample): the rows of every 32nd 128-row tile, lower keys into
+//   Ks[q * ns + slot] (slot = sampled tile * 128 + row in tile).
+// MODE 1 (select): every row; counts lower >= t, appends rows with upper >= t.
+// Queries q0 .. q0 + nq - 1 (nq <= NB).  A warp takes 32 consecutive rows:
+// their indptr / c_i in one coalesced load, then R rows at a time with all
+// their entries' loads in flight before any is used (the per-row dependent
+// global loads of a warp-per-row loop left it latency-bound at ~1.4 TB/s).
 template <int MODE, int NB>
-__global__ void __launch_bounds__(kThreads, 1)
-    stream_kernel(const uint32_t* __restrict__ pk, const int64_t* __restrict__ indptr,
-                  const longlong2* __restrict__ desc, int64_t nch, int r, int sw, const __half* __restrict__ Zh,
-                  int64_t ldzh, int q0, int nq, const float* __restrict__ cb, const float2* __restrict__ qp,
-                  const QParam* __restrict__ qpar, const uint32_t* __restrict__ thr, const int32_t* __restrict__ soff,
+__global__ void __launch_bounds__(kThreads)
+    stream_kernel(const uint32_t* __restrict__ pk, const int64_t* __restrict__ indptr, int64_t n, int r,
+                  const __half* __restrict__ Zh, int64_t ldzh, int q0, int nq, const float* __restrict__ cb,
+                  const float2* __restrict__ qp, const QParam* __restrict__ qpar, const uint32_t* __restrict__ thr,
                   uint32_t* __restrict__ Ks, int64_t ns, int32_t* __restrict__ cand, float* __restrict__ cval,
                   int32_t* __restrict__ ccount, unsigned* __restrict__ nlow) {
+  constexpr int R = rows_per_step<NB>(), M = R * NB;
   extern __shared__ __align__(16) uint8_t smem_raw[];
-  const int stw = sw + kIpWords + kCbWords;                                  // words per stage
-  uint32_t* stage = (uint32_t*)smem_raw;                                     // [kStages][stw]
-  __half* zh = (__half*)(stage + (size_t)kStages * stw);                      // [r][NB]
-  float4* sp = (float4*)(smem_raw + (size_t)kStages * stw * 4 + round_up((int64_t)NB * r * 2, 16));  // [NB]
-  uint64_t* full = (uint64_t*)(sp + NB);         // [kStages]; sp = (tf_pre | 0, 1/s_q, cz, zb)
-  uint64_t* empty = full + kStages;              // [kStages]
-  int2* meta = (int2*)(empty + kStages);         // [kStages] (first row, rows) of the staged chunk
-  uint32_t* sthr = (uint32_t*)(meta + kStages);  // [NB]
-  unsigned* scnt = sthr + NB;                    // [NB]
-  float* xs = (float*)(((uintptr_t)(scnt + NB) + 15) & ~(uintptr_t)15);  // [2][kRowsMax][NB] row sums
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t step = MODE == 0 ? (int64_t)kSampleStride * gridDim.x : gridDim.x;
-  const int64_t c_first = MODE == 0 ? (int64_t)kSampleStride * blockIdx.x : blockIdx.x;
-
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < kStages; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], kConsumers);
-    }
-    fence_barrier_init();
-  }
+  __half* zh = (__half*)smem_raw;                                                   // [r][NB]
+  float4* sp = (float4*)(smem_raw + round_up((int64_t)NB * r * 2, 16));            // [NB]
+  uint32_t* sthr = (uint32_t*)(sp + NB);                                           // [NB]
+  unsigned* scnt = sthr + NB;                                                      // [NB]
   // the queries' fp16 Zh slice as [column][query] (padding queries zero) and their parameters
   for (int64_t t = threadIdx.x; t < (int64_t)r * NB; t += kThreads) {
     const int q = (int)(t % NB);
@@ -1162,208 +1140,154 @@ __global__ void __launch_bounds__(kThreads, 1)
     sthr[q] = tk;
     scnt[q] = 0;
   }
-  for (int t = threadIdx.x; t < 2 * kRowsMax * NB; t += kThreads) xs[t] = 0.f;
   __syncthreads();
-
-  if (warp == kConsumers) {
-    // producer: chunk descriptors of the next 32 chunks in one load per lane,
-    // then lane 0 issues each chunk into the ring as soon as its stage is free.
-    // One mbarrier transaction carries the packed entries, the chunk's indptr
-    // slice and its c_i slice (chunks of more than kRowsMax rows -- runs of
-    // empty rows -- leave those two to global reads).
-    int k = 0;
-    for (int64_t cb0 = c_first; cb0 < nch; cb0 += 32 * step) {
-      const int64_t cl = cb0 + lane * step;
-      longlong2 d0 = make_longlong2(0, 0), d1 = make_longlong2(0, 0);
-      if (cl < nch) {
-        d0 = desc[cl];
-        d1 = desc[cl + 1];
-      }
-      for (int j = 0; j < 32 && cb0 + j * step < nch; ++j, ++k) {
-        const int32_t r0 = (int32_t)__shfl_sync(0xffffffffu, d0.x, j), r1 = (int32_t)__shfl_sync(0xffffffffu, d1.x, j);
-        const int64_t f = __shfl_sync(0xffffffffu, d0.y, j), e1 = __shfl_sync(0xffffffffu, d1.y, j);
-        if (lane == 0) {
-          const int s = k % kStages;
-          if (k >= kStages) mbar_wait(&empty[s], ((k / kStages) - 1) & 1);
-          uint32_t* st = stage + (size_t)s * stw;
-          meta[s] = make_int2(r0, r1 - r0);
-          const int64_t e0 = f & ~(int64_t)3;
-          const uint32_t ebytes = e1 > f ? (uint32_t)(round_up(e1 - e0, 4) * 4) : 0;
-          const bool small = r1 - r0 <= kRowsMax;
-          const int32_t i0 = r0 & ~1, c0 = r0 & ~3;
-          const uint32_t ibytes = small ? (uint32_t)(round_up((int64_t)r1 + 1 - i0, 2) * 8) : 0;
-          const uint32_t cbytes = small && r1 > r0 ? (uint32_t)(round_up((int64_t)r1 - c0, 4) * 4) : 0;
-          const uint32_t tx = ebytes + ibytes + cbytes;
-          if (tx) {
-            mbar_expect_tx(&full[s], tx);
-            if (ebytes) bulk_load(st, pk + e0, ebytes, &full[s]);
-            if (ibytes) bulk_load(st + sw, indptr + i0, ibytes, &full[s]);
-            if (cbytes) bulk_load(st + sw + kIpWords, cb + c0, cbytes, &full[s]);
-          } else {
-            mbar_arrive(&full[s]);
-          }
-        }
-        __syncwarp();
-      }
+  const int lane = threadIdx.x & 31;
+  const int my = oidx<M>(lane);  // this lane's output after the reduce-scatter: row my / NB, query my % NB
+  const int my_r = my / NB, my_q = my % NB;
+  const bool leader = (lane & (32 / M - 1)) == 0 && my_q < nq;
+  // rows per warp block: 32 for the main pass; 8 for the sample pass (1/32 of
+  // the rows -- smaller blocks keep enough warps in flight)
+  constexpr int RB = MODE == 0 ? 8 : 32;
+  const int64_t nw = ((int64_t)gridDim.x * kThreads) >> 5;
+  const int64_t blocks = ((MODE == 0 ? ns : n) + RB - 1) / RB;
+  auto first_row = [&](int64_t blk) {
+    const int64_t t0 = blk * RB;  // MODE 0: sample slot of the block's first row
+    return MODE == 0 ? (t0 / kTile) * kSampleStride * kTile + t0 % kTile : t0;
+  };
+  // the block's indptr / c_i, loaded one block ahead (their latency overlaps the current block's rows)
+  int64_t lo_n = 0;
+  int len_n = 0;
+  float cl_n = 0.f;
+  auto fetch = [&](int64_t blk) {
+    lo_n = 0;
+    len_n = 0;
+    cl_n = 0.f;
+    const int64_t il = first_row(blk) + lane;
+    if (blk < blocks && lane < RB && il < n) {
+      lo_n = __ldg(indptr + il);
+      len_n = (int)(__ldg(indptr + il + 1) - lo_n);
+      cl_n = __ldg(cb + il);
     }
-  } else {
-    // a row's approximate score x~ (any summation order: the bound's gamma_m
-    // term covers it) -> sample key or candidate bookkeeping
-    auto row_out = [&](int32_t i, int32_t j, int q, float v, float c_i, int32_t slot0) {
-      const float4 p = sp[q];
-      const float x = v * p.y;
-      if (MODE == 0) {
-        Ks[(int64_t)(q0 + q) * ns + slot0 + j] = prune::key32(__fsub_rd(x, prune::bound_of(c_i, p.w)));
-      } else if (x + p.z >= p.x) {  // rare: within reach of the threshold
-        const float bd = prune::bound_of(c_i, p.w);
-        const uint32_t tk = sthr[q];
-        if (prune::key32(__fsub_rd(x, bd)) >= tk) atomicAdd(&scnt[q], 1u);
-        if (prune::key32(__fadd_ru(x, bd)) >= tk) {
-          const int slot = atomicAdd(ccount + q0 + q, 1);
-          if (slot < kCap) {
-            cand[(int64_t)(q0 + q) * kCap + slot] = i;
-            cval[(int64_t)(q0 + q) * kCap + slot] = x;
-          }
+  };
+  fetch(((int64_t)blockIdx.x * kThreads + threadIdx.x) >> 5);
+  for (int64_t blk = ((int64_t)blockIdx.x * kThreads + threadIdx.x) >> 5; blk < blocks; blk += nw) {
+    const int64_t t0 = blk * RB;
+    const int64_t i0 = first_row(blk);
+    const int64_t lo = lo_n;
+    const int len_l = len_n;
+    const float cl = cl_n;
+    fetch(blk + nw);
+    if (i0 >= n) continue;  // warp-uniform: the last sampled tile's rows past n
+#pragma unroll 1
+    for (int jj = 0; jj < RB && i0 + jj < n; jj += R) {
+      const uint32_t* rp[R];
+      int len[R];
+      int maxlen = 0;
+#pragma unroll
+      for (int rr = 0; rr < R; ++rr) {
+        rp[rr] = pk + __shfl_sync(0xffffffffu, lo, jj + rr);
+        len[rr] = __shfl_sync(0xffffffffu, len_l, jj + rr);  // 0 for rows past n
+        maxlen = max(maxlen, len[rr]);
+      }
+      float acc[M];
+#pragma unroll
+      for (int m = 0; m < M; ++m) acc[m] = 0.f;
+      for (int off = lane; off < maxlen; off += 64) {  // two entries per row per lane in flight
+        uint32_t w0[R], w1[R];
+#pragma unroll
+        for (int rr = 0; rr < R; ++rr) {
+          w0[rr] = off < len[rr] ? __ldg(rp[rr] + off) : 0u;
+          w1[rr] = off + 32 < len[rr] ? __ldg(rp[rr] + off + 32) : 0u;
+        }
+#pragma unroll
+        for (int rr = 0; rr < R; ++rr) {
+          if (off < len[rr]) entry_fma<NB>(w0[rr], zh, *reinterpret_cast<float(*)[NB]>(acc + rr * NB));
+          if (off + 32 < len[rr]) entry_fma<NB>(w1[rr], zh, *reinterpret_cast<float(*)[NB]>(acc + rr * NB));
         }
       }
-    };
-    constexpr int kCT = 32 * kConsumers;  // consumer threads
-    const int ct = threadIdx.x;
-    const int myq = qidx<NB>(lane);
-    const bool leader = (lane & (kLpr / NB - 1)) == 0 && myq < nq;
-    int k = 0;
-    for (int64_t c = c_first; c < nch; c += step, ++k) {
-      const int s = k % kStages;
-      mbar_wait(&full[s], (k / kStages) & 1);
-      const int2 mt = meta[s];
-      const int32_t r0 = mt.x, nr = mt.y;
-      const uint32_t* sb = stage + (size_t)s * stw;
-      const int64_t* sip = (const int64_t*)(sb + sw) + (r0 & 1);  // sip[j] = indptr[r0 + j]
-      const float* scb = (const float*)(sb + sw + kIpWords) + (r0 & 3);
-      const int32_t slot0 = MODE == 0 ? soff[c / kSampleStride] : 0;
-      if (nr <= kRowsMax) {
-        // merge-style split: every consumer thread takes an equal run of the
-        // chunk's entries whatever the row lengths (C3's rows run from 1 to
-        // >2000 entries), sums them per row and adds the partial row sums
-        // into shared memory; then one thread per (row, query) finishes it
-        float* xk = xs + (k & 1) * kRowsMax * NB;  // double-buffered: the next chunk sums while this one finishes
-        const int64_t f = sip[0], m = sip[nr] - f;
-        const int64_t base = f & ~(int64_t)3;
-        const int64_t a = f + (m * ct) / kCT, b = f + (m * (ct + 1)) / kCT;
-        if (a < b) {
-          int lo = 0, hi = nr - 1;  // the row of entry a: largest j with sip[j] <= a
-          while (lo < hi) {
-            const int mid = (lo + hi + 1) >> 1;
-            if (sip[mid] <= a)
-              lo = mid;
-            else
-              hi = mid - 1;
-          }
-          int32_t j = lo;
-          int64_t next = sip[j + 1];
-          float acc[NB];
+      float c_my = 0.f;
 #pragma unroll
-          for (int q = 0; q < NB; ++q) acc[q] = 0.f;
-          auto flush = [&]() {
-#pragma unroll
-            for (int q = 0; q < NB; ++q)
-              if (acc[q] != 0.f) {
-                atomicAdd(&xk[j * NB + q], acc[q]);
-                acc[q] = 0.f;
-              }
-          };
-          for (int64_t e = a; e < b; e += 4) {
-            uint32_t w[4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) w[u] = e + u < b ? sb[e + u - base] : 0u;
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-              if (e + u < b) {
-                while (e + u >= next) {
-                  flush();
-                  ++j;
-                  next = sip[j + 1];
-                }
-                entry_fma<NB>(w[u], zh, acc);
-              }
+      for (int rr = 0; rr < R; ++rr) {
+        const float c = __shfl_sync(0xffffffffu, cl, jj + rr);
+        if (rr == my_r) c_my = c;
+      }
+      const float v = reduce_scatter<M>(acc, lane);
+      const int64_t i = i0 + jj + my_r;
+      if (leader && jj + my_r < RB && i < n) {
+        const float4 p = sp[my_q];
+        const float x = v * p.y;
+        if (MODE == 0) {
+          Ks[(int64_t)(q0 + my_q) * ns + t0 + jj + my_r] = prune::key32(__fsub_rd(x, prune::bound_of(c_my, p.w)));
+        } else if (x + p.z >= p.x) {  // rare: within reach of the threshold
+          const float bd = prune::bound_of(c_my, p.w);
+          const uint32_t tk = sthr[my_q];
+          if (prune::key32(__fsub_rd(x, bd)) >= tk) atomicAdd(&scnt[my_q], 1u);
+          if (prune::key32(__fadd_ru(x, bd)) >= tk) {
+            const int slot = atomicAdd(ccount + q0 + my_q, 1);
+            if (slot < kCap) {
+              cand[(int64_t)(q0 + my_q) * kCap + slot] = (int32_t)i;
+              cval[(int64_t)(q0 + my_q) * kCap + slot] = x;
             }
           }
-          flush();
-        }
-        asm volatile("bar.sync 1, %0;" ::"r"(kCT) : "memory");  // every partial sum of this chunk is in xk
-        for (int t = ct; t < nr * NB; t += kCT) {
-          const int32_t j = t / NB;
-          const int q = t - j * NB;
-          if (q < nq) row_out(r0 + j, j, q, xk[t], scb[j], slot0);
-          xk[t] = 0.f;
-        }
-      } else {
-        // a run of (mostly empty) rows longer than the staged slices: a lane
-        // group per row, indptr and c_i from global memory.  The barrier keeps
-        // the row-sum buffers' reuse ordered (the previous small chunk's
-        // finishing threads are done with theirs before the next small chunk)
-        asm volatile("bar.sync 1, %0;" ::"r"(kCT) : "memory");
-        const int64_t base = __ldg(indptr + r0) & ~(int64_t)3;
-        constexpr int kGroups = 32 / kLpr;  // rows per warp in flight
-        const int gl = lane & (kLpr - 1);
-        for (int32_t jb = warp * kGroups; jb < nr; jb += kConsumers * kGroups) {
-          const int32_t j = jb + lane / kLpr;  // this lane group's row (warp-uniform loop, ragged tail idles)
-          int64_t e0 = 0, e1 = 0;
-          if (j < nr) {
-            e0 = __ldg(indptr + r0 + j);
-            e1 = __ldg(indptr + r0 + j + 1);
-          }
-          float acc[NB];
-#pragma unroll
-          for (int q = 0; q < NB; ++q) acc[q] = 0.f;
-          for (int64_t e = e0 + gl; e < e1; e += kLpr) entry_fma<NB>(sb[e - base], zh, acc);
-          const float v = reduce_scatter<NB>(acc, lane);
-          if (leader && j < nr) row_out(r0 + j, j, myq, v, __ldg(cb + r0 + j), slot0);
         }
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[s]);  // this warp is done with stage s
     }
   }
   __syncthreads();
   if (MODE == 1 && threadIdx.x < nq && scnt[threadIdx.x]) atomicAdd(nlow + q0 + threadIdx.x, scnt[threadIdx.x]);
 }
 
-// largest NB in {8, 4, 2, 1} not above b whose shared memory fits; 0 if none does
+// queries per pass: FSR_K9S_NB (1/2/4/8) or the largest NB <= b, at most 8, whose Zh slice fits
 inline int pick_nb(int64_t b, int64_t r) {
+  static int forced = [] {
+    const char* e = getenv("FSR_K9S_NB");
+    const int v = e ? atoi(e) : 0;
+    return (v == 1 || v == 2 || v == 4 || v == 8) ? v : 0;
+  }();
   for (int nb = 8; nb >= 1; nb >>= 1)
-    if ((nb <= b || nb == 1) && smem_bytes(nb, r) <= 227 * 1024) return nb;
+    if ((forced ? nb <= forced : nb <= b || nb == 1) && smem_bytes(nb, r) <= 200 * 1024) return nb;
   return 0;
 }
 
 template <int MODE, int NB>
-int launch(fsr_ctx* ctx, const Layout& L, const Work& Wk, const int64_t* indptr, int64_t nnz, int64_t n, int64_t r,
-           int64_t b, int q0, int nq) {
+int launch(fsr_ctx* ctx, const Layout& L, const Work& Wk, const int64_t* indptr, int64_t n, int64_t r, int q0,
+           int nq) {
   const size_t smem = smem_bytes(NB, r);
   FSR_TRY(ensure_smem(ctx, stream_kernel<MODE, NB>, smem));
-  const int64_t nch = nchunks(nnz);
-  const int64_t work = MODE == 0 ? nsample(nnz) : nch;
-  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(work, ctx->num_sms));
-  stream_kernel<MODE, NB><<<grid, kThreads, smem, ctx->stream>>>(
-      L.pk, L.ipl, L.desc, nch, (int)r, (int)stage_words(r), Wk.Zh, ld_of(r), q0, nq, L.cb, Wk.qp, Wk.qpar, Wk.thr,
-      L.soff, Wk.Ks, n, Wk.cand, Wk.cval, Wk.ccount, Wk.nlow);
+  static int per_sm[2][9] = {};
+  int& occ = per_sm[MODE][NB];
+  if (!occ) {
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, stream_kernel<MODE, NB>, kThreads, smem) != cudaSuccess ||
+        occ < 1) {
+      cudaGetLastError();
+      occ = 1;
+    }
+  }
+  const int64_t ns = sample_slots(n);
+  const int64_t rows = MODE == 0 ? ns : n;
+  const int rows_per_cta = (MODE == 0 ? 8 : 32) * (kThreads / 32);
+  const int grid =
+      (int)std::max<int64_t>(1, std::min<int64_t>((rows + rows_per_cta - 1) / rows_per_cta, (int64_t)ctx->num_sms * occ));
+  stream_kernel<MODE, NB><<<grid, kThreads, smem, ctx->stream>>>(L.pk, indptr, n, (int)r, Wk.Zh, ld_of(r), q0, nq,
+                                                                 L.cb, Wk.qp, Wk.qpar, Wk.thr, Wk.Ks, ns, Wk.cand,
+                                                                 Wk.cval, Wk.ccount, Wk.nlow);
   return launched(ctx, MODE == 0 ? "k9s_stream_sample" : "k9s_stream_select");
 }
 
 template <int MODE>
-int launch_groups(fsr_ctx* ctx, const Layout& L, const Work& Wk, const int64_t* indptr, int64_t nnz, int64_t n,
-                  int64_t r, int64_t b) {
+int launch_groups(fsr_ctx* ctx, const Layout& L, const Work& Wk, const int64_t* indptr, int64_t n, int64_t r,
+                  int64_t b) {
   const int nb = pick_nb(b, r);
   for (int64_t q0 = 0; q0 < b; q0 += nb) {
     const int nq = (int)std::min<int64_t>(nb, b - q0);
     if (nb == 8)
-      FSR_TRY((launch<MODE, 8>(ctx, L, Wk, indptr, nnz, n, r, b, (int)q0, nq)));
+      FSR_TRY((launch<MODE, 8>(ctx, L, Wk, indptr, n, r, (int)q0, nq)));
     else if (nb == 4)
-      FSR_TRY((launch<MODE, 4>(ctx, L, Wk, indptr, nnz, n, r, b, (int)q0, nq)));
+      FSR_TRY((launch<MODE, 4>(ctx, L, Wk, indptr, n, r, (int)q0, nq)));
     else if (nb == 2)
-      FSR_TRY((launch<MODE, 2>(ctx, L, Wk, indptr, nnz, n, r, b, (int)q0, nq)));
+      FSR_TRY((launch<MODE, 2>(ctx, L, Wk, indptr, n, r, (int)q0, nq)));
     else
-      FSR_TRY((launch<MODE, 1>(ctx, L, Wk, indptr, nnz, n, r, b, (int)q0, nq)));
+      FSR_TRY((launch<MODE, 1>(ctx, L, Wk, indptr, n, r, (int)q0, nq)));
   }
   return FSR_OK;
 }
@@ -1381,9 +1305,15 @@ inline int finish_stage(fsr_ctx* ctx, const float* cb, const Work& Wk, int64_t n
     StageTimer timer(ctx, FSR_STAGE_TOPK);
     const size_t fsm = kFinishSmem;
     FSR_TRY(ensure_smem(ctx, k9t_finish_kernel, fsm));
+    if (Wk.cex) {
+      k9t_rescore_kernel<<<(unsigned)std::min<int64_t>((b * kCap * 8 + 255) / 256, (int64_t)ctx->num_sms * 8), 256,
+                           0, ctx->stream>>>(b, Wk.cand, Wk.ccount, u_indptr, u_indices, u_values, Wk.Zs, b, eta,
+                                             copy, y_ptr, y_idx, y_val, Wk.cex);
+      FSR_TRY(launched(ctx, "k9t_rescore_kernel"));
+    }
     k9t_finish_kernel<<<(unsigned)b, kFinishThreads, fsm, ctx->stream>>>(
         cb, Wk.qpar, Wk.thr, Wk.cand, Wk.cval, Wk.ccount, Wk.nlow, u_indptr, u_indices, u_values, Wk.Zs, b, eta,
-        copy, y_ptr, y_idx, y_val, topk, top_idx, top_val, Wk.nflag, Wk.nflag + 1, Wk.stats);
+        copy, y_ptr, y_idx, y_val, topk, top_idx, top_val, Wk.nflag, Wk.nflag + 1, Wk.stats, Wk.cex);
     FSR_TRY(launched(ctx, "k9t_finish_kernel"));
     const size_t esm = (size_t)kCap * 32;
     FSR_TRY(ensure_smem(ctx, k9t_empty_kernel, esm));
@@ -1497,17 +1427,9 @@ int fsr_stream_u_build(fsr_ctx* ctx, int64_t n, int64_t r, int64_t nnz, const in
   FSR_REQUIRE(ctx, aligned(out, 256), "stream_u_build: out must be 256-byte aligned");
   const Layout L = layout(out, n, nnz);
   FSR_CUDA(ctx, cudaMemsetAsync(out, 0, layout_bytes(n, nnz), ctx->stream));
-  FSR_CUDA(ctx, cudaMemcpyAsync(L.ipl, indptr, (size_t)(n + 1) * 8, cudaMemcpyDeviceToDevice, ctx->stream));
   pack_kernel<<<grid_for(n * 32, 256, ctx, 8), 256, 0, ctx->stream>>>(n, indptr, indices, values, L.pk, L.cb,
                                                                       L.cmax_bits);
-  FSR_TRY(launched(ctx, "stream_pack_kernel"));
-  const int64_t nch = nchunks(nnz);
-  chunk_rows_kernel<<<(unsigned)((nch + 256) / 256), 256, 0, ctx->stream>>>(n, indptr, nch, L.crow);
-  FSR_TRY(launched(ctx, "chunk_rows_kernel"));
-  chunk_desc_kernel<<<(unsigned)((nch + 256) / 256), 256, 0, ctx->stream>>>(indptr, nch, L.crow, L.desc);
-  FSR_TRY(launched(ctx, "chunk_desc_kernel"));
-  sample_offsets_kernel<<<1, 32, 0, ctx->stream>>>(nch, L.crow, L.soff);
-  return launched(ctx, "sample_offsets_kernel");
+  return launched(ctx, "stream_pack_kernel");
 }
 
 int fsr_filter_stream_applicable(int64_t n, int64_t r, int64_t nnz, int64_t b, int64_t topk) {
@@ -1517,7 +1439,7 @@ int fsr_filter_stream_applicable(int64_t n, int64_t r, int64_t nnz, int64_t b, i
 }
 
 int64_t fsr_filter_stream_workspace_bytes(int64_t n, int64_t r, int64_t b) {
-  return (int64_t)k9t::work_bytes(n, r, b, nullptr, nullptr, n);
+  return (int64_t)k9t::work_bytes(n, r, b, nullptr, nullptr, k9t::stream::sample_slots(n));
 }
 
 int fsr_filter_topk_stream(fsr_ctx* ctx, int64_t n, int64_t r, int64_t nnz, const int64_t* u_indptr,
@@ -1533,22 +1455,22 @@ int fsr_filter_topk_stream(fsr_ctx* ctx, int64_t n, int64_t r, int64_t nnz, cons
               "filter_topk_stream: buffers must be 256-aligned");
   const stream::Layout L = stream::layout(const_cast<void*>(stream_u), n, nnz);
   Work Wk;
-  work_bytes(n, r, b, &Wk, workspace, n);
+  work_bytes(n, r, b, &Wk, workspace, stream::sample_slots(n));
   const int copy = copy_uncovered && eta;
   FSR_TRY(k9t_project(ctx, r, b, u_indptr, u_indices, u_values, w, y_ptr, y_idx, y_val, Wk.Zt, Wk.Zs, Wk.Zh,
                       ld_of(r), Wk.qp, Wk.nflag));
   {
     StageTimer timer(ctx, FSR_STAGE_TOPK);
-    FSR_TRY(stream::launch_groups<0>(ctx, L, Wk, u_indptr, nnz, n, r, b));
+    FSR_TRY(stream::launch_groups<0>(ctx, L, Wk, u_indptr, n, r, b));
     const int64_t target = (2 * topk + stream::kSampleStride - 1) / stream::kSampleStride + 8;
     k9t_threshold_kernel<<<(unsigned)std::min<int64_t>(b, (int64_t)ctx->num_sms * 8), 256, 0, ctx->stream>>>(
-        b, n, 0, Wk.Ks, Wk.qp, L.cmax_bits, target, Wk.thr, Wk.qpar, Wk.ccount, Wk.nlow, Wk.nflag, Wk.nflag + 1,
-        L.soff + stream::nsample(nnz));
+        b, stream::sample_slots(n), stream::sample_valid(n), Wk.Ks, Wk.qp, L.cmax_bits, target, Wk.thr, Wk.qpar,
+        Wk.ccount, Wk.nlow, Wk.nflag, Wk.nflag + 1, nullptr);
     FSR_TRY(launched(ctx, "k9t_threshold_kernel"));
   }
   {
     StageTimer timer(ctx, FSR_STAGE_FILTER_SPMM);
-    FSR_TRY(stream::launch_groups<1>(ctx, L, Wk, u_indptr, nnz, n, r, b));
+    FSR_TRY(stream::launch_groups<1>(ctx, L, Wk, u_indptr, n, r, b));
   }
   return finish_stage(ctx, L.cb, Wk, n, b, u_indptr, u_indices, u_values, eta, copy, y_ptr, y_idx, y_val, topk,
                       top_idx, top_val);

@@ -292,7 +292,8 @@ def filter_device(dec: SpectralDecomposition, h: TransferFunction, queries: Devi
 
 ONLINE_PATHS = ("tc", "stream", "pruned", "exact")
 # below this batch the tensor-core step streams the whole dense U~ for too few
-# queries; the packed-U~ stream (K9s) is faster
+# queries; the exact sparse K9 is faster there -- and, at C3, also faster than
+# the packed-U~ stream K9s (opt-in: set_online_path("stream"))
 TC_MIN_BATCH = 128
 
 
@@ -300,7 +301,7 @@ def online_path(dec, b: int, topk: int, ctx=None) -> str:
     """Which kernels a ``filter_device`` call runs: "tc" (top-k only, fp32
     sparse U~: K9t, the certified tensor-core step of csrc/k9t.cu, b >= 128),
     "stream" (K9s: the same certification on a packed fp16 U~ streamed from
-    HBM, the small-batch path), "pruned" (the certified fp16-gather K9h of
+    HBM; only when preferred), "pruned" (the certified fp16-gather K9h of
     csrc/prune.cuh), or "exact" (unpruned K9 + exact top-k).  The certified
     paths return the top-k of the unpruned sequential-order fp32 path bit for
     bit (for b <= 64 the exact path's narrow kernels sum rows in another
@@ -315,8 +316,7 @@ def online_path(dec, b: int, topk: int, ctx=None) -> str:
     pref = ctx.online_path
     if pref == "tc" and b >= TC_MIN_BATCH and ctx.lib.fsr_filter_tc_applicable(dec.n, dec.r, b, int(topk)):
         return "tc"
-    if (pref == "stream" or (pref == "tc" and b < TC_MIN_BATCH)) and \
-            ctx.lib.fsr_filter_stream_applicable(dec.n, dec.r, dec.U_device.nnz, b, int(topk)):
+    if pref == "stream" and ctx.lib.fsr_filter_stream_applicable(dec.n, dec.r, dec.U_device.nnz, b, int(topk)):
         return "stream"
     if pref in ("tc", "pruned") and topk_pruned(dec.n, b, topk, dec.dtype):
         return "pruned"

@@ -575,8 +575,8 @@ def sparsify(dec: SpectralDecomposition, tau: int) -> SpectralDecomposition:
     values = torch.empty(cap, dtype=U.dtype, device=U.device)
     eta = torch.empty(n, dtype=torch.float64, device=U.device)
     nnz = ctypes.c_int64()
-    ctx.call("sparsify", dt, n, r, N.ptr(U), U.stride(0), tau, N.ptr(indptr), N.ptr(indices), N.ptr(values), cap,
-             N.ptr(eta), ctypes.byref(nnz))
+    ctx.call("sparsify_apply", dt, n, r, N.ptr(U), U.stride(0), T.value, ties.value, N.ptr(indptr), N.ptr(indices),
+             N.ptr(values), N.ptr(eta), ctypes.byref(nnz))
     k = int(nnz.value)
     Ut = DeviceCSR(indptr, indices[:k], values[:k], (n, r))
     return SpectralDecomposition(Ut, dec.eigenvalues, eta, dec.components, Variant.SPARSE,

@@ -259,15 +259,25 @@ def padded_unpruned(dec, qb, K, h=None):
 
 
 @pytest.mark.parametrize("b", [1, 2, 5, 8, 64, 100])
-def test_stream_small_batches_default_route(b):
-    """b < 128 on the default preference takes K9s (one NB-query group per
-    8 queries, ragged last group) and returns the sequential-order unpruned
-    top-k bit for bit; the FilterGraph replay of the same batch too."""
+def test_stream_small_batches(b):
+    """K9s (preferred) on small batches: one NB-query group per 8 queries,
+    ragged last group; the sequential-order unpruned top-k bit for bit, also
+    through a FilterGraph replay."""
     n, r = 140_003, 300
     _, dec = make_dec(n, r, 25, 61)
     qb = queries(n, b, 62, empty=(1,) if b > 4 else ())
     ctx = N.Context.get()
-    assert ctx.online_path == "tc" and ranking.online_path(dec, b, 100) == "stream"
+    assert ranking.online_path(dec, b, 100) == "exact"  # the default for b < TC_MIN_BATCH
+    ctx.set_online_path("stream")
+    try:
+        _stream_small_batch_checks(dec, qb, b)
+    finally:
+        ctx.set_online_path("tc")
+
+
+def _stream_small_batch_checks(dec, qb, b):
+    ctx = N.Context.get()
+    assert ranking.online_path(dec, b, 100) == "stream"
     dq = ranking.DeviceQueries(qb, dec.dtype, dec.eta_device.device)
     ws = torch.empty(ranking.filter_workspace_bytes(dec, b, want_x=False, topk=100), dtype=torch.uint8,
                      device=dec.eta_device.device)
