@@ -112,10 +112,12 @@ def _approx_sims(A, X, scheme, split=None):
     return mm(Ah, Xh) + mm(Ah, Xl) + mm(Al, Xh)
 
 
-def certified_topk(A, X, k: int, slack: int, exclude_offset=None, stats=None, split=None):
+def certified_topk(A, X, k: int, slack: int, exclude_offset=None, stats=None, split=None,
+                   schemes=("bf16", "bf16x3", "exact")):
     """Per row of A: the k best columns of A X^T by (clipped score desc,
     index asc) and their exact clipped scores (A's dtype), from certified
-    bf16 candidates (module doc).  Returns (indices, scores) (rows x k)."""
+    bf16 candidates (module doc).  Returns (indices, scores) (rows x k).
+    ``schemes``: the certification stages to try in order ("exact" last)."""
     import torch
 
     n, d = X.shape
@@ -126,7 +128,7 @@ def certified_topk(A, X, k: int, slack: int, exclude_offset=None, stats=None, sp
     out_c = torch.empty(A.shape[0], k, dtype=torch.int64, device=A.device)
     out_v = torch.empty(A.shape[0], k, dtype=A.dtype, device=A.device)
     todo = rows
-    for scheme in ("bf16", "bf16x3", "exact"):
+    for scheme in schemes:
         if todo.numel() == 0:
             break
         As = A[todo]
@@ -187,10 +189,19 @@ def mutual_knn_graph_device(X, k: int, gamma: float, block: int = 4096, slack: i
         block = min(block, 2048)  # fp32 candidate scores: block x n x 4 bytes
         hi = X.to(torch.bfloat16)
         split = (hi, (X - hi.to(X.dtype)).to(torch.bfloat16))
+    schemes = ["bf16", "bf16x3", "exact"]
     for s in range(0, n, block):
         e = min(n, s + block)
         if certified:
-            c, v = certified_topk(X[s:e], X, k, slack, exclude_offset=s, stats=stats, split=split)
+            st = {}
+            c, v = certified_topk(X[s:e], X, k, slack, exclude_offset=s, stats=st, split=split, schemes=schemes)
+            if schemes[0] == "bf16" and st.get("bf16", 0) < (e - s) // 2:
+                # the bf16 bound is too loose for these descriptors (e.g. d = 2048:
+                # e ~ 0.008 against score gaps ~1e-3): start at bf16x3 from now on
+                schemes = ["bf16x3", "exact"]
+            if stats is not None:
+                for key, v_ in st.items():
+                    stats[key] = stats.get(key, 0) + v_
         else:
             cand = _candidates(Xg[s:e], Xg, kk, exclude_offset=s)
             exact = _rescore(X[s:e], X, cand)
