@@ -887,7 +887,7 @@ struct Work {
   int2* stats;  // per query (candidates, rows re-scored): diagnostics
   float* Xt;
 };
-constexpr int64_t kPreScoreMaxB = 64;  // batches up to this size re-score all candidates on many CTAs
+constexpr int64_t kPreScoreMaxB = 64;  // batches up to this size re-score all candidates on many CTAs (b = 1024: 1.0 ms vs finish 0.46 ms)
 // ks_rows: sample keys per query (K9t: sample_rows(n); the streaming path: n)
 inline size_t work_bytes(int64_t n, int64_t r, int64_t b, Work* w, void* base, int64_t ks_rows) {
   char* p = (char*)base;
