@@ -65,9 +65,17 @@ constexpr int BN = 256;         // queries per tile (TMEM columns per accumulato
 constexpr int BK = 64;          // fp16 K elements per stage = 128 bytes = one SWIZZLE_128B row
 constexpr int STAGES = 4;
 constexpr int A_BYTES = BM * BK * 2;
-constexpr int B_BYTES = BN * BK * 2;
-constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256 + 2 * BN * 16 + 2 * BN * 4 + BN * 4;
+// per query-tile width TN (256 for b > 128; 128 / 64 for smaller batches, so
+// the MMA does not multiply padding queries): stage / shared-memory / TMEM sizes
+template <int TN>
+struct TileCfg {
+  static_assert(TN == 64 || TN == 128 || TN == 256, "query tile of 64, 128 or 256");
+  static constexpr int B_BYTES = TN * BK * 2;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256 + 2 * TN * 16 + 2 * TN * 4 + TN * 4;
+  static constexpr uint32_t TMEM_COLS = 2 * TN;  // double-buffered accumulators (a power of two >= 32)
+};
+constexpr int SMEM = TileCfg<BN>::SMEM;
 constexpr int kSampleStride = 32;  // threshold sample: every 32nd row tile
 constexpr int kCap = 4096;         // candidates per query (row << 12 | slot packs into int64)
 constexpr int kFinishThreads = 256;
@@ -176,13 +184,15 @@ struct QParam {
 // drops from A + B to A + B / CL (ncu at CL = 1: L2 throughput 72%, tensor
 // pipe 48% -- L2-fed).  A stage is refilled only after every member's MMAs
 // consumed it (the commits are multicast: empty barriers count CL arrivals).
-template <int MODE, int CL>
+template <int MODE, int CL, int TN>
 __global__ void __launch_bounds__(kThreads, 1)
     k9t_gemm_kernel(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUtensorMap mB, int n, int b,
                     int r, int tiles_n, int total, const float* __restrict__ cb, const float2* __restrict__ qp,
                     const QParam* __restrict__ qpar, const uint32_t* __restrict__ thr, uint32_t* __restrict__ Ks,
                     int64_t ns, int32_t* __restrict__ cand, float* __restrict__ cval, int32_t* __restrict__ ccount,
                     unsigned* __restrict__ nlow) {
+  using Cfg = TileCfg<TN>;
+  constexpr int STAGE_BYTES = Cfg::STAGE_BYTES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint64_t* full = (uint64_t*)(smem + STAGES * STAGE_BYTES);
@@ -190,16 +200,16 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* tfull = empty + STAGES;  // [2]
   uint64_t* tempty = tfull + 2;      // [2]
   uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
-  float4* spar = (float4*)(smem + STAGES * STAGE_BYTES + 256);  // [2][BN]
-  uint32_t* sthr = (uint32_t*)(spar + 2 * BN);                  // [2][BN]
-  unsigned* scnt = sthr + 2 * BN;                               // [BN]
+  float4* spar = (float4*)(smem + STAGES * STAGE_BYTES + 256);  // [2][TN]
+  uint32_t* sthr = (uint32_t*)(spar + 2 * TN);                  // [2][TN]
+  unsigned* scnt = sthr + 2 * TN;                               // [TN]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int iters = (r + BK - 1) / BK;
   const int rank = CL > 1 ? (int)cluster_rank() : 0;
   const int cluster = blockIdx.x / CL, nclusters = gridDim.x / CL;
   constexpr uint16_t kMask = (uint16_t)((1u << CL) - 1);
-  constexpr int PART_ROWS = BN / CL, PART_BYTES = PART_ROWS * BK * 2;
+  constexpr int PART_ROWS = TN / CL, PART_BYTES = PART_ROWS * BK * 2;
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
@@ -215,8 +225,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     tma_prefetch(&mA);
     tma_prefetch(&mB);
   }
-  if (warp == 1) tmem_alloc(tmem_slot, 512);
-  for (int t = threadIdx.x; t < BN; t += blockDim.x) scnt[t] = 0;
+  if (warp == 1) tmem_alloc(tmem_slot, Cfg::TMEM_COLS);
+  for (int t = threadIdx.x; t < TN; t += blockDim.x) scnt[t] = 0;
   tc_fence_before();
   if (CL > 1)
     cluster_sync();  // every member's barriers exist before any multicast lands
@@ -244,16 +254,16 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_expect_tx(&full[s], STAGE_BYTES);
           tma_load_2d(st, &mA, &full[s], it * BK, ti * BM);
           if (CL == 1)
-            tma_load_2d(st + A_BYTES, &mB, &full[s], it * BK, tj * BN);
+            tma_load_2d(st + A_BYTES, &mB, &full[s], it * BK, tj * TN);
           else
-            tma_load_2d_mc(st + A_BYTES + rank * PART_BYTES, &mB, &full[s], it * BK, tj * BN + rank * PART_ROWS,
+            tma_load_2d_mc(st + A_BYTES + rank * PART_BYTES, &mB, &full[s], it * BK, tj * TN + rank * PART_ROWS,
                            kMask);
         }
         __syncwarp();
       }
     }
   } else if (warp == 1) {
-    constexpr uint32_t idesc = idesc_f16(BM, BN);
+    constexpr uint32_t idesc = idesc_f16(BM, TN);
     int g = 0, tcount = 0;
     for (int idx = cluster; idx < total; idx += nclusters, ++tcount) {
       const int ab = tcount & 1, use = tcount >> 1;
@@ -261,7 +271,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(&tempty[ab], (use - 1) & 1);
         tc_fence_after();
       }
-      const uint32_t d = tmem + ab * BN;
+      const uint32_t d = tmem + ab * TN;
       for (int it = 0; it < iters; ++it, ++g) {
         const int s = g % STAGES;
         mbar_wait(&full[s], (g / STAGES) & 1);
@@ -289,9 +299,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       int ti, tj;
       tile_of(idx, ti, tj);
       const int ab = tcount & 1, use = tcount >> 1, pb = tcount & 1;
-      const int j0 = tj * BN;
+      const int j0 = tj * TN;
       // per-query parameters of this tile's columns
-      for (int t = et; t < BN; t += 128) {
+      for (int t = et; t < TN; t += 128) {
         const int q = j0 + t;
         float4 p = make_float4(__int_as_float(0x7fffffff), 1.f, 0.f, 0.f);
         uint32_t tk = 0xffffffffu;
@@ -305,8 +315,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             tk = thr[q];
           }
         }
-        spar[pb * BN + t] = p;
-        sthr[pb * BN + t] = tk;
+        spar[pb * TN + t] = p;
+        sthr[pb * TN + t] = tk;
       }
       const int row = ti * BM + 32 * q4 + lane;
       const bool row_ok = row < n;
@@ -314,9 +324,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(&tfull[ab], use & 1);
       tc_fence_after();
       epi_barrier();
-      const uint32_t tl = tmem + ((uint32_t)(32 * q4) << 16) + ab * BN;
+      const uint32_t tl = tmem + ((uint32_t)(32 * q4) << 16) + ab * TN;
 #pragma unroll 1
-      for (int cc = 0; cc < BN / 32; ++cc) {
+      for (int cc = 0; cc < TN / 32; ++cc) {
         float v[32];
         tmem_ld32(tl + cc * 32, v);
         if (!row_ok) continue;
@@ -326,7 +336,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int t = 0; t < 32; ++t) {
             const int jj = cc * 32 + t;
             if (j0 + jj < b) {
-              const float4 p = spar[pb * BN + jj];
+              const float4 p = spar[pb * TN + jj];
               const float x = v[t] * p.y;
               Ks[(int64_t)(j0 + jj) * ns + srow] = prune::key32(__fsub_rd(x, prune::bound_of(c, p.w)));
             }
@@ -335,11 +345,11 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int t = 0; t < 32; ++t) {
             const int jj = cc * 32 + t;
-            const float4 p = spar[pb * BN + jj];
+            const float4 p = spar[pb * TN + jj];
             const float x = v[t] * p.y;
             if (x + p.z >= p.x) {  // rare: within reach of the threshold
               const float bd = prune::bound_of(c, p.w);
-              const uint32_t tk = sthr[pb * BN + jj];
+              const uint32_t tk = sthr[pb * TN + jj];
               if (prune::key32(__fsub_rd(x, bd)) >= tk) atomicAdd(&scnt[jj], 1u);
               if (prune::key32(__fadd_ru(x, bd)) >= tk) {
                 const int slot = atomicAdd(ccount + j0 + jj, 1);
@@ -357,7 +367,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (lane == 0) mbar_arrive(&tempty[ab]);
       if (MODE == 1) {
         epi_barrier();
-        for (int t = et; t < BN; t += 128) {
+        for (int t = et; t < TN; t += 128) {
           const unsigned k = scnt[t];
           if (k) {
             atomicAdd(nlow + j0 + t, k);
@@ -373,7 +383,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc(tmem, 512);
+    tmem_dealloc(tmem, Cfg::TMEM_COLS);
   }
 }
 
@@ -822,13 +832,14 @@ inline int64_t sample_rows(int64_t n) {
 }
 
 // persistent grid: as many whole clusters as fit at once (1 CTA per SM)
-template <int CL>
+template <int CL, int TN>
 int cluster_grid(fsr_ctx* ctx) {
   static int cached[64] = {0};
   int& g = cached[ctx->device & 63];
+  constexpr int SMEM = TileCfg<TN>::SMEM;
   if (g) return g;
-  if (ensure_smem(ctx, k9t_gemm_kernel<1, CL>, SMEM) != FSR_OK) return -1;
-  if (ensure_smem(ctx, k9t_gemm_kernel<0, CL>, SMEM) != FSR_OK) return -1;
+  if (ensure_smem(ctx, k9t_gemm_kernel<1, CL, TN>, SMEM) != FSR_OK) return -1;
+  if (ensure_smem(ctx, k9t_gemm_kernel<0, CL, TN>, SMEM) != FSR_OK) return -1;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(ctx->num_sms / CL * CL));
   cfg.blockDim = dim3(kThreads);
@@ -841,7 +852,7 @@ int cluster_grid(fsr_ctx* ctx) {
   cfg.attrs = at;
   cfg.numAttrs = 1;
   int nclusters = 0;
-  if (cudaOccupancyMaxActiveClusters(&nclusters, k9t_gemm_kernel<1, CL>, &cfg) != cudaSuccess || nclusters < 1) {
+  if (cudaOccupancyMaxActiveClusters(&nclusters, k9t_gemm_kernel<1, CL, TN>, &cfg) != cudaSuccess || nclusters < 1) {
     cudaGetLastError();
     nclusters = ctx->num_sms / CL;
   }
@@ -849,10 +860,11 @@ int cluster_grid(fsr_ctx* ctx) {
   return g;
 }
 
-template <int MODE, int CL>
+template <int MODE, int CL, int TN>
 int launch_gemm(fsr_ctx* ctx, int grid, const CUtensorMap& mA, const CUtensorMap& mB, int n, int b, int r,
                 int tiles_n, int total, const float* cb, const float2* qp, const QParam* qpar, const uint32_t* thr,
                 uint32_t* Ks, int64_t ns, int32_t* cand, float* cval, int32_t* ccount, unsigned* nlow) {
+  constexpr int SMEM = TileCfg<TN>::SMEM;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)grid);
   cfg.blockDim = dim3(kThreads);
@@ -865,7 +877,7 @@ int launch_gemm(fsr_ctx* ctx, int grid, const CUtensorMap& mA, const CUtensorMap
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  FSR_CUDA(ctx, cudaLaunchKernelEx(&cfg, k9t_gemm_kernel<MODE, CL>, mA, mB, n, b, r, tiles_n, total, cb, qp, qpar,
+  FSR_CUDA(ctx, cudaLaunchKernelEx(&cfg, k9t_gemm_kernel<MODE, CL, TN>, mA, mB, n, b, r, tiles_n, total, cb, qp, qpar,
                                    thr, Ks, ns, cand, cval, ccount, nlow));
   return launched(ctx, MODE == 0 ? "k9t_gemm_sample" : "k9t_gemm_select");
 }
@@ -918,21 +930,21 @@ inline size_t work_bytes(int64_t n, int64_t r, int64_t b, Work* w, void* base, i
 }
 
 // sample GEMM -> threshold -> selecting GEMM, with CL-CTA clusters
-template <int CL>
+template <int CL, int TN>
 int tc_gemms(fsr_ctx* ctx, const DenseLayout& L, const Work& Wk, int64_t n, int64_t r, int64_t b, int64_t topk) {
   const int64_t ldr = ld_of(r);
   CUtensorMap mA, mB;
   FSR_TRY(make_map_f16(ctx, &mA, L.Ud, n, r, ldr, BM));
-  FSR_TRY(make_map_f16(ctx, &mB, Wk.Zh, b, r, ldr, BN / CL));
-  const int grid = cluster_grid<CL>(ctx);
+  FSR_TRY(make_map_f16(ctx, &mB, Wk.Zh, b, r, ldr, TN / CL));
+  const int grid = cluster_grid<CL, TN>(ctx);
   if (grid <= 0) return set_error(ctx, FSR_ECUDA, "filter_topk_tc: no co-resident %d-CTA clusters", CL);
-  const int tiles_m = (int)((n + BM - 1) / BM), tiles_n = (int)((b + BN - 1) / BN);
+  const int tiles_m = (int)((n + BM - 1) / BM), tiles_n = (int)((b + TN - 1) / TN);
   const int64_t ns = sample_rows(n);
   const int s_tiles = (tiles_m + kSampleStride - 1) / kSampleStride;
   {
     StageTimer timer(ctx, FSR_STAGE_TOPK);
     const int total0 = (s_tiles + CL - 1) / CL * tiles_n;  // work items per cluster
-    FSR_TRY((launch_gemm<0, CL>(ctx, grid, mA, mB, (int)n, (int)b, (int)r, tiles_n, total0, L.cb, Wk.qp, nullptr,
+    FSR_TRY((launch_gemm<0, CL, TN>(ctx, grid, mA, mB, (int)n, (int)b, (int)r, tiles_n, total0, L.cb, Wk.qp, nullptr,
                                nullptr, Wk.Ks, ns, nullptr, nullptr, nullptr, nullptr)));
     // rows of the last sampled tile beyond n hold no key: count only valid rows
     const int64_t last_tile = (int64_t)(s_tiles - 1) * kSampleStride;
@@ -946,7 +958,7 @@ int tc_gemms(fsr_ctx* ctx, const DenseLayout& L, const Work& Wk, int64_t n, int6
   {
     StageTimer timer(ctx, FSR_STAGE_FILTER_SPMM);
     const int total1 = (tiles_m + CL - 1) / CL * tiles_n;
-    FSR_TRY((launch_gemm<1, CL>(ctx, grid, mA, mB, (int)n, (int)b, (int)r, tiles_n, total1, L.cb, Wk.qp, Wk.qpar,
+    FSR_TRY((launch_gemm<1, CL, TN>(ctx, grid, mA, mB, (int)n, (int)b, (int)r, tiles_n, total1, L.cb, Wk.qp, Wk.qpar,
                                Wk.thr, nullptr, 0, Wk.cand, Wk.cval, Wk.ccount, Wk.nlow)));
   }
   return FSR_OK;
@@ -1386,12 +1398,18 @@ int fsr_filter_topk_tc(fsr_ctx* ctx, int64_t n, int64_t r, const int64_t* u_indp
   FSR_TRY(k9t_project(ctx, r, b, u_indptr, u_indices, u_values, w, y_ptr, y_idx, y_val, Wk.Zt, Wk.Zs, Wk.Zh, ldr,
                       Wk.qp, Wk.nflag));
   const int cl = cluster_choice();
-  if (cl == 1)
-    FSR_TRY(tc_gemms<1>(ctx, L, Wk, n, r, b, topk));
-  else if (cl == 2)
-    FSR_TRY(tc_gemms<2>(ctx, L, Wk, n, r, b, topk));
+  const int tn = b <= 64 ? 64 : b <= 128 ? 128 : 256;  // query tile: no MMA work on padding queries
+  if (tn == 64)
+    FSR_TRY((cl == 1 ? tc_gemms<1, 64>(ctx, L, Wk, n, r, b, topk) : cl == 2 ? tc_gemms<2, 64>(ctx, L, Wk, n, r, b, topk)
+                                                                          : tc_gemms<4, 64>(ctx, L, Wk, n, r, b, topk)));
+  else if (tn == 128)
+    FSR_TRY((cl == 1   ? tc_gemms<1, 128>(ctx, L, Wk, n, r, b, topk)
+             : cl == 2 ? tc_gemms<2, 128>(ctx, L, Wk, n, r, b, topk)
+                       : tc_gemms<4, 128>(ctx, L, Wk, n, r, b, topk)));
   else
-    FSR_TRY(tc_gemms<4>(ctx, L, Wk, n, r, b, topk));
+    FSR_TRY((cl == 1   ? tc_gemms<1, 256>(ctx, L, Wk, n, r, b, topk)
+             : cl == 2 ? tc_gemms<2, 256>(ctx, L, Wk, n, r, b, topk)
+                       : tc_gemms<4, 256>(ctx, L, Wk, n, r, b, topk)));
   return finish_stage(ctx, L.cb, Wk, n, b, u_indptr, u_indices, u_values, eta, copy, y_ptr, y_idx, y_val, topk,
                       top_idx, top_val);
 }

@@ -291,10 +291,11 @@ def filter_device(dec: SpectralDecomposition, h: TransferFunction, queries: Devi
 
 
 ONLINE_PATHS = ("tc", "stream", "pruned", "exact")
-# below this batch the tensor-core step streams the whole dense U~ for too few
-# queries; the exact sparse K9 is faster there -- and, at C3, also faster than
-# the packed-U~ stream K9s (opt-in: set_online_path("stream"))
-TC_MIN_BATCH = 128
+# below this batch the tensor-core step (64-query tiles for b <= 64) streams
+# the whole dense U~ for too few queries; the exact sparse K9 is faster there
+# -- and, at C3, also faster than the packed-U~ stream K9s (opt-in:
+# set_online_path("stream"))
+TC_MIN_BATCH = 64
 
 
 def online_path(dec, b: int, topk: int, ctx=None) -> str:
@@ -314,13 +315,23 @@ def online_path(dec, b: int, topk: int, ctx=None) -> str:
     if not topk or not dec.is_sparse or dec.dtype != torch.float32 or not ctx.topk_prune:
         return "exact"
     pref = ctx.online_path
-    if pref == "tc" and b >= TC_MIN_BATCH and ctx.lib.fsr_filter_tc_applicable(dec.n, dec.r, b, int(topk)):
+    if pref == "tc" and b >= TC_MIN_BATCH and tc_pays(dec, b) and \
+            ctx.lib.fsr_filter_tc_applicable(dec.n, dec.r, b, int(topk)):
         return "tc"
     if pref == "stream" and ctx.lib.fsr_filter_stream_applicable(dec.n, dec.r, dec.U_device.nnz, b, int(topk)):
         return "stream"
     if pref in ("tc", "pruned") and topk_pruned(dec.n, b, topk, dec.dtype):
         return "pruned"
     return "exact"
+
+
+def tc_pays(dec, b: int) -> bool:
+    """Cost model of K9t against the sparse K9 for a batch of b: the sparse
+    kernel gathers 4 b bytes of Zs from L2 per nonzero of U~ (~12 TB/s
+    measured), K9t streams the 2 n r byte dense fp16 U~ from HBM (~6.5 TB/s)
+    whatever tau is.  C3, b = 64 measured: 1% exact 1.48 vs K9t 1.90 ms; 2%
+    2.29 vs 1.96; 5% 4.8 vs 2.05 (the model's crossover: density 0.92 / b)."""
+    return 4.0 * dec.U_device.nnz * b / 12.0 >= 2.0 * dec.n * dec.r / 6.5
 
 
 def dense_layout(dec):

@@ -211,11 +211,13 @@ def test_two_devices_one_process():
     np.testing.assert_array_equal(res[0][1].view(np.uint32), res[1][1].view(np.uint32))
 
 
-@pytest.mark.parametrize("b", [1, 7, 64, 200])
+@pytest.mark.parametrize("b", [1, 7, 64, 100, 200])
 def test_tc_small_and_odd_batches(b, monkeypatch):
-    """K9t at batch widths below its default minimum (forced) and not a
-    multiple of the 256-query tile: same top-k as the unpruned path."""
+    """K9t at batch widths below its default minimum (forced), on each query
+    tile width (64: b <= 64, 128: b <= 128, else 256) and not a multiple of
+    it: same top-k as the unpruned path."""
     monkeypatch.setattr(ranking, "TC_MIN_BATCH", 1)
+    monkeypatch.setattr(ranking, "tc_pays", lambda dec, b: True)  # force K9t below its cost-model crossover
     n, r = 70_001, 257
     _, dec = make_dec(n, r, 25, 51)
     qb = queries(n, b, 52, empty=(0,) if b > 2 else ())
@@ -267,7 +269,8 @@ def test_stream_small_batches(b):
     _, dec = make_dec(n, r, 25, 61)
     qb = queries(n, b, 62, empty=(1,) if b > 4 else ())
     ctx = N.Context.get()
-    assert ranking.online_path(dec, b, 100) == "exact"  # the default for b < TC_MIN_BATCH
+    tc = b >= ranking.TC_MIN_BATCH and ranking.tc_pays(dec, b)
+    assert ranking.online_path(dec, b, 100) == ("tc" if tc else "exact")
     ctx.set_online_path("stream")
     try:
         _stream_small_batch_checks(dec, qb, b)
