@@ -67,6 +67,9 @@ _SIGS = {
     "fsr_filter_workspace_bytes": (_c_i64, [_c_int, _c_i64, _c_i64, _c_i64, _c_int]),
     "fsr_filter_batch": (_c_int, [_c_p, _c_int, _c_i64, _c_i64, _c_int, _c_p, _c_p, _c_p, _c_p, _c_i64, _c_p, _c_p,
                                   _c_i64, _c_p, _c_p, _c_p, _c_int, _c_p, _c_p, _c_i64, _c_p, _c_p]),
+    "fsr_u16_columns": (_c_int, [_c_p, _c_i64, _c_p, _c_p]),
+    "fsr_filter_batch_u16": (_c_int, [_c_p, _c_int, _c_i64, _c_i64, _c_int, _c_p, _c_p, _c_p, _c_p, _c_p, _c_i64, _c_p,
+                                      _c_p, _c_i64, _c_p, _c_p, _c_p, _c_int, _c_p, _c_p, _c_i64, _c_p, _c_p]),
     "fsr_dense_u_bytes": (_c_i64, [_c_i64, _c_i64]),
     "fsr_dense_u_build": (_c_int, [_c_p, _c_i64, _c_i64, _c_p, _c_p, _c_p, _c_p]),
     "fsr_filter_tc_workspace_bytes": (_c_i64, [_c_i64, _c_i64, _c_i64]),

@@ -212,6 +212,11 @@ __global__ void __launch_bounds__(256) project_smem_kernel(int64_t r, int64_t b,
   }
 }
 
+__global__ void u16_columns_kernel(int64_t nnz, const int32_t* __restrict__ indices, uint16_t* __restrict__ out) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < nnz; e += (int64_t)gridDim.x * blockDim.x)
+    out[e] = (uint16_t)indices[e];
+}
+
 template <typename T>
 __global__ void copy_uncovered_kernel(int64_t n, const int64_t* __restrict__ y_ptr, const int64_t* __restrict__ y_idx,
                                       const T* __restrict__ y_val, const double* __restrict__ eta, T* __restrict__ X,
@@ -347,7 +352,7 @@ template <typename T>
 int filter_impl(fsr_ctx* ctx, int64_t n, int64_t r, int u_sparse, const int64_t* u_indptr, const int32_t* u_indices,
                 const T* u_values, const T* u_dense, int64_t ldu, const T* w, const double* eta, int64_t b,
                 const int64_t* y_ptr, const int64_t* y_idx, const T* y_val, int copy_uncovered, void* workspace,
-                T* X, int64_t topk, int64_t* top_idx, T* top_val) {
+                T* X, int64_t topk, int64_t* top_idx, T* top_val, const uint16_t* u_cols16 = nullptr) {
   if constexpr (std::is_same<T, float>::value) {
     if (u_sparse && !X && topk > 0 && ctx->topk_prune && fsr::prune::applicable(n, b, topk) &&
         fsr::aligned(workspace, 256))
@@ -372,7 +377,9 @@ int filter_impl(fsr_ctx* ctx, int64_t n, int64_t r, int u_sparse, const int64_t*
   if (u_sparse) {
     if (b == 1) {
       fsr::StageTimer timer(ctx, FSR_STAGE_FILTER_SPMM);
-      if ((size_t)r * sizeof(T) <= 160 * 1024)
+      if (u_cols16 && (size_t)r * sizeof(T) <= 160 * 1024)
+        FSR_TRY((fsr::launch_spmv_smem<T, uint16_t>(ctx, n, u_indptr, u_cols16, u_values, Zs, r, Xout)));
+      else if ((size_t)r * sizeof(T) <= 160 * 1024)
         FSR_TRY(fsr::launch_spmv_smem<T>(ctx, n, u_indptr, u_indices, u_values, Zs, r, Xout));
       else
         FSR_TRY(fsr::launch_spmm<T>(ctx, n, u_indptr, u_indices, u_values, 1, Zs, 1, Xout, 1));
@@ -437,6 +444,23 @@ int fsr_filter_batch(fsr_ctx* ctx, int dtype, int64_t n, int64_t r, int u_sparse
                      const int32_t* u_indices, const void* u_values, const void* u_dense, int64_t ldu, const void* w,
                      const double* eta, int64_t b, const int64_t* y_ptr, const int64_t* y_idx, const void* y_val,
                      int copy_uncovered, void* workspace, void* X, int64_t topk, int64_t* top_idx, void* top_val) {
+  return fsr_filter_batch_u16(ctx, dtype, n, r, u_sparse, u_indptr, u_indices, nullptr, u_values, u_dense, ldu, w, eta,
+                              b, y_ptr, y_idx, y_val, copy_uncovered, workspace, X, topk, top_idx, top_val);
+}
+
+int fsr_u16_columns(fsr_ctx* ctx, int64_t nnz, const int32_t* indices, uint16_t* out) {
+  FSR_REQUIRE(ctx, nnz >= 0 && (nnz == 0 || (indices && out)), "u16_columns: bad args");
+  if (!nnz) return FSR_OK;
+  u16_columns_kernel<<<fsr::grid_for(nnz, 256, ctx, 8), 256, 0, ctx->stream>>>(nnz, indices, out);
+  return fsr::launched(ctx, "u16_columns_kernel");
+}
+
+int fsr_filter_batch_u16(fsr_ctx* ctx, int dtype, int64_t n, int64_t r, int u_sparse, const int64_t* u_indptr,
+                         const int32_t* u_indices, const uint16_t* u_cols16, const void* u_values, const void* u_dense,
+                         int64_t ldu, const void* w, const double* eta, int64_t b, const int64_t* y_ptr,
+                         const int64_t* y_idx, const void* y_val, int copy_uncovered, void* workspace, void* X,
+                         int64_t topk, int64_t* top_idx, void* top_val) {
+  FSR_REQUIRE(ctx, !u_cols16 || (u_sparse && r <= 65536), "filter_batch: 16-bit columns need a sparse U and r <= 65536");
   FSR_REQUIRE(ctx, n >= 1 && r >= 1 && b >= 1 && workspace, "filter_batch: bad shape");
   FSR_REQUIRE(ctx, u_sparse ? (u_indptr && u_indices && u_values) : (u_dense && ldu >= r),
               "filter_batch: missing U");
@@ -451,7 +475,7 @@ int fsr_filter_batch(fsr_ctx* ctx, int dtype, int64_t n, int64_t r, int u_sparse
                                (double*)top_val);
   return filter_impl<float>(ctx, n, r, u_sparse, u_indptr, u_indices, (const float*)u_values, (const float*)u_dense,
                             ldu, (const float*)w, eta, b, y_ptr, y_idx, (const float*)y_val, copy_uncovered, workspace,
-                            (float*)X, topk, top_idx, (float*)top_val);
+                            (float*)X, topk, top_idx, (float*)top_val, u_cols16);
 }
 
 int fsr_topk_rows(fsr_ctx* ctx, int dtype, int64_t b, int64_t n, const void* X, int64_t ldx, int64_t topk,

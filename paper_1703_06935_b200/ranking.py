@@ -280,14 +280,30 @@ def filter_device(dec: SpectralDecomposition, h: TransferFunction, queries: Devi
         workspace = torch.empty(need, dtype=torch.uint8, device=dev)
     ctx.last_online_path = "pruned" if path != "exact" and topk_pruned(n, b, topk, dt) else "exact"
     if dec.is_sparse:
-        uargs = (1, N.ptr(U.indptr), N.ptr(U.indices), N.ptr(U.values), N.ptr(None), 0)
+        # a single fp32 query streams U~ with 16-bit column indices (6 instead of 8 bytes per entry)
+        c16 = u16_columns(dec) if b == 1 and dt == torch.float32 and r <= 65536 else None
+        uargs = (1, N.ptr(U.indptr), N.ptr(U.indices), N.ptr(c16), N.ptr(U.values), N.ptr(None), 0)
     else:
-        uargs = (0, N.ptr(None), N.ptr(None), N.ptr(None), N.ptr(U), U.stride(0))
-    ctx.call("filter_batch", dtc, n, r, *uargs, N.ptr(w), N.ptr(dec.eta_device), b, N.ptr(queries.y_ptr),
+        uargs = (0, N.ptr(None), N.ptr(None), N.ptr(None), N.ptr(None), N.ptr(U), U.stride(0))
+    ctx.call("filter_batch_u16", dtc, n, r, *uargs, N.ptr(w), N.ptr(dec.eta_device), b, N.ptr(queries.y_ptr),
              N.ptr(queries.y_idx), N.ptr(queries.y_val), int(bool(copy_uncovered)), N.ptr(workspace),
              N.ptr(res.X if want_x else None), int(topk), N.ptr(res.top_idx if topk else None),
              N.ptr(res.top_val if topk else None))
     return res
+
+
+def u16_columns(dec):
+    """16-bit copy of U~'s column indices (r <= 65536), built once per
+    decomposition and cached on it (fsr_u16_columns)."""
+    import torch
+
+    cached = getattr(dec, "_cols16", None)
+    if cached is None:
+        U = dec.U_device
+        cached = torch.empty(max(1, U.nnz), dtype=torch.int16, device=U.indices.device)
+        N.Context.get(U.indices.device).call("u16_columns", U.nnz, N.ptr(U.indices), N.ptr(cached))
+        dec._cols16 = cached
+    return cached
 
 
 ONLINE_PATHS = ("tc", "stream", "pruned", "exact")
