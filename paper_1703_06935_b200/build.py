@@ -26,6 +26,11 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
               "-Xptxas", "-warn-spills", "-I" + INCLUDE]
 LINK = ["-lcublas", "-lcusolver"]
+# FSR_DEBUG_CHECKS=1: compile the device-side index / capacity assertions
+# (FSR_DCHECK in csrc/fsr_common.cuh) -- the bounds checks run in place of
+# compute-sanitizer, which this GPU pool does not allow.  Rebuild with --force.
+if os.environ.get("FSR_DEBUG_CHECKS") == "1":
+    NVCC_FLAGS = NVCC_FLAGS + ["-DFSR_DEBUG_CHECKS"]
 
 
 def nvcc() -> str:

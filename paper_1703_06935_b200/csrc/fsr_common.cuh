@@ -16,6 +16,16 @@
 
 #include "../../include/fsr.h"
 
+// Device-side bounds / capacity assertions, compiled only with
+// -DFSR_DEBUG_CHECKS (build.py, FSR_DEBUG_CHECKS=1): a violated check traps
+// the kernel and the next libfsr call reports the CUDA error.
+#ifdef FSR_DEBUG_CHECKS
+#include <cassert>
+#define FSR_DCHECK(cond) assert(cond)
+#else
+#define FSR_DCHECK(cond) ((void)0)
+#endif
+
 struct fsr_ctx {
   int device = 0;
   int num_sms = 148;

@@ -124,6 +124,7 @@ __global__ void __launch_bounds__(256) project_smem_kernel(int64_t r, int64_t b,
             else
               hi = mid - 1;
           }
+          FSR_DCHECK(lo >= 0 && lo < ny && offs[lo] <= t && t < offs[lo + 1]);
           const int64_t src = starts[lo] + (t - offs[lo]);
           cc[u] = u_indices[src];
           vv[u] = u_values[src];
@@ -143,6 +144,7 @@ __global__ void __launch_bounds__(256) project_smem_kernel(int64_t r, int64_t b,
       const T v = y_val[y0 + e];
       for (int64_t t = offs[e] + threadIdx.x; t < offs[e + 1]; t += blockDim.x) {
         const int32_t c = ec[t];
+        FSR_DCHECK(c >= 0 && c < r);
         z[c] = fsr::mul_add_rn(z[c], ev[t], v);
       }
       __syncthreads();

@@ -153,6 +153,7 @@ __global__ void __launch_bounds__(256) densify_kernel(int64_t n, int64_t ldr, co
     for (int64_t e = e0 + lane; e < e1; e += 32) {
       const float v = vals[e];
       ss = __fmaf_ru(v, v, ss);
+      FSR_DCHECK(indices[e] >= 0 && indices[e] < ldr);
       Ud[i * ldr + indices[e]] = __float2half_rn(v);
     }
 #pragma unroll
@@ -187,7 +188,8 @@ struct QParam {
 template <int MODE, int CL, int TN>
 __global__ void __launch_bounds__(kThreads, 1)
     k9t_gemm_kernel(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUtensorMap mB, int n, int b,
-                    int r, int tiles_n, int total, const float* __restrict__ cb, const float2* __restrict__ qp,
+                    int r, int tiles_n, int band, int total, const float* __restrict__ cb,
+                    const float2* __restrict__ qp,
                     const QParam* __restrict__ qpar, const uint32_t* __restrict__ thr, uint32_t* __restrict__ Ks,
                     int64_t ns, int32_t* __restrict__ cand, float* __restrict__ cval, int32_t* __restrict__ ccount,
                     unsigned* __restrict__ nlow) {
@@ -235,9 +237,18 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   // work item idx (per cluster) -> this CTA's (row tile, query tile)
+  // Raster: query tiles in bands of `band` (their fp16 Zh, band x TN x r x 2
+  // bytes, stays L2-resident), row tiles within a band, the band's query
+  // tiles fastest -- so the clusters in flight share row tiles of A (L2 hits)
+  // and a large batch does not re-read its whole Zh from DRAM per row tile
+  // (b = 10000: 40 query tiles, 100 MB of Zh).  band = tiles_n: one band.
+  const int row_groups = total / tiles_n;  // row-tile groups (of CL tiles) per query tile
   auto tile_of = [&](int idx, int& ti, int& tj) {
-    ti = (idx / tiles_n) * CL + rank;
-    tj = idx % tiles_n;
+    const int bnd = idx / (band * row_groups);
+    const int rem = idx - bnd * band * row_groups;
+    const int gw = min(band, tiles_n - bnd * band);  // the last band may be narrower
+    ti = (rem / gw) * CL + rank;
+    tj = bnd * band + rem % gw;
     if (MODE == 0) ti *= kSampleStride;
   };
 
@@ -352,6 +363,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               const uint32_t tk = sthr[pb * TN + jj];
               if (prune::key32(__fsub_rd(x, bd)) >= tk) atomicAdd(&scnt[jj], 1u);
               if (prune::key32(__fadd_ru(x, bd)) >= tk) {
+                FSR_DCHECK(j0 + jj < b && row < n);
                 const int slot = atomicAdd(ccount + j0 + jj, 1);
                 if (slot < kCap) {
                   cand[(int64_t)(j0 + jj) * kCap + slot] = row;
@@ -449,6 +461,7 @@ __global__ void __launch_bounds__(256) k9t_threshold_kernel(int64_t b, int64_t n
       }
       __syncthreads();
       topk::find_bin_t<256>(hist, nb, level == 0 ? target : target - above0, &found_bin, &above);
+      FSR_DCHECK(found_bin < (unsigned)nb);
       if (level == 0) above0 = above;
       prefix = (prefix << HB) | found_bin;
       __syncthreads();
@@ -547,6 +560,7 @@ __global__ void __launch_bounds__(256) k9t_rescore_kernel(
     const int slot = (int)(g - q * kCap);
     const int cnt = ccount[q];
     if (cnt < 0 || cnt > kCap || slot >= cnt) continue;  // group-uniform
+    FSR_DCHECK(cand[g] >= 0);
     const float v = exact_row_group<G>(cand[g], q, indptr, indices, vals, Zs, ldz, eta, copy, y_ptr, y_idx, y_val,
                                        gmask);
     if (gl == 0) pre[g] = v;
@@ -630,6 +644,7 @@ __global__ void __launch_bounds__(kFinishThreads) k9t_finish_kernel(
     __syncthreads();
   }
   const uint32_t lam = prefix << (32 - 2 * HB);
+  FSR_DCHECK(total <= kCap && cnt <= kCap);
   // keep upper >= lambda' (copied rows: exact, upper == lower)
   for (int t = threadIdx.x; t < total; t += blockDim.x) {
     const int32_t i = crow[t];
@@ -642,6 +657,7 @@ __global__ void __launch_bounds__(kFinishThreads) k9t_finish_kernel(
   }
   __syncthreads();
   const unsigned keep = n_keep;
+  FSR_DCHECK(keep >= (unsigned)K || keep > (unsigned)kKeep || total < K);
   if (threadIdx.x == 0) stats[q] = make_int2(total, (int)keep);
   if (keep > (unsigned)kKeep) {
     if (threadIdx.x == 0) flags[atomicAdd(nflag, 1)] = (int)q;
@@ -862,8 +878,9 @@ int cluster_grid(fsr_ctx* ctx) {
 
 template <int MODE, int CL, int TN>
 int launch_gemm(fsr_ctx* ctx, int grid, const CUtensorMap& mA, const CUtensorMap& mB, int n, int b, int r,
-                int tiles_n, int total, const float* cb, const float2* qp, const QParam* qpar, const uint32_t* thr,
-                uint32_t* Ks, int64_t ns, int32_t* cand, float* cval, int32_t* ccount, unsigned* nlow) {
+                int tiles_n, int band, int total, const float* cb, const float2* qp, const QParam* qpar,
+                const uint32_t* thr, uint32_t* Ks, int64_t ns, int32_t* cand, float* cval, int32_t* ccount,
+                unsigned* nlow) {
   constexpr int SMEM = TileCfg<TN>::SMEM;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)grid);
@@ -877,8 +894,8 @@ int launch_gemm(fsr_ctx* ctx, int grid, const CUtensorMap& mA, const CUtensorMap
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  FSR_CUDA(ctx, cudaLaunchKernelEx(&cfg, k9t_gemm_kernel<MODE, CL, TN>, mA, mB, n, b, r, tiles_n, total, cb, qp, qpar,
-                                   thr, Ks, ns, cand, cval, ccount, nlow));
+  FSR_CUDA(ctx, cudaLaunchKernelEx(&cfg, k9t_gemm_kernel<MODE, CL, TN>, mA, mB, n, b, r, tiles_n, band, total, cb, qp,
+                                   qpar, thr, Ks, ns, cand, cval, ccount, nlow));
   return launched(ctx, MODE == 0 ? "k9t_gemm_sample" : "k9t_gemm_select");
 }
 
@@ -939,13 +956,15 @@ int tc_gemms(fsr_ctx* ctx, const DenseLayout& L, const Work& Wk, int64_t n, int6
   const int grid = cluster_grid<CL, TN>(ctx);
   if (grid <= 0) return set_error(ctx, FSR_ECUDA, "filter_topk_tc: no co-resident %d-CTA clusters", CL);
   const int tiles_m = (int)((n + BM - 1) / BM), tiles_n = (int)((b + TN - 1) / TN);
+  // query tiles per raster band: their fp16 Zh within ~32 MB of L2
+  const int band = (int)std::max<int64_t>(1, std::min<int64_t>(tiles_n, (32ll << 20) / ((int64_t)TN * ldr * 2)));
   const int64_t ns = sample_rows(n);
   const int s_tiles = (tiles_m + kSampleStride - 1) / kSampleStride;
   {
     StageTimer timer(ctx, FSR_STAGE_TOPK);
     const int total0 = (s_tiles + CL - 1) / CL * tiles_n;  // work items per cluster
-    FSR_TRY((launch_gemm<0, CL, TN>(ctx, grid, mA, mB, (int)n, (int)b, (int)r, tiles_n, total0, L.cb, Wk.qp, nullptr,
-                               nullptr, Wk.Ks, ns, nullptr, nullptr, nullptr, nullptr)));
+    FSR_TRY((launch_gemm<0, CL, TN>(ctx, grid, mA, mB, (int)n, (int)b, (int)r, tiles_n, band, total0, L.cb, Wk.qp,
+                                    nullptr, nullptr, Wk.Ks, ns, nullptr, nullptr, nullptr, nullptr)));
     // rows of the last sampled tile beyond n hold no key: count only valid rows
     const int64_t last_tile = (int64_t)(s_tiles - 1) * kSampleStride;
     const int64_t n_valid_s = (int64_t)(s_tiles - 1) * BM + std::min<int64_t>(BM, n - last_tile * BM);
@@ -958,8 +977,8 @@ int tc_gemms(fsr_ctx* ctx, const DenseLayout& L, const Work& Wk, int64_t n, int6
   {
     StageTimer timer(ctx, FSR_STAGE_FILTER_SPMM);
     const int total1 = (tiles_m + CL - 1) / CL * tiles_n;
-    FSR_TRY((launch_gemm<1, CL, TN>(ctx, grid, mA, mB, (int)n, (int)b, (int)r, tiles_n, total1, L.cb, Wk.qp, Wk.qpar,
-                               Wk.thr, nullptr, 0, Wk.cand, Wk.cval, Wk.ccount, Wk.nlow)));
+    FSR_TRY((launch_gemm<1, CL, TN>(ctx, grid, mA, mB, (int)n, (int)b, (int)r, tiles_n, band, total1, L.cb, Wk.qp,
+                                    Wk.qpar, Wk.thr, nullptr, 0, Wk.cand, Wk.cval, Wk.ccount, Wk.nlow)));
   }
   return FSR_OK;
 }
@@ -1213,6 +1232,8 @@ __global__ void __launch_bounds__(kThreads)
         }
 #pragma unroll
         for (int rr = 0; rr < R; ++rr) {
+          FSR_DCHECK(!(off < len[rr]) || (int)(w0[rr] & 0xffffu) < r);
+          FSR_DCHECK(!(off + 32 < len[rr]) || (int)(w1[rr] & 0xffffu) < r);
           if (off < len[rr]) entry_fma<NB>(w0[rr], zh, *reinterpret_cast<float(*)[NB]>(acc + rr * NB));
           if (off + 32 < len[rr]) entry_fma<NB>(w1[rr], zh, *reinterpret_cast<float(*)[NB]>(acc + rr * NB));
         }
@@ -1229,6 +1250,7 @@ __global__ void __launch_bounds__(kThreads)
         const float4 p = sp[my_q];
         const float x = v * p.y;
         if (MODE == 0) {
+          FSR_DCHECK(t0 + jj + my_r < ns);
           Ks[(int64_t)(q0 + my_q) * ns + t0 + jj + my_r] = prune::key32(__fsub_rd(x, prune::bound_of(c_my, p.w)));
         } else if (x + p.z >= p.x) {  // rare: within reach of the threshold
           const float bd = prune::bound_of(c_my, p.w);

@@ -468,6 +468,7 @@ __global__ void __launch_bounds__(256) spmv_smem_kernel(int64_t n_rows, const in
       for (int u = 0; u < 4; ++u) {
         const int64_t e = base + 32 * u;
         c[u] = e < e1 ? (int)__ldg(indices + e) : -1;
+        FSR_DCHECK(c[u] < x_len);
         a[u] = e < e1 ? __ldg(vals + e) : T(0);
       }
 #pragma unroll
