@@ -543,7 +543,12 @@ __global__ void __launch_bounds__(256) k9t_rescore_kernel(
     float* __restrict__ pre);
 
 constexpr int kKeep = 1024;  // rows re-scored exactly per query (upper >= lambda_K); more -> fallback
-constexpr size_t kFinishSmem = (size_t)kCap * 12 + (size_t)(1 << topk::kHistBits) * 4 + (size_t)kKeep * 16;
+// Candidates a finish CTA holds in shared memory.  Half the list capacity:
+// 56 KB of shared memory per CTA instead of 80 KB, 4 CTAs per SM instead of 2
+// (the finish is latency-bound on its re-score chains).  C3: at most 1365
+// candidates per query; a query with more takes the exact fallback.
+constexpr int kFinishCap = 2048;
+constexpr size_t kFinishSmem = (size_t)kFinishCap * 12 + (size_t)(1 << topk::kHistBits) * 4 + (size_t)kKeep * 16;
 
 __global__ void __launch_bounds__(256) k9t_rescore_kernel(
     int64_t b, const int32_t* __restrict__ cand, const int32_t* __restrict__ ccount,
@@ -579,16 +584,16 @@ __global__ void __launch_bounds__(kFinishThreads) k9t_finish_kernel(
   extern __shared__ __align__(16) unsigned char dyn[];
   uint64_t* kkey = (uint64_t*)dyn;             // [kKeep] exact order keys of the kept rows
   int64_t* kidx = (int64_t*)(kkey + kKeep);    // [kKeep] row << 12 | slot
-  uint32_t* lkey = (uint32_t*)(kidx + kKeep);  // [kCap] lower-bound keys by slot
-  int32_t* crow = (int32_t*)(lkey + kCap);     // [kCap] rows by slot
-  float* cv = (float*)(crow + kCap);           // [kCap] x~, then exact scores, by slot
-  unsigned* hist = (unsigned*)(cv + kCap);     // [NB]
+  uint32_t* lkey = (uint32_t*)(kidx + kKeep);  // [kFinishCap] lower-bound keys by slot
+  int32_t* crow = (int32_t*)(lkey + kFinishCap);     // [kFinishCap] rows by slot
+  float* cv = (float*)(crow + kFinishCap);           // [kFinishCap] x~, then exact scores, by slot
+  unsigned* hist = (unsigned*)(cv + kFinishCap);     // [NB]
   __shared__ unsigned n_extra, n_extra_ge, n_keep, n_next, found_bin;
   __shared__ unsigned long long above;
   const int64_t q = blockIdx.x;
   const int cnt0 = ccount[q];
   if (cnt0 < 0) return;  // flagged (fallback) or empty observation (k9t_empty)
-  const int cnt = min(cnt0, kCap);
+  const int cnt = min(cnt0, kFinishCap);
   const uint32_t tk = thr[q];
   const float zb = qpar[q].zb;
   if (threadIdx.x == 0) n_extra = n_extra_ge = n_keep = 0;
@@ -610,7 +615,7 @@ __global__ void __launch_bounds__(kFinishThreads) k9t_finish_kernel(
       const unsigned s = atomicAdd(&n_extra, 1u);
       if (prune::key32(v) >= tk) atomicAdd(&n_extra_ge, 1u);
       const int slot = cnt + (int)s;
-      if (slot < kCap) {
+      if (slot < kFinishCap) {
         crow[slot] = (int32_t)i;
         cv[slot] = v;
         lkey[slot] = prune::key32(v);
@@ -619,7 +624,8 @@ __global__ void __launch_bounds__(kFinishThreads) k9t_finish_kernel(
   }
   __syncthreads();
   const int total = cnt + (int)n_extra;
-  if (cnt0 > kCap || total > kCap || (unsigned long long)nlow[q] + n_extra_ge < (unsigned long long)K) {
+  if (cnt0 > kFinishCap || total > kFinishCap ||
+      (unsigned long long)nlow[q] + n_extra_ge < (unsigned long long)K) {
     if (threadIdx.x == 0) flags[atomicAdd(nflag, 1)] = (int)q;  // overflow, or the sampled t was too high
     return;
   }
@@ -644,7 +650,7 @@ __global__ void __launch_bounds__(kFinishThreads) k9t_finish_kernel(
     __syncthreads();
   }
   const uint32_t lam = prefix << (32 - 2 * HB);
-  FSR_DCHECK(total <= kCap && cnt <= kCap);
+  FSR_DCHECK(total <= kFinishCap && cnt <= kFinishCap);
   // keep upper >= lambda' (copied rows: exact, upper == lower)
   for (int t = threadIdx.x; t < total; t += blockDim.x) {
     const int32_t i = crow[t];
