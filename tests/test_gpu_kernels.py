@@ -338,3 +338,36 @@ def test_filter_b1_spmv_skewed_rows(dtype, tol):
         assert err <= tol, (yi, err)
         rows = np.flatnonzero(np.diff(host.U.indptr) == 0)
         np.testing.assert_array_equal(x[rows[~np.isin(rows, yi)]], 0.0)
+
+
+def test_single_query_u16_columns_bitwise():
+    """b = 1 fp32 filtering reads 16-bit column indices (fsr_filter_batch_u16):
+    the same scores, bit for bit, as the int32-column kernel."""
+    from paper_1703_06935_b200 import ranking
+
+    rng = np.random.default_rng(23)
+    n, r = 50_000, 700
+    lens = rng.integers(0, 60, size=n)
+    indptr = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    cols = np.concatenate([np.sort(rng.choice(r, size=k, replace=False)) for k in lens]).astype(np.int32)
+    U = sp.csr_matrix((rng.standard_normal(indptr[-1]), cols, indptr), shape=(n, r))
+    from types import SimpleNamespace
+
+    eta = np.sqrt(np.asarray(U.multiply(U).sum(axis=1)).ravel())
+    host = SimpleNamespace(U=U, eigenvalues=np.sort(rng.uniform(-0.3, 1, r))[::-1].copy(), eta=eta,
+                           variant="sparse", provenance=None, components=None)
+    dec = spectral.SpectralDecomposition.from_host(host, dtype="float32")
+    y = ranking.ObservationVector(n, np.array([3, 999, 40_000]), np.array([1.0, 0.5, 0.2]), cap=3)
+    q = ranking.DeviceQueries(ranking.QueryBatch.from_vectors([y]), dec.dtype, dec.eta_device.device)
+    h = ranking.h_alpha(0.99)
+    x16 = ranking.filter_device(dec, h, q).X.clone()  # the Python path: 16-bit columns for b = 1
+    ctx = N.Context.get()
+    Ud = dec.U_device
+    w = ranking._weights_device(dec, h)
+    ws = torch.empty(int(ctx.lib.fsr_filter_workspace_bytes(N.F32, n, r, 1, 1)), dtype=torch.uint8, device="cuda")
+    x32 = torch.empty(1, n, dtype=torch.float32, device="cuda")
+    ctx.call("filter_batch", N.F32, n, r, 1, N.ptr(Ud.indptr), N.ptr(Ud.indices), N.ptr(Ud.values), N.ptr(None), 0,
+             N.ptr(w), N.ptr(dec.eta_device), 1, N.ptr(q.y_ptr), N.ptr(q.y_idx), N.ptr(q.y_val), 1, N.ptr(ws),
+             N.ptr(x32), 0, N.ptr(None), N.ptr(None))
+    torch.cuda.synchronize()
+    assert torch.equal(x16.view(torch.int32), x32.view(torch.int32))
