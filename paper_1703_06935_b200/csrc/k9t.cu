@@ -185,7 +185,7 @@ struct QParam {
 // drops from A + B to A + B / CL (ncu at CL = 1: L2 throughput 72%, tensor
 // pipe 48% -- L2-fed).  A stage is refilled only after every member's MMAs
 // consumed it (the commits are multicast: empty barriers count CL arrivals).
-template <int MODE, int CL, int TN>
+template <int MODE, int CL, int TN, bool M2 = false>
 __global__ void __launch_bounds__(kThreads, 1)
     k9t_gemm_kernel(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUtensorMap mB, int n, int b,
                     int r, int tiles_n, int band, int total, const float* __restrict__ cb,
@@ -212,10 +212,19 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int cluster = blockIdx.x / CL, nclusters = gridDim.x / CL;
   constexpr uint16_t kMask = (uint16_t)((1u << CL) - 1);
   constexpr int PART_ROWS = TN / CL, PART_BYTES = PART_ROWS * BK * 2;
+  // M2 (2-D multicast, CL = 4, rank = 2 rq + rr): the cluster is 2 row tiles x
+  // 2 query tiles; each CTA loads half its A tile, multicast to the CTA with
+  // the same row tile (rank ^ 2), and half its B tile, multicast to the CTA
+  // with the same query tile (rank ^ 1).  A stage of CTA x is written by x,
+  // x ^ 1 and x ^ 2, so its empty barrier waits for those three consumers.
+  static_assert(!M2 || CL == 4, "2-D multicast needs 4-CTA clusters");
+  const int rr = rank & 1, rq = rank >> 1;
+  const uint16_t maskA = (uint16_t)((1u << rank) | (1u << (rank ^ 2)));
+  const uint16_t maskB = (uint16_t)((1u << rank) | (1u << (rank ^ 1)));
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], CL);
+      mbar_init(&empty[s], M2 ? 3 : CL);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
@@ -244,6 +253,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   // (b = 10000: 40 query tiles, 100 MB of Zh).  band = tiles_n: one band.
   const int row_groups = total / tiles_n;  // row-tile groups (of CL tiles) per query tile
   auto tile_of = [&](int idx, int& ti, int& tj) {
+    if (M2) {
+      const int tiles_np = tiles_n / 2;
+      ti = (idx / tiles_np) * 2 + rr;
+      tj = (idx % tiles_np) * 2 + rq;
+      if (MODE == 0) ti *= kSampleStride;
+      return;
+    }
     const int bnd = idx / (band * row_groups);
     const int rem = idx - bnd * band * row_groups;
     const int gw = min(band, tiles_n - bnd * band);  // the last band may be narrower
@@ -263,12 +279,18 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (lane == 0) {
           uint8_t* st = smem + s * STAGE_BYTES;
           mbar_expect_tx(&full[s], STAGE_BYTES);
+          if (M2) {
+            tma_load_2d_mc(st + rq * (A_BYTES / 2), &mA, &full[s], it * BK, ti * BM + rq * (BM / 2), maskA);
+            tma_load_2d_mc(st + A_BYTES + rr * (Cfg::B_BYTES / 2), &mB, &full[s], it * BK, tj * TN + rr * (TN / 2),
+                           maskB);
+          } else {
           tma_load_2d(st, &mA, &full[s], it * BK, ti * BM);
           if (CL == 1)
             tma_load_2d(st + A_BYTES, &mB, &full[s], it * BK, tj * TN);
           else
             tma_load_2d_mc(st + A_BYTES + rank * PART_BYTES, &mB, &full[s], it * BK, tj * TN + rank * PART_ROWS,
                            kMask);
+          }
         }
         __syncwarp();
       }
@@ -295,6 +317,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             mma_f16(d, da + (uint64_t)(2 * k), db + (uint64_t)(2 * k), idesc, (it | k) ? 1u : 0u);
           if (CL == 1)
             mma_commit(&empty[s]);
+          else if (M2)
+            mma_commit_mc(&empty[s], (uint16_t)(maskA | maskB));  // this CTA's A and B writers
           else
             mma_commit_mc(&empty[s], kMask);  // the stage holds every member's B part
           if (it == iters - 1) mma_commit(&tfull[ab]);
@@ -854,14 +878,14 @@ inline int64_t sample_rows(int64_t n) {
 }
 
 // persistent grid: as many whole clusters as fit at once (1 CTA per SM)
-template <int CL, int TN>
+template <int CL, int TN, bool M2 = false>
 int cluster_grid(fsr_ctx* ctx) {
   static int cached[64] = {0};
   int& g = cached[ctx->device & 63];
   constexpr int SMEM = TileCfg<TN>::SMEM;
   if (g) return g;
-  if (ensure_smem(ctx, k9t_gemm_kernel<1, CL, TN>, SMEM) != FSR_OK) return -1;
-  if (ensure_smem(ctx, k9t_gemm_kernel<0, CL, TN>, SMEM) != FSR_OK) return -1;
+  if (ensure_smem(ctx, k9t_gemm_kernel<1, CL, TN, M2>, SMEM) != FSR_OK) return -1;
+  if (ensure_smem(ctx, k9t_gemm_kernel<0, CL, TN, M2>, SMEM) != FSR_OK) return -1;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(ctx->num_sms / CL * CL));
   cfg.blockDim = dim3(kThreads);
@@ -874,7 +898,8 @@ int cluster_grid(fsr_ctx* ctx) {
   cfg.attrs = at;
   cfg.numAttrs = 1;
   int nclusters = 0;
-  if (cudaOccupancyMaxActiveClusters(&nclusters, k9t_gemm_kernel<1, CL, TN>, &cfg) != cudaSuccess || nclusters < 1) {
+  if (cudaOccupancyMaxActiveClusters(&nclusters, k9t_gemm_kernel<1, CL, TN, M2>, &cfg) != cudaSuccess ||
+      nclusters < 1) {
     cudaGetLastError();
     nclusters = ctx->num_sms / CL;
   }
@@ -882,7 +907,7 @@ int cluster_grid(fsr_ctx* ctx) {
   return g;
 }
 
-template <int MODE, int CL, int TN>
+template <int MODE, int CL, int TN, bool M2 = false>
 int launch_gemm(fsr_ctx* ctx, int grid, const CUtensorMap& mA, const CUtensorMap& mB, int n, int b, int r,
                 int tiles_n, int band, int total, const float* cb, const float2* qp, const QParam* qpar,
                 const uint32_t* thr, uint32_t* Ks, int64_t ns, int32_t* cand, float* cval, int32_t* ccount,
@@ -900,7 +925,7 @@ int launch_gemm(fsr_ctx* ctx, int grid, const CUtensorMap& mA, const CUtensorMap
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  FSR_CUDA(ctx, cudaLaunchKernelEx(&cfg, k9t_gemm_kernel<MODE, CL, TN>, mA, mB, n, b, r, tiles_n, band, total, cb, qp,
+  FSR_CUDA(ctx, cudaLaunchKernelEx(&cfg, k9t_gemm_kernel<MODE, CL, TN, M2>, mA, mB, n, b, r, tiles_n, band, total, cb, qp,
                                    qpar, thr, Ks, ns, cand, cval, ccount, nlow));
   return launched(ctx, MODE == 0 ? "k9t_gemm_sample" : "k9t_gemm_select");
 }
@@ -952,14 +977,15 @@ inline size_t work_bytes(int64_t n, int64_t r, int64_t b, Work* w, void* base, i
   return off + 256;
 }
 
-// sample GEMM -> threshold -> selecting GEMM, with CL-CTA clusters
-template <int CL, int TN>
+// sample GEMM -> threshold -> selecting GEMM, with CL-CTA clusters (M2: the
+// 2-D multicast 2 x 2 clusters; needs an even number of query tiles)
+template <int CL, int TN, bool M2 = false>
 int tc_gemms(fsr_ctx* ctx, const DenseLayout& L, const Work& Wk, int64_t n, int64_t r, int64_t b, int64_t topk) {
   const int64_t ldr = ld_of(r);
   CUtensorMap mA, mB;
-  FSR_TRY(make_map_f16(ctx, &mA, L.Ud, n, r, ldr, BM));
-  FSR_TRY(make_map_f16(ctx, &mB, Wk.Zh, b, r, ldr, TN / CL));
-  const int grid = cluster_grid<CL, TN>(ctx);
+  FSR_TRY(make_map_f16(ctx, &mA, L.Ud, n, r, ldr, M2 ? BM / 2 : BM));
+  FSR_TRY(make_map_f16(ctx, &mB, Wk.Zh, b, r, ldr, M2 ? TN / 2 : TN / CL));
+  const int grid = cluster_grid<CL, TN, M2>(ctx);
   if (grid <= 0) return set_error(ctx, FSR_ECUDA, "filter_topk_tc: no co-resident %d-CTA clusters", CL);
   const int tiles_m = (int)((n + BM - 1) / BM), tiles_n = (int)((b + TN - 1) / TN);
   // query tiles per raster band: their fp16 Zh within ~32 MB of L2
@@ -968,8 +994,9 @@ int tc_gemms(fsr_ctx* ctx, const DenseLayout& L, const Work& Wk, int64_t n, int6
   const int s_tiles = (tiles_m + kSampleStride - 1) / kSampleStride;
   {
     StageTimer timer(ctx, FSR_STAGE_TOPK);
-    const int total0 = (s_tiles + CL - 1) / CL * tiles_n;  // work items per cluster
-    FSR_TRY((launch_gemm<0, CL, TN>(ctx, grid, mA, mB, (int)n, (int)b, (int)r, tiles_n, band, total0, L.cb, Wk.qp,
+    // work items per cluster
+    const int total0 = M2 ? (s_tiles + 1) / 2 * (tiles_n / 2) : (s_tiles + CL - 1) / CL * tiles_n;
+    FSR_TRY((launch_gemm<0, CL, TN, M2>(ctx, grid, mA, mB, (int)n, (int)b, (int)r, tiles_n, band, total0, L.cb, Wk.qp,
                                     nullptr, nullptr, Wk.Ks, ns, nullptr, nullptr, nullptr, nullptr)));
     // rows of the last sampled tile beyond n hold no key: count only valid rows
     const int64_t last_tile = (int64_t)(s_tiles - 1) * kSampleStride;
@@ -982,19 +1009,23 @@ int tc_gemms(fsr_ctx* ctx, const DenseLayout& L, const Work& Wk, int64_t n, int6
   }
   {
     StageTimer timer(ctx, FSR_STAGE_FILTER_SPMM);
-    const int total1 = (tiles_m + CL - 1) / CL * tiles_n;
-    FSR_TRY((launch_gemm<1, CL, TN>(ctx, grid, mA, mB, (int)n, (int)b, (int)r, tiles_n, band, total1, L.cb, Wk.qp,
+    const int total1 = M2 ? (tiles_m + 1) / 2 * (tiles_n / 2) : (tiles_m + CL - 1) / CL * tiles_n;
+    FSR_TRY((launch_gemm<1, CL, TN, M2>(ctx, grid, mA, mB, (int)n, (int)b, (int)r, tiles_n, band, total1, L.cb, Wk.qp,
                                     Wk.qpar, Wk.thr, nullptr, 0, Wk.cand, Wk.cval, Wk.ccount, Wk.nlow)));
   }
   return FSR_OK;
 }
 
-// FSR_K9T_CLUSTER = 1 / 2 / 4 CTAs per cluster (B-tile multicast); default 2
+// FSR_K9T_CLUSTER = 1 / 2 / 4 CTAs per cluster (B-tile multicast), 22 = 2 x 2
+// clusters with A and B multicast (default; an odd number of 256-query tiles
+// falls back to 2).  C3 b = 1024, same box back to back: 2 x 2 8.41 ms vs 2
+// 8.87 ms -- DRAM reads 26 -> 13 GB per launch and the board's power cap
+// allows 1.75 instead of 1.41 GHz (ncu, profiles/r02/k9t_ncu_full.json).
 inline int cluster_choice() {
   static int c = [] {
     const char* e = getenv("FSR_K9T_CLUSTER");
-    const int v = e ? atoi(e) : 2;
-    return (v == 1 || v == 2 || v == 4) ? v : 2;
+    const int v = e ? atoi(e) : 22;
+    return (v == 1 || v == 2 || v == 4 || v == 22) ? v : 22;
   }();
   return c;
 }
@@ -1428,15 +1459,18 @@ int fsr_filter_topk_tc(fsr_ctx* ctx, int64_t n, int64_t r, const int64_t* u_indp
   const int cl = cluster_choice();
   const int tn = b <= 64 ? 64 : b <= 128 ? 128 : 256;  // query tile: no MMA work on padding queries
   if (tn == 64)
-    FSR_TRY((cl == 1 ? tc_gemms<1, 64>(ctx, L, Wk, n, r, b, topk) : cl == 2 ? tc_gemms<2, 64>(ctx, L, Wk, n, r, b, topk)
-                                                                          : tc_gemms<4, 64>(ctx, L, Wk, n, r, b, topk)));
+    FSR_TRY((cl == 1 ? tc_gemms<1, 64>(ctx, L, Wk, n, r, b, topk)
+             : cl == 2 || cl == 22 ? tc_gemms<2, 64>(ctx, L, Wk, n, r, b, topk)
+                                   : tc_gemms<4, 64>(ctx, L, Wk, n, r, b, topk)));
   else if (tn == 128)
     FSR_TRY((cl == 1   ? tc_gemms<1, 128>(ctx, L, Wk, n, r, b, topk)
-             : cl == 2 ? tc_gemms<2, 128>(ctx, L, Wk, n, r, b, topk)
+             : cl == 2 || cl == 22 ? tc_gemms<2, 128>(ctx, L, Wk, n, r, b, topk)
                        : tc_gemms<4, 128>(ctx, L, Wk, n, r, b, topk)));
+  else if (cl == 22 && ((b + 255) / 256) % 2 == 0)
+    FSR_TRY((tc_gemms<4, 256, true>(ctx, L, Wk, n, r, b, topk)));
   else
     FSR_TRY((cl == 1   ? tc_gemms<1, 256>(ctx, L, Wk, n, r, b, topk)
-             : cl == 2 ? tc_gemms<2, 256>(ctx, L, Wk, n, r, b, topk)
+             : cl == 2 || cl == 22 ? tc_gemms<2, 256>(ctx, L, Wk, n, r, b, topk)
                        : tc_gemms<4, 256>(ctx, L, Wk, n, r, b, topk)));
   return finish_stage(ctx, L.cb, Wk, n, b, u_indptr, u_indices, u_values, eta, copy, y_ptr, y_idx, y_val, topk,
                       top_idx, top_val);
