@@ -253,10 +253,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   // (b = 10000: 40 query tiles, 100 MB of Zh).  band = tiles_n: one band.
   const int row_groups = total / tiles_n;  // row-tile groups (of CL tiles) per query tile
   auto tile_of = [&](int idx, int& ti, int& tj) {
-    if (M2) {
-      const int tiles_np = tiles_n / 2;
-      ti = (idx / tiles_np) * 2 + rr;
-      tj = (idx % tiles_np) * 2 + rq;
+    if (M2) {  // the same raster over query-tile pairs
+      const int tiles_np = tiles_n / 2, bandp = max(1, band / 2), rgp = total / tiles_np;
+      const int bnd = idx / (bandp * rgp);
+      const int rem = idx - bnd * bandp * rgp;
+      const int gw = min(bandp, tiles_np - bnd * bandp);
+      ti = (rem / gw) * 2 + rr;
+      tj = (bnd * bandp + rem % gw) * 2 + rq;
       if (MODE == 0) ti *= kSampleStride;
       return;
     }
