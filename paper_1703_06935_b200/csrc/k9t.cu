@@ -426,6 +426,275 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+
+// ---------------------------------------------------- 2-SM (cta_group::2) --
+// The same main pass with CTA-pair MMAs: a cluster of 4 = 2 pairs; pair p
+// multiplies a 256-row tile of U~ (CTA h of the pair holds rows h*128..+128)
+// by query tile 2 qp + p (each CTA holds half the tile's 256 queries), with
+// `tcgen05.mma.cta_group::2` M = 256 N = 256 issued by the pair's even CTA.
+// Per CTA and K-step the stage is A 16 KB + B 16 KB (instead of A + a whole
+// B tile), so 6 stages fit where 4 did; the A rows are also shared across
+// the two pairs (each CTA loads half and multicasts it to its counterpart,
+// rank ^ 2).  Barriers: full[s] lives in each pair's even CTA and counts the
+// pair's 64 KB (the odd CTA's TMA loads signal it, peer bit cleared);
+// empty[s] of every CTA waits for both pairs' MMA commits (its A half is in
+// the other pair's stage too); tempty[] of the even CTA counts the epilogue
+// warps of both CTAs.
+namespace sm2 {
+constexpr int STAGES2 = 6;
+constexpr int BM2 = 256;                          // rows per pair tile
+constexpr int A_HALF = 128 * BK * 2;              // 16 KB: this CTA's 128 rows
+constexpr int B_HALF = 128 * BK * 2;              // 16 KB: this CTA's 128 queries
+constexpr int STAGE2 = A_HALF + B_HALF;
+constexpr int TN2 = 256;
+constexpr int SMEM2 = STAGES2 * STAGE2 + 1024 + 256 + 2 * TN2 * 16 + 2 * TN2 * 4 + TN2 * 4;
+constexpr int kSample2 = kSampleStride;           // every 32nd 256-row tile: the same 1/32 of the rows
+static_assert(SMEM2 <= 227 * 1024, "stages exceed shared memory");
+
+__host__ __device__ constexpr uint32_t idesc_f16_m256(int N) {
+  return (1u << 4) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
+}
+__device__ __forceinline__ void mma2_f16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                         uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void commit2_mc(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"(mask)
+      : "memory");
+}
+// 2-D TMA into this CTA's smem, completion counted on the pair's even CTA's barrier
+__device__ __forceinline__ void tma2_load(void* dst, const CUtensorMap* map, uint64_t* bar, int32_t c0, int32_t c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], "
+      "[%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar) & 0xFEFFFFFFu), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void tma2_load_mc(void* dst, const CUtensorMap* map, uint64_t* bar, int32_t c0, int32_t c1,
+                                             uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+      " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar) & 0xFEFFFFFFu), "r"(c0), "r"(c1), "h"(mask)
+      : "memory");
+}
+// arrive on the pair's even CTA's barrier (this CTA's copy at the same offset)
+__device__ __forceinline__ void mbar_arrive_pair0(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(smem_u32(bar) & 0xFEFFFFFFu) : "memory");
+}
+__device__ __forceinline__ void tmem_alloc2(uint32_t* smem_dst, uint32_t ncols) {
+  asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(smem_dst)),
+               "r"(ncols));
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+}
+__device__ __forceinline__ void tmem_dealloc2(uint32_t taddr, uint32_t ncols) {
+  asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols));
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(kThreads, 1)
+    k9t_gemm2sm_kernel(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUtensorMap mB, int n, int b,
+                       int r, int tiles_np, int total, const float* __restrict__ cb, const float2* __restrict__ qp,
+                       const QParam* __restrict__ qpar, const uint32_t* __restrict__ thr, uint32_t* __restrict__ Ks,
+                       int64_t ns, int32_t* __restrict__ cand, float* __restrict__ cval,
+                       int32_t* __restrict__ ccount, unsigned* __restrict__ nlow) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint64_t* full = (uint64_t*)(smem + STAGES2 * STAGE2);
+  uint64_t* empty = full + STAGES2;
+  uint64_t* tfull = empty + STAGES2;  // [2]
+  uint64_t* tempty = tfull + 2;       // [2]
+  uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
+  float4* spar = (float4*)(smem + STAGES2 * STAGE2 + 256);  // [2][TN2]
+  uint32_t* sthr = (uint32_t*)(spar + 2 * TN2);              // [2][TN2]
+  unsigned* scnt = sthr + 2 * TN2;                           // [TN2]
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int iters = (r + BK - 1) / BK;
+  const int rank = (int)cluster_rank();
+  const int h = rank & 1, p = rank >> 1;  // half within the pair, pair index
+  const bool lead = h == 0;
+  const int cluster = blockIdx.x / 4, nclusters = gridDim.x / 4;
+  const uint16_t maskA = (uint16_t)((1u << rank) | (1u << (rank ^ 2)));
+  const uint16_t maskPair = (uint16_t)(3u << (2 * p));
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES2; ++s) {
+      mbar_init(&full[s], 1);   // the even CTA's producer arrives (with the pair's 64 KB of tx)
+      mbar_init(&empty[s], 2);  // both pairs' MMA commits
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 8);  // 4 epilogue warps in each CTA of the pair
+    }
+    fence_barrier_init();
+  }
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&mA);
+    tma_prefetch(&mB);
+  }
+  if (warp == 1) tmem_alloc2(tmem_slot, 512);
+  for (int t = threadIdx.x; t < TN2; t += blockDim.x) scnt[t] = 0;
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  // item -> (256-row tile, query-tile pair); this CTA's query tile is 2 qp + p
+  auto tile_of = [&](int idx, int& t2, int& tj) {
+    t2 = idx / tiles_np;
+    tj = (idx % tiles_np) * 2 + p;
+    if (MODE == 0) t2 *= kSample2;
+  };
+
+  if (warp == 0) {
+    int g = 0;
+    for (int idx = cluster; idx < total; idx += nclusters) {
+      int t2, tj;
+      tile_of(idx, t2, tj);
+      for (int it = 0; it < iters; ++it, ++g) {
+        const int s = g % STAGES2;
+        mbar_wait(&empty[s], ((g / STAGES2) & 1) ^ 1);
+        if (lane == 0) {
+          uint8_t* st = smem + s * STAGE2;
+          if (lead) mbar_expect_tx(&full[s], 2 * STAGE2);
+          // A: 64 of this CTA's 128 rows (half p of them), multicast to the other pair's CTA h
+          tma2_load_mc(st + p * (A_HALF / 2), &mA, &full[s], it * BK, t2 * BM2 + h * 128 + p * 64, maskA);
+          // B: this CTA's 128 of the query tile's 256 queries
+          tma2_load(st + A_HALF, &mB, &full[s], it * BK, tj * TN2 + h * 128);
+        }
+        __syncwarp();
+      }
+    }
+  } else if (warp == 1) {
+    if (lead) {
+      constexpr uint32_t idesc = idesc_f16_m256(TN2);
+      int g = 0, tcount = 0;
+      for (int idx = cluster; idx < total; idx += nclusters, ++tcount) {
+        const int ab = tcount & 1, use = tcount >> 1;
+        if (use > 0) {
+          mbar_wait(&tempty[ab], (use - 1) & 1);
+          tc_fence_after();
+        }
+        const uint32_t d = tmem + ab * TN2;
+        for (int it = 0; it < iters; ++it, ++g) {
+          const int s = g % STAGES2;
+          mbar_wait(&full[s], (g / STAGES2) & 1);
+          tc_fence_after();
+          const uint32_t sa = smem_u32(smem + s * STAGE2);
+          const uint64_t da = smem_desc_sw128(sa, 16, 1024), db = smem_desc_sw128(sa + A_HALF, 16, 1024);
+          if (lane == 0) {
+#pragma unroll
+            for (int k = 0; k < BK / 16; ++k)
+              mma2_f16(d, da + (uint64_t)(2 * k), db + (uint64_t)(2 * k), idesc, (it | k) ? 1u : 0u);
+            commit2_mc(&empty[s], 0xF);  // every CTA: both pairs read the A halves it wrote
+            if (it == iters - 1) commit2_mc(&tfull[ab], maskPair);
+          }
+          __syncwarp();
+        }
+      }
+    }
+  } else {
+    const int q4 = warp & 3;
+    const int et = threadIdx.x - 64;
+    int tcount = 0;
+    for (int idx = cluster; idx < total; idx += nclusters, ++tcount) {
+      int t2, tj;
+      tile_of(idx, t2, tj);
+      const int ab = tcount & 1, use = tcount >> 1, pb = tcount & 1;
+      const int j0 = tj * TN2;
+      for (int t = et; t < TN2; t += 128) {
+        const int q = j0 + t;
+        float4 pp = make_float4(__int_as_float(0x7fffffff), 1.f, 0.f, 0.f);
+        uint32_t tk = 0xffffffffu;
+        if (q < b) {
+          if (MODE == 0) {
+            const float2 v = qp[q];
+            pp = make_float4(0.f, v.x, 0.f, v.y);
+          } else {
+            const QParam v = qpar[q];
+            pp = make_float4(v.tf_pre, v.inv, v.cz, v.zb);
+            tk = thr[q];
+          }
+        }
+        spar[pb * TN2 + t] = pp;
+        sthr[pb * TN2 + t] = tk;
+      }
+      const int row = t2 * BM2 + h * 128 + 32 * q4 + lane;
+      const bool row_ok = row < n;
+      const float c = row_ok ? __ldg(cb + row) : 0.f;
+      mbar_wait(&tfull[ab], use & 1);
+      tc_fence_after();
+      epi_barrier();
+      const uint32_t tl = tmem + ((uint32_t)(32 * q4) << 16) + ab * TN2;
+#pragma unroll 1
+      for (int cc = 0; cc < TN2 / 32; ++cc) {
+        float v[32];
+        tmem_ld32(tl + cc * 32, v);
+        if (!row_ok) continue;
+        if (MODE == 0) {
+          const int64_t srow = (int64_t)(t2 / kSample2) * BM2 + h * 128 + 32 * q4 + lane;
+#pragma unroll
+          for (int t = 0; t < 32; ++t) {
+            const int jj = cc * 32 + t;
+            if (j0 + jj < b) {
+              const float4 pp = spar[pb * TN2 + jj];
+              const float x = v[t] * pp.y;
+              Ks[(int64_t)(j0 + jj) * ns + srow] = prune::key32(__fsub_rd(x, prune::bound_of(c, pp.w)));
+            }
+          }
+        } else {
+#pragma unroll
+          for (int t = 0; t < 32; ++t) {
+            const int jj = cc * 32 + t;
+            const float4 pp = spar[pb * TN2 + jj];
+            const float x = v[t] * pp.y;
+            if (x + pp.z >= pp.x) {
+              const float bd = prune::bound_of(c, pp.w);
+              const uint32_t tk = sthr[pb * TN2 + jj];
+              if (prune::key32(__fsub_rd(x, bd)) >= tk) atomicAdd(&scnt[jj], 1u);
+              if (prune::key32(__fadd_ru(x, bd)) >= tk) {
+                FSR_DCHECK(j0 + jj < b && row < n);
+                const int slot = atomicAdd(ccount + j0 + jj, 1);
+                if (slot < kCap) {
+                  cand[(int64_t)(j0 + jj) * kCap + slot] = row;
+                  cval[(int64_t)(j0 + jj) * kCap + slot] = x;
+                }
+              }
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_pair0(&tempty[ab]);  // the pair's MMA issuer may reuse this accumulator
+      if (MODE == 1) {
+        epi_barrier();
+        for (int t = et; t < TN2; t += 128) {
+          const unsigned k = scnt[t];
+          if (k) {
+            atomicAdd(nlow + j0 + t, k);
+            scnt[t] = 0;
+          }
+        }
+      }
+    }
+  }
+  cluster_sync();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc2(tmem, 512);
+  }
+}
+
+}  // namespace sm2
+
 // ------------------------------------------------------------- threshold --
 // Per query: t = the target-th largest lower key of the sample (two 12-bit
 // digits), the QParam of the main pass, zeroed counters.  z = 0 queries are
@@ -877,7 +1146,11 @@ constexpr int kCluster = 4;  // CTAs per cluster sharing a query tile (B multica
 inline int64_t sample_rows(int64_t n) {
   const int64_t tiles_m = (n + BM - 1) / BM;
   const int64_t s_tiles = (tiles_m + kSampleStride - 1) / kSampleStride;
-  return (s_tiles + kCluster - 1) / kCluster * kCluster * BM;  // whole clusters of sampled tiles
+  const int64_t rows1 = (s_tiles + kCluster - 1) / kCluster * kCluster * BM;  // whole clusters of sampled tiles
+  // the 2-SM pass samples 256-row tiles
+  const int64_t tiles_m2 = (n + sm2::BM2 - 1) / sm2::BM2;
+  const int64_t rows2 = (tiles_m2 + sm2::kSample2 - 1) / sm2::kSample2 * sm2::BM2;
+  return std::max(rows1, rows2);
 }
 
 // persistent grid: as many whole clusters as fit at once (1 CTA per SM)
@@ -1019,6 +1292,88 @@ int tc_gemms(fsr_ctx* ctx, const DenseLayout& L, const Work& Wk, int64_t n, int6
   return FSR_OK;
 }
 
+// 2-SM main pass (sm2::k9t_gemm2sm_kernel): 4-CTA clusters = 2 CTA pairs
+template <int MODE>
+int launch_gemm2sm(fsr_ctx* ctx, int grid, const CUtensorMap& mA, const CUtensorMap& mB, int n, int b, int r,
+                   int tiles_np, int total, const float* cb, const float2* qp, const QParam* qpar,
+                   const uint32_t* thr, uint32_t* Ks, int64_t ns, int32_t* cand, float* cval, int32_t* ccount,
+                   unsigned* nlow) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = sm2::SMEM2;
+  cfg.stream = ctx->stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 4;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  FSR_CUDA(ctx, cudaLaunchKernelEx(&cfg, sm2::k9t_gemm2sm_kernel<MODE>, mA, mB, n, b, r, tiles_np, total, cb, qp, qpar,
+                                   thr, Ks, ns, cand, cval, ccount, nlow));
+  return launched(ctx, MODE == 0 ? "k9t_gemm2sm_sample" : "k9t_gemm2sm_select");
+}
+
+inline int grid2sm(fsr_ctx* ctx) {
+  static int cached[64] = {0};
+  int& g = cached[ctx->device & 63];
+  if (g) return g;
+  if (ensure_smem(ctx, sm2::k9t_gemm2sm_kernel<1>, sm2::SMEM2) != FSR_OK) return -1;
+  if (ensure_smem(ctx, sm2::k9t_gemm2sm_kernel<0>, sm2::SMEM2) != FSR_OK) return -1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(ctx->num_sms / 4 * 4));
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = sm2::SMEM2;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 4;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  int nclusters = 0;
+  if (cudaOccupancyMaxActiveClusters(&nclusters, sm2::k9t_gemm2sm_kernel<1>, &cfg) != cudaSuccess || nclusters < 1) {
+    cudaGetLastError();
+    nclusters = ctx->num_sms / 4;
+  }
+  g = nclusters * 4;
+  return g;
+}
+
+// sample GEMM -> threshold -> selecting GEMM on the 2-SM pass (an even number of 256-query tiles)
+inline int tc_gemms_2sm(fsr_ctx* ctx, const DenseLayout& L, const Work& Wk, int64_t n, int64_t r, int64_t b,
+                        int64_t topk) {
+  using namespace sm2;
+  const int64_t ldr = ld_of(r);
+  CUtensorMap mA, mB;
+  FSR_TRY(make_map_f16(ctx, &mA, L.Ud, n, r, ldr, 64));
+  FSR_TRY(make_map_f16(ctx, &mB, Wk.Zh, b, r, ldr, 128));
+  const int grid = grid2sm(ctx);
+  if (grid <= 0) return set_error(ctx, FSR_ECUDA, "filter_topk_tc: no co-resident 4-CTA clusters (2-SM)");
+  const int tiles_m2 = (int)((n + BM2 - 1) / BM2), tiles_np = (int)((b + TN2 - 1) / TN2) / 2;
+  const int64_t ns = sample_rows(n);
+  const int s_tiles2 = (tiles_m2 + kSample2 - 1) / kSample2;
+  {
+    StageTimer timer(ctx, FSR_STAGE_TOPK);
+    FSR_TRY((launch_gemm2sm<0>(ctx, grid, mA, mB, (int)n, (int)b, (int)r, tiles_np, s_tiles2 * tiles_np, L.cb, Wk.qp,
+                               nullptr, nullptr, Wk.Ks, ns, nullptr, nullptr, nullptr, nullptr)));
+    const int64_t last_tile = (int64_t)(s_tiles2 - 1) * kSample2;
+    const int64_t n_valid_s = (int64_t)(s_tiles2 - 1) * BM2 + std::min<int64_t>(BM2, n - last_tile * BM2);
+    const int64_t target = (2 * topk + kSampleStride - 1) / kSampleStride + 8;
+    k9t_threshold_kernel<<<(unsigned)std::min<int64_t>(b, (int64_t)ctx->num_sms * 8), 256, 0, ctx->stream>>>(
+        b, ns, n_valid_s, Wk.Ks, Wk.qp, L.cmax_bits, target, Wk.thr, Wk.qpar, Wk.ccount, Wk.nlow, Wk.nflag,
+        Wk.nflag + 1, nullptr);
+    FSR_TRY(launched(ctx, "k9t_threshold_kernel"));
+  }
+  {
+    StageTimer timer(ctx, FSR_STAGE_FILTER_SPMM);
+    FSR_TRY((launch_gemm2sm<1>(ctx, grid, mA, mB, (int)n, (int)b, (int)r, tiles_np, tiles_m2 * tiles_np, L.cb, Wk.qp,
+                               Wk.qpar, Wk.thr, nullptr, 0, Wk.cand, Wk.cval, Wk.ccount, Wk.nlow)));
+  }
+  return FSR_OK;
+}
+
 // FSR_K9T_CLUSTER = 1 / 2 / 4 CTAs per cluster (B-tile multicast), 22 = 2 x 2
 // clusters with A and B multicast (default; an odd number of 256-query tiles
 // falls back to 2).  C3 b = 1024, same box back to back: 2 x 2 8.41 ms vs 2
@@ -1028,7 +1383,7 @@ inline int cluster_choice() {
   static int c = [] {
     const char* e = getenv("FSR_K9T_CLUSTER");
     const int v = e ? atoi(e) : 22;
-    return (v == 1 || v == 2 || v == 4 || v == 22) ? v : 22;
+    return (v == 1 || v == 2 || v == 4 || v == 22 || v == 42) ? v : 22;  // 42: 2-SM pairs (opt-in)
   }();
   return c;
 }
@@ -1463,17 +1818,19 @@ int fsr_filter_topk_tc(fsr_ctx* ctx, int64_t n, int64_t r, const int64_t* u_indp
   const int tn = b <= 64 ? 64 : b <= 128 ? 128 : 256;  // query tile: no MMA work on padding queries
   if (tn == 64)
     FSR_TRY((cl == 1 ? tc_gemms<1, 64>(ctx, L, Wk, n, r, b, topk)
-             : cl == 2 || cl == 22 ? tc_gemms<2, 64>(ctx, L, Wk, n, r, b, topk)
+             : cl == 2 || cl == 22 || cl == 42 ? tc_gemms<2, 64>(ctx, L, Wk, n, r, b, topk)
                                    : tc_gemms<4, 64>(ctx, L, Wk, n, r, b, topk)));
   else if (tn == 128)
     FSR_TRY((cl == 1   ? tc_gemms<1, 128>(ctx, L, Wk, n, r, b, topk)
-             : cl == 2 || cl == 22 ? tc_gemms<2, 128>(ctx, L, Wk, n, r, b, topk)
+             : cl == 2 || cl == 22 || cl == 42 ? tc_gemms<2, 128>(ctx, L, Wk, n, r, b, topk)
                        : tc_gemms<4, 128>(ctx, L, Wk, n, r, b, topk)));
-  else if (cl == 22 && ((b + 255) / 256) % 2 == 0)
+  else if (cl == 42 && ((b + 255) / 256) % 2 == 0)
+    FSR_TRY(tc_gemms_2sm(ctx, L, Wk, n, r, b, topk));
+  else if ((cl == 22 || cl == 42) && ((b + 255) / 256) % 2 == 0)
     FSR_TRY((tc_gemms<4, 256, true>(ctx, L, Wk, n, r, b, topk)));
   else
     FSR_TRY((cl == 1   ? tc_gemms<1, 256>(ctx, L, Wk, n, r, b, topk)
-             : cl == 2 || cl == 22 ? tc_gemms<2, 256>(ctx, L, Wk, n, r, b, topk)
+             : cl == 2 || cl == 22 || cl == 42 ? tc_gemms<2, 256>(ctx, L, Wk, n, r, b, topk)
                        : tc_gemms<4, 256>(ctx, L, Wk, n, r, b, topk)));
   return finish_stage(ctx, L.cb, Wk, n, b, u_indptr, u_indices, u_values, eta, copy, y_ptr, y_idx, y_val, topk,
                       top_idx, top_val);
