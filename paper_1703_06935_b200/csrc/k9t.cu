@@ -1375,15 +1375,17 @@ inline int tc_gemms_2sm(fsr_ctx* ctx, const DenseLayout& L, const Work& Wk, int6
 }
 
 // FSR_K9T_CLUSTER = 1 / 2 / 4 CTAs per cluster (B-tile multicast), 22 = 2 x 2
-// clusters with A and B multicast (default; an odd number of 256-query tiles
-// falls back to 2).  C3 b = 1024, same box back to back: 2 x 2 8.41 ms vs 2
-// 8.87 ms -- DRAM reads 26 -> 13 GB per launch and the board's power cap
-// allows 1.75 instead of 1.41 GHz (ncu, profiles/r02/k9t_ncu_full.json).
+// clusters with A and B multicast, 42 = 2-SM CTA pairs (cta_group::2) in
+// 4-CTA clusters with A multicast across the pairs (default; an odd number of
+// 256-query tiles falls back to 2).  C3 b = 1024, same box back to back: 2
+// 8.87 ms, 2 x 2 8.41 ms (DRAM reads 26 -> 13 GB per launch, the power cap
+// then allows 1.75 instead of 1.41 GHz), 2-SM 7.49 ms (6 stages instead of 4:
+// the MMA issuer waited on data ~20% of the time).
 inline int cluster_choice() {
   static int c = [] {
     const char* e = getenv("FSR_K9T_CLUSTER");
-    const int v = e ? atoi(e) : 22;
-    return (v == 1 || v == 2 || v == 4 || v == 22 || v == 42) ? v : 22;  // 42: 2-SM pairs (opt-in)
+    const int v = e ? atoi(e) : 42;
+    return (v == 1 || v == 2 || v == 4 || v == 22 || v == 42) ? v : 42;
   }();
   return c;
 }
