@@ -903,8 +903,9 @@ def run_fsr(args, cfg, n, rank, world, local_rank):
         hbm_bytes = n * ldr * 2 + b * ldr * 2 + n * 4  # dense fp16 U~ once, fp16 Zh, c_i
         ncu9 = load_profile("k9t_ncu_full.json") or {}
         roofline = {
-            "kernel": "K9t main pass k9t_gemm_kernel<1> (tcgen05.mma kind::f16 M=128 N=256, TMA with B-tile "
-                      "multicast in 2-CTA clusters, double-buffered TMEM accumulators, fused certified selection)",
+            "kernel": "K9t main pass k9t_gemm2sm_kernel<1> (tcgen05.mma.cta_group::2 kind::f16 M=256 N=256 on CTA "
+                      "pairs, 4-CTA clusters with the U~ tile multicast across the pairs, 6 TMA stages, "
+                      "double-buffered TMEM accumulators, fused certified selection)",
             "bound": "tensor", "achieved": achieved, "peak": tpeak, "unit": "TFLOP/s", "frac": achieved / tpeak,
             "peak_kind": tpeak_kind,
             "traffic": ncu9.get("dram_bytes_per_launch") if profile_ok else None,
