@@ -839,12 +839,56 @@ __global__ void __launch_bounds__(256) k9t_rescore_kernel(
     float* __restrict__ pre);
 
 constexpr int kKeep = 1024;  // rows re-scored exactly per query (upper >= lambda_K); more -> fallback
-// Candidates a finish CTA holds in shared memory.  Half the list capacity:
-// 56 KB of shared memory per CTA instead of 80 KB, 4 CTAs per SM instead of 2
-// (the finish is latency-bound on its re-score chains).  C3: at most 1365
-// candidates per query; a query with more takes the exact fallback.
+// Candidates a finish CTA holds in shared memory (C3: at most 1365 per query;
+// a query with more takes the exact fallback).
 constexpr int kFinishCap = 2048;
-constexpr size_t kFinishSmem = (size_t)kFinishCap * 12 + (size_t)(1 << topk::kHistBits) * 4 + (size_t)kKeep * 16;
+// Shared memory of a finish CTA: the radix histogram, later the kept rows'
+// sort keys and indices (16 KB); lower keys, later the kept rows' entry
+// offsets (8 KB); rows, later the kept rows' lengths (8 KB); scores (8 KB);
+// then the query's fp32 zs column (r floats) when it fits kZsSmemMax.
+constexpr size_t kFinishSmem = (size_t)kKeep * 16 + (size_t)kFinishCap * 12;
+static_assert((size_t)(1 << topk::kHistBits) * 4 <= (size_t)kKeep * 16, "histogram aliases the kept keys");
+constexpr int64_t kZsSmemMax = 24576;  // r up to this: zs_q staged in shared memory (96 KB)
+inline size_t finish_smem(int64_t r) { return kFinishSmem + (r <= kZsSmemMax ? (size_t)r * 4 : 0); }
+
+// The sequential fp32 sum of `len` entries from e0 by a G-lane group, the
+// query's zs in shared memory (zsm) or strided in global memory (Zs[c * ldz]):
+// all R loads per lane of a 64-entry round in flight, then the dependent FMA
+// chain in CSR order on broadcast values -- bitwise exact_row / exact_row_group.
+template <int G, bool SMEM>
+__device__ __forceinline__ float seq_sum_group(int64_t e0, int len, const int32_t* __restrict__ indices,
+                                               const float* __restrict__ vals, const float* __restrict__ zsm,
+                                               const float* __restrict__ Zs, int64_t ldz, unsigned mask) {
+  constexpr int R = 64 / G;
+  const int gl = threadIdx.x & (G - 1);
+  float acc = 0.f;
+  for (int base = 0; base < len; base += G * R) {
+    const int m = len - base < G * R ? len - base : G * R;
+    float a[R], z[R];
+    int c[R];
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+      const int t = k * G + gl;
+      c[k] = t < m ? __ldg(indices + e0 + base + t) : 0;
+      a[k] = t < m ? __ldg(vals + e0 + base + t) : 0.f;
+    }
+#pragma unroll
+    for (int k = 0; k < R; ++k) z[k] = SMEM ? zsm[c[k]] : (k * G + gl < m ? __ldg(Zs + (int64_t)c[k] * ldz) : 0.f);
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+      const int mk = m - k * G < G ? m - k * G : G;
+      if (mk <= 0) break;
+      if (mk == G) {
+#pragma unroll
+        for (int e = 0; e < G; ++e)
+          acc = fmaf(__shfl_sync(mask, a[k], e, G), __shfl_sync(mask, z[k], e, G), acc);
+      } else {
+        for (int e = 0; e < mk; ++e) acc = fmaf(__shfl_sync(mask, a[k], e, G), __shfl_sync(mask, z[k], e, G), acc);
+      }
+    }
+  }
+  return acc;
+}
 
 __global__ void __launch_bounds__(256) k9t_rescore_kernel(
     int64_t b, const int32_t* __restrict__ cand, const int32_t* __restrict__ ccount,
@@ -872,23 +916,36 @@ __global__ void __launch_bounds__(kFinishThreads) k9t_finish_kernel(
     const float* __restrict__ cb, const QParam* __restrict__ qpar, const uint32_t* __restrict__ thr,
     const int32_t* __restrict__ cand, const float* __restrict__ cval, const int32_t* __restrict__ ccount,
     const unsigned* __restrict__ nlow, const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices,
-    const float* __restrict__ vals, const float* __restrict__ Zs, int64_t ldz, const double* __restrict__ eta,
-    int copy, const int64_t* __restrict__ y_ptr, const int64_t* __restrict__ y_idx, const float* __restrict__ y_val,
-    int64_t K, int64_t* __restrict__ out_idx, float* __restrict__ out_val, int* __restrict__ nflag,
-    int* __restrict__ flags, int2* __restrict__ stats, const float* __restrict__ pre) {
+    const float* __restrict__ vals, const float* __restrict__ Zs, int64_t ldz, const float* __restrict__ Zt,
+    int64_t r, const double* __restrict__ eta, int copy, const int64_t* __restrict__ y_ptr,
+    const int64_t* __restrict__ y_idx, const float* __restrict__ y_val, int64_t K, int64_t* __restrict__ out_idx,
+    float* __restrict__ out_val, int* __restrict__ nflag, int* __restrict__ flags, int2* __restrict__ stats,
+    const float* __restrict__ pre) {
   constexpr int HB = topk::kHistBits, NB = 1 << HB;
   extern __shared__ __align__(16) unsigned char dyn[];
   uint64_t* kkey = (uint64_t*)dyn;             // [kKeep] exact order keys of the kept rows
   int64_t* kidx = (int64_t*)(kkey + kKeep);    // [kKeep] row << 12 | slot
+  unsigned* hist = (unsigned*)dyn;             // [NB], before kkey / kidx are written
   uint32_t* lkey = (uint32_t*)(kidx + kKeep);  // [kFinishCap] lower-bound keys by slot
-  int32_t* crow = (int32_t*)(lkey + kFinishCap);     // [kFinishCap] rows by slot
-  float* cv = (float*)(crow + kFinishCap);           // [kFinishCap] x~, then exact scores, by slot
-  unsigned* hist = (unsigned*)(cv + kFinishCap);     // [NB]
+  int64_t* ke0 = (int64_t*)lkey;               // [kKeep] after the keep pass: entry offset of kept row t
+  int32_t* crow = (int32_t*)(lkey + kFinishCap);  // [kFinishCap] rows by slot
+  int32_t* klen = crow;                           // [kKeep] after the keep pass: its length (-1: no re-score)
+  float* cv = (float*)(crow + kFinishCap);        // [kFinishCap] x~, then exact scores, by slot
+  float* zsm = cv + kFinishCap;                   // [r] zs_q when r <= kZsSmemMax
   __shared__ unsigned n_extra, n_extra_ge, n_keep, n_next, found_bin;
   __shared__ unsigned long long above;
   const int64_t q = blockIdx.x;
   const int cnt0 = ccount[q];
   if (cnt0 < 0) return;  // flagged (fallback) or empty observation (k9t_empty)
+  const bool zs_smem = pre == nullptr && r <= kZsSmemMax;
+  if (zs_smem) {  // zs_q (= Zt row q, the same fp32 values as Zs[:, q]) in flight while the candidates load
+    const float* src = Zt + q * r;
+    for (int64_t c = threadIdx.x; c < r; c += blockDim.x) {
+      const unsigned dst = (unsigned)__cvta_generic_to_shared(zsm + c);
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(dst), "l"(src + c) : "memory");
+    }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  }
   const int cnt = min(cnt0, kFinishCap);
   const uint32_t tk = thr[q];
   const float zb = qpar[q].zb;
@@ -923,6 +980,7 @@ __global__ void __launch_bounds__(kFinishThreads) k9t_finish_kernel(
   if (cnt0 > kFinishCap || total > kFinishCap ||
       (unsigned long long)nlow[q] + n_extra_ge < (unsigned long long)K) {
     if (threadIdx.x == 0) flags[atomicAdd(nflag, 1)] = (int)q;  // overflow, or the sampled t was too high
+    if (zs_smem) asm volatile("cp.async.wait_all;\n" ::: "memory");
     return;
   }
   // lambda' <= lambda_K (the K-th largest lower bound): two 12-bit radix
@@ -963,27 +1021,52 @@ __global__ void __launch_bounds__(kFinishThreads) k9t_finish_kernel(
   if (threadIdx.x == 0) stats[q] = make_int2(total, (int)keep);
   if (keep > (unsigned)kKeep) {
     if (threadIdx.x == 0) flags[atomicAdd(nflag, 1)] = (int)q;
+    if (zs_smem) asm volatile("cp.async.wait_all;\n" ::: "memory");
     return;
   }
-  // exact re-score of the kept main candidates (8-lane groups, rows from a counter)
-  constexpr int G = 8;
-  const int lane = threadIdx.x & 31, grp = threadIdx.x / G, gl = threadIdx.x & (G - 1);
-  const unsigned gmask = 0xffu << (lane & ~(G - 1));
-  if (threadIdx.x == 0) n_next = kFinishThreads / G;
-  __syncthreads();
   if (pre) {  // small batches: every candidate was re-scored by k9t_rescore_kernel
     for (unsigned t = threadIdx.x; t < keep; t += blockDim.x) {
       const int slot = (int)(kidx[t] & 4095);
       if (slot < cnt) cv[slot] = pre[q * kCap + slot];
     }
   } else {
-    for (unsigned t = grp; t < keep;) {
+    // exact re-score of the kept main candidates.  First every kept row's
+    // extent (and the copied value of an uncovered observed row) with all
+    // loads in flight at once, then 4-lane groups sum the rows sequentially
+    // against zs_q in shared memory.
+    for (unsigned t = threadIdx.x; t < keep; t += blockDim.x) {
       const int64_t packed = kidx[t];
       const int slot = (int)(packed & 4095);
+      const int64_t i = packed >> 12;
+      int len = -1;
       if (slot < cnt) {
-        const float v = exact_row_group<G>(packed >> 12, q, indptr, indices, vals, Zs, ldz, eta, copy, y_ptr, y_idx,
-                                           y_val, gmask);
-        if (gl == 0) cv[slot] = v;
+        float v;
+        if (copied_value(i, q, eta, copy, y_ptr, y_idx, y_val, &v)) {
+          cv[slot] = v;
+        } else {
+          const int64_t e0 = indptr[i], e1 = indptr[i + 1];
+          if (e0 == e1) {
+            cv[slot] = 0.f;
+          } else {
+            ke0[t] = e0;
+            len = (int)(e1 - e0);
+          }
+        }
+      }
+      klen[t] = len;
+    }
+    if (zs_smem) asm volatile("cp.async.wait_all;\n" ::: "memory");
+    constexpr int G = 4;
+    const int lane = threadIdx.x & 31, grp = threadIdx.x / G, gl = threadIdx.x & (G - 1);
+    const unsigned gmask = 0xfu << (lane & ~(G - 1));
+    if (threadIdx.x == 0) n_next = kFinishThreads / G;
+    __syncthreads();
+    for (unsigned t = grp; t < keep;) {
+      const int len = klen[t];
+      if (len > 0) {
+        const float v = zs_smem ? seq_sum_group<G, true>(ke0[t], len, indices, vals, zsm, nullptr, 0, gmask)
+                                : seq_sum_group<G, false>(ke0[t], len, indices, vals, nullptr, Zs + q, ldz, gmask);
+        if (gl == 0) cv[kidx[t] & 4095] = v;
       }
       unsigned nt = 0;
       if (gl == 0) nt = atomicAdd(&n_next, 1u);
@@ -1728,13 +1811,13 @@ int launch_groups(fsr_ctx* ctx, const Layout& L, const Work& Wk, const int64_t* 
 
 // finish (exact re-score of the kept candidates, sort), empty observations,
 // fallback: shared by K9t and the streaming path
-inline int finish_stage(fsr_ctx* ctx, const float* cb, const Work& Wk, int64_t n, int64_t b, const int64_t* u_indptr,
+inline int finish_stage(fsr_ctx* ctx, const float* cb, const Work& Wk, int64_t n, int64_t r, int64_t b, const int64_t* u_indptr,
                         const int32_t* u_indices, const float* u_values, const double* eta, int copy,
                         const int64_t* y_ptr, const int64_t* y_idx, const float* y_val, int64_t topk,
                         int64_t* top_idx, float* top_val) {
   {
     StageTimer timer(ctx, FSR_STAGE_TOPK);
-    const size_t fsm = kFinishSmem;
+    const size_t fsm = finish_smem(r);
     FSR_TRY(ensure_smem(ctx, k9t_finish_kernel, fsm));
     if (Wk.cex) {
       k9t_rescore_kernel<<<(unsigned)std::min<int64_t>((b * kCap * 8 + 255) / 256, (int64_t)ctx->num_sms * 8), 256,
@@ -1743,8 +1826,8 @@ inline int finish_stage(fsr_ctx* ctx, const float* cb, const Work& Wk, int64_t n
       FSR_TRY(launched(ctx, "k9t_rescore_kernel"));
     }
     k9t_finish_kernel<<<(unsigned)b, kFinishThreads, fsm, ctx->stream>>>(
-        cb, Wk.qpar, Wk.thr, Wk.cand, Wk.cval, Wk.ccount, Wk.nlow, u_indptr, u_indices, u_values, Wk.Zs, b, eta,
-        copy, y_ptr, y_idx, y_val, topk, top_idx, top_val, Wk.nflag, Wk.nflag + 1, Wk.stats, Wk.cex);
+        cb, Wk.qpar, Wk.thr, Wk.cand, Wk.cval, Wk.ccount, Wk.nlow, u_indptr, u_indices, u_values, Wk.Zs, b, Wk.Zt,
+        r, eta, copy, y_ptr, y_idx, y_val, topk, top_idx, top_val, Wk.nflag, Wk.nflag + 1, Wk.stats, Wk.cex);
     FSR_TRY(launched(ctx, "k9t_finish_kernel"));
     const size_t esm = (size_t)kCap * 32;
     FSR_TRY(ensure_smem(ctx, k9t_empty_kernel, esm));
@@ -1834,7 +1917,7 @@ int fsr_filter_topk_tc(fsr_ctx* ctx, int64_t n, int64_t r, const int64_t* u_indp
     FSR_TRY((cl == 1   ? tc_gemms<1, 256>(ctx, L, Wk, n, r, b, topk)
              : cl == 2 || cl == 22 || cl == 42 ? tc_gemms<2, 256>(ctx, L, Wk, n, r, b, topk)
                        : tc_gemms<4, 256>(ctx, L, Wk, n, r, b, topk)));
-  return finish_stage(ctx, L.cb, Wk, n, b, u_indptr, u_indices, u_values, eta, copy, y_ptr, y_idx, y_val, topk,
+  return finish_stage(ctx, L.cb, Wk, n, r, b, u_indptr, u_indices, u_values, eta, copy, y_ptr, y_idx, y_val, topk,
                       top_idx, top_val);
 }
 
@@ -1914,7 +1997,7 @@ int fsr_filter_topk_stream(fsr_ctx* ctx, int64_t n, int64_t r, int64_t nnz, cons
     StageTimer timer(ctx, FSR_STAGE_FILTER_SPMM);
     FSR_TRY(stream::launch_groups<1>(ctx, L, Wk, u_indptr, n, r, b));
   }
-  return finish_stage(ctx, L.cb, Wk, n, b, u_indptr, u_indices, u_values, eta, copy, y_ptr, y_idx, y_val, topk,
+  return finish_stage(ctx, L.cb, Wk, n, r, b, u_indptr, u_indices, u_values, eta, copy, y_ptr, y_idx, y_val, topk,
                       top_idx, top_val);
 }
 
