@@ -82,8 +82,12 @@ int fsr_ctx_enable_timing(fsr_ctx* ctx, int on);
  * FSR_OPT_TOPK_PRUNE: 1 (default) = fsr_filter_batch with top-k only (X ==
  * NULL), float32, sparse U, b >= 256 gathers Zs in fp16 and re-scores the
  * rows that can reach the top k exactly in fp32 (certified bound; the same
- * top-k indices and values as 0 = the unpruned fp32 path). */
-enum fsr_option { FSR_OPT_DENSE_PATH = 0, FSR_OPT_SPMM_PANEL_BYTES = 1, FSR_OPT_TOPK_PRUNE = 2 };
+ * top-k indices and values as 0 = the unpruned fp32 path).
+ * FSR_OPT_TOPK_SEGMENTS: segments a row is cut into by the exact top-k when
+ * fewer rows than SMs are selected (0 = automatic; results identical). */
+enum fsr_option {
+  FSR_OPT_DENSE_PATH = 0, FSR_OPT_SPMM_PANEL_BYTES = 1, FSR_OPT_TOPK_PRUNE = 2, FSR_OPT_TOPK_SEGMENTS = 3
+};
 int fsr_ctx_set_option(fsr_ctx* ctx, int option, int64_t value);
 int fsr_stage_time(fsr_ctx* ctx, int stage, double* ms, uint64_t* count);
 int fsr_stage_reset(fsr_ctx* ctx);
@@ -293,6 +297,29 @@ int fsr_filter_batch_u16(fsr_ctx* ctx, int dtype, int64_t n, int64_t r, int u_sp
                          int64_t ldu, const void* w, const double* eta, int64_t b, const int64_t* y_ptr,
                          const int64_t* y_idx, const void* y_val, int copy_uncovered, void* workspace, void* X,
                          int64_t topk, int64_t* top_idx, void* top_val);
+/* ---- K9e: the single-query filter on a sliced-ELL copy of U~ (csrc/k9e.cuh) ---
+ * Replaces, for ONE float32 query on a sparse decomposition, the product
+ * x = U~ (h(L) U~^T y) of specrank.ranking.filter (ranking.py:244-246) that
+ * fsr_filter_batch computes from the CSR.  The layout (built once per
+ * decomposition): rows sorted by length, descending (perm, lens), slices of
+ * 32 rows stored column-major (16-bit column, fp32 value; slice_ptr), rows
+ * longer than long_len left to the CSR (sorted positions [0, n_long)).
+ * fsr_sell_plan sorts and sizes (synchronises; *total_out = entries of the
+ * cols / vals arrays to allocate, >= 1), fsr_sell_pack fills them.
+ * fsr_filter_single_sell = fsr_filter_batch_u16 at b = 1 with the SpMV on
+ * that layout; every x_i is the sequential CSR-order fmaf chain (bitwise the
+ * b >= 256 kernels' sums).  r <= 16384. */
+int64_t fsr_sell_plan_workspace_bytes(int64_t n);
+int fsr_sell_plan(fsr_ctx* ctx, int64_t n, const int64_t* u_indptr, int64_t long_len, int32_t* perm, int32_t* lens,
+                  int64_t* slice_ptr, void* workspace, int64_t* n_long_out, int64_t* total_out);
+int fsr_sell_pack(fsr_ctx* ctx, int64_t n, const int64_t* u_indptr, const int32_t* u_indices, const float* u_values,
+                  const int32_t* perm, const int64_t* slice_ptr, uint16_t* cols, float* vals);
+int fsr_filter_single_sell(fsr_ctx* ctx, int64_t n, int64_t r, const int64_t* u_indptr, const int32_t* u_indices,
+                           const uint16_t* u_cols16, const float* u_values, const int32_t* sell_perm,
+                           const int32_t* sell_lens, const int64_t* sell_slice_ptr, const uint16_t* sell_cols,
+                           const float* sell_vals, int64_t n_long, const float* w, const double* eta,
+                           const int64_t* y_ptr, const int64_t* y_idx, const float* y_val, int copy_uncovered,
+                           void* workspace, float* X, int64_t topk, int64_t* top_idx, float* top_val);
 /* ---- K9t: the ranked-query step on tensor cores (csrc/k9t.cu) ----------------
  * Replaces, for a float32 sparse decomposition and top-k-only output, the
  * per-query loop of ranking.py:229-255 (filter) + ranking.py:390-395 (rank)[:topk]

@@ -70,6 +70,11 @@ _SIGS = {
     "fsr_u16_columns": (_c_int, [_c_p, _c_i64, _c_p, _c_p]),
     "fsr_filter_batch_u16": (_c_int, [_c_p, _c_int, _c_i64, _c_i64, _c_int, _c_p, _c_p, _c_p, _c_p, _c_p, _c_i64, _c_p,
                                       _c_p, _c_i64, _c_p, _c_p, _c_p, _c_int, _c_p, _c_p, _c_i64, _c_p, _c_p]),
+    "fsr_sell_plan_workspace_bytes": (_c_i64, [_c_i64]),
+    "fsr_sell_plan": (_c_int, [_c_p, _c_i64, _c_p, _c_i64, _c_p, _c_p, _c_p, _c_p, _c_i64p, _c_i64p]),
+    "fsr_sell_pack": (_c_int, [_c_p, _c_i64, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p]),
+    "fsr_filter_single_sell": (_c_int, [_c_p, _c_i64, _c_i64, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p,
+                                        _c_i64, _c_p, _c_p, _c_p, _c_p, _c_p, _c_int, _c_p, _c_p, _c_i64, _c_p, _c_p]),
     "fsr_dense_u_bytes": (_c_i64, [_c_i64, _c_i64]),
     "fsr_dense_u_build": (_c_int, [_c_p, _c_i64, _c_i64, _c_p, _c_p, _c_p, _c_p]),
     "fsr_filter_tc_workspace_bytes": (_c_i64, [_c_i64, _c_i64, _c_i64]),
@@ -198,6 +203,8 @@ class Context:
         self.topk_prune = True          # certified paths allowed (FSR_OPT_TOPK_PRUNE)
         self.online_path = os.environ.get("FSR_ONLINE_PATH", "tc")  # "tc" | "pruned" | "exact"
         self.last_online_path = None
+        # b = 1 fp32 on a sparse U~: "sell" (K9e, sliced-ELL stream) or "csr" (warp-per-row SpMV)
+        self.single_query_path = os.environ.get("FSR_SINGLE_QUERY_PATH", "sell")
 
     @classmethod
     def get(cls, device=None) -> "Context":
@@ -255,6 +262,10 @@ class Context:
         or the unpruned fp32 K9 (False).  Both return the same top-k."""
         self.check(self.lib.fsr_ctx_set_option(self.handle, 2, int(bool(on))))
         self.topk_prune = bool(on)
+
+    def set_topk_segments(self, segs: int):
+        """Segments per row of the exact top-k when b < #SMs (0 = automatic); results identical."""
+        self.check(self.lib.fsr_ctx_set_option(self.handle, 3, int(segs)))
 
     def set_online_path(self, path: str):
         """Preferred certified top-k path: "tc" (K9t tensor cores for b >= 128,

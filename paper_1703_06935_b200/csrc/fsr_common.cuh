@@ -40,6 +40,7 @@ struct fsr_ctx {
   int dense_path = 0;           // FSR_OPT_DENSE_PATH: 0 auto (tcgen05 for F32), 1 cuBLAS
   int spmm_panel_bytes = 0;     // FSR_OPT_SPMM_PANEL_BYTES: 0 wide row panels, else L2 panel width
   int topk_prune = 1;           // FSR_OPT_TOPK_PRUNE: certified fp16-pruned K9 for top-k-only fp32 batches
+  int topk_segments = 0;        // FSR_OPT_TOPK_SEGMENTS: 0 auto, else segments per row when b < #SMs
   int* dev_info = nullptr;
   double* host_stage = nullptr;  // pinned staging for small host reads
   size_t host_stage_bytes = 0;

@@ -105,6 +105,10 @@ int fsr_ctx_set_option(fsr_ctx* ctx, int option, int64_t value) {
       if (value < 0 || value > 1) return fsr::set_error(ctx, FSR_EINVAL, "topk prune must be 0 or 1");
       ctx->topk_prune = (int)value;
       return FSR_OK;
+    case FSR_OPT_TOPK_SEGMENTS:
+      if (value < 0 || value > 4096) return fsr::set_error(ctx, FSR_EINVAL, "topk segments must lie in [0, 4096]");
+      ctx->topk_segments = (int)value;
+      return FSR_OK;
     default:
       return fsr::set_error(ctx, FSR_EINVAL, "unknown option %d", option);
   }

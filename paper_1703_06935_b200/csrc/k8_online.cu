@@ -20,6 +20,7 @@
 #include <algorithm>
 #include <cstdlib>
 
+#include "k9e.cuh"
 #include "prune.cuh"
 #include "spmm.cuh"
 #include "topk.cuh"
@@ -100,55 +101,63 @@ __global__ void __launch_bounds__(256) project_smem_kernel(int64_t r, int64_t b,
       for (int64_t e = 0; e < ny; ++e) offs[e + 1] += offs[e];
     }
     __syncthreads();
-    fits = offs[ny] <= kProjCap;
   }
   if (fits) {
-    // flattened over the query's entries, 8 loads per thread in flight before
-    // their shared-memory stores (a row-by-row loop waited one DRAM latency per
-    // row: ~50 us for a 50-row query, the whole step at b = 1)
+    // windows of kProjCap entries, flattened over the query's rows, 8 loads
+    // per thread in flight before their shared-memory stores (a row-by-row
+    // loop waited one DRAM latency per row: ~50 us for a 50-row query, the
+    // whole step at b = 1).  Rows are consumed in query order across windows,
+    // so every z[c] sees its contributions in the reference's order.
     const int64_t tot = offs[ny];
-    for (int64_t t0 = threadIdx.x; t0 < tot; t0 += 8 * (int64_t)blockDim.x) {
-      int32_t cc[8];
-      T vv[8];
+    int64_t e_first = 0;  // first row with entries at or after the window start
+    for (int64_t w0 = 0; w0 < tot; w0 += kProjCap) {
+      const int64_t w1 = min(tot, w0 + (int64_t)kProjCap);
+      for (int64_t t0 = w0 + threadIdx.x; t0 < w1; t0 += 8 * (int64_t)blockDim.x) {
+        int32_t cc[8];
+        T vv[8];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int64_t t = t0 + (int64_t)u * blockDim.x;
-        cc[u] = 0;
-        vv[u] = T(0);
-        if (t < tot) {
-          int lo = 0, hi = (int)ny - 1;  // the row of entry t: largest e with offs[e] <= t
-          while (lo < hi) {
-            const int mid = (lo + hi + 1) >> 1;
-            if (offs[mid] <= t)
-              lo = mid;
-            else
-              hi = mid - 1;
+        for (int u = 0; u < 8; ++u) {
+          const int64_t t = t0 + (int64_t)u * blockDim.x;
+          cc[u] = 0;
+          vv[u] = T(0);
+          if (t < w1) {
+            int lo = 0, hi = (int)ny - 1;  // the row of entry t: largest e with offs[e] <= t
+            while (lo < hi) {
+              const int mid = (lo + hi + 1) >> 1;
+              if (offs[mid] <= t)
+                lo = mid;
+              else
+                hi = mid - 1;
+            }
+            FSR_DCHECK(lo >= 0 && lo < ny && offs[lo] <= t && t < offs[lo + 1]);
+            const int64_t src = starts[lo] + (t - offs[lo]);
+            cc[u] = u_indices[src];
+            vv[u] = u_values[src];
           }
-          FSR_DCHECK(lo >= 0 && lo < ny && offs[lo] <= t && t < offs[lo + 1]);
-          const int64_t src = starts[lo] + (t - offs[lo]);
-          cc[u] = u_indices[src];
-          vv[u] = u_values[src];
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int64_t t = t0 + (int64_t)u * blockDim.x;
+          if (t < w1) {
+            ec[t - w0] = cc[u];
+            ev[t - w0] = vv[u];
+          }
         }
       }
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int64_t t = t0 + (int64_t)u * blockDim.x;
-        if (t < tot) {
-          ec[t] = cc[u];
-          ev[t] = vv[u];
+      __syncthreads();
+      while (e_first < ny && offs[e_first + 1] <= w0) ++e_first;
+      for (int64_t e = e_first; e < ny && offs[e] < w1; ++e) {
+        const T v = y_val[y0 + e];
+        const int64_t a = max(offs[e], w0), z1 = min(offs[e + 1], w1);
+        for (int64_t t = a + threadIdx.x; t < z1; t += blockDim.x) {
+          const int32_t c = ec[t - w0];
+          FSR_DCHECK(c >= 0 && c < r);
+          z[c] = fsr::mul_add_rn(z[c], ev[t - w0], v);
         }
+        __syncthreads();
       }
     }
     __syncthreads();
-    for (int64_t e = 0; e < ny; ++e) {
-      const T v = y_val[y0 + e];
-      for (int64_t t = offs[e] + threadIdx.x; t < offs[e + 1]; t += blockDim.x) {
-        const int32_t c = ec[t];
-        FSR_DCHECK(c >= 0 && c < r);
-        z[c] = fsr::mul_add_rn(z[c], ev[t], v);
-      }
-      __syncthreads();
-    }
   } else {
     __syncthreads();
     for (int64_t e = 0; e < ny; ++e) {
@@ -354,7 +363,8 @@ template <typename T>
 int filter_impl(fsr_ctx* ctx, int64_t n, int64_t r, int u_sparse, const int64_t* u_indptr, const int32_t* u_indices,
                 const T* u_values, const T* u_dense, int64_t ldu, const T* w, const double* eta, int64_t b,
                 const int64_t* y_ptr, const int64_t* y_idx, const T* y_val, int copy_uncovered, void* workspace,
-                T* X, int64_t topk, int64_t* top_idx, T* top_val, const uint16_t* u_cols16 = nullptr) {
+                T* X, int64_t topk, int64_t* top_idx, T* top_val, const uint16_t* u_cols16 = nullptr,
+                const fsr::sell::View* sell = nullptr) {
   if constexpr (std::is_same<T, float>::value) {
     if (u_sparse && !X && topk > 0 && ctx->topk_prune && fsr::prune::applicable(n, b, topk) &&
         fsr::aligned(workspace, 256))
@@ -379,7 +389,15 @@ int filter_impl(fsr_ctx* ctx, int64_t n, int64_t r, int u_sparse, const int64_t*
   if (u_sparse) {
     if (b == 1) {
       fsr::StageTimer timer(ctx, FSR_STAGE_FILTER_SPMM);
-      if (u_cols16 && (size_t)r * sizeof(T) <= 160 * 1024)
+      bool done = false;
+      if constexpr (std::is_same<T, float>::value) {
+        if (sell) {  // K9e: sliced-ELL stream, sequential CSR-order sums (k9e.cuh)
+          FSR_TRY(fsr::sell::launch_spmv(ctx, n, *sell, u_indptr, u_values, Zs, r, Xout));
+          done = true;
+        }
+      }
+      if (done) {
+      } else if (u_cols16 && (size_t)r * sizeof(T) <= 160 * 1024)
         FSR_TRY((fsr::launch_spmv_smem<T, uint16_t>(ctx, n, u_indptr, u_cols16, u_values, Zs, r, Xout)));
       else if ((size_t)r * sizeof(T) <= 160 * 1024)
         FSR_TRY(fsr::launch_spmv_smem<T>(ctx, n, u_indptr, u_indices, u_values, Zs, r, Xout));
@@ -478,6 +496,34 @@ int fsr_filter_batch_u16(fsr_ctx* ctx, int dtype, int64_t n, int64_t r, int u_sp
   return filter_impl<float>(ctx, n, r, u_sparse, u_indptr, u_indices, (const float*)u_values, (const float*)u_dense,
                             ldu, (const float*)w, eta, b, y_ptr, y_idx, (const float*)y_val, copy_uncovered, workspace,
                             (float*)X, topk, top_idx, (float*)top_val, u_cols16);
+}
+
+int fsr_filter_single_sell(fsr_ctx* ctx, int64_t n, int64_t r, const int64_t* u_indptr, const int32_t* u_indices,
+                           const uint16_t* u_cols16, const float* u_values, const int32_t* sell_perm,
+                           const int32_t* sell_lens, const int64_t* sell_slice_ptr, const uint16_t* sell_cols,
+                           const float* sell_vals, int64_t n_long, const float* w, const double* eta,
+                           const int64_t* y_ptr, const int64_t* y_idx, const float* y_val, int copy_uncovered,
+                           void* workspace, float* X, int64_t topk, int64_t* top_idx, float* top_val) {
+  FSR_REQUIRE(ctx, n >= 1 && fsr::sell::applicable(r) && workspace && u_indptr && u_indices && u_cols16 && u_values,
+              "filter_single_sell: bad shape (r <= 16384, sparse U with its 16-bit columns)");
+  FSR_REQUIRE(ctx, sell_perm && sell_lens && sell_slice_ptr && sell_cols && sell_vals && n_long >= 0 &&
+                       n_long % 32 == 0,
+              "filter_single_sell: missing sliced-ELL layout (fsr_sell_plan / fsr_sell_pack)");
+  FSR_REQUIRE(ctx, topk >= 0 && topk <= fsr::topk::kCap / 4 && topk <= n, "filter_single_sell: topk must lie in [0, min(n, %d)]",
+              fsr::topk::kCap / 4);
+  FSR_REQUIRE(ctx, X || topk > 0, "filter_single_sell: nothing to output");
+  FSR_REQUIRE(ctx, topk == 0 || (top_idx && top_val), "filter_single_sell: missing top-k outputs");
+  fsr::sell::View V;
+  V.perm = sell_perm;
+  V.lens = sell_lens;
+  V.slice_ptr = sell_slice_ptr;
+  V.cols = sell_cols;
+  V.vals = sell_vals;
+  V.n_long = n_long;
+  V.csr_cols16 = u_cols16;
+  // b = 1 never takes the pruned branch of filter_impl (prune::applicable needs a wide batch)
+  return filter_impl<float>(ctx, n, r, 1, u_indptr, u_indices, u_values, nullptr, 0, w, eta, 1, y_ptr, y_idx, y_val,
+                            copy_uncovered, workspace, X, topk, top_idx, top_val, u_cols16, &V);
 }
 
 int fsr_topk_rows(fsr_ctx* ctx, int dtype, int64_t b, int64_t n, const void* X, int64_t ldx, int64_t topk,

@@ -1,0 +1,135 @@
+// K9e: the single-query (b = 1) K9 on a sliced-ELL copy of U~.
+//
+// Replaces, for one fp32 query, x = U~ zs of specrank.ranking.filter
+// (/root/reference/pkg/src/specrank/ranking.py:244-246).  The CSR SpMV spends
+// ~0.1 ms at C3 on per-row latency alone (10^6 rows of ~100 entries: row
+// pointers -> entries -> warp reduction, one dependent chain per row).  Here
+// the rows are sorted by length (descending) and cut into slices of 32 rows;
+// a slice stores its entries column-major ([j][lane], 16-bit column + fp32
+// value, padded to the slice's longest row), so one warp = one slice, one
+// thread = one row: every load is a coalesced 64 + 128 bytes, there is no row
+// pointer chase and no cross-lane reduction, and each x_i is the sequential
+// CSR-order fmaf chain -- bitwise the sum of the unpruned wide kernels
+// (spmm_rowpanel_T_kernel) and of K9t's exact re-score.  Rows longer than the
+// plan's long_len (0.1% of the rows, ~1% of the entries at C3) stay in CSR:
+// one warp per row loads 32 entries at a time and runs the same sequential
+// chain through shuffles.  Slices are issued longest first, so the hardware
+// CTA scheduler balances the skewed row lengths.
+#pragma once
+
+#include "fsr_common.cuh"
+
+namespace fsr {
+namespace sell {
+
+struct View {
+  const int32_t* perm = nullptr;       // sorted position -> row of U~ (n)
+  const int32_t* lens = nullptr;       // row length by sorted position (n)
+  const int64_t* slice_ptr = nullptr;  // entry offset of slice s (n_slices + 1); long slices are empty
+  const uint16_t* cols = nullptr;      // [slice][j][lane]
+  const float* vals = nullptr;
+  int64_t n_long = 0;                  // sorted positions [0, n_long) are long rows (a multiple of 32)
+  const uint16_t* csr_cols16 = nullptr;  // 16-bit copy of the CSR columns (long rows)
+};
+
+constexpr int kDepth = 8;
+
+__device__ __forceinline__ float ld_stream(const float* p) { return __ldcs(p); }
+__device__ __forceinline__ unsigned short ld_stream(const uint16_t* p) { return __ldcs(p); }
+
+// grid: ceil(n_long / 8) CTAs of long rows (a warp per row) followed by
+// ceil(n_short_slices / 8) CTAs of slices (a warp per slice).
+template <int DEPTH>
+__global__ void __launch_bounds__(256) sell_spmv_kernel(int64_t n, int64_t n_long, int64_t long_ctas,
+                                                        const int32_t* __restrict__ perm,
+                                                        const int32_t* __restrict__ lens,
+                                                        const int64_t* __restrict__ slice_ptr,
+                                                        const uint16_t* __restrict__ cols,
+                                                        const float* __restrict__ vals,
+                                                        const int64_t* __restrict__ indptr,
+                                                        const uint16_t* __restrict__ csr_cols,
+                                                        const float* __restrict__ csr_vals,
+                                                        const float* __restrict__ z, int64_t r,
+                                                        float* __restrict__ x) {
+  extern __shared__ __align__(16) float zs[];
+  for (int64_t c = threadIdx.x; c < r; c += blockDim.x) zs[c] = z[c];
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if ((int64_t)blockIdx.x < long_ctas) {
+    const int64_t pos = (int64_t)blockIdx.x * 8 + warp;
+    if (pos >= n_long || pos >= n) return;
+    const int64_t i = perm[pos];
+    const int64_t e0 = __ldg(indptr + i), e1 = __ldg(indptr + i + 1);
+    float acc = 0.f;
+    constexpr int U = 4;
+    for (int64_t base = e0; base < e1; base += 32 * U) {
+      float v[U], zz[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t e = base + 32 * u + lane;
+        const bool ok = e < e1;
+        const int c = ok ? (int)ld_stream(csr_cols + e) : 0;
+        FSR_DCHECK(c < r);
+        v[u] = ok ? ld_stream(csr_vals + e) : 0.f;
+        zz[u] = ok ? zs[c] : 0.f;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int cnt = (int)min((int64_t)32, e1 - (base + 32 * u));
+        for (int l = 0; l < cnt; ++l)
+          acc = fmaf(__shfl_sync(0xffffffffu, v[u], l), __shfl_sync(0xffffffffu, zz[u], l), acc);
+      }
+    }
+    if (!lane) x[i] = acc;
+    return;
+  }
+  const int64_t s = (n_long >> 5) + ((int64_t)blockIdx.x - long_ctas) * 8 + warp;
+  const int64_t pos = s * 32 + lane;
+  if (s * 32 >= n) return;
+  const int64_t p0 = __ldg(slice_ptr + s);
+  const int width = (int)((__ldg(slice_ptr + s + 1) - p0) >> 5);
+  const int my_len = pos < n ? __ldg(lens + pos) : 0;
+  const uint16_t* cp = cols + p0 + lane;
+  const float* vp = vals + p0 + lane;
+  float acc = 0.f;
+  int j = 0;
+  for (; j + DEPTH <= width; j += DEPTH) {
+    int c[DEPTH];
+    float v[DEPTH];
+#pragma unroll
+    for (int u = 0; u < DEPTH; ++u) {
+      c[u] = (int)ld_stream(cp + (int64_t)(j + u) * 32);
+      v[u] = ld_stream(vp + (int64_t)(j + u) * 32);
+    }
+#pragma unroll
+    for (int u = 0; u < DEPTH; ++u) {
+      FSR_DCHECK(c[u] < r);
+      if (j + u < my_len) acc = fmaf(v[u], zs[c[u]], acc);
+    }
+  }
+  for (; j < width; ++j) {
+    const int c = (int)ld_stream(cp + (int64_t)j * 32);
+    const float v = ld_stream(vp + (int64_t)j * 32);
+    if (j < my_len) acc = fmaf(v, zs[c], acc);
+  }
+  if (pos < n) x[__ldg(perm + pos)] = acc;
+}
+
+inline bool applicable(int64_t r) { return r >= 1 && r <= 16384; }
+
+inline int launch_spmv(fsr_ctx* ctx, int64_t n, const View& V, const int64_t* indptr, const float* csr_vals,
+                       const float* z, int64_t r, float* x) {
+  const size_t smem = (size_t)r * sizeof(float);
+  FSR_TRY(fsr::ensure_smem(ctx, sell_spmv_kernel<kDepth>, smem));
+  const int64_t long_ctas = ceil_div(std::min(V.n_long, n), 8);
+  const int64_t short_slices = ceil_div(n, 32) - (V.n_long >> 5);
+  const int64_t grid = long_ctas + ceil_div(std::max<int64_t>(short_slices, 0), 8);
+  if (grid <= 0) return FSR_OK;
+  sell_spmv_kernel<kDepth><<<(unsigned)grid, 256, smem, ctx->stream>>>(n, V.n_long, long_ctas, V.perm, V.lens, V.slice_ptr,
+                                                               V.cols, V.vals, indptr, V.csr_cols16, csr_vals, z, r,
+                                                               x);
+  return launched(ctx, "sell_spmv_kernel");
+}
+
+}  // namespace sell
+}  // namespace fsr

@@ -365,6 +365,7 @@ int launch(fsr_ctx* ctx, int64_t b, int64_t n, const T* X, int64_t ldx, int64_t 
   int segs = 1;
   if (b < ctx->num_sms) {
     segs = (int)std::min<int64_t>(ceil_div(2 * ctx->num_sms, b), std::max<int64_t>(1, n / (8 * K)));
+    if (ctx->topk_segments > 0) segs = (int)std::min<int64_t>(ctx->topk_segments, std::max<int64_t>(1, n / (8 * K)));
     segs = std::max(segs, 1);
   }
   if (segs == 1) {

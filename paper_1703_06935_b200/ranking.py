@@ -279,8 +279,20 @@ def filter_device(dec: SpectralDecomposition, h: TransferFunction, queries: Devi
     if workspace is None or workspace.numel() < need:
         workspace = torch.empty(need, dtype=torch.uint8, device=dev)
     ctx.last_online_path = "pruned" if path != "exact" and topk_pruned(n, b, topk, dt) else "exact"
+    if dec.is_sparse and b == 1 and dt == torch.float32 and ctx.single_query_path == "sell":
+        # one fp32 query: K9e streams the sliced-ELL copy of U~ (6 bytes per entry, thread per row)
+        sell = sell_layout(dec)
+        if sell is not None:
+            perm, lens, slice_ptr, scols, svals, n_long = sell
+            ctx.call("filter_single_sell", n, r, N.ptr(U.indptr), N.ptr(U.indices), N.ptr(u16_columns(dec)),
+                     N.ptr(U.values), N.ptr(perm), N.ptr(lens), N.ptr(slice_ptr), N.ptr(scols), N.ptr(svals), n_long,
+                     N.ptr(w), N.ptr(dec.eta_device), N.ptr(queries.y_ptr), N.ptr(queries.y_idx),
+                     N.ptr(queries.y_val), int(bool(copy_uncovered)), N.ptr(workspace),
+                     N.ptr(res.X if want_x else None), int(topk), N.ptr(res.top_idx if topk else None),
+                     N.ptr(res.top_val if topk else None))
+            return res
     if dec.is_sparse:
-        # a single fp32 query streams U~ with 16-bit column indices (6 instead of 8 bytes per entry)
+        # without the sliced-ELL copy a single fp32 query streams the CSR with 16-bit column indices
         c16 = u16_columns(dec) if b == 1 and dt == torch.float32 and r <= 65536 else None
         uargs = (1, N.ptr(U.indptr), N.ptr(U.indices), N.ptr(c16), N.ptr(U.values), N.ptr(None), 0)
     else:
@@ -395,6 +407,45 @@ def stream_layout(dec):
     ctx.call("stream_u_build", dec.n, dec.r, U.nnz, N.ptr(U.indptr), N.ptr(U.indices), N.ptr(U.values), N.ptr(buf))
     dec._stream_u = buf
     return buf
+
+
+SELL_LONG_ROW = 512   # rows of U~ longer than this stay in CSR (a warp per row)
+SELL_MAX_RANK = 16384  # z must fit the SpMV's shared memory (fsr::sell::applicable)
+
+
+def sell_layout(dec):
+    """The sliced-ELL copy of U~ that the single-query filter streams (K9e,
+    csrc/k9e.cuh): rows sorted by length, 32-row slices stored column-major
+    with 16-bit columns (fsr_sell_plan / fsr_sell_pack).  Built once per
+    decomposition and cached on it; None when the layout does not apply
+    (dense or fp64 U, r > 16384, a U~ without entries)."""
+    import ctypes
+    import torch
+
+    cached = dec.__dict__.get("_sell_u", False)
+    if cached is not False:
+        return cached
+    dec._sell_u = None
+    if not dec.is_sparse or dec.dtype != torch.float32 or dec.r > SELL_MAX_RANK or dec.U_device.nnz == 0:
+        return None
+    U = dec.U_device
+    dev = U.indices.device
+    ctx = N.Context.get(dev)
+    n = dec.n
+    ws = torch.empty(int(ctx.lib.fsr_sell_plan_workspace_bytes(n)), dtype=torch.uint8, device=dev)
+    perm = torch.empty(n, dtype=torch.int32, device=dev)
+    lens = torch.empty(n, dtype=torch.int32, device=dev)
+    slice_ptr = torch.empty((n + 31) // 32 + 1, dtype=torch.int64, device=dev)
+    n_long, total = ctypes.c_int64(0), ctypes.c_int64(0)
+    ctx.call("sell_plan", n, N.ptr(U.indptr), SELL_LONG_ROW, N.ptr(perm), N.ptr(lens), N.ptr(slice_ptr), N.ptr(ws),
+             ctypes.byref(n_long), ctypes.byref(total))
+    del ws
+    cols = torch.empty(max(1, total.value), dtype=torch.int16, device=dev)
+    vals = torch.empty(max(1, total.value), dtype=torch.float32, device=dev)
+    ctx.call("sell_pack", n, N.ptr(U.indptr), N.ptr(U.indices), N.ptr(U.values), N.ptr(perm), N.ptr(slice_ptr),
+             N.ptr(cols), N.ptr(vals))
+    dec._sell_u = (perm, lens, slice_ptr, cols, vals, int(n_long.value))
+    return dec._sell_u
 
 
 def last_fallback_count(workspace, dec, b: int, ctx=None) -> int:

@@ -360,8 +360,12 @@ def test_single_query_u16_columns_bitwise():
     y = ranking.ObservationVector(n, np.array([3, 999, 40_000]), np.array([1.0, 0.5, 0.2]), cap=3)
     q = ranking.DeviceQueries(ranking.QueryBatch.from_vectors([y]), dec.dtype, dec.eta_device.device)
     h = ranking.h_alpha(0.99)
-    x16 = ranking.filter_device(dec, h, q).X.clone()  # the Python path: 16-bit columns for b = 1
     ctx = N.Context.get()
+    ctx.single_query_path = "csr"  # the CSR SpMV with 16-bit columns (the default is K9e, below)
+    try:
+        x16 = ranking.filter_device(dec, h, q).X.clone()
+    finally:
+        ctx.single_query_path = "sell"
     Ud = dec.U_device
     w = ranking._weights_device(dec, h)
     ws = torch.empty(int(ctx.lib.fsr_filter_workspace_bytes(N.F32, n, r, 1, 1)), dtype=torch.uint8, device="cuda")
@@ -371,3 +375,73 @@ def test_single_query_u16_columns_bitwise():
              N.ptr(x32), 0, N.ptr(None), N.ptr(None))
     torch.cuda.synchronize()
     assert torch.equal(x16.view(torch.int32), x32.view(torch.int32))
+
+
+# ------------------------------------------- K9e: sliced-ELL single query ---
+def _sequential_x(dec, h, y, n):
+    """Row 0 of the unpruned wide-batch K9 (spmm_rowpanel_T_kernel: every x_i
+    the sequential CSR-order fmaf chain) for a batch of 256 copies of y."""
+    q = ranking.DeviceQueries(ranking.QueryBatch.from_vectors([y] * 256), dec.dtype, dec.eta_device.device)
+    return ranking.filter_device(dec, h, q).X[0].clone()
+
+
+@pytest.mark.parametrize("n,r,long_row", [(3001, 700, 512), (3001, 700, 40), (31, 64, 512), (4096, 300, 1),
+                                          (50_000, 700, 512)])
+def test_single_query_sell_bitwise_sequential(n, r, long_row, monkeypatch):
+    """K9e (b = 1 on the sliced-ELL copy of U~) returns, bit for bit, the
+    sequential-order sums of the wide-batch kernel: skewed rows, empty rows,
+    rows on the CSR long-row path (long_row small: most rows; 1: every row),
+    n not a multiple of 32, n < 32; top-k of the same call = exact rank order."""
+    monkeypatch.setattr(ranking, "SELL_LONG_ROW", long_row)
+    host = _skewed_sparse_dec(n, r, 5) if n != 50_000 else _skewed_sparse_dec(n, r, 6)
+    dec = spectral.SpectralDecomposition.from_host(host, dtype="float32")
+    h = ranking.h_alpha(0.99)
+    ctx = N.Context.get()
+    assert ctx.single_query_path == "sell"
+    lay = ranking.sell_layout(dec)
+    assert lay is not None
+    perm, lens, slice_ptr, cols, vals, n_long = lay
+    rl = np.diff(host.U.indptr)
+    np.testing.assert_array_equal(np.sort(perm.cpu().numpy()), np.arange(n))
+    np.testing.assert_array_equal(lens.cpu().numpy(), rl[perm.cpu().numpy()])
+    assert np.all(np.diff(lens.cpu().numpy()) <= 0) and n_long % 32 == 0
+    assert n_long >= np.count_nonzero(rl > long_row)
+    for yi in ([5], [0, 7, 100, n - 1], [20, 21]):
+        y = ranking.ObservationVector(n, np.array(yi), np.linspace(1.0, 0.5, len(yi)), cap=len(yi))
+        q = ranking.DeviceQueries(ranking.QueryBatch.from_vectors([y]), dec.dtype, dec.eta_device.device)
+        K = min(100, n)
+        res = ranking.filter_device(dec, h, q, topk=K)
+        seq = _sequential_x(dec, h, y, n)
+        assert torch.equal(res.X[0].view(torch.int32), seq.view(torch.int32)), yi
+        x = res.X[0].cpu().numpy()
+        np.testing.assert_array_equal(res.top_idx[0].cpu().numpy(), O.rank(x)[:K])
+        np.testing.assert_array_equal(res.top_val[0].cpu().numpy(), x[O.rank(x)[:K]])
+        w = O.transfer_values(O.h_alpha(0.99), host.eigenvalues)
+        ref = O.filter_scores(host.U, host.eigenvalues, host.eta, w, y.indices, y.values)
+        assert np.linalg.norm(x - ref) <= 1e-5 * max(np.linalg.norm(ref), 1e-30)
+
+
+def test_single_query_sell_graph_replay_and_csr_agree():
+    """FilterGraph at b = 1 runs K9e; its top-100 equals the eager call's and the
+    CSR single-query path's scores agree to rounding (another summation order)."""
+    n, r = 50_000, 700
+    host = _skewed_sparse_dec(n, r, 9)
+    dec = spectral.SpectralDecomposition.from_host(host, dtype="float32")
+    h = ranking.h_alpha(0.9)
+    y = ranking.ObservationVector(n, np.array([3, 999, 40_000]), np.array([1.0, 0.5, 0.2]), cap=3)
+    qb = ranking.QueryBatch.from_vectors([y])
+    q = ranking.DeviceQueries(qb, dec.dtype, dec.eta_device.device)
+    eager = ranking.filter_device(dec, h, q, topk=100)
+    fg = ranking.FilterGraph(dec, h, b=1, nnz_cap=8, topk=100)
+    res = fg.run(qb)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(res.top_idx[0].cpu().numpy(), eager.top_idx[0].cpu().numpy())
+    np.testing.assert_array_equal(res.top_val[0].cpu().numpy(), eager.top_val[0].cpu().numpy())
+    ctx = N.Context.get()
+    ctx.single_query_path = "csr"
+    try:
+        xc = ranking.filter_device(dec, h, q).X[0].cpu().numpy()
+    finally:
+        ctx.single_query_path = "sell"
+    xs = eager.X[0].cpu().numpy()
+    assert np.linalg.norm(xc - xs) <= 2e-6 * np.linalg.norm(xs)
