@@ -41,6 +41,7 @@ struct fsr_ctx {
   int spmm_panel_bytes = 0;     // FSR_OPT_SPMM_PANEL_BYTES: 0 wide row panels, else L2 panel width
   int topk_prune = 1;           // FSR_OPT_TOPK_PRUNE: certified fp16-pruned K9 for top-k-only fp32 batches
   int topk_segments = 0;        // FSR_OPT_TOPK_SEGMENTS: 0 auto, else segments per row when b < #SMs
+  void* topk_state = nullptr;   // persistent, self-cleaning state of the few-row top-k (topk.cuh)
   int* dev_info = nullptr;
   double* host_stage = nullptr;  // pinned staging for small host reads
   size_t host_stage_bytes = 0;

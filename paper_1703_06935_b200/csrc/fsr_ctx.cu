@@ -48,6 +48,7 @@ void fsr_ctx_destroy(fsr_ctx* ctx) {
   else cudaDeviceSynchronize();
   if (ctx->scratch) cudaFree(ctx->scratch);
   if (ctx->scratch_aux) cudaFree(ctx->scratch_aux);
+  if (ctx->topk_state) cudaFree(ctx->topk_state);
   if (ctx->dev_info) cudaFree(ctx->dev_info);
   if (ctx->host_stage) cudaFreeHost(ctx->host_stage);
   fold_pending(ctx);

@@ -357,8 +357,158 @@ __global__ void __launch_bounds__(kThreads) select_kernel(const T* __restrict__ 
   }
 }
 
+// ---- few rows (b < #SMs), fp32: two grid-wide passes -------------------------
+// The segmented path above selects K per segment and merges b * segs * K
+// candidates in one CTA per row (b = 1, n = 1e6: 22 + 35 us).  Here every CTA
+// of a row adds its segment to ONE 12-bit key histogram of the row
+// (hist_kernel), and in the second pass reads that histogram, finds the bin
+// of the K-th key and appends its segment's keys at or above that bin to the
+// row's candidate list; the row's last CTA to finish sorts the candidates by
+// (key desc, index asc) and writes the top K.  More than kCap candidates
+// (masses of keys sharing 12 bits, e.g. a row of zeros) fall back to
+// select_exact over the whole row in that last CTA.  The state (histograms,
+// counters, candidate lists) lives in the context and is left zeroed by the
+// last CTA, so a call needs no memset.
+struct FewRows {
+  unsigned* hist;    // rows x 2^kHistBits
+  unsigned* count;   // rows
+  unsigned* ticket;  // rows
+  uint64_t* ckey;    // rows x kCap
+  int64_t* cidx;     // rows x kCap
+};
+
+inline size_t few_rows_bytes(int rows) {
+  return (size_t)rows * ((size_t)(1 << kHistBits) * 4 + 8 + (size_t)kCap * 16) + 256;
+}
+
+inline int few_rows_state(fsr_ctx* ctx, FewRows* st) {
+  const int rows = ctx->num_sms;
+  if (!ctx->topk_state) {
+    const size_t bytes = few_rows_bytes(rows);
+    cudaError_t e = cudaMalloc(&ctx->topk_state, bytes);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      ctx->topk_state = nullptr;
+      return set_error(ctx, FSR_ENOMEM, "top-k state alloc of %zu bytes failed", bytes);
+    }
+    e = cudaMemsetAsync(ctx->topk_state, 0, bytes, ctx->stream);
+    if (e != cudaSuccess) return cuda_status(ctx, e, "top-k state memset");
+  }
+  char* p = (char*)ctx->topk_state;
+  st->ckey = (uint64_t*)p;
+  p += (size_t)rows * kCap * 8;
+  st->cidx = (int64_t*)p;
+  p += (size_t)rows * kCap * 8;
+  st->hist = (unsigned*)p;
+  p += (size_t)rows * (1 << kHistBits) * 4;
+  st->count = (unsigned*)p;
+  st->ticket = st->count + rows;
+  return FSR_OK;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kThreads) few_rows_hist_kernel(const T* __restrict__ X, int64_t ld, int64_t n,
+                                                                 int64_t seg, unsigned* __restrict__ ghist) {
+  constexpr int nb = 1 << kHistBits;
+  __shared__ unsigned h[nb];
+  for (int t = threadIdx.x; t < nb; t += blockDim.x) h[t] = 0;
+  __syncthreads();
+  const int64_t q = blockIdx.y, b0 = (int64_t)blockIdx.x * seg, b1 = min(n, b0 + seg);
+  if (b1 > b0)
+    for_each_vec<T, 4>(X + q * ld + b0, b1 - b0,
+                       [&](int64_t, T x) { atomicAdd(&h[order_key(x) >> (sizeof(T) * 8 - kHistBits)], 1u); });
+  __syncthreads();
+  for (int t = threadIdx.x; t < nb; t += blockDim.x)
+    if (h[t]) atomicAdd(&ghist[q * nb + t], h[t]);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kThreads) few_rows_select_kernel(const T* __restrict__ X, int64_t ld, int64_t n,
+                                                                   int64_t seg, int64_t K, FewRows st,
+                                                                   T* __restrict__ out_val,
+                                                                   int64_t* __restrict__ out_idx) {
+  constexpr int nb = 1 << kHistBits;
+  constexpr int KB = sizeof(T) * 8;
+  extern __shared__ __align__(16) unsigned char dyn[];
+  uint64_t* ckey = (uint64_t*)dyn;
+  int64_t* cidx = (int64_t*)(ckey + kCap);
+  __shared__ Shared sh;
+  const int64_t q = blockIdx.y, b0 = (int64_t)blockIdx.x * seg, b1 = min(n, b0 + seg);
+  unsigned* ghist = st.hist + q * nb;
+  for (int t = threadIdx.x; t < nb; t += blockDim.x) sh.hist[t] = __ldcg(ghist + t);
+  __syncthreads();
+  find_bin(sh, nb, (unsigned long long)K);
+  const uint64_t bin = sh.found_bin;
+  uint64_t* gkey = st.ckey + q * kCap;
+  int64_t* gidx = st.cidx + q * kCap;
+  if (b1 > b0)
+    for_each_vec<T, 4>(X + q * ld + b0, b1 - b0, [&](int64_t e, T x) {
+      const uint64_t k = order_key(x);
+      if ((k >> (KB - kHistBits)) >= bin) {
+        const unsigned slot = atomicAdd(&st.count[q], 1u);
+        if (slot < (unsigned)kCap) {
+          gkey[slot] = k;
+          gidx[slot] = b0 + e;
+        }
+      }
+    });
+  __threadfence();
+  __syncthreads();
+  if (!threadIdx.x) sh.count = atomicAdd(&st.ticket[q], 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!sh.count) return;
+  __threadfence();
+  const unsigned c = __ldcg(&st.count[q]);
+  __syncthreads();
+  if (c <= (unsigned)kCap) {
+    for (unsigned t = threadIdx.x; t < c; t += blockDim.x) {
+      ckey[t] = __ldcg(gkey + t);
+      cidx[t] = __ldcg(gidx + t);
+    }
+    __syncthreads();
+    bitonic_sort(ckey, cidx, (int)c);
+  } else {
+    Range<T, false> R{X + q * ld, nullptr, n, 0};
+    select_exact<T, false>(R, K, sh, ckey, cidx);
+  }
+  __syncthreads();
+  for (int64_t m = threadIdx.x; m < K; m += blockDim.x) {
+    const int64_t i = cidx[m];
+    out_idx[q * K + m] = i;
+    out_val[q * K + m] = X[q * ld + i];
+  }
+  for (int t = threadIdx.x; t < nb; t += blockDim.x) ghist[t] = 0;
+  if (!threadIdx.x) {
+    st.count[q] = 0;
+    st.ticket[q] = 0;
+  }
+}
+
+inline bool few_rows_applicable(fsr_ctx* ctx, int64_t b, int64_t n, int64_t K) {
+  return ctx->topk_segments == 0 && b < ctx->num_sms && n >= 65536 && K <= n && K <= kCap / 4;
+}
+
+inline int launch_few_rows(fsr_ctx* ctx, int64_t b, int64_t n, const float* X, int64_t ldx, int64_t K, int64_t* top_idx,
+                           float* top_val) {
+  FewRows st;
+  FSR_TRY(few_rows_state(ctx, &st));
+  const size_t smem = (size_t)kCap * 16;
+  FSR_TRY(ensure_smem(ctx, few_rows_select_kernel<float>, smem));
+  int64_t segs = std::max<int64_t>(1, std::min<int64_t>(ceil_div(2 * ctx->num_sms, b), n / 4096));
+  const int64_t seg = ceil_div(ceil_div(n, segs), 1024) * 1024;  // 16-byte aligned segment starts
+  segs = ceil_div(n, seg);
+  dim3 grid((unsigned)segs, (unsigned)b);
+  few_rows_hist_kernel<float><<<grid, kThreads, 0, ctx->stream>>>(X, ldx, n, seg, st.hist);
+  FSR_TRY(launched(ctx, "topk_few_rows_hist_kernel"));
+  few_rows_select_kernel<float><<<grid, kThreads, smem, ctx->stream>>>(X, ldx, n, seg, K, st, top_val, top_idx);
+  return launched(ctx, "topk_few_rows_select_kernel");
+}
+
 template <typename T>
 int launch(fsr_ctx* ctx, int64_t b, int64_t n, const T* X, int64_t ldx, int64_t K, int64_t* top_idx, T* top_val) {
+  if constexpr (std::is_same<T, float>::value) {
+    if (few_rows_applicable(ctx, b, n, K)) return launch_few_rows(ctx, b, n, X, ldx, K, top_idx, top_val);
+  }
   const size_t smem = (size_t)kCap * 16;
   FSR_TRY(ensure_smem(ctx, select_kernel<T, false>, smem));
   FSR_TRY(ensure_smem(ctx, select_kernel<T, true>, smem));

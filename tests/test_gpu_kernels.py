@@ -302,6 +302,45 @@ def test_topk_matches_rank(dtype):
         np.testing.assert_array_equal(idx[j].cpu().numpy(), O.rank(Xr[j])[:K])
 
 
+@pytest.mark.parametrize("b,n,K", [(1, 1_000_003, 100), (3, 200_000, 100), (7, 65_536, 1), (147, 70_001, 17),
+                                   (2, 150_000, 1024)])
+def test_topk_few_rows_histogram_path(b, n, K):
+    """b < #SMs, n >= 65536, fp32: the two-pass histogram top-k (topk.cuh
+    few_rows_*) equals the reference rank order and the segmented path's
+    output bit for bit -- ties (rounded values, a row of zeros with more than
+    kCap candidates -> the in-kernel exact fallback), -0.0, rows whose length
+    is not a multiple of the vector width; the self-cleaning state survives
+    repeated calls."""
+    rng = np.random.default_rng(b * 1000 + K)
+    X = rng.standard_normal((b, n)).astype(np.float32)
+    X[0] = np.round(X[0], 1)
+    if b > 1:
+        X[1] = 0.0
+        X[1, [5, 70, 9000]] = [1.0, -2.0, 1.0]
+    if b > 2:
+        X[2, : n // 2] = -0.0
+        X[2, n // 2:] = np.abs(X[2, n // 2:]) * 1e-30  # one key bin holds half the row
+    Xd = torch.as_tensor(X).cuda()
+    ctx = N.Context.get()
+    out = []
+    for segs in (0, 0, 16):  # histogram path twice (state reuse), then the segmented path
+        ctx.set_topk_segments(segs)
+        idx = torch.empty(b, K, dtype=torch.int64, device="cuda")
+        val = torch.empty(b, K, dtype=torch.float32, device="cuda")
+        try:
+            ctx.call("topk_rows", N.F32, b, n, N.ptr(Xd), n, K, N.ptr(idx), N.ptr(val))
+        finally:
+            ctx.set_topk_segments(0)
+        out.append((idx.cpu().numpy(), val.cpu().numpy()))
+    for j in range(b):
+        order = O.rank(X[j].astype(np.float64))[:K]
+        np.testing.assert_array_equal(out[0][0][j], order)
+        np.testing.assert_array_equal(out[0][1][j].view(np.int32), X[j][order].view(np.int32))
+    for o in out[1:]:
+        np.testing.assert_array_equal(o[0], out[0][0])
+        np.testing.assert_array_equal(o[1].view(np.int32), out[0][1].view(np.int32))
+
+
 # ------------------------------------------------------- K9 at b = 1 -------
 def _skewed_sparse_dec(n, r, seed):
     """Sparse U with skewed rows for the b = 1 SpMV (K9): empty rows, runs of
@@ -406,7 +445,7 @@ def test_single_query_sell_bitwise_sequential(n, r, long_row, monkeypatch):
     np.testing.assert_array_equal(lens.cpu().numpy(), rl[perm.cpu().numpy()])
     assert np.all(np.diff(lens.cpu().numpy()) <= 0) and n_long % 32 == 0
     assert n_long >= np.count_nonzero(rl > long_row)
-    for yi in ([5], [0, 7, 100, n - 1], [20, 21]):
+    for yi in ([5], [0, 7, min(100, n - 2), n - 1], [20, 21]):
         y = ranking.ObservationVector(n, np.array(yi), np.linspace(1.0, 0.5, len(yi)), cap=len(yi))
         q = ranking.DeviceQueries(ranking.QueryBatch.from_vectors([y]), dec.dtype, dec.eta_device.device)
         K = min(100, n)
