@@ -62,6 +62,9 @@ def parse_args():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--skip-e2e", action="store_true")
     ap.add_argument("--no-sweep", action="store_true", help="skip the C5 online sweep")
+    ap.add_argument("--sweep-settle-s", type=float, default=0.5,
+                    help="idle time before each small-batch (b <= 64) sweep point, so a latency point is not "
+                         "measured at the clocks the power cap left behind after the wide-batch points")
     ap.add_argument("--no-parity", action="store_true", help="skip the full-size parity checks")
     ap.add_argument("--no-offline-warmup", action="store_true",
                     help="time the offline decomposition on its first (cold) run")
@@ -555,7 +558,8 @@ def online_parity(sdec, Uh, eta, queries, alpha, K, device, nq=8):
             "topk_identical_order": same, "oracle": "oracle/fsr_oracle.py filter_scores + rank (scipy CSR f64)"}
 
 
-def online_sweep(dec, sdec_default, density_default, cfg, n, r, queries, device, ctx, es, steps=3, warmup=2):
+def online_sweep(dec, sdec_default, density_default, cfg, n, r, queries, device, ctx, es, steps=3, warmup=2,
+                 settle_s=0.0):
     """BASELINE C5: batches {1, 64, 1024, 10000} x U~ density {1, 2, 5}% with h_alpha(0.99),
     plus h_alpha(0.9) and heat exp(-10(1-x)) at 2% / b=1024.  Device-resident, top-100."""
     import torch
@@ -584,7 +588,10 @@ def online_sweep(dec, sdec_default, density_default, cfg, n, r, queries, device,
                 if name != "h_alpha(0.99)" and b != 1024:
                     continue
                 res = ranking.FilterResult()
-                for _ in range(warmup):
+                if b <= 64 and settle_s > 0:
+                    torch.cuda.synchronize()
+                    time.sleep(settle_s)
+                for _ in range(warmup if b > 64 else max(warmup, 5)):
                     ranking.filter_device(sd, h, dq, topk=100, want_x=False, out=res)
                 torch.cuda.synchronize()
                 ctx.stage_reset()
@@ -618,7 +625,8 @@ def online_sweep(dec, sdec_default, density_default, cfg, n, r, queries, device,
                     row["k9_algorithmic_gbs"] = k9_bytes / (k9_ms / max(k9_cnt, 1) * 1e-3) / 1e9
                 row["useful_fp32_tflops"] = 2.0 * kept * b / (k9_ms / max(k9_cnt, 1) * 1e-3) / 1e12
                 if b <= 64 and name == "h_alpha(0.99)":
-                    row.update(graph_sweep_row(sd, h, qb, b, nsteps, warmup, flush, ctx))
+                    row.update(graph_sweep_row(sd, h, qb, b, nsteps, max(warmup, 5), flush, ctx))
+                    row["settle_s"] = settle_s
                 out.append(row)
                 del res
             del dq
@@ -995,7 +1003,8 @@ def run_fsr(args, cfg, n, rank, world, local_rank):
     sweep = None
     if world == 1 and not args.no_sweep:
         del ws, res
-        sweep = online_sweep(dec, sdec, density, cfg, n, r, all_queries, device, ctx, es)
+        sweep = online_sweep(dec, sdec, density, cfg, n, r, all_queries, device, ctx, es,
+                             settle_s=args.sweep_settle_s)
         del dec
 
     # ---------------- CPU baseline (rank 0, N=1) -----------------------------

@@ -411,6 +411,14 @@ def stream_layout(dec):
 
 SELL_LONG_ROW = 512   # rows of U~ longer than this stay in CSR (a warp per row)
 SELL_MAX_RANK = 16384  # z must fit the SpMV's shared memory (fsr::sell::applicable)
+# The long rows' sequential chains run through warp shuffles (3 instructions
+# per entry per warp), so K9e pays only while they hold a small share of the
+# entries: C3 at 1-2% (1% of the entries in rows over 512) 0.19 -> 0.12 ms, at
+# 5% (a third of the entries) 0.35 -> 0.9 ms.  Measured and not kept for the
+# long rows: 32 or 8 rows per warp parked in shared memory with a thread per
+# row's chain, on a side stream (one DRAM latency per 32/128 entries of a
+# row: 0.55 / 0.21 ms at 2%, profiles/r02/k9e_long_rows.md).
+SELL_MAX_LONG_SHARE = 0.03
 
 
 def sell_layout(dec):
@@ -418,7 +426,8 @@ def sell_layout(dec):
     csrc/k9e.cuh): rows sorted by length, 32-row slices stored column-major
     with 16-bit columns (fsr_sell_plan / fsr_sell_pack).  Built once per
     decomposition and cached on it; None when the layout does not apply
-    (dense or fp64 U, r > 16384, a U~ without entries)."""
+    (dense or fp64 U, r > 16384, a U~ without entries, or rows longer than
+    SELL_LONG_ROW holding more than SELL_MAX_LONG_SHARE of the entries)."""
     import ctypes
     import torch
 
@@ -430,6 +439,11 @@ def sell_layout(dec):
         return None
     U = dec.U_device
     dev = U.indices.device
+    row_len = U.indptr[1:] - U.indptr[:-1]
+    long_share = float(row_len[row_len > SELL_LONG_ROW].sum()) / U.nnz
+    del row_len
+    if long_share > SELL_MAX_LONG_SHARE:
+        return None  # the CSR single-query kernel serves this U~
     ctx = N.Context.get(dev)
     n = dec.n
     ws = torch.empty(int(ctx.lib.fsr_sell_plan_workspace_bytes(n)), dtype=torch.uint8, device=dev)

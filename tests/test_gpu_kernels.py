@@ -432,6 +432,7 @@ def test_single_query_sell_bitwise_sequential(n, r, long_row, monkeypatch):
     rows on the CSR long-row path (long_row small: most rows; 1: every row),
     n not a multiple of 32, n < 32; top-k of the same call = exact rank order."""
     monkeypatch.setattr(ranking, "SELL_LONG_ROW", long_row)
+    monkeypatch.setattr(ranking, "SELL_MAX_LONG_SHARE", 1.0)  # exercise the long-row path whatever its share
     host = _skewed_sparse_dec(n, r, 5) if n != 50_000 else _skewed_sparse_dec(n, r, 6)
     dec = spectral.SpectralDecomposition.from_host(host, dtype="float32")
     h = ranking.h_alpha(0.99)
@@ -458,6 +459,23 @@ def test_single_query_sell_bitwise_sequential(n, r, long_row, monkeypatch):
         w = O.transfer_values(O.h_alpha(0.99), host.eigenvalues)
         ref = O.filter_scores(host.U, host.eigenvalues, host.eta, w, y.indices, y.values)
         assert np.linalg.norm(x - ref) <= 1e-5 * max(np.linalg.norm(ref), 1e-30)
+
+
+def test_single_query_sell_policy_long_share(monkeypatch):
+    """A U~ whose long rows hold more than SELL_MAX_LONG_SHARE of the entries
+    keeps the CSR single-query kernel (sell_layout -> None); scores stay within
+    the fp32 tolerance of the oracle."""
+    monkeypatch.setattr(ranking, "SELL_LONG_ROW", 40)
+    n, r = 3001, 700
+    host = _skewed_sparse_dec(n, r, 5)
+    dec = spectral.SpectralDecomposition.from_host(host, dtype="float32")
+    assert ranking.sell_layout(dec) is None
+    h = ranking.h_alpha(0.99)
+    y = ranking.ObservationVector(n, np.array([0, 7, 100]), np.array([1.0, 0.5, 0.2]), cap=3)
+    x = ranking.filter_batch(dec, h, [y])[0]
+    w = O.transfer_values(O.h_alpha(0.99), host.eigenvalues)
+    ref = O.filter_scores(host.U, host.eigenvalues, host.eta, w, y.indices, y.values)
+    assert np.linalg.norm(x - ref) <= 1e-5 * np.linalg.norm(ref)
 
 
 def test_single_query_sell_graph_replay_and_csr_agree():

@@ -1,0 +1,9 @@
+# K9e long-row kernel: tests, long-row threshold sweep at 2% / 5%, bench sweep with settle
+set -x
+O=gpurun_out/r02af; mkdir -p $O
+timeout 1500 python -m pytest tests/test_gpu_kernels.py -x -q -k "sell or topk or b1 or u16" > $O/tests.log 2>&1; echo "tests rc=$?"; tail -3 $O/tests.log
+for L in 128 256 512 1024; do
+for D in 0.02 0.05; do
+timeout 600 python tools/stream_probe.py --batches 1 --sell-long $L --density $D > $O/b1_L${L}_d$D.jsonl 2> $O/b1_L${L}_d$D.err; echo "L=$L d=$D"; head -1 $O/b1_L${L}_d$D.jsonl
+done; done
+timeout 1200 python bench.py --no-cpu-baseline --no-parity > $O/bench.json 2> $O/bench.err; echo "bench rc=$?"

@@ -31,6 +31,7 @@ def main():
     ap.add_argument("--batches", default="1,8,64")
     ap.add_argument("--topk-segs", type=int, default=0, help="FSR_OPT_TOPK_SEGMENTS (0 = automatic)")
     ap.add_argument("--single", default=None, help="b = 1 path: sell (K9e) | csr")
+    ap.add_argument("--sell-long", type=int, default=0, help="ranking.SELL_LONG_ROW override")
     a = ap.parse_args()
     cfg = CONFIGS["C3"]
     dev = torch.device("cuda", 0)
@@ -38,6 +39,8 @@ def main():
     ctx.set_topk_segments(a.topk_segs)
     if a.single:
         ctx.single_query_path = a.single
+    if a.sell_long:
+        ranking.SELL_LONG_ROW = a.sell_long
     S, (y_ptr, y_idx, y_val), _, _, _ = bench.build_inputs(cfg, cfg.n, 256, dev, "float32")
     dec = spectral.decompose(S, cfg.r, p=cfg.p, q=cfg.q, seed=0, dtype="float32", device=dev)
     sd = spectral.sparsify(dec, int(round(a.density * cfg.n * cfg.r)))
