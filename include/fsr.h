@@ -308,7 +308,10 @@ int fsr_filter_batch_u16(fsr_ctx* ctx, int dtype, int64_t n, int64_t r, int u_sp
  * cols / vals arrays to allocate, >= 1), fsr_sell_pack fills them.
  * fsr_filter_single_sell = fsr_filter_batch_u16 at b = 1 with the SpMV on
  * that layout; every x_i is the sequential CSR-order fmaf chain (bitwise the
- * b >= 256 kernels' sums).  r <= 16384. */
+ * b >= 256 kernels' sums).  r <= 16384.  fsr_filter_batch_sell: the same for
+ * 1 <= b <= 64 queries (r <= 12800 when b >= 2), 2 or 4 queries per pass of
+ * the layout.  The long rows' chains run through warp shuffles, so choose
+ * long_len such that they hold a few percent of the entries at most. */
 int64_t fsr_sell_plan_workspace_bytes(int64_t n);
 int fsr_sell_plan(fsr_ctx* ctx, int64_t n, const int64_t* u_indptr, int64_t long_len, int32_t* perm, int32_t* lens,
                   int64_t* slice_ptr, void* workspace, int64_t* n_long_out, int64_t* total_out);
@@ -320,6 +323,12 @@ int fsr_filter_single_sell(fsr_ctx* ctx, int64_t n, int64_t r, const int64_t* u_
                            const float* sell_vals, int64_t n_long, const float* w, const double* eta,
                            const int64_t* y_ptr, const int64_t* y_idx, const float* y_val, int copy_uncovered,
                            void* workspace, float* X, int64_t topk, int64_t* top_idx, float* top_val);
+int fsr_filter_batch_sell(fsr_ctx* ctx, int64_t n, int64_t r, const int64_t* u_indptr, const int32_t* u_indices,
+                          const uint16_t* u_cols16, const float* u_values, const int32_t* sell_perm,
+                          const int32_t* sell_lens, const int64_t* sell_slice_ptr, const uint16_t* sell_cols,
+                          const float* sell_vals, int64_t n_long, const float* w, const double* eta, int64_t b,
+                          const int64_t* y_ptr, const int64_t* y_idx, const float* y_val, int copy_uncovered,
+                          void* workspace, float* X, int64_t topk, int64_t* top_idx, float* top_val);
 /* ---- K9t: the ranked-query step on tensor cores (csrc/k9t.cu) ----------------
  * Replaces, for a float32 sparse decomposition and top-k-only output, the
  * per-query loop of ranking.py:229-255 (filter) + ranking.py:390-395 (rank)[:topk]

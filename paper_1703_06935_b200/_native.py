@@ -75,6 +75,9 @@ _SIGS = {
     "fsr_sell_pack": (_c_int, [_c_p, _c_i64, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p]),
     "fsr_filter_single_sell": (_c_int, [_c_p, _c_i64, _c_i64, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p,
                                         _c_i64, _c_p, _c_p, _c_p, _c_p, _c_p, _c_int, _c_p, _c_p, _c_i64, _c_p, _c_p]),
+    "fsr_filter_batch_sell": (_c_int, [_c_p, _c_i64, _c_i64, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p,
+                                       _c_i64, _c_p, _c_p, _c_i64, _c_p, _c_p, _c_p, _c_int, _c_p, _c_p, _c_i64, _c_p,
+                                       _c_p]),
     "fsr_dense_u_bytes": (_c_i64, [_c_i64, _c_i64]),
     "fsr_dense_u_build": (_c_int, [_c_p, _c_i64, _c_i64, _c_p, _c_p, _c_p, _c_p]),
     "fsr_filter_tc_workspace_bytes": (_c_i64, [_c_i64, _c_i64, _c_i64]),

@@ -406,7 +406,14 @@ int filter_impl(fsr_ctx* ctx, int64_t n, int64_t r, int u_sparse, const int64_t*
     } else {
       // K9 writes X (b x n) directly: smem-staged transposed tiles, no separate pass
       fsr::StageTimer timer(ctx, FSR_STAGE_FILTER_SPMM);
-      FSR_TRY(fsr::launch_spmm_T<T>(ctx, n, u_indptr, u_indices, u_values, b, Zs, b, Xout, n));
+      bool done = false;
+      if constexpr (std::is_same<T, float>::value) {
+        if (sell && fsr::sell::batch_applicable(r, b)) {  // K9e, 2 or 4 queries per pass of the sliced-ELL copy
+          FSR_TRY(fsr::sell::launch_spmm(ctx, n, *sell, u_indptr, u_values, Zs, r, b, Xout, n));
+          done = true;
+        }
+      }
+      if (!done) FSR_TRY(fsr::launch_spmm_T<T>(ctx, n, u_indptr, u_indices, u_values, b, Zs, b, Xout, n));
     }
   } else {
     fsr::StageTimer timer(ctx, FSR_STAGE_FILTER_SPMM);
@@ -498,21 +505,23 @@ int fsr_filter_batch_u16(fsr_ctx* ctx, int dtype, int64_t n, int64_t r, int u_sp
                             (float*)X, topk, top_idx, (float*)top_val, u_cols16);
 }
 
-int fsr_filter_single_sell(fsr_ctx* ctx, int64_t n, int64_t r, const int64_t* u_indptr, const int32_t* u_indices,
-                           const uint16_t* u_cols16, const float* u_values, const int32_t* sell_perm,
-                           const int32_t* sell_lens, const int64_t* sell_slice_ptr, const uint16_t* sell_cols,
-                           const float* sell_vals, int64_t n_long, const float* w, const double* eta,
-                           const int64_t* y_ptr, const int64_t* y_idx, const float* y_val, int copy_uncovered,
-                           void* workspace, float* X, int64_t topk, int64_t* top_idx, float* top_val) {
+int fsr_filter_batch_sell(fsr_ctx* ctx, int64_t n, int64_t r, const int64_t* u_indptr, const int32_t* u_indices,
+                          const uint16_t* u_cols16, const float* u_values, const int32_t* sell_perm,
+                          const int32_t* sell_lens, const int64_t* sell_slice_ptr, const uint16_t* sell_cols,
+                          const float* sell_vals, int64_t n_long, const float* w, const double* eta, int64_t b,
+                          const int64_t* y_ptr, const int64_t* y_idx, const float* y_val, int copy_uncovered,
+                          void* workspace, float* X, int64_t topk, int64_t* top_idx, float* top_val) {
   FSR_REQUIRE(ctx, n >= 1 && fsr::sell::applicable(r) && workspace && u_indptr && u_indices && u_cols16 && u_values,
-              "filter_single_sell: bad shape (r <= 16384, sparse U with its 16-bit columns)");
+              "filter_batch_sell: bad shape (r <= 16384, sparse U with its 16-bit columns)");
+  FSR_REQUIRE(ctx, b == 1 || fsr::sell::batch_applicable(r, b),
+              "filter_batch_sell: b must lie in [1, %d] (and r <= 12800 for b >= 2)", (int)fsr::sell::kMaxBatch);
   FSR_REQUIRE(ctx, sell_perm && sell_lens && sell_slice_ptr && sell_cols && sell_vals && n_long >= 0 &&
                        n_long % 32 == 0,
-              "filter_single_sell: missing sliced-ELL layout (fsr_sell_plan / fsr_sell_pack)");
-  FSR_REQUIRE(ctx, topk >= 0 && topk <= fsr::topk::kCap / 4 && topk <= n, "filter_single_sell: topk must lie in [0, min(n, %d)]",
+              "filter_batch_sell: missing sliced-ELL layout (fsr_sell_plan / fsr_sell_pack)");
+  FSR_REQUIRE(ctx, topk >= 0 && topk <= fsr::topk::kCap / 4 && topk <= n, "filter_batch_sell: topk must lie in [0, min(n, %d)]",
               fsr::topk::kCap / 4);
-  FSR_REQUIRE(ctx, X || topk > 0, "filter_single_sell: nothing to output");
-  FSR_REQUIRE(ctx, topk == 0 || (top_idx && top_val), "filter_single_sell: missing top-k outputs");
+  FSR_REQUIRE(ctx, X || topk > 0, "filter_batch_sell: nothing to output");
+  FSR_REQUIRE(ctx, topk == 0 || (top_idx && top_val), "filter_batch_sell: missing top-k outputs");
   fsr::sell::View V;
   V.perm = sell_perm;
   V.lens = sell_lens;
@@ -521,9 +530,20 @@ int fsr_filter_single_sell(fsr_ctx* ctx, int64_t n, int64_t r, const int64_t* u_
   V.vals = sell_vals;
   V.n_long = n_long;
   V.csr_cols16 = u_cols16;
-  // b = 1 never takes the pruned branch of filter_impl (prune::applicable needs a wide batch)
-  return filter_impl<float>(ctx, n, r, 1, u_indptr, u_indices, u_values, nullptr, 0, w, eta, 1, y_ptr, y_idx, y_val,
+  // b <= 64 never takes the pruned branch of filter_impl (prune::applicable needs b >= 256)
+  return filter_impl<float>(ctx, n, r, 1, u_indptr, u_indices, u_values, nullptr, 0, w, eta, b, y_ptr, y_idx, y_val,
                             copy_uncovered, workspace, X, topk, top_idx, top_val, u_cols16, &V);
+}
+
+int fsr_filter_single_sell(fsr_ctx* ctx, int64_t n, int64_t r, const int64_t* u_indptr, const int32_t* u_indices,
+                           const uint16_t* u_cols16, const float* u_values, const int32_t* sell_perm,
+                           const int32_t* sell_lens, const int64_t* sell_slice_ptr, const uint16_t* sell_cols,
+                           const float* sell_vals, int64_t n_long, const float* w, const double* eta,
+                           const int64_t* y_ptr, const int64_t* y_idx, const float* y_val, int copy_uncovered,
+                           void* workspace, float* X, int64_t topk, int64_t* top_idx, float* top_val) {
+  return fsr_filter_batch_sell(ctx, n, r, u_indptr, u_indices, u_cols16, u_values, sell_perm, sell_lens,
+                               sell_slice_ptr, sell_cols, sell_vals, n_long, w, eta, 1, y_ptr, y_idx, y_val,
+                               copy_uncovered, workspace, X, topk, top_idx, top_val);
 }
 
 int fsr_topk_rows(fsr_ctx* ctx, int dtype, int64_t b, int64_t n, const void* X, int64_t ldx, int64_t topk,

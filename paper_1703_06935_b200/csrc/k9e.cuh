@@ -17,6 +17,8 @@
 // CTA scheduler balances the skewed row lengths.
 #pragma once
 
+#include <type_traits>
+
 #include "fsr_common.cuh"
 
 namespace fsr {
@@ -115,7 +117,150 @@ __global__ void __launch_bounds__(256) sell_spmv_kernel(int64_t n, int64_t n_lon
   if (pos < n) x[__ldg(perm + pos)] = acc;
 }
 
+// Small batches (2 <= b <= 64): the same layout with NB queries per pass.
+// z of the pass's queries sits in shared memory as [column][NB] (one 8- or
+// 16-byte read per entry), every thread keeps NB chains; grid.y = the passes.
+// X is (b x n) row-major (ldx = n): x[q * ldx + row].
+template <int NB, int DEPTH, int THREADS>
+__global__ void __launch_bounds__(THREADS) sell_spmm_kernel(int64_t n, int64_t n_long, int64_t long_ctas,
+                                                            int64_t n_groups,
+                                                            const int32_t* __restrict__ perm,
+                                                            const int32_t* __restrict__ lens,
+                                                            const int64_t* __restrict__ slice_ptr,
+                                                            const uint16_t* __restrict__ cols,
+                                                            const float* __restrict__ vals,
+                                                            const int64_t* __restrict__ indptr,
+                                                            const uint16_t* __restrict__ csr_cols,
+                                                            const float* __restrict__ csr_vals,
+                                                            const float* __restrict__ Zs, int64_t r, int64_t b,
+                                                            float* __restrict__ X, int64_t ldx) {
+  constexpr int WARPS = THREADS / 32;
+  extern __shared__ __align__(16) float zs[];  // [r][NB]
+  const int64_t q0 = (int64_t)blockIdx.y * NB;
+  for (int64_t t = threadIdx.x; t < r * NB; t += blockDim.x) {
+    const int64_t c = t / NB, jj = t % NB;
+    zs[t] = q0 + jj < b ? Zs[c * b + q0 + jj] : 0.f;
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  using ZV = typename std::conditional<NB == 4, float4, float2>::type;
+  const ZV* zv = reinterpret_cast<const ZV*>(zs);
+  // one group per CTA, or resident CTAs striding over the groups (launch_spmm_nb)
+  for (int64_t grp = blockIdx.x; grp < n_groups; grp += gridDim.x) {
+  float acc[NB];
+#pragma unroll
+  for (int jj = 0; jj < NB; ++jj) acc[jj] = 0.f;
+  if (grp < long_ctas) {
+    const int64_t pos = grp * WARPS + warp;
+    if (pos >= n_long || pos >= n) continue;
+    const int64_t i = perm[pos];
+    const int64_t e0 = __ldg(indptr + i), e1 = __ldg(indptr + i + 1);
+    for (int64_t base = e0; base < e1; base += 32) {
+      const int64_t e = base + lane;
+      const bool ok = e < e1;
+      const int c = ok ? (int)ld_stream(csr_cols + e) : 0;
+      FSR_DCHECK(c < r);
+      const float v = ok ? ld_stream(csr_vals + e) : 0.f;
+      float zz[NB];
+#pragma unroll
+      for (int jj = 0; jj < NB; ++jj) zz[jj] = ok ? zs[c * NB + jj] : 0.f;
+      const int cnt = (int)min((int64_t)32, e1 - base);
+      for (int l = 0; l < cnt; ++l) {
+        const float vv = __shfl_sync(0xffffffffu, v, l);
+#pragma unroll
+        for (int jj = 0; jj < NB; ++jj) acc[jj] = fmaf(vv, __shfl_sync(0xffffffffu, zz[jj], l), acc[jj]);
+      }
+    }
+    if (!lane)
+#pragma unroll
+      for (int jj = 0; jj < NB; ++jj)
+        if (q0 + jj < b) X[(q0 + jj) * ldx + i] = acc[jj];
+    continue;
+  }
+  const int64_t s = (n_long >> 5) + (grp - long_ctas) * WARPS + warp;
+  const int64_t pos = s * 32 + lane;
+  if (s * 32 >= n) continue;
+  const int64_t p0 = __ldg(slice_ptr + s);
+  const int width = (int)((__ldg(slice_ptr + s + 1) - p0) >> 5);
+  const int my_len = pos < n ? __ldg(lens + pos) : 0;
+  const uint16_t* cp = cols + p0 + lane;
+  const float* vp = vals + p0 + lane;
+  int j = 0;
+  for (; j + DEPTH <= width; j += DEPTH) {
+    int c[DEPTH];
+    float v[DEPTH];
+#pragma unroll
+    for (int u = 0; u < DEPTH; ++u) {
+      c[u] = (int)ld_stream(cp + (int64_t)(j + u) * 32);
+      v[u] = ld_stream(vp + (int64_t)(j + u) * 32);
+    }
+#pragma unroll
+    for (int u = 0; u < DEPTH; ++u) {
+      FSR_DCHECK(c[u] < r);
+      if (j + u < my_len) {
+        const ZV zq = zv[c[u]];
+        const float* zf = reinterpret_cast<const float*>(&zq);
+#pragma unroll
+        for (int jj = 0; jj < NB; ++jj) acc[jj] = fmaf(v[u], zf[jj], acc[jj]);
+      }
+    }
+  }
+  for (; j < width; ++j) {
+    const int c = (int)ld_stream(cp + (int64_t)j * 32);
+    const float v = ld_stream(vp + (int64_t)j * 32);
+    if (j < my_len) {
+      const ZV zq = zv[c];
+      const float* zf = reinterpret_cast<const float*>(&zq);
+#pragma unroll
+      for (int jj = 0; jj < NB; ++jj) acc[jj] = fmaf(v, zf[jj], acc[jj]);
+    }
+  }
+  if (pos < n) {
+    const int64_t i = __ldg(perm + pos);
+#pragma unroll
+    for (int jj = 0; jj < NB; ++jj)
+      if (q0 + jj < b) X[(q0 + jj) * ldx + i] = acc[jj];
+  }
+  }
+}
+
 inline bool applicable(int64_t r) { return r >= 1 && r <= 16384; }
+constexpr int64_t kMaxBatch = 64;  // beyond it the wide kernels / K9t take over
+// NB = 4 needs r * 16 bytes of shared memory twice per SM
+inline bool batch_applicable(int64_t r, int64_t b) { return applicable(r) && b >= 2 && b <= kMaxBatch && r <= 12800; }
+
+template <int NB, int DEPTH, int THREADS>
+int launch_spmm_nb(fsr_ctx* ctx, int64_t n, const View& V, const int64_t* indptr, const float* csr_vals,
+                   const float* Zs, int64_t r, int64_t b, float* X, int64_t ldx) {
+  constexpr int WARPS = THREADS / 32;
+  auto kern = sell_spmm_kernel<NB, DEPTH, THREADS>;
+  const size_t smem = (size_t)r * NB * sizeof(float);
+  FSR_TRY(fsr::ensure_smem(ctx, kern, smem));
+  const int64_t long_ctas = ceil_div(std::min(V.n_long, n), WARPS);
+  const int64_t short_slices = ceil_div(n, 32) - (V.n_long >> 5);
+  const int64_t n_groups = long_ctas + ceil_div(std::max<int64_t>(short_slices, 0), WARPS);
+  if (n_groups <= 0) return FSR_OK;
+  int per_sm = 1;
+  FSR_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, THREADS, smem));
+  const int64_t passes = ceil_div(b, NB);
+  // up to 4 passes: a CTA per group, issued longest first (measured faster than
+  // resident CTAs striding over the groups: C3 2%, b = 4: 0.228 vs 0.295 ms);
+  // more passes: resident CTAs, 4 passes side by side so that they share the
+  // entry stream through L2 (b = 32: 1.60 vs 1.90 ms)
+  const int64_t resident = (int64_t)ctx->num_sms * std::max(per_sm, 1);
+  const int64_t gx = passes <= 4 ? n_groups : std::min(n_groups, std::max<int64_t>(1, resident / 4));
+  dim3 grid((unsigned)gx, (unsigned)passes);
+  kern<<<grid, THREADS, smem, ctx->stream>>>(n, V.n_long, long_ctas, n_groups, V.perm, V.lens, V.slice_ptr, V.cols, V.vals,
+                                             indptr, V.csr_cols16, csr_vals, Zs, r, b, X, ldx);
+  return launched(ctx, "sell_spmm_kernel");
+}
+
+// X (b x n, ld = ldx) = (U~ Zs)^T for 2 <= b <= kMaxBatch; Zs is r x b.
+inline int launch_spmm(fsr_ctx* ctx, int64_t n, const View& V, const int64_t* indptr, const float* csr_vals,
+                       const float* Zs, int64_t r, int64_t b, float* X, int64_t ldx) {
+  if (b > 2 && r <= 6400) return launch_spmm_nb<4, 16, 512>(ctx, n, V, indptr, csr_vals, Zs, r, b, X, ldx);
+  return launch_spmm_nb<2, 8, 256>(ctx, n, V, indptr, csr_vals, Zs, r, b, X, ldx);
+}
 
 inline int launch_spmv(fsr_ctx* ctx, int64_t n, const View& V, const int64_t* indptr, const float* csr_vals,
                        const float* z, int64_t r, float* x) {

@@ -279,14 +279,16 @@ def filter_device(dec: SpectralDecomposition, h: TransferFunction, queries: Devi
     if workspace is None or workspace.numel() < need:
         workspace = torch.empty(need, dtype=torch.uint8, device=dev)
     ctx.last_online_path = "pruned" if path != "exact" and topk_pruned(n, b, topk, dt) else "exact"
-    if dec.is_sparse and b == 1 and dt == torch.float32 and ctx.single_query_path == "sell":
-        # one fp32 query: K9e streams the sliced-ELL copy of U~ (6 bytes per entry, thread per row)
+    if dec.is_sparse and dt == torch.float32 and ctx.single_query_path == "sell" and \
+            (b == 1 or (b <= SELL_MAX_BATCH and r <= SELL_MAX_BATCH_RANK)):
+        # up to 64 fp32 queries: K9e streams the sliced-ELL copy of U~ (6 bytes per entry, thread per
+        # row, 1 / 2 / 4 queries per pass)
         sell = sell_layout(dec)
         if sell is not None:
             perm, lens, slice_ptr, scols, svals, n_long = sell
-            ctx.call("filter_single_sell", n, r, N.ptr(U.indptr), N.ptr(U.indices), N.ptr(u16_columns(dec)),
+            ctx.call("filter_batch_sell", n, r, N.ptr(U.indptr), N.ptr(U.indices), N.ptr(u16_columns(dec)),
                      N.ptr(U.values), N.ptr(perm), N.ptr(lens), N.ptr(slice_ptr), N.ptr(scols), N.ptr(svals), n_long,
-                     N.ptr(w), N.ptr(dec.eta_device), N.ptr(queries.y_ptr), N.ptr(queries.y_idx),
+                     N.ptr(w), N.ptr(dec.eta_device), b, N.ptr(queries.y_ptr), N.ptr(queries.y_idx),
                      N.ptr(queries.y_val), int(bool(copy_uncovered)), N.ptr(workspace),
                      N.ptr(res.X if want_x else None), int(topk), N.ptr(res.top_idx if topk else None),
                      N.ptr(res.top_val if topk else None))
@@ -419,6 +421,11 @@ SELL_MAX_RANK = 16384  # z must fit the SpMV's shared memory (fsr::sell::applica
 # row's chain, on a side stream (one DRAM latency per 32/128 entries of a
 # row: 0.55 / 0.21 ms at 2%, profiles/r02/k9e_long_rows.md).
 SELL_MAX_LONG_SHARE = 0.03
+# K9e with 2 / 4 queries per pass beats the CSR narrow kernels up to b = 16 (C3 2%: b = 8 0.44 vs
+# 1.33 ms, b = 16 0.89 vs 1.34; b = 32 1.60 vs 1.35; 1%: b = 16 0.50 vs 0.86, b = 64 1.53 vs 1.24;
+# profiles/r02/k9e_long_rows.md); libfsr accepts up to fsr::sell::kMaxBatch = 64
+SELL_MAX_BATCH = 16
+SELL_MAX_BATCH_RANK = 12800  # fsr::sell::batch_applicable
 
 
 def sell_layout(dec):

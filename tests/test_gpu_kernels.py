@@ -461,6 +461,39 @@ def test_single_query_sell_bitwise_sequential(n, r, long_row, monkeypatch):
         assert np.linalg.norm(x - ref) <= 1e-5 * max(np.linalg.norm(ref), 1e-30)
 
 
+@pytest.mark.parametrize("b", [2, 3, 4, 5, 8, 33, 64])
+@pytest.mark.parametrize("n,r,long_row", [(3001, 700, 512), (3001, 700, 40), (50_000, 700, 512)])
+def test_small_batch_sell_bitwise_sequential(b, n, r, long_row, monkeypatch):
+    """K9e with 2 / 4 queries per pass (2 <= b <= 64): every row of X is, bit
+    for bit, the sequential-order row of the wide-batch kernel, ragged last
+    passes and empty queries included; the top-k is the reference rank order."""
+    monkeypatch.setattr(ranking, "SELL_LONG_ROW", long_row)
+    monkeypatch.setattr(ranking, "SELL_MAX_LONG_SHARE", 1.0)
+    monkeypatch.setattr(ranking, "SELL_MAX_BATCH", 64)  # the library's limit (the host routes b <= 16 by default)
+    host = _skewed_sparse_dec(n, r, 5)
+    dec = spectral.SpectralDecomposition.from_host(host, dtype="float32")
+    h = ranking.h_alpha(0.99)
+    rng = np.random.default_rng(b)
+    ys = []
+    for j in range(b):
+        k = 0 if j == 1 else int(rng.integers(1, 6))
+        idx = np.sort(rng.choice(n, size=k, replace=False))
+        ys.append(ranking.ObservationVector(n, idx, rng.uniform(0.1, 1.0, k), cap=max(k, 1)))
+    dev = dec.eta_device.device
+    q = ranking.DeviceQueries(ranking.QueryBatch.from_vectors(ys), dec.dtype, dev)
+    K = 50
+    res = ranking.filter_device(dec, h, q, topk=K)
+    wide = ys + [ys[0]] * (256 - b)
+    qw = ranking.DeviceQueries(ranking.QueryBatch.from_vectors(wide), dec.dtype, dev)
+    seq = ranking.filter_device(dec, h, qw).X[:b]
+    assert torch.equal(res.X.view(torch.int32), seq.view(torch.int32))
+    X = res.X.cpu().numpy()
+    for j in range(b):
+        order = O.rank(X[j].astype(np.float64))[:K]
+        np.testing.assert_array_equal(res.top_idx[j].cpu().numpy(), order)
+        np.testing.assert_array_equal(res.top_val[j].cpu().numpy(), X[j][order])
+
+
 def test_single_query_sell_policy_long_share(monkeypatch):
     """A U~ whose long rows hold more than SELL_MAX_LONG_SHARE of the entries
     keeps the CSR single-query kernel (sell_layout -> None); scores stay within
