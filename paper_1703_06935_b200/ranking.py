@@ -908,11 +908,12 @@ class FilterGraph:
     Python/ctypes work between them.  Batches smaller than ``b`` are padded
     with empty queries.  Results are identical to ``filter_device`` called
     with a batch of the graph's capacity ``b`` (same kernels, same
-    arguments); the kernel path is chosen by ``b``, so a partial batch run
-    eagerly through ``filter_device`` with fewer queries may take a
-    different K9 variant (e.g. the narrow b <= 64 kernel, which sums a row
-    in two interleaved halves) and differ in the last bits of ``top_val``
-    and in the order of near-ties.
+    arguments); the kernel path is chosen by ``b``.  For a float32 sparse
+    decomposition b <= 16 (K9e) and b >= 256 sum every row in CSR order, so
+    their scores agree bit for bit; a partial batch run eagerly through
+    ``filter_device`` with 17 <= b <= 64 queries may take the narrow CSR
+    kernel (a row summed in two interleaved halves) and differ in the last
+    bits of ``top_val`` and in the order of near-ties.
     """
 
     def __init__(self, dec: SpectralDecomposition, h: TransferFunction, b: int, nnz_cap: int, topk: int = 100,

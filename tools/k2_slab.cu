@@ -125,6 +125,177 @@ __global__ void __launch_bounds__(256) slab_kernel(int64_t n_rows, const int64_t
   }
 }
 
+
+// ---- pipelined variant: a producer warp stages (row pointers, entries) of
+// 8-row blocks into a shared-memory ring with bulk async copies; 7 consumer
+// warps gather.  Consumers never wait for their index stream.
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  const uint32_t addr = smem_u32(bar);
+  uint32_t done = 0;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(addr), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
+template <int LPR, int DEPTH, int RB, int CAP, int NS>
+__global__ void __launch_bounds__(256) slab_pipe_kernel(int64_t n_rows, const int64_t* __restrict__ ptr,
+                                                        const int2* __restrict__ ent, const float4* __restrict__ Xs,
+                                                        float* __restrict__ Y, int64_t ldy, int64_t c0, int accumulate) {
+  constexpr int G = 32 / LPR;    // rows in flight per warp
+  constexpr int NC = 7;          // consumer warps
+  constexpr int PW = RB + 2;     // staged row pointers (80 bytes for RB = 8)
+  extern __shared__ __align__(16) unsigned char dyn[];
+  int2* s_ent = reinterpret_cast<int2*>(dyn);                                  // [NS][CAP]
+  int64_t* s_ptr = reinterpret_cast<int64_t*>(dyn + (size_t)NS * CAP * 8);    // [NS][PW]
+  uint64_t* full = reinterpret_cast<uint64_t*>(s_ptr + NS * PW);
+  uint64_t* empty = full + NS;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const int64_t n_blocks = (n_rows + RB - 1) / RB;
+  const int64_t my_blocks = blockIdx.x < n_blocks ? (n_blocks - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+  if (warp == 0) {
+    for (int64_t q0 = 0; q0 < my_blocks; q0 += 32) {
+      const int64_t q = q0 + lane;
+      int64_t p0 = 0, p1 = 0, r0 = 0;
+      if (q < my_blocks) {
+        r0 = ((int64_t)blockIdx.x + q * gridDim.x) * RB;
+        p0 = __ldg(ptr + r0);
+        p1 = __ldg(ptr + min(r0 + RB, n_rows));
+      }
+      const int cnt = (int)min((int64_t)32, my_blocks - q0);
+      for (int l = 0; l < cnt; ++l) {
+        const int64_t b0 = __shfl_sync(0xffffffffu, p0, l), b1 = __shfl_sync(0xffffffffu, p1, l);
+        const int64_t rr = __shfl_sync(0xffffffffu, r0, l);
+        if (lane == 0) {
+          const int64_t qq = q0 + l;
+          const int slot = (int)(qq % NS);
+          mbar_wait(&empty[slot], (uint32_t)(((qq / NS) & 1) ^ 1));
+          const int64_t a0 = b0 & ~(int64_t)1;
+          const uint32_t eb = (uint32_t)((((b1 - a0) * 8) + 15) & ~(int64_t)15);
+          mbar_expect_tx(&full[slot], eb + PW * 8);
+          bulk_g2s(s_ptr + slot * PW, ptr + rr, PW * 8, &full[slot]);
+          if (eb) bulk_g2s(s_ent + (size_t)slot * CAP, ent + a0, eb, &full[slot]);
+        }
+      }
+    }
+    return;
+  }
+  const int cw = warp - 1;
+  const int grp = lane / LPR, sl = lane % LPR;
+  for (int64_t q = cw; q < my_blocks; q += NC) {
+    const int slot = (int)(q % NS);
+    const int64_t r0 = ((int64_t)blockIdx.x + q * gridDim.x) * RB;
+    mbar_wait(&full[slot], (uint32_t)((q / NS) & 1));
+    const int64_t* sp = s_ptr + slot * PW;
+    const int2* st = s_ent + (size_t)slot * CAP;
+    const int64_t a0 = sp[0] & ~(int64_t)1;
+    int row = grp;
+    int j = (int)(sp[row] - a0), e = (int)(sp[row + 1] - a0);
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (accumulate && r0 + row < n_rows) acc = *(reinterpret_cast<const float4*>(Y + (r0 + row) * ldy + c0) + sl);
+    while (true) {
+      while (row < RB && j >= e) {
+        if (r0 + row < n_rows) *(reinterpret_cast<float4*>(Y + (r0 + row) * ldy + c0) + sl) = acc;
+        row += G;
+        if (row < RB) {
+          j = (int)(sp[row] - a0);
+          e = (int)(sp[row + 1] - a0);
+          acc = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (accumulate && r0 + row < n_rows) acc = *(reinterpret_cast<const float4*>(Y + (r0 + row) * ldy + c0) + sl);
+        }
+      }
+      const bool active = row < RB;
+      if (!__any_sync(0xffffffffu, active)) break;
+      const int cnt = active ? min(DEPTH, e - j) : 0;
+      int2 cv[DEPTH];
+      float4 v[DEPTH];
+#pragma unroll
+      for (int g = 0; g < DEPTH; ++g) cv[g] = g < cnt ? st[j + g] : make_int2(0, 0);
+#pragma unroll
+      for (int g = 0; g < DEPTH; ++g)
+        if (g < cnt) v[g] = __ldg(Xs + (int64_t)cv[g].x * LPR + sl);
+#pragma unroll
+      for (int g = 0; g < DEPTH; ++g) {
+        if (g < cnt) {
+          const float a = __int_as_float(cv[g].y);
+          acc.x = fmaf(a, v[g].x, acc.x);
+          acc.y = fmaf(a, v[g].y, acc.y);
+          acc.z = fmaf(a, v[g].z, acc.z);
+          acc.w = fmaf(a, v[g].w, acc.w);
+        }
+      }
+      j += cnt;
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[slot]);
+  }
+}
+
+template <int LPR, int DEPTH, int RB, int CAP, int NS>
+static float run_pipe(int H, int64_t n, int n_panels_timed, const std::vector<int64_t*>& d_ptr,
+                      const std::vector<int2*>& d_ent, const float* d_Xp, float* d_Y, int64_t ldy, int reps) {
+  constexpr int W = 4 * LPR;
+  const int64_t slab_rows = (n + H - 1) / H;
+  const size_t smem = (size_t)NS * CAP * 8 + (size_t)NS * (RB + 2) * 8 + (size_t)NS * 16;
+  auto kern = slab_pipe_kernel<LPR, DEPTH, RB, CAP, NS>;
+  CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int per_sm = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, smem));
+  const unsigned grid = 148u * (unsigned)std::max(per_sm, 1);
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  auto pass = [&](int p) {
+    for (int h = 0; h < H; ++h) {
+      const float4* Xs = reinterpret_cast<const float4*>(d_Xp + ((int64_t)p * n + (int64_t)h * slab_rows) * W);
+      if (getenv("K2_YPANEL"))
+        kern<<<grid, 256, smem>>>(n, d_ptr[h], d_ent[h], Xs, d_Y + (int64_t)p * n * W, W, 0, h > 0);
+      else
+        kern<<<grid, 256, smem>>>(n, d_ptr[h], d_ent[h], Xs, d_Y, ldy, (int64_t)p * W, h > 0);
+    }
+  };
+  pass(0);
+  CK(cudaDeviceSynchronize());
+  CK(cudaEventRecord(e0));
+  for (int r = 0; r < reps; ++r)
+    for (int p = 0; p < n_panels_timed; ++p) pass(p);
+  CK(cudaEventRecord(e1));
+  CK(cudaEventSynchronize(e1));
+  CK(cudaGetLastError());
+  float ms;
+  CK(cudaEventElapsedTime(&ms, e0, e1));
+  return ms / (reps * n_panels_timed);
+}
+
 // Reference: thread per (row, column), CSR order, fmaf.
 __global__ void ref_kernel(int64_t n, const int64_t* ptr, const int32_t* cols, const float* vals, const float* Xp,
                            int W, float* Yref) {
@@ -238,7 +409,7 @@ int main(int argc, char** argv) {
   for (int H : {1, 2, 4}) {
     // slab-major packed copies
     const int64_t slab_rows = (n + H - 1) / H;
-    std::vector<std::vector<int64_t>> sp(H, std::vector<int64_t>(n + 1, 0));
+    std::vector<std::vector<int64_t>> sp(H, std::vector<int64_t>(n + 1 + 16, 0));
     std::vector<std::vector<int2>> se(H);
     for (int h = 0; h < H; ++h) se[h].reserve(nnz / H + n);
     for (int64_t i = 0; i < n; ++i) {
@@ -251,12 +422,14 @@ int main(int argc, char** argv) {
       }
       for (int h = 0; h < H; ++h) sp[h][i + 1] = (int64_t)se[h].size();
     }
+    for (int h = 0; h < H; ++h)
+      for (int t = 1; t <= 16; ++t) sp[h][n + t] = sp[h][n];  // padding the bulk copies may read
     std::vector<int64_t*> d_ptr(H);
     std::vector<int2*> d_ent(H);
     for (int h = 0; h < H; ++h) {
-      CK(cudaMalloc(&d_ptr[h], (n + 1) * 8));
-      CK(cudaMalloc(&d_ent[h], (se[h].size() + 1) * 8));
-      CK(cudaMemcpy(d_ptr[h], sp[h].data(), (n + 1) * 8, cudaMemcpyHostToDevice));
+      CK(cudaMalloc(&d_ptr[h], (n + 1 + 16) * 8));
+      CK(cudaMalloc(&d_ent[h], (se[h].size() + 4) * 8));
+      CK(cudaMemcpy(d_ptr[h], sp[h].data(), (n + 1 + 16) * 8, cudaMemcpyHostToDevice));
       CK(cudaMemcpy(d_ent[h], se[h].data(), se[h].size() * 8, cudaMemcpyHostToDevice));
     }
     auto report = [&](const char* name, int W, float ms) {
@@ -284,6 +457,21 @@ int main(int argc, char** argv) {
       RUN(4, 8, 256, true, "w16_d8_hint");
       RUN(4, 8, 256, false, "w16_d8_nohint");
       RUN(4, 4, 256, true, "w16_d4_hint");
+    }
+#define RUNP(LPR, DEPTH, RB, CAP, NS, NAME)                                                                   \
+  {                                                                                                            \
+    const int npan = (int)(XW / (4 * LPR));                                                                    \
+    const float ms = run_pipe<LPR, DEPTH, RB, CAP, NS>(H, n, npan, d_ptr, d_ent, d_Xp, d_Y, ldy, reps);      \
+    report(NAME, 4 * LPR, ms);                                                                                 \
+  }
+    if (H == 1) {
+      RUNP(4, 4, 8, 512, 14, "pipe_w16_d4");
+      RUNP(4, 8, 8, 512, 14, "pipe_w16_d8");
+    }
+    if (H == 2) {
+      RUNP(8, 4, 8, 512, 14, "pipe_w32_d4");
+      RUNP(8, 8, 8, 512, 14, "pipe_w32_d8");
+      RUNP(8, 8, 8, 512, 28, "pipe_w32_d8_ns28");
     }
     if (H == 2) {
       RUN(4, 8, 256, true, "w16_d8_hint");

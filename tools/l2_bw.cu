@@ -48,6 +48,54 @@ __global__ void gather_kernel(const float4* __restrict__ buf, int64_t rows, int6
   if (acc == 1.2345f) out[0] = acc;
 }
 
+// gather of short rows: LPR lanes x float4 per row (LPR = 8: 128-byte rows, 4
+// random rows per warp access; LPR = 4: 64-byte rows, 8 per access) -- the K2
+// slab kernel's access pattern (tools/k2_slab.cu) without its index stream.
+template <int LPR, int DEPTH>
+__global__ void gather_short_kernel(const float4* __restrict__ buf, int64_t rows, int64_t per_warp, float* out) {
+  const int lane = threadIdx.x & 31, grp = lane / LPR, sl = lane % LPR;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  uint64_t s = 0x9E3779B97F4A7C15ull * (warp * (32 / LPR) + grp + 1);
+  float acc = 0.f;
+  for (int64_t k = 0; k < per_warp; k += DEPTH) {
+    float4 v[DEPTH];
+#pragma unroll
+    for (int g = 0; g < DEPTH; ++g) {
+      s ^= s << 13;
+      s ^= s >> 7;
+      s ^= s << 17;
+      const int64_t row = (int64_t)(((s >> 32) * (uint64_t)rows) >> 32);
+      v[g] = __ldg(buf + row * LPR + sl);
+    }
+#pragma unroll
+    for (int g = 0; g < DEPTH; ++g) acc += v[g].x + v[g].w;
+  }
+  if (acc == 1.2345f) out[0] = acc;
+}
+
+template <int LPR, int DEPTH>
+static void run_short(const char* name, int sms, float* out, cudaEvent_t e0, cudaEvent_t e1) {
+  const int64_t mbs[] = {16, 32, 64};
+  for (int64_t mb : mbs) {
+    const int64_t bytes = mb << 20, rows = bytes / (16 * LPR);
+    float4* buf;
+    cudaMalloc(&buf, bytes);
+    cudaMemset(buf, 0, bytes);
+    const int grid = sms * 8;
+    const int64_t per_warp = 8192;
+    gather_short_kernel<LPR, DEPTH><<<grid, 256>>>(buf, rows, 64, out);
+    cudaEventRecord(e0);
+    gather_short_kernel<LPR, DEPTH><<<grid, 256>>>(buf, rows, per_warp, out);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms;
+    cudaEventElapsedTime(&ms, e0, e1);
+    const double moved = (double)grid * 8 * per_warp * 512;
+    printf(", \"%s_%lldMB_GBs\": %.1f", name, (long long)mb, moved / ms / 1e6);
+    cudaFree(buf);
+  }
+}
+
 int main() {
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
@@ -94,6 +142,10 @@ int main() {
     printf(", \"gather_1KB_rows_%lldMB_GBs\": %.1f", (long long)(bytes >> 20), moved / ms / 1e6);
     cudaFree(buf);
   }
+  run_short<8, 4>("gather_128B_rows_d4", sms, out, e0, e1);
+  run_short<8, 8>("gather_128B_rows_d8", sms, out, e0, e1);
+  run_short<4, 8>("gather_64B_rows_d8", sms, out, e0, e1);
+  run_short<2, 8>("gather_32B_rows_d8", sms, out, e0, e1);
   printf("}\n");
   return 0;
 }
