@@ -296,6 +296,108 @@ static float run_pipe(int H, int64_t n, int n_panels_timed, const std::vector<in
   return ms / (reps * n_panels_timed);
 }
 
+
+// ---- block variant: a warp owns RBW consecutive rows; their entries (one
+// contiguous range of the slab CSR) are staged with one round of coalesced
+// loads, then every LPR-lane group walks its rows (grp, grp + G, ...) on its
+// own -- no lock step between the groups' rows, start-up paid once per RBW rows.
+template <int LPR, int DEPTH, int RBW, int CAP>
+__global__ void __launch_bounds__(256) slab_block_kernel(int64_t n_rows, const int64_t* __restrict__ ptr,
+                                                         const int2* __restrict__ ent, const float4* __restrict__ Xs,
+                                                         float* __restrict__ Y, int64_t ldy, int64_t c0, int accumulate) {
+  constexpr int G = 32 / LPR;
+  extern __shared__ __align__(16) unsigned char dyn[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int2* st = reinterpret_cast<int2*>(dyn) + (size_t)warp * CAP;
+  int64_t* sp = reinterpret_cast<int64_t*>(dyn + (size_t)8 * CAP * 8) + warp * (RBW + 1);
+  const int grp = lane / LPR, sl = lane % LPR;
+  const int64_t r0 = ((int64_t)blockIdx.x * 8 + warp) * RBW;
+  if (r0 >= n_rows) return;
+  for (int t = lane; t <= RBW; t += 32) sp[t] = __ldg(ptr + min(r0 + t, n_rows));
+  __syncwarp();
+  const int64_t p0 = sp[0], p1 = sp[RBW];
+  int row = grp;
+  int64_t j = sp[row], e = sp[row + 1];
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (accumulate && r0 + row < n_rows) acc = *(reinterpret_cast<const float4*>(Y + (r0 + row) * ldy + c0) + sl);
+  for (int64_t base = p0;; base += CAP) {
+    const int64_t wend = min(p1, base + CAP);
+    __syncwarp();
+    for (int64_t t = base + lane; t < wend; t += 32) st[t - base] = __ldg(ent + t);
+    __syncwarp();
+    while (true) {
+      while (row < RBW && j >= e) {
+        if (r0 + row < n_rows) *(reinterpret_cast<float4*>(Y + (r0 + row) * ldy + c0) + sl) = acc;
+        row += G;
+        if (row < RBW) {
+          j = sp[row];
+          e = sp[row + 1];
+          acc = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (accumulate && r0 + row < n_rows)
+            acc = *(reinterpret_cast<const float4*>(Y + (r0 + row) * ldy + c0) + sl);
+        }
+      }
+      const bool active = row < RBW && j < wend;
+      if (!__any_sync(0xffffffffu, active)) break;
+      const int cnt = active ? (int)min((int64_t)DEPTH, min(e, wend) - j) : 0;
+      const int o = (int)(j - base);
+      int2 cv[DEPTH];
+      float4 v[DEPTH];
+#pragma unroll
+      for (int g = 0; g < DEPTH; ++g) cv[g] = g < cnt ? st[o + g] : make_int2(0, 0);
+#pragma unroll
+      for (int g = 0; g < DEPTH; ++g)
+        if (g < cnt) v[g] = __ldg(Xs + (int64_t)cv[g].x * LPR + sl);
+#pragma unroll
+      for (int g = 0; g < DEPTH; ++g) {
+        if (g < cnt) {
+          const float a = __int_as_float(cv[g].y);
+          acc.x = fmaf(a, v[g].x, acc.x);
+          acc.y = fmaf(a, v[g].y, acc.y);
+          acc.z = fmaf(a, v[g].z, acc.z);
+          acc.w = fmaf(a, v[g].w, acc.w);
+        }
+      }
+      j += cnt;
+    }
+    if (wend >= p1) break;
+  }
+}
+
+template <int LPR, int DEPTH, int RBW, int CAP>
+static float run_block(int H, int64_t n, int n_panels_timed, const std::vector<int64_t*>& d_ptr,
+                       const std::vector<int2*>& d_ent, const float* d_Xp, float* d_Y, int64_t ldy, int reps) {
+  constexpr int W = 4 * LPR;
+  const int64_t slab_rows = (n + H - 1) / H;
+  const size_t smem = (size_t)8 * CAP * 8 + (size_t)8 * (RBW + 1) * 8;
+  auto kern = slab_block_kernel<LPR, DEPTH, RBW, CAP>;
+  CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const unsigned grid = (unsigned)((n + 8 * RBW - 1) / (8 * RBW));
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  auto pass = [&](int p) {
+    for (int h = 0; h < H; ++h) {
+      const float4* Xs = reinterpret_cast<const float4*>(d_Xp + ((int64_t)p * n + (int64_t)h * slab_rows) * W);
+      if (getenv("K2_YPANEL"))
+        kern<<<grid, 256, smem>>>(n, d_ptr[h], d_ent[h], Xs, d_Y + (int64_t)p * n * W, W, 0, h > 0);
+      else
+        kern<<<grid, 256, smem>>>(n, d_ptr[h], d_ent[h], Xs, d_Y, ldy, (int64_t)p * W, h > 0);
+    }
+  };
+  pass(0);
+  CK(cudaDeviceSynchronize());
+  CK(cudaEventRecord(e0));
+  for (int r = 0; r < reps; ++r)
+    for (int p = 0; p < n_panels_timed; ++p) pass(p);
+  CK(cudaEventRecord(e1));
+  CK(cudaEventSynchronize(e1));
+  CK(cudaGetLastError());
+  float ms;
+  CK(cudaEventElapsedTime(&ms, e0, e1));
+  return ms / (reps * n_panels_timed);
+}
+
 // Reference: thread per (row, column), CSR order, fmaf.
 __global__ void ref_kernel(int64_t n, const int64_t* ptr, const int32_t* cols, const float* vals, const float* Xp,
                            int W, float* Yref) {
@@ -464,6 +566,24 @@ int main(int argc, char** argv) {
     const float ms = run_pipe<LPR, DEPTH, RB, CAP, NS>(H, n, npan, d_ptr, d_ent, d_Xp, d_Y, ldy, reps);      \
     report(NAME, 4 * LPR, ms);                                                                                 \
   }
+#define RUNB(LPR, DEPTH, RBW, CAP, NAME)                                                                      \
+  {                                                                                                            \
+    const int npan = (int)(XW / (4 * LPR));                                                                    \
+    const float ms = run_block<LPR, DEPTH, RBW, CAP>(H, n, npan, d_ptr, d_ent, d_Xp, d_Y, ldy, reps);        \
+    report(NAME, 4 * LPR, ms);                                                                                 \
+  }
+    if (H == 1) {
+      RUNB(4, 4, 32, 1024, "block_w16_d4_r32");
+      RUNB(4, 8, 32, 1024, "block_w16_d8_r32");
+      RUNB(4, 4, 16, 512, "block_w16_d4_r16");
+    }
+    if (H == 2) {
+      RUNB(8, 4, 32, 1024, "block_w32_d4_r32");
+      RUNB(8, 8, 32, 1024, "block_w32_d8_r32");
+      RUNB(8, 4, 16, 512, "block_w32_d4_r16");
+      RUNB(8, 4, 32, 512, "block_w32_d4_r32_c512");
+      RUNB(8, 2, 32, 1024, "block_w32_d2_r32");
+    }
     if (H == 1) {
       RUNP(4, 4, 8, 512, 14, "pipe_w16_d4");
       RUNP(4, 8, 8, 512, 14, "pipe_w16_d8");
