@@ -621,6 +621,14 @@ def online_sweep(dec, sdec_default, density_default, cfg, n, r, queries, device,
                     s_bytes = -(-b // nb) * (4 * kept + 12 * n)
                     row["k9s_stream_gbs"] = s_bytes / (k9_ms / max(k9_cnt, 1) * 1e-3) / 1e9
                     row["k9s_hbm_frac"] = row["k9s_stream_gbs"] / load_peaks()[0]
+                elif pth == "sell":
+                    # K9e: per pass of 1 / 2 / 4 queries the sliced-ELL entries (6 B each) and the row
+                    # metadata (perm, lens: 8 B per row) stream from HBM once; x is scattered (4 B per row and query)
+                    nbq = 1 if b == 1 else (2 if b == 2 else 4)
+                    lay = ranking.sell_layout(sd)
+                    s_bytes = -(-b // nbq) * (6 * int(lay[3].numel()) + 8 * n) + 4 * n * b
+                    row["k9e_stream_gbs"] = s_bytes / (k9_ms / max(k9_cnt, 1) * 1e-3) / 1e9
+                    row["k9e_hbm_frac"] = row["k9e_stream_gbs"] / load_peaks()[0]
                 else:
                     row["k9_algorithmic_gbs"] = k9_bytes / (k9_ms / max(k9_cnt, 1) * 1e-3) / 1e9
                 row["useful_fp32_tflops"] = 2.0 * kept * b / (k9_ms / max(k9_cnt, 1) * 1e-3) / 1e12

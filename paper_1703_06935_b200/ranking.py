@@ -292,6 +292,7 @@ def filter_device(dec: SpectralDecomposition, h: TransferFunction, queries: Devi
                      N.ptr(queries.y_val), int(bool(copy_uncovered)), N.ptr(workspace),
                      N.ptr(res.X if want_x else None), int(topk), N.ptr(res.top_idx if topk else None),
                      N.ptr(res.top_val if topk else None))
+            ctx.last_online_path = "sell"
             return res
     if dec.is_sparse:
         # without the sliced-ELL copy a single fp32 query streams the CSR with 16-bit column indices
@@ -320,7 +321,7 @@ def u16_columns(dec):
     return cached
 
 
-ONLINE_PATHS = ("tc", "stream", "pruned", "exact")
+ONLINE_PATHS = ("tc", "stream", "pruned", "exact")  # last_online_path also reports "sell" (K9e, b <= 16)
 # below this batch the tensor-core step (64-query tiles for b <= 64) streams
 # the whole dense U~ for too few queries; the exact sparse K9 is faster there
 # -- and, at C3, also faster than the packed-U~ stream K9s (opt-in:
