@@ -485,7 +485,17 @@ __global__ void __launch_bounds__(kThreads) few_rows_select_kernel(const T* __re
 }
 
 inline bool few_rows_applicable(fsr_ctx* ctx, int64_t b, int64_t n, int64_t K) {
-  return ctx->topk_segments == 0 && b < ctx->num_sms && n >= 65536 && K <= n && K <= kCap / 4;
+  if (!(ctx->topk_segments == 0 && b < ctx->num_sms && n >= 65536 && K <= n && K <= kCap / 4)) return false;
+  if (!ctx->topk_state) {
+    // the state is allocated on first use; not while the stream is being captured into a graph
+    // (callers warm up before capturing; otherwise the segmented path serves the captured call)
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(ctx->stream, &cap) != cudaSuccess || cap != cudaStreamCaptureStatusNone) {
+      cudaGetLastError();
+      return false;
+    }
+  }
+  return true;
 }
 
 inline int launch_few_rows(fsr_ctx* ctx, int64_t b, int64_t n, const float* X, int64_t ldx, int64_t K, int64_t* top_idx,

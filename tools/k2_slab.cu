@@ -64,8 +64,8 @@ __device__ __forceinline__ void st_stream4(float4* p, float4 v, uint64_t pol) {
 // columns of the W = 4 LPR wide panel.  ptr: slab CSR row pointers (n + 1),
 // ent: packed (column - slab base, value bits).  Xs: the slab's block of the
 // panel (rows x W, contiguous).  Y: row-major output, ldy floats per row.
-template <int LPR, int DEPTH, int CAP, bool HINTS>
-__global__ void __launch_bounds__(256) slab_kernel(int64_t n_rows, const int64_t* __restrict__ ptr,
+template <int LPR, int DEPTH, int CAP, bool HINTS, int MINB = 1>
+__global__ void __launch_bounds__(256, MINB) slab_kernel(int64_t n_rows, const int64_t* __restrict__ ptr,
                                                    const int2* __restrict__ ent, const float4* __restrict__ Xs,
                                                    float* __restrict__ Y, int64_t ldy, int64_t c0, int accumulate) {
   constexpr int G = 32 / LPR;
@@ -438,7 +438,7 @@ static inline uint64_t xr() {
   return rng_state;
 }
 
-template <int LPR, int DEPTH, int CAP, bool HINTS>
+template <int LPR, int DEPTH, int CAP, bool HINTS, int MINB = 1>
 static float run_cfg(int H, int64_t n, int n_panels_timed, const std::vector<int64_t*>& d_ptr,
                      const std::vector<int2*>& d_ent, const float* d_Xp, float* d_Y, int64_t ldy, int reps) {
   constexpr int W = 4 * LPR, G = 32 / LPR;
@@ -451,9 +451,9 @@ static float run_cfg(int H, int64_t n, int n_panels_timed, const std::vector<int
     for (int h = 0; h < H; ++h) {
       const float4* Xs = reinterpret_cast<const float4*>(d_Xp + ((int64_t)p * n + (int64_t)h * slab_rows) * W);
       if (getenv("K2_YPANEL"))  // panel-major output: panel p at d_Y + p n W, W floats per row
-        slab_kernel<LPR, DEPTH, CAP, HINTS><<<grid, 256>>>(n, d_ptr[h], d_ent[h], Xs, d_Y + (int64_t)p * n * W, W, 0, h > 0);
+        slab_kernel<LPR, DEPTH, CAP, HINTS, MINB><<<grid, 256>>>(n, d_ptr[h], d_ent[h], Xs, d_Y + (int64_t)p * n * W, W, 0, h > 0);
       else
-        slab_kernel<LPR, DEPTH, CAP, HINTS><<<grid, 256>>>(n, d_ptr[h], d_ent[h], Xs, d_Y, ldy, (int64_t)p * W, h > 0);
+        slab_kernel<LPR, DEPTH, CAP, HINTS, MINB><<<grid, 256>>>(n, d_ptr[h], d_ent[h], Xs, d_Y, ldy, (int64_t)p * W, h > 0);
     }
   };
   pass(0);
@@ -576,6 +576,23 @@ int main(int argc, char** argv) {
       RUNB(4, 4, 32, 1024, "block_w16_d4_r32");
       RUNB(4, 8, 32, 1024, "block_w16_d8_r32");
       RUNB(4, 4, 16, 512, "block_w16_d4_r16");
+    }
+#define RUNM(LPR, DEPTH, CAP, MINB, NAME)                                                                     \
+  {                                                                                                            \
+    const int npan = (int)(XW / (4 * LPR));                                                                    \
+    const float ms = run_cfg<LPR, DEPTH, CAP, false, MINB>(H, n, npan, d_ptr, d_ent, d_Xp, d_Y, ldy, reps); \
+    report(NAME, 4 * LPR, ms);                                                                                 \
+  }
+    if (H == 2) {
+      RUNM(8, 4, 128, 8, "w32_d4_occ8");
+      RUNM(8, 4, 128, 6, "w32_d4_occ6");
+      RUNM(8, 2, 128, 8, "w32_d2_occ8");
+      RUNM(8, 6, 128, 6, "w32_d6_occ6");
+      RUNM(8, 3, 128, 8, "w32_d3_occ8");
+    }
+    if (H == 1) {
+      RUNM(4, 4, 256, 8, "w16_d4_occ8");
+      RUNM(4, 6, 256, 6, "w16_d6_occ6");
     }
     if (H == 2) {
       RUNB(8, 4, 32, 1024, "block_w32_d4_r32");
