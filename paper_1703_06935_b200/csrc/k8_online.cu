@@ -85,20 +85,37 @@ __global__ void __launch_bounds__(256) project_smem_kernel(int64_t r, int64_t b,
   int32_t* ec = (int32_t*)(ev + kProjCap);
   __shared__ int64_t offs[kProjMaxRows + 1];
   __shared__ int64_t starts[kProjMaxRows];
+  __shared__ T yv[kProjMaxRows];
   const int64_t j = blockIdx.x;
   const int64_t y0 = y_ptr[j], ny = y_ptr[j + 1] - y0;
+  // w is read last: pull its lines into L2 now (one 128-byte line per thread)
+  if (w)
+    for (int64_t c = (int64_t)threadIdx.x * (128 / sizeof(T)); c < r; c += (int64_t)blockDim.x * (128 / sizeof(T)))
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(w + c));
   for (int64_t c = threadIdx.x; c < r; c += blockDim.x) z[c] = T(0);
   bool fits = ny <= kProjMaxRows;
   if (fits) {
     for (int64_t e = threadIdx.x; e < ny; e += blockDim.x) {
       const int64_t i = y_idx[y0 + e];
+      yv[e] = y_val[y0 + e];
       starts[e] = u_indptr[i];
       offs[e + 1] = u_indptr[i + 1] - u_indptr[i];
     }
     __syncthreads();
-    if (!threadIdx.x) {
-      offs[0] = 0;
-      for (int64_t e = 0; e < ny; ++e) offs[e + 1] += offs[e];
+    if (threadIdx.x < 32) {  // inclusive scan of the row lengths, 32 at a time
+      int64_t carry = 0;
+      if (!threadIdx.x) offs[0] = 0;
+      for (int64_t e0 = 0; e0 < ny; e0 += 32) {
+        const int64_t e = e0 + threadIdx.x;
+        int64_t v = e < ny ? offs[e + 1] : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int64_t u = __shfl_up_sync(0xffffffffu, v, o);
+          if ((int)threadIdx.x >= o) v += u;
+        }
+        if (e < ny) offs[e + 1] = v + carry;
+        carry += __shfl_sync(0xffffffffu, v, 31);
+      }
     }
     __syncthreads();
   }
@@ -147,7 +164,7 @@ __global__ void __launch_bounds__(256) project_smem_kernel(int64_t r, int64_t b,
       __syncthreads();
       while (e_first < ny && offs[e_first + 1] <= w0) ++e_first;
       for (int64_t e = e_first; e < ny && offs[e] < w1; ++e) {
-        const T v = y_val[y0 + e];
+        const T v = yv[e];
         const int64_t a = max(offs[e], w0), z1 = min(offs[e + 1], w1);
         for (int64_t t = a + threadIdx.x; t < z1; t += blockDim.x) {
           const int32_t c = ec[t - w0];

@@ -460,23 +460,42 @@ __global__ void __launch_bounds__(kThreads) few_rows_select_kernel(const T* __re
   __threadfence();
   const unsigned c = __ldcg(&st.count[q]);
   __syncthreads();
+  bool written = false;
   if (c <= (unsigned)kCap) {
     for (unsigned t = threadIdx.x; t < c; t += blockDim.x) {
       ckey[t] = __ldcg(gkey + t);
       cidx[t] = __ldcg(gidx + t);
     }
     __syncthreads();
-    bitonic_sort(ckey, cidx, (int)c);
+    if (c <= 512u) {
+      // few candidates: the rank of each one by counting those before it (the
+      // order is total: indices are distinct) -- c^2 / 512 broadcast reads per
+      // thread instead of the bitonic network's ~45 block-wide rounds
+      for (unsigned t = threadIdx.x; t < c; t += blockDim.x) {
+        const uint64_t k = ckey[t];
+        const int64_t i = cidx[t];
+        unsigned rank = 0;
+        for (unsigned s2 = 0; s2 < c; ++s2) rank += before_in_rank(ckey[s2], cidx[s2], k, i) ? 1u : 0u;
+        if (rank < (unsigned)K) {
+          out_idx[q * K + rank] = i;
+          out_val[q * K + rank] = X[q * ld + i];
+        }
+      }
+      written = true;
+    } else {
+      bitonic_sort(ckey, cidx, (int)c);
+    }
   } else {
     Range<T, false> R{X + q * ld, nullptr, n, 0};
     select_exact<T, false>(R, K, sh, ckey, cidx);
   }
   __syncthreads();
-  for (int64_t m = threadIdx.x; m < K; m += blockDim.x) {
-    const int64_t i = cidx[m];
-    out_idx[q * K + m] = i;
-    out_val[q * K + m] = X[q * ld + i];
-  }
+  if (!written)
+    for (int64_t m = threadIdx.x; m < K; m += blockDim.x) {
+      const int64_t i = cidx[m];
+      out_idx[q * K + m] = i;
+      out_val[q * K + m] = X[q * ld + i];
+    }
   for (int t = threadIdx.x; t < nb; t += blockDim.x) ghist[t] = 0;
   if (!threadIdx.x) {
     st.count[q] = 0;
