@@ -994,7 +994,7 @@ def run_fsr(args, cfg, n, rank, world, local_rank):
         torch.cuda.synchronize()
         e2e_ms = max_over_ranks(t0.elapsed_time(t1), world)
         fg = fgs[0]
-        h2d = fg.h_ptr.numel() * 8 + fg.h_idx.numel() * 8 + fg.h_val.numel() * fg.h_val.element_size()
+        h2d = fg.h_all.numel()  # one copy of the (y_ptr | y_idx | y_val) staging buffer per step
         e2e = {"value": world * b * args.steps / (e2e_ms / 1e3), "unit": "queries/s",
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h // args.steps,
                "api": "ranking.FilterGraph.submit/fetch x2 (pinned staging + one CUDA-graph launch: H2D, K8, K9, "

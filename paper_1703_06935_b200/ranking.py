@@ -927,12 +927,21 @@ class FilterGraph:
         dev = dec.eta_device.device
         dt = dec.dtype
         cap = max(1, nnz_cap)
-        self.h_ptr = torch.zeros(b + 1, dtype=torch.int64).pin_memory()
-        self.h_idx = torch.zeros(cap, dtype=torch.int64).pin_memory()
-        self.h_val = torch.zeros(cap, dtype=dt).pin_memory()
-        self.d_ptr = torch.zeros(b + 1, dtype=torch.int64, device=dev)
-        self.d_idx = torch.zeros(cap, dtype=torch.int64, device=dev)
-        self.d_val = torch.zeros(cap, dtype=dt, device=dev)
+        # (y_ptr, y_idx, y_val) share one pinned staging buffer and one device buffer, so the
+        # graph holds a single H2D copy node instead of three
+        es = torch.empty(0, dtype=dt).element_size()
+        o_idx = -(-(b + 1) * 8 // 256) * 256
+        o_val = o_idx + -(-cap * 8 // 256) * 256
+        total = o_val + -(-cap * es // 256) * 256
+        self.h_all = torch.zeros(total, dtype=torch.uint8).pin_memory()
+        self.d_all = torch.zeros(total, dtype=torch.uint8, device=dev)
+
+        def views(buf):
+            return (buf[: (b + 1) * 8].view(torch.int64), buf[o_idx: o_idx + cap * 8].view(torch.int64),
+                    buf[o_val: o_val + cap * es].view(dt))
+
+        self.h_ptr, self.h_idx, self.h_val = views(self.h_all)
+        self.d_ptr, self.d_idx, self.d_val = views(self.d_all)
         self.queries = _StaticQueries(dec.n, b, self.d_ptr, self.d_idx, self.d_val)
         self.res = FilterResult(top_idx=torch.empty(b, topk, dtype=torch.int64, device=dev),
                                 top_val=torch.empty(b, topk, dtype=dt, device=dev))
@@ -959,9 +968,7 @@ class FilterGraph:
             N.Context.get(dev)  # re-bind libfsr to the current stream
 
     def _body(self):
-        self.d_ptr.copy_(self.h_ptr, non_blocking=True)
-        self.d_idx.copy_(self.h_idx, non_blocking=True)
-        self.d_val.copy_(self.h_val, non_blocking=True)
+        self.d_all.copy_(self.h_all, non_blocking=True)
         filter_device(self.dec, self.h, self.queries, copy_uncovered=self.copy_uncovered, topk=self.topk,
                       want_x=False, out=self.res, workspace=self.ws)
 
