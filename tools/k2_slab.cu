@@ -67,7 +67,8 @@ __device__ __forceinline__ void st_stream4(float4* p, float4 v, uint64_t pol) {
 template <int LPR, int DEPTH, int CAP, bool HINTS, int MINB = 1>
 __global__ void __launch_bounds__(256, MINB) slab_kernel(int64_t n_rows, const int64_t* __restrict__ ptr,
                                                    const int2* __restrict__ ent, const float4* __restrict__ Xs,
-                                                   float* __restrict__ Y, int64_t ldy, int64_t c0, int accumulate) {
+                                                   float* __restrict__ Y, int64_t ldy, int64_t c0, int accumulate,
+                                                   int64_t xs4 = LPR) {
   constexpr int G = 32 / LPR;
   __shared__ int2 stage[8][CAP];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -102,7 +103,7 @@ __global__ void __launch_bounds__(256, MINB) slab_kernel(int64_t n_rows, const i
       for (int g = 0; g < DEPTH; ++g) cv[g] = st[min(j + g, hi - 1)];
 #pragma unroll
       for (int g = 0; g < DEPTH; ++g) {
-        const float4* p = Xs + (int64_t)cv[g].x * LPR + sl;
+        const float4* p = Xs + (int64_t)cv[g].x * xs4 + sl;
         v[g] = HINTS ? ld_hint(p, pol_keep) : __ldg(p);
       }
 #pragma unroll
@@ -438,6 +439,8 @@ static inline uint64_t xr() {
   return rng_state;
 }
 
+__global__ void fill_kernel(float* p, int64_t n, uint64_t seed);
+
 template <int LPR, int DEPTH, int CAP, bool HINTS, int MINB = 1>
 static float run_cfg(int H, int64_t n, int n_panels_timed, const std::vector<int64_t*>& d_ptr,
                      const std::vector<int2*>& d_ent, const float* d_Xp, float* d_Y, int64_t ldy, int reps) {
@@ -447,10 +450,22 @@ static float run_cfg(int H, int64_t n, int n_panels_timed, const std::vector<int
   cudaEvent_t e0, e1;
   CK(cudaEventCreate(&e0));
   CK(cudaEventCreate(&e1));
+  static float* d_Xr = nullptr;  // K2_XROW: X row-major (n x ldy floats), gathers strided by ldy
+  if (getenv("K2_XROW")) {
+    if (!d_Xr) {
+      CK(cudaMalloc(&d_Xr, (size_t)n * ldy * 4));
+      fill_kernel<<<148 * 8, 256>>>(d_Xr, n * ldy, 11);
+    }
+    CK(cudaMemcpy2D(d_Xr, (size_t)ldy * 4, d_Xp, (size_t)W * 4, (size_t)W * 4, (size_t)n, cudaMemcpyDeviceToDevice));
+  }
   auto pass = [&](int p) {
     for (int h = 0; h < H; ++h) {
       const float4* Xs = reinterpret_cast<const float4*>(d_Xp + ((int64_t)p * n + (int64_t)h * slab_rows) * W);
-      if (getenv("K2_YPANEL"))  // panel-major output: panel p at d_Y + p n W, W floats per row
+      if (d_Xr && getenv("K2_XROW")) {
+        const float4* Xr = reinterpret_cast<const float4*>(d_Xr + (int64_t)h * slab_rows * ldy + (int64_t)p * W);
+        slab_kernel<LPR, DEPTH, CAP, HINTS, MINB><<<grid, 256>>>(n, d_ptr[h], d_ent[h], Xr, d_Y, ldy, (int64_t)p * W, h > 0,
+                                                                 ldy / 4);
+      } else if (getenv("K2_YPANEL"))  // panel-major output: panel p at d_Y + p n W, W floats per row
         slab_kernel<LPR, DEPTH, CAP, HINTS, MINB><<<grid, 256>>>(n, d_ptr[h], d_ent[h], Xs, d_Y + (int64_t)p * n * W, W, 0, h > 0);
       else
         slab_kernel<LPR, DEPTH, CAP, HINTS, MINB><<<grid, 256>>>(n, d_ptr[h], d_ent[h], Xs, d_Y, ldy, (int64_t)p * W, h > 0);
