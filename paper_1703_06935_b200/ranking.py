@@ -412,15 +412,21 @@ def stream_layout(dec):
     return buf
 
 
-SELL_LONG_ROW = 512   # rows of U~ longer than this stay in CSR (a warp per row)
+# Rows of U~ longer than the layout's long-row length stay in CSR (a warp per
+# row).  None = chosen per decomposition: the smallest candidate whose long
+# rows hold at most SELL_MAX_LONG_SHARE of the entries.  A slice w entries wide
+# is one thread-per-row chain of w / 8 load round trips, so the widest slices
+# bound the kernel when the stream itself is short (C3 1%: K9 0.094 ms at 512,
+# 0.076 at 320), while the long rows' sequential chains run through warp
+# shuffles (3 instructions per entry per warp) and pay only while they hold a
+# small share of the entries: C3 5% needs 1024 (K9 0.259 ms against the CSR
+# kernel's 0.329; at 512 a third of the entries are long: 0.9 ms).  Measured
+# and not kept for the long rows: 32 or 8 rows per warp parked in shared
+# memory with a thread per row's chain, on a side stream (one DRAM latency per
+# 32/128 entries of a row: 0.55 / 0.21 ms at 2%, profiles/r02/k9e_long_rows.md).
+SELL_LONG_ROW = None
+SELL_LONG_ROW_CANDIDATES = (256, 320, 384, 448, 512, 640, 768, 1024, 1536, 2048)
 SELL_MAX_RANK = 16384  # z must fit the SpMV's shared memory (fsr::sell::applicable)
-# The long rows' sequential chains run through warp shuffles (3 instructions
-# per entry per warp), so K9e pays only while they hold a small share of the
-# entries: C3 at 1-2% (1% of the entries in rows over 512) 0.19 -> 0.12 ms, at
-# 5% (a third of the entries) 0.35 -> 0.9 ms.  Measured and not kept for the
-# long rows: 32 or 8 rows per warp parked in shared memory with a thread per
-# row's chain, on a side stream (one DRAM latency per 32/128 entries of a
-# row: 0.55 / 0.21 ms at 2%, profiles/r02/k9e_long_rows.md).
 SELL_MAX_LONG_SHARE = 0.03
 # K9e with 2 / 4 queries per pass beats the CSR narrow kernels up to b = 16 (C3 2%: b = 8 0.44 vs
 # 1.33 ms, b = 16 0.89 vs 1.34; b = 32 1.60 vs 1.35; 1%: b = 16 0.50 vs 0.86, b = 64 1.53 vs 1.24;
@@ -434,8 +440,9 @@ def sell_layout(dec):
     csrc/k9e.cuh): rows sorted by length, 32-row slices stored column-major
     with 16-bit columns (fsr_sell_plan / fsr_sell_pack).  Built once per
     decomposition and cached on it; None when the layout does not apply
-    (dense or fp64 U, r > 16384, a U~ without entries, or rows longer than
-    SELL_LONG_ROW holding more than SELL_MAX_LONG_SHARE of the entries)."""
+    (dense or fp64 U, r > 16384, a U~ without entries, or no long-row length
+    up to 2048 whose longer rows hold at most SELL_MAX_LONG_SHARE of the
+    entries)."""
     import ctypes
     import torch
 
@@ -448,9 +455,13 @@ def sell_layout(dec):
     U = dec.U_device
     dev = U.indices.device
     row_len = U.indptr[1:] - U.indptr[:-1]
-    long_share = float(row_len[row_len > SELL_LONG_ROW].sum()) / U.nnz
+    long_row = None
+    for cand in ((SELL_LONG_ROW,) if SELL_LONG_ROW else SELL_LONG_ROW_CANDIDATES):
+        if float(row_len[row_len > cand].sum()) <= SELL_MAX_LONG_SHARE * U.nnz:
+            long_row = int(cand)
+            break
     del row_len
-    if long_share > SELL_MAX_LONG_SHARE:
+    if long_row is None:
         return None  # the CSR single-query kernel serves this U~
     ctx = N.Context.get(dev)
     n = dec.n
@@ -459,7 +470,7 @@ def sell_layout(dec):
     lens = torch.empty(n, dtype=torch.int32, device=dev)
     slice_ptr = torch.empty((n + 31) // 32 + 1, dtype=torch.int64, device=dev)
     n_long, total = ctypes.c_int64(0), ctypes.c_int64(0)
-    ctx.call("sell_plan", n, N.ptr(U.indptr), SELL_LONG_ROW, N.ptr(perm), N.ptr(lens), N.ptr(slice_ptr), N.ptr(ws),
+    ctx.call("sell_plan", n, N.ptr(U.indptr), long_row, N.ptr(perm), N.ptr(lens), N.ptr(slice_ptr), N.ptr(ws),
              ctypes.byref(n_long), ctypes.byref(total))
     del ws
     cols = torch.empty(max(1, total.value), dtype=torch.int16, device=dev)

@@ -425,7 +425,7 @@ def _sequential_x(dec, h, y, n):
 
 
 @pytest.mark.parametrize("n,r,long_row", [(3001, 700, 512), (3001, 700, 40), (31, 64, 512), (4096, 300, 1),
-                                          (50_000, 700, 512)])
+                                          (50_000, 700, 512), (50_000, 700, None)])
 def test_single_query_sell_bitwise_sequential(n, r, long_row, monkeypatch):
     """K9e (b = 1 on the sliced-ELL copy of U~) returns, bit for bit, the
     sequential-order sums of the wide-batch kernel: skewed rows, empty rows,
@@ -445,7 +445,8 @@ def test_single_query_sell_bitwise_sequential(n, r, long_row, monkeypatch):
     np.testing.assert_array_equal(np.sort(perm.cpu().numpy()), np.arange(n))
     np.testing.assert_array_equal(lens.cpu().numpy(), rl[perm.cpu().numpy()])
     assert np.all(np.diff(lens.cpu().numpy()) <= 0) and n_long % 32 == 0
-    assert n_long >= np.count_nonzero(rl > long_row)
+    if long_row is not None:  # None: the smallest candidate length within the long-share cap
+        assert n_long >= np.count_nonzero(rl > long_row)
     for yi in ([5], [0, 7, min(100, n - 2), n - 1], [20, 21]):
         y = ranking.ObservationVector(n, np.array(yi), np.linspace(1.0, 0.5, len(yi)), cap=len(yi))
         q = ranking.DeviceQueries(ranking.QueryBatch.from_vectors([y]), dec.dtype, dec.eta_device.device)
@@ -509,6 +510,26 @@ def test_single_query_sell_policy_long_share(monkeypatch):
     w = O.transfer_values(O.h_alpha(0.99), host.eigenvalues)
     ref = O.filter_scores(host.U, host.eigenvalues, host.eta, w, y.indices, y.values)
     assert np.linalg.norm(x - ref) <= 1e-5 * np.linalg.norm(ref)
+
+
+def test_single_query_sell_adaptive_long_row():
+    """Default policy: the smallest candidate long-row length whose longer rows
+    hold at most SELL_MAX_LONG_SHARE of the entries (none -> no layout)."""
+    n, r = 50_000, 700
+    host = _skewed_sparse_dec(n, r, 6)
+    dec = spectral.SpectralDecomposition.from_host(host, dtype="float32")
+    rl = np.diff(host.U.indptr)
+    lay = ranking.sell_layout(dec)
+    ok = [c for c in ranking.SELL_LONG_ROW_CANDIDATES
+          if rl[rl > c].sum() <= ranking.SELL_MAX_LONG_SHARE * host.U.nnz]
+    if not ok:
+        assert lay is None
+        return
+    assert lay is not None
+    n_long = lay[5]
+    # every row over the chosen length sits in the long region, and the region holds whole slices
+    assert n_long % 32 == 0 and n_long >= np.count_nonzero(rl > ok[0])
+    assert n_long < np.count_nonzero(rl > ok[0]) + 32
 
 
 def test_single_query_sell_graph_replay_and_csr_agree():
