@@ -425,7 +425,7 @@ def stream_layout(dec):
 # memory with a thread per row's chain, on a side stream (one DRAM latency per
 # 32/128 entries of a row: 0.55 / 0.21 ms at 2%, profiles/r02/k9e_long_rows.md).
 SELL_LONG_ROW = None
-SELL_LONG_ROW_CANDIDATES = (256, 320, 384, 448, 512, 640, 768, 1024, 1536, 2048)
+SELL_LONG_ROW_CANDIDATES = (64, 96, 128, 192, 256, 320, 384, 448, 512, 640, 768, 1024, 1536, 2048)
 SELL_MAX_RANK = 16384  # z must fit the SpMV's shared memory (fsr::sell::applicable)
 SELL_MAX_LONG_SHARE = 0.03
 # K9e with 2 / 4 queries per pass beats the CSR narrow kernels up to b = 16 (C3 2%: b = 8 0.44 vs
