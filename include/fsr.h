@@ -302,7 +302,8 @@ int fsr_filter_batch_u16(fsr_ctx* ctx, int dtype, int64_t n, int64_t r, int u_sp
  * x = U~ (h(L) U~^T y) of specrank.ranking.filter (ranking.py:244-246) that
  * fsr_filter_batch computes from the CSR.  The layout (built once per
  * decomposition): rows sorted by length, descending (perm, lens), slices of
- * 32 rows stored column-major (16-bit column, fp32 value; slice_ptr), rows
+ * 32 rows stored column-major in pairs of entries (16-bit column, fp32 value;
+ * slice_ptr; [j / 2][lane][j % 2]), rows
  * longer than long_len left to the CSR (sorted positions [0, n_long)).
  * fsr_sell_plan sorts and sizes (synchronises; *total_out = entries of the
  * cols / vals arrays to allocate, >= 1), fsr_sell_pack fills them.

@@ -16,13 +16,13 @@ __global__ void row_lens_kernel(int64_t n, const int64_t* __restrict__ indptr, i
   }
 }
 
-// widths[s] = 32 * (longest row of slice s), 0 for the slices of long rows;
+// widths[s] = 32 * (longest row of slice s, rounded up to even), 0 for the slices of long rows;
 // n_long = the sorted positions below the first slice whose longest row fits.
 __global__ void slice_widths_kernel(int64_t n, int64_t n_slices, const int32_t* __restrict__ lens_sorted,
                                     int64_t long_len, int64_t* __restrict__ widths) {
   for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < n_slices; s += (int64_t)gridDim.x * blockDim.x) {
     const int64_t l = lens_sorted[s * 32];  // descending: the slice's first row is its longest
-    widths[s] = l > long_len ? 0 : 32 * l;
+    widths[s] = l > long_len ? 0 : 32 * ((l + 1) & ~(int64_t)1);  // even: entries are stored in pairs
   }
 }
 
@@ -35,8 +35,8 @@ __global__ void count_long_kernel(int64_t n_slices, const int32_t* __restrict__ 
   if (!(threadIdx.x & 31) && mine) atomicAdd(long_slices, mine);
 }
 
-// One warp per slice: lane = row; the row's entries go to [j][lane], the
-// padding up to the slice width is (column 0, value 0) and never summed.
+// One warp per slice: lane = row; the row's entries go to [j / 2][lane][j % 2], the
+// padding up to the (even) slice width is (column 0, value 0) and never summed.
 __global__ void __launch_bounds__(256) sell_pack_kernel(int64_t n, int64_t n_slices,
                                                         const int64_t* __restrict__ indptr,
                                                         const int32_t* __restrict__ indices,
@@ -59,8 +59,9 @@ __global__ void __launch_bounds__(256) sell_pack_kernel(int64_t n, int64_t n_sli
   }
   for (int64_t j = 0; j < width; ++j) {
     const bool ok = j < len;
-    cols[p0 + j * 32 + lane] = ok ? (uint16_t)indices[e0 + j] : (uint16_t)0;
-    vals[p0 + j * 32 + lane] = ok ? values[e0 + j] : 0.f;
+    const int64_t at = p0 + (j >> 1) * 64 + lane * 2 + (j & 1);
+    cols[at] = ok ? (uint16_t)indices[e0 + j] : (uint16_t)0;
+    vals[at] = ok ? values[e0 + j] : 0.f;
   }
 }
 

@@ -5,9 +5,10 @@
 // ~0.1 ms at C3 on per-row latency alone (10^6 rows of ~100 entries: row
 // pointers -> entries -> warp reduction, one dependent chain per row).  Here
 // the rows are sorted by length (descending) and cut into slices of 32 rows;
-// a slice stores its entries column-major ([j][lane], 16-bit column + fp32
-// value, padded to the slice's longest row), so one warp = one slice, one
-// thread = one row: every load is a coalesced 64 + 128 bytes, there is no row
+// a slice stores its entries column-major in pairs ([j / 2][lane][j % 2],
+// 16-bit column + fp32 value, padded to the slice's longest row rounded up to
+// even), so one warp = one slice, one thread = one row: every load is a
+// coalesced 128 + 256 bytes (two entries of each row), there is no row
 // pointer chase and no cross-lane reduction, and each x_i is the sequential
 // CSR-order fmaf chain -- bitwise the sum of the unpruned wide kernels
 // (spmm_rowpanel_T_kernel) and of K9t's exact re-score.  Rows longer than the
@@ -28,7 +29,7 @@ struct View {
   const int32_t* perm = nullptr;       // sorted position -> row of U~ (n)
   const int32_t* lens = nullptr;       // row length by sorted position (n)
   const int64_t* slice_ptr = nullptr;  // entry offset of slice s (n_slices + 1); long slices are empty
-  const uint16_t* cols = nullptr;      // [slice][j][lane]
+  const uint16_t* cols = nullptr;      // [slice][j / 2][lane][j % 2], slice widths even
   const float* vals = nullptr;
   int64_t n_long = 0;                  // sorted positions [0, n_long) are long rows (a multiple of 32)
   const uint16_t* csr_cols16 = nullptr;  // 16-bit copy of the CSR columns (long rows)
@@ -38,6 +39,8 @@ constexpr int kDepth = 8;
 
 __device__ __forceinline__ float ld_stream(const float* p) { return __ldcs(p); }
 __device__ __forceinline__ unsigned short ld_stream(const uint16_t* p) { return __ldcs(p); }
+__device__ __forceinline__ uint32_t ld_stream(const uint32_t* p) { return __ldcs(p); }
+__device__ __forceinline__ float2 ld_stream(const float2* p) { return __ldcs(p); }
 
 // grid: ceil(n_long / 8) CTAs of long rows (a warp per row) followed by
 // ceil(n_short_slices / 8) CTAs of slices (a warp per slice).
@@ -91,28 +94,34 @@ __global__ void __launch_bounds__(256) sell_spmv_kernel(int64_t n, int64_t n_lon
   const int64_t p0 = __ldg(slice_ptr + s);
   const int width = (int)((__ldg(slice_ptr + s + 1) - p0) >> 5);
   const int my_len = pos < n ? __ldg(lens + pos) : 0;
-  const uint16_t* cp = cols + p0 + lane;
-  const float* vp = vals + p0 + lane;
+  // entries come in pairs: one 4-byte load = two columns, one 8-byte load = two
+  // values of the row (12 bytes in flight per 3 registers instead of per 4)
+  const uint32_t* cp = reinterpret_cast<const uint32_t*>(cols + p0) + lane;
+  const float2* vp = reinterpret_cast<const float2*>(vals + p0) + lane;
+  const int pairs = width >> 1;
   float acc = 0.f;
-  int j = 0;
-  for (; j + DEPTH <= width; j += DEPTH) {
-    int c[DEPTH];
-    float v[DEPTH];
+  int jp = 0;
+  for (; jp + DEPTH <= pairs; jp += DEPTH) {
+    uint32_t c[DEPTH];
+    float2 v[DEPTH];
 #pragma unroll
     for (int u = 0; u < DEPTH; ++u) {
-      c[u] = (int)ld_stream(cp + (int64_t)(j + u) * 32);
-      v[u] = ld_stream(vp + (int64_t)(j + u) * 32);
+      c[u] = ld_stream(cp + (int64_t)(jp + u) * 32);
+      v[u] = ld_stream(vp + (int64_t)(jp + u) * 32);
     }
 #pragma unroll
     for (int u = 0; u < DEPTH; ++u) {
-      FSR_DCHECK(c[u] < r);
-      if (j + u < my_len) acc = fmaf(v[u], zs[c[u]], acc);
+      const int j = 2 * (jp + u);
+      FSR_DCHECK((int)(c[u] & 0xffffu) < r && (int)(c[u] >> 16) < r);
+      if (j < my_len) acc = fmaf(v[u].x, zs[c[u] & 0xffffu], acc);
+      if (j + 1 < my_len) acc = fmaf(v[u].y, zs[c[u] >> 16], acc);
     }
   }
-  for (; j < width; ++j) {
-    const int c = (int)ld_stream(cp + (int64_t)j * 32);
-    const float v = ld_stream(vp + (int64_t)j * 32);
-    if (j < my_len) acc = fmaf(v, zs[c], acc);
+  for (; jp < pairs; ++jp) {
+    const uint32_t c = ld_stream(cp + (int64_t)jp * 32);
+    const float2 v = ld_stream(vp + (int64_t)jp * 32);
+    if (2 * jp < my_len) acc = fmaf(v.x, zs[c & 0xffffu], acc);
+    if (2 * jp + 1 < my_len) acc = fmaf(v.y, zs[c >> 16], acc);
   }
   if (pos < n) x[__ldg(perm + pos)] = acc;
 }
@@ -183,37 +192,38 @@ __global__ void __launch_bounds__(THREADS) sell_spmm_kernel(int64_t n, int64_t n
   const int64_t p0 = __ldg(slice_ptr + s);
   const int width = (int)((__ldg(slice_ptr + s + 1) - p0) >> 5);
   const int my_len = pos < n ? __ldg(lens + pos) : 0;
-  const uint16_t* cp = cols + p0 + lane;
-  const float* vp = vals + p0 + lane;
-  int j = 0;
-  for (; j + DEPTH <= width; j += DEPTH) {
-    int c[DEPTH];
-    float v[DEPTH];
+  const uint32_t* cp = reinterpret_cast<const uint32_t*>(cols + p0) + lane;
+  const float2* vp = reinterpret_cast<const float2*>(vals + p0) + lane;
+  const int pairs = width >> 1;
+  auto step = [&](float vv, uint32_t cc) {
+    FSR_DCHECK((int)cc < r);
+    const ZV zq = zv[cc];
+    const float* zf = reinterpret_cast<const float*>(&zq);
 #pragma unroll
-    for (int u = 0; u < DEPTH; ++u) {
-      c[u] = (int)ld_stream(cp + (int64_t)(j + u) * 32);
-      v[u] = ld_stream(vp + (int64_t)(j + u) * 32);
+    for (int jj = 0; jj < NB; ++jj) acc[jj] = fmaf(vv, zf[jj], acc[jj]);
+  };
+  constexpr int DP = DEPTH / 2;  // pairs in flight
+  int jp = 0;
+  for (; jp + DP <= pairs; jp += DP) {
+    uint32_t c[DP];
+    float2 v[DP];
+#pragma unroll
+    for (int u = 0; u < DP; ++u) {
+      c[u] = ld_stream(cp + (int64_t)(jp + u) * 32);
+      v[u] = ld_stream(vp + (int64_t)(jp + u) * 32);
     }
 #pragma unroll
-    for (int u = 0; u < DEPTH; ++u) {
-      FSR_DCHECK(c[u] < r);
-      if (j + u < my_len) {
-        const ZV zq = zv[c[u]];
-        const float* zf = reinterpret_cast<const float*>(&zq);
-#pragma unroll
-        for (int jj = 0; jj < NB; ++jj) acc[jj] = fmaf(v[u], zf[jj], acc[jj]);
-      }
+    for (int u = 0; u < DP; ++u) {
+      const int j = 2 * (jp + u);
+      if (j < my_len) step(v[u].x, c[u] & 0xffffu);
+      if (j + 1 < my_len) step(v[u].y, c[u] >> 16);
     }
   }
-  for (; j < width; ++j) {
-    const int c = (int)ld_stream(cp + (int64_t)j * 32);
-    const float v = ld_stream(vp + (int64_t)j * 32);
-    if (j < my_len) {
-      const ZV zq = zv[c];
-      const float* zf = reinterpret_cast<const float*>(&zq);
-#pragma unroll
-      for (int jj = 0; jj < NB; ++jj) acc[jj] = fmaf(v, zf[jj], acc[jj]);
-    }
+  for (; jp < pairs; ++jp) {
+    const uint32_t c = ld_stream(cp + (int64_t)jp * 32);
+    const float2 v = ld_stream(vp + (int64_t)jp * 32);
+    if (2 * jp < my_len) step(v.x, c & 0xffffu);
+    if (2 * jp + 1 < my_len) step(v.y, c >> 16);
   }
   if (pos < n) {
     const int64_t i = __ldg(perm + pos);
