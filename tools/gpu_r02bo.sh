@@ -1,6 +1,6 @@
 # round-2 closing verification: GPU suite, smoke, default bench (C3 + C5 sweep), reference arm, launch lists (online step, b = 1 replay)
 set -x
-O=gpurun_out/r02bl; mkdir -p $O
+O=gpurun_out/r02bo; mkdir -p $O
 timeout 2400 python -m pytest tests -m gpu -q -rs > $O/gputest.log 2>&1; echo "pytest rc=$?"; tail -4 $O/gputest.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "smoke rc=$?"
 timeout 1200 python bench.py > $O/bench.json 2> $O/bench.err; echo "bench rc=$?"
