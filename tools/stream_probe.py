@@ -32,6 +32,7 @@ def main():
     ap.add_argument("--topk-segs", type=int, default=0, help="FSR_OPT_TOPK_SEGMENTS (0 = automatic)")
     ap.add_argument("--single", default=None, help="b = 1 path: sell (K9e) | csr")
     ap.add_argument("--sell-long", type=int, default=0, help="ranking.SELL_LONG_ROW override")
+    ap.add_argument("--sell-share", type=float, default=0.0, help="ranking.SELL_MAX_LONG_SHARE override")
     a = ap.parse_args()
     cfg = CONFIGS["C3"]
     dev = torch.device("cuda", 0)
@@ -41,6 +42,8 @@ def main():
         ctx.single_query_path = a.single
     if a.sell_long:
         ranking.SELL_LONG_ROW = a.sell_long
+    if a.sell_share:
+        ranking.SELL_MAX_LONG_SHARE = a.sell_share
     S, (y_ptr, y_idx, y_val), _, _, _ = bench.build_inputs(cfg, cfg.n, 256, dev, "float32")
     dec = spectral.decompose(S, cfg.r, p=cfg.p, q=cfg.q, seed=0, dtype="float32", device=dev)
     sd = spectral.sparsify(dec, int(round(a.density * cfg.n * cfg.r)))
